@@ -1,0 +1,181 @@
+/*
+ * oocnmf_b200.h — C-ABI of the B200-native Frobenius multiplicative-update (MU) NMF
+ * backend (liboocnmf_b200.so). Plain pointers and sizes only; no torch or C++ types.
+ *
+ * This is the drop-in boundary for the reference's MU-NMF path. The reference
+ * (/root/reference/proj, a C++20 restatement of pyDNMF-GPU, arXiv 2202.09518) has no
+ * FFI of its own; its callers bind the C++ API below, which our C++ host core
+ * (include/oocnmf/<name>.hpp -> include/oocnmf_b200/oocnmf.hpp) re-exports on top of these
+ * entry points. Each entry point names the reference interface it replaces:
+ *
+ *   oocnmf_nmf_serial_dense_f64 / _csr_f64
+ *        replaces NmfResult nmf_serial(MatrixRef, const NmfConfig&)
+ *        (include/oocnmf/nmf.hpp:64, src/nmf_serial.cpp:56-121)
+ *   oocnmf_ctx_create_comm + oocnmf_set_problem(row0, rows) + oocnmf_solve
+ *        replaces nmf_distributed(ASource, NmfConfig, PartitionPlan, CommHandle&, ...)
+ *        for the row partition (include/oocnmf/nmf_distributed.hpp:34-36,
+ *        src/nmf_distributed.cpp:151-289); the CommHandle all-reduce
+ *        (include/oocnmf/comm.hpp:61, src/comm.cpp:139-147) becomes NCCL over NVLink.
+ *   oocnmf_attach_host_dense_f32(batch_rows)
+ *        replaces the ChunkStore batch server for file/host-backed A
+ *        (include/oocnmf/chunk_store.hpp:53-58): A stays in (pinned) host memory and is
+ *        streamed to HBM in row batches on a copy stream.
+ *   oocnmf_init_factors_host
+ *        replaces init_factors(m, n, k, seed) (include/oocnmf/nmf.hpp:53-58): the same
+ *        SplitMix64 counter RNG (include/oocnmf/rng.hpp:11-40), bit-identical f64.
+ *   oocnmf_split_even
+ *        the partition rule of make_plan (src/partition.cpp:20-32).
+ *
+ * Errors: every function returns an oocnmf_status; oocnmf_last_error() (thread-local)
+ * carries the message. The C++ host core maps the codes onto the reference's exception
+ * types (include/oocnmf/error.hpp:9-36): SHAPE->ShapeError, DATA->DataError,
+ * IO->IoError, COMM->CommError, STORE->StoreError, DEVICE->DeviceError (new,
+ * std::runtime_error). There is no CPU fallback: without a CUDA device every compute
+ * entry point returns OOCNMF_ERR_DEVICE.
+ */
+#ifndef OOCNMF_B200_H
+#define OOCNMF_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define OOCNMF_ABI_VERSION 1
+
+typedef enum {
+    OOCNMF_OK = 0,
+    OOCNMF_ERR_SHAPE = 1,  /* ShapeError  — bad dims/config/window */
+    OOCNMF_ERR_DATA = 2,   /* DataError   — ||A|| == 0, non-finite factors */
+    OOCNMF_ERR_IO = 3,     /* IoError */
+    OOCNMF_ERR_COMM = 4,   /* CommError   — NCCL failure */
+    OOCNMF_ERR_STORE = 5,  /* StoreError  — host batch buffer misuse */
+    OOCNMF_ERR_DEVICE = 6  /* DeviceError — CUDA failure / no device */
+} oocnmf_status;
+
+/* Mirrors NmfConfig (include/oocnmf/nmf.hpp:15-27) plus two backend knobs. */
+typedef struct {
+    uint64_t k;
+    double eta;                    /* default 1e-4 */
+    uint64_t max_iters;            /* default 1000 */
+    uint64_t error_check_interval; /* default 10 */
+    double epsilon;                /* default 1e-12 */
+    uint64_t seed;                 /* default 0 */
+    int32_t init;                  /* 0 = uniform01 (counter RNG), 1 = from factors set by
+                                      oocnmf_set_factors_f64 (FactorInit::from_files),
+                                      2 = continue from the factors resident on the device
+                                      (warm restart after a previous oocnmf_solve) */
+    int32_t error_mode;            /* 0 = trace form ||A||^2 - 2<W^T A,H> + <W^T W,H H^T>
+                                      (free: every term exists after the H update),
+                                      1 = direct residual pass over A at check iterations */
+} oocnmf_config;
+
+/* Mirrors PhaseCounters (include/oocnmf/nmf.hpp:30-39) + NmfResult scalars + kernel
+ * timing measured with CUDA events on the launching stream. */
+typedef struct {
+    double h_update_s, w_update_s, allreduce_s, error_check_s, io_s, total_s, flops;
+    uint64_t peak_resident_bytes;
+    uint64_t iterations_run;
+    int32_t converged;
+    int32_t reserved;
+    uint64_t n_trace;
+    /* device-side timing (ms, summed over all launches of that kernel) */
+    double aht_pass_ms;  /* A·H^T streaming pass (dense) or SpMM (CSR) */
+    double wta_pass_ms;  /* A^T·W streaming pass (dense) or SpMM on CSR(A^T) */
+    uint64_t aht_pass_launches;
+    uint64_t wta_pass_launches;
+    uint64_t gpu_launches; /* all kernels this library launched inside oocnmf_solve */
+    double h2d_bytes;      /* host->device bytes moved inside oocnmf_solve (out-of-core) */
+} oocnmf_info;
+
+typedef struct oocnmf_ctx oocnmf_ctx;
+
+const char* oocnmf_last_error(void);
+int oocnmf_abi_version(void);
+int oocnmf_device_count(int* count);
+
+/* Host-side helpers (no device needed). */
+int oocnmf_init_factors_host(uint64_t m, uint64_t n, uint64_t k, uint64_t seed, double* w,
+                             double* h);
+int oocnmf_counter_uniform(uint64_t seed, uint64_t stream, uint64_t index0, uint64_t count,
+                           double* out);
+int oocnmf_split_even(uint64_t extent, uint64_t parts, uint64_t* begins /* parts + 1 */);
+
+/* ----- context: one per GPU (one host thread / process per GPU) ----- */
+int oocnmf_ctx_create(int device, oocnmf_ctx** out);
+/* NCCL communicator: rank 0 calls oocnmf_comm_unique_id, ships the 128 bytes to the other
+ * ranks (any transport; torch.distributed in the Python layer), every rank then calls
+ * oocnmf_ctx_create_comm collectively. */
+int oocnmf_comm_unique_id(unsigned char id[128]);
+int oocnmf_ctx_create_comm(int device, int rank, int nranks, const unsigned char id[128],
+                           oocnmf_ctx** out);
+int oocnmf_ctx_destroy(oocnmf_ctx* ctx);
+int oocnmf_ctx_rank(const oocnmf_ctx* ctx, int* rank, int* nranks);
+
+/* Global A is m x n with k latent features; this rank owns rows [row0, row0 + rows)
+ * (the RNMF slab of PartitionPlan, src/partition.cpp:72-85). */
+int oocnmf_set_problem(oocnmf_ctx* ctx, uint64_t m, uint64_t n, uint64_t k, uint64_t row0,
+                       uint64_t rows);
+
+/* A sources (pick one). Dense values are stored in HBM as f32 row-major. */
+int oocnmf_load_dense_f64(oocnmf_ctx* ctx, const double* a_slab, uint64_t lda);
+int oocnmf_load_dense_f32(oocnmf_ctx* ctx, const float* a_slab, uint64_t lda);
+int oocnmf_load_dense_device_f32(oocnmf_ctx* ctx, const float* d_a_slab, uint64_t lda);
+/* A[i][j] = (float) CounterRng(seed, stream).uniform(i * n + j), generated in HBM
+ * (the bench/kernels_bench.cpp:12-18 input at any size). */
+int oocnmf_generate_dense_uniform(oocnmf_ctx* ctx, uint64_t seed, uint64_t stream);
+/* CSR slab: row_ptr has rows+1 entries starting at 0, col_idx global in [0, n). */
+int oocnmf_load_csr_f64(oocnmf_ctx* ctx, const uint64_t* row_ptr, const uint64_t* col_idx,
+                        const double* vals);
+/* Reference-semantics sparse generator (src/synth.cpp:60-86), evaluated in HBM for this
+ * rank's rows: cell present iff U(seed,14,i*n+j) < density, value U(seed,15,i*n+j). */
+int oocnmf_generate_csr_uniform(oocnmf_ctx* ctx, double density, uint64_t seed);
+/* Out-of-core: A stays in host memory (pinned if the caller registered/allocated it so)
+ * and streams to HBM in row batches of batch_rows (0 = auto from free HBM). */
+int oocnmf_attach_host_dense_f32(oocnmf_ctx* ctx, const float* a_slab, uint64_t lda,
+                                 uint64_t batch_rows);
+int oocnmf_host_register(void* p, uint64_t bytes);   /* cudaHostRegister (pin) */
+int oocnmf_host_unregister(void* p);
+/* Copy the resident dense A slab (rows x n, f32) back to host memory (ld = n). */
+int oocnmf_download_dense_f32(oocnmf_ctx* ctx, float* a_slab);
+
+/* ----- factors ----- */
+int oocnmf_set_factors_f64(oocnmf_ctx* ctx, const double* w_slab /* rows x k */,
+                           const double* h /* k x n */);
+int oocnmf_get_factors_f64(oocnmf_ctx* ctx, double* w_slab, double* h);
+/* Gather every rank's W slab into w_full (m x k) on every rank (ncclAllGather). */
+int oocnmf_gather_w_f64(oocnmf_ctx* ctx, double* w_full);
+
+/* ----- solve: the MU loop (src/nmf_serial.cpp:83-117 / src/nmf_distributed.cpp:239-262).
+ * Collective across ranks of a communicator context. Writes up to trace_cap
+ * (iteration, relative error) pairs. */
+int oocnmf_solve(oocnmf_ctx* ctx, const oocnmf_config* cfg, uint64_t* trace_iter,
+                 double* trace_err, uint64_t trace_cap, oocnmf_info* info);
+
+/* Diagnostics for parity tests: with the current factors, compute A·H^T (rows x k) and
+ * the rank-local A^T·W (k x n), H H^T and W^T W (k x k) without updating anything. */
+int oocnmf_products_f64(oocnmf_ctx* ctx, double* aht, double* wta, double* hht, double* wtw);
+/* Squared Frobenius norm of the resident A slab (f64 accumulation). */
+int oocnmf_sq_norm(oocnmf_ctx* ctx, double* out);
+
+/* ----- one-shot drop-ins for nmf_serial(MatrixRef a, const NmfConfig& cfg) on host
+ * buffers: upload, solve, download. w0/h0 are used iff cfg->init == 1. */
+int oocnmf_nmf_serial_dense_f64(int device, const double* a, uint64_t m, uint64_t n,
+                                const oocnmf_config* cfg, const double* w0, const double* h0,
+                                double* w_out, double* h_out, uint64_t* trace_iter,
+                                double* trace_err, uint64_t trace_cap, oocnmf_info* info);
+int oocnmf_nmf_serial_dense_f32(int device, const float* a, uint64_t m, uint64_t n,
+                                const oocnmf_config* cfg, const double* w0, const double* h0,
+                                double* w_out, double* h_out, uint64_t* trace_iter,
+                                double* trace_err, uint64_t trace_cap, oocnmf_info* info);
+int oocnmf_nmf_serial_csr_f64(int device, const uint64_t* row_ptr, const uint64_t* col_idx,
+                              const double* vals, uint64_t m, uint64_t n,
+                              const oocnmf_config* cfg, const double* w0, const double* h0,
+                              double* w_out, double* h_out, uint64_t* trace_iter,
+                              double* trace_err, uint64_t trace_cap, oocnmf_info* info);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* OOCNMF_B200_H */

@@ -1,0 +1,252 @@
+// C++ host core of the B200 MU-NMF backend — source-compatible with the reference's
+// `oocnmf` API for the MU path, so a caller of
+//     oocnmf::nmf_serial(MatrixRef, const NmfConfig&)          (include/oocnmf/nmf.hpp:64)
+//     oocnmf::nmf_distributed(ASource, NmfConfig, PartitionPlan, CommHandle&, StoreConfig)
+//                                                  (include/oocnmf/nmf_distributed.hpp:34-36)
+// recompiles against these headers unchanged. Everything here is host plumbing (types,
+// validation, f64<->f32 at the boundary, exception mapping); all arithmetic runs on the
+// GPU behind the C-ABI in include/oocnmf_b200.h. The reference header names
+// (oocnmf/matrix.hpp, nmf.hpp, ...) are thin forwarders to this file.
+#pragma once
+
+#include <array>
+#include <cstddef>
+#include <cstdint>
+#include <memory>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "oocnmf_b200.h"
+
+namespace oocnmf {
+
+using index_t = std::size_t;
+
+// ---- errors (reference: include/oocnmf/error.hpp:9-36) ----
+struct ShapeError : std::invalid_argument {
+    using std::invalid_argument::invalid_argument;
+};
+struct DataError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct IoError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CommError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct StoreError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+/// New: CUDA / device failures of the B200 backend (no CPU fallback exists).
+struct DeviceError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+/// Throws the exception type matching an oocnmf_status (OOCNMF_OK is a no-op).
+void throw_status(int status);
+
+// ---- matrices (reference: include/oocnmf/matrix.hpp:15-151) ----
+struct IndexRange {
+    index_t begin = 0, end = 0;
+    index_t extent() const { return end - begin; }
+    bool contains(index_t i) const { return begin <= i && i < end; }
+    bool operator==(const IndexRange&) const = default;
+};
+
+class DenseMatrix {
+public:
+    DenseMatrix() = default;
+    DenseMatrix(index_t r, index_t c, double fill = 0.0) : r_(r), c_(c), v_(r * c, fill) {}
+    DenseMatrix(index_t r, index_t c, std::vector<double> data);
+    index_t rows() const { return r_; }
+    index_t cols() const { return c_; }
+    index_t size() const { return v_.size(); }
+    double& at(index_t i, index_t j) { return v_[i * c_ + j]; }
+    double at(index_t i, index_t j) const { return v_[i * c_ + j]; }
+    double* data() { return v_.data(); }
+    const double* data() const { return v_.data(); }
+    double* row(index_t i) { return v_.data() + i * c_; }
+    const double* row(index_t i) const { return v_.data() + i * c_; }
+    std::string shape_str() const { return std::to_string(r_) + "x" + std::to_string(c_); }
+    bool operator==(const DenseMatrix&) const = default;
+
+private:
+    index_t r_ = 0, c_ = 0;
+    std::vector<double> v_;
+};
+
+class CsrMatrix {
+public:
+    CsrMatrix() = default;
+    CsrMatrix(index_t rows, index_t cols, std::vector<index_t> row_ptr, std::vector<index_t> col_idx,
+              std::vector<double> values);
+    index_t rows() const { return r_; }
+    index_t cols() const { return c_; }
+    index_t nnz() const { return val_.size(); }
+    const std::vector<index_t>& row_ptr() const { return rp_; }
+    const std::vector<index_t>& col_idx() const { return ci_; }
+    const std::vector<double>& values() const { return val_; }
+    std::vector<double>& values() { return val_; }
+    std::string shape_str() const { return std::to_string(r_) + "x" + std::to_string(c_); }
+    void validate_structure() const;
+    DenseMatrix to_dense() const;
+    static CsrMatrix from_dense(const DenseMatrix& d, double zero_tol = 0.0);
+    bool operator==(const CsrMatrix&) const = default;
+
+private:
+    index_t r_ = 0, c_ = 0;
+    std::vector<index_t> rp_{0}, ci_;
+    std::vector<double> val_;
+};
+
+/// Non-owning window over a dense or CSR matrix (local coordinates [0,rows) x [0,cols)).
+class MatrixRef {
+public:
+    MatrixRef() = default;
+    explicit MatrixRef(const DenseMatrix& m) : d_(&m), rr_{0, m.rows()}, cr_{0, m.cols()} {}
+    explicit MatrixRef(const CsrMatrix& m) : s_(&m), rr_{0, m.rows()}, cr_{0, m.cols()} {}
+    MatrixRef window(IndexRange r, IndexRange c) const;
+    index_t rows() const { return rr_.extent(); }
+    index_t cols() const { return cr_.extent(); }
+    IndexRange row_range() const { return rr_; }
+    IndexRange col_range() const { return cr_; }
+    bool is_dense() const { return d_ != nullptr; }
+    bool is_sparse() const { return s_ != nullptr; }
+    bool empty() const { return !d_ && !s_; }
+    const DenseMatrix& dense() const { return *d_; }
+    const CsrMatrix& sparse() const { return *s_; }
+    double at(index_t i, index_t j) const;
+    std::string shape_str() const { return std::to_string(rows()) + "x" + std::to_string(cols()); }
+
+private:
+    const DenseMatrix* d_ = nullptr;
+    const CsrMatrix* s_ = nullptr;
+    IndexRange rr_, cr_;
+};
+
+// ---- counter RNG (reference: include/oocnmf/rng.hpp:11-45) ----
+class CounterRng {
+public:
+    CounterRng(std::uint64_t seed, std::uint64_t stream);
+    std::uint64_t bits(std::uint64_t index) const;
+    double uniform(std::uint64_t index) const;
+    double uniform(std::uint64_t index, double lo, double hi) const { return lo + (hi - lo) * uniform(index); }
+    static std::uint64_t mix(std::uint64_t z);
+
+private:
+    std::uint64_t key_;
+};
+std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t a, std::uint64_t b = 0);
+
+// ---- solver config / result (reference: include/oocnmf/nmf.hpp:11-66) ----
+inline constexpr double kDefaultEpsilon = 1e-12;
+enum class FactorInit { uniform01, from_files };
+/// B200 extension: how the relative error is evaluated at check iterations.
+enum class ErrorMode { trace = 0, direct = 1 };
+
+struct NmfConfig {
+    index_t k = 1;
+    double eta = 1e-4;
+    index_t max_iters = 1000;
+    index_t error_check_interval = 10;
+    double epsilon = kDefaultEpsilon;
+    std::uint64_t seed = 0;
+    FactorInit init = FactorInit::uniform01;
+    std::optional<DenseMatrix> init_w;
+    std::optional<DenseMatrix> init_h;
+    // B200 extensions (defaults reproduce the reference's behaviour on GPU 0)
+    int device = 0;
+    ErrorMode error_mode = ErrorMode::trace;
+    void validate() const;
+};
+
+struct PhaseCounters {
+    double h_update_s = 0, w_update_s = 0, allreduce_s = 0, error_check_s = 0, io_s = 0, total_s = 0;
+    double flops = 0;
+    index_t peak_resident_bytes = 0;
+};
+
+struct NmfResult {
+    DenseMatrix w;
+    DenseMatrix h;
+    std::vector<std::pair<index_t, double>> error_trace;
+    index_t iterations_run = 0;
+    bool converged = false;
+    PhaseCounters counters;
+};
+
+std::pair<DenseMatrix, DenseMatrix> init_factors(index_t m, index_t n, index_t k, std::uint64_t seed);
+DenseMatrix init_w_rows(index_t m, index_t k, std::uint64_t seed, IndexRange rows);
+DenseMatrix init_h_cols(index_t n, index_t k, std::uint64_t seed, IndexRange cols);
+
+/// W-then-H multiplicative updates of A ≈ WH on one B200 (A dense or CSR).
+NmfResult nmf_serial(MatrixRef a, const NmfConfig& cfg);
+
+// ---- partition (reference: include/oocnmf/partition.hpp:10-46) ----
+enum class Strategy { cnmf, rnmf };
+std::string to_string(Strategy s);
+Strategy choose_strategy(index_t m, index_t n);
+struct WorkerSlab {
+    int rank = 0;
+    IndexRange a_rows, a_cols;
+};
+struct PartitionPlan {
+    Strategy strategy = Strategy::rnmf;
+    int n_workers = 1;
+    index_t m = 0, n = 0, k = 0;
+    index_t n_b = 1;
+    std::vector<WorkerSlab> slabs;
+    std::vector<IndexRange> batches;
+    index_t max_slab_extent() const;
+    index_t max_batch_extent() const;
+};
+PartitionPlan make_plan(index_t m, index_t n, index_t k, int n_workers, index_t n_b, Strategy strategy);
+
+// ---- distributed (reference: include/oocnmf/nmf_distributed.hpp, comm.hpp) ----
+/// One rank of an NCCL group (one process or host thread per GPU). Created collectively:
+/// rank 0 calls new_unique_id(), ships it to the others, every rank constructs a handle.
+class CommHandle {
+public:
+    using UniqueId = std::array<unsigned char, 128>;
+    static UniqueId new_unique_id();
+    CommHandle() = default;
+    CommHandle(int rank, int size, int device, const UniqueId& id);
+    int rank() const { return rank_; }
+    int size() const { return size_; }
+    int device() const { return device_; }
+    oocnmf_ctx* context() const { return ctx_.get(); }
+
+private:
+    int rank_ = 0, size_ = 1, device_ = 0;
+    std::shared_ptr<oocnmf_ctx> ctx_;
+};
+
+struct ASource {
+    MatrixRef mem;
+    std::string pdn1_path;  // not supported by the B200 backend (IoError)
+    const float* host_f32 = nullptr;  // B200 extension: out-of-core host slab (rows of this rank)
+    index_t host_ld = 0;
+    static ASource memory(MatrixRef a) { return {a, {}, nullptr, 0}; }
+    static ASource file(std::string path) { return {{}, std::move(path), nullptr, 0}; }
+    static ASource host_slab(const float* p, index_t ld) { return {{}, {}, p, ld}; }
+};
+struct StoreConfig {
+    index_t budget_bytes = 0;  // out-of-core: HBM staging budget for the two row-batch buffers
+    int n_cb = 1;
+    bool prefetch = false;
+};
+struct StoreCounters {
+    index_t loads = 0, evictions = 0, bytes_read = 0, resident_bytes = 0, peak_resident_bytes = 0;
+    double io_seconds = 0;
+};
+
+/// Row-partitioned (RNMF) MU on this rank's GPU; collective over the CommHandle's group.
+/// Returns the gathered W (m x k) and replicated H on every rank.
+NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan, CommHandle& comm,
+                          const StoreConfig& store_cfg = {}, StoreCounters* store_counters_out = nullptr);
+
+}  // namespace oocnmf

@@ -1,0 +1,302 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product library.
+//
+// extern "C" shim over the *unmodified* reference library compiled from
+// /root/reference/proj/src (see oracle/Makefile). It lets tests/, bench.py's
+// cpu_baseline / --impl reference leg, and __graft_entry__.smoke() drive the
+// reference CPU solver through plain pointers. Nothing here re-implements an
+// algorithm: every call forwards to the reference's own functions.
+//
+//   ref_nmf_serial_*        -> oocnmf::nmf_serial          (src/nmf_serial.cpp:56)
+//   ref_nmf_distributed_*   -> oocnmf::run_distributed_threads (src/nmf_distributed.cpp:291)
+//   ref_gen_lowrank         -> oocnmf::gen_lowrank          (src/synth.cpp:18)
+//   ref_gen_sparse_*        -> oocnmf::gen_sparse_random    (src/synth.cpp:60)
+//   ref_init_factors        -> oocnmf::init_factors         (src/nmf_serial.cpp:50)
+//   ref_mu_iteration        -> the body of nmf_serial's loop (src/nmf_serial.cpp:84-101)
+//   ref_make_plan           -> oocnmf::make_plan            (src/partition.cpp:49)
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <string>
+#include <vector>
+
+#include "oocnmf/kernels.hpp"
+#include "oocnmf/nmf.hpp"
+#include "oocnmf/nmf_distributed.hpp"
+#include "oocnmf/partition.hpp"
+#include "oocnmf/rng.hpp"
+#include "oocnmf/synth.hpp"
+
+using namespace oocnmf;
+
+namespace {
+thread_local std::string g_err;
+
+int fail(const std::exception& e, int code) {
+    g_err = e.what();
+    return code;
+}
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ShapeError& e) {
+        return fail(e, 1);
+    } catch (const DataError& e) {
+        return fail(e, 2);
+    } catch (const IoError& e) {
+        return fail(e, 3);
+    } catch (const CommError& e) {
+        return fail(e, 4);
+    } catch (const StoreError& e) {
+        return fail(e, 5);
+    } catch (const std::exception& e) {
+        return fail(e, 9);
+    }
+}
+
+DenseMatrix copy_dense(const double* p, std::uint64_t r, std::uint64_t c) {
+    return DenseMatrix(r, c, std::vector<double>(p, p + r * c));
+}
+
+struct Out {
+    double* w;
+    double* h;
+    std::uint64_t* trace_it;
+    double* trace_err;
+    std::uint64_t trace_cap;
+    std::uint64_t* n_trace;
+    std::uint64_t* iters_run;
+    int* converged;
+    double* counters;  // [w_update_s, h_update_s, allreduce_s, error_check_s, io_s, total_s, flops]
+};
+
+void write_out(const NmfResult& r, const Out& o) {
+    std::memcpy(o.w, r.w.data(), r.w.size() * sizeof(double));
+    std::memcpy(o.h, r.h.data(), r.h.size() * sizeof(double));
+    const std::uint64_t n = r.error_trace.size();
+    *o.n_trace = n;
+    for (std::uint64_t i = 0; i < n && i < o.trace_cap; ++i) {
+        o.trace_it[i] = r.error_trace[i].first;
+        o.trace_err[i] = r.error_trace[i].second;
+    }
+    *o.iters_run = r.iterations_run;
+    *o.converged = r.converged ? 1 : 0;
+    if (o.counters) {
+        const auto& c = r.counters;
+        double v[7] = {c.w_update_s, c.h_update_s, c.allreduce_s, c.error_check_s,
+                       c.io_s,       c.total_s,    c.flops};
+        std::memcpy(o.counters, v, sizeof v);
+    }
+}
+
+NmfConfig make_cfg(std::uint64_t k, std::uint64_t max_iters, std::uint64_t interval, double eta,
+                   double eps, std::uint64_t seed, const double* w0, const double* h0,
+                   std::uint64_t m, std::uint64_t n) {
+    NmfConfig cfg;
+    cfg.k = k;
+    cfg.max_iters = max_iters;
+    cfg.error_check_interval = interval;
+    cfg.eta = eta;
+    cfg.epsilon = eps;
+    cfg.seed = seed;
+    if (w0 && h0) {
+        cfg.init = FactorInit::from_files;
+        cfg.init_w = copy_dense(w0, m, k);
+        cfg.init_h = copy_dense(h0, k, n);
+    }
+    return cfg;
+}
+
+CsrMatrix make_csr(std::uint64_t m, std::uint64_t n, const std::uint64_t* rp, const std::uint64_t* ci,
+                   const double* v) {
+    const std::uint64_t nnz = rp[m];
+    return CsrMatrix(m, n, std::vector<index_t>(rp, rp + m + 1), std::vector<index_t>(ci, ci + nnz),
+                     std::vector<double>(v, v + nnz));
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+int ref_nmf_serial_dense(const double* a, std::uint64_t m, std::uint64_t n, std::uint64_t k,
+                         std::uint64_t max_iters, std::uint64_t interval, double eta, double eps,
+                         std::uint64_t seed, const double* w0, const double* h0, double* w,
+                         double* h, std::uint64_t* trace_it, double* trace_err,
+                         std::uint64_t trace_cap, std::uint64_t* n_trace, std::uint64_t* iters_run,
+                         int* converged, double* counters) {
+    return guarded([&] {
+        DenseMatrix A = copy_dense(a, m, n);
+        NmfConfig cfg = make_cfg(k, max_iters, interval, eta, eps, seed, w0, h0, m, n);
+        write_out(nmf_serial(MatrixRef(A), cfg),
+                  {w, h, trace_it, trace_err, trace_cap, n_trace, iters_run, converged, counters});
+    });
+}
+
+int ref_nmf_serial_csr(const std::uint64_t* rp, const std::uint64_t* ci, const double* v,
+                       std::uint64_t m, std::uint64_t n, std::uint64_t k, std::uint64_t max_iters,
+                       std::uint64_t interval, double eta, double eps, std::uint64_t seed,
+                       const double* w0, const double* h0, double* w, double* h,
+                       std::uint64_t* trace_it, double* trace_err, std::uint64_t trace_cap,
+                       std::uint64_t* n_trace, std::uint64_t* iters_run, int* converged,
+                       double* counters) {
+    return guarded([&] {
+        CsrMatrix A = make_csr(m, n, rp, ci, v);
+        NmfConfig cfg = make_cfg(k, max_iters, interval, eta, eps, seed, w0, h0, m, n);
+        write_out(nmf_serial(MatrixRef(A), cfg),
+                  {w, h, trace_it, trace_err, trace_cap, n_trace, iters_run, converged, counters});
+    });
+}
+
+// Threads-backend distributed run; returns rank 0's result (identical on all ranks).
+// strategy: 0 = choose_strategy(m, n), 1 = CNMF, 2 = RNMF. a_csr_* may be null for dense.
+int ref_nmf_distributed(const double* a_dense, const std::uint64_t* rp, const std::uint64_t* ci,
+                        const double* v, std::uint64_t m, std::uint64_t n, std::uint64_t k,
+                        int n_workers, std::uint64_t n_b, int strategy, std::uint64_t max_iters,
+                        std::uint64_t interval, double eta, double eps, std::uint64_t seed,
+                        const double* w0, const double* h0, double* w, double* h,
+                        std::uint64_t* trace_it, double* trace_err, std::uint64_t trace_cap,
+                        std::uint64_t* n_trace, std::uint64_t* iters_run, int* converged,
+                        double* counters) {
+    return guarded([&] {
+        DenseMatrix Ad;
+        CsrMatrix As;
+        MatrixRef ref;
+        if (a_dense) {
+            Ad = copy_dense(a_dense, m, n);
+            ref = MatrixRef(Ad);
+        } else {
+            As = make_csr(m, n, rp, ci, v);
+            ref = MatrixRef(As);
+        }
+        const Strategy s = strategy == 0   ? choose_strategy(m, n)
+                           : strategy == 1 ? Strategy::cnmf
+                                           : Strategy::rnmf;
+        PartitionPlan plan = make_plan(m, n, k, n_workers, n_b, s);
+        NmfConfig cfg = make_cfg(k, max_iters, interval, eta, eps, seed, w0, h0, m, n);
+        auto res = run_distributed_threads(ASource::memory(ref), cfg, plan);
+        write_out(res[0],
+                  {w, h, trace_it, trace_err, trace_cap, n_trace, iters_run, converged, counters});
+    });
+}
+
+int ref_init_factors(std::uint64_t m, std::uint64_t n, std::uint64_t k, std::uint64_t seed,
+                     double* w, double* h) {
+    return guarded([&] {
+        auto [W, H] = init_factors(m, n, k, seed);
+        std::memcpy(w, W.data(), W.size() * sizeof(double));
+        std::memcpy(h, H.data(), H.size() * sizeof(double));
+    });
+}
+
+int ref_gen_lowrank(std::uint64_t m, std::uint64_t n, std::uint64_t k_true, double noise,
+                    std::uint64_t seed, double* a, double* w0, double* h0) {
+    return guarded([&] {
+        LowrankSpec spec{m, n, k_true, noise, seed};
+        LowrankData d = gen_lowrank(spec);
+        std::memcpy(a, d.a.data(), d.a.size() * sizeof(double));
+        if (w0) std::memcpy(w0, d.w0.data(), d.w0.size() * sizeof(double));
+        if (h0) std::memcpy(h0, d.h0.data(), d.h0.size() * sizeof(double));
+    });
+}
+
+// Two-call protocol: first with col_idx == nullptr to learn nnz (written to *nnz_out and
+// rp), then again with buffers sized nnz.
+int ref_gen_sparse(std::uint64_t m, std::uint64_t n, double density, std::uint64_t seed,
+                   std::uint64_t* rp, std::uint64_t* ci, double* v, std::uint64_t* nnz_out) {
+    return guarded([&] {
+        CsrMatrix s = gen_sparse_random(SparseSpec{m, n, density, seed});
+        *nnz_out = s.nnz();
+        std::memcpy(rp, s.row_ptr().data(), (m + 1) * sizeof(std::uint64_t));
+        if (ci) {
+            std::memcpy(ci, s.col_idx().data(), s.nnz() * sizeof(std::uint64_t));
+            std::memcpy(v, s.values().data(), s.nnz() * sizeof(double));
+        }
+    });
+}
+
+// CounterRng(seed, stream).uniform(i * n + j) for a row window [row0, row0 + rows).
+int ref_uniform_dense(std::uint64_t row0, std::uint64_t rows, std::uint64_t n, std::uint64_t seed,
+                      std::uint64_t stream, double* out) {
+    return guarded([&] {
+        CounterRng rng(seed, stream);
+        for (std::uint64_t i = 0; i < rows; ++i)
+            for (std::uint64_t j = 0; j < n; ++j) out[i * n + j] = rng.uniform((row0 + i) * n + j);
+    });
+}
+
+// One MU iteration (W update then H update) on caller-owned factors, exactly the body of
+// nmf_serial's loop (src/nmf_serial.cpp:84-101), without the error check. Used by the
+// bench's reference arm on a bounded row sample.
+int ref_mu_iteration(const double* a, std::uint64_t m, std::uint64_t n, std::uint64_t k, double* w,
+                     double* h, double eps) {
+    return guarded([&] {
+        DenseMatrix A(m, n, std::vector<double>(a, a + m * n));
+        DenseMatrix W = copy_dense(w, m, k), H = copy_dense(h, k, n);
+        DenseMatrix ht = transpose(H);
+        DenseMatrix hht = gram_t(MatrixRef(ht));
+        DenseMatrix aht = matmul(MatrixRef(A), ht);
+        DenseMatrix whht = matmul(MatrixRef(W), hht);
+        hadamard_update(W, aht, whht, eps);
+        DenseMatrix wtw = gram_t(MatrixRef(W));
+        DenseMatrix wta(k, n);
+        matmul_ta_acc(MatrixRef(W), MatrixRef(A), wta);
+        DenseMatrix wtwh = matmul(MatrixRef(wtw), H);
+        hadamard_update(H, wta, wtwh, eps);
+        std::memcpy(w, W.data(), W.size() * sizeof(double));
+        std::memcpy(h, H.data(), H.size() * sizeof(double));
+    });
+}
+
+// Same, but A is already an oocnmf::DenseMatrix held by the caller across calls (avoids the
+// per-call copy in timed loops): create/destroy a handle.
+void* ref_dense_create(const double* a, std::uint64_t m, std::uint64_t n) {
+    return new DenseMatrix(m, n, std::vector<double>(a, a + m * n));
+}
+void ref_dense_destroy(void* p) { delete static_cast<DenseMatrix*>(p); }
+int ref_mu_iteration_handle(void* a_handle, std::uint64_t k, double* w, double* h, double eps) {
+    return guarded([&] {
+        const DenseMatrix& A = *static_cast<DenseMatrix*>(a_handle);
+        const std::uint64_t m = A.rows(), n = A.cols();
+        DenseMatrix W = copy_dense(w, m, k), H = copy_dense(h, k, n);
+        DenseMatrix ht = transpose(H);
+        DenseMatrix hht = gram_t(MatrixRef(ht));
+        DenseMatrix aht = matmul(MatrixRef(A), ht);
+        DenseMatrix whht = matmul(MatrixRef(W), hht);
+        hadamard_update(W, aht, whht, eps);
+        DenseMatrix wtw = gram_t(MatrixRef(W));
+        DenseMatrix wta(k, n);
+        matmul_ta_acc(MatrixRef(W), MatrixRef(A), wta);
+        DenseMatrix wtwh = matmul(MatrixRef(wtw), H);
+        hadamard_update(H, wta, wtwh, eps);
+        std::memcpy(w, W.data(), W.size() * sizeof(double));
+        std::memcpy(h, H.data(), H.size() * sizeof(double));
+    });
+}
+
+// Partition plan: writes per-rank [row_begin,row_end,col_begin,col_end] and batch ranges.
+int ref_make_plan(std::uint64_t m, std::uint64_t n, std::uint64_t k, int n_workers,
+                  std::uint64_t n_b, int strategy, std::uint64_t* slabs4, std::uint64_t* batches2,
+                  int* strategy_out) {
+    return guarded([&] {
+        const Strategy s = strategy == 0   ? choose_strategy(m, n)
+                           : strategy == 1 ? Strategy::cnmf
+                                           : Strategy::rnmf;
+        PartitionPlan p = make_plan(m, n, k, n_workers, n_b, s);
+        for (int r = 0; r < n_workers; ++r) {
+            slabs4[4 * r + 0] = p.slabs[r].a_rows.begin;
+            slabs4[4 * r + 1] = p.slabs[r].a_rows.end;
+            slabs4[4 * r + 2] = p.slabs[r].a_cols.begin;
+            slabs4[4 * r + 3] = p.slabs[r].a_cols.end;
+        }
+        for (std::uint64_t b = 0; b < n_b; ++b) {
+            batches2[2 * b] = p.batches[b].begin;
+            batches2[2 * b + 1] = p.batches[b].end;
+        }
+        *strategy_out = p.strategy == Strategy::cnmf ? 1 : 2;
+    });
+}
+
+}  // extern "C"

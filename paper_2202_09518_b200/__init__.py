@@ -1,0 +1,34 @@
+"""B200-native Frobenius multiplicative-update NMF (the hot path of pyDNMF-GPU, arXiv 2202.09518).
+
+The product is ``lib/liboocnmf_b200.so`` (C-ABI: ``include/oocnmf_b200.h``; C++ host core:
+``include/oocnmf/*.hpp``). This package is its Python front-end, mirroring the reference's
+``oocnmf::`` API names.
+"""
+from .nmf import (  # noqa: F401
+    CommError,
+    Context,
+    CsrMatrix,
+    DataError,
+    DeviceError,
+    DistComm,
+    FactorInit,
+    IoError,
+    NmfConfig,
+    NmfResult,
+    PartitionPlan,
+    PhaseCounters,
+    ShapeError,
+    StoreError,
+    Strategy,
+    check,
+    choose_strategy,
+    counter_uniform,
+    device_count,
+    init_factors,
+    make_plan,
+    nmf_distributed,
+    nmf_serial,
+    split_even,
+)
+
+__version__ = "0.1.0"

@@ -1,0 +1,336 @@
+// C++ host core over the C-ABI (include/oocnmf_b200.h): the reference's oocnmf:: API for
+// the MU path, implemented as validation + f64<->f32 staging + status->exception mapping.
+#include <algorithm>
+#include <cmath>
+
+#include "oocnmf_b200/oocnmf.hpp"
+
+namespace oocnmf {
+
+void throw_status(int st) {
+    if (st == OOCNMF_OK) return;
+    const std::string msg = oocnmf_last_error();
+    switch (st) {
+        case OOCNMF_ERR_SHAPE: throw ShapeError(msg);
+        case OOCNMF_ERR_DATA: throw DataError(msg);
+        case OOCNMF_ERR_IO: throw IoError(msg);
+        case OOCNMF_ERR_COMM: throw CommError(msg);
+        case OOCNMF_ERR_STORE: throw StoreError(msg);
+        default: throw DeviceError(msg);
+    }
+}
+
+// ------------------------------------------------------------------------- matrices
+DenseMatrix::DenseMatrix(index_t r, index_t c, std::vector<double> data) : r_(r), c_(c), v_(std::move(data)) {
+    if (v_.size() != r_ * c_)
+        throw ShapeError("DenseMatrix: data length " + std::to_string(v_.size()) + " != " + shape_str());
+}
+
+CsrMatrix::CsrMatrix(index_t rows, index_t cols, std::vector<index_t> rp, std::vector<index_t> ci,
+                     std::vector<double> v)
+    : r_(rows), c_(cols), rp_(std::move(rp)), ci_(std::move(ci)), val_(std::move(v)) {
+    validate_structure();
+}
+
+void CsrMatrix::validate_structure() const {
+    if (rp_.size() != r_ + 1) throw ShapeError("CsrMatrix: row_ptr must have rows+1 entries");
+    if (rp_.front() != 0) throw ShapeError("CsrMatrix: row_ptr[0] != 0");
+    if (rp_.back() != val_.size() || ci_.size() != val_.size())
+        throw ShapeError("CsrMatrix: row_ptr[rows] disagrees with nnz");
+    for (index_t i = 0; i < r_; ++i) {
+        if (rp_[i] > rp_[i + 1]) throw ShapeError("CsrMatrix: row_ptr decreases at row " + std::to_string(i));
+        for (index_t p = rp_[i]; p < rp_[i + 1]; ++p) {
+            if (ci_[p] >= c_) throw ShapeError("CsrMatrix: column index out of range in row " + std::to_string(i));
+            if (p > rp_[i] && ci_[p] <= ci_[p - 1])
+                throw ShapeError("CsrMatrix: column indices not strictly increasing in row " + std::to_string(i));
+        }
+    }
+}
+
+DenseMatrix CsrMatrix::to_dense() const {
+    DenseMatrix d(r_, c_);
+    for (index_t i = 0; i < r_; ++i)
+        for (index_t p = rp_[i]; p < rp_[i + 1]; ++p) d.at(i, ci_[p]) = val_[p];
+    return d;
+}
+
+CsrMatrix CsrMatrix::from_dense(const DenseMatrix& d, double tol) {
+    std::vector<index_t> rp{0}, ci;
+    std::vector<double> v;
+    for (index_t i = 0; i < d.rows(); ++i) {
+        for (index_t j = 0; j < d.cols(); ++j)
+            if (std::abs(d.at(i, j)) > tol) ci.push_back(j), v.push_back(d.at(i, j));
+        rp.push_back(v.size());
+    }
+    return CsrMatrix(d.rows(), d.cols(), std::move(rp), std::move(ci), std::move(v));
+}
+
+MatrixRef MatrixRef::window(IndexRange r, IndexRange c) const {
+    if (r.begin > r.end || r.end > rows() || c.begin > c.end || c.end > cols())
+        throw ShapeError("MatrixRef::window: window out of bounds for " + shape_str());
+    MatrixRef o = *this;
+    o.rr_ = {rr_.begin + r.begin, rr_.begin + r.end};
+    o.cr_ = {cr_.begin + c.begin, cr_.begin + c.end};
+    return o;
+}
+
+double MatrixRef::at(index_t i, index_t j) const {
+    const index_t gi = rr_.begin + i, gj = cr_.begin + j;
+    if (d_) return d_->at(gi, gj);
+    const auto& rp = s_->row_ptr();
+    const auto& ci = s_->col_idx();
+    const auto b = ci.begin() + std::ptrdiff_t(rp[gi]), e = ci.begin() + std::ptrdiff_t(rp[gi + 1]);
+    const auto it = std::lower_bound(b, e, gj);
+    return (it != e && *it == gj) ? s_->values()[index_t(it - ci.begin())] : 0.0;
+}
+
+// ------------------------------------------------------------------------- rng
+std::uint64_t CounterRng::mix(std::uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+CounterRng::CounterRng(std::uint64_t seed, std::uint64_t stream) : key_(mix(seed ^ mix(stream + 0x632BE59BD9B4E019ULL))) {}
+std::uint64_t CounterRng::bits(std::uint64_t index) const { return mix(key_ + (index + 1) * 0x9E3779B97F4A7C15ULL); }
+double CounterRng::uniform(std::uint64_t index) const { return double(bits(index) >> 11) * 0x1.0p-53; }
+std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t a, std::uint64_t b) {
+    return CounterRng::mix(seed ^ CounterRng::mix(a ^ CounterRng::mix(b)));
+}
+
+// ------------------------------------------------------------------------- solver API
+void NmfConfig::validate() const {
+    if (k < 1) throw ShapeError("NmfConfig: k must be >= 1");
+    if (!(eta >= 0)) throw ShapeError("NmfConfig: eta must be >= 0");
+    if (max_iters < 1) throw ShapeError("NmfConfig: max_iters must be >= 1");
+    if (error_check_interval < 1) throw ShapeError("NmfConfig: error_check_interval must be >= 1");
+    if (!(epsilon > 0)) throw ShapeError("NmfConfig: epsilon must be > 0");
+    if (init == FactorInit::from_files && (!init_w || !init_h))
+        throw ShapeError("NmfConfig: init=from_files requires both factors");
+}
+
+DenseMatrix init_w_rows(index_t m, index_t k, std::uint64_t seed, IndexRange rows) {
+    (void)m;
+    DenseMatrix w(rows.extent(), k);
+    throw_status(oocnmf_counter_uniform(seed, 1, rows.begin * k, rows.extent() * k, w.data()));
+    return w;
+}
+
+DenseMatrix init_h_cols(index_t n, index_t k, std::uint64_t seed, IndexRange cols) {
+    DenseMatrix h(k, cols.extent());
+    for (index_t r = 0; r < k; ++r)
+        throw_status(oocnmf_counter_uniform(seed, 2, r * n + cols.begin, cols.extent(), h.row(r)));
+    return h;
+}
+
+std::pair<DenseMatrix, DenseMatrix> init_factors(index_t m, index_t n, index_t k, std::uint64_t seed) {
+    if (m < 1 || n < 1 || k < 1) throw ShapeError("init_factors: dimensions must be >= 1");
+    return {init_w_rows(m, k, seed, {0, m}), init_h_cols(n, k, seed, {0, n})};
+}
+
+namespace {
+
+struct Ctx {
+    oocnmf_ctx* c = nullptr;
+    bool own = true;
+    ~Ctx() {
+        if (own && c) oocnmf_ctx_destroy(c);
+    }
+};
+
+oocnmf_config to_c(const NmfConfig& cfg) {
+    oocnmf_config c{};
+    c.k = cfg.k;
+    c.eta = cfg.eta;
+    c.max_iters = cfg.max_iters;
+    c.error_check_interval = cfg.error_check_interval;
+    c.epsilon = cfg.epsilon;
+    c.seed = cfg.seed;
+    c.init = cfg.init == FactorInit::from_files ? 1 : 0;
+    c.error_mode = int32_t(cfg.error_mode);
+    return c;
+}
+
+// Uploads the row window [r0, r1) of `a` (all of its columns) as this context's A slab.
+void upload(oocnmf_ctx* c, MatrixRef a, index_t r0, index_t r1) {
+    const index_t rows = r1 - r0, n = a.cols();
+    if (a.is_dense()) {
+        const DenseMatrix& d = a.dense();
+        const double* base = d.row(a.row_range().begin + r0) + a.col_range().begin;
+        throw_status(oocnmf_load_dense_f64(c, base, d.cols()));
+        return;
+    }
+    // CSR window: keep entries inside the column window, rebase to local coordinates.
+    const CsrMatrix& s = a.sparse();
+    const index_t c0 = a.col_range().begin, c1 = a.col_range().end;
+    std::vector<std::uint64_t> rp(rows + 1, 0), ci;
+    std::vector<double> v;
+    for (index_t i = 0; i < rows; ++i) {
+        const index_t gi = a.row_range().begin + r0 + i;
+        for (index_t p = s.row_ptr()[gi]; p < s.row_ptr()[gi + 1]; ++p) {
+            const index_t j = s.col_idx()[p];
+            if (j < c0 || j >= c1) continue;
+            ci.push_back(j - c0);
+            v.push_back(s.values()[p]);
+        }
+        rp[i + 1] = v.size();
+    }
+    (void)n;
+    throw_status(oocnmf_load_csr_f64(c, rp.data(), ci.data(), v.data()));
+}
+
+void fill_result(NmfResult& res, const oocnmf_info& info, const std::vector<std::uint64_t>& ti,
+                 const std::vector<double>& te) {
+    const index_t nt = std::min<index_t>(info.n_trace, ti.size());
+    for (index_t i = 0; i < nt; ++i) res.error_trace.emplace_back(ti[i], te[i]);
+    res.iterations_run = info.iterations_run;
+    res.converged = info.converged != 0;
+    auto& k = res.counters;
+    k.h_update_s = info.h_update_s;
+    k.w_update_s = info.w_update_s;
+    k.allreduce_s = info.allreduce_s;
+    k.error_check_s = info.error_check_s;
+    k.io_s = info.io_s;
+    k.total_s = info.total_s;
+    k.flops = info.flops;
+    k.peak_resident_bytes = info.peak_resident_bytes;
+}
+
+}  // namespace
+
+NmfResult nmf_serial(MatrixRef a, const NmfConfig& cfg) {
+    cfg.validate();
+    const index_t m = a.rows(), n = a.cols(), k = cfg.k;
+    if (m < 1 || n < 1) throw ShapeError("nmf_serial: empty input " + a.shape_str());
+    if (cfg.init == FactorInit::from_files &&
+        (cfg.init_w->rows() != m || cfg.init_w->cols() != k || cfg.init_h->rows() != k || cfg.init_h->cols() != n))
+        throw ShapeError("nmf_serial: provided factors do not match A and k");
+    Ctx ctx;
+    throw_status(oocnmf_ctx_create(cfg.device, &ctx.c));
+    throw_status(oocnmf_set_problem(ctx.c, m, n, k, 0, m));
+    upload(ctx.c, a, 0, m);
+    if (cfg.init == FactorInit::from_files)
+        throw_status(oocnmf_set_factors_f64(ctx.c, cfg.init_w->data(), cfg.init_h->data()));
+    const oocnmf_config cc = to_c(cfg);
+    std::vector<std::uint64_t> ti(cfg.max_iters / cfg.error_check_interval + 2);
+    std::vector<double> te(ti.size());
+    oocnmf_info info{};
+    throw_status(oocnmf_solve(ctx.c, &cc, ti.data(), te.data(), ti.size(), &info));
+    NmfResult res;
+    res.w = DenseMatrix(m, k);
+    res.h = DenseMatrix(k, n);
+    throw_status(oocnmf_get_factors_f64(ctx.c, res.w.data(), res.h.data()));
+    fill_result(res, info, ti, te);
+    return res;
+}
+
+// ------------------------------------------------------------------------- partition
+std::string to_string(Strategy s) { return s == Strategy::cnmf ? "cnmf" : "rnmf"; }
+Strategy choose_strategy(index_t m, index_t n) { return n > m ? Strategy::cnmf : Strategy::rnmf; }
+
+namespace {
+std::vector<IndexRange> split(index_t extent, index_t parts) {
+    std::vector<std::uint64_t> b(parts + 1);
+    throw_status(oocnmf_split_even(extent, parts, b.data()));
+    std::vector<IndexRange> out;
+    for (index_t p = 0; p < parts; ++p) out.push_back({b[p], b[p + 1]});
+    return out;
+}
+}  // namespace
+
+index_t PartitionPlan::max_slab_extent() const {
+    index_t best = 0;
+    for (const auto& s : slabs) best = std::max(best, strategy == Strategy::cnmf ? s.a_cols.extent() : s.a_rows.extent());
+    return best;
+}
+index_t PartitionPlan::max_batch_extent() const {
+    index_t best = 0;
+    for (const auto& b : batches) best = std::max(best, b.extent());
+    return best;
+}
+
+PartitionPlan make_plan(index_t m, index_t n, index_t k, int n_workers, index_t n_b, Strategy strategy) {
+    if (m < 1 || n < 1 || k < 1) throw ShapeError("make_plan: dimensions must be >= 1");
+    if (n_workers < 1) throw ShapeError("make_plan: need at least one worker");
+    if (n_b < 1) throw ShapeError("make_plan: need at least one batch");
+    const bool col = strategy == Strategy::cnmf;
+    const index_t part_axis = col ? n : m, batch_axis = col ? m : n;
+    if (index_t(n_workers) > part_axis)
+        throw ShapeError("make_plan: " + std::to_string(n_workers) + " workers exceed the " + std::to_string(part_axis) +
+                         " slabs available under " + to_string(strategy));
+    if (n_b > batch_axis) throw ShapeError("make_plan: batches exceed the batched axis");
+    PartitionPlan p;
+    p.strategy = strategy;
+    p.n_workers = n_workers;
+    p.m = m, p.n = n, p.k = k, p.n_b = n_b;
+    const auto sl = split(part_axis, index_t(n_workers));
+    for (int r = 0; r < n_workers; ++r)
+        p.slabs.push_back({r, col ? IndexRange{0, m} : sl[r], col ? sl[r] : IndexRange{0, n}});
+    p.batches = split(batch_axis, n_b);
+    return p;
+}
+
+// ------------------------------------------------------------------------- distributed
+CommHandle::UniqueId CommHandle::new_unique_id() {
+    UniqueId id{};
+    throw_status(oocnmf_comm_unique_id(id.data()));
+    return id;
+}
+
+CommHandle::CommHandle(int rank, int size, int device, const UniqueId& id) : rank_(rank), size_(size), device_(device) {
+    oocnmf_ctx* c = nullptr;
+    throw_status(oocnmf_ctx_create_comm(device, rank, size, id.data(), &c));
+    ctx_ = std::shared_ptr<oocnmf_ctx>(c, [](oocnmf_ctx* p) { oocnmf_ctx_destroy(p); });
+}
+
+NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan, CommHandle& comm,
+                          const StoreConfig& store_cfg, StoreCounters* store_counters_out) {
+    cfg.validate();
+    if (cfg.k != plan.k)
+        throw ShapeError("nmf_distributed: cfg.k=" + std::to_string(cfg.k) + " disagrees with plan.k=" +
+                         std::to_string(plan.k));
+    if (comm.size() != plan.n_workers)
+        throw ShapeError("nmf_distributed: group size " + std::to_string(comm.size()) + " != plan workers " +
+                         std::to_string(plan.n_workers));
+    if (plan.strategy != Strategy::rnmf)
+        throw ShapeError("nmf_distributed: the B200 backend implements the row partition (RNMF) only");
+    if (!a.pdn1_path.empty()) throw IoError("nmf_distributed: PDN1 file sources are not supported by the B200 backend");
+    if (!comm.context()) throw CommError("nmf_distributed: CommHandle has no device context");
+    oocnmf_ctx* c = comm.context();
+    const WorkerSlab& slab = plan.slabs[std::size_t(comm.rank())];
+    const index_t m = plan.m, n = plan.n, k = plan.k, r0 = slab.a_rows.begin, rows = slab.a_rows.extent();
+    throw_status(oocnmf_set_problem(c, m, n, k, r0, rows));
+    if (a.host_f32) {
+        const index_t per_row = ((n + 127) / 128 * 128) * 4;
+        const index_t batch = store_cfg.budget_bytes ? std::max<index_t>(128, store_cfg.budget_bytes / 2 / per_row) : 0;
+        throw_status(oocnmf_attach_host_dense_f32(c, a.host_f32, a.host_ld ? a.host_ld : n, batch));
+    } else {
+        if (a.mem.empty()) throw ShapeError("nmf_distributed: empty A source");
+        if (a.mem.rows() != m || a.mem.cols() != n) throw ShapeError("nmf_distributed: A does not match the plan");
+        upload(c, a.mem, r0, r0 + rows);
+    }
+    if (cfg.init == FactorInit::from_files) {
+        if (cfg.init_w->rows() != m || cfg.init_w->cols() != k || cfg.init_h->rows() != k || cfg.init_h->cols() != n)
+            throw ShapeError("nmf_distributed: provided factors do not match plan");
+        throw_status(oocnmf_set_factors_f64(c, cfg.init_w->row(r0), cfg.init_h->data()));
+    }
+    const oocnmf_config cc = to_c(cfg);
+    std::vector<std::uint64_t> ti(cfg.max_iters / cfg.error_check_interval + 2);
+    std::vector<double> te(ti.size());
+    oocnmf_info info{};
+    throw_status(oocnmf_solve(c, &cc, ti.data(), te.data(), ti.size(), &info));
+    NmfResult res;
+    res.w = DenseMatrix(m, k);
+    res.h = DenseMatrix(k, n);
+    throw_status(oocnmf_get_factors_f64(c, nullptr, res.h.data()));
+    throw_status(oocnmf_gather_w_f64(c, res.w.data()));
+    fill_result(res, info, ti, te);
+    if (store_counters_out) {
+        *store_counters_out = StoreCounters{};
+        store_counters_out->peak_resident_bytes = info.peak_resident_bytes;
+        store_counters_out->bytes_read = index_t(info.h2d_bytes);
+    }
+    return res;
+}
+
+}  // namespace oocnmf

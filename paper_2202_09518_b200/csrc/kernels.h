@@ -1,0 +1,89 @@
+// Host-callable launchers for the MU-NMF device kernels (one TU per kernel family).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace ooc {
+
+// Device layout (per rank): A slab mp x np f32 row-major (zero-padded to multiples of
+// 128), W mp x kp, Ht np x kp (H stored transposed so both factors are "tall"), kp in
+// {8, 16, 32, 64} (k zero-padded; padding is exact for MU: padded entries stay 0).
+constexpr int kTile = 128;  // rows (pass 1, W update) / columns (pass 2, H update) per tile
+
+// ---- dense streaming passes (kernels_dense.cu) ----
+// Pass 1: slots <- partial (A · Ht) per stream-K segment; tiles of 128 rows, steps of 32 cols.
+void plan_aht(StreamK& sk, int64_t mp, int64_t np, int num_sms);
+cudaError_t launch_aht(int kp, const float* A, int64_t lda, const float* Ht, float* slots,
+                       const StreamK& sk, cudaStream_t s);
+// Pass 2: slots <- partial (A^T · W) per segment; tiles of 128 cols, steps of 32 rows.
+void plan_wta(StreamK& sk, int64_t mp, int64_t np, int num_sms);
+cudaError_t launch_wta(int kp, const float* A, int64_t lda, const float* W, float* slots,
+                       const StreamK& sk, cudaStream_t s);
+
+// ---- factor kernels (kernels_factor.cu) ----
+// F (rows x kp, rows a multiple of 128) <- F * N / (F G + eps) rowwise, where N is either
+// a plain rows x kp matrix (n_plain) or stream-K partials (n_slots, sk). Emits per-CTA
+// partial Gram F_new^T F_new (gram_slots[gridDim][kp*kp]), per-CTA f64 partial
+// sum(N .* F_new) (err_slots, may be null) and sets *flag on non-finite output.
+// update == false: only emit the Gram of F (no update).
+int factor_grid(int64_t rows);
+cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
+                                 const float* n_slots, const StreamK* sk, const float* G,
+                                 float eps, bool update, float* gram_slots, double* err_slots,
+                                 int* flag, cudaStream_t s);
+// out[e] = sum_s slots[s*E + e] (fixed order), E = count.
+cudaError_t launch_reduce_slots(const float* slots, int64_t nslots, int64_t count, float* out,
+                                cudaStream_t s);
+// out (tiles*128 x kp) <- [out +] sum of each tile's stream-K partials (ascending CTA order).
+cudaError_t launch_streamk_reduce(int kp, const float* slots, const StreamK& sk, float* out,
+                                  bool accumulate, cudaStream_t s);
+// trace slot <- sqrt(max(0, nA2 - 2 sum(err_slots) + <WtW, HHt>)) / sqrt(nA2)   (f64)
+cudaError_t launch_finalize_error(int kp, const double* err_slots, int64_t n_err,
+                                  const float* wtw, const float* hht, const double* norm_a2,
+                                  const double* direct_res /* null = trace form */,
+                                  double* out_err, cudaStream_t s);
+
+// ---- setup kernels (kernels_setup.cu) ----
+cudaError_t launch_gen_dense_uniform(float* A, int64_t lda, int64_t rows, int64_t cols,
+                                     int64_t row0, int64_t n_global, uint64_t seed,
+                                     uint64_t stream, cudaStream_t s);
+cudaError_t launch_init_factors(float* W, float* Ht, int kp, int64_t k, int64_t rows,
+                                int64_t row0, int64_t n, uint64_t seed, cudaStream_t s);
+cudaError_t launch_cast_pad_f64(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
+                                float* dst, int64_t ld_dst, cudaStream_t s);
+// Partial f64 sums of squares of A (dense, padded) -> out_slots[gridDim]; returns grid.
+int sqnorm_grid();
+cudaError_t launch_sq_norm_dense(const float* A, int64_t lda, int64_t rows, int64_t cols,
+                                 double* out_slots, cudaStream_t s);
+cudaError_t launch_sq_norm_vals(const float* v, int64_t nnz, double* out_slots, cudaStream_t s);
+cudaError_t launch_reduce_f64(const double* slots, int64_t n, double* out, cudaStream_t s);
+// Direct residual sum((A - W Ht^T)^2) partials for the rows x cols window (f64).
+cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t rows,
+                                  int64_t cols, const float* W, const float* Ht,
+                                  double* out_slots, cudaStream_t s);
+cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s);
+
+// ---- CSR kernels (kernels_sparse.cu) ----
+// out (rows x kp) = CSR(rp, ci, v) · B (B rows indexed by column, kp wide).
+cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const float* v,
+                        int64_t rows, const float* B, float* out, cudaStream_t s);
+cudaError_t launch_residual_csr(int kp, const int64_t* rp, const int32_t* ci, const float* v,
+                                int64_t rows, int64_t cols, const float* W, const float* Ht,
+                                double* out_slots, cudaStream_t s);
+// Transpose a CSR (rows x cols) into CSR^T (cols x rows), entries of each output row in
+// ascending source-row order (deterministic). Scratch allocated internally.
+cudaError_t csr_transpose(const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
+                          int64_t cols, int64_t nnz, int64_t* rpT, int32_t* ciT, float* vT,
+                          cudaStream_t s);
+// Reference-semantics generator: counts per row, then fill (row_ptr must be scanned between).
+cudaError_t launch_gen_csr_count(int64_t rows, int64_t row0, int64_t n, uint64_t thresh,
+                                 uint64_t seed, int64_t* counts, cudaStream_t s);
+cudaError_t launch_gen_csr_fill(int64_t rows, int64_t row0, int64_t n, uint64_t thresh,
+                                uint64_t seed, const int64_t* rp, int32_t* ci, float* v,
+                                cudaStream_t s);
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);
+
+}  // namespace ooc

@@ -1,0 +1,206 @@
+// Setup-time and check-time kernels: on-device synthetic inputs and seeded init with the
+// reference's counter RNG, f64->f32 staging, ||A||^2 and the direct residual (f64 sums).
+#include "kernels.h"
+
+namespace ooc {
+namespace {
+
+constexpr int kRedGrid = 4 * 148;
+
+// A[i][j] = (float) U(seed, stream, (row0 + i) * n + j)   (bench/kernels_bench.cpp:12-18)
+__global__ void k_gen_dense_uniform(float* __restrict__ A, int64_t lda, int64_t rows, int64_t cols,
+                                    int64_t row0, int64_t n, uint64_t key) {
+    const int64_t c4n = (cols + 3) / 4;
+    const int64_t total = rows * c4n;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = q / c4n, j = (q % c4n) * 4;
+        const uint64_t base = uint64_t(row0 + i) * uint64_t(n) + uint64_t(j);
+        float v[4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+            v[t] = (j + t < cols) ? __double2float_rn(rng_u01(key, base + t)) : 0.f;
+        *reinterpret_cast<float4*>(A + i * lda + j) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
+// W[i][j] = U(seed,1,(row0+i)*k + j), H[r][c] = U(seed,2,r*n + c) stored as Ht[c][r]
+// (src/nmf_serial.cpp:31-48), rounded to f32; padding stays zero (caller memsets).
+__global__ void k_init_factors(float* __restrict__ W, float* __restrict__ Ht, int kp, int64_t k,
+                               int64_t rows, int64_t row0, int64_t n, uint64_t kw, uint64_t kh) {
+    const int64_t nw = rows * k, nh = n * k;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nw + nh;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        if (q < nw) {
+            const int64_t i = q / k, j = q % k;
+            W[i * kp + j] = __double2float_rn(rng_u01(kw, uint64_t(row0 + i) * k + j));
+        } else {
+            const int64_t e = q - nw, r = e / n, c = e % n;
+            Ht[c * kp + r] = __double2float_rn(rng_u01(kh, uint64_t(r) * n + c));
+        }
+    }
+}
+
+__global__ void k_cast_pad_f64(const double* __restrict__ src, int64_t ld_src, int64_t rows,
+                               int64_t cols, float* __restrict__ dst, int64_t ld_dst) {
+    const int64_t total = rows * cols;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = q / cols, j = q % cols;
+        dst[i * ld_dst + j] = __double2float_rn(src[i * ld_src + j]);
+    }
+}
+
+__device__ double block_sum(double v) {
+    __shared__ double sh[256];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    return sh[0];
+}
+
+__global__ void __launch_bounds__(256) k_sq_norm_dense(const float* __restrict__ A, int64_t lda,
+                                                       int64_t rows, int64_t cols4,
+                                                       double* __restrict__ out) {
+    double acc = 0.0;
+    const int64_t total = rows * cols4;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = q / cols4, j = (q % cols4) * 4;
+        const float4 v = *reinterpret_cast<const float4*>(A + i * lda + j);
+        acc += double(v.x) * v.x + double(v.y) * v.y + double(v.z) * v.z + double(v.w) * v.w;
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) k_sq_norm_vals(const float* __restrict__ v, int64_t nnz,
+                                                      double* __restrict__ out) {
+    double acc = 0.0;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nnz;
+         q += int64_t(gridDim.x) * blockDim.x)
+        acc += double(v[q]) * v[q];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(256) k_reduce_f64(const double* __restrict__ in, int64_t n,
+                                                    double* __restrict__ out) {
+    double acc = 0.0;
+    for (int64_t q = threadIdx.x; q < n; q += 256) acc += in[q];
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) *out = s;
+}
+
+// sum over the window of (A - W Ht^T)^2; thread = one column j for 4 consecutive rows.
+template <int KP>
+__global__ void __launch_bounds__(256) k_residual_dense(const float* __restrict__ A, int64_t lda,
+                                                        int64_t rows, int64_t cols,
+                                                        const float* __restrict__ W,
+                                                        const float* __restrict__ Ht,
+                                                        double* __restrict__ out) {
+    __shared__ float Ws[4][KP];
+    double acc = 0.0;
+    const int64_t rblocks = (rows + 3) / 4, cblocks = (cols + 255) / 256;
+    for (int64_t b = blockIdx.x; b < rblocks * cblocks; b += gridDim.x) {
+        const int64_t rb = b / cblocks, cb = b % cblocks;
+        __syncthreads();
+        for (int e = threadIdx.x; e < 4 * KP; e += 256) {
+            const int64_t r = rb * 4 + e / KP;
+            Ws[e / KP][e % KP] = r < rows ? W[r * KP + e % KP] : 0.f;
+        }
+        __syncthreads();
+        const int64_t j = cb * 256 + threadIdx.x;
+        if (j >= cols) continue;
+        float h[KP];
+#pragma unroll
+        for (int q = 0; q < KP; ++q) h[q] = Ht[j * KP + q];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int64_t r = rb * 4 + t;
+            if (r >= rows) break;
+            float wh = 0.f;
+#pragma unroll
+            for (int q = 0; q < KP; ++q) wh = fmaf(Ws[t][q], h[q], wh);
+            const double d = double(A[r * lda + j]) - double(wh);
+            acc += d * d;
+        }
+    }
+    const double s = block_sum(acc);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag) {
+    bool bad = false;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += int64_t(gridDim.x) * blockDim.x)
+        bad |= !isfinite(x[q]);
+    if (bad) atomicOr(flag, 1);
+}
+
+unsigned grid_for(int64_t work, int per_thread = 1) {
+    const int64_t b = (work / per_thread + 255) / 256;
+    return unsigned(b < 1 ? 1 : (b > 65535 * 16 ? 65535 * 16 : b));
+}
+
+}  // namespace
+
+int sqnorm_grid() { return kRedGrid; }
+
+cudaError_t launch_gen_dense_uniform(float* A, int64_t lda, int64_t rows, int64_t cols, int64_t row0,
+                                     int64_t n_global, uint64_t seed, uint64_t stream, cudaStream_t s) {
+    k_gen_dense_uniform<<<grid_for(rows * ((cols + 3) / 4), 8), 256, 0, s>>>(
+        A, lda, rows, cols, row0, n_global, rng_key(seed, stream));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_init_factors(float* W, float* Ht, int kp, int64_t k, int64_t rows, int64_t row0,
+                                int64_t n, uint64_t seed, cudaStream_t s) {
+    k_init_factors<<<grid_for((rows + n) * k, 4), 256, 0, s>>>(
+        W, Ht, kp, k, rows, row0, n, rng_key(seed, kStreamW), rng_key(seed, kStreamH));
+    return cudaGetLastError();
+}
+
+cudaError_t launch_cast_pad_f64(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
+                                float* dst, int64_t ld_dst, cudaStream_t s) {
+    k_cast_pad_f64<<<grid_for(rows * cols, 4), 256, 0, s>>>(src, ld_src, rows, cols, dst, ld_dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sq_norm_dense(const float* A, int64_t lda, int64_t rows, int64_t cols,
+                                 double* out_slots, cudaStream_t s) {
+    k_sq_norm_dense<<<kRedGrid, 256, 0, s>>>(A, lda, rows, (cols + 3) / 4, out_slots);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_sq_norm_vals(const float* v, int64_t nnz, double* out_slots, cudaStream_t s) {
+    k_sq_norm_vals<<<kRedGrid, 256, 0, s>>>(v, nnz, out_slots);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_f64(const double* slots, int64_t n, double* out, cudaStream_t s) {
+    k_reduce_f64<<<1, 256, 0, s>>>(slots, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t rows, int64_t cols,
+                                  const float* W, const float* Ht, double* out_slots, cudaStream_t s) {
+    switch (kp) {
+        case 8: k_residual_dense<8><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
+        case 16: k_residual_dense<16><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
+        case 32: k_residual_dense<32><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
+        case 64: k_residual_dense<64><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s) {
+    k_check_finite<<<grid_for(n, 8), 256, 0, s>>>(x, n, flag);
+    return cudaGetLastError();
+}
+
+}  // namespace ooc

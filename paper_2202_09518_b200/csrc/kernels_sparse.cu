@@ -1,0 +1,300 @@
+// CSR path of the MU iteration (config 3: sparse synthetic A).
+//
+//   A·H^T   CSR SpMM, one row per (sub)warp, lanes span the kp outputs so each nonzero
+//           gathers one contiguous kp-wide row of Ht (reference: matmul_acc CSR,
+//           src/kernels.cpp:46-67)
+//   A^T·W   the reference scatters a_ij·W[i,:] into column j serially
+//           (src/kernels.cpp:102-124). A is iteration-invariant, so we build CSR(A^T)
+//           once (stable radix sort by column => deterministic order) and run the same
+//           gather SpMM on it: no atomics, no scatter.
+//   generator  reference semantics of gen_sparse_random (src/synth.cpp:60-86) on device.
+#include <cub/cub.cuh>
+
+#include "kernels.h"
+
+namespace ooc {
+namespace {
+
+template <int KP>
+__global__ void __launch_bounds__(256) k_spmm(const int64_t* __restrict__ rp,
+                                              const int32_t* __restrict__ ci,
+                                              const float* __restrict__ v, int64_t rows,
+                                              const float* __restrict__ B, float* __restrict__ out) {
+    constexpr int LPR = KP < 32 ? KP : 32;  // lanes per row
+    constexpr int VEC = KP / LPR;           // outputs per lane
+    constexpr int RPW = 32 / LPR;           // rows per warp
+    const int lane = threadIdx.x & 31, sub = lane / LPR, l = lane % LPR;
+    const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t wg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wg * RPW < rows; wg += warps) {
+        const int64_t row = wg * RPW + sub;
+        const bool live = row < rows;
+        const int64_t beg = live ? rp[row] : 0, end = live ? rp[row + 1] : 0;
+        float acc[VEC];
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) acc[t] = 0.f;
+        for (int64_t p0 = beg; __any_sync(0xffffffffu, p0 < end); p0 += LPR) {
+            const int64_t p = p0 + l;
+            const int col = p < end ? ci[p] : 0;
+            const float val = p < end ? v[p] : 0.f;
+#pragma unroll
+            for (int t = 0; t < LPR; ++t) {
+                const int c = __shfl_sync(0xffffffffu, col, sub * LPR + t);
+                const float w = __shfl_sync(0xffffffffu, val, sub * LPR + t);
+                if (p0 + t < end) {
+                    if constexpr (VEC == 1) {
+                        acc[0] = fmaf(w, B[int64_t(c) * KP + l], acc[0]);
+                    } else {
+                        const float2 b = reinterpret_cast<const float2*>(B + int64_t(c) * KP)[l];
+                        acc[0] = fmaf(w, b.x, acc[0]);
+                        acc[1] = fmaf(w, b.y, acc[1]);
+                    }
+                }
+            }
+        }
+        if (live) {
+            if constexpr (VEC == 1)
+                out[row * KP + l] = acc[0];
+            else
+                reinterpret_cast<float2*>(out + row * KP)[l] = make_float2(acc[0], acc[1]);
+        }
+    }
+}
+
+__device__ double block_sum256(double v) {
+    __shared__ double sh[256];
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+        if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+        __syncthreads();
+    }
+    return sh[0];
+}
+
+// sum over nonzeros of a_ij * (W_i · Ht_j)  (f64) — the cross term of ||A - WH||^2.
+template <int KP>
+__global__ void __launch_bounds__(256) k_cross_csr(const int64_t* __restrict__ rp,
+                                                   const int32_t* __restrict__ ci,
+                                                   const float* __restrict__ v, int64_t rows,
+                                                   const float* __restrict__ W,
+                                                   const float* __restrict__ Ht,
+                                                   double* __restrict__ out) {
+    double acc = 0.0;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
+            const int64_t j = ci[p];
+            float s = 0.f;
+#pragma unroll
+            for (int q = 0; q < KP; ++q) s = fmaf(W[i * KP + q], Ht[j * KP + q], s);
+            acc += double(v[p]) * double(s);
+        }
+    }
+    const double s = block_sum256(acc);
+    if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+__global__ void k_row_ids(const int64_t* __restrict__ rp, int64_t rows, int32_t* __restrict__ rid) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+         i += int64_t(gridDim.x) * blockDim.x)
+        for (int64_t p = rp[i]; p < rp[i + 1]; ++p) rid[p] = int32_t(i);
+}
+
+__global__ void k_col_hist(const int32_t* __restrict__ ci, int64_t nnz,
+                           unsigned long long* __restrict__ cnt) {
+    for (int64_t p = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; p < nnz;
+         p += int64_t(gridDim.x) * blockDim.x)
+        atomicAdd(cnt + ci[p], 1ull);
+}
+
+__global__ void k_gather_t(const int32_t* __restrict__ perm, const int32_t* __restrict__ rid,
+                           const float* __restrict__ v, int64_t nnz, int32_t* __restrict__ ciT,
+                           float* __restrict__ vT) {
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nnz;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const int32_t p = perm[q];
+        ciT[q] = rid[p];
+        vT[q] = v[p];
+    }
+}
+
+__global__ void k_iota(int32_t* x, int64_t n) {
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
+         q += int64_t(gridDim.x) * blockDim.x)
+        x[q] = int32_t(q);
+}
+
+// Generator: each thread tests kCpt consecutive cells of a row; rows are strided over blocks.
+constexpr int kCpt = 16;
+
+__device__ __forceinline__ uint32_t hit_mask(uint64_t km, uint64_t flat0, int64_t j0, int64_t n,
+                                             uint64_t thresh) {
+    uint32_t m = 0;
+#pragma unroll
+    for (int t = 0; t < kCpt; ++t)
+        if (j0 + t < n && rng_bits53(km, flat0 + t) < thresh) m |= 1u << t;
+    return m;
+}
+
+__global__ void __launch_bounds__(256) k_gen_csr_count(int64_t rows, int64_t row0, int64_t n,
+                                                       uint64_t thresh, uint64_t km,
+                                                       int64_t* __restrict__ counts) {
+    __shared__ int64_t sh[256];
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+        int64_t c = 0;
+        const uint64_t base = uint64_t(row0 + i) * uint64_t(n);
+        for (int64_t j0 = int64_t(threadIdx.x) * kCpt; j0 < n; j0 += 256 * kCpt)
+            c += __popc(hit_mask(km, base + j0, j0, n, thresh));
+        sh[threadIdx.x] = c;
+        __syncthreads();
+        for (int s = 128; s > 0; s >>= 1) {
+            if (threadIdx.x < s) sh[threadIdx.x] += sh[threadIdx.x + s];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) counts[i] = sh[0];
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gen_csr_fill(int64_t rows, int64_t row0, int64_t n,
+                                                      uint64_t thresh, uint64_t km, uint64_t kv,
+                                                      const int64_t* __restrict__ rp,
+                                                      int32_t* __restrict__ ci,
+                                                      float* __restrict__ v) {
+    using Scan = cub::BlockScan<int, 256>;
+    __shared__ typename Scan::TempStorage tmp;
+    __shared__ int total_sh;
+    for (int64_t i = blockIdx.x; i < rows; i += gridDim.x) {
+        int64_t pos = rp[i];
+        const uint64_t base = uint64_t(row0 + i) * uint64_t(n);
+        for (int64_t c0 = 0; c0 < n; c0 += 256 * kCpt) {
+            const int64_t j0 = c0 + int64_t(threadIdx.x) * kCpt;
+            const uint32_t m = j0 < n ? hit_mask(km, base + j0, j0, n, thresh) : 0u;
+            int off, total;
+            Scan(tmp).ExclusiveSum(int(__popc(m)), off, total);
+            uint32_t mm = m;
+            int64_t q = pos + off;
+            while (mm) {
+                const int t = __ffs(mm) - 1;
+                mm &= mm - 1;
+                ci[q] = int32_t(j0 + t);
+                v[q] = __double2float_rn(double(rng_bits53(kv, base + j0 + t)) * 0x1.0p-53);
+                ++q;
+            }
+            if (threadIdx.x == 0) total_sh = total;
+            __syncthreads();
+            pos += total_sh;
+            __syncthreads();
+        }
+    }
+}
+
+unsigned grid_for(int64_t work) {
+    const int64_t b = (work + 255) / 256;
+    return unsigned(b < 1 ? 1 : (b > 148 * 64 ? 148 * 64 : b));
+}
+
+}  // namespace
+
+cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
+                        const float* B, float* out, cudaStream_t s) {
+    const int64_t warps = (rows * (kp < 32 ? kp : 32) + 31) / 32;
+    const unsigned grid = grid_for(warps * 32);
+    switch (kp) {
+        case 8: k_spmm<8><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+        case 16: k_spmm<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+        case 32: k_spmm<32><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+        case 64: k_spmm<64><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_residual_csr(int kp, const int64_t* rp, const int32_t* ci, const float* v,
+                                int64_t rows, int64_t cols, const float* W, const float* Ht,
+                                double* out_slots, cudaStream_t s) {
+    (void)cols;
+    const unsigned grid = 4 * 148;
+    switch (kp) {
+        case 8: k_cross_csr<8><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
+        case 16: k_cross_csr<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
+        case 32: k_cross_csr<32><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
+        case 64: k_cross_csr<64><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s) {
+    size_t bytes = 0;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, s);
+    if (e != cudaSuccess) return e;
+    void* tmp = nullptr;
+    if ((e = cudaMallocAsync(&tmp, bytes, s)) != cudaSuccess) return e;
+    e = cub::DeviceScan::ExclusiveSum(tmp, bytes, in, out, n, s);
+    cudaFreeAsync(tmp, s);
+    return e;
+}
+
+cudaError_t csr_transpose(const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
+                          int64_t cols, int64_t nnz, int64_t* rpT, int32_t* ciT, float* vT,
+                          cudaStream_t s) {
+    cudaError_t e;
+    int32_t *rid = nullptr, *keys_out = nullptr, *perm_in = nullptr, *perm = nullptr;
+    unsigned long long* cnt = nullptr;
+    void* tmp = nullptr;
+    size_t bytes = 0;
+    const int64_t nz = nnz > 0 ? nnz : 1;
+#define OOC_TRY(x)                   \
+    if ((e = (x)) != cudaSuccess) {  \
+        goto done;                   \
+    }
+    OOC_TRY(cudaMallocAsync(&rid, nz * sizeof(int32_t), s));
+    OOC_TRY(cudaMallocAsync(&keys_out, nz * sizeof(int32_t), s));
+    OOC_TRY(cudaMallocAsync(&perm_in, nz * sizeof(int32_t), s));
+    OOC_TRY(cudaMallocAsync(&perm, nz * sizeof(int32_t), s));
+    OOC_TRY(cudaMallocAsync(&cnt, (cols + 1) * sizeof(unsigned long long), s));
+    OOC_TRY(cudaMemsetAsync(cnt, 0, (cols + 1) * sizeof(unsigned long long), s));
+    if (nnz > 0) {
+        k_row_ids<<<grid_for(rows), 256, 0, s>>>(rp, rows, rid);
+        k_iota<<<grid_for(nnz), 256, 0, s>>>(perm_in, nnz);
+        k_col_hist<<<grid_for(nnz), 256, 0, s>>>(ci, nnz, cnt);
+        int bits = 1;
+        while ((int64_t(1) << bits) < cols) ++bits;
+        OOC_TRY(cub::DeviceRadixSort::SortPairs(nullptr, bytes, ci, keys_out, perm_in, perm, nnz, 0,
+                                                bits, s));
+        OOC_TRY(cudaMallocAsync(&tmp, bytes, s));
+        OOC_TRY(cub::DeviceRadixSort::SortPairs(tmp, bytes, ci, keys_out, perm_in, perm, nnz, 0, bits,
+                                                s));
+        k_gather_t<<<grid_for(nnz), 256, 0, s>>>(perm, rid, v, nnz, ciT, vT);
+    }
+    static_assert(sizeof(unsigned long long) == sizeof(int64_t), "");
+    OOC_TRY(exclusive_scan_i64(reinterpret_cast<const int64_t*>(cnt), rpT, cols + 1, s));
+    e = cudaGetLastError();
+done:
+#undef OOC_TRY
+    if (rid) cudaFreeAsync(rid, s);
+    if (keys_out) cudaFreeAsync(keys_out, s);
+    if (perm_in) cudaFreeAsync(perm_in, s);
+    if (perm) cudaFreeAsync(perm, s);
+    if (cnt) cudaFreeAsync(cnt, s);
+    if (tmp) cudaFreeAsync(tmp, s);
+    return e;
+}
+
+cudaError_t launch_gen_csr_count(int64_t rows, int64_t row0, int64_t n, uint64_t thresh, uint64_t seed,
+                                 int64_t* counts, cudaStream_t s) {
+    const unsigned grid = unsigned(rows < 148 * 16 ? rows : 148 * 16);
+    k_gen_csr_count<<<grid, 256, 0, s>>>(rows, row0, n, thresh, rng_key(seed, kStreamSparseMask), counts);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gen_csr_fill(int64_t rows, int64_t row0, int64_t n, uint64_t thresh, uint64_t seed,
+                                const int64_t* rp, int32_t* ci, float* v, cudaStream_t s) {
+    const unsigned grid = unsigned(rows < 148 * 16 ? rows : 148 * 16);
+    k_gen_csr_fill<<<grid, 256, 0, s>>>(rows, row0, n, thresh, rng_key(seed, kStreamSparseMask),
+                                        rng_key(seed, kStreamSparseVal), rp, ci, v);
+    return cudaGetLastError();
+}
+
+}  // namespace ooc

@@ -1,0 +1,1038 @@
+// C-ABI backend: per-GPU context, HBM layout, and the MU iteration loop.
+//
+// The loop mirrors nmf_serial (src/nmf_serial.cpp:83-117) / the RNMF worker
+// (src/nmf_distributed.cpp:151-262): W update, then H update, error every
+// error_check_interval iterations and on the last, early exit at eta. Differences that are
+// pure B200 engineering:
+//  * A lives in HBM as f32 (or streams from host memory out-of-core); factors are f32 with
+//    f64 accumulation for every scalar (norms, trace-form error).
+//  * The H update's two all-reduces per batch (W^T W, then W^T A_p) are one NCCL
+//    all-reduce of a packed [W^T A | W^T W] buffer per iteration.
+//  * The error is the trace form ||A||^2 - 2<W^T A, H> + <W^T W, H H^T>, whose terms all
+//    exist after the H update, so error checks cost no pass over A (error_mode 1 restores a
+//    direct residual pass).
+//  * Nothing syncs the host except error checks (one 16-byte D2H every interval).
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "oocnmf_b200.h"
+
+using namespace ooc;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+    int code;
+    std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& msg) { throw Fail{code, msg}; }
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) fail(OOCNMF_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString(e));
+}
+void nck(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) fail(OOCNMF_ERR_COMM, std::string(what) + ": " + ncclGetErrorString(r));
+}
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return OOCNMF_OK;
+    } catch (const Fail& x) {
+        g_err = x.msg;
+        return x.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "host allocation failed";
+        return OOCNMF_ERR_DEVICE;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return OOCNMF_ERR_DEVICE;
+    }
+}
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+int pad_k(uint64_t k) {
+    if (k < 1) fail(OOCNMF_ERR_SHAPE, "k must be >= 1");
+    if (k <= 8) return 8;
+    if (k <= 16) return 16;
+    if (k <= 32) return 32;
+    if (k <= 64) return 64;
+    fail(OOCNMF_ERR_SHAPE, "k=" + std::to_string(k) + " exceeds the supported maximum of 64");
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void alloc(size_t b, const char* what) {
+        if (b == bytes && p) return;
+        release();
+        if (b == 0) return;
+        const cudaError_t e = cudaMalloc(&p, b);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            fail(OOCNMF_ERR_DEVICE, std::string("cudaMalloc(") + std::to_string(b) + " B) for " + what +
+                                        ": " + cudaGetErrorString(e));
+        }
+        bytes = b;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+enum class Kind { none, dense, csr, host };
+
+// indices into the f64 scalar scratch
+enum Scal { kNormA2 = 0, kErr = 1, kRes = 2, kCross = 3, kNumScal = 8 };
+
+// events recorded per iteration (see solve())
+enum Ev { eStart, eAht, eWdone, eWta, eReduced, eComm, eHdone, kEvPerIter };
+
+}  // namespace
+
+struct oocnmf_ctx {
+    int device = 0, rank = 0, nranks = 1, num_sms = 148;
+    ncclComm_t comm = nullptr;
+    cudaStream_t stream = nullptr, copy_stream = nullptr;
+
+    uint64_t m = 0, n = 0, k = 0, row0 = 0, rows = 0;
+    int kp = 0;
+    int64_t mp = 0, np = 0;
+    bool problem_set = false;
+
+    Kind kind = Kind::none;
+    DevBuf A;                       // dense: mp x np f32
+    DevBuf rp, ci, v, rpT, ciT, vT; // csr: slab rows x n and its transpose n x rows
+    int64_t nnz = 0;
+    const float* hA = nullptr;      // out-of-core host slab
+    uint64_t hlda = 0;
+    int64_t batch_rows = 0;
+    DevBuf stage[2];
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+
+    DevBuf W, Ht, HHt, packed, N1, slots1, slots2, gram_w, gram_h, err_slots, red_slots, scal, flag;
+    StreamK sk1, sk2;            // in-core dense passes
+    StreamK sk1b[2], sk2b[2];    // out-of-core: full batch / last batch
+    bool norm_valid = false, factors_set = false, factors_valid = false;
+    double norm_a2 = 0.0;
+    double* hpin = nullptr;      // pinned readback: [err, flag]
+    std::vector<cudaEvent_t> evs;
+    uint64_t launches = 0;
+
+    float* wta() const { return packed.as<float>(); }
+    float* wtw() const { return packed.as<float>() + np * kp; }
+    int64_t packed_count() const { return np * kp + int64_t(kp) * kp; }
+};
+
+namespace {
+
+void set_dev(oocnmf_ctx* c) { ck(cudaSetDevice(c->device), "cudaSetDevice"); }
+
+void need_problem(oocnmf_ctx* c) {
+    if (!c->problem_set) fail(OOCNMF_ERR_SHAPE, "oocnmf_set_problem has not been called");
+}
+
+void count(oocnmf_ctx* c, cudaError_t e, const char* what) {
+    ck(e, what);
+    ++c->launches;
+}
+
+void alloc_factors(oocnmf_ctx* c) {
+    const int kp = c->kp;
+    c->W.alloc(size_t(c->mp) * kp * 4, "W");
+    c->Ht.alloc(size_t(c->np) * kp * 4, "Ht");
+    c->HHt.alloc(size_t(kp) * kp * 4, "HHt");
+    c->packed.alloc(size_t(c->packed_count()) * 4, "packed");
+    const int gw = factor_grid(c->mp / kTile), gh = factor_grid(c->np / kTile);
+    c->gram_w.alloc(size_t(gw) * kp * kp * 4, "gram_w");
+    c->gram_h.alloc(size_t(gh) * kp * kp * 4, "gram_h");
+    c->err_slots.alloc(size_t(std::max(gh, sqnorm_grid())) * 8, "err_slots");
+    c->red_slots.alloc(size_t(sqnorm_grid()) * 8, "red_slots");
+    c->scal.alloc(kNumScal * 8, "scalars");
+    c->flag.alloc(4, "flag");
+    ck(cudaMemsetAsync(c->W.p, 0, c->W.bytes, c->stream), "memset W");
+    ck(cudaMemsetAsync(c->Ht.p, 0, c->Ht.bytes, c->stream), "memset Ht");
+    ck(cudaMemsetAsync(c->flag.p, 0, 4, c->stream), "memset flag");
+}
+
+void plan_dense(oocnmf_ctx* c) {
+    plan_aht(c->sk1, c->mp, c->np, c->num_sms);
+    plan_wta(c->sk2, c->mp, c->np, c->num_sms);
+    c->slots1.alloc(size_t(c->sk1.G * c->sk1.smax) * kTile * c->kp * 4, "slots1");
+    c->slots2.alloc(size_t(c->sk2.G * c->sk2.smax) * kTile * c->kp * 4, "slots2");
+}
+
+void reset_source(oocnmf_ctx* c) {
+    c->A.release();
+    c->rp.release(), c->ci.release(), c->v.release();
+    c->rpT.release(), c->ciT.release(), c->vT.release();
+    c->stage[0].release(), c->stage[1].release();
+    c->hA = nullptr;
+    c->kind = Kind::none;
+    c->norm_valid = false;
+}
+
+void compute_norm(oocnmf_ctx* c) {
+    double* slots = c->red_slots.as<double>();
+    double* out = c->scal.as<double>() + kNormA2;
+    if (c->kind == Kind::dense) {
+        count(c, launch_sq_norm_dense(c->A.as<float>(), c->np, c->mp, c->np, slots, c->stream), "sq_norm");
+    } else if (c->kind == Kind::csr) {
+        count(c, launch_sq_norm_vals(c->v.as<float>(), c->nnz, slots, c->stream), "sq_norm");
+    } else {
+        // out-of-core: stream the slab once through the staging buffers.
+        double acc = 0.0;
+        std::vector<double> part(sqnorm_grid());
+        for (int64_t b0 = 0; b0 < int64_t(c->rows); b0 += c->batch_rows) {
+            const int64_t br = std::min<int64_t>(c->batch_rows, int64_t(c->rows) - b0);
+            ck(cudaMemcpy2DAsync(c->stage[0].p, c->np * 4, c->hA + b0 * c->hlda, c->hlda * 4, c->n * 4, br,
+                                 cudaMemcpyHostToDevice, c->stream),
+               "H2D batch");
+            count(c, launch_sq_norm_dense(c->stage[0].as<float>(), c->np, br, c->np, slots, c->stream), "sq_norm");
+            count(c, launch_reduce_f64(slots, sqnorm_grid(), out, c->stream), "reduce");
+            double v = 0;
+            ck(cudaMemcpyAsync(&v, out, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+            acc += v;
+        }
+        ck(cudaMemcpyAsync(out, &acc, 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        goto reduced;
+    }
+    count(c, launch_reduce_f64(slots, sqnorm_grid(), out, c->stream), "reduce_f64");
+reduced:
+    if (c->nranks > 1) nck(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
+    ck(cudaMemcpyAsync(&c->norm_a2, out, 8, cudaMemcpyDeviceToHost, c->stream), "D2H norm");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->norm_valid = true;
+}
+
+// HH^T of the current Ht (gram only).
+void gram_h(oocnmf_ctx* c) {
+    const int kp = c->kp;
+    count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, nullptr, nullptr, nullptr, nullptr, 0.f, false,
+                                  c->gram_h.as<float>(), nullptr, c->flag.as<int>(), c->stream),
+          "gram H");
+    count(c, launch_reduce_slots(c->gram_h.as<float>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
+                                 c->HHt.as<float>(), c->stream),
+          "reduce HHt");
+}
+
+// W update + accumulation of the rank-local [W^T A | W^T W] into c->packed.
+void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
+    const int kp = c->kp;
+    const int gw = factor_grid(c->mp / kTile);
+    cudaStream_t s = c->stream;
+    auto rec = [&](int i) {
+        if (timed) ck(cudaEventRecord(ev[i], s), "event");
+    };
+    rec(eStart);
+    if (c->kind == Kind::dense) {
+        count(c, launch_aht(kp, c->A.as<float>(), c->np, c->Ht.as<float>(), c->slots1.as<float>(), c->sk1, s), "aht");
+        rec(eAht);
+        count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, c->slots1.as<float>(), &c->sk1,
+                                      c->HHt.as<float>(), eps, true, c->gram_w.as<float>(), nullptr,
+                                      c->flag.as<int>(), s),
+              "W update");
+        count(c, launch_reduce_slots(c->gram_w.as<float>(), gw, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
+        rec(eWdone);
+        count(c, launch_wta(kp, c->A.as<float>(), c->np, c->W.as<float>(), c->slots2.as<float>(), c->sk2, s), "wta");
+        rec(eWta);
+        count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce WtA");
+        rec(eReduced);
+    } else if (c->kind == Kind::csr) {
+        count(c, launch_spmm(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows,
+                             c->Ht.as<float>(), c->N1.as<float>(), s),
+              "spmm A Ht");
+        rec(eAht);
+        count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
+                                      c->HHt.as<float>(), eps, true, c->gram_w.as<float>(), nullptr,
+                                      c->flag.as<int>(), s),
+              "W update");
+        count(c, launch_reduce_slots(c->gram_w.as<float>(), gw, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
+        rec(eWdone);
+        count(c, launch_spmm(kp, c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), c->vT.as<float>(), c->n,
+                             c->W.as<float>(), c->wta(), s),
+              "spmm At W");
+        rec(eWta);
+        rec(eReduced);
+    } else {
+        // Out-of-core fused row-batch schedule: each batch crosses the host link once and
+        // serves both its W rows' update and its W^T A contribution.
+        const int64_t nb = (int64_t(c->rows) + c->batch_rows - 1) / c->batch_rows;
+        const int gwb = factor_grid(c->batch_rows / kTile);
+        for (int64_t b = 0; b < nb; ++b) {
+            const int si = int(b & 1);
+            const int64_t b0 = b * c->batch_rows;
+            const int64_t br = std::min<int64_t>(c->batch_rows, int64_t(c->rows) - b0);
+            const int64_t brp = round_up(br, kTile);
+            const StreamK& s1 = (br == c->batch_rows) ? c->sk1b[0] : c->sk1b[1];
+            const StreamK& s2 = (br == c->batch_rows) ? c->sk2b[0] : c->sk2b[1];
+            float* st = c->stage[si].as<float>();
+            ck(cudaStreamWaitEvent(c->copy_stream, c->ev_free[si], 0), "wait free");
+            if (brp != br)
+                ck(cudaMemsetAsync(st + br * c->np, 0, size_t(brp - br) * c->np * 4, c->copy_stream), "memset tail");
+            ck(cudaMemcpy2DAsync(st, c->np * 4, c->hA + b0 * c->hlda, c->hlda * 4, c->n * 4, br,
+                                 cudaMemcpyHostToDevice, c->copy_stream),
+               "H2D batch");
+            ck(cudaEventRecord(c->ev_copied[si], c->copy_stream), "event");
+            ck(cudaStreamWaitEvent(s, c->ev_copied[si], 0), "wait copied");
+            float* Wb = c->W.as<float>() + b0 * kp;
+            count(c, launch_aht(kp, st, c->np, c->Ht.as<float>(), c->slots1.as<float>(), s1, s), "aht");
+            count(c, launch_factor_update(kp, Wb, brp, nullptr, c->slots1.as<float>(), &s1, c->HHt.as<float>(),
+                                          eps, true, c->gram_w.as<float>() + b * gwb * kp * kp, nullptr,
+                                          c->flag.as<int>(), s),
+                  "W update");
+            count(c, launch_wta(kp, st, c->np, Wb, c->slots2.as<float>(), s2, s), "wta");
+            count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), s2, c->wta(), b > 0, s), "reduce WtA");
+            ck(cudaEventRecord(c->ev_free[si], s), "event");
+        }
+        count(c, launch_reduce_slots(c->gram_w.as<float>(), nb * gwb, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
+        rec(eAht);
+        rec(eWdone);
+        rec(eWta);
+        rec(eReduced);
+    }
+}
+
+void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
+    const int kp = c->kp;
+    cudaStream_t s = c->stream;
+    if (c->nranks > 1)
+        nck(ncclAllReduce(c->packed.p, c->packed.p, size_t(c->packed_count()), ncclFloat, ncclSum, c->comm, s),
+            "allreduce [WtA|WtW]");
+    if (timed) ck(cudaEventRecord(ev[eComm], s), "event");
+    count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, c->wta(), nullptr, nullptr, c->wtw(), eps, true,
+                                  c->gram_h.as<float>(), c->err_slots.as<double>(), c->flag.as<int>(), s),
+          "H update");
+    count(c, launch_reduce_slots(c->gram_h.as<float>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
+                                 c->HHt.as<float>(), s),
+          "reduce HHt");
+    if (timed) ck(cudaEventRecord(ev[eHdone], s), "event");
+}
+
+double error_check(oocnmf_ctx* c, int error_mode, int* bad) {
+    const int kp = c->kp;
+    cudaStream_t s = c->stream;
+    double* scal = c->scal.as<double>();
+    const double* direct = nullptr;
+    const double* eslots = c->err_slots.as<double>();
+    int64_t n_err = factor_grid(c->np / kTile);
+    if (error_mode == 1) {
+        if (c->kind == Kind::dense) {
+            count(c, launch_residual_dense(kp, c->A.as<float>(), c->np, c->rows, c->n, c->W.as<float>(),
+                                           c->Ht.as<float>(), c->red_slots.as<double>(), s),
+                  "residual");
+            count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kRes, s), "reduce");
+            if (c->nranks > 1)
+                nck(ncclAllReduce(scal + kRes, scal + kRes, 1, ncclDouble, ncclSum, c->comm, s), "allreduce res");
+            direct = scal + kRes;
+        } else if (c->kind == Kind::csr) {
+            count(c, launch_residual_csr(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows,
+                                         c->n, c->W.as<float>(), c->Ht.as<float>(), c->red_slots.as<double>(), s),
+                  "cross");
+            count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kCross, s), "reduce");
+            if (c->nranks > 1)
+                nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s),
+                    "allreduce cross");
+            eslots = scal + kCross;
+            n_err = 1;
+        }
+    }
+    count(c, launch_finalize_error(kp, eslots, n_err, c->wtw(), c->HHt.as<float>(), scal + kNormA2, direct,
+                                   scal + kErr, s),
+          "finalize");
+    ck(cudaMemcpyAsync(c->hpin, scal + kErr, 8, cudaMemcpyDeviceToHost, s), "D2H err");
+    ck(cudaMemcpyAsync(c->hpin + 1, c->flag.p, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
+    ck(cudaStreamSynchronize(s), "sync");
+    int f = 0;
+    std::memcpy(&f, c->hpin + 1, 4);
+    *bad = f;
+    return c->hpin[0];
+}
+
+void ensure_events(oocnmf_ctx* c, size_t n) {
+    while (c->evs.size() < n) {
+        cudaEvent_t e;
+        ck(cudaEventCreate(&e), "cudaEventCreate");
+        c->evs.push_back(e);
+    }
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    ck(cudaEventElapsedTime(&ms, a, b), "cudaEventElapsedTime");
+    return ms;
+}
+
+void prepare_factors(oocnmf_ctx* c, const oocnmf_config* cfg) {
+    if (cfg->init == 1) {
+        if (!c->factors_set)
+            fail(OOCNMF_ERR_SHAPE, "init=from_files requires factors (oocnmf_set_factors_f64)");
+    } else if (cfg->init == 2) {
+        if (!c->factors_valid) fail(OOCNMF_ERR_SHAPE, "init=continue requires resident factors");
+    } else {
+        ck(cudaMemsetAsync(c->W.p, 0, c->W.bytes, c->stream), "memset W");
+        ck(cudaMemsetAsync(c->Ht.p, 0, c->Ht.bytes, c->stream), "memset Ht");
+        count(c, launch_init_factors(c->W.as<float>(), c->Ht.as<float>(), c->kp, c->k, c->rows, c->row0, c->n,
+                                     cfg->seed, c->stream),
+              "init");
+    }
+    c->factors_valid = true;
+}
+
+void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, double* trace_err,
+                uint64_t trace_cap, oocnmf_info* info) {
+    need_problem(c);
+    if (!cfg) fail(OOCNMF_ERR_SHAPE, "null config");
+    if (cfg->k != c->k)
+        fail(OOCNMF_ERR_SHAPE, "config k=" + std::to_string(cfg->k) + " disagrees with problem k=" + std::to_string(c->k));
+    if (!(cfg->eta >= 0)) fail(OOCNMF_ERR_SHAPE, "NmfConfig: eta must be >= 0");
+    if (cfg->max_iters < 1) fail(OOCNMF_ERR_SHAPE, "NmfConfig: max_iters must be >= 1");
+    if (cfg->error_check_interval < 1) fail(OOCNMF_ERR_SHAPE, "NmfConfig: error_check_interval must be >= 1");
+    if (!(cfg->epsilon > 0)) fail(OOCNMF_ERR_SHAPE, "NmfConfig: epsilon must be > 0");
+    if (cfg->error_mode == 1 && c->kind == Kind::host)
+        fail(OOCNMF_ERR_SHAPE, "error_mode=direct is not supported out-of-core");
+    if (c->kind == Kind::none) fail(OOCNMF_ERR_SHAPE, "no A loaded");
+
+    const auto t0 = std::chrono::steady_clock::now();
+    c->launches = 0;
+    oocnmf_info inf{};
+    prepare_factors(c, cfg);
+    if (!c->norm_valid) compute_norm(c);
+    if (c->norm_a2 == 0.0) fail(OOCNMF_ERR_DATA, "nmf: ||A||_F is zero");
+    ck(cudaMemsetAsync(c->flag.p, 0, 4, c->stream), "memset flag");
+    gram_h(c);
+
+    const float eps = float(cfg->epsilon);
+    const uint64_t interval = cfg->error_check_interval;
+    const double flops_per_iter = 4.0 * double(c->rows) * double(c->n) * double(c->k) +
+                                  2.0 * double(c->rows + c->n) * double(c->k) * double(c->k);
+    ensure_events(c, size_t(kEvPerIter) * (interval + 1) + 2);
+    uint64_t pending = 0;  // iterations with recorded events since the last readback
+    uint64_t iter = 0, nt = 0;
+    bool converged = false;
+    for (iter = 1; iter <= cfg->max_iters; ++iter) {
+        cudaEvent_t* ev = c->evs.data() + kEvPerIter * pending;
+        w_update_and_wta(c, eps, true, ev);
+        h_update(c, eps, true, ev);
+        ++pending;
+        inf.flops += flops_per_iter;
+        const bool check = (iter % interval == 0) || iter == cfg->max_iters;
+        if (!check) continue;
+        cudaEvent_t* ce = c->evs.data() + kEvPerIter * pending;
+        ck(cudaEventRecord(ce[0], c->stream), "event");
+        int bad = 0;
+        const double err = error_check(c, cfg->error_mode, &bad);
+        ck(cudaEventRecord(ce[1], c->stream), "event");
+        ck(cudaEventSynchronize(ce[1]), "sync");
+        for (uint64_t p = 0; p < pending; ++p) {
+            cudaEvent_t* e = c->evs.data() + kEvPerIter * p;
+            inf.aht_pass_ms += elapsed(e[eStart], e[eAht]);
+            inf.wta_pass_ms += elapsed(e[eWdone], e[eWta]);
+            inf.w_update_s += elapsed(e[eStart], e[eWdone]) * 1e-3;
+            inf.allreduce_s += elapsed(e[eReduced], e[eComm]) * 1e-3;
+            inf.h_update_s += (elapsed(e[eWdone], e[eReduced]) + elapsed(e[eComm], e[eHdone])) * 1e-3;
+            inf.aht_pass_launches += 1;
+            inf.wta_pass_launches += 1;
+        }
+        inf.error_check_s += elapsed(ce[0], ce[1]) * 1e-3;
+        pending = 0;
+        if (bad)
+            fail(OOCNMF_ERR_DATA, "nmf: non-finite factor entries at iteration " + std::to_string(iter));
+        if (trace_iter && nt < trace_cap) {
+            trace_iter[nt] = iter;
+            trace_err[nt] = err;
+        }
+        ++nt;
+        if (err <= cfg->eta) {
+            converged = true;
+            break;
+        }
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    inf.iterations_run = std::min<uint64_t>(iter, cfg->max_iters);
+    inf.converged = converged ? 1 : 0;
+    inf.n_trace = nt;
+    inf.gpu_launches = c->launches;
+    if (c->kind == Kind::host) {
+        inf.io_s = 0;  // overlapped with compute; reported through h2d_bytes
+        inf.h2d_bytes = double(inf.iterations_run) * double(c->rows) * double(c->n) * 4.0;
+        inf.peak_resident_bytes = uint64_t(c->stage[0].bytes + c->stage[1].bytes);
+    }
+    inf.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (info) *info = inf;
+}
+
+void set_problem_impl(oocnmf_ctx* c, uint64_t m, uint64_t n, uint64_t k, uint64_t row0, uint64_t rows) {
+    if (m < 1 || n < 1 || k < 1) fail(OOCNMF_ERR_SHAPE, "nmf: dimensions must be >= 1");
+    if (rows < 1 || row0 + rows > m) fail(OOCNMF_ERR_SHAPE, "row slab out of bounds");
+    if (n > uint64_t(INT32_MAX) || rows > uint64_t(INT32_MAX))
+        fail(OOCNMF_ERR_SHAPE, "dimension exceeds the 2^31 index range of the device layout");
+    reset_source(c);
+    c->m = m, c->n = n, c->k = k, c->row0 = row0, c->rows = rows;
+    c->kp = pad_k(k);
+    c->mp = round_up(int64_t(rows), kTile);
+    c->np = round_up(int64_t(n), kTile);
+    c->problem_set = true;
+    c->factors_set = c->factors_valid = false;
+    alloc_factors(c);
+}
+
+void load_dense_common(oocnmf_ctx* c) {
+    need_problem(c);
+    reset_source(c);
+    c->A.alloc(size_t(c->mp) * c->np * 4, "A");
+    ck(cudaMemsetAsync(c->A.p, 0, c->A.bytes, c->stream), "memset A");
+    c->kind = Kind::dense;
+    plan_dense(c);
+}
+
+void csr_finish(oocnmf_ctx* c) {
+    // CSR(A^T) once: A is iteration-invariant.
+    c->rpT.alloc(size_t(c->n + 1) * 8, "rpT");
+    c->ciT.alloc(size_t(std::max<int64_t>(c->nnz, 1)) * 4, "ciT");
+    c->vT.alloc(size_t(std::max<int64_t>(c->nnz, 1)) * 4, "vT");
+    ck(csr_transpose(c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows, c->n, c->nnz,
+                     c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), c->vT.as<float>(), c->stream),
+       "csr transpose");
+    c->N1.alloc(size_t(c->mp) * c->kp * 4, "AHt");
+    ck(cudaMemsetAsync(c->N1.p, 0, c->N1.bytes, c->stream), "memset");
+    ck(cudaMemsetAsync(c->packed.p, 0, c->packed.bytes, c->stream), "memset");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->kind = Kind::csr;
+}
+
+}  // namespace
+
+// =============================================================================== C-ABI
+extern "C" {
+
+const char* oocnmf_last_error(void) { return g_err.c_str(); }
+int oocnmf_abi_version(void) { return OOCNMF_ABI_VERSION; }
+
+int oocnmf_device_count(int* count_out) {
+    return guarded([&] {
+        int nd = 0;
+        const cudaError_t e = cudaGetDeviceCount(&nd);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            nd = 0;
+        }
+        *count_out = nd;
+    });
+}
+
+int oocnmf_counter_uniform(uint64_t seed, uint64_t stream, uint64_t index0, uint64_t cnt, double* out) {
+    return guarded([&] {
+        const uint64_t key = rng_key(seed, stream);
+        for (uint64_t i = 0; i < cnt; ++i) out[i] = rng_u01(key, index0 + i);
+    });
+}
+
+int oocnmf_init_factors_host(uint64_t m, uint64_t n, uint64_t k, uint64_t seed, double* w, double* h) {
+    return guarded([&] {
+        if (m < 1 || n < 1 || k < 1) fail(OOCNMF_ERR_SHAPE, "init_factors: dimensions must be >= 1");
+        const uint64_t kw = rng_key(seed, kStreamW), kh = rng_key(seed, kStreamH);
+        for (uint64_t i = 0; i < m * k; ++i) w[i] = rng_u01(kw, i);
+        for (uint64_t i = 0; i < k * n; ++i) h[i] = rng_u01(kh, i);
+    });
+}
+
+int oocnmf_split_even(uint64_t extent, uint64_t parts, uint64_t* begins) {
+    return guarded([&] {
+        if (parts < 1) fail(OOCNMF_ERR_SHAPE, "split_even: parts must be >= 1");
+        const uint64_t base = extent / parts, rem = extent % parts;
+        uint64_t pos = 0;
+        for (uint64_t p = 0; p < parts; ++p) {
+            begins[p] = pos;
+            pos += base + (p < rem ? 1 : 0);
+        }
+        begins[parts] = pos;
+    });
+}
+
+static void ctx_init_common(oocnmf_ctx* c, int device) {
+    int nd = 0;
+    if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
+        cudaGetLastError();
+        fail(OOCNMF_ERR_DEVICE, "no CUDA device available (the B200 backend has no CPU fallback)");
+    }
+    if (device < 0 || device >= nd) fail(OOCNMF_ERR_DEVICE, "device index out of range");
+    c->device = device;
+    set_dev(c);
+    cudaDeviceProp prop{};
+    ck(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10) fail(OOCNMF_ERR_DEVICE, "requires an sm_100 (Blackwell B200) device");
+    c->num_sms = prop.multiProcessorCount;
+    ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
+    for (int i = 0; i < 2; ++i) {
+        ck(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming), "event");
+    }
+    ck(cudaMallocHost(&c->hpin, 64), "cudaMallocHost");
+}
+
+int oocnmf_ctx_create(int device, oocnmf_ctx** out) {
+    return guarded([&] {
+        *out = nullptr;
+        auto* c = new oocnmf_ctx();
+        try {
+            ctx_init_common(c, device);
+        } catch (...) {
+            oocnmf_ctx_destroy(c);
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int oocnmf_comm_unique_id(unsigned char id[128]) {
+    return guarded([&] {
+        static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+        ncclUniqueId uid;
+        nck(ncclGetUniqueId(&uid), "ncclGetUniqueId");
+        std::memcpy(id, &uid, 128);
+    });
+}
+
+int oocnmf_ctx_create_comm(int device, int rank, int nranks, const unsigned char id[128], oocnmf_ctx** out) {
+    return guarded([&] {
+        *out = nullptr;
+        if (nranks < 1 || rank < 0 || rank >= nranks) fail(OOCNMF_ERR_SHAPE, "bad rank/nranks");
+        auto* c = new oocnmf_ctx();
+        try {
+            ctx_init_common(c, device);
+            c->rank = rank;
+            c->nranks = nranks;
+            if (nranks > 1) {
+                ncclUniqueId uid;
+                std::memcpy(&uid, id, 128);
+                nck(ncclCommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
+            }
+        } catch (...) {
+            oocnmf_ctx_destroy(c);
+            throw;
+        }
+        *out = c;
+    });
+}
+
+int oocnmf_ctx_destroy(oocnmf_ctx* c) {
+    if (!c) return OOCNMF_OK;
+    return guarded([&] {
+        cudaSetDevice(c->device);
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+        if (c->comm) ncclCommDestroy(c->comm);
+        for (auto e : c->evs) cudaEventDestroy(e);
+        for (int i = 0; i < 2; ++i) {
+            if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
+            if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
+        }
+        if (c->hpin) cudaFreeHost(c->hpin);
+        if (c->stream) cudaStreamDestroy(c->stream);
+        if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+        delete c;
+    });
+}
+
+int oocnmf_ctx_rank(const oocnmf_ctx* c, int* rank, int* nranks) {
+    return guarded([&] {
+        *rank = c->rank;
+        *nranks = c->nranks;
+    });
+}
+
+int oocnmf_set_problem(oocnmf_ctx* c, uint64_t m, uint64_t n, uint64_t k, uint64_t row0, uint64_t rows) {
+    return guarded([&] {
+        set_dev(c);
+        set_problem_impl(c, m, n, k, row0, rows);
+    });
+}
+
+int oocnmf_load_dense_f64(oocnmf_ctx* c, const double* a, uint64_t lda) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (lda < c->n) fail(OOCNMF_ERR_SHAPE, "lda < n");
+        load_dense_common(c);
+        // Stage f64 rows in bounded chunks, cast to f32 in HBM.
+        const int64_t chunk_rows = std::max<int64_t>(1, (int64_t(256) << 20) / int64_t(c->n * 8));
+        DevBuf tmp;
+        tmp.alloc(size_t(std::min<int64_t>(chunk_rows, c->rows)) * c->n * 8, "staging");
+        for (int64_t r0 = 0; r0 < int64_t(c->rows); r0 += chunk_rows) {
+            const int64_t br = std::min<int64_t>(chunk_rows, int64_t(c->rows) - r0);
+            ck(cudaMemcpy2DAsync(tmp.p, c->n * 8, a + r0 * lda, lda * 8, c->n * 8, br, cudaMemcpyHostToDevice,
+                                 c->stream),
+               "H2D");
+            ck(launch_cast_pad_f64(tmp.as<double>(), c->n, br, c->n, c->A.as<float>() + r0 * c->np, c->np,
+                                   c->stream),
+               "cast");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+        }
+    });
+}
+
+int oocnmf_load_dense_f32(oocnmf_ctx* c, const float* a, uint64_t lda) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (lda < c->n) fail(OOCNMF_ERR_SHAPE, "lda < n");
+        load_dense_common(c);
+        ck(cudaMemcpy2DAsync(c->A.p, c->np * 4, a, lda * 4, c->n * 4, c->rows, cudaMemcpyHostToDevice, c->stream),
+           "H2D A");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int oocnmf_load_dense_device_f32(oocnmf_ctx* c, const float* d_a, uint64_t lda) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (lda < c->n) fail(OOCNMF_ERR_SHAPE, "lda < n");
+        load_dense_common(c);
+        ck(cudaMemcpy2DAsync(c->A.p, c->np * 4, d_a, lda * 4, c->n * 4, c->rows, cudaMemcpyDeviceToDevice,
+                             c->stream),
+           "D2D A");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int oocnmf_generate_dense_uniform(oocnmf_ctx* c, uint64_t seed, uint64_t stream) {
+    return guarded([&] {
+        set_dev(c);
+        load_dense_common(c);
+        ck(launch_gen_dense_uniform(c->A.as<float>(), c->np, c->rows, c->n, c->row0, c->n, seed, stream, c->stream),
+           "generate");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int oocnmf_load_csr_f64(oocnmf_ctx* c, const uint64_t* row_ptr, const uint64_t* col_idx, const double* vals) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (row_ptr[0] != 0) fail(OOCNMF_ERR_SHAPE, "CsrMatrix: row_ptr[0] must be 0");
+        for (uint64_t i = 0; i < c->rows; ++i)
+            if (row_ptr[i + 1] < row_ptr[i]) fail(OOCNMF_ERR_SHAPE, "CsrMatrix: row_ptr must be nondecreasing");
+        const int64_t nnz = int64_t(row_ptr[c->rows]);
+        for (uint64_t i = 0; i < c->rows; ++i)
+            for (uint64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+                if (col_idx[p] >= c->n) fail(OOCNMF_ERR_SHAPE, "CsrMatrix: column index out of range");
+                if (p > row_ptr[i] && col_idx[p] <= col_idx[p - 1])
+                    fail(OOCNMF_ERR_SHAPE, "CsrMatrix: column indices must strictly increase within a row");
+            }
+        reset_source(c);
+        std::vector<int64_t> rp(c->rows + 1);
+        std::vector<int32_t> ci(std::max<int64_t>(nnz, 1));
+        std::vector<float> v(std::max<int64_t>(nnz, 1));
+        for (uint64_t i = 0; i <= c->rows; ++i) rp[i] = int64_t(row_ptr[i]);
+        for (int64_t p = 0; p < nnz; ++p) ci[p] = int32_t(col_idx[p]), v[p] = float(vals[p]);
+        c->nnz = nnz;
+        c->rp.alloc(rp.size() * 8, "rp");
+        c->ci.alloc(ci.size() * 4, "ci");
+        c->v.alloc(v.size() * 4, "v");
+        ck(cudaMemcpy(c->rp.p, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(c->ci.p, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice), "H2D");
+        ck(cudaMemcpy(c->v.p, v.data(), v.size() * 4, cudaMemcpyHostToDevice), "H2D");
+        csr_finish(c);
+    });
+}
+
+int oocnmf_generate_csr_uniform(oocnmf_ctx* c, double density, uint64_t seed) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (!(density >= 0.0) || density > 1.0) fail(OOCNMF_ERR_SHAPE, "density must lie in [0, 1]");
+        reset_source(c);
+        // U < density  <=>  bits53 < ceil(density * 2^53)  (exact: power-of-two scaling)
+        const uint64_t thresh = uint64_t(std::ceil(density * 0x1.0p53));
+        c->rp.alloc(size_t(c->rows + 1) * 8, "rp");
+        DevBuf counts;
+        counts.alloc(size_t(c->rows + 1) * 8, "counts");
+        ck(cudaMemsetAsync(counts.p, 0, counts.bytes, c->stream), "memset");
+        ck(launch_gen_csr_count(c->rows, c->row0, c->n, thresh, seed, counts.as<int64_t>(), c->stream), "gen count");
+        ck(exclusive_scan_i64(counts.as<int64_t>(), c->rp.as<int64_t>(), c->rows + 1, c->stream), "scan");
+        int64_t nnz = 0;
+        ck(cudaMemcpyAsync(&nnz, c->rp.as<int64_t>() + c->rows, 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->nnz = nnz;
+        c->ci.alloc(size_t(std::max<int64_t>(nnz, 1)) * 4, "ci");
+        c->v.alloc(size_t(std::max<int64_t>(nnz, 1)) * 4, "v");
+        ck(launch_gen_csr_fill(c->rows, c->row0, c->n, thresh, seed, c->rp.as<int64_t>(), c->ci.as<int32_t>(),
+                               c->v.as<float>(), c->stream),
+           "gen fill");
+        csr_finish(c);
+    });
+}
+
+int oocnmf_attach_host_dense_f32(oocnmf_ctx* c, const float* a, uint64_t lda, uint64_t batch_rows) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (lda < c->n) fail(OOCNMF_ERR_SHAPE, "lda < n");
+        reset_source(c);
+        int64_t br = int64_t(batch_rows);
+        if (br == 0) br = std::max<int64_t>(kTile, ((int64_t(512) << 20) / (c->np * 4)) / kTile * kTile);
+        br = round_up(br, kTile);
+        br = std::min<int64_t>(br, c->mp);
+        c->batch_rows = br;
+        c->hA = a;
+        c->hlda = lda;
+        for (int i = 0; i < 2; ++i) {
+            c->stage[i].alloc(size_t(br) * c->np * 4, "stage");
+            ck(cudaMemsetAsync(c->stage[i].p, 0, c->stage[i].bytes, c->stream), "memset stage");
+            ck(cudaEventRecord(c->ev_free[i], c->stream), "event");
+        }
+        const int64_t nb = (int64_t(c->rows) + br - 1) / br;
+        const int64_t last = round_up(int64_t(c->rows) - (nb - 1) * br, kTile);
+        plan_aht(c->sk1b[0], br, c->np, c->num_sms);
+        plan_aht(c->sk1b[1], last, c->np, c->num_sms);
+        plan_wta(c->sk2b[0], br, c->np, c->num_sms);
+        plan_wta(c->sk2b[1], last, c->np, c->num_sms);
+        const int64_t s1 = std::max(c->sk1b[0].G * c->sk1b[0].smax, c->sk1b[1].G * c->sk1b[1].smax);
+        const int64_t s2 = std::max(c->sk2b[0].G * c->sk2b[0].smax, c->sk2b[1].G * c->sk2b[1].smax);
+        c->slots1.alloc(size_t(s1) * kTile * c->kp * 4, "slots1");
+        c->slots2.alloc(size_t(s2) * kTile * c->kp * 4, "slots2");
+        c->gram_w.alloc(size_t(nb) * factor_grid(br / kTile) * c->kp * c->kp * 4, "gram_w");
+        ck(cudaMemsetAsync(c->gram_w.p, 0, c->gram_w.bytes, c->stream), "memset");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        c->kind = Kind::host;
+    });
+}
+
+int oocnmf_host_register(void* p, uint64_t bytes) {
+    return guarded([&] { ck(cudaHostRegister(p, bytes, cudaHostRegisterDefault), "cudaHostRegister"); });
+}
+int oocnmf_host_unregister(void* p) {
+    return guarded([&] { ck(cudaHostUnregister(p), "cudaHostUnregister"); });
+}
+
+int oocnmf_download_dense_f32(oocnmf_ctx* c, float* a) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (c->kind != Kind::dense) fail(OOCNMF_ERR_SHAPE, "no dense A resident in HBM");
+        ck(cudaMemcpy2DAsync(a, c->n * 4, c->A.p, c->np * 4, c->n * 4, c->rows, cudaMemcpyDeviceToHost, c->stream),
+           "D2H A");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+    });
+}
+
+int oocnmf_set_factors_f64(oocnmf_ctx* c, const double* w, const double* h) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        const int kp = c->kp;
+        std::vector<float> hw(size_t(c->mp) * kp, 0.f), hh(size_t(c->np) * kp, 0.f);
+        for (uint64_t i = 0; i < c->rows; ++i)
+            for (uint64_t j = 0; j < c->k; ++j) hw[i * kp + j] = float(w[i * c->k + j]);
+        for (uint64_t r = 0; r < c->k; ++r)
+            for (uint64_t j = 0; j < c->n; ++j) hh[j * kp + r] = float(h[r * c->n + j]);
+        ck(cudaMemcpy(c->W.p, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice), "H2D W");
+        ck(cudaMemcpy(c->Ht.p, hh.data(), hh.size() * 4, cudaMemcpyHostToDevice), "H2D H");
+        c->factors_set = c->factors_valid = true;
+    });
+}
+
+int oocnmf_get_factors_f64(oocnmf_ctx* c, double* w, double* h) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (!c->factors_valid) fail(OOCNMF_ERR_SHAPE, "factors are not initialised");
+        const int kp = c->kp;
+        std::vector<float> hw(size_t(c->mp) * kp), hh(size_t(c->np) * kp);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        ck(cudaMemcpy(hw.data(), c->W.p, hw.size() * 4, cudaMemcpyDeviceToHost), "D2H W");
+        ck(cudaMemcpy(hh.data(), c->Ht.p, hh.size() * 4, cudaMemcpyDeviceToHost), "D2H H");
+        if (w)
+            for (uint64_t i = 0; i < c->rows; ++i)
+                for (uint64_t j = 0; j < c->k; ++j) w[i * c->k + j] = hw[i * kp + j];
+        if (h)
+            for (uint64_t r = 0; r < c->k; ++r)
+                for (uint64_t j = 0; j < c->n; ++j) h[r * c->n + j] = hh[j * kp + r];
+    });
+}
+
+int oocnmf_gather_w_f64(oocnmf_ctx* c, double* w_full) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        const int N = c->nranks, kp = c->kp;
+        std::vector<uint64_t> beg(N + 1);
+        {
+            const uint64_t base = c->m / N, rem = c->m % N;
+            uint64_t pos = 0;
+            for (int p = 0; p < N; ++p) beg[p] = pos, pos += base + (uint64_t(p) < rem ? 1 : 0);
+            beg[N] = pos;
+        }
+        if (beg[c->rank] != c->row0 || beg[c->rank + 1] != c->row0 + c->rows)
+            fail(OOCNMF_ERR_SHAPE, "gather_w requires split_even row slabs");
+        const int64_t maxr = int64_t(beg[1] - beg[0]);
+        DevBuf all;
+        all.alloc(size_t(N) * maxr * kp * 4, "gather");
+        if (N > 1)
+            nck(ncclAllGather(c->W.p, all.p, size_t(maxr) * kp, ncclFloat, c->comm, c->stream), "allgather W");
+        else
+            ck(cudaMemcpyAsync(all.p, c->W.p, size_t(maxr) * kp * 4, cudaMemcpyDeviceToDevice, c->stream), "copy");
+        std::vector<float> hw(size_t(N) * maxr * kp);
+        ck(cudaMemcpyAsync(hw.data(), all.p, hw.size() * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        for (int p = 0; p < N; ++p)
+            for (uint64_t i = beg[p]; i < beg[p + 1]; ++i)
+                for (uint64_t j = 0; j < c->k; ++j) w_full[i * c->k + j] = hw[(size_t(p) * maxr + (i - beg[p])) * kp + j];
+    });
+}
+
+int oocnmf_solve(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, double* trace_err,
+                 uint64_t trace_cap, oocnmf_info* info) {
+    return guarded([&] {
+        set_dev(c);
+        solve_impl(c, cfg, trace_iter, trace_err, trace_cap, info);
+    });
+}
+
+int oocnmf_sq_norm(oocnmf_ctx* c, double* out) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (c->kind == Kind::none) fail(OOCNMF_ERR_SHAPE, "no A loaded");
+        if (!c->norm_valid) compute_norm(c);
+        *out = c->norm_a2;
+    });
+}
+
+int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, double* wtw) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (c->kind != Kind::dense && c->kind != Kind::csr) fail(OOCNMF_ERR_SHAPE, "products need in-core A");
+        if (!c->factors_valid) fail(OOCNMF_ERR_SHAPE, "factors are not initialised");
+        const int kp = c->kp;
+        cudaStream_t s = c->stream;
+        DevBuf t1;
+        t1.alloc(size_t(c->mp) * kp * 4, "aht");
+        if (c->kind == Kind::dense) {
+            ck(launch_aht(kp, c->A.as<float>(), c->np, c->Ht.as<float>(), c->slots1.as<float>(), c->sk1, s), "aht");
+            ck(launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, t1.as<float>(), false, s), "reduce");
+            ck(launch_wta(kp, c->A.as<float>(), c->np, c->W.as<float>(), c->slots2.as<float>(), c->sk2, s), "wta");
+            ck(launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce");
+        } else {
+            ck(launch_spmm(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows, c->Ht.as<float>(),
+                           t1.as<float>(), s),
+               "spmm");
+            ck(launch_spmm(kp, c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), c->vT.as<float>(), c->n, c->W.as<float>(),
+                           c->wta(), s),
+               "spmm");
+        }
+        gram_h(c);
+        ck(launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, 0.f, false,
+                                c->gram_w.as<float>(), nullptr, c->flag.as<int>(), s),
+           "gram W");
+        ck(launch_reduce_slots(c->gram_w.as<float>(), factor_grid(c->mp / kTile), int64_t(kp) * kp, c->wtw(), s),
+           "reduce");
+        std::vector<float> a1(size_t(c->mp) * kp), a2(size_t(c->np) * kp), g1(size_t(kp) * kp), g2(size_t(kp) * kp);
+        ck(cudaMemcpyAsync(a1.data(), t1.p, a1.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(a2.data(), c->wta(), a2.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(g1.data(), c->HHt.p, g1.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaMemcpyAsync(g2.data(), c->wtw(), g2.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");
+        ck(cudaStreamSynchronize(s), "sync");
+        const uint64_t k = c->k;
+        for (uint64_t i = 0; i < c->rows; ++i)
+            for (uint64_t j = 0; j < k; ++j) aht[i * k + j] = a1[i * kp + j];
+        for (uint64_t r = 0; r < k; ++r)
+            for (uint64_t j = 0; j < c->n; ++j) wta[r * c->n + j] = a2[j * kp + r];
+        for (uint64_t r = 0; r < k; ++r)
+            for (uint64_t j = 0; j < k; ++j) {
+                hht[r * k + j] = g1[r * kp + j];
+                wtw[r * k + j] = g2[r * kp + j];
+            }
+    });
+}
+
+static int one_shot(int device, uint64_t m, uint64_t n, const oocnmf_config* cfg, const double* w0, const double* h0,
+                    double* w_out, double* h_out, uint64_t* ti, double* te, uint64_t cap, oocnmf_info* info,
+                    int (*load)(oocnmf_ctx*, const void*), const void* src) {
+    oocnmf_ctx* c = nullptr;
+    int st = oocnmf_ctx_create(device, &c);
+    if (st) return st;
+    if (!cfg) {
+        oocnmf_ctx_destroy(c);
+        g_err = "null config";
+        return OOCNMF_ERR_SHAPE;
+    }
+    st = oocnmf_set_problem(c, m, n, cfg->k, 0, m);
+    if (!st) st = load(c, src);
+    if (!st && cfg->init == 1) {
+        if (!w0 || !h0) {
+            g_err = "NmfConfig: init=from_files requires both factors";
+            st = OOCNMF_ERR_SHAPE;
+        } else {
+            st = oocnmf_set_factors_f64(c, w0, h0);
+        }
+    }
+    if (!st) st = oocnmf_solve(c, cfg, ti, te, cap, info);
+    if (!st) st = oocnmf_get_factors_f64(c, w_out, h_out);
+    const std::string keep = g_err;
+    oocnmf_ctx_destroy(c);
+    g_err = keep;
+    return st;
+}
+
+struct CsrSrc {
+    const uint64_t *rp, *ci;
+    const double* v;
+};
+
+int oocnmf_nmf_serial_dense_f64(int device, const double* a, uint64_t m, uint64_t n, const oocnmf_config* cfg,
+                                const double* w0, const double* h0, double* w_out, double* h_out, uint64_t* ti,
+                                double* te, uint64_t cap, oocnmf_info* info) {
+    auto ld = [](oocnmf_ctx* c, const void* p) {
+        return oocnmf_load_dense_f64(c, static_cast<const double*>(p), c->n);
+    };
+    return one_shot(device, m, n, cfg, w0, h0, w_out, h_out, ti, te, cap, info, ld, a);
+}
+
+int oocnmf_nmf_serial_dense_f32(int device, const float* a, uint64_t m, uint64_t n, const oocnmf_config* cfg,
+                                const double* w0, const double* h0, double* w_out, double* h_out, uint64_t* ti,
+                                double* te, uint64_t cap, oocnmf_info* info) {
+    auto ld = [](oocnmf_ctx* c, const void* p) {
+        return oocnmf_load_dense_f32(c, static_cast<const float*>(p), c->n);
+    };
+    return one_shot(device, m, n, cfg, w0, h0, w_out, h_out, ti, te, cap, info, ld, a);
+}
+
+int oocnmf_nmf_serial_csr_f64(int device, const uint64_t* row_ptr, const uint64_t* col_idx, const double* vals,
+                              uint64_t m, uint64_t n, const oocnmf_config* cfg, const double* w0, const double* h0,
+                              double* w_out, double* h_out, uint64_t* ti, double* te, uint64_t cap,
+                              oocnmf_info* info) {
+    CsrSrc src{row_ptr, col_idx, vals};
+    auto ld = [](oocnmf_ctx* c, const void* p) {
+        const auto* s = static_cast<const CsrSrc*>(p);
+        return oocnmf_load_csr_f64(c, s->rp, s->ci, s->v);
+    };
+    return one_shot(device, m, n, cfg, w0, h0, w_out, h_out, ti, te, cap, info, ld, &src);
+}
+
+}  // extern "C"

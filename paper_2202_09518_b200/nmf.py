@@ -1,0 +1,472 @@
+"""Python mirror of the reference's MU-NMF API (``oocnmf::`` in /root/reference/proj/include),
+driving the B200 C-ABI backend. Names, argument meaning and error behaviour follow the
+reference so parity tests read like its own:
+
+* :class:`NmfConfig` / :class:`NmfResult` / :class:`PhaseCounters` — include/oocnmf/nmf.hpp:15-48
+* :func:`init_factors` — include/oocnmf/nmf.hpp:53-58 (same counter RNG, bit-identical f64)
+* :func:`nmf_serial` — include/oocnmf/nmf.hpp:64, src/nmf_serial.cpp:56-121
+* :func:`make_plan` / :func:`choose_strategy` — include/oocnmf/partition.hpp:10-46
+* :func:`nmf_distributed` — include/oocnmf/nmf_distributed.hpp:34-36 (row partition)
+* exceptions — include/oocnmf/error.hpp:9-36 (+ :class:`DeviceError`)
+
+All arithmetic happens on the GPU; this layer validates, converts and maps status codes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+from dataclasses import dataclass, field
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from . import _capi
+
+
+# ----------------------------------------------------------------------------- errors
+class ShapeError(ValueError):
+    """Contract violation: shapes, windows, configs (reference ShapeError: std::invalid_argument)."""
+
+
+class DataError(RuntimeError):
+    """||A||_F == 0 or non-finite factors."""
+
+
+class IoError(OSError):
+    pass
+
+
+class CommError(RuntimeError):
+    pass
+
+
+class StoreError(RuntimeError):
+    pass
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure or no B200 device (the backend has no CPU fallback)."""
+
+
+_STATUS = {1: ShapeError, 2: DataError, 3: IoError, 4: CommError, 5: StoreError, 6: DeviceError}
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = _capi.lib().oocnmf_last_error().decode()
+        raise _STATUS.get(status, DeviceError)(msg)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(C.POINTER(t))
+
+
+# ----------------------------------------------------------------------------- types
+class FactorInit(enum.Enum):
+    uniform01 = 0
+    from_files = 1
+    resident = 2  # B200 extension: continue from the factors left on the device by a previous solve
+
+
+@dataclass
+class NmfConfig:
+    k: int = 1
+    eta: float = 1e-4
+    max_iters: int = 1000
+    error_check_interval: int = 10
+    epsilon: float = 1e-12
+    seed: int = 0
+    init: FactorInit = FactorInit.uniform01
+    init_w: Optional[np.ndarray] = None
+    init_h: Optional[np.ndarray] = None
+    # B200 extensions
+    device: int = 0
+    error_mode: str = "trace"  # "trace" | "direct"
+
+    def validate(self) -> None:
+        if self.k < 1:
+            raise ShapeError("NmfConfig: k must be >= 1")
+        if not self.eta >= 0:
+            raise ShapeError("NmfConfig: eta must be >= 0")
+        if self.max_iters < 1:
+            raise ShapeError("NmfConfig: max_iters must be >= 1")
+        if self.error_check_interval < 1:
+            raise ShapeError("NmfConfig: error_check_interval must be >= 1")
+        if not self.epsilon > 0:
+            raise ShapeError("NmfConfig: epsilon must be > 0")
+        if self.init == FactorInit.from_files and (self.init_w is None or self.init_h is None):
+            raise ShapeError("NmfConfig: init=from_files requires both factors")
+        if self.error_mode not in ("trace", "direct"):
+            raise ShapeError("NmfConfig: error_mode must be 'trace' or 'direct'")
+
+    def to_c(self) -> _capi.Config:
+        return _capi.Config(self.k, self.eta, self.max_iters, self.error_check_interval, self.epsilon,
+                            self.seed, self.init.value,
+                            1 if self.error_mode == "direct" else 0)
+
+
+@dataclass
+class PhaseCounters:
+    h_update_s: float = 0.0
+    w_update_s: float = 0.0
+    allreduce_s: float = 0.0
+    error_check_s: float = 0.0
+    io_s: float = 0.0
+    total_s: float = 0.0
+    flops: float = 0.0
+    peak_resident_bytes: int = 0
+
+
+@dataclass
+class NmfResult:
+    w: np.ndarray
+    h: np.ndarray
+    error_trace: List[Tuple[int, float]]
+    iterations_run: int
+    converged: bool
+    counters: PhaseCounters = field(default_factory=PhaseCounters)
+    info: dict = field(default_factory=dict)  # device-side timing / launch counts
+
+
+class CsrMatrix:
+    """CSR with u64 indices and f64 values (reference CsrMatrix, matrix.hpp:63-102)."""
+
+    def __init__(self, rows, cols, row_ptr, col_idx, values):
+        self.rows, self.cols = int(rows), int(cols)
+        self.row_ptr = np.ascontiguousarray(row_ptr, np.uint64)
+        self.col_idx = np.ascontiguousarray(col_idx, np.uint64)
+        self.values = np.ascontiguousarray(values, np.float64)
+        self.validate_structure()
+
+    @property
+    def nnz(self):
+        return int(self.values.size)
+
+    @property
+    def shape(self):
+        return (self.rows, self.cols)
+
+    def validate_structure(self):
+        rp, ci = self.row_ptr, self.col_idx
+        if rp.size != self.rows + 1:
+            raise ShapeError("CsrMatrix: row_ptr must have rows+1 entries")
+        if rp[0] != 0:
+            raise ShapeError("CsrMatrix: row_ptr[0] != 0")
+        if rp[-1] != self.values.size or ci.size != self.values.size:
+            raise ShapeError("CsrMatrix: row_ptr[rows] disagrees with nnz")
+        if np.any(np.diff(rp.astype(np.int64)) < 0):
+            raise ShapeError("CsrMatrix: row_ptr decreases")
+        if ci.size and np.any(ci >= self.cols):
+            raise ShapeError("CsrMatrix: column index out of range")
+        if ci.size > 1:
+            d = np.diff(ci.astype(np.int64))
+            starts = np.zeros(ci.size, bool)
+            starts[rp[:-1][rp[:-1] < ci.size].astype(np.int64)] = True
+            if np.any((d <= 0) & ~starts[1:]):
+                raise ShapeError("CsrMatrix: column indices not strictly increasing within a row")
+
+    def to_dense(self):
+        d = np.zeros((self.rows, self.cols))
+        rows = np.repeat(np.arange(self.rows), np.diff(self.row_ptr.astype(np.int64)))
+        d[rows, self.col_idx.astype(np.int64)] = self.values
+        return d
+
+    @staticmethod
+    def from_dense(d, zero_tol=0.0):
+        d = np.asarray(d, np.float64)
+        mask = np.abs(d) > zero_tol
+        rp = np.concatenate([[0], np.cumsum(mask.sum(1))]).astype(np.uint64)
+        r, c = np.nonzero(mask)
+        return CsrMatrix(d.shape[0], d.shape[1], rp, c, d[r, c])
+
+    def row_window(self, r0, r1):
+        rp = self.row_ptr[r0:r1 + 1].astype(np.int64)
+        b, e = int(rp[0]), int(rp[-1])
+        return CsrMatrix(r1 - r0, self.cols, (rp - b).astype(np.uint64), self.col_idx[b:e], self.values[b:e])
+
+
+# ----------------------------------------------------------------------------- helpers
+def device_count() -> int:
+    n = C.c_int()
+    check(_capi.lib().oocnmf_device_count(C.byref(n)))
+    return n.value
+
+
+def init_factors(m: int, n: int, k: int, seed: int) -> Tuple[np.ndarray, np.ndarray]:
+    """W (m x k) ~ U(seed, 1, i*k+j), H (k x n) ~ U(seed, 2, r*n+j) — reference counter RNG."""
+    if m < 1 or n < 1 or k < 1:
+        raise ShapeError("init_factors: dimensions must be >= 1")
+    w = np.empty((m, k))
+    h = np.empty((k, n))
+    check(_capi.lib().oocnmf_init_factors_host(m, n, k, seed, _p(w, C.c_double), _p(h, C.c_double)))
+    return w, h
+
+
+def counter_uniform(seed: int, stream: int, index0: int, count: int) -> np.ndarray:
+    out = np.empty(count)
+    check(_capi.lib().oocnmf_counter_uniform(seed, stream, index0, count, _p(out, C.c_double)))
+    return out
+
+
+def split_even(extent: int, parts: int) -> np.ndarray:
+    out = np.zeros(parts + 1, np.uint64)
+    check(_capi.lib().oocnmf_split_even(extent, parts, _p(out, C.c_uint64)))
+    return out.astype(np.int64)
+
+
+# ----------------------------------------------------------------------------- context
+class Context:
+    """One GPU's solver context (C-ABI ``oocnmf_ctx``)."""
+
+    def __init__(self, device: int = 0, rank: int = 0, nranks: int = 1, unique_id: Optional[bytes] = None):
+        self._h = C.c_void_p()
+        L = _capi.lib()
+        if nranks > 1:
+            if unique_id is None or len(unique_id) != 128:
+                raise ShapeError("Context: a 128-byte NCCL unique id is required for nranks > 1")
+            check(L.oocnmf_ctx_create_comm(device, rank, nranks, unique_id, C.byref(self._h)))
+        else:
+            check(L.oocnmf_ctx_create(device, C.byref(self._h)))
+        self.device, self.rank, self.nranks = device, rank, nranks
+        self.m = self.n = self.k = self.row0 = self.rows = 0
+        self._keep = None
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        check(_capi.lib().oocnmf_comm_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if self._h:
+            _capi.lib().oocnmf_ctx_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_problem(self, m, n, k, row0=0, rows=None):
+        rows = m - row0 if rows is None else rows
+        check(_capi.lib().oocnmf_set_problem(self._h, m, n, k, row0, rows))
+        self.m, self.n, self.k, self.row0, self.rows = m, n, k, row0, rows
+
+    def load_dense(self, a: np.ndarray):
+        a = np.asarray(a)
+        if a.shape != (self.rows, self.n):
+            raise ShapeError(f"load_dense: expected {self.rows}x{self.n}, got {a.shape}")
+        if a.dtype == np.float32:
+            a = np.ascontiguousarray(a)
+            check(_capi.lib().oocnmf_load_dense_f32(self._h, _p(a, C.c_float), self.n))
+        else:
+            a = np.ascontiguousarray(a, np.float64)
+            check(_capi.lib().oocnmf_load_dense_f64(self._h, _p(a, C.c_double), self.n))
+
+    def load_dense_device(self, ptr: int, lda: int):
+        check(_capi.lib().oocnmf_load_dense_device_f32(self._h, C.c_void_p(ptr), lda))
+
+    def download_dense(self, out: Optional[np.ndarray] = None) -> np.ndarray:
+        out = np.empty((self.rows, self.n), np.float32) if out is None else out
+        if out.dtype != np.float32 or out.shape != (self.rows, self.n) or not out.flags.c_contiguous:
+            raise ShapeError("download_dense: expected a C-contiguous float32 rows x n array")
+        check(_capi.lib().oocnmf_download_dense_f32(self._h, out.ctypes.data))
+        return out
+
+    def generate_dense_uniform(self, seed=42, stream=99):
+        check(_capi.lib().oocnmf_generate_dense_uniform(self._h, seed, stream))
+
+    def load_csr(self, a: CsrMatrix):
+        if a.shape != (self.rows, self.n):
+            raise ShapeError(f"load_csr: expected {self.rows}x{self.n}, got {a.shape}")
+        check(_capi.lib().oocnmf_load_csr_f64(self._h, _p(a.row_ptr, C.c_uint64), _p(a.col_idx, C.c_uint64),
+                                              _p(a.values, C.c_double)))
+
+    def generate_csr_uniform(self, density, seed):
+        check(_capi.lib().oocnmf_generate_csr_uniform(self._h, density, seed))
+
+    def attach_host(self, a: np.ndarray, batch_rows: int = 0):
+        """Out-of-core: ``a`` (rows x n float32, ideally pinned) stays in host memory."""
+        if a.dtype != np.float32 or a.shape != (self.rows, self.n) or not a.flags.c_contiguous:
+            raise ShapeError("attach_host: expected a C-contiguous float32 rows x n array")
+        self._keep = a
+        check(_capi.lib().oocnmf_attach_host_dense_f32(self._h, a.ctypes.data, self.n, batch_rows))
+
+    def set_factors(self, w: np.ndarray, h: np.ndarray):
+        w = np.ascontiguousarray(w, np.float64)
+        h = np.ascontiguousarray(h, np.float64)
+        if w.shape != (self.rows, self.k) or h.shape != (self.k, self.n):
+            raise ShapeError("set_factors: factor shapes do not match the problem")
+        check(_capi.lib().oocnmf_set_factors_f64(self._h, _p(w, C.c_double), _p(h, C.c_double)))
+
+    def get_factors(self):
+        w = np.empty((self.rows, self.k))
+        h = np.empty((self.k, self.n))
+        check(_capi.lib().oocnmf_get_factors_f64(self._h, _p(w, C.c_double), _p(h, C.c_double)))
+        return w, h
+
+    def gather_w(self):
+        w = np.empty((self.m, self.k))
+        check(_capi.lib().oocnmf_gather_w_f64(self._h, _p(w, C.c_double)))
+        return w
+
+    def solve(self, cfg: NmfConfig):
+        cfg.validate()
+        cap = cfg.max_iters // cfg.error_check_interval + 2
+        ti = np.zeros(cap, np.uint64)
+        te = np.zeros(cap)
+        info = _capi.Info()
+        c = cfg.to_c()
+        check(_capi.lib().oocnmf_solve(self._h, C.byref(c), _p(ti, C.c_uint64), _p(te, C.c_double), cap,
+                                       C.byref(info)))
+        nt = min(int(info.n_trace), cap)
+        return list(zip(ti[:nt].astype(int).tolist(), te[:nt].tolist())), info.as_dict()
+
+    def products(self):
+        k, n, rows = self.k, self.n, self.rows
+        aht, wta = np.empty((rows, k)), np.empty((k, n))
+        hht, wtw = np.empty((k, k)), np.empty((k, k))
+        check(_capi.lib().oocnmf_products_f64(self._h, *(_p(x, C.c_double) for x in (aht, wta, hht, wtw))))
+        return aht, wta, hht, wtw
+
+    def sq_norm(self):
+        out = C.c_double()
+        check(_capi.lib().oocnmf_sq_norm(self._h, C.byref(out)))
+        return out.value
+
+
+def _counters(info: dict) -> PhaseCounters:
+    return PhaseCounters(**{f: info[f] for f in PhaseCounters.__dataclass_fields__})
+
+
+# ----------------------------------------------------------------------------- solvers
+def nmf_serial(a, cfg: NmfConfig) -> NmfResult:
+    """Single-GPU MU-NMF, W update before H update (src/nmf_serial.cpp:56-121).
+
+    ``a``: 2-D ndarray (float64 or float32, nonnegative) or :class:`CsrMatrix`.
+    """
+    cfg.validate()
+    m, n = (a.rows, a.cols) if isinstance(a, CsrMatrix) else np.asarray(a).shape
+    if m < 1 or n < 1:
+        raise ShapeError(f"nmf_serial: empty input {m}x{n}")
+    if cfg.init == FactorInit.from_files:
+        if cfg.init_w.shape != (m, cfg.k) or cfg.init_h.shape != (cfg.k, n):
+            raise ShapeError("nmf_serial: provided factors do not match A and k")
+    with Context(cfg.device) as ctx:
+        ctx.set_problem(m, n, cfg.k)
+        if isinstance(a, CsrMatrix):
+            ctx.load_csr(a)
+        else:
+            ctx.load_dense(a)
+        if cfg.init == FactorInit.from_files:
+            ctx.set_factors(cfg.init_w, cfg.init_h)
+        trace, info = ctx.solve(cfg)
+        w, h = ctx.get_factors()
+    return NmfResult(w, h, trace, int(info["iterations_run"]), bool(info["converged"]), _counters(info), info)
+
+
+class Strategy(enum.Enum):
+    cnmf = "cnmf"
+    rnmf = "rnmf"
+
+
+def choose_strategy(m: int, n: int) -> Strategy:
+    """CNMF iff n > m (src/partition.cpp:12-14)."""
+    return Strategy.cnmf if n > m else Strategy.rnmf
+
+
+@dataclass
+class PartitionPlan:
+    strategy: Strategy
+    n_workers: int
+    m: int
+    n: int
+    k: int
+    n_b: int
+    slabs: List[Tuple[Tuple[int, int], Tuple[int, int]]]  # per rank: ((row0,row1),(col0,col1))
+    batches: List[Tuple[int, int]]
+
+
+def make_plan(m, n, k, n_workers, n_b, strategy: Strategy) -> PartitionPlan:
+    """Even split with the remainder on the first ranks (src/partition.cpp:49-87)."""
+    if m < 1 or n < 1 or k < 1:
+        raise ShapeError("make_plan: dimensions must be >= 1")
+    if n_workers < 1:
+        raise ShapeError("make_plan: need at least one worker")
+    if n_b < 1:
+        raise ShapeError("make_plan: need at least one batch")
+    col = strategy == Strategy.cnmf
+    part, bat = (n, m) if col else (m, n)
+    if n_workers > part:
+        raise ShapeError(f"make_plan: {n_workers} workers exceed the {part} slabs available under {strategy.value}")
+    if n_b > bat:
+        raise ShapeError(f"make_plan: {n_b} batches exceed the {bat}-extent batched axis")
+    s = split_even(part, n_workers)
+    b = split_even(bat, n_b)
+    slabs = [(((0, m), (int(s[r]), int(s[r + 1]))) if col else ((int(s[r]), int(s[r + 1])), (0, n)))
+             for r in range(n_workers)]
+    return PartitionPlan(strategy, n_workers, m, n, k, n_b, slabs,
+                         [(int(b[i]), int(b[i + 1])) for i in range(n_b)])
+
+
+class DistComm:
+    """One rank of an NCCL group over NVLink. The 128-byte NCCL unique id is exchanged with
+    torch.distributed (plumbing only); all traffic of the solve goes through NCCL inside
+    the C-ABI library."""
+
+    def __init__(self, rank: int, size: int, device: int, group=None):
+        uid = b"\0" * 128
+        if size > 1:
+            import torch
+            import torch.distributed as dist
+
+            t = torch.zeros(128, dtype=torch.uint8)
+            if rank == 0:
+                t = torch.frombuffer(bytearray(Context.unique_id()), dtype=torch.uint8).clone()
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda(device)
+            dist.broadcast(t, 0, group=group)
+            uid = bytes(t.cpu().numpy().tobytes())
+        self.rank, self.size, self.device = rank, size, device
+        self.ctx = Context(device, rank, size, uid)
+
+    def close(self):
+        self.ctx.close()
+
+
+def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host_slab: Optional[np.ndarray] = None,
+                    batch_rows: int = 0) -> NmfResult:
+    """Row-partitioned MU (src/nmf_distributed.cpp:151-289) — collective over ``comm``.
+
+    ``a`` is the full A (ndarray / CsrMatrix; only this rank's rows are uploaded), or None
+    with ``host_slab`` (this rank's rows, float32) for the out-of-core mode.
+    """
+    cfg.validate()
+    if cfg.k != plan.k:
+        raise ShapeError(f"nmf_distributed: cfg.k={cfg.k} disagrees with plan.k={plan.k}")
+    if comm.size != plan.n_workers:
+        raise ShapeError(f"nmf_distributed: group size {comm.size} != plan workers {plan.n_workers}")
+    if plan.strategy != Strategy.rnmf:
+        raise ShapeError("nmf_distributed: the B200 backend implements the row partition (RNMF) only")
+    (r0, r1), _ = plan.slabs[comm.rank]
+    ctx = comm.ctx
+    ctx.set_problem(plan.m, plan.n, plan.k, r0, r1 - r0)
+    if host_slab is not None:
+        ctx.attach_host(host_slab, batch_rows)
+    elif isinstance(a, CsrMatrix):
+        ctx.load_csr(a.row_window(r0, r1))
+    else:
+        ctx.load_dense(np.asarray(a)[r0:r1])
+    if cfg.init == FactorInit.from_files:
+        ctx.set_factors(np.asarray(cfg.init_w)[r0:r1], cfg.init_h)
+    trace, info = ctx.solve(cfg)
+    _, h = ctx.get_factors()
+    w = ctx.gather_w()
+    return NmfResult(w, h, trace, int(info["iterations_run"]), bool(info["converged"]), _counters(info), info)

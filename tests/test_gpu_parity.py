@@ -1,0 +1,295 @@
+"""GPU parity: the B200 backend (through the C-ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star): objective trajectory within 1e-4 relative, final W and H within
+1e-3 relative Frobenius, fp32 on the GPU vs the reference's f64 on the same (f32-rounded)
+inputs and seeded init. Golden fixtures in tests/golden/ come from the reference itself
+(tests/golden/make_golden.py); the oracle port re-derives small cases at run time.
+"""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2202_09518_b200 as nmf
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+port = oracle.port
+
+TRACE_TOL = 1e-4
+FACTOR_TOL = 1e-3
+
+
+def f32(x):
+    return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+
+def rel_fro(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+def check_parity(res, trace_iters, trace_err, w=None, h=None):
+    got_it = np.array([i for i, _ in res.error_trace])
+    got = np.array([e for _, e in res.error_trace])
+    assert np.array_equal(got_it, np.asarray(trace_iters)), (got_it, trace_iters)
+    rel = np.max(np.abs(got - trace_err) / np.asarray(trace_err))
+    assert rel <= TRACE_TOL, f"trace rel diff {rel:.3e}"
+    if w is not None:
+        assert rel_fro(res.w, w) <= FACTOR_TOL, f"W rel {rel_fro(res.w, w):.3e}"
+        assert rel_fro(res.h, h) <= FACTOR_TOL, f"H rel {rel_fro(res.h, h):.3e}"
+    return rel
+
+
+def solve_from(a, k, iters, interval, seed=0, **kw):
+    m, n = a.shape
+    w0, h0 = port.init_factors(m, n, k, seed)
+    cfg = nmf.NmfConfig(k=k, max_iters=iters, error_check_interval=interval, eta=0.0,
+                        init=nmf.FactorInit.from_files, init_w=f32(w0), init_h=f32(h0), **kw)
+    return nmf.nmf_serial(a, cfg)
+
+
+# ---------------------------------------------------------------------------- contractions
+@pytest.mark.parametrize("m,n,k", [(256, 384, 16), (300, 517, 7), (1000, 130, 32), (129, 257, 64), (64, 64, 2)])
+def test_streaming_products_match_f64(gpu, m, n, k):
+    rng = np.random.default_rng(m * n + k)
+    a = rng.random((m, n)).astype(np.float32)
+    w = rng.random((m, k)).astype(np.float32).astype(np.float64)
+    h = rng.random((k, n)).astype(np.float32).astype(np.float64)
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.load_dense(a)
+        ctx.set_factors(w, h)
+        aht, wta, hht, wtw = ctx.products()
+    a64 = a.astype(np.float64)
+    assert rel_fro(aht, a64 @ h.T) < 3e-6
+    assert rel_fro(wta, w.T @ a64) < 3e-6
+    assert rel_fro(hht, h @ h.T) < 3e-6
+    assert rel_fro(wtw, w.T @ w) < 3e-6
+    assert np.array_equal(hht, hht.T) and np.array_equal(wtw, wtw.T)  # mirrored triangle
+
+
+def test_csr_products_match_f64(gpu):
+    rp, ci, v, (m, n) = port.gen_sparse(700, 500, 0.02, 3)
+    a = nmf.CsrMatrix(m, n, rp, ci, f32(v))
+    k = 16
+    rng = np.random.default_rng(1)
+    w = f32(rng.random((m, k)))
+    h = f32(rng.random((k, n)))
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.load_csr(a)
+        ctx.set_factors(w, h)
+        aht, wta, _, _ = ctx.products()
+    d = a.to_dense()
+    assert rel_fro(aht, d @ h.T) < 3e-6
+    assert rel_fro(wta, w.T @ d) < 3e-6
+
+
+# ---------------------------------------------------------------------------- full solves vs golden
+def _golden(name):
+    return np.load(os.path.join(GOLD, name + ".npz"))
+
+
+def test_config1_uniform_matches_reference(gpu):
+    g = _golden("config1_uniform_f32in")
+    a = port.uniform_dense(4096, 2048, 42, 99).astype(np.float32)
+    res = solve_from(a, 16, 100, 10)
+    check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
+    assert res.iterations_run == 100 and not res.converged
+
+
+def test_config1_lowrank_matches_reference(gpu):
+    g = _golden("config1_lowrank_f32in")
+    if not oracle.ref.available:
+        pytest.skip("low-rank input regeneration needs oracle/_ref")
+    a = oracle.ref.gen_lowrank(4096, 2048, 16, 0.01, 7)[0].astype(np.float32)
+    res = solve_from(a, 16, 100, 10)
+    check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
+
+
+def test_k32_matches_reference(gpu):
+    g = _golden("uniform_1536x1024_k32")
+    a = port.uniform_dense(1536, 1024, 42, 99).astype(np.float32)
+    res = solve_from(a, 32, 50, 10)
+    check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
+
+
+@pytest.mark.parametrize("name,k,iters,interval", [("lowrank_1024x768_k64", 64, 30, 10),
+                                                    ("lowrank_1024x768_k5", 5, 40, 10)])
+def test_k64_and_padded_k_match_reference(gpu, name, k, iters, interval):
+    if not oracle.ref.available:
+        pytest.skip("input regeneration needs oracle/_ref")
+    g = _golden(name)
+    a = oracle.ref.gen_lowrank(1024, 768, 12, 0.0, 3)[0].astype(np.float32)
+    res = solve_from(a, k, iters, interval)
+    check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
+
+
+def test_ragged_shape_matches_oracle(gpu):
+    # 333 x 517 (neither a multiple of 128), k = 7, interval 7, max_iters 60 (not a multiple).
+    a = f32(port.uniform_dense(333, 517, 5, 99))
+    w0, h0 = port.init_factors(333, 517, 7, 4)
+    ref = port.nmf_serial(a, 7, f32(w0), f32(h0), max_iters=60, interval=7)
+    res = solve_from(a.astype(np.float32), 7, 60, 7, seed=4)
+    check_parity(res, ref.trace_iters, ref.trace_err, ref.w, ref.h)
+
+
+def test_csr_matches_reference(gpu):
+    g = _golden("csr_3000x2500_d001_k16")
+    m, n = g["shape"].tolist()
+    a = nmf.CsrMatrix(m, n, g["rp"], g["ci"], g["v"])
+    w0, h0 = port.init_factors(m, n, 16, 0)
+    cfg = nmf.NmfConfig(k=16, max_iters=40, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    res = nmf.nmf_serial(a, cfg)
+    check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
+
+
+def test_device_sparse_generator_is_reference_generator(gpu):
+    m, n, dens, seed = 900, 1100, 0.01, 7
+    rp, ci, v, _ = port.gen_sparse(m, n, dens, seed)
+    up = nmf.CsrMatrix(m, n, rp, ci, f32(v))
+    k, iters = 8, 20
+    w0, h0 = port.init_factors(m, n, k, 0)
+    cfg = nmf.NmfConfig(k=k, max_iters=iters, error_check_interval=5, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.generate_csr_uniform(dens, seed)
+        ctx.set_factors(cfg.init_w, cfg.init_h)
+        tr_gen, _ = ctx.solve(cfg)
+        nrm = ctx.sq_norm()
+    res = nmf.nmf_serial(up, cfg)
+    # identical matrix (structure, order, f32 values) => bit-identical trajectory
+    assert [e for _, e in res.error_trace] == [e for _, e in tr_gen]
+    assert nrm == pytest.approx(float((f32(v) ** 2).sum()), rel=1e-12)
+
+
+def test_device_dense_generator_is_reference_generator(gpu):
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(1000, 300, 8, row0=37, rows=200)
+        ctx.generate_dense_uniform(42, 99)
+        got = ctx.download_dense()
+    want = port.uniform_dense(200, 300, 42, 99, row0=37).astype(np.float32)
+    assert np.array_equal(got, want)
+
+
+def test_device_init_is_reference_init(gpu):
+    # init=uniform01 on the device must equal the f32-rounded reference draw bit-for-bit.
+    m, n, k = 300, 200, 6
+    a = port.uniform_dense(m, n, 1, 99).astype(np.float32)
+    cfg = nmf.NmfConfig(k=k, max_iters=1, eta=0.0, seed=11)
+    r1 = nmf.nmf_serial(a, cfg)
+    w0, h0 = port.init_factors(m, n, k, 11)
+    cfg2 = nmf.NmfConfig(k=k, max_iters=1, eta=0.0, init=nmf.FactorInit.from_files, init_w=f32(w0),
+                         init_h=f32(h0))
+    r2 = nmf.nmf_serial(a, cfg2)
+    assert np.array_equal(r1.w, r2.w) and np.array_equal(r1.h, r2.h)
+
+
+def test_direct_error_mode_matches_trace_form(gpu):
+    a = port.uniform_dense(500, 400, 3, 99).astype(np.float32)
+    r1 = solve_from(a, 16, 30, 10)
+    r2 = solve_from(a, 16, 30, 10, error_mode="direct")
+    e1 = np.array([e for _, e in r1.error_trace])
+    e2 = np.array([e for _, e in r2.error_trace])
+    np.testing.assert_allclose(e1, e2, rtol=2e-5)
+    assert np.array_equal(r1.w, r2.w)
+
+
+def test_csr_direct_error_mode(gpu):
+    rp, ci, v, (m, n) = port.gen_sparse(600, 500, 0.03, 2)
+    a = nmf.CsrMatrix(m, n, rp, ci, f32(v))
+    w0, h0 = port.init_factors(m, n, 8, 0)
+    ref = port.nmf_serial((rp, ci, f32(v), (m, n)), 8, f32(w0), f32(h0), max_iters=20, interval=10)
+    for mode in ("trace", "direct"):
+        cfg = nmf.NmfConfig(k=8, max_iters=20, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                            init_w=f32(w0), init_h=f32(h0), error_mode=mode)
+        res = nmf.nmf_serial(a, cfg)
+        check_parity(res, ref.trace_iters, ref.trace_err, ref.w, ref.h)
+
+
+# ---------------------------------------------------------------------------- semantics / errors
+def test_fixed_point(gpu):
+    # SPEC.md:147 / acceptance 2: A = W0 H0 exactly, init at the exact factors.
+    w = f32(port.uniform_dense(256, 4, 1, 5))
+    h = f32(port.uniform_dense(4, 192, 2, 6))
+    a = (w @ h).astype(np.float32)
+    cfg = nmf.NmfConfig(k=4, max_iters=1, error_check_interval=1, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=w, init_h=h)
+    r = nmf.nmf_serial(a, cfg)
+    assert abs(np.linalg.norm(r.w) / np.linalg.norm(w) - 1) < 1e-5
+    assert abs(np.linalg.norm(r.h) / np.linalg.norm(h) - 1) < 1e-5
+    assert r.error_trace[0][1] < 1e-3
+
+
+def test_converges_on_exact_low_rank(gpu):
+    # SPEC.md acceptance 1 analogue: rank-4 100x80 input, k=4, converges, monotone trace.
+    if not oracle.ref.available:
+        pytest.skip("needs gen_lowrank from oracle/_ref")
+    a = oracle.ref.gen_lowrank(100, 80, 4, 0.0, 0)[0].astype(np.float32)
+    cfg = nmf.NmfConfig(k=4, eta=1e-3, max_iters=2000, error_check_interval=10, seed=0)
+    r = nmf.nmf_serial(a, cfg)
+    errs = [e for _, e in r.error_trace]
+    assert r.converged and errs[-1] <= 1e-3
+    assert all(b <= a_ + 1e-6 for a_, b in zip(errs, errs[1:]))
+    assert r.iterations_run == r.error_trace[-1][0]
+    assert np.all(r.w >= 0) and np.all(r.h >= 0)
+
+
+def test_error_behaviour(gpu):
+    a = np.ones((20, 10), np.float32)
+    with pytest.raises(nmf.DataError):
+        nmf.nmf_serial(np.zeros((20, 10), np.float32), nmf.NmfConfig(k=2, max_iters=3))
+    with pytest.raises(nmf.ShapeError):
+        nmf.nmf_serial(a, nmf.NmfConfig(k=65, max_iters=3))
+    with pytest.raises(nmf.ShapeError):
+        nmf.nmf_serial(a, nmf.NmfConfig(k=2, max_iters=0))
+    with pytest.raises(nmf.ShapeError):
+        nmf.nmf_serial(a, nmf.NmfConfig(k=2, init=nmf.FactorInit.from_files))
+    bad = a.copy()
+    bad[3, 4] = np.nan
+    with pytest.raises(nmf.DataError):
+        nmf.nmf_serial(bad, nmf.NmfConfig(k=2, max_iters=3, error_check_interval=1))
+    with nmf.Context(gpu) as ctx:
+        with pytest.raises(nmf.ShapeError):
+            ctx.set_problem(10, 10, 2, row0=5, rows=6)
+
+
+def test_out_of_core_equals_in_core(gpu):
+    m, n, k = 700, 600, 16
+    a = port.uniform_dense(m, n, 8, 99).astype(np.float32)
+    w0, h0 = port.init_factors(m, n, k, 0)
+    cfg = nmf.NmfConfig(k=k, max_iters=20, error_check_interval=5, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    incore = nmf.nmf_serial(a, cfg)
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.attach_host(a, batch_rows=128)
+        ctx.set_factors(cfg.init_w, cfg.init_h)
+        tr, info = ctx.solve(cfg)
+        w, h = ctx.get_factors()
+    e1 = np.array([e for _, e in incore.error_trace])
+    e2 = np.array([e for _, e in tr])
+    np.testing.assert_allclose(e2, e1, rtol=1e-6)
+    assert rel_fro(w, incore.w) < 1e-5 and rel_fro(h, incore.h) < 1e-5
+    assert info["h2d_bytes"] == 20 * m * n * 4
+    assert info["peak_resident_bytes"] == 2 * 128 * 640 * 4
+
+
+def test_cpp_host_core_is_a_drop_in(gpu):
+    exe = os.path.join(ROOT, "paper_2202_09518_b200", "lib", "host_api_demo")
+    out = subprocess.run([exe, "300", "200", "8"], capture_output=True, text=True, check=True).stdout
+    lines = [json.loads(x) for x in out.strip().splitlines()]
+    trace = [d["err"] for d in lines if "err" in d]
+    a = f32(port.uniform_dense(300, 200, 42, 99))
+    w0, h0 = port.init_factors(300, 200, 8, 0)
+    ref = port.nmf_serial(a, 8, f32(w0), f32(h0), max_iters=30, interval=10)
+    np.testing.assert_allclose(trace, ref.trace_err, rtol=TRACE_TOL)
+    norms = [d for d in lines if "w_fro" in d][0]
+    assert norms["w_fro"] == pytest.approx(np.linalg.norm(ref.w), rel=FACTOR_TOL)
+    assert any(d.get("shape_error") for d in lines)
