@@ -231,11 +231,17 @@ def test_converges_on_exact_low_rank(gpu):
     # SPEC.md acceptance 1 analogue: rank-4 100x80 input, k=4, converges, monotone trace.
     if not oracle.ref.available:
         pytest.skip("needs gen_lowrank from oracle/_ref")
+    # (The reference itself reaches 1.67e-3 after 2000 iterations on this input, so eta is
+    # set where the reference converges and the early exit must fire at the same check.)
     a = oracle.ref.gen_lowrank(100, 80, 4, 0.0, 0)[0].astype(np.float32)
-    cfg = nmf.NmfConfig(k=4, eta=1e-3, max_iters=2000, error_check_interval=10, seed=0)
+    w0, h0 = port.init_factors(100, 80, 4, 0)
+    ref = port.nmf_serial(a.astype(np.float64), 4, f32(w0), f32(h0), max_iters=2000, interval=10, eta=2e-3)
+    assert ref.converged
+    cfg = nmf.NmfConfig(k=4, eta=2e-3, max_iters=2000, error_check_interval=10, seed=0)
     r = nmf.nmf_serial(a, cfg)
     errs = [e for _, e in r.error_trace]
-    assert r.converged and errs[-1] <= 1e-3
+    assert r.converged and errs[-1] <= 2e-3
+    assert abs(r.iterations_run - ref.iterations_run) <= 20, (r.iterations_run, ref.iterations_run)
     assert all(b <= a_ + 1e-6 for a_, b in zip(errs, errs[1:]))
     assert r.iterations_run == r.error_trace[-1][0]
     assert np.all(r.w >= 0) and np.all(r.h >= 0)
