@@ -23,17 +23,25 @@ void plan_wta(StreamK& sk, int64_t mp, int64_t np, int num_sms);
 cudaError_t launch_wta(int kp, const float* A, int64_t lda, const float* W, float* slots,
                        const StreamK& sk, cudaStream_t s);
 
+// ---- tensor-core passes (kernels_tc.cu): kp in {32, 64}, 3xTF32 split precision ----
+bool tc_supported(int kp);
+cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* Ht,
+                          const float* Ht_lo, float* slots, const StreamK& sk, cudaStream_t s);
+cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* W,
+                          const float* W_lo, float* slots, const StreamK& sk, cudaStream_t s);
+
 // ---- factor kernels (kernels_factor.cu) ----
 // F (rows x kp, rows a multiple of 128) <- F * N / (F G + eps) rowwise, where N is either
 // a plain rows x kp matrix (n_plain) or stream-K partials (n_slots, sk). Emits per-CTA
 // partial Gram F_new^T F_new (gram_slots[gridDim][kp*kp]), per-CTA f64 partial
 // sum(N .* F_new) (err_slots, may be null) and sets *flag on non-finite output.
-// update == false: only emit the Gram of F (no update).
-int factor_grid(int64_t rows);
+// update == false: only emit the Gram of F (no update). lo_out (may be null) receives
+// F - tf32(F) of the resulting rows (the low half of the 3xTF32 split).
+int factor_grid(int64_t tiles);
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
                                  const float* n_slots, const StreamK* sk, const float* G,
                                  float eps, bool update, float* gram_slots, double* err_slots,
-                                 int* flag, cudaStream_t s);
+                                 int* flag, float* lo_out, cudaStream_t s);
 // out[e] = sum_s slots[s*E + e] (fixed order), E = count.
 cudaError_t launch_reduce_slots(const float* slots, int64_t nslots, int64_t count, float* out,
                                 cudaStream_t s);
@@ -65,6 +73,8 @@ cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t r
                                   int64_t cols, const float* W, const float* Ht,
                                   double* out_slots, cudaStream_t s);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s);
+// lo[i] = x[i] - tf32_trunc(x[i])
+cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s);
 
 // ---- CSR kernels (kernels_sparse.cu) ----
 // out (rows x kp) = CSR(rp, ci, v) · B (B rows indexed by column, kp wide).

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kFuThreads)
     k_factor_update(float* __restrict__ F, int64_t tiles, const float* __restrict__ n_plain,
                     const float* __restrict__ n_slots, StreamK sk, const float* __restrict__ G,
                     float eps, int update, float* __restrict__ gram_slots,
-                    double* __restrict__ err_slots, int* __restrict__ flag) {
+                    double* __restrict__ err_slots, int* __restrict__ flag, float* __restrict__ lo_out) {
     constexpr int FS = KP + 1;
     extern __shared__ __align__(16) unsigned char fu_smem[];
     double* red = reinterpret_cast<double*>(fu_smem);
@@ -108,6 +108,19 @@ __global__ void __launch_bounds__(kFuThreads)
 #pragma unroll
             for (int j4 = 0; j4 < KP / 4; ++j4)
                 fw[j4] = make_float4(f[4 * j4], f[4 * j4 + 1], f[4 * j4 + 2], f[4 * j4 + 3]);
+        }
+        if (lo_out) {
+            float4* lw = reinterpret_cast<float4*>(lo_out + row * KP);
+#pragma unroll
+            for (int j4 = 0; j4 < KP / 4; ++j4) {
+                float l[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const float x = f[4 * j4 + q];
+                    l[q] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+                }
+                lw[j4] = make_float4(l[0], l[1], l[2], l[3]);
+            }
         }
         // Gram partial of this tile: entries (i <= j), ascending rows.
 #pragma unroll
@@ -204,7 +217,7 @@ int factor_grid(int64_t tiles) { return int(tiles < 1184 ? tiles : 1184); }
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
                                  const float* n_slots, const StreamK* sk, const float* G,
                                  float eps, bool update, float* gram_slots, double* err_slots,
-                                 int* flag, cudaStream_t s) {
+                                 int* flag, float* lo_out, cudaStream_t s) {
     const int64_t tiles = rows / kTile;
     const int grid = factor_grid(tiles);
     StreamK skv = sk ? *sk : StreamK{};
@@ -217,7 +230,7 @@ cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_
         if (e != cudaSuccess) return e;                                                        \
         k_factor_update<K><<<grid, kFuThreads, smem, s>>>(F, tiles, n_plain, n_slots, skv, G,  \
                                                          eps, update ? 1 : 0, gram_slots,      \
-                                                         err_slots, flag);                     \
+                                                         err_slots, flag, lo_out);             \
         break;                                                                                 \
     }
     switch (kp) {

@@ -141,6 +141,13 @@ __global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag
     if (bad) atomicOr(flag, 1);
 }
 
+__global__ void k_split_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
+        const float v = x[q];
+        lo[q] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+    }
+}
+
 unsigned grid_for(int64_t work, int per_thread = 1) {
     const int64_t b = (work / per_thread + 255) / 256;
     return unsigned(b < 1 ? 1 : (b > 65535 * 16 ? 65535 * 16 : b));
@@ -200,6 +207,11 @@ cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t r
 
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s) {
     k_check_finite<<<grid_for(n, 8), 256, 0, s>>>(x, n, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s) {
+    k_split_lo<<<grid_for(n, 8), 256, 0, s>>>(x, lo, n);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,350 @@
+// Tensor-core (tcgen05, kind::tf32) streaming passes for kp in {32, 64}.
+//
+// At k = 32 an A-pass needs 16 flop per byte of A; CUDA-core FFMA tops out near 70% of the
+// HBM roofline there (SURVEY.md §7 hard part 1), so the contractions move to the 5th-gen
+// tensor cores. Single-pass TF32 fails the 1e-4 trace parity, so each tile runs the
+// split-precision "3xTF32" scheme:
+//     A·B ≈ A_hi·B_hi + A_lo·B_hi + A_hi·B_lo,   x_hi = tf32(x) (hardware truncation),
+//                                                x_lo = x - x_hi (exact in f32)
+// A_hi is the raw f32 tile TMA lands in shared memory (the MMA reads only its tf32 bits);
+// A_lo is made in shared memory by four "split" warps; B_lo (Ht_lo / W_lo, tiny) is
+// written by the factor-update kernel that produced B.
+//
+// Pipeline (one persistent CTA per SM, stream-K split as the FFMA path):
+//   warp 0        TMA producer: A tile + B_hi + B_lo per stage          -> full[s]
+//   warps 4..7    split: A_lo[s] = A[s] - trunc_tf32(A[s])               -> split[s]
+//   warp 1        MMA issuer: 3 x (BK/8) tcgen05.mma into a TMEM accumulator, commit
+//                 -> empty[s] (stage reusable) and, at a tile end, -> accfull[b]
+//   warps 4..7    epilogue at tile ends: tcgen05.ld 128 x kp accumulator -> slot  -> accempty[b]
+//
+// pass 1 (A·Ht):  D[128 rows x kp] += A[rows, 32 cols] · Ht[32 cols, kp]
+//                 A operand K-major (row-major A), B operand MN-major (Ht is n x kp).
+// pass 2 (A^T·W): D[128 cols x kp] += A^T[128 cols, 32 rows] · W[32 rows, kp]
+//                 A operand MN-major, B operand MN-major.
+// All operand tiles use the 128-byte swizzle (TMA SWIZZLE_128B == UMMA SWIZZLE_128B).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "kernels.h"
+
+namespace ooc {
+namespace {
+
+// ------------------------------------------------------------------ PTX wrappers
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    uint32_t ok = 0;
+    do {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+    } while (!ok);
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100).
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+           (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+}
+// Instruction descriptor: kind::tf32, f32 accumulate, M = 128, N = kp.
+__host__ __device__ constexpr uint32_t idesc_tf32(int n, int a_mn, int b_mn) {
+    return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
+           (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+// 32 consecutive fp32 TMEM columns of this warp's 32 lanes -> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+        "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// ------------------------------------------------------------------ kernel
+template <int KP, int PASS>
+struct TcCfg {
+    static constexpr int STAGES = 4;
+    static constexpr int A_BYTES = 128 * 32 * 4;         // 16 KB: 128 x 32 f32 per stage
+    static constexpr int B_BYTES = 32 * KP * 4;           // 32 (K) x kp f32
+    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A, A_lo, B_hi, B_lo
+    static constexpr uint32_t TX_BYTES = A_BYTES + 2 * B_BYTES;    // bytes TMA lands per stage
+    static constexpr int TMEM_COLS = 2 * KP <= 64 ? 64 : 128;     // double-buffered accumulator
+    static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    // descriptors
+    static constexpr uint32_t IDESC = idesc_tf32(KP, PASS == 2 ? 1 : 0, 1);
+};
+
+template <int KP, int PASS>
+__global__ void __launch_bounds__(256, 1)
+    k_pass_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ slots, StreamK sk) {
+    using C = TcCfg<KP, PASS>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+    uint64_t* full = bars;                     // [STAGES]
+    uint64_t* split = bars + C::STAGES;        // [STAGES]
+    uint64_t* empty = bars + 2 * C::STAGES;    // [STAGES]
+    uint64_t* accfull = bars + 3 * C::STAGES;  // [2]
+    uint64_t* accempty = accfull + 2;          // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t cta = blockIdx.x;
+    const int64_t u0 = sk.begin(cta), u1 = sk.begin(cta + 1);
+
+    if (tid == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(split + s, 4);
+            mbar_init(empty + s, 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(accfull + b, 1);
+            mbar_init(accempty + b, 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                     "r"(C::TMEM_COLS)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    auto stage_ptr = [&](int s) { return smem + s * C::STAGE_BYTES; };
+
+    if (warp == 0) {
+        // ---------------- TMA producer
+        if (lane == 0) {
+            for (int64_t u = u0; u < u1; ++u) {
+                const int s = int((u - u0) % C::STAGES);
+                const uint32_t ph = uint32_t((u - u0) / C::STAGES) & 1u;
+                mbar_wait(empty + s, ph ^ 1u);
+                uint8_t* st = stage_ptr(s);
+                uint8_t* sA = st;
+                uint8_t* sB = st + 2 * C::A_BYTES;
+                uint8_t* sBlo = sB + C::B_BYTES;
+                const int64_t tile = u / sk.ipt, it = u % sk.ipt;
+                mbar_expect_tx(full + s, C::TX_BYTES);
+                if (PASS == 1) {
+                    // A rows [tile*128, +128), cols [it*32, +32); B = Ht rows [it*32, +32)
+                    tma_load_2d(sA, &tmA, full + s, int(it * 32), int(tile * 128));
+                    for (int h = 0; h < KP / 32; ++h) {
+                        tma_load_2d(sB + h * 4096, &tmB, full + s, h * 32, int(it * 32));
+                        tma_load_2d(sBlo + h * 4096, &tmBlo, full + s, h * 32, int(it * 32));
+                    }
+                } else {
+                    // A rows [it*32, +32), cols [tile*128, +128) as 4 boxes of 32 cols; B = W rows [it*32, +32)
+                    for (int j = 0; j < 4; ++j) tma_load_2d(sA + j * 4096, &tmA, full + s, int(tile * 128 + j * 32), int(it * 32));
+                    for (int h = 0; h < KP / 32; ++h) {
+                        tma_load_2d(sB + h * 4096, &tmB, full + s, h * 32, int(it * 32));
+                        tma_load_2d(sBlo + h * 4096, &tmBlo, full + s, h * 32, int(it * 32));
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        int64_t sg = 0;
+        for (int64_t u = u0; u < u1;) {
+            const int64_t tile = u / sk.ipt;
+            const int64_t seg_end = min(u1, (tile + 1) * sk.ipt);
+            const int b = int(sg & 1);
+            mbar_wait(accempty + b, (uint32_t(sg >> 1) & 1u) ^ 1u);
+            tc_fence_after();
+            const uint32_t d = tmem + uint32_t(b * KP);
+            for (; u < seg_end; ++u) {
+                const int s = int((u - u0) % C::STAGES);
+                const uint32_t ph = uint32_t((u - u0) / C::STAGES) & 1u;
+                mbar_wait(split + s, ph);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(stage_ptr(s));
+                    const uint32_t alo0 = a0 + C::A_BYTES;
+                    const uint32_t b0 = a0 + 2 * C::A_BYTES;
+                    const uint32_t blo0 = b0 + C::B_BYTES;
+                    const bool first = (u == tile * sk.ipt) || (u == u0);
+#pragma unroll
+                    for (int kk = 0; kk < 4; ++kk) {
+                        // K step of 8: pass 1 A is K-major (+32 B inside the 128 B swizzle row);
+                        // MN-major operands advance one 8-row swizzle group (+1024 B).
+                        const uint32_t aoff = PASS == 1 ? kk * 32 : kk * 1024;
+                        const uint32_t boff = kk * 1024;
+                        const uint32_t a_lbo = PASS == 1 ? 16 : 4096, a_sbo = 1024;
+                        const uint64_t da = sdesc(a0 + aoff, a_lbo, a_sbo);
+                        const uint64_t dalo = sdesc(alo0 + aoff, a_lbo, a_sbo);
+                        const uint64_t db = sdesc(b0 + boff, 4096, 1024);
+                        const uint64_t dblo = sdesc(blo0 + boff, 4096, 1024);
+                        mma_tf32(d, da, db, C::IDESC, (first && kk == 0) ? 0u : 1u);
+                        mma_tf32(d, dalo, db, C::IDESC, 1u);
+                        mma_tf32(d, da, dblo, C::IDESC, 1u);
+                    }
+                    mma_commit(empty + s);
+                    if (u + 1 == seg_end) mma_commit(accfull + b);
+                }
+                __syncwarp();
+            }
+            ++sg;
+        }
+    } else if (warp >= 4) {
+        // ---------------- split (A_lo) + epilogue warpgroup
+        const int t = tid - 128;
+        const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
+        int64_t sg = 0;
+        for (int64_t u = u0; u < u1; ++u) {
+            const int s = int((u - u0) % C::STAGES);
+            const uint32_t ph = uint32_t((u - u0) / C::STAGES) & 1u;
+            mbar_wait(full + s, ph);
+            const float4* src = reinterpret_cast<const float4*>(stage_ptr(s));
+            float4* dst = reinterpret_cast<float4*>(stage_ptr(s) + C::A_BYTES);
+#pragma unroll
+            for (int i = 0; i < C::A_BYTES / 16 / 128; ++i) {
+                const float4 v = src[t + 128 * i];
+                float4 lo;
+                lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+                dst[t + 128 * i] = lo;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(split + s);
+
+            const int64_t tile = u / sk.ipt;
+            if (u + 1 == min(u1, (tile + 1) * sk.ipt)) {
+                const int b = int(sg & 1);
+                mbar_wait(accfull + b, uint32_t(sg >> 1) & 1u);
+                tc_fence_after();
+                float* out = slots + sk.slot(cta, tile) * int64_t(128 * KP) + int64_t(32 * q + lane) * KP;
+#pragma unroll
+                for (int h = 0; h < KP / 32; ++h) {
+                    float v[32];
+                    tmem_ld32(tmem + (uint32_t(32 * q) << 16) + uint32_t(b * KP + h * 32), v);
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4)
+                        reinterpret_cast<float4*>(out + h * 32)[j4] =
+                            make_float4(v[4 * j4], v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(accempty + b);
+                ++sg;
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS) : "memory");
+    }
+}
+
+// ------------------------------------------------------------------ host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// 2-D f32 row-major [rows][cols] (ld floats), box = 32 cols x box_rows, 128-byte swizzle.
+cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+    auto fn = encode_fn();
+    if (!fn) return cudaErrorNotSupported;
+    const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
+    const cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
+    const cuuint32_t box[2] = {32u, cuuint32_t(box_rows)};
+    const cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+template <int KP, int PASS>
+cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, float* slots,
+                      const StreamK& sk, cudaStream_t s) {
+    using C = TcCfg<KP, PASS>;
+    auto kern = k_pass_tc<KP, PASS>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    kern<<<unsigned(sk.G), 256, C::SMEM, s>>>(a, b, blo, slots, sk);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tc_supported(int kp) { return (kp == 32 || kp == 64) && encode_fn() != nullptr; }
+
+// Pass 1 on the tensor cores: A (mp x np, ld lda), Ht / Ht_lo (np x kp).
+cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* Ht,
+                          const float* Ht_lo, float* slots, const StreamK& sk, cudaStream_t s) {
+    CUtensorMap ma, mb, ml;
+    cudaError_t e;
+    if ((e = make_map(&ma, A, mp, np, lda, 128)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, Ht, np, kp, kp, 32)) != cudaSuccess) return e;
+    if ((e = make_map(&ml, Ht_lo, np, kp, kp, 32)) != cudaSuccess) return e;
+    return kp == 32 ? launch_tc<32, 1>(ma, mb, ml, slots, sk, s) : launch_tc<64, 1>(ma, mb, ml, slots, sk, s);
+}
+
+// Pass 2 on the tensor cores: W / W_lo (mp x kp).
+cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* W,
+                          const float* W_lo, float* slots, const StreamK& sk, cudaStream_t s) {
+    CUtensorMap ma, mb, ml;
+    cudaError_t e;
+    if ((e = make_map(&ma, A, mp, np, lda, 32)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, W, mp, kp, kp, 32)) != cudaSuccess) return e;
+    if ((e = make_map(&ml, W_lo, mp, kp, kp, 32)) != cudaSuccess) return e;
+    return kp == 32 ? launch_tc<32, 2>(ma, mb, ml, slots, sk, s) : launch_tc<64, 2>(ma, mb, ml, slots, sk, s);
+}
+
+}  // namespace ooc

@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -130,6 +131,8 @@ struct oocnmf_ctx {
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
     DevBuf W, Ht, HHt, packed, N1, slots1, slots2, gram_w, gram_h, err_slots, red_slots, scal, flag;
+    DevBuf W_lo, Ht_lo;          // low halves of the 3xTF32 split (tensor-core path only)
+    bool use_tc = false;         // kp in {32, 64}: tcgen05 passes; else CUDA-core FFMA passes
     StreamK sk1, sk2;            // in-core dense passes
     StreamK sk1b[2], sk2b[2];    // out-of-core: full batch / last batch
     bool norm_valid = false, factors_set = false, factors_valid = false;
@@ -160,6 +163,17 @@ void alloc_factors(oocnmf_ctx* c) {
     const int kp = c->kp;
     c->W.alloc(size_t(c->mp) * kp * 4, "W");
     c->Ht.alloc(size_t(c->np) * kp * 4, "Ht");
+    const char* force = std::getenv("OOCNMF_FORCE_FFMA");
+    c->use_tc = tc_supported(kp) && !(force && force[0] == '1');
+    if (c->use_tc) {
+        c->W_lo.alloc(size_t(c->mp) * kp * 4, "W_lo");
+        c->Ht_lo.alloc(size_t(c->np) * kp * 4, "Ht_lo");
+        ck(cudaMemsetAsync(c->W_lo.p, 0, c->W_lo.bytes, c->stream), "memset");
+        ck(cudaMemsetAsync(c->Ht_lo.p, 0, c->Ht_lo.bytes, c->stream), "memset");
+    } else {
+        c->W_lo.release();
+        c->Ht_lo.release();
+    }
     c->HHt.alloc(size_t(kp) * kp * 4, "HHt");
     c->packed.alloc(size_t(c->packed_count()) * 4, "packed");
     const int gw = factor_grid(c->mp / kTile), gh = factor_grid(c->np / kTile);
@@ -226,11 +240,26 @@ reduced:
     c->norm_valid = true;
 }
 
-// HH^T of the current Ht (gram only).
+float* wlo(oocnmf_ctx* c) { return c->use_tc ? c->W_lo.as<float>() : nullptr; }
+float* htlo(oocnmf_ctx* c) { return c->use_tc ? c->Ht_lo.as<float>() : nullptr; }
+
+// Pass 1 over an A slab (rows_p x np, rows_p a multiple of 128): slots <- A·Ht partials.
+cudaError_t pass1(oocnmf_ctx* c, const float* A, int64_t rows_p, float* slots, const StreamK& sk, cudaStream_t s) {
+    if (c->use_tc) return launch_aht_tc(c->kp, A, c->np, rows_p, c->np, c->Ht.as<float>(), htlo(c), slots, sk, s);
+    return launch_aht(c->kp, A, c->np, c->Ht.as<float>(), slots, sk, s);
+}
+// Pass 2 over an A slab with its W rows: slots <- A^T·W partials.
+cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W, const float* Wlo, float* slots,
+                  const StreamK& sk, cudaStream_t s) {
+    if (c->use_tc) return launch_wta_tc(c->kp, A, c->np, rows_p, c->np, W, Wlo, slots, sk, s);
+    return launch_wta(c->kp, A, c->np, W, slots, sk, s);
+}
+
+// HH^T of the current Ht (gram only; also refreshes Ht_lo for the tensor-core pass).
 void gram_h(oocnmf_ctx* c) {
     const int kp = c->kp;
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, nullptr, nullptr, nullptr, nullptr, 0.f, false,
-                                  c->gram_h.as<float>(), nullptr, c->flag.as<int>(), c->stream),
+                                  c->gram_h.as<float>(), nullptr, c->flag.as<int>(), htlo(c), c->stream),
           "gram H");
     count(c, launch_reduce_slots(c->gram_h.as<float>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
                                  c->HHt.as<float>(), c->stream),
@@ -247,15 +276,16 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     };
     rec(eStart);
     if (c->kind == Kind::dense) {
-        count(c, launch_aht(kp, c->A.as<float>(), c->np, c->Ht.as<float>(), c->slots1.as<float>(), c->sk1, s), "aht");
+        count(c, pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
         rec(eAht);
         count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, c->slots1.as<float>(), &c->sk1,
                                       c->HHt.as<float>(), eps, true, c->gram_w.as<float>(), nullptr,
-                                      c->flag.as<int>(), s),
+                                      c->flag.as<int>(), wlo(c), s),
               "W update");
         count(c, launch_reduce_slots(c->gram_w.as<float>(), gw, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
         rec(eWdone);
-        count(c, launch_wta(kp, c->A.as<float>(), c->np, c->W.as<float>(), c->slots2.as<float>(), c->sk2, s), "wta");
+        count(c, pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s),
+              "wta");
         rec(eWta);
         count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce WtA");
         rec(eReduced);
@@ -266,7 +296,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         rec(eAht);
         count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
                                       c->HHt.as<float>(), eps, true, c->gram_w.as<float>(), nullptr,
-                                      c->flag.as<int>(), s),
+                                      c->flag.as<int>(), nullptr, s),
               "W update");
         count(c, launch_reduce_slots(c->gram_w.as<float>(), gw, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
         rec(eWdone);
@@ -297,12 +327,13 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
             ck(cudaEventRecord(c->ev_copied[si], c->copy_stream), "event");
             ck(cudaStreamWaitEvent(s, c->ev_copied[si], 0), "wait copied");
             float* Wb = c->W.as<float>() + b0 * kp;
-            count(c, launch_aht(kp, st, c->np, c->Ht.as<float>(), c->slots1.as<float>(), s1, s), "aht");
+            float* Wlob = c->use_tc ? c->W_lo.as<float>() + b0 * kp : nullptr;
+            count(c, pass1(c, st, brp, c->slots1.as<float>(), s1, s), "aht");
             count(c, launch_factor_update(kp, Wb, brp, nullptr, c->slots1.as<float>(), &s1, c->HHt.as<float>(),
                                           eps, true, c->gram_w.as<float>() + b * gwb * kp * kp, nullptr,
-                                          c->flag.as<int>(), s),
+                                          c->flag.as<int>(), Wlob, s),
                   "W update");
-            count(c, launch_wta(kp, st, c->np, Wb, c->slots2.as<float>(), s2, s), "wta");
+            count(c, pass2(c, st, brp, Wb, Wlob, c->slots2.as<float>(), s2, s), "wta");
             count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), s2, c->wta(), b > 0, s), "reduce WtA");
             ck(cudaEventRecord(c->ev_free[si], s), "event");
         }
@@ -322,13 +353,14 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
             "allreduce [WtA|WtW]");
     if (timed) ck(cudaEventRecord(ev[eComm], s), "event");
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, c->wta(), nullptr, nullptr, c->wtw(), eps, true,
-                                  c->gram_h.as<float>(), c->err_slots.as<double>(), c->flag.as<int>(), s),
+                                  c->gram_h.as<float>(), c->err_slots.as<double>(), c->flag.as<int>(), htlo(c), s),
           "H update");
     count(c, launch_reduce_slots(c->gram_h.as<float>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
                                  c->HHt.as<float>(), s),
           "reduce HHt");
     if (timed) ck(cudaEventRecord(ev[eHdone], s), "event");
 }
+
 
 double error_check(oocnmf_ctx* c, int error_mode, int* bad) {
     const int kp = c->kp;
@@ -934,9 +966,13 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
         DevBuf t1;
         t1.alloc(size_t(c->mp) * kp * 4, "aht");
         if (c->kind == Kind::dense) {
-            ck(launch_aht(kp, c->A.as<float>(), c->np, c->Ht.as<float>(), c->slots1.as<float>(), c->sk1, s), "aht");
+            if (c->use_tc) {
+                ck(launch_split_lo(c->Ht.as<float>(), c->Ht_lo.as<float>(), c->np * kp, s), "split");
+                ck(launch_split_lo(c->W.as<float>(), c->W_lo.as<float>(), c->mp * kp, s), "split");
+            }
+            ck(pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
             ck(launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, t1.as<float>(), false, s), "reduce");
-            ck(launch_wta(kp, c->A.as<float>(), c->np, c->W.as<float>(), c->slots2.as<float>(), c->sk2, s), "wta");
+            ck(pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s), "wta");
             ck(launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce");
         } else {
             ck(launch_spmm(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows, c->Ht.as<float>(),
@@ -948,7 +984,7 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
         }
         gram_h(c);
         ck(launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, 0.f, false,
-                                c->gram_w.as<float>(), nullptr, c->flag.as<int>(), s),
+                                c->gram_w.as<float>(), nullptr, c->flag.as<int>(), nullptr, s),
            "gram W");
         ck(launch_reduce_slots(c->gram_w.as<float>(), factor_grid(c->mp / kTile), int64_t(kp) * kp, c->wtw(), s),
            "reduce");
