@@ -61,10 +61,23 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-// UMMA shared-memory descriptor, SWIZZLE_128B, version 1 (sm_100).
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor, version 1 (sm_100). Layout 2 = SWIZZLE_128B (16-byte
+// granules XOR row%8; K-major tf32 operands), layout 1 = SWIZZLE_128B_BASE32B (32-byte
+// granules XOR row%4; the only 128-byte swizzle kind::tf32 accepts for MN-major operands —
+// verified on B200 by tools/tc_micro3.cu: MN-major tf32 with plain SWIZZLE_128B reads zeros).
+constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128B32 = 1;
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
-           (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(2) << 61);
+           (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(layout) << 61);
+}
+// K-major, 128-byte rows of K, 8-row swizzle groups; one MMA K step (8 x f32) = +32 B.
+__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int kk) {
+    return sdesc(base + kk * 32, 16, 1024, kLayoutSW128);
+}
+// MN-major, 128-byte rows of MN (32 f32), one row per K index, 4-row swizzle groups (512 B),
+// MN atoms of 32 elements every `atom_stride` bytes; one MMA K step (8 rows) = +1024 B.
+__device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int kk, uint32_t atom_stride) {
+    return sdesc(base + kk * 1024, atom_stride, 512, kLayoutSW128B32);
 }
 // Instruction descriptor: kind::tf32, f32 accumulate, M = 128, N = kp.
 __host__ __device__ constexpr uint32_t idesc_tf32(int n, int a_mn, int b_mn) {
@@ -86,14 +99,16 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
     uint32_t r[32];
     asm volatile(
+        // wait::ld inside the same asm: the destination registers are only defined after it.
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
-        "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
         : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
           "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
           "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
           "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        : "r"(taddr)
+        : "memory");
 #pragma unroll
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
@@ -209,15 +224,12 @@ __global__ void __launch_bounds__(256, 1)
                     const bool first = (u == tile * sk.ipt) || (u == u0);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        // K step of 8: pass 1 A is K-major (+32 B inside the 128 B swizzle row);
-                        // MN-major operands advance one 8-row swizzle group (+1024 B).
-                        const uint32_t aoff = PASS == 1 ? kk * 32 : kk * 1024;
-                        const uint32_t boff = kk * 1024;
-                        const uint32_t a_lbo = PASS == 1 ? 16 : 4096, a_sbo = 1024;
-                        const uint64_t da = sdesc(a0 + aoff, a_lbo, a_sbo);
-                        const uint64_t dalo = sdesc(alo0 + aoff, a_lbo, a_sbo);
-                        const uint64_t db = sdesc(b0 + boff, 4096, 1024);
-                        const uint64_t dblo = sdesc(blo0 + boff, 4096, 1024);
+                        // pass 1: A K-major; pass 2: A MN-major (4 atoms of 32 columns, 4 KB
+                        // apart). B (Ht / W tiles) is always MN-major (kp/32 atoms, 4 KB apart).
+                        const uint64_t da = PASS == 1 ? desc_kmajor(a0, kk) : desc_mnmajor(a0, kk, 4096);
+                        const uint64_t dalo = PASS == 1 ? desc_kmajor(alo0, kk) : desc_mnmajor(alo0, kk, 4096);
+                        const uint64_t db = desc_mnmajor(b0, kk, 4096);
+                        const uint64_t dblo = desc_mnmajor(blo0, kk, 4096);
                         mma_tf32(d, da, db, C::IDESC, (first && kk == 0) ? 0u : 1u);
                         mma_tf32(d, dalo, db, C::IDESC, 1u);
                         mma_tf32(d, da, dblo, C::IDESC, 1u);
@@ -296,8 +308,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D f32 row-major [rows][cols] (ld floats), box = 32 cols x box_rows, 128-byte swizzle.
-cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows) {
+// 2-D f32 row-major [rows][cols] (ld floats), box = 32 cols x box_rows. K-major operand tiles
+// use the 16-byte-granule 128B swizzle, MN-major ones the 32-byte-granule variant that
+// matches UMMA's SWIZZLE_128B_BASE32B layout.
+cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                     bool mn_major) {
     auto fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
     const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
@@ -305,7 +320,9 @@ cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t co
     const cuuint32_t box[2] = {32u, cuuint32_t(box_rows)};
     const cuuint32_t estr[2] = {1u, 1u};
     const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -330,9 +347,9 @@ cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
                           const float* Ht_lo, float* slots, const StreamK& sk, cudaStream_t s) {
     CUtensorMap ma, mb, ml;
     cudaError_t e;
-    if ((e = make_map(&ma, A, mp, np, lda, 128)) != cudaSuccess) return e;
-    if ((e = make_map(&mb, Ht, np, kp, kp, 32)) != cudaSuccess) return e;
-    if ((e = make_map(&ml, Ht_lo, np, kp, kp, 32)) != cudaSuccess) return e;
+    if ((e = make_map(&ma, A, mp, np, lda, 128, false)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, Ht, np, kp, kp, 32, true)) != cudaSuccess) return e;
+    if ((e = make_map(&ml, Ht_lo, np, kp, kp, 32, true)) != cudaSuccess) return e;
     return kp == 32 ? launch_tc<32, 1>(ma, mb, ml, slots, sk, s) : launch_tc<64, 1>(ma, mb, ml, slots, sk, s);
 }
 
@@ -341,9 +358,9 @@ cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
                           const float* W_lo, float* slots, const StreamK& sk, cudaStream_t s) {
     CUtensorMap ma, mb, ml;
     cudaError_t e;
-    if ((e = make_map(&ma, A, mp, np, lda, 32)) != cudaSuccess) return e;
-    if ((e = make_map(&mb, W, mp, kp, kp, 32)) != cudaSuccess) return e;
-    if ((e = make_map(&ml, W_lo, mp, kp, kp, 32)) != cudaSuccess) return e;
+    if ((e = make_map(&ma, A, mp, np, lda, 32, true)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, W, mp, kp, kp, 32, true)) != cudaSuccess) return e;
+    if ((e = make_map(&ml, W_lo, mp, kp, kp, 32, true)) != cudaSuccess) return e;
     return kp == 32 ? launch_tc<32, 2>(ma, mb, ml, slots, sk, s) : launch_tc<64, 2>(ma, mb, ml, slots, sk, s);
 }
 
