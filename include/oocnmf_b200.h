@@ -66,9 +66,12 @@ typedef struct {
                                       oocnmf_set_factors_f64 (FactorInit::from_files),
                                       2 = continue from the factors resident on the device
                                       (warm restart after a previous oocnmf_solve) */
-    int32_t error_mode;            /* 0 = trace form ||A||^2 - 2<W^T A,H> + <W^T W,H H^T>
-                                      (free: every term exists after the H update),
-                                      1 = direct residual pass over A at check iterations */
+    int32_t error_mode;            /* 0 = auto: trace form ||A||^2 - 2<W^T A,H> + <W^T W,H H^T>
+                                      (free: every term exists after the H update), re-done
+                                      with the direct residual when it reports < 0.1 (where
+                                      the trace form's cancellation costs accuracy);
+                                      1 = direct residual (f64) at every check;
+                                      2 = trace form only */
 } oocnmf_config;
 
 /* Mirrors PhaseCounters (include/oocnmf/nmf.hpp:30-39) + NmfResult scalars + kernel

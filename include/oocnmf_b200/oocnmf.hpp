@@ -146,7 +146,7 @@ std::uint64_t derive_seed(std::uint64_t seed, std::uint64_t a, std::uint64_t b =
 inline constexpr double kDefaultEpsilon = 1e-12;
 enum class FactorInit { uniform01, from_files };
 /// B200 extension: how the relative error is evaluated at check iterations.
-enum class ErrorMode { trace = 0, direct = 1 };
+enum class ErrorMode { automatic = 0, direct = 1, trace = 2 };
 
 struct NmfConfig {
     index_t k = 1;
@@ -160,7 +160,7 @@ struct NmfConfig {
     std::optional<DenseMatrix> init_h;
     // B200 extensions (defaults reproduce the reference's behaviour on GPU 0)
     int device = 0;
-    ErrorMode error_mode = ErrorMode::trace;
+    ErrorMode error_mode = ErrorMode::automatic;
     void validate() const;
 };
 

@@ -40,17 +40,18 @@ cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
 int factor_grid(int64_t tiles);
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
                                  const float* n_slots, const StreamK* sk, const float* G,
-                                 float eps, bool update, float* gram_slots, double* err_slots,
+                                 float eps, bool update, double* gram_slots, double* err_slots,
                                  int* flag, float* lo_out, cudaStream_t s);
-// out[e] = sum_s slots[s*E + e] (fixed order), E = count.
-cudaError_t launch_reduce_slots(const float* slots, int64_t nslots, int64_t count, float* out,
-                                cudaStream_t s);
+// out[e] = sum_s slots[s*E + e] in f64 (fixed order), E = count; written as f32 (out32) and,
+// if out64 != null, f64.
+cudaError_t launch_reduce_slots(const double* slots, int64_t nslots, int64_t count, float* out32,
+                                double* out64, cudaStream_t s);
 // out (tiles*128 x kp) <- [out +] sum of each tile's stream-K partials (ascending CTA order).
 cudaError_t launch_streamk_reduce(int kp, const float* slots, const StreamK& sk, float* out,
                                   bool accumulate, cudaStream_t s);
 // trace slot <- sqrt(max(0, nA2 - 2 sum(err_slots) + <WtW, HHt>)) / sqrt(nA2)   (f64)
 cudaError_t launch_finalize_error(int kp, const double* err_slots, int64_t n_err,
-                                  const float* wtw, const float* hht, const double* norm_a2,
+                                  const double* wtw, const double* hht, const double* norm_a2,
                                   const double* direct_res /* null = trace form */,
                                   double* out_err, cudaStream_t s);
 

@@ -32,7 +32,7 @@ template <int KP>
 __global__ void __launch_bounds__(kFuThreads)
     k_factor_update(float* __restrict__ F, int64_t tiles, const float* __restrict__ n_plain,
                     const float* __restrict__ n_slots, StreamK sk, const float* __restrict__ G,
-                    float eps, int update, float* __restrict__ gram_slots,
+                    float eps, int update, double* __restrict__ gram_slots,
                     double* __restrict__ err_slots, int* __restrict__ flag, float* __restrict__ lo_out) {
     constexpr int FS = KP + 1;
     extern __shared__ __align__(16) unsigned char fu_smem[];
@@ -44,9 +44,9 @@ __global__ void __launch_bounds__(kFuThreads)
         for (int e = tid; e < KP * KP; e += kFuThreads) Gs[e] = G[e];
 
     constexpr int NE = (KP * KP + kFuThreads - 1) / kFuThreads;  // gram entries per thread
-    float gacc[NE];
+    double gacc[NE];  // f64: the Gram feeds <W^T W, H H^T> of the trace-form error
 #pragma unroll
-    for (int q = 0; q < NE; ++q) gacc[q] = 0.f;
+    for (int q = 0; q < NE; ++q) gacc[q] = 0.0;
     double eacc = 0.0;
     bool bad = false;
     __syncthreads();
@@ -132,15 +132,15 @@ __global__ void __launch_bounds__(kFuThreads)
             if (e < KP * KP) {
                 const int i = e / KP, j = e % KP;
                 if (i <= j) {
-                    float s = gacc[q];
-                    for (int r = 0; r < kTile; ++r) s = fmaf(Fs[r * FS + i], Fs[r * FS + j], s);
+                    double s = gacc[q];  // f32 x f32 products are exact in f64
+                    for (int r = 0; r < kTile; ++r) s = fma(double(Fs[r * FS + i]), double(Fs[r * FS + j]), s);
                     gacc[q] = s;
                 }
             }
         }
         __syncthreads();
     }
-    float* gout = gram_slots + int64_t(blockIdx.x) * KP * KP;
+    double* gout = gram_slots + int64_t(blockIdx.x) * KP * KP;
 #pragma unroll
     for (int q = 0; q < NE; ++q) {
         const int e = tid + q * kFuThreads;
@@ -160,16 +160,19 @@ __global__ void __launch_bounds__(kFuThreads)
 }
 
 // One warp per output element; lanes stride the slots, then a fixed shuffle tree.
-__global__ void k_reduce_slots(const float* __restrict__ slots, int64_t nslots, int64_t count,
-                               float* __restrict__ out) {
+__global__ void k_reduce_slots(const double* __restrict__ slots, int64_t nslots, int64_t count,
+                               float* __restrict__ out32, double* __restrict__ out64) {
     const int64_t e = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (e >= count) return;
-    float s = 0.f;
+    double s = 0.0;
     for (int64_t q = lane; q < nslots; q += 32) s += slots[q * count + e];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[e] = s;
+    if (lane == 0) {
+        out32[e] = float(s);
+        if (out64) out64[e] = s;
+    }
 }
 
 template <int KP>
@@ -190,7 +193,7 @@ __global__ void k_streamk_reduce(const float* __restrict__ slots, StreamK sk, fl
 }
 
 __global__ void k_finalize_error(int kp, const double* __restrict__ err_slots, int64_t n_err,
-                                 const float* __restrict__ wtw, const float* __restrict__ hht,
+                                 const double* __restrict__ wtw, const double* __restrict__ hht,
                                  const double* __restrict__ norm_a2,
                                  const double* __restrict__ direct_res, double* __restrict__ out) {
     __shared__ double sh[256];
@@ -203,7 +206,7 @@ __global__ void k_finalize_error(int kp, const double* __restrict__ err_slots, i
         for (int64_t q = tid; q < n_err; q += blockDim.x) a += err_slots[q];
         const double cross = block_sum_f64(a, sh);
         double b = 0.0;
-        for (int e = tid; e < kp * kp; e += blockDim.x) b += double(wtw[e]) * double(hht[e]);
+        for (int e = tid; e < kp * kp; e += blockDim.x) b += wtw[e] * hht[e];
         const double quad = block_sum_f64(b, sh);
         res = *norm_a2 - 2.0 * cross + quad;
     }
@@ -216,7 +219,7 @@ int factor_grid(int64_t tiles) { return int(tiles < 1184 ? tiles : 1184); }
 
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
                                  const float* n_slots, const StreamK* sk, const float* G,
-                                 float eps, bool update, float* gram_slots, double* err_slots,
+                                 float eps, bool update, double* gram_slots, double* err_slots,
                                  int* flag, float* lo_out, cudaStream_t s) {
     const int64_t tiles = rows / kTile;
     const int grid = factor_grid(tiles);
@@ -244,10 +247,10 @@ cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_
     return cudaGetLastError();
 }
 
-cudaError_t launch_reduce_slots(const float* slots, int64_t nslots, int64_t count, float* out,
-                                cudaStream_t s) {
+cudaError_t launch_reduce_slots(const double* slots, int64_t nslots, int64_t count, float* out32,
+                                double* out64, cudaStream_t s) {
     const int64_t threads = count * 32;
-    k_reduce_slots<<<unsigned((threads + 255) / 256), 256, 0, s>>>(slots, nslots, count, out);
+    k_reduce_slots<<<unsigned((threads + 255) / 256), 256, 0, s>>>(slots, nslots, count, out32, out64);
     return cudaGetLastError();
 }
 
@@ -263,8 +266,8 @@ cudaError_t launch_streamk_reduce(int kp, const float* slots, const StreamK& sk,
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize_error(int kp, const double* err_slots, int64_t n_err, const float* wtw,
-                                  const float* hht, const double* norm_a2, const double* direct_res,
+cudaError_t launch_finalize_error(int kp, const double* err_slots, int64_t n_err, const double* wtw,
+                                  const double* hht, const double* norm_a2, const double* direct_res,
                                   double* out_err, cudaStream_t s) {
     k_finalize_error<<<1, 256, 0, s>>>(kp, err_slots, n_err, wtw, hht, norm_a2, direct_res, out_err);
     return cudaGetLastError();

@@ -122,10 +122,12 @@ __global__ void __launch_bounds__(256) k_residual_dense(const float* __restrict_
         for (int t = 0; t < 4; ++t) {
             const int64_t r = rb * 4 + t;
             if (r >= rows) break;
-            float wh = 0.f;
+            // (WH)_rj in f64 from the f32 factors (products exact): the residual keeps its
+            // relative accuracy even when ||A - WH|| << ||A|| (where the trace form cancels).
+            double wh = 0.0;
 #pragma unroll
-            for (int q = 0; q < KP; ++q) wh = fmaf(Ws[t][q], h[q], wh);
-            const double d = double(A[r * lda + j]) - double(wh);
+            for (int q = 0; q < KP; ++q) wh = fma(double(Ws[t][q]), double(h[q]), wh);
+            const double d = double(A[r * lda + j]) - wh;
             acc += d * d;
         }
     }

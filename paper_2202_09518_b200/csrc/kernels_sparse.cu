@@ -84,10 +84,10 @@ __global__ void __launch_bounds__(256) k_cross_csr(const int64_t* __restrict__ r
          i += int64_t(gridDim.x) * blockDim.x) {
         for (int64_t p = rp[i]; p < rp[i + 1]; ++p) {
             const int64_t j = ci[p];
-            float s = 0.f;
+            double s = 0.0;
 #pragma unroll
-            for (int q = 0; q < KP; ++q) s = fmaf(W[i * KP + q], Ht[j * KP + q], s);
-            acc += double(v[p]) * double(s);
+            for (int q = 0; q < KP; ++q) s = fma(double(W[i * KP + q]), double(Ht[j * KP + q]), s);
+            acc += double(v[p]) * s;
         }
     }
     const double s = block_sum256(acc);

@@ -3,25 +3,32 @@
 // At k = 32 an A-pass needs 16 flop per byte of A; CUDA-core FFMA tops out near 70% of the
 // HBM roofline there (SURVEY.md §7 hard part 1), so the contractions move to the 5th-gen
 // tensor cores. Single-pass TF32 fails the 1e-4 trace parity, so each tile runs the
-// split-precision "3xTF32" scheme:
-//     A·B ≈ A_hi·B_hi + A_lo·B_hi + A_hi·B_lo,   x_hi = tf32(x) (hardware truncation),
+// split-precision "3xTF32" scheme
+//     A·B ≈ A_hi·B_hi + A_hi·B_lo + A_lo·B_hi,   x_hi = tf32(x) (hardware truncation),
 //                                                x_lo = x - x_hi (exact in f32)
+// arranged so the streamed A tile is read from shared memory only once per K step:
+//   MMA 1 (SS): D'[:, 0:2kp] += A_hi(smem) · [B_hi | B_lo](smem)     one N = 2kp MMA
+//   MMA 2 (TS): D'[:, 0:kp]  += A_lo(TMEM) · B_hi(smem)              A_lo never touches smem
+//   epilogue:   D = D'[:, 0:kp] + D'[:, kp:2kp]
 // A_hi is the raw f32 tile TMA lands in shared memory (the MMA reads only its tf32 bits);
-// A_lo is made in shared memory by four "split" warps; B_lo (Ht_lo / W_lo, tiny) is
-// written by the factor-update kernel that produced B.
+// A_lo is produced by four "split" warps that read the tile and tcgen05.st the low halves
+// straight into TMEM in the K-major operand layout (transposing for pass 2); B_lo
+// (Ht_lo / W_lo) is written by the factor-update kernel that produced B.
 //
 // Pipeline (one persistent CTA per SM, stream-K split as the FFMA path):
-//   warp 0        TMA producer: A tile + B_hi + B_lo per stage          -> full[s]
-//   warps 4..7    split: A_lo[s] = A[s] - trunc_tf32(A[s])               -> split[s]
-//   warp 1        MMA issuer: 3 x (BK/8) tcgen05.mma into a TMEM accumulator, commit
-//                 -> empty[s] (stage reusable) and, at a tile end, -> accfull[b]
-//   warps 4..7    epilogue at tile ends: tcgen05.ld 128 x kp accumulator -> slot  -> accempty[b]
+//   warp 0      TMA producer: A tile + B_hi + B_lo per stage                 -> full[s]
+//   warps 4..7  split: A_lo[s] -> TMEM                                        -> split[s]
+//   warp 1      MMA issuer; commit -> empty[s] (smem stage + TMEM A_lo slot free) and, at
+//               a tile end, -> accfull[b]
+//   warps 4..7  epilogue at tile ends: tcgen05.ld the 128 x 2kp accumulator -> slot -> accempty[b]
 //
 // pass 1 (A·Ht):  D[128 rows x kp] += A[rows, 32 cols] · Ht[32 cols, kp]
-//                 A operand K-major (row-major A), B operand MN-major (Ht is n x kp).
+//                 A K-major (row-major A tile), B MN-major (Ht is n x kp).
 // pass 2 (A^T·W): D[128 cols x kp] += A^T[128 cols, 32 rows] · W[32 rows, kp]
-//                 A operand MN-major, B operand MN-major.
-// All operand tiles use the 128-byte swizzle (TMA SWIZZLE_128B == UMMA SWIZZLE_128B).
+//                 A MN-major (4 atoms of 32 columns), B MN-major.
+// Swizzles (verified on B200 with tools/tc_micro*.cu): K-major tf32 operands use
+// SWIZZLE_128B (TMA SWIZZLE_128B); MN-major tf32 operands must use SWIZZLE_128B_BASE32B
+// (TMA SWIZZLE_128B_ATOM_32B) — with the plain 128B swizzle the MMA reads zeros.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -51,20 +58,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "memory");
     } while (!ok);
 }
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y) {
+// L2 eviction policies (the encodings CUTLASS uses for TMA cache hints).
+constexpr uint64_t kEvictFirst = 0x12F0000000000000ull, kEvictLast = 0x14F0000000000000ull;
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+                                            uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
-            smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
 // UMMA shared-memory descriptor, version 1 (sm_100). Layout 2 = SWIZZLE_128B (16-byte
-// granules XOR row%8; K-major tf32 operands), layout 1 = SWIZZLE_128B_BASE32B (32-byte
-// granules XOR row%4; the only 128-byte swizzle kind::tf32 accepts for MN-major operands —
-// verified on B200 by tools/tc_micro3.cu: MN-major tf32 with plain SWIZZLE_128B reads zeros).
+// granules XOR row%8), layout 1 = SWIZZLE_128B_BASE32B (32-byte granules XOR row%4).
 constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128B32 = 1;
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
@@ -79,15 +87,22 @@ __device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int kk) {
 __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int kk, uint32_t atom_stride) {
     return sdesc(base + kk * 1024, atom_stride, 512, kLayoutSW128B32);
 }
-// Instruction descriptor: kind::tf32, f32 accumulate, M = 128, N = kp.
+// Instruction descriptor: kind::tf32, f32 accumulate, M = 128.
 __host__ __device__ constexpr uint32_t idesc_tf32(int n, int a_mn, int b_mn) {
     return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
            (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 }
-__device__ __forceinline__ void mma_tf32(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
         "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(
+            d),
+        "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
         : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
@@ -95,36 +110,55 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 
-// 32 consecutive fp32 TMEM columns of this warp's 32 lanes -> 32 registers per thread.
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-    uint32_t r[32];
+#define OOC_R32(r)                                                                                               \
+    "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),  \
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),   \
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),  \
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+#define OOC_W32(r)                                                                                               \
+    "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]), \
+        "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]),          \
+        "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]),          \
+        "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+
+// 32 consecutive 32-bit TMEM columns of this warp's 32 lanes <-> 32 registers per thread.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+    // wait::ld inside the same asm: the destination registers are only defined after it.
     asm volatile(
-        // wait::ld inside the same asm: the destination registers are only defined after it.
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
         "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
         "tcgen05.wait::ld.sync.aligned;"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-          "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-          "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : OOC_R32(r)
         : "r"(taddr)
         : "memory");
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%"
+        "18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n\t"
+        "tcgen05.wait::st.sync.aligned;" ::"r"(taddr),
+        OOC_W32(r)
+        : "memory");
+}
+
+__device__ __forceinline__ uint32_t lo_bits(float x) {
+    return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
 }
 
 // ------------------------------------------------------------------ kernel
 template <int KP, int PASS>
 struct TcCfg {
-    static constexpr int STAGES = 4;
-    static constexpr int A_BYTES = 128 * 32 * 4;         // 16 KB: 128 x 32 f32 per stage
-    static constexpr int B_BYTES = 32 * KP * 4;           // 32 (K) x kp f32
-    static constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;  // A, A_lo, B_hi, B_lo
-    static constexpr uint32_t TX_BYTES = A_BYTES + 2 * B_BYTES;    // bytes TMA lands per stage
-    static constexpr int TMEM_COLS = 2 * KP <= 64 ? 64 : 128;     // double-buffered accumulator
+    static constexpr int STAGES = KP == 32 ? 6 : 5;
+    static constexpr int A_BYTES = 128 * 32 * 4;              // 16 KB: 128 x 32 f32 per stage
+    static constexpr int B_BYTES = 32 * KP * 4;                // 32 (K) x kp f32
+    static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A, B_hi, B_lo (B_lo right after B_hi)
+    static constexpr uint32_t TX_BYTES = STAGE_BYTES;          // everything arrives by TMA
+    static constexpr int ACC_COLS = 2 * KP;                    // D' = [hi | lo] columns per buffer
+    static constexpr int ALO_COL0 = 2 * ACC_COLS;              // A_lo slots after 2 accumulators
+    static constexpr int TMEM_COLS = (ALO_COL0 + STAGES * 32) <= 256 ? 256 : 512;
     static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    // descriptors
-    static constexpr uint32_t IDESC = idesc_tf32(KP, PASS == 2 ? 1 : 0, 1);
+    static constexpr uint32_t IDESC_SS = idesc_tf32(2 * KP, PASS == 2 ? 1 : 0, 1);  // A_hi · [B_hi|B_lo]
+    static constexpr uint32_t IDESC_TS = idesc_tf32(KP, 0, 1);                       // A_lo(TMEM, K-major) · B_hi
 };
 
 template <int KP, int PASS>
@@ -170,122 +204,132 @@ __global__ void __launch_bounds__(256, 1)
     const uint32_t tmem = *tmem_slot;
 
     auto stage_ptr = [&](int s) { return smem + s * C::STAGE_BYTES; };
-
+    // Loop-carried ring / tile counters instead of 64-bit divisions per unit.
     if (warp == 0) {
         // ---------------- TMA producer
         if (lane == 0) {
+            int s = 0;
+            uint32_t ph = 0;
+            int64_t tile = u0 / sk.ipt, it = u0 % sk.ipt;
             for (int64_t u = u0; u < u1; ++u) {
-                const int s = int((u - u0) % C::STAGES);
-                const uint32_t ph = uint32_t((u - u0) / C::STAGES) & 1u;
                 mbar_wait(empty + s, ph ^ 1u);
-                uint8_t* st = stage_ptr(s);
-                uint8_t* sA = st;
-                uint8_t* sB = st + 2 * C::A_BYTES;
+                uint8_t* sA = stage_ptr(s);
+                uint8_t* sB = sA + C::A_BYTES;
                 uint8_t* sBlo = sB + C::B_BYTES;
-                const int64_t tile = u / sk.ipt, it = u % sk.ipt;
                 mbar_expect_tx(full + s, C::TX_BYTES);
                 if (PASS == 1) {
                     // A rows [tile*128, +128), cols [it*32, +32); B = Ht rows [it*32, +32)
-                    tma_load_2d(sA, &tmA, full + s, int(it * 32), int(tile * 128));
-                    for (int h = 0; h < KP / 32; ++h) {
-                        tma_load_2d(sB + h * 4096, &tmB, full + s, h * 32, int(it * 32));
-                        tma_load_2d(sBlo + h * 4096, &tmBlo, full + s, h * 32, int(it * 32));
-                    }
+                    tma_load_2d(sA, &tmA, full + s, int(it * 32), int(tile * 128), kEvictFirst);
                 } else {
                     // A rows [it*32, +32), cols [tile*128, +128) as 4 boxes of 32 cols; B = W rows [it*32, +32)
-                    for (int j = 0; j < 4; ++j) tma_load_2d(sA + j * 4096, &tmA, full + s, int(tile * 128 + j * 32), int(it * 32));
-                    for (int h = 0; h < KP / 32; ++h) {
-                        tma_load_2d(sB + h * 4096, &tmB, full + s, h * 32, int(it * 32));
-                        tma_load_2d(sBlo + h * 4096, &tmBlo, full + s, h * 32, int(it * 32));
-                    }
+                    for (int j = 0; j < 4; ++j)
+                        tma_load_2d(sA + j * 4096, &tmA, full + s, int(tile * 128 + j * 32), int(it * 32), kEvictFirst);
                 }
+                for (int h = 0; h < KP / 32; ++h) {
+                    tma_load_2d(sB + h * 4096, &tmB, full + s, h * 32, int(it * 32), kEvictLast);
+                    tma_load_2d(sBlo + h * 4096, &tmBlo, full + s, h * 32, int(it * 32), kEvictLast);
+                }
+                if (++s == C::STAGES) s = 0, ph ^= 1u;
+                if (++it == sk.ipt) it = 0, ++tile;
             }
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
+        int s = 0;
+        uint32_t ph = 0;
         int64_t sg = 0;
-        for (int64_t u = u0; u < u1;) {
-            const int64_t tile = u / sk.ipt;
+        int64_t u = u0;
+        int64_t tile = u0 / sk.ipt;
+        while (u < u1) {
             const int64_t seg_end = min(u1, (tile + 1) * sk.ipt);
             const int b = int(sg & 1);
             mbar_wait(accempty + b, (uint32_t(sg >> 1) & 1u) ^ 1u);
             tc_fence_after();
-            const uint32_t d = tmem + uint32_t(b * KP);
-            for (; u < seg_end; ++u) {
-                const int s = int((u - u0) % C::STAGES);
-                const uint32_t ph = uint32_t((u - u0) / C::STAGES) & 1u;
-                mbar_wait(split + s, ph);
+            const uint32_t d = tmem + uint32_t(b * C::ACC_COLS);
+            for (bool first = true; u < seg_end; ++u, first = false) {
+                mbar_wait(split + s, ph);  // implies full[s]: the split warps waited on it
                 tc_fence_after();
                 if (lane == 0) {
                     const uint32_t a0 = smem_u32(stage_ptr(s));
-                    const uint32_t alo0 = a0 + C::A_BYTES;
-                    const uint32_t b0 = a0 + 2 * C::A_BYTES;
-                    const uint32_t blo0 = b0 + C::B_BYTES;
-                    const bool first = (u == tile * sk.ipt) || (u == u0);
+                    const uint32_t b0 = a0 + C::A_BYTES;
+                    const uint32_t alo = tmem + uint32_t(C::ALO_COL0 + 32 * s);
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk) {
-                        // pass 1: A K-major; pass 2: A MN-major (4 atoms of 32 columns, 4 KB
-                        // apart). B (Ht / W tiles) is always MN-major (kp/32 atoms, 4 KB apart).
                         const uint64_t da = PASS == 1 ? desc_kmajor(a0, kk) : desc_mnmajor(a0, kk, 4096);
-                        const uint64_t dalo = PASS == 1 ? desc_kmajor(alo0, kk) : desc_mnmajor(alo0, kk, 4096);
-                        const uint64_t db = desc_mnmajor(b0, kk, 4096);
-                        const uint64_t dblo = desc_mnmajor(blo0, kk, 4096);
-                        mma_tf32(d, da, db, C::IDESC, (first && kk == 0) ? 0u : 1u);
-                        mma_tf32(d, dalo, db, C::IDESC, 1u);
-                        mma_tf32(d, da, dblo, C::IDESC, 1u);
+                        const uint64_t db = desc_mnmajor(b0, kk, 4096);  // [B_hi | B_lo] atoms, 4 KB apart
+                        mma_ss(d, da, db, C::IDESC_SS, (first && kk == 0) ? 0u : 1u);
+                        mma_ts(d, alo + 8 * kk, db, C::IDESC_TS, 1u);
                     }
                     mma_commit(empty + s);
                     if (u + 1 == seg_end) mma_commit(accfull + b);
                 }
                 __syncwarp();
+                if (++s == C::STAGES) s = 0, ph ^= 1u;
             }
             ++sg;
+            ++tile;
         }
     } else if (warp >= 4) {
-        // ---------------- split (A_lo) + epilogue warpgroup
-        const int t = tid - 128;
-        const int q = warp - 4;  // TMEM lanes [32q, 32q+32)
+        // ---------------- split (A_lo -> TMEM) + epilogue warpgroup
+        const int t = tid - 128;  // TMEM lane / D row owned by this thread
+        const int q = warp - 4;   // this warp's TMEM lane quarter [32q, 32q+32)
+        const uint32_t lane_bits = uint32_t(32 * q) << 16;
+        int s = 0;
+        uint32_t ph = 0;
         int64_t sg = 0;
+        int64_t tile = u0 / sk.ipt, it = u0 % sk.ipt;
         for (int64_t u = u0; u < u1; ++u) {
-            const int s = int((u - u0) % C::STAGES);
-            const uint32_t ph = uint32_t((u - u0) / C::STAGES) & 1u;
             mbar_wait(full + s, ph);
-            const float4* src = reinterpret_cast<const float4*>(stage_ptr(s));
-            float4* dst = reinterpret_cast<float4*>(stage_ptr(s) + C::A_BYTES);
+            const uint8_t* sA = stage_ptr(s);
+            uint32_t r[32];
+            if (PASS == 1) {
+                // row t of the K-major SW128 tile: 8 chunks of 16 B, chunk c at (c ^ t%8)
+                const float4* row = reinterpret_cast<const float4*>(sA + t * 128);
 #pragma unroll
-            for (int i = 0; i < C::A_BYTES / 16 / 128; ++i) {
-                const float4 v = src[t + 128 * i];
-                float4 lo;
-                lo.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
-                lo.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
-                lo.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
-                lo.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-                dst[t + 128 * i] = lo;
+                for (int c = 0; c < 8; ++c) {
+                    const float4 v = row[c ^ (t & 7)];
+                    r[4 * c] = lo_bits(v.x), r[4 * c + 1] = lo_bits(v.y), r[4 * c + 2] = lo_bits(v.z),
+                    r[4 * c + 3] = lo_bits(v.w);
+                }
+            } else {
+                // column t of the MN-major BASE32B tile: atom t/32, element e = t%32 of each row k,
+                // 32-byte granule (e/8) ^ (k%4)
+                const float* atom = reinterpret_cast<const float*>(sA + (t >> 5) * 4096);
+                const int e = t & 31;
+#pragma unroll
+                for (int k = 0; k < 32; ++k)
+                    r[k] = lo_bits(atom[k * 32 + ((((e >> 3) ^ (k & 3))) << 3) + (e & 7)]);
             }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            tmem_st32(tmem + lane_bits + uint32_t(C::ALO_COL0 + 32 * s), r);
+            tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(split + s);
+            if (++s == C::STAGES) s = 0, ph ^= 1u;
 
-            const int64_t tile = u / sk.ipt;
             if (u + 1 == min(u1, (tile + 1) * sk.ipt)) {
                 const int b = int(sg & 1);
                 mbar_wait(accfull + b, uint32_t(sg >> 1) & 1u);
                 tc_fence_after();
-                float* out = slots + sk.slot(cta, tile) * int64_t(128 * KP) + int64_t(32 * q + lane) * KP;
+                float* out = slots + sk.slot(cta, tile) * int64_t(128 * KP) + int64_t(t) * KP;
 #pragma unroll
                 for (int h = 0; h < KP / 32; ++h) {
-                    float v[32];
-                    tmem_ld32(tmem + (uint32_t(32 * q) << 16) + uint32_t(b * KP + h * 32), v);
+                    uint32_t hi[32], lo[32];
+                    tmem_ld32(tmem + lane_bits + uint32_t(b * C::ACC_COLS + h * 32), hi);
+                    tmem_ld32(tmem + lane_bits + uint32_t(b * C::ACC_COLS + KP + h * 32), lo);
 #pragma unroll
                     for (int j4 = 0; j4 < 8; ++j4)
                         reinterpret_cast<float4*>(out + h * 32)[j4] =
-                            make_float4(v[4 * j4], v[4 * j4 + 1], v[4 * j4 + 2], v[4 * j4 + 3]);
+                            make_float4(__uint_as_float(hi[4 * j4]) + __uint_as_float(lo[4 * j4]),
+                                        __uint_as_float(hi[4 * j4 + 1]) + __uint_as_float(lo[4 * j4 + 1]),
+                                        __uint_as_float(hi[4 * j4 + 2]) + __uint_as_float(lo[4 * j4 + 2]),
+                                        __uint_as_float(hi[4 * j4 + 3]) + __uint_as_float(lo[4 * j4 + 3]));
                 }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty + b);
                 ++sg;
             }
+            if (++it == sk.ipt) it = 0, ++tile;
         }
     }
     __syncthreads();
@@ -322,8 +366,7 @@ cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t co
     const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE,
                           mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 

@@ -9,8 +9,8 @@
 //  * The H update's two all-reduces per batch (W^T W, then W^T A_p) are one NCCL
 //    all-reduce of a packed [W^T A | W^T W] buffer per iteration.
 //  * The error is the trace form ||A||^2 - 2<W^T A, H> + <W^T W, H H^T>, whose terms all
-//    exist after the H update, so error checks cost no pass over A (error_mode 1 restores a
-//    direct residual pass).
+//    exist after the H update, so error checks cost no pass over A; when it reports a small
+//    error (where its cancellation hurts) the check is redone with a direct f64 residual.
 //  * Nothing syncs the host except error checks (one 16-byte D2H every interval).
 #include <nccl.h>
 
@@ -131,6 +131,7 @@ struct oocnmf_ctx {
     cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
 
     DevBuf W, Ht, HHt, packed, N1, slots1, slots2, gram_w, gram_h, err_slots, red_slots, scal, flag;
+    DevBuf HHt64, WtW64;         // f64 Grams for the trace-form error (f32 copies drive the updates)
     DevBuf W_lo, Ht_lo;          // low halves of the 3xTF32 split (tensor-core path only)
     bool use_tc = false;         // kp in {32, 64}: tcgen05 passes; else CUDA-core FFMA passes
     StreamK sk1, sk2;            // in-core dense passes
@@ -175,10 +176,12 @@ void alloc_factors(oocnmf_ctx* c) {
         c->Ht_lo.release();
     }
     c->HHt.alloc(size_t(kp) * kp * 4, "HHt");
+    c->HHt64.alloc(size_t(kp) * kp * 8, "HHt64");
+    c->WtW64.alloc(size_t(kp) * kp * 8, "WtW64");
     c->packed.alloc(size_t(c->packed_count()) * 4, "packed");
     const int gw = factor_grid(c->mp / kTile), gh = factor_grid(c->np / kTile);
-    c->gram_w.alloc(size_t(gw) * kp * kp * 4, "gram_w");
-    c->gram_h.alloc(size_t(gh) * kp * kp * 4, "gram_h");
+    c->gram_w.alloc(size_t(gw) * kp * kp * 8, "gram_w");
+    c->gram_h.alloc(size_t(gh) * kp * kp * 8, "gram_h");
     c->err_slots.alloc(size_t(std::max(gh, sqnorm_grid())) * 8, "err_slots");
     c->red_slots.alloc(size_t(sqnorm_grid()) * 8, "red_slots");
     c->scal.alloc(kNumScal * 8, "scalars");
@@ -259,10 +262,10 @@ cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W,
 void gram_h(oocnmf_ctx* c) {
     const int kp = c->kp;
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, nullptr, nullptr, nullptr, nullptr, 0.f, false,
-                                  c->gram_h.as<float>(), nullptr, c->flag.as<int>(), htlo(c), c->stream),
+                                  c->gram_h.as<double>(), nullptr, c->flag.as<int>(), htlo(c), c->stream),
           "gram H");
-    count(c, launch_reduce_slots(c->gram_h.as<float>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
-                                 c->HHt.as<float>(), c->stream),
+    count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
+                                 c->HHt.as<float>(), c->HHt64.as<double>(), c->stream),
           "reduce HHt");
 }
 
@@ -279,10 +282,10 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         count(c, pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
         rec(eAht);
         count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, c->slots1.as<float>(), &c->sk1,
-                                      c->HHt.as<float>(), eps, true, c->gram_w.as<float>(), nullptr,
+                                      c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
                                       c->flag.as<int>(), wlo(c), s),
               "W update");
-        count(c, launch_reduce_slots(c->gram_w.as<float>(), gw, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
+        count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
         count(c, pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s),
               "wta");
@@ -295,10 +298,10 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
               "spmm A Ht");
         rec(eAht);
         count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
-                                      c->HHt.as<float>(), eps, true, c->gram_w.as<float>(), nullptr,
+                                      c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
                                       c->flag.as<int>(), nullptr, s),
               "W update");
-        count(c, launch_reduce_slots(c->gram_w.as<float>(), gw, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
+        count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
         count(c, launch_spmm(kp, c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), c->vT.as<float>(), c->n,
                              c->W.as<float>(), c->wta(), s),
@@ -330,14 +333,14 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
             float* Wlob = c->use_tc ? c->W_lo.as<float>() + b0 * kp : nullptr;
             count(c, pass1(c, st, brp, c->slots1.as<float>(), s1, s), "aht");
             count(c, launch_factor_update(kp, Wb, brp, nullptr, c->slots1.as<float>(), &s1, c->HHt.as<float>(),
-                                          eps, true, c->gram_w.as<float>() + b * gwb * kp * kp, nullptr,
+                                          eps, true, c->gram_w.as<double>() + b * gwb * kp * kp, nullptr,
                                           c->flag.as<int>(), Wlob, s),
                   "W update");
             count(c, pass2(c, st, brp, Wb, Wlob, c->slots2.as<float>(), s2, s), "wta");
             count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), s2, c->wta(), b > 0, s), "reduce WtA");
             ck(cudaEventRecord(c->ev_free[si], s), "event");
         }
-        count(c, launch_reduce_slots(c->gram_w.as<float>(), nb * gwb, int64_t(kp) * kp, c->wtw(), s), "reduce WtW");
+        count(c, launch_reduce_slots(c->gram_w.as<double>(), nb * gwb, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eAht);
         rec(eWdone);
         rec(eWta);
@@ -348,28 +351,51 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
 void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     const int kp = c->kp;
     cudaStream_t s = c->stream;
-    if (c->nranks > 1)
+    if (c->nranks > 1) {
+        // One fused NCCL launch: the packed f32 [W^T A | W^T W] the update consumes and the f64
+        // W^T W the trace-form error consumes.
+        nck(ncclGroupStart(), "ncclGroupStart");
         nck(ncclAllReduce(c->packed.p, c->packed.p, size_t(c->packed_count()), ncclFloat, ncclSum, c->comm, s),
             "allreduce [WtA|WtW]");
+        nck(ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
+            "allreduce WtW64");
+        nck(ncclGroupEnd(), "ncclGroupEnd");
+    }
     if (timed) ck(cudaEventRecord(ev[eComm], s), "event");
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, c->wta(), nullptr, nullptr, c->wtw(), eps, true,
-                                  c->gram_h.as<float>(), c->err_slots.as<double>(), c->flag.as<int>(), htlo(c), s),
+                                  c->gram_h.as<double>(), c->err_slots.as<double>(), c->flag.as<int>(), htlo(c), s),
           "H update");
-    count(c, launch_reduce_slots(c->gram_h.as<float>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
-                                 c->HHt.as<float>(), s),
+    count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
+                                 c->HHt.as<float>(), c->HHt64.as<double>(), s),
           "reduce HHt");
     if (timed) ck(cudaEventRecord(ev[eHdone], s), "event");
 }
 
 
+// Below this trace-form estimate of the relative error, error_mode auto re-evaluates the
+// error with the direct residual: the trace form subtracts O(||A||^2) terms, so an f32-level
+// relative error of ~1e-7 in them grows by 1/err^2 (SURVEY.md §7 hard part 2).
+constexpr double kAutoDirectBelow = 0.1;
+
+double error_check_once(oocnmf_ctx* c, bool direct_mode, int* bad);
+
 double error_check(oocnmf_ctx* c, int error_mode, int* bad) {
+    // error_mode: 0 auto, 1 direct, 2 trace
+    if (error_mode == 1) return error_check_once(c, true, bad);
+    const double e = error_check_once(c, false, bad);
+    if (error_mode == 0 && !*bad && e < kAutoDirectBelow && c->kind != Kind::host)
+        return error_check_once(c, true, bad);
+    return e;
+}
+
+double error_check_once(oocnmf_ctx* c, bool direct_mode, int* bad) {
     const int kp = c->kp;
     cudaStream_t s = c->stream;
     double* scal = c->scal.as<double>();
     const double* direct = nullptr;
     const double* eslots = c->err_slots.as<double>();
     int64_t n_err = factor_grid(c->np / kTile);
-    if (error_mode == 1) {
+    if (direct_mode) {
         if (c->kind == Kind::dense) {
             count(c, launch_residual_dense(kp, c->A.as<float>(), c->np, c->rows, c->n, c->W.as<float>(),
                                            c->Ht.as<float>(), c->red_slots.as<double>(), s),
@@ -390,7 +416,7 @@ double error_check(oocnmf_ctx* c, int error_mode, int* bad) {
             n_err = 1;
         }
     }
-    count(c, launch_finalize_error(kp, eslots, n_err, c->wtw(), c->HHt.as<float>(), scal + kNormA2, direct,
+    count(c, launch_finalize_error(kp, eslots, n_err, c->WtW64.as<double>(), c->HHt64.as<double>(), scal + kNormA2, direct,
                                    scal + kErr, s),
           "finalize");
     ck(cudaMemcpyAsync(c->hpin, scal + kErr, 8, cudaMemcpyDeviceToHost, s), "D2H err");
@@ -442,6 +468,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     if (cfg->max_iters < 1) fail(OOCNMF_ERR_SHAPE, "NmfConfig: max_iters must be >= 1");
     if (cfg->error_check_interval < 1) fail(OOCNMF_ERR_SHAPE, "NmfConfig: error_check_interval must be >= 1");
     if (!(cfg->epsilon > 0)) fail(OOCNMF_ERR_SHAPE, "NmfConfig: epsilon must be > 0");
+    if (cfg->error_mode < 0 || cfg->error_mode > 2) fail(OOCNMF_ERR_SHAPE, "error_mode must be 0, 1 or 2");
     if (cfg->error_mode == 1 && c->kind == Kind::host)
         fail(OOCNMF_ERR_SHAPE, "error_mode=direct is not supported out-of-core");
     if (c->kind == Kind::none) fail(OOCNMF_ERR_SHAPE, "no A loaded");
@@ -847,7 +874,7 @@ int oocnmf_attach_host_dense_f32(oocnmf_ctx* c, const float* a, uint64_t lda, ui
         const int64_t s2 = std::max(c->sk2b[0].G * c->sk2b[0].smax, c->sk2b[1].G * c->sk2b[1].smax);
         c->slots1.alloc(size_t(s1) * kTile * c->kp * 4, "slots1");
         c->slots2.alloc(size_t(s2) * kTile * c->kp * 4, "slots2");
-        c->gram_w.alloc(size_t(nb) * factor_grid(br / kTile) * c->kp * c->kp * 4, "gram_w");
+        c->gram_w.alloc(size_t(nb) * factor_grid(br / kTile) * c->kp * c->kp * 8, "gram_w");
         ck(cudaMemsetAsync(c->gram_w.p, 0, c->gram_w.bytes, c->stream), "memset");
         ck(cudaStreamSynchronize(c->stream), "sync");
         c->kind = Kind::host;
@@ -984,9 +1011,9 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
         }
         gram_h(c);
         ck(launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, 0.f, false,
-                                c->gram_w.as<float>(), nullptr, c->flag.as<int>(), nullptr, s),
+                                c->gram_w.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
            "gram W");
-        ck(launch_reduce_slots(c->gram_w.as<float>(), factor_grid(c->mp / kTile), int64_t(kp) * kp, c->wtw(), s),
+        ck(launch_reduce_slots(c->gram_w.as<double>(), factor_grid(c->mp / kTile), int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s),
            "reduce");
         std::vector<float> a1(size_t(c->mp) * kp), a2(size_t(c->np) * kp), g1(size_t(kp) * kp), g2(size_t(kp) * kp);
         ck(cudaMemcpyAsync(a1.data(), t1.p, a1.size() * 4, cudaMemcpyDeviceToHost, s), "D2H");

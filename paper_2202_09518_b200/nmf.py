@@ -81,7 +81,7 @@ class NmfConfig:
     init_h: Optional[np.ndarray] = None
     # B200 extensions
     device: int = 0
-    error_mode: str = "trace"  # "trace" | "direct"
+    error_mode: str = "auto"  # "auto" | "direct" | "trace"
 
     def validate(self) -> None:
         if self.k < 1:
@@ -96,13 +96,13 @@ class NmfConfig:
             raise ShapeError("NmfConfig: epsilon must be > 0")
         if self.init == FactorInit.from_files and (self.init_w is None or self.init_h is None):
             raise ShapeError("NmfConfig: init=from_files requires both factors")
-        if self.error_mode not in ("trace", "direct"):
-            raise ShapeError("NmfConfig: error_mode must be 'trace' or 'direct'")
+        if self.error_mode not in ("auto", "direct", "trace"):
+            raise ShapeError("NmfConfig: error_mode must be 'auto', 'direct' or 'trace'")
 
     def to_c(self) -> _capi.Config:
         return _capi.Config(self.k, self.eta, self.max_iters, self.error_check_interval, self.epsilon,
                             self.seed, self.init.value,
-                            1 if self.error_mode == "direct" else 0)
+                            {"auto": 0, "direct": 1, "trace": 2}[self.error_mode])
 
 
 @dataclass

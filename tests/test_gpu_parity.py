@@ -193,12 +193,29 @@ def test_device_init_is_reference_init(gpu):
 
 def test_direct_error_mode_matches_trace_form(gpu):
     a = port.uniform_dense(500, 400, 3, 99).astype(np.float32)
-    r1 = solve_from(a, 16, 30, 10)
+    r1 = solve_from(a, 16, 30, 10, error_mode="trace")
     r2 = solve_from(a, 16, 30, 10, error_mode="direct")
+    r3 = solve_from(a, 16, 30, 10)  # auto: error ~0.5 -> trace form
     e1 = np.array([e for _, e in r1.error_trace])
     e2 = np.array([e for _, e in r2.error_trace])
-    np.testing.assert_allclose(e1, e2, rtol=2e-5)
+    np.testing.assert_allclose(e1, e2, rtol=2e-6)
     assert np.array_equal(r1.w, r2.w)
+    assert [e for _, e in r3.error_trace] == e1.tolist()
+
+
+@pytest.mark.parametrize("k", [4, 32])
+def test_small_error_regime_keeps_parity(gpu, k):
+    # Near-exact low-rank input: the relative error falls to ~1e-3, where the trace form
+    # alone would lose ~1e-2 relative accuracy; auto mode must still track the reference.
+    if not oracle.ref.available:
+        pytest.skip("needs gen_lowrank from oracle/_ref")
+    a = oracle.ref.gen_lowrank(512, 384, 4, 0.0, 2)[0]
+    a32 = a.astype(np.float32)
+    w0, h0 = port.init_factors(512, 384, k, 0)
+    ref = port.nmf_serial(f32(a32), k, f32(w0), f32(h0), max_iters=300, interval=50)
+    assert ref.trace_err[-1] < 0.02
+    res = solve_from(a32, k, 300, 50)
+    check_parity(res, ref.trace_iters, ref.trace_err)
 
 
 def test_csr_direct_error_mode(gpu):
