@@ -11,37 +11,40 @@ namespace ooc {
 // Device layout (per rank): A slab mp x np f32 row-major (zero-padded to multiples of
 // 128), W mp x kp, Ht np x kp (H stored transposed so both factors are "tall"), kp in
 // {8, 16, 32, 64} (k zero-padded; padding is exact for MU: padded entries stay 0).
+// The tensor-core path also keeps W_cat / Ht_cat (rows x 2kp) = [F | F - tf32(F)].
 constexpr int kTile = 128;  // rows (pass 1, W update) / columns (pass 2, H update) per tile
 
-// ---- dense streaming passes (kernels_dense.cu) ----
-// Pass 1: slots <- partial (A · Ht) per stream-K segment; tiles of 128 rows, steps of 32 cols.
-void plan_aht(StreamK& sk, int64_t mp, int64_t np, int num_sms);
+// ---- dense streaming passes ----
+// Stream-K plans: tiles of 128 rows (pass 1) / 128 columns (pass 2), reduction steps of
+// `step` columns / rows (32 for the FFMA kernels, kTcStep for the tensor-core kernels).
+constexpr int kFfmaStep = 32, kTcStep = 64;
+void plan_aht(StreamK& sk, int64_t mp, int64_t np, int num_sms, int step);
+void plan_wta(StreamK& sk, int64_t mp, int64_t np, int num_sms, int step);
+// CUDA-core (FFMA) passes, kernels_dense.cu: any kp.
 cudaError_t launch_aht(int kp, const float* A, int64_t lda, const float* Ht, float* slots,
                        const StreamK& sk, cudaStream_t s);
-// Pass 2: slots <- partial (A^T · W) per segment; tiles of 128 cols, steps of 32 rows.
-void plan_wta(StreamK& sk, int64_t mp, int64_t np, int num_sms);
 cudaError_t launch_wta(int kp, const float* A, int64_t lda, const float* W, float* slots,
                        const StreamK& sk, cudaStream_t s);
-
-// ---- tensor-core passes (kernels_tc.cu): kp in {32, 64}, 3xTF32 split precision ----
+// Tensor-core passes, kernels_tc.cu: kp in {32, 64}, 3xTF32 split precision; the factor
+// operand is its [F | F_lo] concatenation (rows x 2kp).
 bool tc_supported(int kp);
-cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* Ht,
-                          const float* Ht_lo, float* slots, const StreamK& sk, cudaStream_t s);
-cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* W,
-                          const float* W_lo, float* slots, const StreamK& sk, cudaStream_t s);
+cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np,
+                          const float* Ht_cat, float* slots, const StreamK& sk, cudaStream_t s);
+cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np,
+                          const float* W_cat, float* slots, const StreamK& sk, cudaStream_t s);
 
 // ---- factor kernels (kernels_factor.cu) ----
 // F (rows x kp, rows a multiple of 128) <- F * N / (F G + eps) rowwise, where N is either
 // a plain rows x kp matrix (n_plain) or stream-K partials (n_slots, sk). Emits per-CTA
-// partial Gram F_new^T F_new (gram_slots[gridDim][kp*kp]), per-CTA f64 partial
+// partial Gram F_new^T F_new in f64 (gram_slots[gridDim][kp*kp]), per-CTA f64 partial
 // sum(N .* F_new) (err_slots, may be null) and sets *flag on non-finite output.
-// update == false: only emit the Gram of F (no update). lo_out (may be null) receives
-// F - tf32(F) of the resulting rows (the low half of the 3xTF32 split).
+// update == false: only emit the Gram of F (no update). cat_out (may be null) receives the
+// rows of [F | F - tf32(F)] (rows x 2kp) for the tensor-core passes.
 int factor_grid(int64_t tiles);
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
                                  const float* n_slots, const StreamK* sk, const float* G,
                                  float eps, bool update, double* gram_slots, double* err_slots,
-                                 int* flag, float* lo_out, cudaStream_t s);
+                                 int* flag, float* cat_out, cudaStream_t s);
 // out[e] = sum_s slots[s*E + e] in f64 (fixed order), E = count; written as f32 (out32) and,
 // if out64 != null, f64.
 cudaError_t launch_reduce_slots(const double* slots, int64_t nslots, int64_t count, float* out32,
@@ -63,7 +66,7 @@ cudaError_t launch_init_factors(float* W, float* Ht, int kp, int64_t k, int64_t 
                                 int64_t row0, int64_t n, uint64_t seed, cudaStream_t s);
 cudaError_t launch_cast_pad_f64(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
                                 float* dst, int64_t ld_dst, cudaStream_t s);
-// Partial f64 sums of squares of A (dense, padded) -> out_slots[gridDim]; returns grid.
+// Partial f64 sums of squares of A (dense, padded) -> out_slots[sqnorm_grid()].
 int sqnorm_grid();
 cudaError_t launch_sq_norm_dense(const float* A, int64_t lda, int64_t rows, int64_t cols,
                                  double* out_slots, cudaStream_t s);
@@ -74,8 +77,8 @@ cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t r
                                   int64_t cols, const float* W, const float* Ht,
                                   double* out_slots, cudaStream_t s);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s);
-// lo[i] = x[i] - tf32_trunc(x[i])
-cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s);
+// cat (rows x 2kp) <- [F | F - tf32_trunc(F)] for F (rows x kp)
+cudaError_t launch_split_cat(const float* F, float* cat, int64_t rows, int kp, cudaStream_t s);
 
 // ---- CSR kernels (kernels_sparse.cu) ----
 // out (rows x kp) = CSR(rp, ci, v) · B (B rows indexed by column, kp wide).

@@ -299,11 +299,11 @@ cudaError_t launch_sk(K kernel, size_t smem, const StreamK& sk, cudaStream_t s, 
 
 }  // namespace
 
-void plan_aht(StreamK& sk, int64_t mp, int64_t np, int num_sms) {
-    sk.plan(mp / kTile, np / 32, num_sms);
+void plan_aht(StreamK& sk, int64_t mp, int64_t np, int num_sms, int step) {
+    sk.plan(mp / kTile, np / step, num_sms);
 }
-void plan_wta(StreamK& sk, int64_t mp, int64_t np, int num_sms) {
-    sk.plan(np / kTile, mp / 32, num_sms);
+void plan_wta(StreamK& sk, int64_t mp, int64_t np, int num_sms, int step) {
+    sk.plan(np / kTile, mp / step, num_sms);
 }
 
 cudaError_t launch_aht(int kp, const float* A, int64_t lda, const float* Ht, float* slots,

@@ -33,7 +33,7 @@ __global__ void __launch_bounds__(kFuThreads)
     k_factor_update(float* __restrict__ F, int64_t tiles, const float* __restrict__ n_plain,
                     const float* __restrict__ n_slots, StreamK sk, const float* __restrict__ G,
                     float eps, int update, double* __restrict__ gram_slots,
-                    double* __restrict__ err_slots, int* __restrict__ flag, float* __restrict__ lo_out) {
+                    double* __restrict__ err_slots, int* __restrict__ flag, float* __restrict__ cat_out) {
     constexpr int FS = KP + 1;
     extern __shared__ __align__(16) unsigned char fu_smem[];
     double* red = reinterpret_cast<double*>(fu_smem);
@@ -109,8 +109,9 @@ __global__ void __launch_bounds__(kFuThreads)
             for (int j4 = 0; j4 < KP / 4; ++j4)
                 fw[j4] = make_float4(f[4 * j4], f[4 * j4 + 1], f[4 * j4 + 2], f[4 * j4 + 3]);
         }
-        if (lo_out) {
-            float4* lw = reinterpret_cast<float4*>(lo_out + row * KP);
+        if (cat_out) {
+            // [F | F - tf32(F)] row of the tensor-core operand (one TMA box carries both halves)
+            float4* cw = reinterpret_cast<float4*>(cat_out + row * 2 * KP);
 #pragma unroll
             for (int j4 = 0; j4 < KP / 4; ++j4) {
                 float l[4];
@@ -119,7 +120,8 @@ __global__ void __launch_bounds__(kFuThreads)
                     const float x = f[4 * j4 + q];
                     l[q] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
                 }
-                lw[j4] = make_float4(l[0], l[1], l[2], l[3]);
+                cw[j4] = make_float4(f[4 * j4], f[4 * j4 + 1], f[4 * j4 + 2], f[4 * j4 + 3]);
+                cw[KP / 4 + j4] = make_float4(l[0], l[1], l[2], l[3]);
             }
         }
         // Gram partial of this tile: entries (i <= j), ascending rows.
@@ -220,7 +222,7 @@ int factor_grid(int64_t tiles) { return int(tiles < 1184 ? tiles : 1184); }
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
                                  const float* n_slots, const StreamK* sk, const float* G,
                                  float eps, bool update, double* gram_slots, double* err_slots,
-                                 int* flag, float* lo_out, cudaStream_t s) {
+                                 int* flag, float* cat_out, cudaStream_t s) {
     const int64_t tiles = rows / kTile;
     const int grid = factor_grid(tiles);
     StreamK skv = sk ? *sk : StreamK{};
@@ -233,7 +235,7 @@ cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_
         if (e != cudaSuccess) return e;                                                        \
         k_factor_update<K><<<grid, kFuThreads, smem, s>>>(F, tiles, n_plain, n_slots, skv, G,  \
                                                          eps, update ? 1 : 0, gram_slots,      \
-                                                         err_slots, flag, lo_out);             \
+                                                         err_slots, flag, cat_out);            \
         break;                                                                                 \
     }
     switch (kp) {

@@ -143,10 +143,13 @@ __global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag
     if (bad) atomicOr(flag, 1);
 }
 
-__global__ void k_split_lo(const float* __restrict__ x, float* __restrict__ lo, int64_t n) {
+__global__ void k_split_cat(const float* __restrict__ F, float* __restrict__ cat, int64_t rows, int kp) {
+    const int64_t n = rows * kp;
     for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
-        const float v = x[q];
-        lo[q] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        const int64_t r = q / kp, j = q % kp;
+        const float v = F[q];
+        cat[r * 2 * kp + j] = v;
+        cat[r * 2 * kp + kp + j] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
     }
 }
 
@@ -212,8 +215,8 @@ cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream
     return cudaGetLastError();
 }
 
-cudaError_t launch_split_lo(const float* x, float* lo, int64_t n, cudaStream_t s) {
-    k_split_lo<<<grid_for(n, 8), 256, 0, s>>>(x, lo, n);
+cudaError_t launch_split_cat(const float* F, float* cat, int64_t rows, int kp, cudaStream_t s) {
+    k_split_cat<<<grid_for(rows * kp, 8), 256, 0, s>>>(F, cat, rows, kp);
     return cudaGetLastError();
 }
 

@@ -60,12 +60,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
 }
 // L2 eviction policies (the encodings CUTLASS uses for TMA cache hints).
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull, kEvictLast = 0x14F0000000000000ull;
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y,
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z,
                                             uint64_t policy) {
     asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-        " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "l"(policy)
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
         : "memory");
 }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -146,25 +146,31 @@ __device__ __forceinline__ uint32_t lo_bits(float x) {
 }
 
 // ------------------------------------------------------------------ kernel
+// One pipeline stage covers kTcStep (= 64) K indices: 64 columns of A (pass 1) or 64 rows
+// (pass 2). Every stage arrives in two TMA operations (A tile, [B_hi | B_lo] tile) — TMA
+// operations, not bytes, bound a single-issuer ring with small boxes (tools/tma_stream_bench.cu).
 template <int KP, int PASS>
 struct TcCfg {
-    static constexpr int STAGES = KP == 32 ? 6 : 5;
-    static constexpr int A_BYTES = 128 * 32 * 4;              // 16 KB: 128 x 32 f32 per stage
-    static constexpr int B_BYTES = 32 * KP * 4;                // 32 (K) x kp f32
-    static constexpr int STAGE_BYTES = A_BYTES + 2 * B_BYTES;  // A, B_hi, B_lo (B_lo right after B_hi)
-    static constexpr uint32_t TX_BYTES = STAGE_BYTES;          // everything arrives by TMA
-    static constexpr int ACC_COLS = 2 * KP;                    // D' = [hi | lo] columns per buffer
-    static constexpr int ALO_COL0 = 2 * ACC_COLS;              // A_lo slots after 2 accumulators
-    static constexpr int TMEM_COLS = (ALO_COL0 + STAGES * 32) <= 256 ? 256 : 512;
+    static constexpr int BK = kTcStep;                          // K per stage
+    static constexpr int KSTEPS = BK / 8;                       // tf32 MMA K = 8
+    static constexpr int A_BYTES = 128 * BK * 4;                // 32 KB
+    static constexpr int B_BYTES = BK * 2 * KP * 4;             // [B_hi | B_lo], 16 / 32 KB
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int STAGES = KP == 32 ? 4 : 3;
+    static constexpr uint32_t TX_BYTES = STAGE_BYTES;
+    static constexpr uint32_t ATOM_STRIDE = BK * 128;           // MN-major atoms: BK rows x 128 B
+    static constexpr int ACC_COLS = 2 * KP;                     // D' = [hi | lo] per accumulator
+    static constexpr int ALO_COL0 = 2 * ACC_COLS;               // A_lo slots after 2 accumulators
+    static constexpr int TMEM_COLS = (ALO_COL0 + STAGES * BK) <= 256 ? 256 : 512;
     static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
     static constexpr uint32_t IDESC_SS = idesc_tf32(2 * KP, PASS == 2 ? 1 : 0, 1);  // A_hi · [B_hi|B_lo]
-    static constexpr uint32_t IDESC_TS = idesc_tf32(KP, 0, 1);                       // A_lo(TMEM, K-major) · B_hi
+    static constexpr uint32_t IDESC_TS = idesc_tf32(KP, 0, 1);                       // A_lo(TMEM) · B_hi
 };
 
 template <int KP, int PASS>
 __global__ void __launch_bounds__(256, 1)
     k_pass_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              const __grid_constant__ CUtensorMap tmBlo, float* __restrict__ slots, StreamK sk) {
+              float* __restrict__ slots, StreamK sk) {
     using C = TcCfg<KP, PASS>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -214,21 +220,13 @@ __global__ void __launch_bounds__(256, 1)
             for (int64_t u = u0; u < u1; ++u) {
                 mbar_wait(empty + s, ph ^ 1u);
                 uint8_t* sA = stage_ptr(s);
-                uint8_t* sB = sA + C::A_BYTES;
-                uint8_t* sBlo = sB + C::B_BYTES;
                 mbar_expect_tx(full + s, C::TX_BYTES);
-                if (PASS == 1) {
-                    // A rows [tile*128, +128), cols [it*32, +32); B = Ht rows [it*32, +32)
-                    tma_load_2d(sA, &tmA, full + s, int(it * 32), int(tile * 128), kEvictFirst);
-                } else {
-                    // A rows [it*32, +32), cols [tile*128, +128) as 4 boxes of 32 cols; B = W rows [it*32, +32)
-                    for (int j = 0; j < 4; ++j)
-                        tma_load_2d(sA + j * 4096, &tmA, full + s, int(tile * 128 + j * 32), int(it * 32), kEvictFirst);
-                }
-                for (int h = 0; h < KP / 32; ++h) {
-                    tma_load_2d(sB + h * 4096, &tmB, full + s, h * 32, int(it * 32), kEvictLast);
-                    tma_load_2d(sBlo + h * 4096, &tmBlo, full + s, h * 32, int(it * 32), kEvictLast);
-                }
+                if (PASS == 1)  // rows [tile*128, +128), K-atoms [2 it, 2 it + 2): atom j -> +16 KB
+                    tma_load_3d(sA, &tmA, full + s, 0, int(tile * 128), int(it * (C::BK / 32)), kEvictFirst);
+                else            // rows [it*64, +64), column atoms [4 tile, +4): atom j -> +8 KB
+                    tma_load_3d(sA, &tmA, full + s, 0, int(it * C::BK), int(tile * 4), kEvictFirst);
+                // factor rows [it*64, +64) of [F | F_lo]: 2kp/32 atoms of 8 KB
+                tma_load_3d(sA + C::A_BYTES, &tmB, full + s, 0, int(it * C::BK), 0, kEvictLast);
                 if (++s == C::STAGES) s = 0, ph ^= 1u;
                 if (++it == sk.ipt) it = 0, ++tile;
             }
@@ -252,11 +250,12 @@ __global__ void __launch_bounds__(256, 1)
                 if (lane == 0) {
                     const uint32_t a0 = smem_u32(stage_ptr(s));
                     const uint32_t b0 = a0 + C::A_BYTES;
-                    const uint32_t alo = tmem + uint32_t(C::ALO_COL0 + 32 * s);
+                    const uint32_t alo = tmem + uint32_t(C::ALO_COL0 + C::BK * s);
 #pragma unroll
-                    for (int kk = 0; kk < 4; ++kk) {
-                        const uint64_t da = PASS == 1 ? desc_kmajor(a0, kk) : desc_mnmajor(a0, kk, 4096);
-                        const uint64_t db = desc_mnmajor(b0, kk, 4096);  // [B_hi | B_lo] atoms, 4 KB apart
+                    for (int kk = 0; kk < C::KSTEPS; ++kk) {
+                        const uint64_t da = PASS == 1 ? desc_kmajor(a0 + (kk >> 2) * 16384, kk & 3)
+                                                      : desc_mnmajor(a0, kk, C::ATOM_STRIDE);
+                        const uint64_t db = desc_mnmajor(b0, kk, C::ATOM_STRIDE);  // [hi atoms | lo atoms]
                         mma_ss(d, da, db, C::IDESC_SS, (first && kk == 0) ? 0u : 1u);
                         mma_ts(d, alo + 8 * kk, db, C::IDESC_TS, 1u);
                     }
@@ -281,26 +280,32 @@ __global__ void __launch_bounds__(256, 1)
         for (int64_t u = u0; u < u1; ++u) {
             mbar_wait(full + s, ph);
             const uint8_t* sA = stage_ptr(s);
-            uint32_t r[32];
-            if (PASS == 1) {
-                // row t of the K-major SW128 tile: 8 chunks of 16 B, chunk c at (c ^ t%8)
-                const float4* row = reinterpret_cast<const float4*>(sA + t * 128);
+            const uint32_t dst = tmem + lane_bits + uint32_t(C::ALO_COL0 + C::BK * s);
 #pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    const float4 v = row[c ^ (t & 7)];
-                    r[4 * c] = lo_bits(v.x), r[4 * c + 1] = lo_bits(v.y), r[4 * c + 2] = lo_bits(v.z),
-                    r[4 * c + 3] = lo_bits(v.w);
+            for (int h = 0; h < C::BK / 32; ++h) {
+                uint32_t r[32];
+                if (PASS == 1) {
+                    // row t of K-atom h (K-major SW128): 8 chunks of 16 B, chunk c at (c ^ t%8)
+                    const float4* row = reinterpret_cast<const float4*>(sA + h * 16384 + t * 128);
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float4 v = row[c ^ (t & 7)];
+                        r[4 * c] = lo_bits(v.x), r[4 * c + 1] = lo_bits(v.y), r[4 * c + 2] = lo_bits(v.z),
+                        r[4 * c + 3] = lo_bits(v.w);
+                    }
+                } else {
+                    // column t of the MN-major BASE32B tile (atom t/32, element e = t%32), rows
+                    // 32h..32h+31: 32-byte granule (e/8) ^ (k%4) of 128-byte row k
+                    const float* atom = reinterpret_cast<const float*>(sA + (t >> 5) * C::ATOM_STRIDE);
+                    const int e = t & 31;
+#pragma unroll
+                    for (int kr = 0; kr < 32; ++kr) {
+                        const int k = 32 * h + kr;
+                        r[kr] = lo_bits(atom[k * 32 + (((e >> 3) ^ (k & 3)) << 3) + (e & 7)]);
+                    }
                 }
-            } else {
-                // column t of the MN-major BASE32B tile: atom t/32, element e = t%32 of each row k,
-                // 32-byte granule (e/8) ^ (k%4)
-                const float* atom = reinterpret_cast<const float*>(sA + (t >> 5) * 4096);
-                const int e = t & 31;
-#pragma unroll
-                for (int k = 0; k < 32; ++k)
-                    r[k] = lo_bits(atom[k * 32 + ((((e >> 3) ^ (k & 3))) << 3) + (e & 7)]);
+                tmem_st32(dst + 32 * h, r);
             }
-            tmem_st32(tmem + lane_bits + uint32_t(C::ALO_COL0 + 32 * s), r);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(split + s);
@@ -352,18 +357,20 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-// 2-D f32 row-major [rows][cols] (ld floats), box = 32 cols x box_rows. K-major operand tiles
+// View a row-major f32 matrix [rows][cols] (ld floats) as 3-D (32 columns of an atom, rows,
+// cols/32 atoms) and box (32, box_rows, box_atoms): one TMA operation lands box_atoms
+// atoms of box_rows x 128 B, atom j at j * box_rows * 128 B in shared memory. K-major tiles
 // use the 16-byte-granule 128B swizzle, MN-major ones the 32-byte-granule variant that
 // matches UMMA's SWIZZLE_128B_BASE32B layout.
 cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
-                     bool mn_major) {
+                     int box_atoms, bool mn_major) {
     auto fn = encode_fn();
     if (!fn) return cudaErrorNotSupported;
-    const cuuint64_t dims[2] = {cuuint64_t(cols), cuuint64_t(rows)};
-    const cuuint64_t strides[1] = {cuuint64_t(ld) * 4};
-    const cuuint32_t box[2] = {32u, cuuint32_t(box_rows)};
-    const cuuint32_t estr[2] = {1u, 1u};
-    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+    const cuuint64_t dims[3] = {32u, cuuint64_t(rows), cuuint64_t(cols / 32)};
+    const cuuint64_t strides[2] = {cuuint64_t(ld) * 4, 128u};
+    const cuuint32_t box[3] = {32u, cuuint32_t(box_rows), cuuint32_t(box_atoms)};
+    const cuuint32_t estr[3] = {1u, 1u, 1u};
+    const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, estr,
                           CU_TENSOR_MAP_INTERLEAVE_NONE,
                           mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -371,13 +378,12 @@ cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t co
 }
 
 template <int KP, int PASS>
-cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo, float* slots,
-                      const StreamK& sk, cudaStream_t s) {
+cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, float* slots, const StreamK& sk, cudaStream_t s) {
     using C = TcCfg<KP, PASS>;
     auto kern = k_pass_tc<KP, PASS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
-    kern<<<unsigned(sk.G), 256, C::SMEM, s>>>(a, b, blo, slots, sk);
+    kern<<<unsigned(sk.G), 256, C::SMEM, s>>>(a, b, slots, sk);
     return cudaGetLastError();
 }
 
@@ -385,26 +391,24 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensor
 
 bool tc_supported(int kp) { return (kp == 32 || kp == 64) && encode_fn() != nullptr; }
 
-// Pass 1 on the tensor cores: A (mp x np, ld lda), Ht / Ht_lo (np x kp).
-cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* Ht,
-                          const float* Ht_lo, float* slots, const StreamK& sk, cudaStream_t s) {
-    CUtensorMap ma, mb, ml;
+// Pass 1 on the tensor cores: A (mp x np, ld lda) K-major, Ht_cat (np x 2kp) MN-major.
+cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* Ht_cat,
+                          float* slots, const StreamK& sk, cudaStream_t s) {
+    CUtensorMap ma, mb;
     cudaError_t e;
-    if ((e = make_map(&ma, A, mp, np, lda, 128, false)) != cudaSuccess) return e;
-    if ((e = make_map(&mb, Ht, np, kp, kp, 32, true)) != cudaSuccess) return e;
-    if ((e = make_map(&ml, Ht_lo, np, kp, kp, 32, true)) != cudaSuccess) return e;
-    return kp == 32 ? launch_tc<32, 1>(ma, mb, ml, slots, sk, s) : launch_tc<64, 1>(ma, mb, ml, slots, sk, s);
+    if ((e = make_map(&ma, A, mp, np, lda, 128, kTcStep / 32, false)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, Ht_cat, np, 2 * kp, 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
+    return kp == 32 ? launch_tc<32, 1>(ma, mb, slots, sk, s) : launch_tc<64, 1>(ma, mb, slots, sk, s);
 }
 
-// Pass 2 on the tensor cores: W / W_lo (mp x kp).
-cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* W,
-                          const float* W_lo, float* slots, const StreamK& sk, cudaStream_t s) {
-    CUtensorMap ma, mb, ml;
+// Pass 2 on the tensor cores: A MN-major (4 column atoms per 128-column tile), W_cat (mp x 2kp).
+cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* W_cat,
+                          float* slots, const StreamK& sk, cudaStream_t s) {
+    CUtensorMap ma, mb;
     cudaError_t e;
-    if ((e = make_map(&ma, A, mp, np, lda, 32, true)) != cudaSuccess) return e;
-    if ((e = make_map(&mb, W, mp, kp, kp, 32, true)) != cudaSuccess) return e;
-    if ((e = make_map(&ml, W_lo, mp, kp, kp, 32, true)) != cudaSuccess) return e;
-    return kp == 32 ? launch_tc<32, 2>(ma, mb, ml, slots, sk, s) : launch_tc<64, 2>(ma, mb, ml, slots, sk, s);
+    if ((e = make_map(&ma, A, mp, np, lda, kTcStep, 4, true)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, W_cat, mp, 2 * kp, 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
+    return kp == 32 ? launch_tc<32, 2>(ma, mb, slots, sk, s) : launch_tc<64, 2>(ma, mb, slots, sk, s);
 }
 
 }  // namespace ooc

@@ -132,7 +132,7 @@ struct oocnmf_ctx {
 
     DevBuf W, Ht, HHt, packed, N1, slots1, slots2, gram_w, gram_h, err_slots, red_slots, scal, flag;
     DevBuf HHt64, WtW64;         // f64 Grams for the trace-form error (f32 copies drive the updates)
-    DevBuf W_lo, Ht_lo;          // low halves of the 3xTF32 split (tensor-core path only)
+    DevBuf W_cat, Ht_cat;        // [F | F - tf32(F)] (rows x 2kp): tensor-core operands only
     bool use_tc = false;         // kp in {32, 64}: tcgen05 passes; else CUDA-core FFMA passes
     StreamK sk1, sk2;            // in-core dense passes
     StreamK sk1b[2], sk2b[2];    // out-of-core: full batch / last batch
@@ -167,13 +167,13 @@ void alloc_factors(oocnmf_ctx* c) {
     const char* force = std::getenv("OOCNMF_FORCE_FFMA");
     c->use_tc = tc_supported(kp) && !(force && force[0] == '1');
     if (c->use_tc) {
-        c->W_lo.alloc(size_t(c->mp) * kp * 4, "W_lo");
-        c->Ht_lo.alloc(size_t(c->np) * kp * 4, "Ht_lo");
-        ck(cudaMemsetAsync(c->W_lo.p, 0, c->W_lo.bytes, c->stream), "memset");
-        ck(cudaMemsetAsync(c->Ht_lo.p, 0, c->Ht_lo.bytes, c->stream), "memset");
+        c->W_cat.alloc(size_t(c->mp) * 2 * kp * 4, "W_cat");
+        c->Ht_cat.alloc(size_t(c->np) * 2 * kp * 4, "Ht_cat");
+        ck(cudaMemsetAsync(c->W_cat.p, 0, c->W_cat.bytes, c->stream), "memset");
+        ck(cudaMemsetAsync(c->Ht_cat.p, 0, c->Ht_cat.bytes, c->stream), "memset");
     } else {
-        c->W_lo.release();
-        c->Ht_lo.release();
+        c->W_cat.release();
+        c->Ht_cat.release();
     }
     c->HHt.alloc(size_t(kp) * kp * 4, "HHt");
     c->HHt64.alloc(size_t(kp) * kp * 8, "HHt64");
@@ -192,8 +192,9 @@ void alloc_factors(oocnmf_ctx* c) {
 }
 
 void plan_dense(oocnmf_ctx* c) {
-    plan_aht(c->sk1, c->mp, c->np, c->num_sms);
-    plan_wta(c->sk2, c->mp, c->np, c->num_sms);
+    const int step = c->use_tc ? kTcStep : kFfmaStep;
+    plan_aht(c->sk1, c->mp, c->np, c->num_sms, step);
+    plan_wta(c->sk2, c->mp, c->np, c->num_sms, step);
     c->slots1.alloc(size_t(c->sk1.G * c->sk1.smax) * kTile * c->kp * 4, "slots1");
     c->slots2.alloc(size_t(c->sk2.G * c->sk2.smax) * kTile * c->kp * 4, "slots2");
 }
@@ -243,22 +244,22 @@ reduced:
     c->norm_valid = true;
 }
 
-float* wlo(oocnmf_ctx* c) { return c->use_tc ? c->W_lo.as<float>() : nullptr; }
-float* htlo(oocnmf_ctx* c) { return c->use_tc ? c->Ht_lo.as<float>() : nullptr; }
+float* wlo(oocnmf_ctx* c) { return c->use_tc ? c->W_cat.as<float>() : nullptr; }
+float* htlo(oocnmf_ctx* c) { return c->use_tc ? c->Ht_cat.as<float>() : nullptr; }
 
 // Pass 1 over an A slab (rows_p x np, rows_p a multiple of 128): slots <- A·Ht partials.
 cudaError_t pass1(oocnmf_ctx* c, const float* A, int64_t rows_p, float* slots, const StreamK& sk, cudaStream_t s) {
-    if (c->use_tc) return launch_aht_tc(c->kp, A, c->np, rows_p, c->np, c->Ht.as<float>(), htlo(c), slots, sk, s);
+    if (c->use_tc) return launch_aht_tc(c->kp, A, c->np, rows_p, c->np, c->Ht_cat.as<float>(), slots, sk, s);
     return launch_aht(c->kp, A, c->np, c->Ht.as<float>(), slots, sk, s);
 }
-// Pass 2 over an A slab with its W rows: slots <- A^T·W partials.
-cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W, const float* Wlo, float* slots,
+// Pass 2 over an A slab with its W rows (W rows x kp, Wcat rows x 2kp): slots <- A^T·W partials.
+cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W, const float* Wcat, float* slots,
                   const StreamK& sk, cudaStream_t s) {
-    if (c->use_tc) return launch_wta_tc(c->kp, A, c->np, rows_p, c->np, W, Wlo, slots, sk, s);
+    if (c->use_tc) return launch_wta_tc(c->kp, A, c->np, rows_p, c->np, Wcat, slots, sk, s);
     return launch_wta(c->kp, A, c->np, W, slots, sk, s);
 }
 
-// HH^T of the current Ht (gram only; also refreshes Ht_lo for the tensor-core pass).
+// HH^T of the current Ht (gram only; also refreshes Ht_cat for the tensor-core pass).
 void gram_h(oocnmf_ctx* c) {
     const int kp = c->kp;
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, nullptr, nullptr, nullptr, nullptr, 0.f, false,
@@ -330,7 +331,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
             ck(cudaEventRecord(c->ev_copied[si], c->copy_stream), "event");
             ck(cudaStreamWaitEvent(s, c->ev_copied[si], 0), "wait copied");
             float* Wb = c->W.as<float>() + b0 * kp;
-            float* Wlob = c->use_tc ? c->W_lo.as<float>() + b0 * kp : nullptr;
+            float* Wlob = c->use_tc ? c->W_cat.as<float>() + b0 * 2 * kp : nullptr;
             count(c, pass1(c, st, brp, c->slots1.as<float>(), s1, s), "aht");
             count(c, launch_factor_update(kp, Wb, brp, nullptr, c->slots1.as<float>(), &s1, c->HHt.as<float>(),
                                           eps, true, c->gram_w.as<double>() + b * gwb * kp * kp, nullptr,
@@ -866,10 +867,11 @@ int oocnmf_attach_host_dense_f32(oocnmf_ctx* c, const float* a, uint64_t lda, ui
         }
         const int64_t nb = (int64_t(c->rows) + br - 1) / br;
         const int64_t last = round_up(int64_t(c->rows) - (nb - 1) * br, kTile);
-        plan_aht(c->sk1b[0], br, c->np, c->num_sms);
-        plan_aht(c->sk1b[1], last, c->np, c->num_sms);
-        plan_wta(c->sk2b[0], br, c->np, c->num_sms);
-        plan_wta(c->sk2b[1], last, c->np, c->num_sms);
+        const int step = c->use_tc ? kTcStep : kFfmaStep;
+        plan_aht(c->sk1b[0], br, c->np, c->num_sms, step);
+        plan_aht(c->sk1b[1], last, c->np, c->num_sms, step);
+        plan_wta(c->sk2b[0], br, c->np, c->num_sms, step);
+        plan_wta(c->sk2b[1], last, c->np, c->num_sms, step);
         const int64_t s1 = std::max(c->sk1b[0].G * c->sk1b[0].smax, c->sk1b[1].G * c->sk1b[1].smax);
         const int64_t s2 = std::max(c->sk2b[0].G * c->sk2b[0].smax, c->sk2b[1].G * c->sk2b[1].smax);
         c->slots1.alloc(size_t(s1) * kTile * c->kp * 4, "slots1");
@@ -994,8 +996,8 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
         t1.alloc(size_t(c->mp) * kp * 4, "aht");
         if (c->kind == Kind::dense) {
             if (c->use_tc) {
-                ck(launch_split_lo(c->Ht.as<float>(), c->Ht_lo.as<float>(), c->np * kp, s), "split");
-                ck(launch_split_lo(c->W.as<float>(), c->W_lo.as<float>(), c->mp * kp, s), "split");
+                ck(launch_split_cat(c->Ht.as<float>(), c->Ht_cat.as<float>(), c->np, kp, s), "split");
+                ck(launch_split_cat(c->W.as<float>(), c->W_cat.as<float>(), c->mp, kp, s), "split");
             }
             ck(pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
             ck(launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, t1.as<float>(), false, s), "reduce");
