@@ -416,24 +416,31 @@ def make_plan(m, n, k, n_workers, n_b, strategy: Strategy) -> PartitionPlan:
                          [(int(b[i]), int(b[i + 1])) for i in range(n_b)])
 
 
+def exchange_unique_id(rank: int, make_id, device: Optional[int] = None, group=None) -> bytes:
+    """Broadcast rank 0's 128-byte NCCL unique id to every rank with torch.distributed
+    (gloo or nccl process group; plumbing only)."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.zeros(128, dtype=torch.uint8)
+    if rank == 0:
+        uid = make_id()
+        if len(uid) != 128:
+            raise ShapeError("exchange_unique_id: the id must be 128 bytes")
+        t = torch.frombuffer(bytearray(uid), dtype=torch.uint8).clone()
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda(device)
+    dist.broadcast(t, 0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
+
+
 class DistComm:
-    """One rank of an NCCL group over NVLink. The 128-byte NCCL unique id is exchanged with
-    torch.distributed (plumbing only); all traffic of the solve goes through NCCL inside
-    the C-ABI library."""
+    """One rank of an NCCL group over NVLink (the B200 CommHandle). The NCCL unique id is
+    exchanged with torch.distributed; all traffic of the solve goes through NCCL inside the
+    C-ABI library."""
 
     def __init__(self, rank: int, size: int, device: int, group=None):
-        uid = b"\0" * 128
-        if size > 1:
-            import torch
-            import torch.distributed as dist
-
-            t = torch.zeros(128, dtype=torch.uint8)
-            if rank == 0:
-                t = torch.frombuffer(bytearray(Context.unique_id()), dtype=torch.uint8).clone()
-            if dist.get_backend(group) == "nccl":
-                t = t.cuda(device)
-            dist.broadcast(t, 0, group=group)
-            uid = bytes(t.cpu().numpy().tobytes())
+        uid = exchange_unique_id(rank, Context.unique_id, device, group) if size > 1 else b"\0" * 128
         self.rank, self.size, self.device = rank, size, device
         self.ctx = Context(device, rank, size, uid)
 

@@ -1,0 +1,62 @@
+"""Worker for tests/test_multi_gpu.py — launched with torch.distributed.run, one rank per GPU.
+
+Runs the row-partitioned solve through the public API (nmf_distributed over NCCL) on dense,
+CSR and out-of-core sources and writes rank 0's results to the JSON path in argv[1].
+"""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import oracle  # noqa: E402
+import paper_2202_09518_b200 as nmf  # noqa: E402
+
+
+def f32(x):
+    return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+
+def main(out_path):
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    comm = nmf.DistComm(rank, world, local)
+    port = oracle.port
+    results = {}
+
+    def run(name, a, m, n, k, iters, interval, host_slab=None, batch_rows=0, **kw):
+        plan = nmf.make_plan(m, n, k, world, 1, nmf.Strategy.rnmf)
+        w0, h0 = port.init_factors(m, n, k, 0)
+        cfg = nmf.NmfConfig(k=k, max_iters=iters, error_check_interval=interval, eta=0.0,
+                            init=nmf.FactorInit.from_files, init_w=f32(w0), init_h=f32(h0), device=local, **kw)
+        slab = None
+        if host_slab is not None:
+            (r0, r1), _ = plan.slabs[rank]
+            slab = np.ascontiguousarray(host_slab[r0:r1])
+        res = nmf.nmf_distributed(a, cfg, plan, comm, host_slab=slab, batch_rows=batch_rows)
+        results[name] = {"trace": [e for _, e in res.error_trace], "iters": [i for i, _ in res.error_trace],
+                         "w_fro": float(np.linalg.norm(res.w)), "h_fro": float(np.linalg.norm(res.h)),
+                         "w_sum": float(res.w.sum()), "h_sum": float(res.h.sum()),
+                         "allreduce_s": res.counters.allreduce_s, "w_shape": list(res.w.shape)}
+
+    a = port.uniform_dense(1100, 900, 42, 99).astype(np.float32)
+    run("dense_k16", a, 1100, 900, 16, 30, 10)
+    run("dense_k32", a, 1100, 900, 32, 30, 10)
+    rp, ci, v, (m, n) = port.gen_sparse(1500, 1200, 0.02, 3)
+    run("csr_k16", nmf.CsrMatrix(m, n, rp, ci, f32(v)), m, n, 16, 20, 10)
+    run("ooc_k32", None, 1100, 900, 32, 20, 10, host_slab=a, batch_rows=128)
+    if rank == 0:
+        with open(out_path, "w") as f:
+            json.dump(results, f)
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1])

@@ -1,0 +1,80 @@
+"""Multi-GPU (NCCL over NVLink) row-partitioned solve vs the oracle's row-partitioned run.
+
+Skipped unless at least 2 GPUs are visible. Launches tests/dist_worker.py with
+torch.distributed.run (one rank per GPU) and compares rank 0's trajectory and gathered
+factors with the CPU oracle (same f32-rounded inputs and init).
+"""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2202_09518_b200 as nmf
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def f32(x):
+    return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.fixture(scope="module")
+def dist_results(tmp_path_factory):
+    n = nmf.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    out = tmp_path_factory.mktemp("dist") / "r.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "dist_worker.py"),
+           str(out)]
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT)
+    return world, json.load(open(out))
+
+
+def _check(r, ref, tol=1e-4):
+    assert r["iters"] == ref.trace_iters.tolist()
+    rel = np.max(np.abs(np.array(r["trace"]) - ref.trace_err) / ref.trace_err)
+    assert rel <= tol, rel
+    assert r["w_fro"] == pytest.approx(np.linalg.norm(ref.w), rel=1e-3)
+    assert r["h_fro"] == pytest.approx(np.linalg.norm(ref.h), rel=1e-3)
+
+
+@pytest.mark.parametrize("name,k", [("dense_k16", 16), ("dense_k32", 32)])
+def test_dense_rnmf_matches_oracle(dist_results, name, k):
+    world, res = dist_results
+    a = f32(oracle.port.uniform_dense(1100, 900, 42, 99))
+    w0, h0 = oracle.port.init_factors(1100, 900, k, 0)
+    ref = oracle.port.nmf_rnmf(a, k, f32(w0), f32(h0), world, 1, max_iters=30, interval=10)
+    _check(res[name], ref)
+    assert res[name]["w_shape"] == [1100, k]
+
+
+def test_csr_rnmf_matches_oracle(dist_results):
+    world, res = dist_results
+    rp, ci, v, shape = oracle.port.gen_sparse(1500, 1200, 0.02, 3)
+    w0, h0 = oracle.port.init_factors(1500, 1200, 16, 0)
+    ref = oracle.port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
+    _check(res["csr_k16"], ref)
+
+
+def test_out_of_core_rnmf_matches_oracle(dist_results):
+    world, res = dist_results
+    a = f32(oracle.port.uniform_dense(1100, 900, 42, 99))
+    w0, h0 = oracle.port.init_factors(1100, 900, 32, 0)
+    ref = oracle.port.nmf_rnmf(a, 32, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
+    _check(res["ooc_k32"], ref)
