@@ -1,17 +1,20 @@
 #!/usr/bin/env python
-"""Benchmark of the MU-NMF hot path (BASELINE.json metric: MU iters/sec and A-pass GB/s vs
-the HBM roofline).
+"""Benchmark of the MU-NMF hot path (BASELINE.json metric: MU iters/sec and A-pass GB/s vs the
+HBM roofline).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload dense]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload dense|sparse|ooc]
 
-A "step" is one MU iteration (W update then H update, error every 10 iterations as the
-reference default) over the synthetic dense 65536 x 65536 f32 A with k = 32 (config 2),
-row-partitioned over N GPUs (strong scaling). One JSON line on rank 0.
+A "step" is one MU iteration (W update then H update; error every 10 iterations as the
+reference default). Default workload = config 2: synthetic dense 65536 x 65536 f32 A, k = 32,
+row-partitioned over N GPUs (strong scaling), one JSON line on rank 0.
+  --workload sparse : config 3, CSR 2^22 x 2^22, density 1e-5 (reference generator), k = 32
+  --workload ooc    : config 4 (scaled to this host's RAM): A in pinned host memory, streamed
+                      over the host link every iteration, k = 64
 
---impl reference times the reference's own CPU solver (oracle/_ref, compiled from
+--impl reference times the reference's own CPU solver (oracle/_ref, compiled from the
 /root/reference sources; the oracle port if absent) on this box's host cores, one MU
-iteration per step on a bounded row sample, extrapolated to the full matrix (cost is
-linear in rows).
+iteration per step on a bounded row sample, extrapolated to the full matrix.
 """
 import argparse
 import json
@@ -35,14 +38,21 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["dense"], default="dense")
-    p.add_argument("--m", type=int, default=65536)
-    p.add_argument("--n", type=int, default=65536)
-    p.add_argument("--k", type=int, default=32)
+    p.add_argument("--workload", choices=["dense", "sparse", "ooc"], default="dense")
+    p.add_argument("--m", type=int, default=None)
+    p.add_argument("--n", type=int, default=None)
+    p.add_argument("--k", type=int, default=None)
+    p.add_argument("--density", type=float, default=1e-5)
+    p.add_argument("--ooc-gb", type=float, default=64.0, help="host A slab per rank (GB) for --workload ooc")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
-    return p.parse_args()
+    a = p.parse_args()
+    dflt = {"dense": (65536, 65536, 32), "sparse": (1 << 22, 1 << 22, 32), "ooc": (None, 65536, 64)}[a.workload]
+    a.m = a.m or dflt[0]
+    a.n = a.n or dflt[1]
+    a.k = a.k or dflt[2]
+    return a
 
 
 def peaks():
@@ -109,15 +119,23 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_reference_rate(m, n, k, seconds, steps=None, warmup=0):
-    """Reference CPU solver, one MU iteration per step on a row sample; returns (it/s
-    extrapolated to m rows, dict)."""
+# ----------------------------------------------------------------------------- CPU reference
+def _ref_impl():
+    import oracle
+
+    impl = oracle.ref if oracle.ref.available else oracle.port
+    return impl, ("reference" if impl is oracle.ref else "port")
+
+
+def cpu_reference_dense(m, n, k, seconds, steps=None, warmup=0):
+    """Reference CPU solver, one MU iteration per step on a 1024-row sample of the uniform A;
+    returns (it/s extrapolated to m rows, cpu_baseline dict). Cost is linear in rows here
+    (every term of the iteration is O(rows * n * k) except O(n k^2) ones, < 0.1%)."""
     import numpy as np
 
     import oracle
 
-    impl = oracle.ref if oracle.ref.available else oracle.port
-    kind = "reference" if impl is oracle.ref else "port"
+    impl, kind = _ref_impl()
     rows = 1024
     a = impl.uniform_dense(rows, n, 42, 99)
     w, h = oracle.port.init_factors(m, n, k, 0)
@@ -152,21 +170,83 @@ def cpu_reference_rate(m, n, k, seconds, steps=None, warmup=0):
                             f"uniform A, k={k}; {per_it:.3f} s/iter scaled by {rows}/{m} rows (cost is linear in rows)"}
 
 
+def cpu_reference_sparse(samples, m, k, seconds):
+    """samples: [(rows_i, CsrMatrix)] row samples of the same matrix. The reference's CSR
+    iteration costs a + b*rows (a = the O(n k^2) H-side terms); fit a, b from two sample
+    sizes and extrapolate to m rows."""
+    import numpy as np
+
+    import oracle
+
+    impl = oracle.ref
+    if not impl.available:
+        return None, None
+    kind = "reference"
+    pts = []
+    for rows, s in samples:
+        n = s.cols
+        w0, h0 = oracle.port.init_factors(rows, n, k, 0)
+        hnd = impl.csr_handle(s.row_ptr, s.col_idx, s.values, rows, n)
+        per = []
+        t_end = time.perf_counter() + seconds / len(samples)
+        try:
+            while True:
+                t0 = time.perf_counter()
+                impl.mu_iteration_csr_handle(hnd, w0, h0)  # loop body of nmf_serial, no error check
+                per.append(time.perf_counter() - t0)
+                if time.perf_counter() > t_end or len(per) >= 5:
+                    break
+        finally:
+            impl.csr_free(hnd)
+        pts.append((rows, min(per), s.nnz))
+    (r1, t1, _), (r2, t2, _) = pts[0], pts[-1]
+    b = (t2 - t1) / (r2 - r1)
+    a = t1 - b * r1
+    per_full = a + b * m
+    rate = 1.0 / per_full
+    return rate, {"value": rate, "unit": "it/s", "cores": int(os.environ.get("OMP_NUM_THREADS", CPU_CORES)),
+                  "kind": kind,
+                  "sample": f"reference MU iteration (nmf_serial loop body, no error check) on row samples "
+                            f"{[(p[0], p[2]) for p in pts]} (rows, nnz) of the same CSR; fit t = a + b*rows "
+                            f"(a={a:.3f}s, b={b:.3e}s/row) extrapolated to {m} rows: {per_full:.1f} s/iter"}
+
+
+# ----------------------------------------------------------------------------- helpers
+def roofline(info, bytes_per_launch, peak, peak_src, traffic=None, bound="hbm", unit="GB/s"):
+    per = {}
+    for name, key in (("aht_pass (A.H^T)", "aht_pass_ms"), ("wta_pass (A^T.W)", "wta_pass_ms")):
+        launches = max(1, int(info[key.replace("_ms", "_launches")]))
+        per[name] = info[key] / launches
+    dom = max(per, key=per.get)
+    b = bytes_per_launch[dom] if isinstance(bytes_per_launch, dict) else bytes_per_launch
+    achieved = b / (per[dom] * 1e-3) / 1e9
+    return {"bound": bound, "achieved": achieved, "peak": peak, "unit": unit, "frac": achieved / peak,
+            "traffic": traffic.get(dom.split()[0]) if traffic else None, "kernel": dom,
+            "algorithmic_bytes_per_launch": b, "avg_launch_ms": per[dom], "per_kernel_ms": per,
+            "peak_source": peak_src}
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
-    m, n, k, K, W = args.m, args.n, args.k, args.steps, max(3, args.warmup)
-    workload = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
-    metric = f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, NCCL all-reduce)"
+    K, W, k = args.steps, max(3, args.warmup), args.k
 
     if args.impl == "reference":
         if rank != 0:
             return
-        rate, cb = cpu_reference_rate(m, n, k, args.cpu_seconds, steps=K, warmup=W)
+        m, n = args.m or 65536, args.n
+        if args.workload != "dense":
+            print(json.dumps({"impl": "reference", "unavailable": f"--impl reference implemented for the "
+                                                                  f"default (dense) workload only"}))
+            return
+        rate, cb = cpu_reference_dense(m, n, k, args.cpu_seconds, steps=K, warmup=W)
         cb["sample"] = cb["sample"].replace("MU iterations", f"timed MU iterations after {W} warm-up")
-        print(json.dumps({"impl": "reference", "metric": metric, "value": rate, "unit": "it/s", "n_gpus": args.gpus,
+        workload = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
+        print(json.dumps({"impl": "reference", "metric": f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, "
+                                                         f"NCCL all-reduce)",
+                          "value": rate, "unit": "it/s", "n_gpus": args.gpus,
                           "steps": K, "warmup": W, "ms_per_step": 1e3 / rate, "higher_is_better": True,
                           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                           "config": {"workload": workload, "m": m, "n": n, "k": k, "parallelism": "host cores"},
@@ -184,13 +264,6 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    plan = nmf.make_plan(m, n, k, world, 1, nmf.Strategy.rnmf)
-    (r0, r1), _ = plan.slabs[rank]
-    rows = r1 - r0
-    comm = nmf.DistComm(rank, world, local) if world > 1 else None
-    ctx = comm.ctx if comm else nmf.Context(local)
-    ctx.set_problem(m, n, k, r0, rows)
-    ctx.generate_dense_uniform(42, 99)
 
     def barrier():
         if world > 1:
@@ -204,7 +277,73 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    # warm-up: W iterations from the seeded init
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t)
+        return float(t.item())
+
+    comm = nmf.DistComm(rank, world, local) if world > 1 else None
+    ctx = comm.ctx if comm else nmf.Context(local)
+    kp = 8 if k <= 8 else 16 if k <= 16 else 32 if k <= 32 else 64
+    hbm, peak_src = peaks()
+    extra = {}
+    host_buf = None
+
+    # ------------------------------------------------------------------ set up A
+    n = args.n
+    if args.workload == "ooc":
+        rows_per_rank = args.m // world if args.m else int(args.ooc_gb * 1e9 / (n * 4)) // 128 * 128
+        m = rows_per_rank * world
+    else:
+        m = args.m
+    plan = nmf.make_plan(m, n, k, world, 1, nmf.Strategy.rnmf)
+    (r0, r1), _ = plan.slabs[rank]
+    rows = r1 - r0
+    t_setup = time.perf_counter()
+    if args.workload == "dense":
+        ctx.set_problem(m, n, k, r0, rows)
+        ctx.generate_dense_uniform(42, 99)
+        workload = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
+        metric = f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, NCCL all-reduce)"
+        bytes_per_launch = rows * n * 4 + (n + rows) * k * 4
+    elif args.workload == "sparse":
+        ctx.set_problem(m, n, k, r0, rows)
+        ctx.generate_csr_uniform(args.density, 1)
+        import ctypes as C
+
+        cnt = C.c_uint64()
+        nmf.check(nmf._capi.lib().oocnmf_csr_nnz(ctx._h, C.byref(cnt)))
+        nnz = int(cnt.value)
+        workload = (f"sparse synthetic CSR {m}x{n}, density {args.density} (reference generator "
+                    f"synth.cpp:60-86 on device, seed 1), nnz/rank={nnz}, k={k}, RNMF row slabs")
+        metric = f"MU iters/sec (sparse CSR {m}x{n} density {args.density}, k={k}, 1D row-partitioned)"
+        # gather model: CSR (8 B/nnz) + row_ptr + one kp-wide factor row per
+        # nonzero + output, per SpMM; pass 2 runs on CSR(A^T) (n rows)
+        bytes_per_launch = {"aht_pass (A.H^T)": nnz * 8 + (rows + 1) * 8 + nnz * kp * 4 + rows * kp * 4,
+                            "wta_pass (A^T.W)": nnz * 8 + (n + 1) * 8 + nnz * kp * 4 + n * kp * 4}
+        extra["nnz_per_rank"] = nnz
+    else:
+        # out-of-core: A slab in pinned host memory, generated on the device in chunks
+        ctx.set_problem(m, n, k, r0, rows)
+        host_buf = np.empty((rows, n), np.float32)
+        nmf.check(nmf._capi.lib().oocnmf_host_register(host_buf.ctypes.data, host_buf.nbytes))
+        chunk = max(128, (8 << 30) // (n * 4) // 128 * 128)
+        with nmf.Context(local) as gen:
+            for c0 in range(0, rows, chunk):
+                cr = min(chunk, rows - c0)
+                gen.set_problem(m, n, k, r0 + c0, cr)
+                gen.generate_dense_uniform(42, 99)
+                gen.download_dense(host_buf[c0:c0 + cr])
+        ctx.attach_host(host_buf)
+        workload = (f"out-of-core dense {m}x{n} f32 uniform A, {rows * n * 4 / 1e9:.1f} GB pinned host slab/rank "
+                    f"(config 4 scaled to this host's RAM), k={k}, streamed every iteration")
+        metric = f"MU iters/sec (out-of-core dense {m}x{n}, k={k}, host-link streaming)"
+        bytes_per_launch = rows * n * 4
+    extra["setup_s"] = time.perf_counter() - t_setup
+
+    # ------------------------------------------------------------------ timed solve
     ctx.solve(nmf.NmfConfig(k=k, max_iters=W, error_check_interval=W, eta=0.0, seed=0))
     cfg = nmf.NmfConfig(k=k, max_iters=K, error_check_interval=10, eta=0.0, init=nmf.FactorInit.resident)
     barrier()
@@ -217,69 +356,100 @@ def main():
     barrier()
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     value = K / (ms / 1e3)
-    hbm, peak_src = peaks()
 
-    # dominant streaming kernel: algorithmic bytes per launch / its CUDA-event duration
-    per = {}
-    for name, key in (("aht_pass (A.H^T)", "aht_pass_ms"), ("wta_pass (A^T.W)", "wta_pass_ms")):
-        launches = max(1, int(info[key.replace("_ms", "_launches")]))
-        per[name] = info[key] / launches
-    dom = max(per, key=per.get)
-    bytes_per_launch = rows * n * 4 + (n + rows) * k * 4
-    achieved = bytes_per_launch / (per[dom] * 1e-3) / 1e9
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
-    if os.path.exists(prof):
-        try:
-            traffic = json.load(open(prof)).get(dom.split()[0])
-        except Exception:
-            traffic = None
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                "traffic": traffic, "kernel": dom, "algorithmic_bytes_per_launch": bytes_per_launch,
-                "avg_launch_ms": per[dom], "per_kernel_ms": per, "peak_source": peak_src}
-    a_pass_gbs = 2 * m * n * 4 * value / 1e9  # whole-job A traffic, both passes
+    if args.workload == "dense" and world == 1 and (m, n, k) == (65536, 65536, 32):
+        prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
+        if os.path.exists(prof):
+            traffic = json.load(open(prof))
+    if args.workload == "ooc":
+        # host-link roofline: measured pinned H2D bandwidth on this GPU (concurrently on all ranks)
+        probe = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+        dev = torch.empty_like(probe, device="cuda")
+        for _ in range(2):
+            dev.copy_(probe, non_blocking=True)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(8):
+            dev.copy_(probe, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        link = 8 * probe.numel() / (e0.elapsed_time(e1) * 1e-3) / 1e9
+        link = min(link, max_over_ranks(link)) if world == 1 else -max_over_ranks(-link)
+        achieved = rows * n * 4 * value / 1e9
+        roof = {"bound": "host-link", "achieved": achieved, "peak": link, "unit": "GB/s", "frac": achieved / link,
+                "traffic": None, "kernel": "row-batch sweep (H2D copy stream, overlapped compute)",
+                "algorithmic_bytes_per_launch": rows * n * 4, "avg_launch_ms": ms / K,
+                "peak_source": "measured pinned H2D (torch copy_ of a 1 GiB pinned buffer, 8 reps) on this box",
+                "hbm_pass_ms": {"aht_pass (A.H^T)": info["aht_pass_ms"] / max(1, info["aht_pass_launches"]),
+                                "wta_pass (A^T.W)": info["wta_pass_ms"] / max(1, info["wta_pass_launches"])}}
+    else:
+        roof = roofline(info, bytes_per_launch, hbm, peak_src, traffic)
+    extra["a_pass_gbs_total"] = sum_over_ranks(2 * rows * n * 4 * value / 1e9) if args.workload == "dense" else None
 
-    # ---- e2e: host buffers through the public API, H2D/D2H inside the timed region
+    # ------------------------------------------------------------------ e2e through the public API
     e2e = None
-    if not args.no_e2e:
-        host = np.empty((rows, n), np.float32)
-        ctx.download_dense(host)
-        nmf.check(nmf._capi.lib().oocnmf_host_register(host.ctypes.data, host.nbytes))
+    if not args.no_e2e and args.workload in ("dense", "sparse"):
+        if args.workload == "dense":
+            host = np.empty((rows, n), np.float32)
+            ctx.download_dense(host)
+            nmf.check(nmf._capi.lib().oocnmf_host_register(host.ctypes.data, host.nbytes))
+            h2d = rows * n * 4
+        else:
+            host = ctx.download_csr()
+            h2d = host.nnz * 12 + (rows + 1) * 8
         try:
             barrier()
             t0 = time.perf_counter()
-            if world == 1:
+            ecfg = nmf.NmfConfig(k=k, max_iters=K, error_check_interval=10, eta=0.0, seed=0, device=local)
+            if world == 1 and args.workload == "dense":
                 import ctypes as C
 
-                c = nmf.NmfConfig(k=k, max_iters=K, error_check_interval=10, eta=0.0, seed=0).to_c()
+                c = ecfg.to_c()
                 wout, hout = np.empty((rows, k)), np.empty((k, n))
                 ti, te = np.zeros(K // 10 + 2, np.uint64), np.zeros(K // 10 + 2)
                 inf = nmf._capi.Info()
                 nmf.check(nmf._capi.lib().oocnmf_nmf_serial_dense_f32(
-                    local, host.ctypes.data_as(C.POINTER(C.c_float)), rows, n, C.byref(c),
-                    None, None, wout.ctypes.data_as(C.POINTER(C.c_double)), hout.ctypes.data_as(C.POINTER(C.c_double)),
+                    local, host.ctypes.data_as(C.POINTER(C.c_float)), rows, n, C.byref(c), None, None,
+                    wout.ctypes.data_as(C.POINTER(C.c_double)), hout.ctypes.data_as(C.POINTER(C.c_double)),
                     ti.ctypes.data_as(C.POINTER(C.c_uint64)), te.ctypes.data_as(C.POINTER(C.c_double)), ti.size,
                     C.byref(inf)))
             else:
                 ctx.set_problem(m, n, k, r0, rows)
-                ctx.load_dense(host)
-                ctx.solve(nmf.NmfConfig(k=k, max_iters=K, error_check_interval=10, eta=0.0, seed=0))
+                if args.workload == "dense":
+                    ctx.load_dense(host)
+                else:
+                    ctx.load_csr(host)
+                ctx.solve(ecfg)
                 ctx.get_factors()
-                ctx.gather_w()
+                if world > 1:
+                    ctx.gather_w()
             torch.cuda.synchronize()
             e2e_s = max_over_ranks(time.perf_counter() - t0)
         finally:
-            nmf._capi.lib().oocnmf_host_unregister(host.ctypes.data)
-        kp = 8 if k <= 8 else 16 if k <= 16 else 32 if k <= 32 else 64
+            if args.workload == "dense":
+                nmf._capi.lib().oocnmf_host_unregister(host.ctypes.data)
         d2h = (((rows + 127) // 128 * 128) + (n + 127) // 128 * 128) * kp * 4 + 16 * (K // 10 + 1)
-        e2e = {"value": K / e2e_s, "unit": "it/s", "h2d_bytes_per_step": rows * n * 4 / K,
-               "d2h_bytes_per_step": d2h / K,
-               "note": f"one public-API solve of {K} iterations on host (pinned) f32 buffers: A uploaded once "
-                       f"({rows * n * 4 / 1e9:.2f} GB/rank), W/H downloaded once; bytes are per step"}
+        e2e = {"value": K / e2e_s, "unit": "it/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+               "note": f"one public-API solve of {K} iterations on host buffers (A uploaded once: {h2d / 1e9:.2f} "
+                       f"GB/rank; W/H downloaded once); bytes are per step"}
+    elif args.workload == "ooc":
+        e2e = {"value": value, "unit": "it/s", "h2d_bytes_per_step": rows * n * 4, "d2h_bytes_per_step": 16,
+               "note": "out-of-core: the timed solve already reads A from pinned host memory every iteration"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        _, cpu = cpu_reference_rate(m, n, k, args.cpu_seconds)
+        if args.workload == "dense":
+            _, cpu = cpu_reference_dense(m, n, k, args.cpu_seconds)
+        elif args.workload == "sparse":
+            samples = []
+            for sr in (2048, 8192):
+                with nmf.Context(local) as g:
+                    g.set_problem(m, n, k, 0, sr)
+                    g.generate_csr_uniform(args.density, 1)
+                    samples.append((sr, g.download_csr()))
+            _, cpu = cpu_reference_sparse(samples, m, k, args.cpu_seconds)
 
     if rank == 0:
         out = {"metric": metric, "value": value, "unit": "it/s", "n_gpus": world, "steps": K, "warmup": W,
@@ -287,11 +457,14 @@ def main():
                "dtype": "f32", "data": "synthetic",
                "config": {"workload": workload, "m": m, "n": n, "k": k, "parallelism": f"rnmf-dp{world}",
                           "rows_per_rank": rows, "error_check_interval": 10,
-                          "l2": f"A slab {rows * n * 4 / 1e9:.1f} GB/rank >> 126 MB L2 (no flush needed)"},
-               "a_pass_gbs": a_pass_gbs, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
-               "clocks": clk.summary(), "gpu_launches": int(info["gpu_launches"]),
-               "final_rel_error": trace[-1][1] if trace else None}
+                          "l2": f"A slab >> 126 MB L2 (no flush needed)"},
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+               "gpu_launches": int(info["gpu_launches"]), "final_rel_error": trace[-1][1] if trace else None}
+        out.update({k_: v for k_, v in extra.items() if v is not None})
         print(json.dumps(out))
+    if host_buf is not None:
+        ctx.close()
+        nmf._capi.lib().oocnmf_host_unregister(host_buf.ctypes.data)
     if comm:
         comm.close()
         torch.distributed.destroy_process_group()

@@ -142,6 +142,9 @@ int oocnmf_host_register(void* p, uint64_t bytes);   /* cudaHostRegister (pin) *
 int oocnmf_host_unregister(void* p);
 /* Copy the resident dense A slab (rows x n, f32) back to host memory (ld = n). */
 int oocnmf_download_dense_f32(oocnmf_ctx* ctx, float* a_slab);
+/* Resident CSR slab: nnz, then row_ptr (rows+1), col_idx, vals (f32 widened to f64). */
+int oocnmf_csr_nnz(oocnmf_ctx* ctx, uint64_t* nnz);
+int oocnmf_download_csr(oocnmf_ctx* ctx, uint64_t* row_ptr, uint64_t* col_idx, double* vals);
 
 /* ----- factors ----- */
 int oocnmf_set_factors_f64(oocnmf_ctx* ctx, const double* w_slab /* rows x k */,

@@ -350,6 +350,24 @@ class Ref(_Lib):
         f.argtypes = [C.c_void_p, _u64, _pd, _pd, _dbl]
         self._check(f(hnd, w.shape[1], _ptr(w), _ptr(h), eps))
 
+    def csr_handle(self, rp, ci, v, m, n):
+        self._csr_keep = (np.ascontiguousarray(rp, np.uint64), np.ascontiguousarray(ci, np.uint64),
+                          np.ascontiguousarray(v, np.float64))
+        f = self.lib.ref_csr_create
+        f.restype = C.c_void_p
+        f.argtypes = [_pu, _pu, _pd, _u64, _u64]
+        return f(_ptr(self._csr_keep[0], _pu), _ptr(self._csr_keep[1], _pu), _ptr(self._csr_keep[2]), m, n)
+
+    def csr_free(self, hnd):
+        f = self.lib.ref_csr_destroy
+        f.argtypes = [C.c_void_p]
+        f(hnd)
+
+    def mu_iteration_csr_handle(self, hnd, w, h, eps=1e-12):
+        f = self.lib.ref_mu_iteration_csr_handle
+        f.argtypes = [C.c_void_p, _u64, _pd, _pd, _dbl]
+        self._check(f(hnd, w.shape[1], _ptr(w), _ptr(h), eps))
+
 
 port = Port()
 ref = Ref()

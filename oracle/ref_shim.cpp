@@ -276,6 +276,32 @@ int ref_mu_iteration_handle(void* a_handle, std::uint64_t k, double* w, double* 
     });
 }
 
+// CSR variant for the sparse bench sample (A held by the library across timed iterations).
+void* ref_csr_create(const std::uint64_t* rp, const std::uint64_t* ci, const double* v, std::uint64_t m,
+                     std::uint64_t n) {
+    return new CsrMatrix(make_csr(m, n, rp, ci, v));
+}
+void ref_csr_destroy(void* p) { delete static_cast<CsrMatrix*>(p); }
+int ref_mu_iteration_csr_handle(void* a_handle, std::uint64_t k, double* w, double* h, double eps) {
+    return guarded([&] {
+        const CsrMatrix& A = *static_cast<CsrMatrix*>(a_handle);
+        const std::uint64_t m = A.rows(), n = A.cols();
+        DenseMatrix W = copy_dense(w, m, k), H = copy_dense(h, k, n);
+        DenseMatrix ht = transpose(H);
+        DenseMatrix hht = gram_t(MatrixRef(ht));
+        DenseMatrix aht = matmul(MatrixRef(A), ht);
+        DenseMatrix whht = matmul(MatrixRef(W), hht);
+        hadamard_update(W, aht, whht, eps);
+        DenseMatrix wtw = gram_t(MatrixRef(W));
+        DenseMatrix wta(k, n);
+        matmul_ta_acc(MatrixRef(W), MatrixRef(A), wta);
+        DenseMatrix wtwh = matmul(MatrixRef(wtw), H);
+        hadamard_update(H, wta, wtwh, eps);
+        std::memcpy(w, W.data(), W.size() * sizeof(double));
+        std::memcpy(h, H.data(), H.size() * sizeof(double));
+    });
+}
+
 // Partition plan: writes per-rank [row_begin,row_end,col_begin,col_end] and batch ranges.
 int ref_make_plan(std::uint64_t m, std::uint64_t n, std::uint64_t k, int n_workers,
                   std::uint64_t n_b, int strategy, std::uint64_t* slabs4, std::uint64_t* batches2,

@@ -59,6 +59,8 @@ _SIGS = {
     "oocnmf_host_register": ([vp, u64], C.c_int),
     "oocnmf_host_unregister": ([vp], C.c_int),
     "oocnmf_download_dense_f32": ([vp, vp], C.c_int),
+    "oocnmf_csr_nnz": ([vp, pu], C.c_int),
+    "oocnmf_download_csr": ([vp, pu, pu, pd], C.c_int),
     "oocnmf_set_factors_f64": ([vp, pd, pd], C.c_int),
     "oocnmf_get_factors_f64": ([vp, pd, pd], C.c_int),
     "oocnmf_gather_w_f64": ([vp, pd], C.c_int),

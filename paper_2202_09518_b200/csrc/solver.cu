@@ -901,6 +901,28 @@ int oocnmf_download_dense_f32(oocnmf_ctx* c, float* a) {
     });
 }
 
+int oocnmf_csr_nnz(oocnmf_ctx* c, uint64_t* nnz) {
+    return guarded([&] {
+        if (c->kind != Kind::csr) fail(OOCNMF_ERR_SHAPE, "no CSR A resident in HBM");
+        *nnz = uint64_t(c->nnz);
+    });
+}
+
+int oocnmf_download_csr(oocnmf_ctx* c, uint64_t* row_ptr, uint64_t* col_idx, double* vals) {
+    return guarded([&] {
+        set_dev(c);
+        if (c->kind != Kind::csr) fail(OOCNMF_ERR_SHAPE, "no CSR A resident in HBM");
+        std::vector<int64_t> rp(c->rows + 1);
+        std::vector<int32_t> ci(size_t(std::max<int64_t>(c->nnz, 1)));
+        std::vector<float> v(ci.size());
+        ck(cudaMemcpy(rp.data(), c->rp.p, rp.size() * 8, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(ci.data(), c->ci.p, ci.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+        ck(cudaMemcpy(v.data(), c->v.p, v.size() * 4, cudaMemcpyDeviceToHost), "D2H");
+        for (size_t i = 0; i < rp.size(); ++i) row_ptr[i] = uint64_t(rp[i]);
+        for (int64_t p = 0; p < c->nnz; ++p) col_idx[p] = uint64_t(ci[p]), vals[p] = double(v[p]);
+    });
+}
+
 int oocnmf_set_factors_f64(oocnmf_ctx* c, const double* w, const double* h) {
     return guarded([&] {
         set_dev(c);

@@ -292,6 +292,15 @@ class Context:
     def generate_csr_uniform(self, density, seed):
         check(_capi.lib().oocnmf_generate_csr_uniform(self._h, density, seed))
 
+    def download_csr(self) -> CsrMatrix:
+        nnz = C.c_uint64()
+        check(_capi.lib().oocnmf_csr_nnz(self._h, C.byref(nnz)))
+        rp = np.empty(self.rows + 1, np.uint64)
+        ci = np.empty(max(nnz.value, 1), np.uint64)
+        v = np.empty(max(nnz.value, 1))
+        check(_capi.lib().oocnmf_download_csr(self._h, _p(rp, C.c_uint64), _p(ci, C.c_uint64), _p(v, C.c_double)))
+        return CsrMatrix(self.rows, self.n, rp, ci[:nnz.value], v[:nnz.value])
+
     def attach_host(self, a: np.ndarray, batch_rows: int = 0):
         """Out-of-core: ``a`` (rows x n float32, ideally pinned) stays in host memory."""
         if a.dtype != np.float32 or a.shape != (self.rows, self.n) or not a.flags.c_contiguous:
