@@ -38,7 +38,7 @@ __global__ void __launch_bounds__(kFuThreads)
     extern __shared__ __align__(16) unsigned char fu_smem[];
     double* red = reinterpret_cast<double*>(fu_smem);
     float* Gs = reinterpret_cast<float*>(red + kFuThreads);
-    float* Fs = Gs + KP * KP;
+    double* Fs = reinterpret_cast<double*>(Gs + KP * KP);
     const int tid = threadIdx.x;
     if (update)
         for (int e = tid; e < KP * KP; e += kFuThreads) Gs[e] = G[e];
@@ -125,18 +125,21 @@ __global__ void __launch_bounds__(kFuThreads)
             }
         }
         // Gram partial of this tile: entries (i <= j), ascending rows.
+        // Rows go to smem already widened to f64 (f32 x f32 products are exact in f64); each
+        // thread then runs NE independent accumulation chains over the 128 rows (rows outer),
+        // so the f64 FMA latency is hidden by ILP instead of serialising 128-long chains.
 #pragma unroll
-        for (int j = 0; j < KP; ++j) Fs[tid * FS + j] = f[j];
+        for (int j = 0; j < KP; ++j) Fs[tid * FS + j] = double(f[j]);
         __syncthreads();
+        {
+            // thread t owns entries e = t + 128 q: column j = e % KP, rows i = e / KP
+            const int j0 = tid % KP;
+            for (int r = 0; r < kTile; ++r) {
+                const double fj = Fs[r * FS + j0];
 #pragma unroll
-        for (int q = 0; q < NE; ++q) {
-            const int e = tid + q * kFuThreads;
-            if (e < KP * KP) {
-                const int i = e / KP, j = e % KP;
-                if (i <= j) {
-                    double s = gacc[q];  // f32 x f32 products are exact in f64
-                    for (int r = 0; r < kTile; ++r) s = fma(double(Fs[r * FS + i]), double(Fs[r * FS + j]), s);
-                    gacc[q] = s;
+                for (int q = 0; q < NE; ++q) {
+                    const int e = tid + q * kFuThreads;
+                    if (e < KP * KP) gacc[q] = fma(Fs[r * FS + e / KP], fj, gacc[q]);
                 }
             }
         }
@@ -228,8 +231,8 @@ cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_
     StreamK skv = sk ? *sk : StreamK{};
 #define OOC_FU(K)                                                                              \
     case K: {                                                                                  \
-        const int smem =                                                                       \
-            int(kFuThreads * sizeof(double) + (K * K + kFuThreads * (K + 1)) * sizeof(float)); \
+        const int smem = int(kFuThreads * sizeof(double) + K * K * sizeof(float) +            \
+                             kFuThreads * (K + 1) * sizeof(double));                           \
         cudaError_t e = cudaFuncSetAttribute(                                                  \
             k_factor_update<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
         if (e != cudaSuccess) return e;                                                        \

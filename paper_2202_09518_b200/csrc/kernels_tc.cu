@@ -68,6 +68,11 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         "l"(map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z), "l"(policy)
         : "memory");
 }
+__device__ __forceinline__ bool elect_one() {
+    uint32_t p = 0;
+    asm volatile("{\n .reg .pred q;\n elect.sync _|q, 0xffffffff;\n selp.u32 %0, 1, 0, q;\n}" : "=r"(p));
+    return p != 0;
+}
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
@@ -247,15 +252,18 @@ __global__ void __launch_bounds__(256, 1)
             for (bool first = true; u < seg_end; ++u, first = false) {
                 mbar_wait(split + s, ph);  // implies full[s]: the split warps waited on it
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a0 = smem_u32(stage_ptr(s));
-                    const uint32_t b0 = a0 + C::A_BYTES;
-                    const uint32_t alo = tmem + uint32_t(C::ALO_COL0 + C::BK * s);
+                // Descriptors are built warp-uniformly (uniform registers) once per stage; the
+                // K steps only add the start-address offset (>> 4) to the low word.
+                const uint32_t a0 = smem_u32(stage_ptr(s));
+                const uint64_t da0 = PASS == 1 ? desc_kmajor(a0, 0) : desc_mnmajor(a0, 0, C::ATOM_STRIDE);
+                const uint64_t db0 = desc_mnmajor(a0 + C::A_BYTES, 0, C::ATOM_STRIDE);  // [hi atoms | lo atoms]
+                const uint32_t alo = tmem + uint32_t(C::ALO_COL0 + C::BK * s);
+                if (elect_one()) {
 #pragma unroll
                     for (int kk = 0; kk < C::KSTEPS; ++kk) {
-                        const uint64_t da = PASS == 1 ? desc_kmajor(a0 + (kk >> 2) * 16384, kk & 3)
-                                                      : desc_mnmajor(a0, kk, C::ATOM_STRIDE);
-                        const uint64_t db = desc_mnmajor(b0, kk, C::ATOM_STRIDE);  // [hi atoms | lo atoms]
+                        const uint64_t da =
+                            da0 + uint64_t(PASS == 1 ? (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4) : kk * 64);
+                        const uint64_t db = db0 + uint64_t(kk * 64);
                         mma_ss(d, da, db, C::IDESC_SS, (first && kk == 0) ? 0u : 1u);
                         mma_ts(d, alo + 8 * kk, db, C::IDESC_TS, 1u);
                     }
