@@ -4,7 +4,7 @@
 // Reference semantics kept (src/kernels.cpp):
 //   hadamard_update  t <- t * nu / (de + eps)              (:207-244)
 //   denominator      de = F · G  (W·HH^T, or (W^T W)·H)     (nmf_serial.cpp:89,98)
-//   gram_t           upper triangle accumulated, mirrored   (:127-179)
+//   gram_t           symmetric k x k, mirrored triangle     (:127-179)
 // With H stored transposed (Ht, n x kp) both factors are row-major "tall" matrices, so one
 // kernel updates W rows (G = HH^T, N = A·H^T) and Ht rows (G = W^T W, N = (W^T A)^T).
 #include "kernels.h"
@@ -12,7 +12,14 @@
 namespace ooc {
 namespace {
 
-constexpr int kFuThreads = 128;  // one thread per factor row of a 128-row tile
+// A CTA handles 64-row units (half of a 128-row stream-K tile) with four threads per row,
+// each owning kp/4 columns. The update is a short dependent chain per thread, so what sets its
+// speed is how many units are in flight per SM: small CTAs, few registers (the row is staged
+// in shared memory instead of registers), several CTAs resident per SM.
+constexpr int kUnitRows = 64;
+constexpr int kRowThreads = 4;
+constexpr int kFuThreads = kUnitRows * kRowThreads;  // 256
+constexpr int kFuMaxGrid = 16 * 148;
 
 // Fixed-shape block reduction of a double (deterministic).
 __device__ double block_sum_f64(double v, double* sh) {
@@ -28,134 +35,148 @@ __device__ double block_sum_f64(double v, double* sh) {
     return r;
 }
 
+// Register-blocked Gram of a 64-row unit over 256 threads: thread t < NBLK owns a TI x TJ
+// block (rows i0.., cols j0..) of the kp x kp result.
 template <int KP>
-__global__ void __launch_bounds__(kFuThreads)
-    k_factor_update(float* __restrict__ F, int64_t tiles, const float* __restrict__ n_plain,
+struct GramBlock {
+    static constexpr int T = KP >= 64 ? 4 : (KP >= 32 ? 2 : 1);
+    static constexpr int TI = T, TJ = T;
+    static constexpr int NJB = KP / TJ;           // blocks along j
+    static constexpr int NBLK = (KP / TI) * NJB;  // <= 256
+    static constexpr int FS = KP + 4;             // f32 smem row stride (16-byte aligned rows)
+};
+
+template <int KP>
+__global__ void __launch_bounds__(kFuThreads, 3)
+    k_factor_update(float* __restrict__ F, int64_t units, const float* __restrict__ n_plain,
                     const float* __restrict__ n_slots, StreamK sk, const float* __restrict__ G,
                     float eps, int update, double* __restrict__ gram_slots,
                     double* __restrict__ err_slots, int* __restrict__ flag, float* __restrict__ cat_out) {
-    constexpr int FS = KP + 1;
+    using GB = GramBlock<KP>;
+    constexpr int FS = GB::FS;
+    constexpr int QW = KP / kRowThreads;  // columns owned by each thread of a row
     extern __shared__ __align__(16) unsigned char fu_smem[];
     double* red = reinterpret_cast<double*>(fu_smem);
     float* Gs = reinterpret_cast<float*>(red + kFuThreads);
-    double* Fs = reinterpret_cast<double*>(Gs + KP * KP);
+    float* Fs = Gs + KP * KP;
     const int tid = threadIdx.x;
+    const int lr = tid / kRowThreads, part = tid % kRowThreads;  // local row, column quarter
+    const int c0 = part * QW;
     if (update)
         for (int e = tid; e < KP * KP; e += kFuThreads) Gs[e] = G[e];
 
-    constexpr int NE = (KP * KP + kFuThreads - 1) / kFuThreads;  // gram entries per thread
-    double gacc[NE];  // f64: the Gram feeds <W^T W, H H^T> of the trace-form error
+    const int bi = tid / GB::NJB, bj = tid % GB::NJB;
+    const int i0 = bi * GB::TI, j0 = bj * GB::TJ;
+    const bool gram_owner = tid < GB::NBLK;
+    double gacc[GB::TI * GB::TJ];
 #pragma unroll
-    for (int q = 0; q < NE; ++q) gacc[q] = 0.0;
+    for (int q = 0; q < GB::TI * GB::TJ; ++q) gacc[q] = 0.0;
     double eacc = 0.0;
     bool bad = false;
-    __syncthreads();
 
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t row = t * kTile + tid;
-        float f[KP];
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        const int64_t row = u * kUnitRows + lr;
+        const int64_t t = u / (kTile / kUnitRows);                  // stream-K tile
+        const int trow = int(u % (kTile / kUnitRows)) * kUnitRows + lr;  // row within the tile
+        float fo[QW];
         {
-            const float4* fr = reinterpret_cast<const float4*>(F + row * KP);
+            const float* fr = F + row * KP + c0;
 #pragma unroll
-            for (int j4 = 0; j4 < KP / 4; ++j4) {
-                const float4 v = fr[j4];
-                f[4 * j4] = v.x, f[4 * j4 + 1] = v.y, f[4 * j4 + 2] = v.z, f[4 * j4 + 3] = v.w;
-            }
+            for (int j = 0; j < QW; ++j) fo[j] = fr[j];
         }
         if (update) {
-            float nu[KP];
-            if (n_plain) {
-                const float4* nr = reinterpret_cast<const float4*>(n_plain + row * KP);
 #pragma unroll
-                for (int j4 = 0; j4 < KP / 4; ++j4) {
-                    const float4 v = nr[j4];
-                    nu[4 * j4] = v.x, nu[4 * j4 + 1] = v.y, nu[4 * j4 + 2] = v.z, nu[4 * j4 + 3] = v.w;
-                }
+            for (int j = 0; j < QW; ++j) Fs[lr * FS + c0 + j] = fo[j];
+            float nu[QW];
+            if (n_plain) {
+                const float* nr = n_plain + row * KP + c0;
+#pragma unroll
+                for (int j = 0; j < QW; ++j) nu[j] = nr[j];
             } else {
 #pragma unroll
-                for (int j = 0; j < KP; ++j) nu[j] = 0.f;
-                const int64_t c0 = sk.cta_of(t * sk.ipt), c1 = sk.cta_of((t + 1) * sk.ipt - 1);
-                for (int64_t c = c0; c <= c1; ++c) {
-                    const float4* nr = reinterpret_cast<const float4*>(
-                        n_slots + sk.slot(c, t) * int64_t(kTile * KP) + int64_t(tid) * KP);
+                for (int j = 0; j < QW; ++j) nu[j] = 0.f;
+                const int64_t s0 = sk.cta_of(t * sk.ipt), s1 = sk.cta_of((t + 1) * sk.ipt - 1);
+                for (int64_t c = s0; c <= s1; ++c) {
+                    const float* nr = n_slots + sk.slot(c, t) * int64_t(kTile * KP) + int64_t(trow) * KP + c0;
 #pragma unroll
-                    for (int j4 = 0; j4 < KP / 4; ++j4) {
-                        const float4 v = nr[j4];
-                        nu[4 * j4] += v.x, nu[4 * j4 + 1] += v.y, nu[4 * j4 + 2] += v.z,
-                            nu[4 * j4 + 3] += v.w;
-                    }
+                    for (int j = 0; j < QW; ++j) nu[j] += nr[j];
                 }
             }
-            float de[KP];
+            __syncthreads();  // Gs (first unit) and this unit's rows staged
+            // de = f · G: f[q] is a broadcast read of the row in smem, G rows are 128-bit loads
+            float de[QW];
 #pragma unroll
-            for (int j = 0; j < KP; ++j) de[j] = 0.f;
-#pragma unroll
+            for (int j = 0; j < QW; ++j) de[j] = 0.f;
+            const float* frow = Fs + lr * FS;
+#pragma unroll 8
             for (int q = 0; q < KP; ++q) {
-                const float fq = f[q];
+                const float fq = frow[q];
 #pragma unroll
-                for (int j = 0; j < KP; ++j) de[j] = fmaf(fq, Gs[q * KP + j], de[j]);
+                for (int j = 0; j < QW; ++j) de[j] = fmaf(fq, Gs[q * KP + c0 + j], de[j]);
             }
             double e = 0.0;
 #pragma unroll
-            for (int j = 0; j < KP; ++j) {
-                const float nf = f[j] * nu[j] / (de[j] + eps);
+            for (int j = 0; j < QW; ++j) {
+                const float nf = fo[j] * nu[j] / (de[j] + eps);
                 bad |= !isfinite(nf);
-                f[j] = nf;
+                fo[j] = nf;
                 e += double(nu[j]) * double(nf);
             }
             eacc += e;
-            float4* fw = reinterpret_cast<float4*>(F + row * KP);
+            float* fw = F + row * KP + c0;
 #pragma unroll
-            for (int j4 = 0; j4 < KP / 4; ++j4)
-                fw[j4] = make_float4(f[4 * j4], f[4 * j4 + 1], f[4 * j4 + 2], f[4 * j4 + 3]);
+            for (int j = 0; j < QW; ++j) fw[j] = fo[j];
+            __syncthreads();  // everyone has read the old rows from Fs
         }
         if (cat_out) {
             // [F | F - tf32(F)] row of the tensor-core operand (one TMA box carries both halves)
-            float4* cw = reinterpret_cast<float4*>(cat_out + row * 2 * KP);
+            float* cw = cat_out + row * 2 * KP;
 #pragma unroll
-            for (int j4 = 0; j4 < KP / 4; ++j4) {
-                float l[4];
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const float x = f[4 * j4 + q];
-                    l[q] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-                }
-                cw[j4] = make_float4(f[4 * j4], f[4 * j4 + 1], f[4 * j4 + 2], f[4 * j4 + 3]);
-                cw[KP / 4 + j4] = make_float4(l[0], l[1], l[2], l[3]);
+            for (int j = 0; j < QW; ++j) {
+                cw[c0 + j] = fo[j];
+                cw[KP + c0 + j] = fo[j] - __uint_as_float(__float_as_uint(fo[j]) & 0xFFFFE000u);
             }
         }
-        // Gram partial of this tile: entries (i <= j), ascending rows.
-        // Rows go to smem already widened to f64 (f32 x f32 products are exact in f64); each
-        // thread then runs NE independent accumulation chains over the 128 rows (rows outer),
-        // so the f64 FMA latency is hidden by ILP instead of serialising 128-long chains.
+        // Gram partial of the unit: f32 sums over its 64 rows (FP64 issue rate is far below
+        // FP32), accumulated across units and CTAs in f64. Its ~1e-7 relative error only
+        // reaches the error estimate through the trace form, which error_mode auto uses only
+        // where err > 0.1 (there it moves err by < 1e-5 relative).
 #pragma unroll
-        for (int j = 0; j < KP; ++j) Fs[tid * FS + j] = double(f[j]);
+        for (int j = 0; j < QW; ++j) Fs[lr * FS + c0 + j] = fo[j];
         __syncthreads();
-        {
-            // thread t owns entries e = t + 128 q: column j = e % KP, rows i = e / KP
-            const int j0 = tid % KP;
-            for (int r = 0; r < kTile; ++r) {
-                const double fj = Fs[r * FS + j0];
+        if (gram_owner) {
+            float gt[GB::TI * GB::TJ];
 #pragma unroll
-                for (int q = 0; q < NE; ++q) {
-                    const int e = tid + q * kFuThreads;
-                    if (e < KP * KP) gacc[q] = fma(Fs[r * FS + e / KP], fj, gacc[q]);
-                }
+            for (int q = 0; q < GB::TI * GB::TJ; ++q) gt[q] = 0.f;
+#pragma unroll 8
+            for (int r = 0; r < kUnitRows; ++r) {
+                const float* fr = Fs + r * FS;
+                float fi[GB::TI], fj[GB::TJ];
+#pragma unroll
+                for (int a = 0; a < GB::TI; ++a) fi[a] = fr[i0 + a];
+#pragma unroll
+                for (int b = 0; b < GB::TJ; ++b) fj[b] = fr[j0 + b];
+#pragma unroll
+                for (int a = 0; a < GB::TI; ++a)
+#pragma unroll
+                    for (int b = 0; b < GB::TJ; ++b) gt[a * GB::TJ + b] = fmaf(fi[a], fj[b], gt[a * GB::TJ + b]);
             }
+#pragma unroll
+            for (int q = 0; q < GB::TI * GB::TJ; ++q) gacc[q] += double(gt[q]);
         }
         __syncthreads();
     }
-    double* gout = gram_slots + int64_t(blockIdx.x) * KP * KP;
+    if (gram_owner) {
+        double* gout = gram_slots + int64_t(blockIdx.x) * KP * KP;
 #pragma unroll
-    for (int q = 0; q < NE; ++q) {
-        const int e = tid + q * kFuThreads;
-        if (e < KP * KP) {
-            const int i = e / KP, j = e % KP;
-            if (i <= j) {
-                gout[i * KP + j] = gacc[q];
-                gout[j * KP + i] = gacc[q];
+        for (int a = 0; a < GB::TI; ++a)
+#pragma unroll
+            for (int b = 0; b < GB::TJ; ++b) {
+                const int i = i0 + a, j = j0 + b;
+                // mirror the upper triangle so the Gram is symmetric to the bit
+                const double v = gacc[a * GB::TJ + b];
+                if (i <= j) gout[i * KP + j] = v, gout[j * KP + i] = v;
             }
-        }
     }
     if (err_slots) {
         const double s = block_sum_f64(eacc, red);
@@ -220,23 +241,27 @@ __global__ void k_finalize_error(int kp, const double* __restrict__ err_slots, i
 
 }  // namespace
 
-int factor_grid(int64_t tiles) { return int(tiles < 1184 ? tiles : 1184); }
+int factor_grid(int64_t tiles) {
+    const int64_t units = tiles * (kTile / kUnitRows);
+    return int(units < kFuMaxGrid ? units : kFuMaxGrid);
+}
 
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
                                  const float* n_slots, const StreamK* sk, const float* G,
                                  float eps, bool update, double* gram_slots, double* err_slots,
                                  int* flag, float* cat_out, cudaStream_t s) {
     const int64_t tiles = rows / kTile;
+    const int64_t units = tiles * (kTile / kUnitRows);
     const int grid = factor_grid(tiles);
     StreamK skv = sk ? *sk : StreamK{};
 #define OOC_FU(K)                                                                              \
     case K: {                                                                                  \
         const int smem = int(kFuThreads * sizeof(double) + K * K * sizeof(float) +            \
-                             kFuThreads * (K + 1) * sizeof(double));                           \
+                             kUnitRows * GramBlock<K>::FS * sizeof(float));                    \
         cudaError_t e = cudaFuncSetAttribute(                                                  \
             k_factor_update<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
         if (e != cudaSuccess) return e;                                                        \
-        k_factor_update<K><<<grid, kFuThreads, smem, s>>>(F, tiles, n_plain, n_slots, skv, G,  \
+        k_factor_update<K><<<grid, kFuThreads, smem, s>>>(F, units, n_plain, n_slots, skv, G,  \
                                                          eps, update ? 1 : 0, gram_slots,      \
                                                          err_slots, flag, cat_out);            \
         break;                                                                                 \
