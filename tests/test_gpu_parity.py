@@ -36,8 +36,11 @@ def check_parity(res, trace_iters, trace_err, w=None, h=None):
     got_it = np.array([i for i, _ in res.error_trace])
     got = np.array([e for _, e in res.error_trace])
     assert np.array_equal(got_it, np.asarray(trace_iters)), (got_it, trace_iters)
-    rel = np.max(np.abs(got - trace_err) / np.asarray(trace_err))
-    assert rel <= TRACE_TOL, f"trace rel diff {rel:.3e}"
+    # 1e-4 relative, floored at 1e-6 absolute: an exactly factorisable input drives the f64
+    # reference to ~1e-12, below the f32 representation floor (~1e-7) of any f32 solver.
+    ref = np.asarray(trace_err)
+    assert np.all(np.abs(got - ref) <= np.maximum(TRACE_TOL * ref, 1e-6)), (got, ref)
+    rel = np.max(np.abs(got - ref) / np.maximum(ref, 1e-2))
     if w is not None:
         assert rel_fro(res.w, w) <= FACTOR_TOL, f"W rel {rel_fro(res.w, w):.3e}"
         assert rel_fro(res.h, h) <= FACTOR_TOL, f"H rel {rel_fro(res.h, h):.3e}"
@@ -316,3 +319,62 @@ def test_cpp_host_core_is_a_drop_in(gpu):
     norms = [d for d in lines if "w_fro" in d][0]
     assert norms["w_fro"] == pytest.approx(np.linalg.norm(ref.w), rel=FACTOR_TOL)
     assert any(d.get("shape_error") for d in lines)
+
+
+# ---------------------------------------------------------------------------- edge cases
+@pytest.mark.parametrize("m,n,k", [(1, 1, 1), (2, 3, 1), (3, 2, 2), (130, 1, 1), (1, 300, 1), (5, 7, 9)])
+def test_tiny_and_degenerate_shapes(gpu, m, n, k):
+    a = (port.uniform_dense(m, n, 4, 99) + 0.1).astype(np.float32)
+    w0, h0 = port.init_factors(m, n, k, 3)
+    ref = port.nmf_serial(f32(a), k, f32(w0), f32(h0), max_iters=12, interval=4)
+    res = solve_from(a, k, 12, 4, seed=3)
+    check_parity(res, ref.trace_iters, ref.trace_err, ref.w, ref.h)
+
+
+def test_csr_with_empty_rows_and_columns(gpu):
+    m, n, k = 300, 260, 8
+    d = port.uniform_dense(m, n, 6, 99)
+    d[d < 0.9] = 0.0
+    d[10:40] = 0.0          # empty rows
+    d[:, 100:150] = 0.0     # empty columns
+    c = nmf.CsrMatrix.from_dense(f32(d))
+    w0, h0 = port.init_factors(m, n, k, 0)
+    ref = port.nmf_serial((c.row_ptr, c.col_idx, c.values, (m, n)), k, f32(w0), f32(h0), max_iters=20, interval=5)
+    cfg = nmf.NmfConfig(k=k, max_iters=20, error_check_interval=5, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    res = nmf.nmf_serial(c, cfg)
+    check_parity(res, ref.trace_iters, ref.trace_err, ref.w, ref.h)
+    # rows of W with an empty A row go to zero after one update (0 * x / (y + eps))
+    assert np.all(res.w[10:40] == 0)
+
+
+def test_out_of_core_batch_larger_than_slab_and_ragged_last_batch(gpu):
+    m, n, k = 333, 200, 32
+    a = port.uniform_dense(m, n, 9, 99).astype(np.float32)
+    w0, h0 = port.init_factors(m, n, k, 0)
+    ref = port.nmf_serial(f32(a), k, f32(w0), f32(h0), max_iters=10, interval=5)
+    for br in (128, 256, 4096):
+        with nmf.Context(gpu) as ctx:
+            ctx.set_problem(m, n, k)
+            ctx.attach_host(a, batch_rows=br)
+            ctx.set_factors(f32(w0), f32(h0))
+            tr, _ = ctx.solve(nmf.NmfConfig(k=k, max_iters=10, error_check_interval=5, eta=0.0,
+                                            init=nmf.FactorInit.from_files, init_w=f32(w0), init_h=f32(h0)))
+            w, h = ctx.get_factors()
+        np.testing.assert_allclose([e for _, e in tr], ref.trace_err, rtol=TRACE_TOL)
+        assert rel_fro(w, ref.w) < FACTOR_TOL and rel_fro(h, ref.h) < FACTOR_TOL
+
+
+def test_resident_warm_restart_continues_trajectory(gpu):
+    a = port.uniform_dense(400, 300, 2, 99).astype(np.float32)
+    w0, h0 = port.init_factors(400, 300, 16, 0)
+    ref = port.nmf_serial(f32(a), 16, f32(w0), f32(h0), max_iters=20, interval=10)
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(400, 300, 16)
+        ctx.load_dense(a)
+        ctx.set_factors(f32(w0), f32(h0))
+        ctx.solve(nmf.NmfConfig(k=16, max_iters=10, error_check_interval=10, eta=0.0,
+                                init=nmf.FactorInit.from_files, init_w=f32(w0), init_h=f32(h0)))
+        tr, _ = ctx.solve(nmf.NmfConfig(k=16, max_iters=10, error_check_interval=10, eta=0.0,
+                                        init=nmf.FactorInit.resident))
+    assert tr[0][1] == pytest.approx(ref.trace_err[1], rel=TRACE_TOL)
