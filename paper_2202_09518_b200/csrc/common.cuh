@@ -65,6 +65,18 @@ struct StreamK {
 };
 
 // ---------------------------------------------------------------------------
+// 3xTF32 split: x = hi + lo + r with hi = trunc_tf32(x) (what the tensor core reads from a
+// raw f32 operand) and lo = rna_tf32(x - hi). Rounding lo to nearest (instead of letting the
+// MMA truncate it) keeps the residual r (|r| <= 2^-21 |x|) unbiased, so it averages out over
+// the long K reductions instead of accumulating a one-signed bias.
+__device__ __forceinline__ float tf32_lo(float x) {
+    const float rem = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(rem));
+    return __uint_as_float(r);
+}
+
+// ---------------------------------------------------------------------------
 // small PTX helpers
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

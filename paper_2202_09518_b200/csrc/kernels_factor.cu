@@ -134,7 +134,7 @@ __global__ void __launch_bounds__(kFuThreads, 3)
 #pragma unroll
             for (int j = 0; j < QW; ++j) {
                 cw[c0 + j] = fo[j];
-                cw[KP + c0 + j] = fo[j] - __uint_as_float(__float_as_uint(fo[j]) & 0xFFFFE000u);
+                cw[KP + c0 + j] = tf32_lo(fo[j]);
             }
         }
         // Gram partial of the unit: f32 sums over its 64 rows (FP64 issue rate is far below

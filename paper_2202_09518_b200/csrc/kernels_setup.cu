@@ -149,7 +149,7 @@ __global__ void k_split_cat(const float* __restrict__ F, float* __restrict__ cat
         const int64_t r = q / kp, j = q % kp;
         const float v = F[q];
         cat[r * 2 * kp + j] = v;
-        cat[r * 2 * kp + kp + j] = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        cat[r * 2 * kp + kp + j] = tf32_lo(v);
     }
 }
 

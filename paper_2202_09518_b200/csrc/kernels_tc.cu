@@ -1,36 +1,45 @@
-// Tensor-core (tcgen05, kind::tf32) streaming passes for kp in {32, 64}.
+// Tensor-core (tcgen05, kind::tf32) streaming passes for kp in {16, 32, 64}.
 //
 // At k = 32 an A-pass needs 16 flop per byte of A; CUDA-core FFMA tops out near 70% of the
 // HBM roofline there (SURVEY.md §7 hard part 1), so the contractions move to the 5th-gen
 // tensor cores. Single-pass TF32 fails the 1e-4 trace parity, so each tile runs the
 // split-precision "3xTF32" scheme
 //     A·B ≈ A_hi·B_hi + A_hi·B_lo + A_lo·B_hi,   x_hi = tf32(x) (hardware truncation),
-//                                                x_lo = x - x_hi (exact in f32)
-// arranged so the streamed A tile is read from shared memory only once per K step:
-//   MMA 1 (SS): D'[:, 0:2kp] += A_hi(smem) · [B_hi | B_lo](smem)     one N = 2kp MMA
-//   MMA 2 (TS): D'[:, 0:kp]  += A_lo(TMEM) · B_hi(smem)              A_lo never touches smem
-//   epilogue:   D = D'[:, 0:kp] + D'[:, kp:2kp]
-// A_hi is the raw f32 tile TMA lands in shared memory (the MMA reads only its tf32 bits);
-// A_lo is produced by four "split" warps that read the tile and tcgen05.st the low halves
-// straight into TMEM in the K-major operand layout (transposing for pass 2); B_lo
-// (Ht_lo / W_lo) is written by the factor-update kernel that produced B.
+//                                                x_lo = rna_tf32(x - x_hi) (common.cuh tf32_lo)
+// with both A halves in TMEM (the split warps tcgen05.st them there, transposing for pass 2)
+// and [B_hi | B_lo] in shared memory (B_lo written by the factor-update kernel):
+//   kp >= 32:  hi chain  H  += A_hi · B_hi              (N = kp)
+//              lo chain  L  += A_hi · B_lo + A_lo · B_hi (2 x N = kp)
+//   kp = 16:   D' = [H | L]: one N = 32 MMA A_hi · [B_hi | B_lo] plus A_lo · B_hi into L
 //
-// Pipeline (one persistent CTA per SM, stream-K split as the FFMA path):
-//   warp 0      TMA producer: A tile + B_hi + B_lo per stage                 -> full[s]
-//   warps 4..7  split: A_lo[s] -> TMEM                                        -> split[s]
-//   warp 1      MMA issuer; commit -> empty[s] (smem stage + TMEM A_lo slot free) and, at
-//               a tile end, -> accfull[b]
-//   warps 4..7  epilogue at tile ends: tcgen05.ld the 128 x 2kp accumulator -> slot -> accempty[b]
+// Numerics (tools/bias_probe.py, signed mean relative error of A·Ht vs f64): the tensor
+// core's f32 accumulation truncates once per MMA, so one TMEM accumulator carried through a
+// tile's whole K range biased the products by -1e-5..-4e-5 — enough to drift low-rank
+// trajectories past the 1e-4 parity bar. The hi chain therefore restarts every K step (64,
+// 8 MMAs) in a fresh TMEM buffer that drain warps add into round-to-nearest f32 register
+// sums; the lo chain (values ~2^-11 of H, so its own truncation is negligible) restarts every
+// LO_UNITS steps. The remaining bias is a constant ~-3e-7 for any K (FFMA path: unbiased,
+// rms 5e-8..1.3e-7); OOCNMF_TC_DRAIN=n lengthens the hi chain to n steps (developer knob).
 //
-// pass 1 (A·Ht):  D[128 rows x kp] += A[rows, 32 cols] · Ht[32 cols, kp]
-//                 A K-major (row-major A tile), B MN-major (Ht is n x kp).
-// pass 2 (A^T·W): D[128 cols x kp] += A^T[128 cols, 32 rows] · W[32 rows, kp]
-//                 A MN-major (4 atoms of 32 columns), B MN-major.
-// Swizzles (verified on B200 with tools/tc_micro*.cu): K-major tf32 operands use
-// SWIZZLE_128B (TMA SWIZZLE_128B); MN-major tf32 operands must use SWIZZLE_128B_BASE32B
-// (TMA SWIZZLE_128B_ATOM_32B) — with the plain 128B swizzle the MMA reads zeros.
+// Pipeline (one persistent CTA per SM, 16 warps, stream-K split as the FFMA path):
+//   warp 0       TMA producer: A ring (32 KB stages, freed by the split warps as soon as the
+//                tile is in TMEM) and B ring ([B_hi | B_lo] rows, freed by the MMAs)
+//   warps 4..11  split: A tile -> [A_hi | A_lo] TMEM slot (two warpgroups, one K half each)
+//   warp 1       MMA issuer (elect.sync, uniform descriptors); commits free B stages and
+//                A slots and signal closed hi / lo chains
+//   warps 12..15 drain: closed chains -> f32 row sums; at a tile end, row sums -> slot
+//
+// pass 1 (A·Ht):  D[128 rows x kp] += A[rows, 64 cols] · Ht[64 cols, kp]
+//                 A tile row-major (TMA 128B swizzle), B MN-major (Ht is n x kp).
+// pass 2 (A^T·W): D[128 cols x kp] += A^T[128 cols, 64 rows] · W[64 rows, kp]
+//                 A tile as 4 MN atoms of 32 columns, B MN-major.
+// Swizzles (verified on B200 with tools/tc_micro*.cu): MN-major tf32 operands must use
+// SWIZZLE_128B_BASE32B (TMA SWIZZLE_128B_ATOM_32B) — with the plain 128B swizzle the MMA
+// reads zeros.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+
+#include <cstdlib>
 
 #include "kernels.h"
 
@@ -48,13 +57,16 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
+// The suspend-time hint lets a waiting warp sleep until the phase flips instead of spinning:
+// without it the producer / drain / MMA warps' try_wait loops took ~30% of all issued
+// instructions (ncu source page) from the split warps that share their SM sub-partitions.
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     uint32_t ok = 0;
     do {
         asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}"
             : "=r"(ok)
-            : "r"(smem_u32(b)), "r"(parity)
+            : "r"(smem_u32(b)), "r"(parity), "r"(0x989680u)
             : "memory");
     } while (!ok);
 }
@@ -76,16 +88,13 @@ __device__ __forceinline__ bool elect_one() {
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 
-// UMMA shared-memory descriptor, version 1 (sm_100). Layout 2 = SWIZZLE_128B (16-byte
-// granules XOR row%8), layout 1 = SWIZZLE_128B_BASE32B (32-byte granules XOR row%4).
-constexpr uint32_t kLayoutSW128 = 2, kLayoutSW128B32 = 1;
+// UMMA shared-memory descriptor, version 1 (sm_100). Layout 1 = SWIZZLE_128B_BASE32B
+// (32-byte granules XOR row%4); (layout 2 = SWIZZLE_128B, 16-byte granules XOR row%8, is
+// what K-major operands would use — A now reaches the MMA through TMEM instead).
+constexpr uint32_t kLayoutSW128B32 = 1;
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
            (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46) | (uint64_t(layout) << 61);
-}
-// K-major, 128-byte rows of K, 8-row swizzle groups; one MMA K step (8 x f32) = +32 B.
-__device__ __forceinline__ uint64_t desc_kmajor(uint32_t base, int kk) {
-    return sdesc(base + kk * 32, 16, 1024, kLayoutSW128);
 }
 // MN-major, 128-byte rows of MN (32 f32), one row per K index, 4-row swizzle groups (512 B),
 // MN atoms of 32 elements every `atom_stride` bytes; one MMA K step (8 rows) = +1024 B.
@@ -96,12 +105,6 @@ __device__ __forceinline__ uint64_t desc_mnmajor(uint32_t base, int kk, uint32_t
 __host__ __device__ constexpr uint32_t idesc_tf32(int n, int a_mn, int b_mn) {
     return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
            (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
-}
-__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-    asm volatile(
-        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
-        "l"(a), "l"(b), "r"(idesc), "r"(acc)
-        : "memory");
 }
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
@@ -137,17 +140,21 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
         : "r"(taddr)
         : "memory");
 }
+// (no wait: the caller issues tmem_st_wait() once after its last store)
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%"
-        "18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};\n\t"
-        "tcgen05.wait::st.sync.aligned;" ::"r"(taddr),
+        "18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
         OOC_W32(r)
         : "memory");
 }
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// tf32_lo(x) as the MMA will read it: adding half a tf32 ulp to the bits of the remainder
+// and letting the tensor core's truncation drop the low 13 bits is round-to-nearest (ties
+// away), one integer add instead of cvt.rna on the split warps' critical path.
 __device__ __forceinline__ uint32_t lo_bits(float x) {
-    return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u));
+    return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)) + 0x1000u;
 }
 
 // ------------------------------------------------------------------ kernel
@@ -158,48 +165,102 @@ template <int KP, int PASS>
 struct TcCfg {
     static constexpr int BK = kTcStep;                          // K per stage
     static constexpr int KSTEPS = BK / 8;                       // tf32 MMA K = 8
-    static constexpr int A_BYTES = 128 * BK * 4;                // 32 KB
-    static constexpr int B_BYTES = BK * 2 * KP * 4;             // [B_hi | B_lo], 16 / 32 KB
-    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int STAGES = KP == 32 ? 4 : 3;
-    static constexpr uint32_t TX_BYTES = STAGE_BYTES;
     static constexpr uint32_t ATOM_STRIDE = BK * 128;           // MN-major atoms: BK rows x 128 B
-    static constexpr int ACC_COLS = 2 * KP;                     // D' = [hi | lo] per accumulator
-    static constexpr int ALO_COL0 = 2 * ACC_COLS;               // A_lo slots after 2 accumulators
-    static constexpr int TMEM_COLS = (ALO_COL0 + STAGES * BK) <= 256 ? 256 : 512;
-    static constexpr size_t SMEM = size_t(STAGES) * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-    static constexpr uint32_t IDESC_SS = idesc_tf32(2 * KP, PASS == 2 ? 1 : 0, 1);  // A_hi · [B_hi|B_lo]
-    static constexpr uint32_t IDESC_TS = idesc_tf32(KP, 0, 1);                       // A_lo(TMEM) · B_hi
+    // Two shared-memory rings. A stages (the streamed 128 x 64 tile) are consumed by the split
+    // warps alone — the MMAs read A_hi / A_lo from TMEM — and are released as soon as they are
+    // split, so a stage's lifetime is HBM latency + split and the ring keeps enough bytes in
+    // flight; B stages ([B_hi | B_lo] factor rows, L2-resident) live until their MMAs retire.
+    static constexpr int A_BYTES = 128 * BK * 4;                // 32 KB
+    static constexpr int B_BYTES = BK * 2 * KP * 4;             // 8 / 16 / 32 KB
+    static constexpr int A_STAGES = KP == 64 ? 4 : (KP == 32 ? 5 : 6);
+    static constexpr int B_STAGES = KP == 64 ? 3 : 4;
+    // SEP (kp >= 32): the large A_hi·B_hi products chain in per-chunk "hi" buffers (kp columns)
+    // drained every chunk; the small A_hi·B_lo + A_lo·B_hi products chain in "lo" buffers
+    // drained every LO_UNITS units, so the per-unit drain reads and adds only kp columns.
+    // kp = 16: one N = 32 MMA writes D' = [hi | lo] and the drain reads both halves.
+    static constexpr bool SEP = KP >= 32;
+    static constexpr int LO_UNITS = 16;
+    static constexpr int ACC_COLS = SEP ? KP : 2 * KP;
+    static constexpr int NBUF = SEP ? 2 : 3;                    // hi (or D') buffers
+    static constexpr int NLO = SEP ? 2 : 0;                     // lo buffers
+    static constexpr int ASLOTS = KP == 64 ? 2 : 3;             // [A_hi | A_lo] operand slots
+    static constexpr int ASLOT_COLS = 2 * BK;
+    static constexpr int LO_COL0 = NBUF * ACC_COLS;
+    static constexpr int A_COL0 = LO_COL0 + NLO * KP;
+    static_assert(A_COL0 + ASLOTS * ASLOT_COLS <= 512, "TMEM budget");
+    static_assert(BK == 64, "two split warpgroups, one 32-wide K half each");
+    static constexpr int TMEM_COLS = (A_COL0 + ASLOTS * ASLOT_COLS) <= 256 ? 256 : 512;
+    static constexpr size_t RING_BYTES = size_t(A_STAGES) * A_BYTES + size_t(B_STAGES) * B_BYTES;
+    static constexpr size_t SMEM = RING_BYTES + 1024 /*align*/ + 512 /*barriers*/;
+    static_assert(SMEM <= 232448, "shared memory budget");
+    // A(TMEM, K-major) · B(MN-major): the hi-chain MMA (N = 2kp writes D' when !SEP) and
+    // the N = kp lo-chain MMAs
+    static constexpr uint32_t IDESC_HI = idesc_tf32(SEP ? KP : 2 * KP, 0, 1);
+    static constexpr uint32_t IDESC_KP = idesc_tf32(KP, 0, 1);
+    static constexpr uint32_t LO_DESC_OFF = SEP ? (KP / 32) * ATOM_STRIDE >> 4 : 0;  // B_lo atoms
+};
+
+// Unit bookkeeping shared by the MMA issuer and the drain warps: which chains close after
+// this unit. Hi chunks are `drain_units` long, lo chunks LO_UNITS; both are cut at tile ends
+// and at the CTA's last unit.
+struct ChainClock {
+    int64_t it;
+    int hu = 0, lu = 0;
+    __device__ void step(int64_t u, int64_t u1, int64_t ipt, int du, int lo_units, bool& tile_end, bool& hi_close,
+                         bool& lo_close) {
+        tile_end = ++it == ipt;
+        if (tile_end) it = 0;
+        const bool cut = tile_end || u + 1 == u1;
+        hi_close = cut || ++hu == du;
+        lo_close = cut || ++lu == lo_units;
+        if (hi_close) hu = 0;
+        if (lo_close) lu = 0;
+    }
 };
 
 template <int KP, int PASS>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(512, 1)
     k_pass_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              float* __restrict__ slots, StreamK sk) {
+              float* __restrict__ slots, StreamK sk, int drain_units) {
     using C = TcCfg<KP, PASS>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
-    uint64_t* full = bars;                     // [STAGES]
-    uint64_t* split = bars + C::STAGES;        // [STAGES]
-    uint64_t* empty = bars + 2 * C::STAGES;    // [STAGES]
-    uint64_t* accfull = bars + 3 * C::STAGES;  // [2]
-    uint64_t* accempty = accfull + 2;          // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + 2);
+    // 1024-byte aligned, derived from the __shared__ array so loads compile to LDS, not LD
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::RING_BYTES);
+    uint64_t* fullA = bars;                      // [A_STAGES]  TMA -> split
+    uint64_t* emptyA = fullA + C::A_STAGES;      // [A_STAGES]  split -> TMA
+    uint64_t* fullB = emptyA + C::A_STAGES;      // [B_STAGES]  TMA -> split / MMA
+    uint64_t* emptyB = fullB + C::B_STAGES;      // [B_STAGES]  MMA -> TMA
+    uint64_t* split = emptyB + C::B_STAGES;      // [ASLOTS]    split -> MMA (A slot + B_lo ready)
+    uint64_t* accfull = split + C::ASLOTS;       // [NBUF]
+    uint64_t* accempty = accfull + C::NBUF;    // [NBUF]
+    uint64_t* afree = accempty + C::NBUF;      // [ASLOTS]
+    uint64_t* lofull = afree + C::ASLOTS;      // [NLO]
+    uint64_t* loempty = lofull + C::NLO;       // [NLO]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(loempty + C::NLO);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int64_t cta = blockIdx.x;
     const int64_t u0 = sk.begin(cta), u1 = sk.begin(cta + 1);
 
     if (tid == 0) {
-        for (int s = 0; s < C::STAGES; ++s) {
-            mbar_init(full + s, 1);
-            mbar_init(split + s, 4);
-            mbar_init(empty + s, 1);
+        for (int s = 0; s < C::A_STAGES; ++s) {
+            mbar_init(fullA + s, 1);
+            mbar_init(emptyA + s, 8);
         }
-        for (int b = 0; b < 2; ++b) {
+        for (int s = 0; s < C::B_STAGES; ++s) {
+            mbar_init(fullB + s, 1);
+            mbar_init(emptyB + s, 1);
+        }
+        for (int r = 0; r < C::ASLOTS; ++r) mbar_init(split + r, 8);
+        for (int b = 0; b < C::NBUF; ++b) {
             mbar_init(accfull + b, 1);
             mbar_init(accempty + b, 4);
+        }
+        for (int r = 0; r < C::ASLOTS; ++r) mbar_init(afree + r, 1);
+        for (int b = 0; b < C::NLO; ++b) {
+            mbar_init(lofull + b, 1);
+            mbar_init(loempty + b, 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -214,90 +275,106 @@ __global__ void __launch_bounds__(256, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    auto stage_ptr = [&](int s) { return smem + s * C::STAGE_BYTES; };
+    auto a_stage = [&](int s) { return smem + s * C::A_BYTES; };
+    auto b_stage = [&](int s) { return smem + C::A_STAGES * C::A_BYTES + s * C::B_BYTES; };
     // Loop-carried ring / tile counters instead of 64-bit divisions per unit.
     if (warp == 0) {
         // ---------------- TMA producer
         if (lane == 0) {
-            int s = 0;
-            uint32_t ph = 0;
+            int sa = 0, sb = 0;
+            uint32_t pha = 0, phb = 0;
             int64_t tile = u0 / sk.ipt, it = u0 % sk.ipt;
             for (int64_t u = u0; u < u1; ++u) {
-                mbar_wait(empty + s, ph ^ 1u);
-                uint8_t* sA = stage_ptr(s);
-                mbar_expect_tx(full + s, C::TX_BYTES);
+                mbar_wait(emptyA + sa, pha ^ 1u);
+                uint8_t* sA = a_stage(sa);
+                mbar_expect_tx(fullA + sa, C::A_BYTES);
                 if (PASS == 1)  // rows [tile*128, +128), K-atoms [2 it, 2 it + 2): atom j -> +16 KB
-                    tma_load_3d(sA, &tmA, full + s, 0, int(tile * 128), int(it * (C::BK / 32)), kEvictFirst);
+                    tma_load_3d(sA, &tmA, fullA + sa, 0, int(tile * 128), int(it * (C::BK / 32)), kEvictFirst);
                 else            // rows [it*64, +64), column atoms [4 tile, +4): atom j -> +8 KB
-                    tma_load_3d(sA, &tmA, full + s, 0, int(it * C::BK), int(tile * 4), kEvictFirst);
+                    tma_load_3d(sA, &tmA, fullA + sa, 0, int(it * C::BK), int(tile * 4), kEvictFirst);
+                if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
                 // factor rows [it*64, +64) of [F | F_lo]: 2kp/32 atoms of 8 KB
-                tma_load_3d(sA + C::A_BYTES, &tmB, full + s, 0, int(it * C::BK), 0, kEvictLast);
-                if (++s == C::STAGES) s = 0, ph ^= 1u;
+                mbar_wait(emptyB + sb, phb ^ 1u);
+                mbar_expect_tx(fullB + sb, C::B_BYTES);
+                tma_load_3d(b_stage(sb), &tmB, fullB + sb, 0, int(it * C::BK), 0, kEvictLast);
+                if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
                 if (++it == sk.ipt) it = 0, ++tile;
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
-        int s = 0;
-        uint32_t ph = 0;
-        int64_t sg = 0;
-        int64_t u = u0;
-        int64_t tile = u0 / sk.ipt;
-        while (u < u1) {
-            const int64_t seg_end = min(u1, (tile + 1) * sk.ipt);
-            const int b = int(sg & 1);
-            mbar_wait(accempty + b, (uint32_t(sg >> 1) & 1u) ^ 1u);
+        // ---------------- MMA issuer (header: numerics for the chain lengths)
+        int sb = 0, r = 0, b = 0, lb = 0;
+        uint32_t phb = 0, rph = 0, aph = 0, lph = 0;
+        bool hi_open = true, lo_open = true;
+        ChainClock clk{u0 % sk.ipt};
+        for (int64_t u = u0; u < u1; ++u) {
+            if (hi_open) mbar_wait(accempty + b, aph ^ 1u);
+            if (C::SEP && lo_open) mbar_wait(loempty + lb, lph ^ 1u);
+            mbar_wait(fullB + sb, phb);
+            mbar_wait(split + r, rph);  // A slot r written
             tc_fence_after();
             const uint32_t d = tmem + uint32_t(b * C::ACC_COLS);
-            for (bool first = true; u < seg_end; ++u, first = false) {
-                mbar_wait(split + s, ph);  // implies full[s]: the split warps waited on it
-                tc_fence_after();
-                // Descriptors are built warp-uniformly (uniform registers) once per stage; the
-                // K steps only add the start-address offset (>> 4) to the low word.
-                const uint32_t a0 = smem_u32(stage_ptr(s));
-                const uint64_t da0 = PASS == 1 ? desc_kmajor(a0, 0) : desc_mnmajor(a0, 0, C::ATOM_STRIDE);
-                const uint64_t db0 = desc_mnmajor(a0 + C::A_BYTES, 0, C::ATOM_STRIDE);  // [hi atoms | lo atoms]
-                const uint32_t alo = tmem + uint32_t(C::ALO_COL0 + C::BK * s);
-                if (elect_one()) {
+            const uint32_t dlo = tmem + uint32_t(C::LO_COL0 + lb * KP);
+            // The B descriptor is built warp-uniformly (uniform registers) once per stage; the
+            // K steps only add the start-address offset (>> 4) to the low word.
+            const uint64_t db0 = desc_mnmajor(smem_u32(b_stage(sb)), 0, C::ATOM_STRIDE);
+            const uint32_t ahi = tmem + uint32_t(C::A_COL0 + r * C::ASLOT_COLS), alo = ahi + C::BK;
+            if (elect_one()) {
 #pragma unroll
-                    for (int kk = 0; kk < C::KSTEPS; ++kk) {
-                        const uint64_t da =
-                            da0 + uint64_t(PASS == 1 ? (((kk >> 2) * 16384 + (kk & 3) * 32) >> 4) : kk * 64);
-                        const uint64_t db = db0 + uint64_t(kk * 64);
-                        mma_ss(d, da, db, C::IDESC_SS, (first && kk == 0) ? 0u : 1u);
-                        mma_ts(d, alo + 8 * kk, db, C::IDESC_TS, 1u);
+                for (int kk = 0; kk < C::KSTEPS; ++kk) {
+                    const uint64_t db = db0 + uint64_t(kk * 64);  // [hi atoms | lo atoms]
+                    const uint64_t dbl = db + C::LO_DESC_OFF;     // B_lo atoms (SEP)
+                    mma_ts(d, ahi + 8 * kk, db, C::IDESC_HI, (hi_open && kk == 0) ? 0u : 1u);
+                    if constexpr (C::SEP) {
+                        mma_ts(dlo, ahi + 8 * kk, dbl, C::IDESC_KP, (lo_open && kk == 0) ? 0u : 1u);
+                        mma_ts(dlo, alo + 8 * kk, db, C::IDESC_KP, 1u);
+                    } else {
+                        (void)dbl;
+                        mma_ts(d + KP, alo + 8 * kk, db, C::IDESC_KP, 1u);
                     }
-                    mma_commit(empty + s);
-                    if (u + 1 == seg_end) mma_commit(accfull + b);
                 }
-                __syncwarp();
-                if (++s == C::STAGES) s = 0, ph ^= 1u;
+                mma_commit(emptyB + sb);
+                mma_commit(afree + r);
             }
-            ++sg;
-            ++tile;
+            if (++r == C::ASLOTS) r = 0, rph ^= 1u;
+            if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
+            bool tile_end, hi_close, lo_close;
+            clk.step(u, u1, sk.ipt, drain_units, C::LO_UNITS, tile_end, hi_close, lo_close);
+            if (hi_close) {
+                if (elect_one()) mma_commit(accfull + b);
+                if (++b == C::NBUF) b = 0, aph ^= 1u;
+            }
+            if (C::SEP && lo_close) {
+                if (elect_one()) mma_commit(lofull + lb);
+                if (++lb == C::NLO) lb = 0, lph ^= 1u;
+            }
+            hi_open = hi_close, lo_open = lo_close;
+            __syncwarp();
         }
-    } else if (warp >= 4) {
-        // ---------------- split (A_lo -> TMEM) + epilogue warpgroup
-        const int t = tid - 128;  // TMEM lane / D row owned by this thread
-        const int q = warp - 4;   // this warp's TMEM lane quarter [32q, 32q+32)
-        const uint32_t lane_bits = uint32_t(32 * q) << 16;
-        int s = 0;
-        uint32_t ph = 0;
-        int64_t sg = 0;
-        int64_t tile = u0 / sk.ipt, it = u0 % sk.ipt;
+    } else if (warp >= 4 && warp < 12) {
+        // ---------------- split warps: A tile -> [A_hi | A_lo] in TMEM slot r. Two warpgroups:
+        // warp w owns TMEM lane quarter w % 4 (tile rows t) and K half h = (w - 4) / 4.
+        const int t = 32 * (warp & 3) + lane;  // TMEM lane / tile row owned by this thread
+        const int h = (warp - 4) >> 2;
+        const uint32_t lane_bits = uint32_t(32 * (warp & 3)) << 16;
+        int sa = 0, rs = 0;
+        uint32_t pha = 0, rph = 0;
         for (int64_t u = u0; u < u1; ++u) {
-            mbar_wait(full + s, ph);
-            const uint8_t* sA = stage_ptr(s);
-            const uint32_t dst = tmem + lane_bits + uint32_t(C::ALO_COL0 + C::BK * s);
-#pragma unroll
-            for (int h = 0; h < C::BK / 32; ++h) {
-                uint32_t r[32];
+            mbar_wait(fullA + sa, pha);
+            mbar_wait(afree + rs, rph ^ 1u);
+            tc_fence_after();
+            const uint8_t* sA = a_stage(sa);
+            const uint32_t dst = tmem + lane_bits + uint32_t(C::A_COL0 + rs * C::ASLOT_COLS);
+            {
+                uint32_t r[32], x[32];
                 if (PASS == 1) {
                     // row t of K-atom h (K-major SW128): 8 chunks of 16 B, chunk c at (c ^ t%8)
                     const float4* row = reinterpret_cast<const float4*>(sA + h * 16384 + t * 128);
 #pragma unroll
                     for (int c = 0; c < 8; ++c) {
                         const float4 v = row[c ^ (t & 7)];
+                        x[4 * c] = __float_as_uint(v.x), x[4 * c + 1] = __float_as_uint(v.y),
+                        x[4 * c + 2] = __float_as_uint(v.z), x[4 * c + 3] = __float_as_uint(v.w);
                         r[4 * c] = lo_bits(v.x), r[4 * c + 1] = lo_bits(v.y), r[4 * c + 2] = lo_bits(v.z),
                         r[4 * c + 3] = lo_bits(v.w);
                     }
@@ -309,40 +386,83 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
                     for (int kr = 0; kr < 32; ++kr) {
                         const int k = 32 * h + kr;
-                        r[kr] = lo_bits(atom[k * 32 + (((e >> 3) ^ (k & 3)) << 3) + (e & 7)]);
+                        const float v = atom[k * 32 + (((e >> 3) ^ (k & 3)) << 3) + (e & 7)];
+                        x[kr] = __float_as_uint(v);
+                        r[kr] = lo_bits(v);
                     }
                 }
-                tmem_st32(dst + 32 * h, r);
+                tmem_st32(dst + 32 * h, x);         // A_hi: raw bits, the MMA truncates to tf32
+                tmem_st32(dst + C::BK + 32 * h, r);  // A_lo
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(emptyA + sa);  // the tile is in registers / TMEM now
+            if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
+            tmem_st_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(split + s);
-            if (++s == C::STAGES) s = 0, ph ^= 1u;
-
-            if (u + 1 == min(u1, (tile + 1) * sk.ipt)) {
-                const int b = int(sg & 1);
-                mbar_wait(accfull + b, uint32_t(sg >> 1) & 1u);
-                tc_fence_after();
-                float* out = slots + sk.slot(cta, tile) * int64_t(128 * KP) + int64_t(t) * KP;
+            if (lane == 0) mbar_arrive(split + rs);
+            if (++rs == C::ASLOTS) rs = 0, rph ^= 1u;
+        }
+    } else if (warp >= 12) {
+        // ---------------- drain warpgroup: closed chains -> f32 row sums; at a tile end (or
+        // the CTA's last unit) the tile's row t -> its stream-K slot
+        const int t = tid - 384;
+        const uint32_t lane_bits = uint32_t(32 * (warp & 3)) << 16;
+        float acc[KP];
+#pragma unroll
+        for (int j = 0; j < KP; ++j) acc[j] = 0.f;
+        int64_t tile = u0 / sk.ipt;
+        int b = 0, lb = 0;
+        uint32_t aph = 0, lph = 0;
+        ChainClock clk{u0 % sk.ipt};
+        // add `cols` (multiple of 32, or 32 with the KP = 16 [hi | lo] fold) TMEM columns
+        auto add_cols = [&](uint32_t src) {
+            if constexpr (KP == 16) {
+                uint32_t v[32];  // D' = [hi(16) | lo(16)] in one 32-column load
+                tmem_ld32(src, v);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(v[j]) + __uint_as_float(v[16 + j]);
+            } else {
 #pragma unroll
                 for (int h = 0; h < KP / 32; ++h) {
-                    uint32_t hi[32], lo[32];
-                    tmem_ld32(tmem + lane_bits + uint32_t(b * C::ACC_COLS + h * 32), hi);
-                    tmem_ld32(tmem + lane_bits + uint32_t(b * C::ACC_COLS + KP + h * 32), lo);
+                    uint32_t v[32];
+                    tmem_ld32(src + h * 32, v);
 #pragma unroll
-                    for (int j4 = 0; j4 < 8; ++j4)
-                        reinterpret_cast<float4*>(out + h * 32)[j4] =
-                            make_float4(__uint_as_float(hi[4 * j4]) + __uint_as_float(lo[4 * j4]),
-                                        __uint_as_float(hi[4 * j4 + 1]) + __uint_as_float(lo[4 * j4 + 1]),
-                                        __uint_as_float(hi[4 * j4 + 2]) + __uint_as_float(lo[4 * j4 + 2]),
-                                        __uint_as_float(hi[4 * j4 + 3]) + __uint_as_float(lo[4 * j4 + 3]));
+                    for (int j = 0; j < 32; ++j) acc[32 * h + j] += __uint_as_float(v[j]);
                 }
+            }
+        };
+        for (int64_t u = u0; u < u1; ++u) {
+            bool tile_end, hi_close, lo_close;
+            clk.step(u, u1, sk.ipt, drain_units, C::LO_UNITS, tile_end, hi_close, lo_close);
+            if (hi_close) {
+                mbar_wait(accfull + b, aph);
+                tc_fence_after();
+                add_cols(tmem + lane_bits + uint32_t(b * C::ACC_COLS));
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(accempty + b);
-                ++sg;
+                if (++b == C::NBUF) b = 0, aph ^= 1u;
             }
-            if (++it == sk.ipt) it = 0, ++tile;
+            if (C::SEP && lo_close) {
+                mbar_wait(lofull + lb, lph);
+                tc_fence_after();
+                add_cols(tmem + lane_bits + uint32_t(C::LO_COL0 + lb * KP));
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(loempty + lb);
+                if (++lb == C::NLO) lb = 0, lph ^= 1u;
+            }
+            if (tile_end || u + 1 == u1) {
+                float* out = slots + sk.slot(cta, tile) * int64_t(128 * KP) + int64_t(t) * KP;
+#pragma unroll
+                for (int j4 = 0; j4 < KP / 4; ++j4) {
+                    reinterpret_cast<float4*>(out)[j4] =
+                        make_float4(acc[4 * j4], acc[4 * j4 + 1], acc[4 * j4 + 2], acc[4 * j4 + 3]);
+                    acc[4 * j4] = acc[4 * j4 + 1] = acc[4 * j4 + 2] = acc[4 * j4 + 3] = 0.f;
+                }
+                ++tile;
+            }
         }
     }
     __syncthreads();
@@ -385,19 +505,29 @@ cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t co
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// K steps (64 each) per TMEM accumulation chain; OOCNMF_TC_DRAIN overrides (developer knob).
+int tc_drain_units() {
+    static int du = [] {
+        const char* e = getenv("OOCNMF_TC_DRAIN");
+        const int v = e ? atoi(e) : 0;
+        return v > 0 ? v : 1;
+    }();
+    return du;
+}
+
 template <int KP, int PASS>
 cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, float* slots, const StreamK& sk, cudaStream_t s) {
     using C = TcCfg<KP, PASS>;
     auto kern = k_pass_tc<KP, PASS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
-    kern<<<unsigned(sk.G), 256, C::SMEM, s>>>(a, b, slots, sk);
+    kern<<<unsigned(sk.G), 512, C::SMEM, s>>>(a, b, slots, sk, tc_drain_units());
     return cudaGetLastError();
 }
 
 }  // namespace
 
-bool tc_supported(int kp) { return (kp == 32 || kp == 64) && encode_fn() != nullptr; }
+bool tc_supported(int kp) { return (kp == 16 || kp == 32 || kp == 64) && encode_fn() != nullptr; }
 
 // Pass 1 on the tensor cores: A (mp x np, ld lda) K-major, Ht_cat (np x 2kp) MN-major.
 cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* Ht_cat,
@@ -406,7 +536,9 @@ cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
     cudaError_t e;
     if ((e = make_map(&ma, A, mp, np, lda, 128, kTcStep / 32, false)) != cudaSuccess) return e;
     if ((e = make_map(&mb, Ht_cat, np, 2 * kp, 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
-    return kp == 32 ? launch_tc<32, 1>(ma, mb, slots, sk, s) : launch_tc<64, 1>(ma, mb, slots, sk, s);
+    return kp == 16   ? launch_tc<16, 1>(ma, mb, slots, sk, s)
+           : kp == 32 ? launch_tc<32, 1>(ma, mb, slots, sk, s)
+                      : launch_tc<64, 1>(ma, mb, slots, sk, s);
 }
 
 // Pass 2 on the tensor cores: A MN-major (4 column atoms per 128-column tile), W_cat (mp x 2kp).
@@ -416,7 +548,9 @@ cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
     cudaError_t e;
     if ((e = make_map(&ma, A, mp, np, lda, kTcStep, 4, true)) != cudaSuccess) return e;
     if ((e = make_map(&mb, W_cat, mp, 2 * kp, 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
-    return kp == 32 ? launch_tc<32, 2>(ma, mb, slots, sk, s) : launch_tc<64, 2>(ma, mb, slots, sk, s);
+    return kp == 16   ? launch_tc<16, 2>(ma, mb, slots, sk, s)
+           : kp == 32 ? launch_tc<32, 2>(ma, mb, slots, sk, s)
+                      : launch_tc<64, 2>(ma, mb, slots, sk, s);
 }
 
 }  // namespace ooc
