@@ -56,6 +56,8 @@ int run(int pass, int kp, int mp, int np, int sms) {
 
 int main() {
     int bad = 0;
+    bad += run(1, 16, 256, 256, 148);
+    bad += run(2, 16, 256, 384, 148);
     bad += run(1, 32, 128, 128, 1);
     bad += run(1, 32, 256, 256, 148);
     bad += run(1, 64, 256, 256, 148);
