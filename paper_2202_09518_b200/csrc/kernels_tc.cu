@@ -8,17 +8,17 @@
 //                                                x_lo = rna_tf32(x - x_hi) (common.cuh tf32_lo)
 // with both A halves in TMEM (the split warps tcgen05.st them there, transposing for pass 2)
 // and [B_hi | B_lo] in shared memory (B_lo written by the factor-update kernel):
-//   kp >= 32:  hi chain  H  += A_hi · B_hi              (N = kp)
+//   kp <= 32:  D' = [H | L]: one N = 2kp MMA A_hi · [B_hi | B_lo], plus A_lo · B_hi into L
+//   kp = 64:   hi chain  H  += A_hi · B_hi              (N = kp)
 //              lo chain  L  += A_hi · B_lo + A_lo · B_hi (2 x N = kp)
-//   kp = 16:   D' = [H | L]: one N = 32 MMA A_hi · [B_hi | B_lo] plus A_lo · B_hi into L
 //
 // Numerics (tools/bias_probe.py, signed mean relative error of A·Ht vs f64): the tensor
 // core's f32 accumulation truncates once per MMA, so one TMEM accumulator carried through a
 // tile's whole K range biased the products by -1e-5..-4e-5 — enough to drift low-rank
 // trajectories past the 1e-4 parity bar. The hi chain therefore restarts every K step (64,
 // 8 MMAs) in a fresh TMEM buffer that drain warps add into round-to-nearest f32 register
-// sums; the lo chain (values ~2^-11 of H, so its own truncation is negligible) restarts every
-// LO_UNITS steps. The remaining bias is a constant ~-3e-7 for any K (FFMA path: unbiased,
+// sums (kp = 64: the lo chain, values ~2^-11 of H so its own truncation is negligible,
+// restarts every LO_UNITS steps). The remaining bias is a constant ~-3e-7 for any K (FFMA path: unbiased,
 // rms 5e-8..1.3e-7); OOCNMF_TC_DRAIN=n lengthens the hi chain to n steps (developer knob).
 //
 // Pipeline (one persistent CTA per SM, 16 warps, stream-K split as the FFMA path):
@@ -70,6 +70,20 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "memory");
     } while (!ok);
 }
+// Developer stall profile (tools/tc_stall.cu, -DOOC_TC_PROFILE): cycles each role spends in
+// each wait, summed over CTAs. Compiled out of the product.
+#ifdef OOC_TC_PROFILE
+__device__ unsigned long long g_tc_prof[16];
+#define TC_WAIT(idx, call)                          \
+    do {                                            \
+        const long long t_ = clock64();             \
+        call;                                       \
+        prof[idx] += clock64() - t_;                \
+    } while (0)
+#else
+#define TC_WAIT(idx, call) call
+#endif
+
 // L2 eviction policies (the encodings CUTLASS uses for TMA cache hints).
 constexpr uint64_t kEvictFirst = 0x12F0000000000000ull, kEvictLast = 0x14F0000000000000ull;
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int x, int y, int z,
@@ -174,14 +188,18 @@ struct TcCfg {
     static constexpr int B_BYTES = BK * 2 * KP * 4;             // 8 / 16 / 32 KB
     static constexpr int A_STAGES = KP == 64 ? 4 : (KP == 32 ? 5 : 6);
     static constexpr int B_STAGES = KP == 64 ? 3 : 4;
-    // SEP (kp >= 32): the large A_hi·B_hi products chain in per-chunk "hi" buffers (kp columns)
-    // drained every chunk; the small A_hi·B_lo + A_lo·B_hi products chain in "lo" buffers
-    // drained every LO_UNITS units, so the per-unit drain reads and adds only kp columns.
-    // kp = 16: one N = 32 MMA writes D' = [hi | lo] and the drain reads both halves.
-    static constexpr bool SEP = KP >= 32;
+    // kp <= 32: one N = 2kp MMA writes D' = [H | L] = A_hi · [B_hi | B_lo], a second adds
+    // A_lo · B_hi into L, and the drain reads both halves every chunk (16 MMAs per K step).
+    // SEP (kp = 64): H and L are separate chains (3 MMAs of N = kp per 8-deep K step); the
+    // per-unit drain reads only H's kp columns and L is drained every LO_UNITS units, which
+    // halves the drain traffic where D' would be 128 columns. (The tensor pipe is far from
+    // bound either way — tools/tc_rate.cu: ~400 cycles per K step at kp = 32 against ~1100
+    // for the HBM stream — but under the board's power cap every SM-side byte and
+    // instruction costs clock, so the layouts minimise both.)
+    static constexpr bool SEP = KP >= 64;
     static constexpr int LO_UNITS = 16;
     static constexpr int ACC_COLS = SEP ? KP : 2 * KP;
-    static constexpr int NBUF = SEP ? 2 : 3;                    // hi (or D') buffers
+    static constexpr int NBUF = KP == 16 ? 3 : 2;               // H (or D') buffers
     static constexpr int NLO = SEP ? 2 : 0;                     // lo buffers
     static constexpr int ASLOTS = KP == 64 ? 2 : 3;             // [A_hi | A_lo] operand slots
     static constexpr int ASLOT_COLS = 2 * BK;
@@ -274,6 +292,10 @@ __global__ void __launch_bounds__(512, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+#ifdef OOC_TC_PROFILE
+    long long prof[16] = {};
+    const long long t_start = clock64();
+#endif
 
     auto a_stage = [&](int s) { return smem + s * C::A_BYTES; };
     auto b_stage = [&](int s) { return smem + C::A_STAGES * C::A_BYTES + s * C::B_BYTES; };
@@ -285,7 +307,7 @@ __global__ void __launch_bounds__(512, 1)
             uint32_t pha = 0, phb = 0;
             int64_t tile = u0 / sk.ipt, it = u0 % sk.ipt;
             for (int64_t u = u0; u < u1; ++u) {
-                mbar_wait(emptyA + sa, pha ^ 1u);
+                TC_WAIT(0, mbar_wait(emptyA + sa, pha ^ 1u));
                 uint8_t* sA = a_stage(sa);
                 mbar_expect_tx(fullA + sa, C::A_BYTES);
                 if (PASS == 1)  // rows [tile*128, +128), K-atoms [2 it, 2 it + 2): atom j -> +16 KB
@@ -294,7 +316,7 @@ __global__ void __launch_bounds__(512, 1)
                     tma_load_3d(sA, &tmA, fullA + sa, 0, int(it * C::BK), int(tile * 4), kEvictFirst);
                 if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
                 // factor rows [it*64, +64) of [F | F_lo]: 2kp/32 atoms of 8 KB
-                mbar_wait(emptyB + sb, phb ^ 1u);
+                TC_WAIT(1, mbar_wait(emptyB + sb, phb ^ 1u));
                 mbar_expect_tx(fullB + sb, C::B_BYTES);
                 tma_load_3d(b_stage(sb), &tmB, fullB + sb, 0, int(it * C::BK), 0, kEvictLast);
                 if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
@@ -308,10 +330,10 @@ __global__ void __launch_bounds__(512, 1)
         bool hi_open = true, lo_open = true;
         ChainClock clk{u0 % sk.ipt};
         for (int64_t u = u0; u < u1; ++u) {
-            if (hi_open) mbar_wait(accempty + b, aph ^ 1u);
-            if (C::SEP && lo_open) mbar_wait(loempty + lb, lph ^ 1u);
-            mbar_wait(fullB + sb, phb);
-            mbar_wait(split + r, rph);  // A slot r written
+            if (hi_open) TC_WAIT(5, mbar_wait(accempty + b, aph ^ 1u));
+            if (C::SEP && lo_open) TC_WAIT(5, mbar_wait(loempty + lb, lph ^ 1u));
+            TC_WAIT(6, mbar_wait(fullB + sb, phb));
+            TC_WAIT(7, mbar_wait(split + r, rph));  // A slot r written
             tc_fence_after();
             const uint32_t d = tmem + uint32_t(b * C::ACC_COLS);
             const uint32_t dlo = tmem + uint32_t(C::LO_COL0 + lb * KP);
@@ -360,8 +382,8 @@ __global__ void __launch_bounds__(512, 1)
         int sa = 0, rs = 0;
         uint32_t pha = 0, rph = 0;
         for (int64_t u = u0; u < u1; ++u) {
-            mbar_wait(fullA + sa, pha);
-            mbar_wait(afree + rs, rph ^ 1u);
+            TC_WAIT(2, mbar_wait(fullA + sa, pha));
+            TC_WAIT(3, mbar_wait(afree + rs, rph ^ 1u));
             tc_fence_after();
             const uint8_t* sA = a_stage(sa);
             const uint32_t dst = tmem + lane_bits + uint32_t(C::A_COL0 + rs * C::ASLOT_COLS);
@@ -415,14 +437,14 @@ __global__ void __launch_bounds__(512, 1)
         int b = 0, lb = 0;
         uint32_t aph = 0, lph = 0;
         ChainClock clk{u0 % sk.ipt};
-        // add `cols` (multiple of 32, or 32 with the KP = 16 [hi | lo] fold) TMEM columns
+        // add one closed chain (D' = [H | L] folded, or one SEP chain) into the row sums
         auto add_cols = [&](uint32_t src) {
             if constexpr (KP == 16) {
                 uint32_t v[32];  // D' = [hi(16) | lo(16)] in one 32-column load
                 tmem_ld32(src, v);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(v[j]) + __uint_as_float(v[16 + j]);
-            } else {
+            } else if constexpr (C::SEP) {  // one chain's kp columns
 #pragma unroll
                 for (int h = 0; h < KP / 32; ++h) {
                     uint32_t v[32];
@@ -430,13 +452,22 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) acc[32 * h + j] += __uint_as_float(v[j]);
                 }
+            } else {  // D' = [H | L]
+#pragma unroll
+                for (int h = 0; h < KP / 32; ++h) {
+                    uint32_t hi[32], lo[32];
+                    tmem_ld32(src + h * 32, hi);
+                    tmem_ld32(src + KP + h * 32, lo);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) acc[32 * h + j] += __uint_as_float(hi[j]) + __uint_as_float(lo[j]);
+                }
             }
         };
         for (int64_t u = u0; u < u1; ++u) {
             bool tile_end, hi_close, lo_close;
             clk.step(u, u1, sk.ipt, drain_units, C::LO_UNITS, tile_end, hi_close, lo_close);
             if (hi_close) {
-                mbar_wait(accfull + b, aph);
+                TC_WAIT(8, mbar_wait(accfull + b, aph));
                 tc_fence_after();
                 add_cols(tmem + lane_bits + uint32_t(b * C::ACC_COLS));
                 tc_fence_before();
@@ -445,7 +476,7 @@ __global__ void __launch_bounds__(512, 1)
                 if (++b == C::NBUF) b = 0, aph ^= 1u;
             }
             if (C::SEP && lo_close) {
-                mbar_wait(lofull + lb, lph);
+                TC_WAIT(8, mbar_wait(lofull + lb, lph));
                 tc_fence_after();
                 add_cols(tmem + lane_bits + uint32_t(C::LO_COL0 + lb * KP));
                 tc_fence_before();
@@ -465,6 +496,15 @@ __global__ void __launch_bounds__(512, 1)
             }
         }
     }
+#ifdef OOC_TC_PROFILE
+    // per role: lane 0 of warp 0 (producer), warp 1 (MMA), warp 4 (split), warp 12 (drain)
+    if (lane == 0 && (warp == 0 || warp == 1 || warp == 4 || warp == 12)) {
+        for (int j = 0; j < 9; ++j)
+            if (prof[j]) atomicAdd(&g_tc_prof[j], (unsigned long long)prof[j]);
+        atomicAdd(&g_tc_prof[9 + (warp == 0 ? 0 : warp == 1 ? 1 : warp == 4 ? 2 : 3)],
+                  (unsigned long long)(clock64() - t_start));
+    }
+#endif
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
@@ -526,6 +566,16 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, float* slots, 
 }
 
 }  // namespace
+
+#ifdef OOC_TC_PROFILE
+void tc_profile_read(unsigned long long* out16, bool reset) {
+    cudaMemcpyFromSymbol(out16, g_tc_prof, 16 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_tc_prof, z, sizeof(z));
+    }
+}
+#endif
 
 bool tc_supported(int kp) { return (kp == 16 || kp == 32 || kp == 64) && encode_fn() != nullptr; }
 

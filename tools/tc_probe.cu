@@ -2,7 +2,7 @@
 // prints max relative error vs a host f64 reference, plus a few entries. Not part of the
 // product; build: nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -I include \
 //   -I paper_2202_09518_b200/csrc tools/tc_probe.cu paper_2202_09518_b200/csrc/kernels_tc.cu \
-//   paper_2202_09518_b200/csrc/kernels_factor.cu -o /tmp/tc_probe
+//   paper_2202_09518_b200/csrc/kernels_factor.cu paper_2202_09518_b200/csrc/kernels_dense.cu -lcuda -o tools/tc_probe
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
