@@ -12,14 +12,26 @@
 namespace ooc {
 namespace {
 
-// A CTA handles 64-row units (half of a 128-row stream-K tile) with four threads per row,
-// each owning kp/4 columns. The update is a short dependent chain per thread, so what sets its
-// speed is how many units are in flight per SM: small CTAs, few registers (the row is staged
-// in shared memory instead of registers), several CTAs resident per SM.
-constexpr int kUnitRows = 64;
-constexpr int kRowThreads = 4;
-constexpr int kFuThreads = kUnitRows * kRowThreads;  // 256
-constexpr int kFuMaxGrid = 16 * 148;
+// A CTA of 512 threads owns whole 128-row tiles and loops over them:
+//   1. the tile's F rows and numerator rows (plain, or the sum of the tile's stream-K
+//      partials in ascending CTA order) are staged in shared memory with coalesced loads,
+//      each thread keeping all of its kp/4 loads in flight;
+//   2. warp w updates 32 rows x one quarter of the columns: lane = row, so f[q] is a
+//      conflict-free read of the lane's own (padded) row and the G row segment is the same
+//      for the whole warp (a broadcast) — kp/4 FMAs per f[q], 3 wavefronts per 8 FMAs; the
+//      update f * n / (de + eps) and its n·f_new term of the trace-form error follow;
+//   3. the new rows go back to global memory (and [F | lo(F)] for the tensor-core operand)
+//      with coalesced stores;
+//   4. Gram partial: thread (block b, row group g) accumulates a GT x GT block of
+//      F_new^T F_new over its row group in f32 registers across the CTA's tiles; at the end the
+//      row groups are summed in f64 (fixed order) into one kp x kp slot per CTA.
+// With 16 warps per CTA and up to 4 CTAs per SM the per-row dependent chain is hidden by
+// occupancy (the previous layouts were latency-bound at 40-55 us for 65536 x 32 —
+// tools/fu_bench.cu).
+constexpr int kFuRows = kTile;          // rows per tile
+constexpr int kFuThreads = 4 * kFuRows;  // 4 threads per row in the update
+constexpr int kFuCtasPerSm = 2;
+constexpr int kFuMaxParts = 64;          // stream-K partials of one tile summed via smem offsets
 
 // Fixed-shape block reduction of a double (deterministic).
 __device__ double block_sum_f64(double v, double* sh) {
@@ -35,152 +47,171 @@ __device__ double block_sum_f64(double v, double* sh) {
     return r;
 }
 
-// Register-blocked Gram of a 64-row unit over 256 threads: thread t < NBLK owns a TI x TJ
-// block (rows i0.., cols j0..) of the kp x kp result.
 template <int KP>
-struct GramBlock {
-    static constexpr int T = KP >= 64 ? 4 : (KP >= 32 ? 2 : 1);
-    static constexpr int TI = T, TJ = T;
-    static constexpr int NJB = KP / TJ;           // blocks along j
-    static constexpr int NBLK = (KP / TI) * NJB;  // <= 256
-    static constexpr int FS = KP + 4;             // f32 smem row stride (16-byte aligned rows)
+struct FuCfg {
+    static constexpr int FS = KP + 1;                  // padded f32 row stride
+    static constexpr int QC = KP / 4;                  // update columns per thread
+    static constexpr int GT = KP >= 32 ? 4 : 2;        // Gram thread block GT x GT
+    static constexpr int GB = KP / GT;
+    static constexpr int NGB = GB * GB;                // Gram blocks (<= 512)
+    static constexpr int RG = kFuThreads / NGB;        // row groups
+    static_assert(NGB <= kFuThreads && kFuThreads % NGB == 0 && kFuRows % RG == 0, "Gram blocking");
+    static constexpr int EPT = kFuRows * KP / kFuThreads;  // staged elements per thread
+    // smem: G (f32) | Fs | Ns (f32, padded rows) ; the Gram partials (RG x KP x KP f32) reuse
+    // Fs/Ns at the end
+    static constexpr size_t ROWS_BYTES = 2 * size_t(kFuRows) * FS * 4;
+    static constexpr size_t PART_BYTES = size_t(RG) * KP * KP * 4;
+    static_assert(PART_BYTES <= ROWS_BYTES, "Gram partials fit in the row buffers");
+    static constexpr size_t SMEM = size_t(KP * KP) * 4 + ROWS_BYTES + size_t(kFuThreads) * 8;
 };
 
 template <int KP>
-__global__ void __launch_bounds__(kFuThreads, 3)
-    k_factor_update(float* __restrict__ F, int64_t units, const float* __restrict__ n_plain,
+__global__ void __launch_bounds__(kFuThreads, 2)
+    k_factor_update(float* __restrict__ F, int64_t tiles, const float* __restrict__ n_plain,
                     const float* __restrict__ n_slots, StreamK sk, const float* __restrict__ G,
                     float eps, int update, double* __restrict__ gram_slots,
                     double* __restrict__ err_slots, int* __restrict__ flag, float* __restrict__ cat_out) {
-    using GB = GramBlock<KP>;
-    constexpr int FS = GB::FS;
-    constexpr int QW = KP / kRowThreads;  // columns owned by each thread of a row
+    using C = FuCfg<KP>;
+    constexpr int FS = C::FS, GT = C::GT, QC = C::QC;
     extern __shared__ __align__(16) unsigned char fu_smem[];
-    double* red = reinterpret_cast<double*>(fu_smem);
-    float* Gs = reinterpret_cast<float*>(red + kFuThreads);
-    float* Fs = Gs + KP * KP;
-    const int tid = threadIdx.x;
-    const int lr = tid / kRowThreads, part = tid % kRowThreads;  // local row, column quarter
-    const int c0 = part * QW;
+    float* Gs = reinterpret_cast<float*>(fu_smem);  // KP x KP
+    float* Fs = Gs + KP * KP;                         // kFuRows x FS: old rows
+    float* Ns = Fs + kFuRows * FS;                    // kFuRows x FS: numerator, then new rows
+    double* red = reinterpret_cast<double*>(Ns + kFuRows * FS);  // kFuThreads (8-byte aligned)
+    __shared__ int64_t part_off[kFuMaxParts];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (update)
         for (int e = tid; e < KP * KP; e += kFuThreads) Gs[e] = G[e];
-
-    const int bi = tid / GB::NJB, bj = tid % GB::NJB;
-    const int i0 = bi * GB::TI, j0 = bj * GB::TJ;
-    const bool gram_owner = tid < GB::NBLK;
-    double gacc[GB::TI * GB::TJ];
+    // update role: warp -> (row block of 32, column quarter)
+    const int urow = (warp & 3) * 32 + lane, uc0 = (warp >> 2) * QC;
+    // Gram role
+    const int gblk = tid % C::NGB, grg = tid / C::NGB;
+    const int gi0 = (gblk / C::GB) * GT, gj0 = (gblk % C::GB) * GT;
+    float gacc[GT * GT];
 #pragma unroll
-    for (int q = 0; q < GB::TI * GB::TJ; ++q) gacc[q] = 0.0;
+    for (int q = 0; q < GT * GT; ++q) gacc[q] = 0.f;
     double eacc = 0.0;
     bool bad = false;
 
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        const int64_t row = u * kUnitRows + lr;
-        const int64_t t = u / (kTile / kUnitRows);                  // stream-K tile
-        const int trow = int(u % (kTile / kUnitRows)) * kUnitRows + lr;  // row within the tile
-        float fo[QW];
-        {
-            const float* fr = F + row * KP + c0;
-#pragma unroll
-            for (int j = 0; j < QW; ++j) fo[j] = fr[j];
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int64_t base = t * kFuRows * KP;
+        int nparts = 0;
+        int64_t cfirst = 0;
+        if (update && !n_plain) {
+            // the tile's partials, ascending CTA order (64-bit divisions once per tile)
+            cfirst = sk.cta_of(t * sk.ipt);
+            nparts = int(sk.cta_of((t + 1) * sk.ipt - 1) - cfirst + 1);
+            for (int q = tid; q < nparts && q < kFuMaxParts; q += kFuThreads)
+                part_off[q] = sk.slot(cfirst + q, t) * int64_t(kTile * KP);
+            __syncthreads();
         }
-        if (update) {
+        // 1. stage (element e = tid + kFuThreads * i)
+        {
+            float fv[C::EPT], nv[C::EPT];
 #pragma unroll
-            for (int j = 0; j < QW; ++j) Fs[lr * FS + c0 + j] = fo[j];
-            float nu[QW];
-            if (n_plain) {
-                const float* nr = n_plain + row * KP + c0;
+            for (int i = 0; i < C::EPT; ++i) fv[i] = F[base + tid + i * kFuThreads];
+            if (update) {
+                if (n_plain) {
 #pragma unroll
-                for (int j = 0; j < QW; ++j) nu[j] = nr[j];
-            } else {
+                    for (int i = 0; i < C::EPT; ++i) nv[i] = n_plain[base + tid + i * kFuThreads];
+                } else {
 #pragma unroll
-                for (int j = 0; j < QW; ++j) nu[j] = 0.f;
-                const int64_t s0 = sk.cta_of(t * sk.ipt), s1 = sk.cta_of((t + 1) * sk.ipt - 1);
-                for (int64_t c = s0; c <= s1; ++c) {
-                    const float* nr = n_slots + sk.slot(c, t) * int64_t(kTile * KP) + int64_t(trow) * KP + c0;
+                    for (int i = 0; i < C::EPT; ++i) nv[i] = 0.f;
+                    for (int q = 0; q < nparts; ++q) {
+                        const float* src =
+                            n_slots + (q < kFuMaxParts ? part_off[q] : sk.slot(cfirst + q, t) * int64_t(kTile * KP));
+                        float pv[C::EPT];
 #pragma unroll
-                    for (int j = 0; j < QW; ++j) nu[j] += nr[j];
+                        for (int i = 0; i < C::EPT; ++i) pv[i] = src[tid + i * kFuThreads];
+#pragma unroll
+                        for (int i = 0; i < C::EPT; ++i) nv[i] += pv[i];
+                    }
                 }
             }
-            __syncthreads();  // Gs (first unit) and this unit's rows staged
-            // de = f · G: f[q] is a broadcast read of the row in smem, G rows are 128-bit loads
-            float de[QW];
 #pragma unroll
-            for (int j = 0; j < QW; ++j) de[j] = 0.f;
-            const float* frow = Fs + lr * FS;
+            for (int i = 0; i < C::EPT; ++i) {
+                const int e = tid + i * kFuThreads, r = e / KP, j = e % KP;
+                Fs[r * FS + j] = fv[i];
+                if (update) Ns[r * FS + j] = nv[i];
+            }
+        }
+        __syncthreads();
+        // 2. update: lane = row urow, columns [uc0, uc0 + QC)
+        if (update) {
+            const float* fr = Fs + urow * FS;
+            float de[QC];
+#pragma unroll
+            for (int j = 0; j < QC; ++j) de[j] = 0.f;
 #pragma unroll 8
             for (int q = 0; q < KP; ++q) {
-                const float fq = frow[q];
+                const float fq = fr[q];
+                const float* g = Gs + q * KP + uc0;
 #pragma unroll
-                for (int j = 0; j < QW; ++j) de[j] = fmaf(fq, Gs[q * KP + c0 + j], de[j]);
+                for (int j = 0; j < QC; ++j) de[j] = fmaf(fq, g[j], de[j]);
             }
+            float* nr = Ns + urow * FS + uc0;
             double e = 0.0;
 #pragma unroll
-            for (int j = 0; j < QW; ++j) {
-                const float nf = fo[j] * nu[j] / (de[j] + eps);
+            for (int j = 0; j < QC; ++j) {
+                const float nu = nr[j];
+                const float nf = fr[uc0 + j] * nu / (de[j] + eps);
                 bad |= !isfinite(nf);
-                fo[j] = nf;
-                e += double(nu[j]) * double(nf);
+                e += double(nu) * double(nf);
+                nr[j] = nf;  // (row, column quarter) is private to this thread
             }
             eacc += e;
-            float* fw = F + row * KP + c0;
-#pragma unroll
-            for (int j = 0; j < QW; ++j) fw[j] = fo[j];
-            __syncthreads();  // everyone has read the old rows from Fs
-        }
-        if (cat_out) {
-            // [F | F - tf32(F)] row of the tensor-core operand (one TMA box carries both halves)
-            float* cw = cat_out + row * 2 * KP;
-#pragma unroll
-            for (int j = 0; j < QW; ++j) {
-                cw[c0 + j] = fo[j];
-                cw[KP + c0 + j] = tf32_lo(fo[j]);
+        } else {
+            for (int e = tid; e < kFuRows * KP; e += kFuThreads) {
+                const int r = e / KP, j = e % KP;
+                Ns[r * FS + j] = Fs[r * FS + j];
             }
         }
-        // Gram partial of the unit: f32 sums over its 64 rows (FP64 issue rate is far below
-        // FP32), accumulated across units and CTAs in f64. Its ~1e-7 relative error only
-        // reaches the error estimate through the trace form, which error_mode auto uses only
-        // where err > 0.1 (there it moves err by < 1e-5 relative).
-#pragma unroll
-        for (int j = 0; j < QW; ++j) Fs[lr * FS + c0 + j] = fo[j];
         __syncthreads();
-        if (gram_owner) {
-            float gt[GB::TI * GB::TJ];
+        // 3. write back (coalesced)
 #pragma unroll
-            for (int q = 0; q < GB::TI * GB::TJ; ++q) gt[q] = 0.f;
-#pragma unroll 8
-            for (int r = 0; r < kUnitRows; ++r) {
-                const float* fr = Fs + r * FS;
-                float fi[GB::TI], fj[GB::TJ];
-#pragma unroll
-                for (int a = 0; a < GB::TI; ++a) fi[a] = fr[i0 + a];
-#pragma unroll
-                for (int b = 0; b < GB::TJ; ++b) fj[b] = fr[j0 + b];
-#pragma unroll
-                for (int a = 0; a < GB::TI; ++a)
-#pragma unroll
-                    for (int b = 0; b < GB::TJ; ++b) gt[a * GB::TJ + b] = fmaf(fi[a], fj[b], gt[a * GB::TJ + b]);
+        for (int i = 0; i < C::EPT; ++i) {
+            const int e = tid + i * kFuThreads, r = e / KP, j = e % KP;
+            const float v = Ns[r * FS + j];
+            if (update) F[base + e] = v;
+            if (cat_out) {
+                float* cw = cat_out + (t * kFuRows + r) * 2 * KP;
+                cw[j] = v;
+                cw[KP + j] = tf32_lo(v);
             }
-#pragma unroll
-            for (int q = 0; q < GB::TI * GB::TJ; ++q) gacc[q] += double(gt[q]);
         }
-        __syncthreads();
+        // 4. Gram partial of the tile's new rows
+#pragma unroll 4
+        for (int r = grg; r < kFuRows; r += C::RG) {
+            const float* row = Ns + r * FS;
+            float fi[GT], fj[GT];
+#pragma unroll
+            for (int a = 0; a < GT; ++a) fi[a] = row[gi0 + a], fj[a] = row[gj0 + a];
+#pragma unroll
+            for (int a = 0; a < GT; ++a)
+#pragma unroll
+                for (int b = 0; b < GT; ++b) gacc[a * GT + b] = fmaf(fi[a], fj[b], gacc[a * GT + b]);
+        }
+        __syncthreads();  // Fs / Ns are rewritten by the next tile
     }
-    if (gram_owner) {
-        double* gout = gram_slots + int64_t(blockIdx.x) * KP * KP;
+    // row groups -> f64 CTA sum in fixed order (partials parked in the row buffers)
+    float* part = Fs;
 #pragma unroll
-        for (int a = 0; a < GB::TI; ++a)
+    for (int a = 0; a < GT; ++a)
 #pragma unroll
-            for (int b = 0; b < GB::TJ; ++b) {
-                const int i = i0 + a, j = j0 + b;
-                // mirror the upper triangle so the Gram is symmetric to the bit
-                const double v = gacc[a * GB::TJ + b];
-                if (i <= j) gout[i * KP + j] = v, gout[j * KP + i] = v;
-            }
+        for (int b = 0; b < GT; ++b) part[(grg * KP + gi0 + a) * KP + gj0 + b] = gacc[a * GT + b];
+    __syncthreads();
+    double* gout = gram_slots + int64_t(blockIdx.x) * KP * KP;
+    for (int e = tid; e < KP * KP; e += kFuThreads) {
+        const int i = e / KP, j = e % KP;
+        // mirror the upper triangle so the Gram is symmetric to the bit
+        const int src = i <= j ? e : j * KP + i;
+        double sum = 0.0;
+        for (int g = 0; g < C::RG; ++g) sum += double(part[g * KP * KP + src]);
+        gout[e] = sum;
     }
     if (err_slots) {
-        const double s = block_sum_f64(eacc, red);
-        if (tid == 0) err_slots[blockIdx.x] = s;
+        const double sum = block_sum_f64(eacc, red);
+        if (tid == 0) err_slots[blockIdx.x] = sum;
     }
     if (bad) atomicOr(flag, 1);
 }
@@ -242,8 +273,13 @@ __global__ void k_finalize_error(int kp, const double* __restrict__ err_slots, i
 }  // namespace
 
 int factor_grid(int64_t tiles) {
-    const int64_t units = tiles * (kTile / kUnitRows);
-    return int(units < kFuMaxGrid ? units : kFuMaxGrid);
+    static int sms = [] {
+        int d = 0, n = 148;
+        if (cudaGetDevice(&d) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+        return n;
+    }();
+    const int64_t cap = int64_t(sms) * kFuCtasPerSm;
+    return int(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
 }
 
 cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_plain,
@@ -251,19 +287,16 @@ cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_
                                  float eps, bool update, double* gram_slots, double* err_slots,
                                  int* flag, float* cat_out, cudaStream_t s) {
     const int64_t tiles = rows / kTile;
-    const int64_t units = tiles * (kTile / kUnitRows);
     const int grid = factor_grid(tiles);
     StreamK skv = sk ? *sk : StreamK{};
 #define OOC_FU(K)                                                                              \
     case K: {                                                                                  \
-        const int smem = int(kFuThreads * sizeof(double) + K * K * sizeof(float) +            \
-                             kUnitRows * GramBlock<K>::FS * sizeof(float));                    \
-        cudaError_t e = cudaFuncSetAttribute(                                                  \
-            k_factor_update<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);            \
-        if (e != cudaSuccess) return e;                                                        \
-        k_factor_update<K><<<grid, kFuThreads, smem, s>>>(F, units, n_plain, n_slots, skv, G,  \
-                                                         eps, update ? 1 : 0, gram_slots,      \
-                                                         err_slots, flag, cat_out);            \
+        static const cudaError_t attr = cudaFuncSetAttribute(                                  \
+            k_factor_update<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(FuCfg<K>::SMEM)); \
+        if (attr != cudaSuccess) return attr;                                                  \
+        k_factor_update<K><<<grid, kFuThreads, FuCfg<K>::SMEM, s>>>(F, tiles, n_plain, n_slots, skv, G, \
+                                                                 eps, update ? 1 : 0, gram_slots, \
+                                                                 err_slots, flag, cat_out);    \
         break;                                                                                 \
     }
     switch (kp) {

@@ -141,6 +141,13 @@ struct oocnmf_ctx {
     double* hpin = nullptr;      // pinned readback: [err, flag]
     std::vector<cudaEvent_t> evs;
     uint64_t launches = 0;
+    // CUDA graph of one block of iterations (the launches between two error checks),
+    // replayed while its key (buffers, shapes, eps, block length) is unchanged.
+    cudaGraphExec_t graph = nullptr;
+    std::vector<uint64_t> graph_key;
+    uint64_t graph_launches = 0;
+    bool graph_broken = false;   // capture failed once: iterate eagerly (same kernels)
+    bool capturing = false;
 
     float* wta() const { return packed.as<float>(); }
     float* wtw() const { return packed.as<float>() + np * kp; }
@@ -268,13 +275,18 @@ void gram_h(oocnmf_ctx* c) {
           "reduce HHt");
 }
 
+// A timing event: inside a graph capture it must be an external event-record node.
+void record(oocnmf_ctx* c, cudaEvent_t e, cudaStream_t s) {
+    ck(c->capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s), "event");
+}
+
 // W update + accumulation of the rank-local [W^T A | W^T W] into c->packed.
 void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     const int kp = c->kp;
     const int gw = factor_grid(c->mp / kTile);
     cudaStream_t s = c->stream;
     auto rec = [&](int i) {
-        if (timed) ck(cudaEventRecord(ev[i], s), "event");
+        if (timed) record(c, ev[i], s);
     };
     rec(eStart);
     if (c->kind == Kind::dense) {
@@ -360,14 +372,14 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
             "allreduce WtW64");
         nck(ncclGroupEnd(), "ncclGroupEnd");
     }
-    if (timed) ck(cudaEventRecord(ev[eComm], s), "event");
+    if (timed) record(c, ev[eComm], s);
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, c->wta(), nullptr, nullptr, c->wtw(), eps, true,
                                   c->gram_h.as<double>(), c->err_slots.as<double>(), c->flag.as<int>(), htlo(c), s),
           "H update");
     count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
                                  c->HHt.as<float>(), c->HHt64.as<double>(), s),
           "reduce HHt");
-    if (timed) ck(cudaEventRecord(ev[eHdone], s), "event");
+    if (timed) record(c, ev[eHdone], s);
 }
 
 
@@ -457,6 +469,72 @@ void prepare_factors(oocnmf_ctx* c, const oocnmf_config* cfg) {
     c->factors_valid = true;
 }
 
+// `count` MU iterations; iteration i records its events into ev + kEvPerIter * i. In-core
+// problems replay a captured CUDA graph of the whole block (one launch instead of ~10 per
+// iteration and no host round trips between them); OOCNMF_NO_GRAPH=1 iterates eagerly.
+void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
+    static const bool no_graph = [] {
+        const char* e = std::getenv("OOCNMF_NO_GRAPH");
+        return e && e[0] == '1';
+    }();
+    auto eager = [&] {
+        for (uint64_t i = 0; i < count; ++i) {
+            w_update_and_wta(c, eps, true, ev + kEvPerIter * i);
+            h_update(c, eps, true, ev + kEvPerIter * i);
+        }
+    };
+    if (no_graph || c->graph_broken || c->kind == Kind::host) return eager();
+    uint32_t eps_bits;
+    std::memcpy(&eps_bits, &eps, 4);
+    const std::vector<uint64_t> key = {
+        uint64_t(c->kind), uint64_t(c->kp), uint64_t(c->mp), uint64_t(c->np), c->rows, count, eps_bits,
+        uint64_t(c->use_tc), uint64_t(reinterpret_cast<uintptr_t>(c->comm)),
+        uint64_t(reinterpret_cast<uintptr_t>(ev)), uint64_t(reinterpret_cast<uintptr_t>(c->A.p)),
+        uint64_t(reinterpret_cast<uintptr_t>(c->rp.p)), uint64_t(reinterpret_cast<uintptr_t>(c->rpT.p)),
+        uint64_t(reinterpret_cast<uintptr_t>(c->W.p)), uint64_t(reinterpret_cast<uintptr_t>(c->Ht.p)),
+        uint64_t(reinterpret_cast<uintptr_t>(c->W_cat.p)), uint64_t(reinterpret_cast<uintptr_t>(c->Ht_cat.p)),
+        uint64_t(reinterpret_cast<uintptr_t>(c->packed.p)), uint64_t(reinterpret_cast<uintptr_t>(c->slots1.p)),
+        uint64_t(reinterpret_cast<uintptr_t>(c->slots2.p)), uint64_t(reinterpret_cast<uintptr_t>(c->N1.p)),
+        uint64_t(reinterpret_cast<uintptr_t>(c->gram_w.p)), uint64_t(reinterpret_cast<uintptr_t>(c->gram_h.p)),
+        uint64_t(c->sk1.G), uint64_t(c->sk1.tiles), uint64_t(c->sk2.G), uint64_t(c->sk2.tiles)};
+    if (!c->graph || key != c->graph_key) {
+        if (c->graph) cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+        const uint64_t l0 = c->launches;
+        cudaGraph_t g = nullptr;
+        bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            c->capturing = true;
+            try {
+                eager();
+            } catch (...) {
+                c->capturing = false;
+                cudaStreamEndCapture(c->stream, &g);
+                if (g) cudaGraphDestroy(g);
+                cudaGetLastError();
+                c->launches = l0;
+                c->graph_broken = true;  // replay eagerly from now on
+                return eager();
+            }
+            c->capturing = false;
+            ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && g;
+        }
+        ok = ok && cudaGraphInstantiate(&c->graph, g, 0) == cudaSuccess;
+        if (g) cudaGraphDestroy(g);
+        c->graph_launches = c->launches - l0;
+        c->launches = l0;
+        if (!ok) {
+            cudaGetLastError();
+            c->graph = nullptr;
+            c->graph_broken = true;
+            return eager();
+        }
+        c->graph_key = key;
+    }
+    ck(cudaGraphLaunch(c->graph, c->stream), "cudaGraphLaunch");
+    c->launches += c->graph_launches;
+}
+
 void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, double* trace_err,
                 uint64_t trace_cap, oocnmf_info* info) {
     need_problem(c);
@@ -489,14 +567,14 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     uint64_t pending = 0;  // iterations with recorded events since the last readback
     uint64_t iter = 0, nt = 0;
     bool converged = false;
-    for (iter = 1; iter <= cfg->max_iters; ++iter) {
-        cudaEvent_t* ev = c->evs.data() + kEvPerIter * pending;
-        w_update_and_wta(c, eps, true, ev);
-        h_update(c, eps, true, ev);
-        ++pending;
-        inf.flops += flops_per_iter;
-        const bool check = (iter % interval == 0) || iter == cfg->max_iters;
-        if (!check) continue;
+    // blocks of iterations end exactly at the error checks (iter % interval == 0, or the last)
+    for (uint64_t next = 1; next <= cfg->max_iters;) {
+        const uint64_t block = std::min<uint64_t>(interval - (next - 1) % interval, cfg->max_iters - next + 1);
+        run_iterations(c, eps, block, c->evs.data());
+        pending = block;
+        inf.flops += flops_per_iter * double(block);
+        iter = next + block - 1;
+        next += block;
         cudaEvent_t* ce = c->evs.data() + kEvPerIter * pending;
         ck(cudaEventRecord(ce[0], c->stream), "event");
         int bad = 0;
@@ -528,7 +606,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         }
     }
     ck(cudaStreamSynchronize(c->stream), "sync");
-    inf.iterations_run = std::min<uint64_t>(iter, cfg->max_iters);
+    inf.iterations_run = iter;
     inf.converged = converged ? 1 : 0;
     inf.n_trace = nt;
     inf.gpu_launches = c->launches;
@@ -710,6 +788,7 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
         if (c->stream) cudaStreamSynchronize(c->stream);
         if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
         if (c->comm) ncclCommDestroy(c->comm);
+        if (c->graph) cudaGraphExecDestroy(c->graph);
         for (auto e : c->evs) cudaEventDestroy(e);
         for (int i = 0; i < 2; ++i) {
             if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
