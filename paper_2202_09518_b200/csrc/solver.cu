@@ -787,8 +787,10 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
         cudaSetDevice(c->device);
         if (c->stream) cudaStreamSynchronize(c->stream);
         if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
-        if (c->comm) ncclCommDestroy(c->comm);
+        // the graph holds NCCL work on c->comm: release it before the communicator
         if (c->graph) cudaGraphExecDestroy(c->graph);
+        c->graph = nullptr;
+        if (c->comm) ncclCommDestroy(c->comm);
         for (auto e : c->evs) cudaEventDestroy(e);
         for (int i = 0; i < 2; ++i) {
             if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
