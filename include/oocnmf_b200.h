@@ -121,6 +121,10 @@ int oocnmf_ctx_rank(const oocnmf_ctx* ctx, int* rank, int* nranks);
 int oocnmf_set_problem(oocnmf_ctx* ctx, uint64_t m, uint64_t n, uint64_t k, uint64_t row0,
                        uint64_t rows);
 
+/* The problem set on this context (for layered callers). */
+int oocnmf_problem_dims(const oocnmf_ctx* ctx, uint64_t* m, uint64_t* n, uint64_t* k, uint64_t* row0,
+                        uint64_t* rows);
+
 /* A sources (pick one). Dense values are stored in HBM as f32 row-major. */
 int oocnmf_load_dense_f64(oocnmf_ctx* ctx, const double* a_slab, uint64_t lda);
 int oocnmf_load_dense_f32(oocnmf_ctx* ctx, const float* a_slab, uint64_t lda);
@@ -164,6 +168,64 @@ int oocnmf_solve(oocnmf_ctx* ctx, const oocnmf_config* cfg, uint64_t* trace_iter
 int oocnmf_products_f64(oocnmf_ctx* ctx, double* aht, double* wta, double* hht, double* wtw);
 /* Squared Frobenius norm of the resident A slab (f64 accumulation). */
 int oocnmf_sq_norm(oocnmf_ctx* ctx, double* out);
+
+/* ----- model selection (NMFk), the consumer of the MU path -----
+ * replaces select_k / cluster_columns / silhouette / pearson_correlation_matrix /
+ * perturb_dense / perturb_sparse (include/oocnmf/model_selection.hpp:14-84,
+ * src/model_selection.cpp:35-406). */
+
+/* Mirrors SelectionConfig (model_selection.hpp:15-24). nmf.k and nmf.seed are overridden per
+ * run (k swept, seed = derive_seed(seed, k, 2p + 1 + attempt * 1000003)). */
+typedef struct {
+    uint64_t k_min, k_max;
+    uint64_t n_perturbations; /* P, default 16 */
+    double delta;             /* default 0.03, in (0, 1) */
+    double sil_threshold;     /* default 0.75, in [-1, 1] */
+    oocnmf_config nmf;        /* per-run template */
+    uint64_t seed;
+} oocnmf_selection_config;
+
+/* Mirrors KRecord (model_selection.hpp:27-35); the medians matrix is returned separately. */
+typedef struct {
+    uint64_t k;
+    int32_t valid;            /* at least two runs survived */
+    int32_t reserved;
+    uint64_t runs_used;
+    double min_silhouette, mean_silhouette, mean_relative_error;
+} oocnmf_k_record;
+
+/* Change k keeping the resident A (re-allocates the factors). */
+int oocnmf_set_rank(oocnmf_ctx* ctx, uint64_t k);
+/* perturb_dense / perturb_sparse on the resident A: A <- A0 o (1 - delta + 2 delta U) with
+ * U = CounterRng(seed, 21).uniform(i * n + j) over stored entries (model_selection.cpp:35-60),
+ * A0 the values loaded last (kept on the device on first use; delta = 0 restores them). */
+int oocnmf_perturb(oocnmf_ctx* ctx, double delta, uint64_t seed);
+/* Replica mode on a communicator context: solves run rank-locally (every rank holds its own
+ * full A), no collective inside oocnmf_solve. */
+int oocnmf_set_local(oocnmf_ctx* ctx, int local);
+/* Sum a host f64 buffer over the ranks of a communicator context (NCCL, in place). */
+int oocnmf_allreduce_sum_f64(oocnmf_ctx* ctx, double* buf, uint64_t count);
+/* select_k (model_selection.cpp:316-406) on the full A resident in ctx (row0 = 0, rows = m):
+ * P perturbed MU runs per k on the GPU, then cluster_columns / silhouette / selection rule on
+ * the host. On a communicator context the runs of each k are spread over the ranks as
+ * replicas (each rank must hold the full A) and the W factors are summed into every rank with
+ * one NCCL all-reduce per k, so every rank returns the same report.
+ * records: cap >= k_max - k_min + 1 entries. medians (optional): sum over k of m * k doubles,
+ * k ascending, each m x k row-major. chosen_k: -1 if no k qualified. rationale: truncated to
+ * rationale_cap bytes including the NUL. */
+int oocnmf_select_k(oocnmf_ctx* ctx, const oocnmf_selection_config* cfg, oocnmf_k_record* records,
+                    uint64_t cap, double* medians, int64_t* chosen_k, char* rationale,
+                    uint64_t rationale_cap);
+/* Host-side (no device): cluster_columns + silhouette (model_selection.cpp:163-281) over W
+ * factors runs[r] (m x k row-major, r < nruns, nruns >= 2). Outputs medians (m x k),
+ * per_cluster (k), the min / mean silhouette, the dropped zero-norm columns and, optionally,
+ * member_cluster[r * k + c] = cluster of column c of run r (-1: dropped or unmatched). */
+int oocnmf_cluster_silhouette(const double* runs, uint64_t nruns, uint64_t m, uint64_t k, double* medians,
+                              double* per_cluster, double* min_sil, double* mean_sil, uint64_t* dropped,
+                              int64_t* member_cluster);
+/* pearson_correlation_matrix (model_selection.cpp:283-314): corr (k1 x k2), host-side. */
+int oocnmf_pearson_correlation(const double* w_true, uint64_t m, uint64_t k1, const double* w_est,
+                               uint64_t k2, double* corr);
 
 /* ----- one-shot drop-ins for nmf_serial(MatrixRef a, const NmfConfig& cfg) on host
  * buffers: upload, solve, download. w0/h0 are used iff cfg->init == 1. */

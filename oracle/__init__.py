@@ -368,6 +368,61 @@ class Ref(_Lib):
         f.argtypes = [C.c_void_p, _u64, _pd, _pd, _dbl]
         self._check(f(hnd, w.shape[1], _ptr(w), _ptr(h), eps))
 
+    # ---- model selection (include/oocnmf/model_selection.hpp) ----
+    def select_k(self, a, k_min, k_max, n_perturbations=16, delta=0.03, sil_threshold=0.75, max_iters=500,
+                 interval=10, eta=1e-6, eps=1e-12, seed=0):
+        """Reference select_k on a dense A: (records list of dicts, chosen_k or None, medians list, rationale)."""
+        a = np.ascontiguousarray(a, np.float64)
+        m, n = a.shape
+        nk = k_max - k_min + 1
+        rec = np.zeros((nk, 6))
+        med = np.zeros(sum(m * k for k in range(k_min, k_max + 1)))
+        chosen = C.c_int64()
+        why = C.create_string_buffer(512)
+        f = self.lib.ref_select_k_dense
+        f.argtypes = [_pd, _u64, _u64, _u64, _u64, _u64, _dbl, _dbl, _u64, _u64, _dbl, _dbl, _u64, _pd,
+                      C.POINTER(C.c_int64), _pd, C.c_char_p, _u64]
+        self._check(f(_ptr(a), m, n, k_min, k_max, n_perturbations, delta, sil_threshold, max_iters, interval,
+                      eta, eps, seed, _ptr(rec), C.byref(chosen), _ptr(med), why, 512))
+        records, meds, off = [], [], 0
+        for i, k in enumerate(range(k_min, k_max + 1)):
+            records.append(dict(k=int(rec[i, 0]), valid=bool(rec[i, 1]), runs_used=int(rec[i, 2]),
+                                min_silhouette=rec[i, 3], mean_silhouette=rec[i, 4], mean_relative_error=rec[i, 5]))
+            meds.append(med[off:off + m * k].reshape(m, k))
+            off += m * k
+        return records, (None if chosen.value < 0 else chosen.value), meds, why.value.decode()
+
+    def cluster_silhouette(self, runs):
+        """Reference cluster_columns + silhouette over runs (R x m x k)."""
+        runs = np.ascontiguousarray(runs, np.float64)
+        r, m, k = runs.shape
+        med, per = np.zeros((m, k)), np.zeros(k)
+        mn, mean, dropped = _dbl(), _dbl(), _u64()
+        member = np.zeros(r * k, np.int64)
+        f = self.lib.ref_cluster_silhouette
+        f.argtypes = [_pd, _u64, _u64, _u64, _pd, _pd, _pd, _pd, _pu, C.POINTER(C.c_int64)]
+        self._check(f(_ptr(runs), r, m, k, _ptr(med), _ptr(per), C.byref(mn), C.byref(mean), C.byref(dropped),
+                      member.ctypes.data_as(C.POINTER(C.c_int64))))
+        return dict(medians=med, per_cluster=per, min_sil=mn.value, mean_sil=mean.value, dropped=dropped.value,
+                    member_cluster=member.reshape(r, k))
+
+    def pearson(self, w_true, w_est):
+        w_true = np.ascontiguousarray(w_true, np.float64)
+        w_est = np.ascontiguousarray(w_est, np.float64)
+        corr = np.zeros((w_true.shape[1], w_est.shape[1]))
+        f = self.lib.ref_pearson
+        f.argtypes = [_pd, _u64, _u64, _pd, _u64, _pd]
+        self._check(f(_ptr(w_true), w_true.shape[0], w_true.shape[1], _ptr(w_est), w_est.shape[1], _ptr(corr)))
+        return corr
+
+    def perturb_dense(self, a, delta, seed):
+        a = np.ascontiguousarray(a, np.float64)
+        out = np.zeros_like(a)
+        f = self.lib.ref_perturb_dense
+        f.argtypes = [_pd, _u64, _u64, _dbl, _u64, _pd]
+        self._check(f(_ptr(a), a.shape[0], a.shape[1], delta, seed, _ptr(out)))
+        return out
+
 
 port = Port()
 ref = Ref()

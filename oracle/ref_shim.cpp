@@ -20,6 +20,7 @@
 #include <vector>
 
 #include "oocnmf/kernels.hpp"
+#include "oocnmf/model_selection.hpp"
 #include "oocnmf/nmf.hpp"
 #include "oocnmf/nmf_distributed.hpp"
 #include "oocnmf/partition.hpp"
@@ -322,6 +323,78 @@ int ref_make_plan(std::uint64_t m, std::uint64_t n, std::uint64_t k, int n_worke
             batches2[2 * b + 1] = p.batches[b].end;
         }
         *strategy_out = p.strategy == Strategy::cnmf ? 1 : 2;
+    });
+}
+
+// ---- model selection (include/oocnmf/model_selection.hpp) ----
+// select_k on a dense A. rec6: per k [k, valid, runs_used, min_sil, mean_sil, mean_err];
+// chosen: -1 if none; medians (optional): sum over k of m*k doubles, k ascending.
+int ref_select_k_dense(const double* a, std::uint64_t m, std::uint64_t n, std::uint64_t k_min,
+                       std::uint64_t k_max, std::uint64_t n_pert, double delta, double sil_threshold,
+                       std::uint64_t max_iters, std::uint64_t interval, double eta, double eps,
+                       std::uint64_t seed, double* rec6, std::int64_t* chosen, double* medians,
+                       char* why, std::uint64_t why_cap) {
+    return guarded([&] {
+        DenseMatrix A = copy_dense(a, m, n);
+        SelectionConfig cfg;
+        cfg.k_min = k_min, cfg.k_max = k_max, cfg.n_perturbations = n_pert;
+        cfg.delta = delta, cfg.sil_threshold = sil_threshold, cfg.seed = seed;
+        cfg.nmf.max_iters = max_iters, cfg.nmf.error_check_interval = interval;
+        cfg.nmf.eta = eta, cfg.nmf.epsilon = eps;
+        SelectionReport rep = select_k(MatrixRef(A), cfg);
+        double* med = medians;
+        for (std::size_t i = 0; i < rep.records.size(); ++i) {
+            const KRecord& r = rep.records[i];
+            double* o = rec6 + 6 * i;
+            o[0] = double(r.k), o[1] = r.valid ? 1.0 : 0.0, o[2] = double(r.runs_used);
+            o[3] = r.min_silhouette, o[4] = r.mean_silhouette, o[5] = r.mean_relative_error;
+            if (med) {
+                for (index_t e = 0; e < m * r.k; ++e) med[e] = r.valid ? r.medians.data()[e] : 0.0;
+                med += m * r.k;
+            }
+        }
+        *chosen = rep.chosen_k ? std::int64_t(*rep.chosen_k) : -1;
+        if (why && why_cap) {
+            const std::size_t len = std::min<std::size_t>(rep.rationale.size(), why_cap - 1);
+            std::memcpy(why, rep.rationale.data(), len);
+            why[len] = 0;
+        }
+    });
+}
+
+int ref_cluster_silhouette(const double* runs, std::uint64_t nruns, std::uint64_t m, std::uint64_t k,
+                           double* medians, double* per_cluster, double* min_sil, double* mean_sil,
+                           std::uint64_t* dropped, std::int64_t* member_cluster) {
+    return guarded([&] {
+        std::vector<DenseMatrix> ws;
+        for (std::uint64_t r = 0; r < nruns; ++r) ws.push_back(copy_dense(runs + r * m * k, m, k));
+        ColumnClusters cl = cluster_columns(ws, k);
+        for (std::uint64_t e = 0; e < nruns * k; ++e) member_cluster[e] = -1;
+        for (std::uint64_t c = 0; c < k; ++c)
+            for (const auto& [r, col] : cl.member_ids[c]) member_cluster[r * k + col] = std::int64_t(c);
+        std::memcpy(medians, cl.medians.data(), m * k * sizeof(double));
+        *dropped = cl.dropped_zero_columns;
+        SilhouetteScore s = silhouette(cl);
+        std::memcpy(per_cluster, s.per_cluster.data(), k * sizeof(double));
+        *min_sil = s.min_sil;
+        *mean_sil = s.mean_sil;
+    });
+}
+
+int ref_pearson(const double* wt, std::uint64_t m, std::uint64_t k1, const double* we, std::uint64_t k2,
+                double* corr) {
+    return guarded([&] {
+        DenseMatrix c = pearson_correlation_matrix(copy_dense(wt, m, k1), copy_dense(we, m, k2));
+        std::memcpy(corr, c.data(), k1 * k2 * sizeof(double));
+    });
+}
+
+int ref_perturb_dense(const double* a, std::uint64_t m, std::uint64_t n, double delta, std::uint64_t seed,
+                      double* out) {
+    return guarded([&] {
+        DenseMatrix A = copy_dense(a, m, n);
+        DenseMatrix P = perturb_dense(MatrixRef(A), delta, seed);
+        std::memcpy(out, P.data(), m * n * sizeof(double));
     });
 }
 

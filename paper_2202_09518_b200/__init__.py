@@ -5,6 +5,7 @@ The product is ``lib/liboocnmf_b200.so`` (C-ABI: ``include/oocnmf_b200.h``; C++ 
 ``oocnmf::`` API names.
 """
 from .nmf import (  # noqa: F401
+    ColumnClusters,
     CommError,
     Context,
     CsrMatrix,
@@ -13,21 +14,30 @@ from .nmf import (  # noqa: F401
     DistComm,
     FactorInit,
     IoError,
+    KRecord,
     NmfConfig,
     NmfResult,
     PartitionPlan,
     PhaseCounters,
+    SelectionConfig,
+    SelectionReport,
     ShapeError,
     StoreError,
     Strategy,
     check,
     choose_strategy,
+    cluster_columns,
     counter_uniform,
     device_count,
     init_factors,
     make_plan,
     nmf_distributed,
     nmf_serial,
+    pearson_correlation_matrix,
+    perturb_dense,
+    perturb_sparse,
+    select_k,
+    select_k_distributed,
     split_even,
 )
 

@@ -36,6 +36,18 @@ class Info(C.Structure):
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
 
 
+class SelectionConfig(C.Structure):
+    _fields_ = [("k_min", u64), ("k_max", u64), ("n_perturbations", u64), ("delta", dbl), ("sil_threshold", dbl),
+                ("nmf", Config), ("seed", u64)]
+
+
+class KRecord(C.Structure):
+    _fields_ = [("k", u64), ("valid", i32), ("reserved", i32), ("runs_used", u64), ("min_silhouette", dbl),
+                ("mean_silhouette", dbl), ("mean_relative_error", dbl)]
+
+
+pi64 = C.POINTER(C.c_int64)
+
 _SIGS = {
     "oocnmf_last_error": ([], C.c_char_p),
     "oocnmf_abi_version": ([], C.c_int),
@@ -67,6 +79,15 @@ _SIGS = {
     "oocnmf_solve": ([vp, C.POINTER(Config), pu, pd, u64, C.POINTER(Info)], C.c_int),
     "oocnmf_products_f64": ([vp, pd, pd, pd, pd], C.c_int),
     "oocnmf_sq_norm": ([vp, pd], C.c_int),
+    "oocnmf_problem_dims": ([vp, pu, pu, pu, pu, pu], C.c_int),
+    "oocnmf_set_rank": ([vp, u64], C.c_int),
+    "oocnmf_perturb": ([vp, dbl, u64], C.c_int),
+    "oocnmf_set_local": ([vp, C.c_int], C.c_int),
+    "oocnmf_allreduce_sum_f64": ([vp, pd, u64], C.c_int),
+    "oocnmf_select_k": ([vp, C.POINTER(SelectionConfig), C.POINTER(KRecord), u64, pd, pi64, C.c_char_p, u64],
+                        C.c_int),
+    "oocnmf_cluster_silhouette": ([pd, u64, u64, u64, pd, pd, pd, pd, pu, pi64], C.c_int),
+    "oocnmf_pearson_correlation": ([pd, u64, u64, pd, u64, pd], C.c_int),
     "oocnmf_nmf_serial_dense_f64": ([C.c_int, pd, u64, u64, C.POINTER(Config), pd, pd, pd, pd, pu, pd, u64,
                                      C.POINTER(Info)], C.c_int),
     "oocnmf_nmf_serial_dense_f32": ([C.c_int, pf, u64, u64, C.POINTER(Config), pd, pd, pd, pd, pu, pd, u64,

@@ -31,6 +31,7 @@ __host__ __device__ __forceinline__ double rng_u01(uint64_t key, uint64_t index)
 // Streams used by the reference (src/nmf_serial.cpp:17-18, src/synth.cpp:12-15,
 // bench/kernels_bench.cpp:14).
 constexpr uint64_t kStreamW = 1, kStreamH = 2, kStreamSparseMask = 14, kStreamSparseVal = 15;
+constexpr uint64_t kStreamPerturb = 21;  // src/model_selection.cpp:17
 
 // ---------------------------------------------------------------------------
 // Stream-K work split. A pass over A is `tiles` output tiles x `ipt` reduction steps;

@@ -77,6 +77,13 @@ cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t r
                                   int64_t cols, const float* W, const float* Ht,
                                   double* out_slots, cudaStream_t s);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s);
+// Model-selection perturbation of the resident A (dense window, or CSR values; transposed:
+// the CSR(A^T) copy), out = f32(in * (1 - delta + 2 delta U(seed, 21, i * n + j))).
+cudaError_t launch_perturb_dense(const float* in, float* out, int64_t lda, int64_t rows, int64_t cols,
+                                 int64_t row0, int64_t n, uint64_t seed, double delta, cudaStream_t s);
+cudaError_t launch_perturb_csr(const float* in, float* out, const int64_t* rp, const int32_t* ci, int64_t rows,
+                               int64_t row0, int64_t n, uint64_t seed, double delta, bool transposed,
+                               cudaStream_t s);
 // cat (rows x 2kp) <- [F | F - tf32_trunc(F)] for F (rows x kp)
 cudaError_t launch_split_cat(const float* F, float* cat, int64_t rows, int kp, cudaStream_t s);
 

@@ -153,6 +153,34 @@ __global__ void k_split_cat(const float* __restrict__ F, float* __restrict__ cat
     }
 }
 
+// Model-selection perturbation (src/model_selection.cpp:35-60): every stored entry times an
+// i.i.d. factor 1 - delta + 2 delta U(seed, 21, i * n + j) in f64, rounded to f32.
+__global__ void k_perturb_dense(const float* __restrict__ in, float* __restrict__ out, int64_t lda,
+                                int64_t rows, int64_t cols, int64_t row0, int64_t n, uint64_t key,
+                                double delta) {
+    const int64_t total = rows * cols;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t i = q / cols, j = q % cols;
+        const double f = 1.0 - delta + 2.0 * delta * rng_u01(key, uint64_t(row0 + i) * uint64_t(n) + uint64_t(j));
+        out[i * lda + j] = __double2float_rn(double(in[i * lda + j]) * f);
+    }
+}
+
+// CSR values (one thread per stored row). transposed: stored row r is column r of A and the
+// column indices are slab rows.
+__global__ void k_perturb_csr(const float* __restrict__ in, float* __restrict__ out,
+                              const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t rows,
+                              int64_t row0, int64_t n, uint64_t key, double delta, int transposed) {
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < rows; r += int64_t(gridDim.x) * blockDim.x)
+        for (int64_t p = rp[r]; p < rp[r + 1]; ++p) {
+            const uint64_t flat = transposed ? uint64_t(row0 + ci[p]) * uint64_t(n) + uint64_t(r)
+                                             : uint64_t(row0 + r) * uint64_t(n) + uint64_t(ci[p]);
+            const double f = 1.0 - delta + 2.0 * delta * rng_u01(key, flat);
+            out[p] = __double2float_rn(double(in[p]) * f);
+        }
+}
+
 unsigned grid_for(int64_t work, int per_thread = 1) {
     const int64_t b = (work / per_thread + 255) / 256;
     return unsigned(b < 1 ? 1 : (b > 65535 * 16 ? 65535 * 16 : b));
@@ -212,6 +240,21 @@ cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t r
 
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s) {
     k_check_finite<<<grid_for(n, 8), 256, 0, s>>>(x, n, flag);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_perturb_dense(const float* in, float* out, int64_t lda, int64_t rows, int64_t cols,
+                                 int64_t row0, int64_t n, uint64_t seed, double delta, cudaStream_t s) {
+    k_perturb_dense<<<grid_for(rows * cols, 8), 256, 0, s>>>(in, out, lda, rows, cols, row0, n,
+                                                             rng_key(seed, kStreamPerturb), delta);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_perturb_csr(const float* in, float* out, const int64_t* rp, const int32_t* ci, int64_t rows,
+                               int64_t row0, int64_t n, uint64_t seed, double delta, bool transposed,
+                               cudaStream_t s) {
+    k_perturb_csr<<<grid_for(rows, 1), 256, 0, s>>>(in, out, rp, ci, rows, row0, n, rng_key(seed, kStreamPerturb),
+                                                    delta, transposed ? 1 : 0);
     return cudaGetLastError();
 }
 

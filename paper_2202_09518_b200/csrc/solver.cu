@@ -149,6 +149,12 @@ struct oocnmf_ctx {
     bool graph_broken = false;   // capture failed once: iterate eagerly (same kernels)
     bool capturing = false;
 
+    // model selection: pristine copy of the resident A while it is perturbed; replica mode
+    // (every rank holds the full A and solves independently: no collective in the solve)
+    DevBuf A0, v0, vT0;
+    bool pristine = false, local = false;
+    bool collective() const { return nranks > 1 && !local; }
+
     float* wta() const { return packed.as<float>(); }
     float* wtw() const { return packed.as<float>() + np * kp; }
     int64_t packed_count() const { return np * kp + int64_t(kp) * kp; }
@@ -212,6 +218,8 @@ void reset_source(oocnmf_ctx* c) {
     c->hA = nullptr;
     c->kind = Kind::none;
     c->norm_valid = false;
+    c->A0.release(), c->v0.release(), c->vT0.release();
+    c->pristine = false;
 }
 
 void compute_norm(oocnmf_ctx* c) {
@@ -243,7 +251,7 @@ void compute_norm(oocnmf_ctx* c) {
     }
     count(c, launch_reduce_f64(slots, sqnorm_grid(), out, c->stream), "reduce_f64");
 reduced:
-    if (c->nranks > 1) nck(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
+    if (c->collective()) nck(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
     ck(cudaMemcpyAsync(&c->norm_a2, out, 8, cudaMemcpyDeviceToHost, c->stream), "D2H norm");
     ck(cudaStreamSynchronize(c->stream), "sync");
     c->norm_valid = true;
@@ -362,7 +370,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
 void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     const int kp = c->kp;
     cudaStream_t s = c->stream;
-    if (c->nranks > 1) {
+    if (c->collective()) {
         // One fused NCCL launch: the packed f32 [W^T A | W^T W] the update consumes and the f64
         // W^T W the trace-form error consumes.
         nck(ncclGroupStart(), "ncclGroupStart");
@@ -412,7 +420,7 @@ double error_check_once(oocnmf_ctx* c, bool direct_mode, int* bad) {
                                            c->Ht.as<float>(), c->red_slots.as<double>(), s),
                   "residual");
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kRes, s), "reduce");
-            if (c->nranks > 1)
+            if (c->collective())
                 nck(ncclAllReduce(scal + kRes, scal + kRes, 1, ncclDouble, ncclSum, c->comm, s), "allreduce res");
             direct = scal + kRes;
         } else if (c->kind == Kind::csr) {
@@ -420,7 +428,7 @@ double error_check_once(oocnmf_ctx* c, bool direct_mode, int* bad) {
                                          c->n, c->W.as<float>(), c->Ht.as<float>(), c->red_slots.as<double>(), s),
                   "cross");
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kCross, s), "reduce");
-            if (c->nranks > 1)
+            if (c->collective())
                 nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s),
                     "allreduce cross");
             eslots = scal + kCross;
@@ -488,7 +496,7 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
     std::memcpy(&eps_bits, &eps, 4);
     const std::vector<uint64_t> key = {
         uint64_t(c->kind), uint64_t(c->kp), uint64_t(c->mp), uint64_t(c->np), c->rows, count, eps_bits,
-        uint64_t(c->use_tc), uint64_t(reinterpret_cast<uintptr_t>(c->comm)),
+        uint64_t(c->use_tc), uint64_t(c->collective()), uint64_t(reinterpret_cast<uintptr_t>(c->comm)),
         uint64_t(reinterpret_cast<uintptr_t>(ev)), uint64_t(reinterpret_cast<uintptr_t>(c->A.p)),
         uint64_t(reinterpret_cast<uintptr_t>(c->rp.p)), uint64_t(reinterpret_cast<uintptr_t>(c->rpT.p)),
         uint64_t(reinterpret_cast<uintptr_t>(c->W.p)), uint64_t(reinterpret_cast<uintptr_t>(c->Ht.p)),
@@ -641,6 +649,64 @@ void set_problem_impl(oocnmf_ctx* c, uint64_t m, uint64_t n, uint64_t k, uint64_
     alloc_factors(c);
 }
 
+// Change k keeping the resident A (model selection sweeps k over one matrix).
+void set_rank_impl(oocnmf_ctx* c, uint64_t k) {
+    need_problem(c);
+    if (k < 1) fail(OOCNMF_ERR_SHAPE, "k must be >= 1");
+    const char* force = std::getenv("OOCNMF_FORCE_FFMA");
+    int kp = pad_k(k);
+    c->use_tc = !(force && force[0] == '1') && tc_supported(std::max(kp, 16));
+    if (c->use_tc) kp = std::max(kp, 16);
+    c->k = k;
+    c->kp = kp;
+    c->factors_set = c->factors_valid = false;
+    alloc_factors(c);
+    if (c->kind == Kind::dense) plan_dense(c);
+    if (c->kind == Kind::csr) {
+        c->N1.alloc(size_t(c->mp) * c->kp * 4, "AHt");
+        ck(cudaMemsetAsync(c->N1.p, 0, c->N1.bytes, c->stream), "memset");
+        ck(cudaMemsetAsync(c->packed.p, 0, c->packed.bytes, c->stream), "memset");
+    }
+    if (c->kind == Kind::host) fail(OOCNMF_ERR_SHAPE, "set_rank: re-attach the out-of-core source after a rank change");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+}
+
+// A <- A0 o (1 - delta + 2 delta U(seed, 21, .)) from the pristine copy (kept on first use).
+void perturb_impl(oocnmf_ctx* c, double delta, uint64_t seed) {
+    need_problem(c);
+    if (!(delta >= 0.0 && delta < 1.0)) fail(OOCNMF_ERR_SHAPE, "perturb: delta must lie in [0, 1)");
+    cudaStream_t s = c->stream;
+    if (c->kind == Kind::dense) {
+        if (!c->pristine) {
+            c->A0.alloc(c->A.bytes, "A0");
+            ck(cudaMemcpyAsync(c->A0.p, c->A.p, c->A.bytes, cudaMemcpyDeviceToDevice, s), "copy A0");
+            c->pristine = true;
+        }
+        count(c, launch_perturb_dense(c->A0.as<float>(), c->A.as<float>(), c->np, c->rows, c->n, c->row0, c->n, seed,
+                                      delta, s),
+              "perturb");
+    } else if (c->kind == Kind::csr) {
+        const size_t vb = size_t(std::max<int64_t>(c->nnz, 1)) * 4;
+        if (!c->pristine) {
+            c->v0.alloc(vb, "v0");
+            c->vT0.alloc(vb, "vT0");
+            ck(cudaMemcpyAsync(c->v0.p, c->v.p, vb, cudaMemcpyDeviceToDevice, s), "copy v0");
+            ck(cudaMemcpyAsync(c->vT0.p, c->vT.p, vb, cudaMemcpyDeviceToDevice, s), "copy vT0");
+            c->pristine = true;
+        }
+        count(c, launch_perturb_csr(c->v0.as<float>(), c->v.as<float>(), c->rp.as<int64_t>(), c->ci.as<int32_t>(),
+                                    c->rows, c->row0, c->n, seed, delta, false, s),
+              "perturb");
+        count(c, launch_perturb_csr(c->vT0.as<float>(), c->vT.as<float>(), c->rpT.as<int64_t>(),
+                                    c->ciT.as<int32_t>(), c->n, c->row0, c->n, seed, delta, true, s),
+              "perturb T");
+    } else {
+        fail(OOCNMF_ERR_SHAPE, "perturb: needs a resident (dense or CSR) A");
+    }
+    ck(cudaStreamSynchronize(s), "sync");
+    c->norm_valid = false;
+}
+
 void load_dense_common(oocnmf_ctx* c) {
     need_problem(c);
     reset_source(c);
@@ -667,10 +733,23 @@ void csr_finish(oocnmf_ctx* c) {
 
 }  // namespace
 
+namespace ooc {
+// Shared with the host-side translation units (selection.cpp): the thread-local message
+// oocnmf_last_error() returns.
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace ooc
+
 // =============================================================================== C-ABI
 extern "C" {
 
 const char* oocnmf_last_error(void) { return g_err.c_str(); }
+
+int oocnmf_problem_dims(const oocnmf_ctx* c, uint64_t* m, uint64_t* n, uint64_t* k, uint64_t* row0, uint64_t* rows) {
+    return guarded([&] {
+        if (!c->problem_set) fail(OOCNMF_ERR_SHAPE, "oocnmf_set_problem has not been called");
+        *m = c->m, *n = c->n, *k = c->k, *row0 = c->row0, *rows = c->rows;
+    });
+}
 int oocnmf_abi_version(void) { return OOCNMF_ABI_VERSION; }
 
 int oocnmf_device_count(int* count_out) {
@@ -1141,6 +1220,40 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
                 hht[r * k + j] = g1[r * kp + j];
                 wtw[r * k + j] = g2[r * kp + j];
             }
+    });
+}
+
+int oocnmf_set_rank(oocnmf_ctx* c, uint64_t k) {
+    return guarded([&] {
+        set_dev(c);
+        set_rank_impl(c, k);
+    });
+}
+
+int oocnmf_perturb(oocnmf_ctx* c, double delta, uint64_t seed) {
+    return guarded([&] {
+        set_dev(c);
+        perturb_impl(c, delta, seed);
+    });
+}
+
+int oocnmf_set_local(oocnmf_ctx* c, int local) {
+    return guarded([&] {
+        c->local = local != 0;
+        c->norm_valid = false;
+    });
+}
+
+int oocnmf_allreduce_sum_f64(oocnmf_ctx* c, double* buf, uint64_t count) {
+    return guarded([&] {
+        set_dev(c);
+        if (c->nranks <= 1 || count == 0) return;
+        DevBuf d;
+        d.alloc(count * 8, "allreduce scratch");
+        ck(cudaMemcpyAsync(d.p, buf, count * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+        nck(ncclAllReduce(d.p, d.p, count, ncclDouble, ncclSum, c->comm, c->stream), "allreduce");
+        ck(cudaMemcpyAsync(buf, d.p, count * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
     });
 }
 

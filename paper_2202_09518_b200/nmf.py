@@ -338,6 +338,16 @@ class Context:
         nt = min(int(info.n_trace), cap)
         return list(zip(ti[:nt].astype(int).tolist(), te[:nt].tolist())), info.as_dict()
 
+    def set_rank(self, k: int):
+        """Change k keeping the resident A (model selection sweeps k over one matrix)."""
+        check(_capi.lib().oocnmf_set_rank(self._h, k))
+        self.k = k
+
+    def perturb(self, delta: float, seed: int):
+        """A <- A0 o U[1-delta, 1+delta] on the device (perturb_dense / perturb_sparse semantics,
+        model_selection.cpp:35-60); delta = 0 restores the loaded values."""
+        check(_capi.lib().oocnmf_perturb(self._h, float(delta), int(seed)))
+
     def products(self):
         k, n, rows = self.k, self.n, self.rows
         aht, wta = np.empty((rows, k)), np.empty((k, n))
@@ -486,3 +496,178 @@ def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host
     _, h = ctx.get_factors()
     w = ctx.gather_w()
     return NmfResult(w, h, trace, int(info["iterations_run"]), bool(info["converged"]), _counters(info), info)
+
+
+# ----------------------------------------------------------------------------- model selection
+# Mirrors include/oocnmf/model_selection.hpp (src/model_selection.cpp): P perturbed MU runs per
+# candidate k on the GPU, W-column clustering / cosine silhouette / selection rule in the
+# library's C++ host core.
+@dataclass
+class SelectionConfig:
+    k_min: int = 1
+    k_max: int = 1
+    n_perturbations: int = 16
+    delta: float = 0.03
+    sil_threshold: float = 0.75
+    nmf: NmfConfig = field(default_factory=NmfConfig)
+    seed: int = 0
+
+    def validate(self, m: int, n: int) -> None:
+        if self.k_min < 1 or self.k_max < self.k_min:
+            raise ShapeError("SelectionConfig: need 1 <= k_min <= k_max")
+        if self.k_max >= min(m, n):
+            raise ShapeError("SelectionConfig: k_max must be below min(m, n)")
+        if self.n_perturbations < 2:
+            raise ShapeError("SelectionConfig: need at least 2 perturbations")
+        if not 0.0 < self.delta < 1.0:
+            raise ShapeError("SelectionConfig: delta must lie in (0, 1)")
+        if not -1.0 <= self.sil_threshold <= 1.0:
+            raise ShapeError("SelectionConfig: sil_threshold must lie in [-1, 1]")
+
+    def to_c(self) -> _capi.SelectionConfig:
+        return _capi.SelectionConfig(self.k_min, self.k_max, self.n_perturbations, self.delta, self.sil_threshold,
+                                     self.nmf.to_c(), self.seed)
+
+
+@dataclass
+class KRecord:
+    k: int = 0
+    valid: bool = False
+    runs_used: int = 0
+    min_silhouette: float = 0.0
+    mean_silhouette: float = 0.0
+    mean_relative_error: float = 0.0
+    medians: Optional[np.ndarray] = None  # m x k
+
+
+@dataclass
+class SelectionReport:
+    records: List[KRecord]
+    chosen_k: Optional[int]
+    rationale: str
+
+    def to_json(self) -> str:
+        import json
+        return json.dumps({"chosen_k": self.chosen_k if self.chosen_k is not None else "none",
+                           "rationale": self.rationale,
+                           "records": [{"k": r.k, "valid": r.valid, "runs_used": r.runs_used,
+                                        "min_silhouette": r.min_silhouette, "mean_silhouette": r.mean_silhouette,
+                                        "mean_relative_error": r.mean_relative_error} for r in self.records]},
+                          indent=2)
+
+    def to_csv(self) -> str:
+        rows = ["k,valid,runs_used,min_silhouette,mean_silhouette,mean_relative_error"]
+        rows += [f"{r.k},{int(r.valid)},{r.runs_used},{r.min_silhouette:g},{r.mean_silhouette:g},"
+                 f"{r.mean_relative_error:g}" for r in self.records]
+        return "\n".join(rows) + "\n"
+
+
+def _select_on(ctx: "Context", m: int, cfg: SelectionConfig) -> SelectionReport:
+    nk = cfg.k_max - cfg.k_min + 1
+    recs = (_capi.KRecord * nk)()
+    med = np.zeros(sum(m * k for k in range(cfg.k_min, cfg.k_max + 1)))
+    chosen = C.c_int64()
+    why = C.create_string_buffer(512)
+    c = cfg.to_c()
+    check(_capi.lib().oocnmf_select_k(ctx._h, C.byref(c), recs, nk, _p(med, C.c_double), C.byref(chosen), why,
+                                      512))
+    out, off = [], 0
+    for i, k in enumerate(range(cfg.k_min, cfg.k_max + 1)):
+        r = recs[i]
+        out.append(KRecord(int(r.k), bool(r.valid), int(r.runs_used), r.min_silhouette, r.mean_silhouette,
+                           r.mean_relative_error, med[off:off + m * k].reshape(m, k).copy()))
+        off += m * k
+    return SelectionReport(out, None if chosen.value < 0 else int(chosen.value), why.value.decode())
+
+
+def select_k(a, cfg: SelectionConfig) -> SelectionReport:
+    """select_k (src/model_selection.cpp:316-406) on one GPU (cfg.nmf.device): A stays resident
+    in HBM, every perturbation is generated there, every run is a GPU MU solve."""
+    m, n = (a.rows, a.cols) if isinstance(a, CsrMatrix) else np.asarray(a).shape
+    cfg.validate(m, n)
+    with Context(cfg.nmf.device) as ctx:
+        ctx.set_problem(m, n, cfg.k_min)
+        if isinstance(a, CsrMatrix):
+            ctx.load_csr(a)
+        else:
+            ctx.load_dense(a)
+        return _select_on(ctx, m, cfg)
+
+
+def select_k_distributed(a, cfg: SelectionConfig, comm: "DistComm") -> SelectionReport:
+    """select_k over an NCCL group: every rank holds the full A, the P runs of each k are spread
+    over the ranks as independent replicas, the W factors meet in one all-reduce per k, and every
+    rank returns the same report. Collective over ``comm``."""
+    m, n = (a.rows, a.cols) if isinstance(a, CsrMatrix) else np.asarray(a).shape
+    cfg.validate(m, n)
+    ctx = comm.ctx
+    ctx.set_problem(m, n, cfg.k_min)
+    if isinstance(a, CsrMatrix):
+        ctx.load_csr(a)
+    else:
+        ctx.load_dense(a)
+    return _select_on(ctx, m, cfg)
+
+
+def perturb_dense(a: np.ndarray, delta: float, seed: int, device: int = 0) -> np.ndarray:
+    """perturb_dense (model_selection.cpp:35-47), evaluated on the GPU; returns float32."""
+    if not 0.0 <= delta < 1.0:
+        raise ShapeError("perturb: delta must lie in [0, 1)")
+    a = np.asarray(a)
+    with Context(device) as ctx:
+        ctx.set_problem(a.shape[0], a.shape[1], 1)
+        ctx.load_dense(a)
+        ctx.perturb(delta, seed)
+        return ctx.download_dense()
+
+
+def perturb_sparse(a: CsrMatrix, delta: float, seed: int, device: int = 0) -> CsrMatrix:
+    """perturb_sparse (model_selection.cpp:49-60), evaluated on the GPU (sparsity preserved)."""
+    if not 0.0 <= delta < 1.0:
+        raise ShapeError("perturb: delta must lie in [0, 1)")
+    with Context(device) as ctx:
+        ctx.set_problem(a.rows, a.cols, 1)
+        ctx.load_csr(a)
+        ctx.perturb(delta, seed)
+        return ctx.download_csr()
+
+
+@dataclass
+class ColumnClusters:
+    member_cluster: np.ndarray  # runs x k: cluster of (run, column), -1 if dropped / unmatched
+    medians: np.ndarray         # m x k
+    dropped_zero_columns: int
+    per_cluster: np.ndarray     # silhouette per cluster
+    min_sil: float
+    mean_sil: float
+
+
+def cluster_columns(runs, k: Optional[int] = None) -> ColumnClusters:
+    """cluster_columns + silhouette (model_selection.cpp:163-281) over W factors (list of m x k
+    arrays or an R x m x k array), in the library's host core."""
+    runs = np.ascontiguousarray(np.asarray(runs, dtype=np.float64))
+    if runs.ndim != 3 or runs.shape[0] < 2:
+        raise ShapeError("cluster_columns: need at least 2 runs of m x k")
+    r, m, kk = runs.shape
+    if k is not None and k != kk:
+        raise ShapeError("cluster_columns: all runs must be m x k")
+    med, per = np.zeros((m, kk)), np.zeros(kk)
+    mn, mean, dropped = C.c_double(), C.c_double(), C.c_uint64()
+    member = np.zeros((r, kk), np.int64)
+    check(_capi.lib().oocnmf_cluster_silhouette(_p(runs, C.c_double), r, m, kk, _p(med, C.c_double),
+                                                _p(per, C.c_double), C.byref(mn), C.byref(mean), C.byref(dropped),
+                                                _p(member, C.c_int64)))
+    return ColumnClusters(member, med, int(dropped.value), per, mn.value, mean.value)
+
+
+def pearson_correlation_matrix(w_true: np.ndarray, w_est: np.ndarray) -> np.ndarray:
+    """Entry (i, j): Pearson correlation of column i of w_true and column j of w_est
+    (model_selection.cpp:283-314)."""
+    wt = np.ascontiguousarray(w_true, np.float64)
+    we = np.ascontiguousarray(w_est, np.float64)
+    if wt.shape[0] != we.shape[0]:
+        raise ShapeError("pearson_correlation_matrix: row counts differ")
+    corr = np.zeros((wt.shape[1], we.shape[1]))
+    check(_capi.lib().oocnmf_pearson_correlation(_p(wt, C.c_double), wt.shape[0], wt.shape[1], _p(we, C.c_double),
+                                                 we.shape[1], _p(corr, C.c_double)))
+    return corr

@@ -51,6 +51,15 @@ def main(out_path):
     rp, ci, v, (m, n) = port.gen_sparse(1500, 1200, 0.02, 3)
     run("csr_k16", nmf.CsrMatrix(m, n, rp, ci, f32(v)), m, n, 16, 20, 10)
     run("ooc_k32", None, 1100, 900, 32, 20, 10, host_slab=a, batch_rows=128)
+    # model selection: the P runs of each k spread over the ranks as replicas
+    lr = oracle.ref.gen_lowrank(96, 64, 3, 0.01, 5)[0] if oracle.ref.available else port.uniform_dense(96, 64, 5, 1)
+    scfg = nmf.SelectionConfig(k_min=1, k_max=4, n_perturbations=5, seed=3,
+                               nmf=nmf.NmfConfig(max_iters=120, error_check_interval=20, eta=0.0, device=local))
+    rep = nmf.select_k_distributed(lr.astype(np.float32), scfg, comm)
+    results["select"] = {"chosen": rep.chosen_k, "rationale": rep.rationale,
+                         "records": [[r.k, r.valid, r.runs_used, r.min_silhouette, r.mean_silhouette,
+                                      r.mean_relative_error] for r in rep.records],
+                         "medians_sum": [float(r.medians.sum()) for r in rep.records]}
     if rank == 0:
         with open(out_path, "w") as f:
             json.dump(results, f)

@@ -1,0 +1,91 @@
+"""Model selection (NMFk) on the GPU vs the compiled reference.
+
+select_k runs P perturbed MU factorizations per k; ours run on the B200 path (perturbation in
+HBM, tcgen05 passes), the reference's in f64 on the CPU, on the same f32-rounded A with the
+same derived seeds. Per-k records must agree to the tolerance the MU parity bar implies
+(trajectory 1e-4, factors 1e-3) and the chosen k must be identical."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2202_09518_b200 as nmf
+
+pytestmark = pytest.mark.gpu
+needs_ref = pytest.mark.skipif(not oracle.ref.available, reason="needs oracle/_ref")
+
+
+def _lowrank(m, n, k, noise, seed):
+    return oracle.ref.gen_lowrank(m, n, k, noise, seed)[0].astype(np.float32)
+
+
+@needs_ref
+def test_perturb_dense_matches_reference(gpu):
+    a = oracle.port.uniform_dense(123, 77, 4, 9).astype(np.float32)
+    got = nmf.perturb_dense(a, 0.03, 1234, device=gpu)
+    want = oracle.ref.perturb_dense(a.astype(np.float64), 0.03, 1234)
+    np.testing.assert_allclose(got, want, rtol=1e-7, atol=0)  # f32 rounding of the f64 product
+    assert np.all(got != a)  # every entry moved
+
+
+def test_perturb_sparse_keeps_pattern_and_matches_dense(gpu):
+    rp, ci, v, (m, n) = oracle.port.gen_sparse(300, 200, 0.05, 2)
+    s = nmf.CsrMatrix(m, n, rp, ci, v.astype(np.float32).astype(np.float64))
+    p = nmf.perturb_sparse(s, 0.1, 77, device=gpu)
+    assert np.array_equal(p.row_ptr, s.row_ptr) and np.array_equal(p.col_idx, s.col_idx)
+    d = nmf.perturb_dense(s.to_dense().astype(np.float32), 0.1, 77, device=gpu)
+    np.testing.assert_array_equal(p.to_dense(), d.astype(np.float64))
+
+
+@needs_ref
+@pytest.mark.parametrize("k_true,kmax,expect", [(3, 5, 3), (5, 7, 3)])
+def test_select_k_matches_reference(gpu, k_true, kmax, expect):
+    # (at 300 iterations the k = 5 ensemble is not yet stable above k = 3: the reference
+    # chooses 3 there too — the comparison is with the reference, not with k_true)
+    a = _lowrank(120, 90, k_true, 0.01, 11 + k_true)
+    kw = dict(n_perturbations=6, delta=0.03, sil_threshold=0.75, max_iters=300, interval=25, eta=0.0, seed=5)
+    recs, chosen, meds, why = oracle.ref.select_k(a.astype(np.float64), 1, kmax, **kw)
+    cfg = nmf.SelectionConfig(k_min=1, k_max=kmax, n_perturbations=6, delta=0.03, sil_threshold=0.75, seed=5,
+                              nmf=nmf.NmfConfig(max_iters=300, error_check_interval=25, eta=0.0, device=gpu))
+    rep = nmf.select_k(a, cfg)
+    assert rep.chosen_k == chosen == expect
+    assert rep.rationale.split(" and ")[0] == why.split(" and ")[0]
+    for got, want, med in zip(rep.records, recs, meds):
+        assert (got.k, got.valid, got.runs_used) == (want["k"], want["valid"], want["runs_used"])
+        assert got.mean_relative_error == pytest.approx(want["mean_relative_error"], rel=2e-5)
+        # silhouettes are cosine statistics of factors that agree to ~1e-5 (measured ~1e-6)
+        assert got.min_silhouette == pytest.approx(want["min_silhouette"], abs=1e-4)
+        assert got.mean_silhouette == pytest.approx(want["mean_silhouette"], abs=1e-4)
+        if got.k == k_true:
+            assert np.linalg.norm(got.medians - med) <= 1e-3 * np.linalg.norm(med)
+
+
+def test_select_k_on_csr_agrees_with_dense(gpu):
+    rp, ci, v, (m, n) = oracle.port.gen_sparse(150, 110, 0.3, 4)
+    s = nmf.CsrMatrix(m, n, rp, ci, v.astype(np.float32).astype(np.float64))
+    cfg = nmf.SelectionConfig(k_min=1, k_max=3, n_perturbations=4, seed=2,
+                              nmf=nmf.NmfConfig(max_iters=100, error_check_interval=20, eta=0.0, device=gpu))
+    rs, rd = nmf.select_k(s, cfg), nmf.select_k(s.to_dense().astype(np.float32), cfg)
+    assert rs.chosen_k == rd.chosen_k
+    for a, b in zip(rs.records, rd.records):
+        assert a.runs_used == b.runs_used
+        assert a.mean_relative_error == pytest.approx(b.mean_relative_error, rel=1e-4)
+        assert a.min_silhouette == pytest.approx(b.min_silhouette, abs=2e-3)
+
+
+def test_select_k_leaves_context_pristine(gpu):
+    a = oracle.port.uniform_dense(64, 48, 8, 1).astype(np.float32)
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(64, 48, 1)
+        ctx.load_dense(a)
+        cfg = nmf.SelectionConfig(k_min=1, k_max=2, n_perturbations=3,
+                                  nmf=nmf.NmfConfig(max_iters=20, error_check_interval=10, eta=0.0))
+        from paper_2202_09518_b200.nmf import _select_on
+        rep = _select_on(ctx, 64, cfg)
+        assert len(rep.records) == 2 and all(r.runs_used == 3 for r in rep.records)
+        np.testing.assert_array_equal(ctx.download_dense(), a)  # perturbation undone
+
+
+def test_select_k_validation(gpu):
+    a = np.ones((20, 10), np.float32)
+    with pytest.raises(nmf.ShapeError, match="below min"):
+        nmf.select_k(a, nmf.SelectionConfig(k_min=1, k_max=10))

@@ -78,3 +78,20 @@ def test_out_of_core_rnmf_matches_oracle(dist_results):
     w0, h0 = oracle.port.init_factors(1100, 900, 32, 0)
     ref = oracle.port.nmf_rnmf(a, 32, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
     _check(res["ooc_k32"], ref)
+
+
+def test_distributed_select_k_equals_single_gpu(dist_results):
+    # Replica-parallel select_k must reproduce the single-GPU sweep exactly: the same runs, the
+    # same deterministic kernels, W factors exchanged bit-for-bit through the all-reduce (each
+    # slot is written by exactly one rank).
+    _, res = dist_results
+    r = res["select"]
+    lr = oracle.ref.gen_lowrank(96, 64, 3, 0.01, 5)[0] if oracle.ref.available else oracle.port.uniform_dense(96, 64, 5, 1)
+    scfg = nmf.SelectionConfig(k_min=1, k_max=4, n_perturbations=5, seed=3,
+                               nmf=nmf.NmfConfig(max_iters=120, error_check_interval=20, eta=0.0))
+    rep = nmf.select_k(lr.astype(np.float32), scfg)
+    assert r["chosen"] == rep.chosen_k and r["rationale"] == rep.rationale
+    for got, want in zip(r["records"], rep.records):
+        assert got == [want.k, want.valid, want.runs_used, want.min_silhouette, want.mean_silhouette,
+                       want.mean_relative_error]
+    assert r["medians_sum"] == [float(x.medians.sum()) for x in rep.records]
