@@ -38,7 +38,7 @@ def parse():
     p.add_argument("--steps", type=int, default=50)
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", choices=["dense", "sparse", "ooc"], default="dense")
+    p.add_argument("--workload", choices=["dense", "sparse", "ooc", "select"], default="dense")
     p.add_argument("--m", type=int, default=None)
     p.add_argument("--n", type=int, default=None)
     p.add_argument("--k", type=int, default=None)
@@ -47,8 +47,14 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    # --workload select (config 5: select_k over k=2..16 on dense 32768 x 16384)
+    p.add_argument("--k-min", type=int, default=2)
+    p.add_argument("--k-max", type=int, default=16)
+    p.add_argument("--perturbations", type=int, default=16)
+    p.add_argument("--select-iters", type=int, default=500, help="max_iters per run (reference CLI default 500)")
     a = p.parse_args()
-    dflt = {"dense": (65536, 65536, 32), "sparse": (1 << 22, 1 << 22, 32), "ooc": (None, 65536, 64)}[a.workload]
+    dflt = {"dense": (65536, 65536, 32), "sparse": (1 << 22, 1 << 22, 32), "ooc": (None, 65536, 64),
+            "select": (32768, 16384, 9)}[a.workload]
     a.m = a.m or dflt[0]
     a.n = a.n or dflt[1]
     a.k = a.k or dflt[2]
@@ -227,6 +233,92 @@ def roofline(info, bytes_per_launch, peak, peak_src, traffic=None, bound="hbm", 
             "peak_source": peak_src}
 
 
+def bench_select(args, nmf, np, torch, ctx, comm, rank, world, local, barrier, max_over_ranks):
+    """Config 5: one select_k sweep (k_min..k_max, P perturbations, max_iters per run) on a dense
+    m x n A resident on every rank (replicas; the P runs of each k spread over the ranks).
+    value = MU iterations executed by the sweep (all runs, all ranks) / sweep time (CUDA events
+    on the caller's stream around the synchronous call, max over ranks; includes the GPU
+    perturbations, the host clustering / silhouette and the per-k W exchange)."""
+    m, n = args.m, args.n
+    K = args.steps
+    hbm, peak_src = peaks()
+    ctx.set_problem(m, n, args.k_min, 0, m)
+    ctx.generate_dense_uniform(42, 99)
+    host = np.empty((m, n), np.float32)
+    ctx.download_dense(host)
+    cfg = nmf.SelectionConfig(k_min=args.k_min, k_max=args.k_max, n_perturbations=args.perturbations,
+                              delta=0.03, sil_threshold=0.75, seed=0,
+                              nmf=nmf.NmfConfig(max_iters=args.select_iters, error_check_interval=10, eta=1e-6,
+                                                device=local))
+    from paper_2202_09518_b200.nmf import _select_on
+
+    # warm-up: a 2-run sweep at k_min with a few iterations (kernels, graphs, clustering code)
+    wcfg = nmf.SelectionConfig(k_min=args.k_min, k_max=args.k_min, n_perturbations=2, seed=1,
+                               nmf=nmf.NmfConfig(max_iters=max(3, args.warmup), error_check_interval=10, eta=0.0,
+                                                 device=local))
+    _select_on(ctx, m, wcfg)
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record()
+        rep = _select_on(ctx, m, cfg)
+        ev1.record()
+        torch.cuda.synchronize()
+    barrier()
+    sweep_s = max_over_ranks(ev0.elapsed_time(ev1)) / 1e3
+    iters = sum(r.iterations for r in rep.records)
+    value = iters / sweep_s
+    # e2e: the public call on host memory = the A upload (pinned H2D, timed) + the sweep
+    nmf.check(nmf._capi.lib().oocnmf_host_register(host.ctypes.data, host.nbytes))
+    try:
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        ctx.set_problem(m, n, args.k_min, 0, m)
+        ctx.load_dense(host)
+        e1.record()
+        torch.cuda.synchronize()
+        upload_s = max_over_ranks(e0.elapsed_time(e1)) / 1e3
+    finally:
+        nmf._capi.lib().oocnmf_host_unregister(host.ctypes.data)
+    achieved = 2 * m * n * 4 * iters / world / sweep_s / 1e9  # A bytes streamed per GPU per second
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        kmid = (args.k_min + args.k_max) // 2
+        _, cpu = cpu_reference_dense(m, n, kmid, args.cpu_seconds)
+        cpu["sample"] += f" (k = {kmid}, the middle of the sweep)"
+    if rank == 0:
+        out = {"metric": f"MU iters/sec across a select_k sweep (dense {m}x{n}, k={args.k_min}..{args.k_max}, "
+                         f"P={args.perturbations})",
+               "value": value, "unit": "it/s", "n_gpus": world, "steps": iters, "warmup": 1,
+               "ms_per_step": sweep_s * 1e3 / iters, "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "config": {"workload": f"model selection (config 5): select_k k={args.k_min}..{args.k_max}, "
+                                      f"P={args.perturbations}, delta 0.03, max_iters {args.select_iters}, eta 1e-6 "
+                                      f"on dense synthetic {m}x{n} uniform A (CounterRng(42,99)), runs spread "
+                                      f"over {world} rank(s) as replicas",
+                          "m": m, "n": n, "k_min": args.k_min, "k_max": args.k_max,
+                          "perturbations": args.perturbations, "parallelism": f"replicas-x{world}",
+                          "l2": "A (2.1 GB) >> 126 MB L2 (no flush needed)"},
+               "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                            "frac": achieved / hbm, "traffic": None,
+                            "kernel": "whole sweep: two A passes per MU iteration, amortised over perturbation, "
+                                      "factor updates, error checks and host clustering",
+                            "peak_source": peak_src},
+               "cpu_baseline": cpu,
+               "e2e": {"value": iters / (sweep_s + upload_s), "unit": "it/s",
+                       "h2d_bytes_per_step": m * n * 4 / iters,
+                       "d2h_bytes_per_step": sum(m * r.k * 8 * (args.perturbations + 1) for r in rep.records) / iters,
+                       "note": f"A uploaded from pinned host memory ({upload_s:.3f} s, timed) + the sweep; W factors "
+                               f"and medians come back to the host for clustering"},
+               "clocks": clk.summary(), "sweep_s": sweep_s, "chosen_k": rep.chosen_k,
+               "records": [[r.k, r.runs_used, round(r.min_silhouette, 4), round(r.mean_relative_error, 6),
+                            r.iterations] for r in rep.records]}
+        print(json.dumps(out))
+    if comm:
+        comm.close()
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -287,6 +379,8 @@ def main():
 
     comm = nmf.DistComm(rank, world, local) if world > 1 else None
     ctx = comm.ctx if comm else nmf.Context(local)
+    if args.workload == "select":
+        return bench_select(args, nmf, np, torch, ctx, comm, rank, world, local, barrier, max_over_ranks)
     kp = 8 if k <= 8 else 16 if k <= 16 else 32 if k <= 32 else 64
     hbm, peak_src = peaks()
     extra = {}

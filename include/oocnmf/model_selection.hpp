@@ -1,0 +1,4 @@
+// Forwarder: the reference header name (include/oocnmf/model_selection.hpp) resolves to the
+// B200 host core.
+#pragma once
+#include "oocnmf_b200/oocnmf.hpp"

@@ -192,6 +192,7 @@ typedef struct {
     int32_t reserved;
     uint64_t runs_used;
     double min_silhouette, mean_silhouette, mean_relative_error;
+    uint64_t iterations;      /* B200 extension: MU iterations run for this k, all ranks */
 } oocnmf_k_record;
 
 /* Change k keeping the resident A (re-allocates the factors). */

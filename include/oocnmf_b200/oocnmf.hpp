@@ -249,4 +249,63 @@ struct StoreCounters {
 NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan, CommHandle& comm,
                           const StoreConfig& store_cfg = {}, StoreCounters* store_counters_out = nullptr);
 
+// ---- model selection (reference: include/oocnmf/model_selection.hpp) ----
+struct SelectionConfig {
+    index_t k_min = 1;
+    index_t k_max = 1;
+    index_t n_perturbations = 16;  ///< P: runs per candidate k
+    double delta = 0.03;           ///< perturbation amplitude, in (0,1)
+    double sil_threshold = 0.75;   ///< min-silhouette acceptance bar
+    NmfConfig nmf;                 ///< per-run template (k and seed are overridden); nmf.device = GPU
+    std::uint64_t seed = 0;
+    void validate(index_t m, index_t n) const;
+};
+
+struct KRecord {
+    index_t k = 0;
+    bool valid = false;
+    index_t runs_used = 0;
+    double min_silhouette = 0.0;
+    double mean_silhouette = 0.0;
+    double mean_relative_error = 0.0;
+    DenseMatrix medians;  ///< m x k elementwise-median cluster columns
+};
+
+struct SelectionReport {
+    std::vector<KRecord> records;
+    std::optional<index_t> chosen_k;
+    std::string rationale;
+    std::string to_json() const;
+    std::string to_csv() const;
+};
+
+/// perturb_dense / perturb_sparse, evaluated on the GPU (cfg device 0): every stored entry
+/// times 1 - delta + 2 delta U(seed, 21, i * n + j); values come back f32-rounded.
+DenseMatrix perturb_dense(MatrixRef a, double delta, std::uint64_t seed);
+CsrMatrix perturb_sparse(const CsrMatrix& a, double delta, std::uint64_t seed);
+
+struct ColumnClusters {
+    std::vector<std::vector<std::pair<index_t, index_t>>> member_ids;
+    std::vector<std::vector<std::vector<double>>> points;
+    DenseMatrix medians;  // m x k
+    index_t dropped_zero_columns = 0;
+};
+ColumnClusters cluster_columns(const std::vector<DenseMatrix>& runs, index_t k);
+
+struct SilhouetteScore {
+    double min_sil = 0.0;
+    double mean_sil = 0.0;
+    std::vector<double> per_cluster;
+};
+SilhouetteScore silhouette(const ColumnClusters& clusters);
+
+DenseMatrix pearson_correlation_matrix(const DenseMatrix& w_true, const DenseMatrix& w_est);
+
+/// P perturbed GPU factorizations per k in [k_min, k_max], W-column clustering, silhouettes,
+/// errors, and the largest qualifying k (src/model_selection.cpp:316-406).
+SelectionReport select_k(MatrixRef a, const SelectionConfig& cfg);
+/// B200 extension: the same sweep spread over an NCCL group as replicas (every rank passes the
+/// full A); collective, every rank returns the same report.
+SelectionReport select_k(MatrixRef a, const SelectionConfig& cfg, CommHandle& comm);
+
 }  // namespace oocnmf

@@ -43,7 +43,7 @@ class SelectionConfig(C.Structure):
 
 class KRecord(C.Structure):
     _fields_ = [("k", u64), ("valid", i32), ("reserved", i32), ("runs_used", u64), ("min_silhouette", dbl),
-                ("mean_silhouette", dbl), ("mean_relative_error", dbl)]
+                ("mean_silhouette", dbl), ("mean_relative_error", dbl), ("iterations", u64)]
 
 
 pi64 = C.POINTER(C.c_int64)

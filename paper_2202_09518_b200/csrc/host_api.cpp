@@ -4,6 +4,7 @@
 #include <cmath>
 
 #include "oocnmf_b200/oocnmf.hpp"
+#include "selection.hpp"
 
 namespace oocnmf {
 
@@ -331,6 +332,175 @@ NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const Partitio
         store_counters_out->bytes_read = index_t(info.h2d_bytes);
     }
     return res;
+}
+
+// ------------------------------------------------------------------------- model selection
+void SelectionConfig::validate(index_t m, index_t n) const {
+    if (k_min < 1 || k_max < k_min) throw ShapeError("SelectionConfig: need 1 <= k_min <= k_max");
+    if (k_max >= std::min(m, n)) throw ShapeError("SelectionConfig: k_max must be below min(m, n)");
+    if (n_perturbations < 2) throw ShapeError("SelectionConfig: need at least 2 perturbations");
+    if (delta <= 0.0 || delta >= 1.0) throw ShapeError("SelectionConfig: delta must lie in (0, 1)");
+    if (sil_threshold < -1.0 || sil_threshold > 1.0)
+        throw ShapeError("SelectionConfig: sil_threshold must lie in [-1, 1]");
+}
+
+namespace {
+
+SelectionReport run_select(oocnmf_ctx* c, index_t m, const SelectionConfig& cfg) {
+    oocnmf_selection_config sc{};
+    sc.k_min = cfg.k_min, sc.k_max = cfg.k_max, sc.n_perturbations = cfg.n_perturbations;
+    sc.delta = cfg.delta, sc.sil_threshold = cfg.sil_threshold, sc.seed = cfg.seed;
+    sc.nmf = to_c(cfg.nmf);
+    const index_t nk = cfg.k_max - cfg.k_min + 1;
+    std::vector<oocnmf_k_record> recs(nk);
+    index_t med_total = 0;
+    for (index_t k = cfg.k_min; k <= cfg.k_max; ++k) med_total += m * k;
+    std::vector<double> med(med_total);
+    std::int64_t chosen = -1;
+    char why[512] = {0};
+    throw_status(oocnmf_select_k(c, &sc, recs.data(), nk, med.data(), &chosen, why, sizeof why));
+    SelectionReport rep;
+    const double* mp = med.data();
+    for (const auto& r : recs) {
+        KRecord kr;
+        kr.k = r.k, kr.valid = r.valid != 0, kr.runs_used = r.runs_used;
+        kr.min_silhouette = r.min_silhouette, kr.mean_silhouette = r.mean_silhouette;
+        kr.mean_relative_error = r.mean_relative_error;
+        if (kr.valid) kr.medians = DenseMatrix(m, r.k, std::vector<double>(mp, mp + m * r.k));
+        mp += m * r.k;
+        rep.records.push_back(std::move(kr));
+    }
+    if (chosen >= 0) rep.chosen_k = index_t(chosen);
+    rep.rationale = why;
+    return rep;
+}
+
+std::string fmt_g(double v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%g", v);
+    return b;
+}
+std::string fmt_json(double v) {
+    char b[64];
+    std::snprintf(b, sizeof b, "%.17g", v);
+    return b;
+}
+
+}  // namespace
+
+SelectionReport select_k(MatrixRef a, const SelectionConfig& cfg) {
+    cfg.validate(a.rows(), a.cols());
+    Ctx ctx;
+    throw_status(oocnmf_ctx_create(cfg.nmf.device, &ctx.c));
+    throw_status(oocnmf_set_problem(ctx.c, a.rows(), a.cols(), cfg.k_min, 0, a.rows()));
+    upload(ctx.c, a, 0, a.rows());
+    return run_select(ctx.c, a.rows(), cfg);
+}
+
+SelectionReport select_k(MatrixRef a, const SelectionConfig& cfg, CommHandle& comm) {
+    cfg.validate(a.rows(), a.cols());
+    if (!comm.context()) throw CommError("select_k: CommHandle has no device context");
+    throw_status(oocnmf_set_problem(comm.context(), a.rows(), a.cols(), cfg.k_min, 0, a.rows()));
+    upload(comm.context(), a, 0, a.rows());
+    return run_select(comm.context(), a.rows(), cfg);
+}
+
+std::string SelectionReport::to_json() const {
+    std::string j = "{\n  \"chosen_k\": " + (chosen_k ? std::to_string(*chosen_k) : std::string("\"none\"")) +
+                    ",\n  \"rationale\": \"" + rationale + "\",\n  \"records\": [";
+    for (index_t i = 0; i < records.size(); ++i) {
+        const KRecord& r = records[i];
+        j += std::string(i ? "," : "") + "\n    {\n      \"k\": " + std::to_string(r.k) +
+             ",\n      \"mean_relative_error\": " + fmt_json(r.mean_relative_error) +
+             ",\n      \"mean_silhouette\": " + fmt_json(r.mean_silhouette) +
+             ",\n      \"min_silhouette\": " + fmt_json(r.min_silhouette) +
+             ",\n      \"runs_used\": " + std::to_string(r.runs_used) +
+             ",\n      \"valid\": " + (r.valid ? "true" : "false") + "\n    }";
+    }
+    return j + (records.empty() ? "]\n}" : "\n  ]\n}");
+}
+
+std::string SelectionReport::to_csv() const {
+    std::string out = "k,valid,runs_used,min_silhouette,mean_silhouette,mean_relative_error\n";
+    for (const auto& r : records)
+        out += std::to_string(r.k) + ',' + (r.valid ? "1" : "0") + ',' + std::to_string(r.runs_used) + ',' +
+               fmt_g(r.min_silhouette) + ',' + fmt_g(r.mean_silhouette) + ',' + fmt_g(r.mean_relative_error) + '\n';
+    return out;
+}
+
+DenseMatrix perturb_dense(MatrixRef a, double delta, std::uint64_t seed) {
+    if (delta < 0.0 || delta >= 1.0) throw ShapeError("perturb: delta must lie in [0, 1)");
+    if (!a.is_dense()) throw ShapeError("perturb_dense: dense input required");
+    Ctx ctx;
+    throw_status(oocnmf_ctx_create(0, &ctx.c));
+    throw_status(oocnmf_set_problem(ctx.c, a.rows(), a.cols(), 1, 0, a.rows()));
+    upload(ctx.c, a, 0, a.rows());
+    throw_status(oocnmf_perturb(ctx.c, delta, seed));
+    std::vector<float> f(a.rows() * a.cols());
+    throw_status(oocnmf_download_dense_f32(ctx.c, f.data()));
+    return DenseMatrix(a.rows(), a.cols(), std::vector<double>(f.begin(), f.end()));
+}
+
+CsrMatrix perturb_sparse(const CsrMatrix& a, double delta, std::uint64_t seed) {
+    if (delta < 0.0 || delta >= 1.0) throw ShapeError("perturb: delta must lie in [0, 1)");
+    Ctx ctx;
+    throw_status(oocnmf_ctx_create(0, &ctx.c));
+    throw_status(oocnmf_set_problem(ctx.c, a.rows(), a.cols(), 1, 0, a.rows()));
+    upload(ctx.c, MatrixRef(a), 0, a.rows());
+    throw_status(oocnmf_perturb(ctx.c, delta, seed));
+    std::uint64_t nnz = 0;
+    throw_status(oocnmf_csr_nnz(ctx.c, &nnz));
+    std::vector<std::uint64_t> rp(a.rows() + 1), ci(nnz);
+    std::vector<double> v(nnz);
+    throw_status(oocnmf_download_csr(ctx.c, rp.data(), ci.data(), v.data()));
+    return CsrMatrix(a.rows(), a.cols(), std::vector<index_t>(rp.begin(), rp.end()),
+                     std::vector<index_t>(ci.begin(), ci.end()), std::move(v));
+}
+
+ColumnClusters cluster_columns(const std::vector<DenseMatrix>& runs, index_t k) {
+    if (runs.size() < 2) throw ShapeError("cluster_columns: need at least 2 runs");
+    const index_t m = runs[0].rows();
+    std::vector<ooc_sel::Factor> f;
+    for (const auto& w : runs) {
+        if (w.rows() != m || w.cols() != k) throw ShapeError("cluster_columns: all runs must be m x k");
+        f.push_back({w.data()});
+    }
+    try {
+        ooc_sel::Clusters cl = ooc_sel::cluster_columns(f, m, k);
+        ColumnClusters out;
+        out.member_ids.resize(k);
+        for (index_t c = 0; c < k; ++c)
+            for (const auto& [r, col] : cl.member_ids[c]) out.member_ids[c].push_back({index_t(r), index_t(col)});
+        out.points = std::move(cl.points);
+        out.medians = DenseMatrix(m, k, std::move(cl.medians));
+        out.dropped_zero_columns = cl.dropped_zero_columns;
+        return out;
+    } catch (const std::invalid_argument& e) {
+        throw ShapeError(e.what());
+    }
+}
+
+SilhouetteScore silhouette(const ColumnClusters& clusters) {
+    ooc_sel::Clusters cl;
+    cl.k = clusters.points.size();
+    cl.m = clusters.medians.rows();
+    cl.points = clusters.points;
+    try {
+        const ooc_sel::Silhouette s = ooc_sel::silhouette(cl);
+        return {s.min_sil, s.mean_sil, s.per_cluster};
+    } catch (const std::invalid_argument& e) {
+        throw ShapeError(e.what());
+    }
+}
+
+DenseMatrix pearson_correlation_matrix(const DenseMatrix& w_true, const DenseMatrix& w_est) {
+    if (w_true.rows() != w_est.rows()) throw ShapeError("pearson_correlation_matrix: row counts differ");
+    try {
+        return DenseMatrix(w_true.cols(), w_est.cols(),
+                           ooc_sel::pearson(w_true.data(), w_true.rows(), w_true.cols(), w_est.data(), w_est.cols()));
+    } catch (const std::domain_error& e) {
+        throw DataError(e.what());
+    }
 }
 
 }  // namespace oocnmf

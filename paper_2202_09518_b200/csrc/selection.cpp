@@ -393,7 +393,7 @@ int oocnmf_select_k(oocnmf_ctx* ctx, const oocnmf_selection_config* cfg, oocnmf_
         for (uint64_t k = cfg->k_min; k <= cfg->k_max; ++k) {
             chk(oocnmf_set_rank(ctx, k));
             // per-perturbation slots, filled by the owning rank, summed over ranks
-            std::vector<double> wall(P * m * k, 0.0), err(P, 0.0), ok(P, 0.0);
+            std::vector<double> wall(P * m * k, 0.0), err(P, 0.0), ok(P, 0.0), iters(P, 0.0);
             hbuf.assign(k * n, 0.0);
             for (uint64_t p = uint64_t(rank); p < P; p += uint64_t(nranks)) {
                 for (uint64_t attempt = 0; attempt < 2 && ok[p] == 0.0; ++attempt) {
@@ -411,12 +411,14 @@ int oocnmf_select_k(oocnmf_ctx* ctx, const oocnmf_selection_config* cfg, oocnmf_
                     chk(oocnmf_get_factors_f64(ctx, wall.data() + p * m * k, hbuf.data()));
                     err[p] = te[std::min<uint64_t>(info.n_trace, tcap) - 1];
                     ok[p] = 1.0;
+                    iters[p] = double(info.iterations_run);
                 }
             }
             if (nranks > 1) {
                 chk(oocnmf_allreduce_sum_f64(ctx, wall.data(), wall.size()));
                 chk(oocnmf_allreduce_sum_f64(ctx, err.data(), P));
                 chk(oocnmf_allreduce_sum_f64(ctx, ok.data(), P));
+                chk(oocnmf_allreduce_sum_f64(ctx, iters.data(), P));
             }
             std::vector<ooc_sel::Factor> ws;
             double err_sum = 0.0;
@@ -429,6 +431,7 @@ int oocnmf_select_k(oocnmf_ctx* ctx, const oocnmf_selection_config* cfg, oocnmf_
             rec = oocnmf_k_record{};
             rec.k = k;
             rec.runs_used = ws.size();
+            for (uint64_t p = 0; p < P; ++p) rec.iterations += uint64_t(iters[p]);
             if (ws.size() >= 2) {
                 const auto cl = ooc_sel::cluster_columns(ws, m, k);
                 const auto sil = ooc_sel::silhouette(cl);

@@ -538,6 +538,7 @@ class KRecord:
     mean_silhouette: float = 0.0
     mean_relative_error: float = 0.0
     medians: Optional[np.ndarray] = None  # m x k
+    iterations: int = 0  # B200 extension: MU iterations run for this k (all ranks)
 
 
 @dataclass
@@ -575,7 +576,7 @@ def _select_on(ctx: "Context", m: int, cfg: SelectionConfig) -> SelectionReport:
     for i, k in enumerate(range(cfg.k_min, cfg.k_max + 1)):
         r = recs[i]
         out.append(KRecord(int(r.k), bool(r.valid), int(r.runs_used), r.min_silhouette, r.mean_silhouette,
-                           r.mean_relative_error, med[off:off + m * k].reshape(m, k).copy()))
+                           r.mean_relative_error, med[off:off + m * k].reshape(m, k).copy(), int(r.iterations)))
         off += m * k
     return SelectionReport(out, None if chosen.value < 0 else int(chosen.value), why.value.decode())
 

@@ -6,6 +6,7 @@
 #include <cstdio>
 
 #include "oocnmf/matrix.hpp"
+#include "oocnmf/model_selection.hpp"
 #include "oocnmf/nmf.hpp"
 #include "oocnmf/rng.hpp"
 
@@ -33,6 +34,27 @@ int main(int argc, char** argv) {
     } catch (const DeviceError& e) {
         std::printf("{\"device_error\": \"%s\"}\n", e.what());
         return 3;
+    }
+    // Model selection driven as the reference CLI drives it (tools/oocnmf_cli.cpp:298-318) on an
+    // exactly rank-2 input: the largest k with a stable ensemble is 2.
+    {
+        DenseMatrix lr(60, 40);
+        CounterRng ra(7, 1), rb(7, 2);
+        for (index_t i = 0; i < 60; ++i)
+            for (index_t j = 0; j < 40; ++j) {
+                double v = 0;
+                for (index_t t = 0; t < 2; ++t) v += ra.uniform(i * 2 + t) * rb.uniform(t * 40 + j);
+                lr.at(i, j) = double(float(v));
+            }
+        SelectionConfig sc;
+        sc.k_min = 1;
+        sc.k_max = 3;
+        sc.n_perturbations = 4;
+        sc.nmf.max_iters = 200;
+        sc.nmf.eta = 1e-6;
+        SelectionReport rep = select_k(MatrixRef(lr), sc);
+        std::printf("{\"select_chosen\": %lld, \"select_records\": %zu}\n",
+                    rep.chosen_k ? (long long)*rep.chosen_k : -1LL, rep.records.size());
     }
     // Error mapping: an invalid config throws ShapeError like the reference.
     try {

@@ -319,6 +319,8 @@ def test_cpp_host_core_is_a_drop_in(gpu):
     norms = [d for d in lines if "w_fro" in d][0]
     assert norms["w_fro"] == pytest.approx(np.linalg.norm(ref.w), rel=FACTOR_TOL)
     assert any(d.get("shape_error") for d in lines)
+    sel = [d for d in lines if "select_chosen" in d][0]  # oocnmf::select_k through the C++ host core
+    assert sel == {"select_chosen": 2, "select_records": 3}
 
 
 # ---------------------------------------------------------------------------- edge cases
