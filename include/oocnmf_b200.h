@@ -125,6 +125,16 @@ int oocnmf_set_problem(oocnmf_ctx* ctx, uint64_t m, uint64_t n, uint64_t k, uint
 int oocnmf_problem_dims(const oocnmf_ctx* ctx, uint64_t* m, uint64_t* n, uint64_t* k, uint64_t* row0,
                         uint64_t* rows);
 
+/* Column partition (CNMF, src/nmf_distributed.cpp:112-149, partition.cpp:12-14): this rank
+ * owns all m rows and the columns [col0, col0 + cols) of the m x n A. W (m x k) is replicated,
+ * H is the local k x cols slab; per iteration the ranks sum A·H^T (m x k) and H H^T (k x k)
+ * with NCCL. Load the column slab (m x cols) with oocnmf_load_dense_* / oocnmf_load_csr_f64
+ * (column indices local to the slab); oocnmf_set_factors_f64 takes the full W and the H slab;
+ * oocnmf_gather_h_f64 returns the full H (k x n) on every rank. */
+int oocnmf_set_problem_cols(oocnmf_ctx* ctx, uint64_t m, uint64_t n, uint64_t k, uint64_t col0,
+                            uint64_t cols);
+int oocnmf_gather_h_f64(oocnmf_ctx* ctx, double* h_full);
+
 /* A sources (pick one). Dense values are stored in HBM as f32 row-major. */
 int oocnmf_load_dense_f64(oocnmf_ctx* ctx, const double* a_slab, uint64_t lda);
 int oocnmf_load_dense_f32(oocnmf_ctx* ctx, const float* a_slab, uint64_t lda);

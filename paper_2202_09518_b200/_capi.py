@@ -80,6 +80,8 @@ _SIGS = {
     "oocnmf_products_f64": ([vp, pd, pd, pd, pd], C.c_int),
     "oocnmf_sq_norm": ([vp, pd], C.c_int),
     "oocnmf_problem_dims": ([vp, pu, pu, pu, pu, pu], C.c_int),
+    "oocnmf_set_problem_cols": ([vp, u64, u64, u64, u64, u64], C.c_int),
+    "oocnmf_gather_h_f64": ([vp, pd], C.c_int),
     "oocnmf_set_rank": ([vp, u64], C.c_int),
     "oocnmf_perturb": ([vp, dbl, u64], C.c_int),
     "oocnmf_set_local": ([vp, C.c_int], C.c_int),

@@ -293,12 +293,41 @@ NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const Partitio
     if (comm.size() != plan.n_workers)
         throw ShapeError("nmf_distributed: group size " + std::to_string(comm.size()) + " != plan workers " +
                          std::to_string(plan.n_workers));
-    if (plan.strategy != Strategy::rnmf)
-        throw ShapeError("nmf_distributed: the B200 backend implements the row partition (RNMF) only");
     if (!a.pdn1_path.empty()) throw IoError("nmf_distributed: PDN1 file sources are not supported by the B200 backend");
     if (!comm.context()) throw CommError("nmf_distributed: CommHandle has no device context");
     oocnmf_ctx* c = comm.context();
     const WorkerSlab& slab = plan.slabs[std::size_t(comm.rank())];
+    if (plan.strategy == Strategy::cnmf) {
+        // column partition (src/nmf_distributed.cpp:112-149): W replicated, H column slabs
+        if (a.host_f32) throw ShapeError("nmf_distributed: out-of-core streaming is row-partitioned (RNMF) only");
+        if (a.mem.empty()) throw ShapeError("nmf_distributed: empty A source");
+        const index_t m = plan.m, n = plan.n, k = plan.k, c0 = slab.a_cols.begin, cols = slab.a_cols.extent();
+        if (a.mem.rows() != m || a.mem.cols() != n) throw ShapeError("nmf_distributed: A does not match the plan");
+        throw_status(oocnmf_set_problem_cols(c, m, n, k, c0, cols));
+        upload(c, a.mem.window({0, m}, {c0, c0 + cols}), 0, m);
+        if (cfg.init == FactorInit::from_files) {
+            if (cfg.init_w->rows() != m || cfg.init_w->cols() != k || cfg.init_h->rows() != k ||
+                cfg.init_h->cols() != n)
+                throw ShapeError("nmf_distributed: provided factors do not match plan");
+            DenseMatrix hs(k, cols);
+            for (index_t r = 0; r < k; ++r)
+                for (index_t j = 0; j < cols; ++j) hs.at(r, j) = cfg.init_h->at(r, c0 + j);
+            throw_status(oocnmf_set_factors_f64(c, cfg.init_w->data(), hs.data()));
+        }
+        const oocnmf_config cc = to_c(cfg);
+        std::vector<std::uint64_t> ti(cfg.max_iters / cfg.error_check_interval + 2);
+        std::vector<double> te(ti.size());
+        oocnmf_info info{};
+        throw_status(oocnmf_solve(c, &cc, ti.data(), te.data(), ti.size(), &info));
+        NmfResult res;
+        res.w = DenseMatrix(m, k);
+        res.h = DenseMatrix(k, n);
+        throw_status(oocnmf_get_factors_f64(c, res.w.data(), nullptr));
+        throw_status(oocnmf_gather_h_f64(c, res.h.data()));
+        fill_result(res, info, ti, te);
+        if (store_counters_out) *store_counters_out = StoreCounters{};
+        return res;
+    }
     const index_t m = plan.m, n = plan.n, k = plan.k, r0 = slab.a_rows.begin, rows = slab.a_rows.extent();
     throw_status(oocnmf_set_problem(c, m, n, k, r0, rows));
     if (a.host_f32) {

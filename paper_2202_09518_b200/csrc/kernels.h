@@ -53,17 +53,22 @@ cudaError_t launch_reduce_slots(const double* slots, int64_t nslots, int64_t cou
 cudaError_t launch_streamk_reduce(int kp, const float* slots, const StreamK& sk, float* out,
                                   bool accumulate, cudaStream_t s);
 // trace slot <- sqrt(max(0, nA2 - 2 sum(err_slots) + <WtW, HHt>)) / sqrt(nA2)   (f64)
+// Predication (no host round trip): if pred_in is set and *pred_in == 0 the kernel does
+// nothing; if pred_out is set it receives (err < threshold).
 cudaError_t launch_finalize_error(int kp, const double* err_slots, int64_t n_err,
                                   const double* wtw, const double* hht, const double* norm_a2,
                                   const double* direct_res /* null = trace form */,
-                                  double* out_err, cudaStream_t s);
+                                  double* out_err, cudaStream_t s, const int* pred_in = nullptr,
+                                  int* pred_out = nullptr, double threshold = 0.0);
 
 // ---- setup kernels (kernels_setup.cu) ----
 cudaError_t launch_gen_dense_uniform(float* A, int64_t lda, int64_t rows, int64_t cols,
                                      int64_t row0, int64_t n_global, uint64_t seed,
                                      uint64_t stream, cudaStream_t s);
+// W rows [row0, row0 + rows) and H columns [col0, col0 + n) of n_global (Ht, n x kp)
 cudaError_t launch_init_factors(float* W, float* Ht, int kp, int64_t k, int64_t rows,
-                                int64_t row0, int64_t n, uint64_t seed, cudaStream_t s);
+                                int64_t row0, int64_t n, int64_t n_global, int64_t col0, uint64_t seed,
+                                cudaStream_t s);
 cudaError_t launch_cast_pad_f64(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
                                 float* dst, int64_t ld_dst, cudaStream_t s);
 // Partial f64 sums of squares of A (dense, padded) -> out_slots[sqnorm_grid()].
@@ -75,7 +80,7 @@ cudaError_t launch_reduce_f64(const double* slots, int64_t n, double* out, cudaS
 // Direct residual sum((A - W Ht^T)^2) partials for the rows x cols window (f64).
 cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t rows,
                                   int64_t cols, const float* W, const float* Ht,
-                                  double* out_slots, cudaStream_t s);
+                                  double* out_slots, cudaStream_t s, const int* pred = nullptr);
 cudaError_t launch_check_finite(const float* x, int64_t n, int* flag, cudaStream_t s);
 // Model-selection perturbation of the resident A (dense window, or CSR values; transposed:
 // the CSR(A^T) copy), out = f32(in * (1 - delta + 2 delta U(seed, 21, i * n + j))).
@@ -93,7 +98,8 @@ cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const floa
                         int64_t rows, const float* B, float* out, cudaStream_t s);
 cudaError_t launch_residual_csr(int kp, const int64_t* rp, const int32_t* ci, const float* v,
                                 int64_t rows, int64_t cols, const float* W, const float* Ht,
-                                double* out_slots, cudaStream_t s);
+                                double* out_slots, cudaStream_t s,
+                                const int* pred = nullptr);
 // Transpose a CSR (rows x cols) into CSR^T (cols x rows), entries of each output row in
 // ascending source-row order (deterministic). Scratch allocated internally.
 cudaError_t csr_transpose(const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,

@@ -252,9 +252,11 @@ __global__ void k_streamk_reduce(const float* __restrict__ slots, StreamK sk, fl
 __global__ void k_finalize_error(int kp, const double* __restrict__ err_slots, int64_t n_err,
                                  const double* __restrict__ wtw, const double* __restrict__ hht,
                                  const double* __restrict__ norm_a2,
-                                 const double* __restrict__ direct_res, double* __restrict__ out) {
+                                 const double* __restrict__ direct_res, double* __restrict__ out,
+                                 const int* __restrict__ pred_in, int* __restrict__ pred_out, double threshold) {
     __shared__ double sh[256];
     const int tid = threadIdx.x;
+    if (pred_in && *pred_in == 0) return;
     double res;
     if (direct_res) {
         res = *direct_res;
@@ -267,7 +269,11 @@ __global__ void k_finalize_error(int kp, const double* __restrict__ err_slots, i
         const double quad = block_sum_f64(b, sh);
         res = *norm_a2 - 2.0 * cross + quad;
     }
-    if (tid == 0) *out = sqrt(res > 0.0 ? res : 0.0) / sqrt(*norm_a2);
+    if (tid == 0) {
+        const double e = sqrt(res > 0.0 ? res : 0.0) / sqrt(*norm_a2);
+        *out = e;
+        if (pred_out) *pred_out = e < threshold ? 1 : 0;
+    }
 }
 
 }  // namespace
@@ -331,8 +337,10 @@ cudaError_t launch_streamk_reduce(int kp, const float* slots, const StreamK& sk,
 
 cudaError_t launch_finalize_error(int kp, const double* err_slots, int64_t n_err, const double* wtw,
                                   const double* hht, const double* norm_a2, const double* direct_res,
-                                  double* out_err, cudaStream_t s) {
-    k_finalize_error<<<1, 256, 0, s>>>(kp, err_slots, n_err, wtw, hht, norm_a2, direct_res, out_err);
+                                  double* out_err, cudaStream_t s, const int* pred_in, int* pred_out,
+                                  double threshold) {
+    k_finalize_error<<<1, 256, 0, s>>>(kp, err_slots, n_err, wtw, hht, norm_a2, direct_res, out_err, pred_in,
+                                       pred_out, threshold);
     return cudaGetLastError();
 }
 

@@ -24,10 +24,12 @@ __global__ void k_gen_dense_uniform(float* __restrict__ A, int64_t lda, int64_t 
     }
 }
 
-// W[i][j] = U(seed,1,(row0+i)*k + j), H[r][c] = U(seed,2,r*n + c) stored as Ht[c][r]
-// (src/nmf_serial.cpp:31-48), rounded to f32; padding stays zero (caller memsets).
+// W[i][j] = U(seed,1,(row0+i)*k + j), H[r][c] = U(seed,2,r*n_global + col0 + c) stored as
+// Ht[c][r] (src/nmf_serial.cpp:31-48; init_w_rows / init_h_cols windows), rounded to f32;
+// padding stays zero (caller memsets).
 __global__ void k_init_factors(float* __restrict__ W, float* __restrict__ Ht, int kp, int64_t k,
-                               int64_t rows, int64_t row0, int64_t n, uint64_t kw, uint64_t kh) {
+                               int64_t rows, int64_t row0, int64_t n, int64_t n_global, int64_t col0,
+                               uint64_t kw, uint64_t kh) {
     const int64_t nw = rows * k, nh = n * k;
     for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nw + nh;
          q += int64_t(gridDim.x) * blockDim.x) {
@@ -36,7 +38,7 @@ __global__ void k_init_factors(float* __restrict__ W, float* __restrict__ Ht, in
             W[i * kp + j] = __double2float_rn(rng_u01(kw, uint64_t(row0 + i) * k + j));
         } else {
             const int64_t e = q - nw, r = e / n, c = e % n;
-            Ht[c * kp + r] = __double2float_rn(rng_u01(kh, uint64_t(r) * n + c));
+            Ht[c * kp + r] = __double2float_rn(rng_u01(kh, uint64_t(r) * n_global + uint64_t(col0 + c)));
         }
     }
 }
@@ -101,7 +103,8 @@ __global__ void __launch_bounds__(256) k_residual_dense(const float* __restrict_
                                                         int64_t rows, int64_t cols,
                                                         const float* __restrict__ W,
                                                         const float* __restrict__ Ht,
-                                                        double* __restrict__ out) {
+                                                        double* __restrict__ out, const int* __restrict__ pred) {
+    if (pred && *pred == 0) return;  // device-side predication (error_mode auto)
     __shared__ float Ws[4][KP];
     double acc = 0.0;
     const int64_t rblocks = (rows + 3) / 4, cblocks = (cols + 255) / 256;
@@ -198,9 +201,9 @@ cudaError_t launch_gen_dense_uniform(float* A, int64_t lda, int64_t rows, int64_
 }
 
 cudaError_t launch_init_factors(float* W, float* Ht, int kp, int64_t k, int64_t rows, int64_t row0,
-                                int64_t n, uint64_t seed, cudaStream_t s) {
+                                int64_t n, int64_t n_global, int64_t col0, uint64_t seed, cudaStream_t s) {
     k_init_factors<<<grid_for((rows + n) * k, 4), 256, 0, s>>>(
-        W, Ht, kp, k, rows, row0, n, rng_key(seed, kStreamW), rng_key(seed, kStreamH));
+        W, Ht, kp, k, rows, row0, n, n_global, col0, rng_key(seed, kStreamW), rng_key(seed, kStreamH));
     return cudaGetLastError();
 }
 
@@ -227,12 +230,13 @@ cudaError_t launch_reduce_f64(const double* slots, int64_t n, double* out, cudaS
 }
 
 cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t rows, int64_t cols,
-                                  const float* W, const float* Ht, double* out_slots, cudaStream_t s) {
+                                  const float* W, const float* Ht, double* out_slots, cudaStream_t s,
+                                  const int* pred) {
     switch (kp) {
-        case 8: k_residual_dense<8><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
-        case 16: k_residual_dense<16><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
-        case 32: k_residual_dense<32><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
-        case 64: k_residual_dense<64><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots); break;
+        case 8: k_residual_dense<8><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots, pred); break;
+        case 16: k_residual_dense<16><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots, pred); break;
+        case 32: k_residual_dense<32><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots, pred); break;
+        case 64: k_residual_dense<64><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots, pred); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

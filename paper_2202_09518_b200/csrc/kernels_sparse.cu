@@ -78,7 +78,8 @@ __global__ void __launch_bounds__(256) k_cross_csr(const int64_t* __restrict__ r
                                                    const float* __restrict__ v, int64_t rows,
                                                    const float* __restrict__ W,
                                                    const float* __restrict__ Ht,
-                                                   double* __restrict__ out) {
+                                                   double* __restrict__ out, const int* __restrict__ pred) {
+    if (pred && *pred == 0) return;  // device-side predication (error_mode auto)
     double acc = 0.0;
     for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
          i += int64_t(gridDim.x) * blockDim.x) {
@@ -212,14 +213,14 @@ cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const floa
 
 cudaError_t launch_residual_csr(int kp, const int64_t* rp, const int32_t* ci, const float* v,
                                 int64_t rows, int64_t cols, const float* W, const float* Ht,
-                                double* out_slots, cudaStream_t s) {
+                                double* out_slots, cudaStream_t s, const int* pred) {
     (void)cols;
     const unsigned grid = 4 * 148;
     switch (kp) {
-        case 8: k_cross_csr<8><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
-        case 16: k_cross_csr<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
-        case 32: k_cross_csr<32><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
-        case 64: k_cross_csr<64><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots); break;
+        case 8: k_cross_csr<8><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots, pred); break;
+        case 16: k_cross_csr<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots, pred); break;
+        case 32: k_cross_csr<32><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots, pred); break;
+        case 64: k_cross_csr<64><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots, pred); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -116,6 +116,10 @@ struct oocnmf_ctx {
     cudaStream_t stream = nullptr, copy_stream = nullptr;
 
     uint64_t m = 0, n = 0, k = 0, row0 = 0, rows = 0;
+    // Column partition (CNMF, src/nmf_distributed.cpp:112-149): this rank owns all m rows and
+    // the columns [col0, col0 + n) of n_global; W is replicated, H (Ht) is the local slab.
+    bool cnmf = false;
+    uint64_t col0 = 0, n_global = 0;
     int kp = 0;
     int64_t mp = 0, np = 0;
     bool problem_set = false;
@@ -143,9 +147,13 @@ struct oocnmf_ctx {
     uint64_t launches = 0;
     // CUDA graph of one block of iterations (the launches between two error checks),
     // replayed while its key (buffers, shapes, eps, block length) is unchanged.
-    cudaGraphExec_t graph = nullptr;
-    std::vector<uint64_t> graph_key;
-    uint64_t graph_launches = 0;
+    struct Graph {
+        std::vector<uint64_t> key;
+        cudaGraphExec_t exec = nullptr;
+        uint64_t launches = 0;
+    };
+    std::vector<Graph> graphs;  // small cache: the two event sets of the solve loop alternate
+    DevBuf errs, flags, pred;   // device-side error checks: per-check value / NaN flag, predicate
     bool graph_broken = false;   // capture failed once: iterate eagerly (same kernels)
     bool capturing = false;
 
@@ -208,6 +216,10 @@ void plan_dense(oocnmf_ctx* c) {
     plan_wta(c->sk2, c->mp, c->np, c->num_sms, step);
     c->slots1.alloc(size_t(c->sk1.G * c->sk1.smax) * kTile * c->kp * 4, "slots1");
     c->slots2.alloc(size_t(c->sk2.G * c->sk2.smax) * kTile * c->kp * 4, "slots2");
+    if (c->cnmf) {
+        c->N1.alloc(size_t(c->mp) * c->kp * 4, "AHt");
+        ck(cudaMemsetAsync(c->N1.p, 0, c->N1.bytes, c->stream), "memset");
+    }
 }
 
 void reset_source(oocnmf_ctx* c) {
@@ -272,15 +284,39 @@ cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W,
     return launch_wta(c->kp, A, c->np, W, slots, sk, s);
 }
 
+// HH^T from the per-CTA Gram slots of the last H pass; under CNMF each rank holds a column
+// slab of H, so the f32 and f64 Grams are summed over the ranks (the reference's HH^T
+// all-reduce, src/nmf_distributed.cpp:115).
+void finish_hht(oocnmf_ctx* c) {
+    const int kp = c->kp;
+    count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
+                                 c->HHt.as<float>(), c->HHt64.as<double>(), c->stream),
+          "reduce HHt");
+    if (c->cnmf && c->collective()) {
+        nck(ncclGroupStart(), "ncclGroupStart");
+        nck(ncclAllReduce(c->HHt.p, c->HHt.p, size_t(kp) * kp, ncclFloat, ncclSum, c->comm, c->stream),
+            "allreduce HHt");
+        nck(ncclAllReduce(c->HHt64.p, c->HHt64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, c->stream),
+            "allreduce HHt64");
+        nck(ncclGroupEnd(), "ncclGroupEnd");
+    }
+}
+
 // HH^T of the current Ht (gram only; also refreshes Ht_cat for the tensor-core pass).
 void gram_h(oocnmf_ctx* c) {
     const int kp = c->kp;
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, nullptr, nullptr, nullptr, nullptr, 0.f, false,
                                   c->gram_h.as<double>(), nullptr, c->flag.as<int>(), htlo(c), c->stream),
           "gram H");
-    count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
-                                 c->HHt.as<float>(), c->HHt64.as<double>(), c->stream),
-          "reduce HHt");
+    finish_hht(c);
+}
+
+// CNMF: A·H^T of this rank's column slab (in N1) summed over the ranks before the
+// (replicated) W update (src/nmf_distributed.cpp:124).
+void allreduce_aht(oocnmf_ctx* c) {
+    if (c->cnmf && c->collective())
+        nck(ncclAllReduce(c->N1.p, c->N1.p, size_t(c->mp) * c->kp, ncclFloat, ncclSum, c->comm, c->stream),
+            "allreduce AHt");
 }
 
 // A timing event: inside a graph capture it must be an external event-record node.
@@ -300,10 +336,21 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     if (c->kind == Kind::dense) {
         count(c, pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
         rec(eAht);
-        count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, c->slots1.as<float>(), &c->sk1,
-                                      c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
-                                      c->flag.as<int>(), wlo(c), s),
-              "W update");
+        if (c->cnmf) {
+            // the column slab's A·H^T partials -> one m x kp buffer, summed over the ranks
+            count(c, launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, c->N1.as<float>(), false, s),
+                  "reduce AHt");
+            allreduce_aht(c);
+            count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
+                                          c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
+                                          c->flag.as<int>(), wlo(c), s),
+                  "W update");
+        } else {
+            count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, c->slots1.as<float>(), &c->sk1,
+                                          c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
+                                          c->flag.as<int>(), wlo(c), s),
+                  "W update");
+        }
         count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
         count(c, pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s),
@@ -316,6 +363,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
                              c->Ht.as<float>(), c->N1.as<float>(), s),
               "spmm A Ht");
         rec(eAht);
+        allreduce_aht(c);
         count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
                                       c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
                                       c->flag.as<int>(), nullptr, s),
@@ -370,9 +418,10 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
 void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     const int kp = c->kp;
     cudaStream_t s = c->stream;
-    if (c->collective()) {
+    if (c->collective() && !c->cnmf) {
         // One fused NCCL launch: the packed f32 [W^T A | W^T W] the update consumes and the f64
-        // W^T W the trace-form error consumes.
+        // W^T W the trace-form error consumes. (CNMF: W^T A of the column slab and W^T W of the
+        // replicated W are already complete on every rank.)
         nck(ncclGroupStart(), "ncclGroupStart");
         nck(ncclAllReduce(c->packed.p, c->packed.p, size_t(c->packed_count()), ncclFloat, ncclSum, c->comm, s),
             "allreduce [WtA|WtW]");
@@ -384,9 +433,7 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, c->wta(), nullptr, nullptr, c->wtw(), eps, true,
                                   c->gram_h.as<double>(), c->err_slots.as<double>(), c->flag.as<int>(), htlo(c), s),
           "H update");
-    count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
-                                 c->HHt.as<float>(), c->HHt64.as<double>(), s),
-          "reduce HHt");
+    finish_hht(c);
     if (timed) record(c, ev[eHdone], s);
 }
 
@@ -396,55 +443,58 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
 // relative error of ~1e-7 in them grows by 1/err^2 (SURVEY.md §7 hard part 2).
 constexpr double kAutoDirectBelow = 0.1;
 
-double error_check_once(oocnmf_ctx* c, bool direct_mode, int* bad);
-
-double error_check(oocnmf_ctx* c, int error_mode, int* bad) {
-    // error_mode: 0 auto, 1 direct, 2 trace
-    if (error_mode == 1) return error_check_once(c, true, bad);
-    const double e = error_check_once(c, false, bad);
-    if (error_mode == 0 && !*bad && e < kAutoDirectBelow && c->kind != Kind::host)
-        return error_check_once(c, true, bad);
-    return e;
-}
-
-double error_check_once(oocnmf_ctx* c, bool direct_mode, int* bad) {
+// Enqueue the error evaluation of one check with no host round trip: errs[slot] <- the
+// relative error, flags[slot] <- the sticky non-finite flag. error_mode 0 (auto) computes the
+// trace form and then the direct residual predicated on the device-side estimate being below
+// kAutoDirectBelow (the residual kernels and the second finalize read the predicate and exit
+// when it is 0); 1 (direct) always takes the residual; 2 (trace) never. Out-of-core runs use
+// the trace form only.
+void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
     const int kp = c->kp;
     cudaStream_t s = c->stream;
     double* scal = c->scal.as<double>();
-    const double* direct = nullptr;
+    double* out = c->errs.as<double>() + slot;
+    int* pred = c->pred.as<int>();
+    const bool direct = error_mode != 2 && c->kind != Kind::host;
+    const double threshold = error_mode == 1 ? INFINITY : kAutoDirectBelow;
     const double* eslots = c->err_slots.as<double>();
     int64_t n_err = factor_grid(c->np / kTile);
-    if (direct_mode) {
+    if (c->cnmf && c->collective()) {
+        // CNMF: <W^T A, H> is a sum over the column slabs
+        count(c, launch_reduce_f64(eslots, n_err, scal + kCross, s), "reduce cross");
+        nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s), "allreduce cross");
+        eslots = scal + kCross;
+        n_err = 1;
+    }
+    count(c, launch_finalize_error(kp, eslots, n_err, c->WtW64.as<double>(), c->HHt64.as<double>(), scal + kNormA2,
+                                   nullptr, out, s, nullptr, direct ? pred : nullptr, threshold),
+          "finalize");
+    if (direct) {
         if (c->kind == Kind::dense) {
             count(c, launch_residual_dense(kp, c->A.as<float>(), c->np, c->rows, c->n, c->W.as<float>(),
-                                           c->Ht.as<float>(), c->red_slots.as<double>(), s),
+                                           c->Ht.as<float>(), c->red_slots.as<double>(), s, pred),
                   "residual");
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kRes, s), "reduce");
             if (c->collective())
                 nck(ncclAllReduce(scal + kRes, scal + kRes, 1, ncclDouble, ncclSum, c->comm, s), "allreduce res");
-            direct = scal + kRes;
-        } else if (c->kind == Kind::csr) {
+            count(c, launch_finalize_error(kp, nullptr, 0, c->WtW64.as<double>(), c->HHt64.as<double>(),
+                                           scal + kNormA2, scal + kRes, out, s, pred),
+                  "finalize direct");
+        } else {
             count(c, launch_residual_csr(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows,
-                                         c->n, c->W.as<float>(), c->Ht.as<float>(), c->red_slots.as<double>(), s),
+                                         c->n, c->W.as<float>(), c->Ht.as<float>(), c->red_slots.as<double>(), s,
+                                         pred),
                   "cross");
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kCross, s), "reduce");
             if (c->collective())
                 nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s),
                     "allreduce cross");
-            eslots = scal + kCross;
-            n_err = 1;
+            count(c, launch_finalize_error(kp, scal + kCross, 1, c->WtW64.as<double>(), c->HHt64.as<double>(),
+                                           scal + kNormA2, nullptr, out, s, pred),
+                  "finalize direct");
         }
     }
-    count(c, launch_finalize_error(kp, eslots, n_err, c->WtW64.as<double>(), c->HHt64.as<double>(), scal + kNormA2, direct,
-                                   scal + kErr, s),
-          "finalize");
-    ck(cudaMemcpyAsync(c->hpin, scal + kErr, 8, cudaMemcpyDeviceToHost, s), "D2H err");
-    ck(cudaMemcpyAsync(c->hpin + 1, c->flag.p, 4, cudaMemcpyDeviceToHost, s), "D2H flag");
-    ck(cudaStreamSynchronize(s), "sync");
-    int f = 0;
-    std::memcpy(&f, c->hpin + 1, 4);
-    *bad = f;
-    return c->hpin[0];
+    ck(cudaMemcpyAsync(c->flags.as<int>() + slot, c->flag.p, 4, cudaMemcpyDeviceToDevice, s), "flag");
 }
 
 void ensure_events(oocnmf_ctx* c, size_t n) {
@@ -471,7 +521,7 @@ void prepare_factors(oocnmf_ctx* c, const oocnmf_config* cfg) {
         ck(cudaMemsetAsync(c->W.p, 0, c->W.bytes, c->stream), "memset W");
         ck(cudaMemsetAsync(c->Ht.p, 0, c->Ht.bytes, c->stream), "memset Ht");
         count(c, launch_init_factors(c->W.as<float>(), c->Ht.as<float>(), c->kp, c->k, c->rows, c->row0, c->n,
-                                     cfg->seed, c->stream),
+                                     c->n_global, c->col0, cfg->seed, c->stream),
               "init");
     }
     c->factors_valid = true;
@@ -496,7 +546,7 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
     std::memcpy(&eps_bits, &eps, 4);
     const std::vector<uint64_t> key = {
         uint64_t(c->kind), uint64_t(c->kp), uint64_t(c->mp), uint64_t(c->np), c->rows, count, eps_bits,
-        uint64_t(c->use_tc), uint64_t(c->collective()), uint64_t(reinterpret_cast<uintptr_t>(c->comm)),
+        uint64_t(c->use_tc), uint64_t(c->collective()), uint64_t(c->cnmf), uint64_t(reinterpret_cast<uintptr_t>(c->comm)),
         uint64_t(reinterpret_cast<uintptr_t>(ev)), uint64_t(reinterpret_cast<uintptr_t>(c->A.p)),
         uint64_t(reinterpret_cast<uintptr_t>(c->rp.p)), uint64_t(reinterpret_cast<uintptr_t>(c->rpT.p)),
         uint64_t(reinterpret_cast<uintptr_t>(c->W.p)), uint64_t(reinterpret_cast<uintptr_t>(c->Ht.p)),
@@ -505,9 +555,15 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
         uint64_t(reinterpret_cast<uintptr_t>(c->slots2.p)), uint64_t(reinterpret_cast<uintptr_t>(c->N1.p)),
         uint64_t(reinterpret_cast<uintptr_t>(c->gram_w.p)), uint64_t(reinterpret_cast<uintptr_t>(c->gram_h.p)),
         uint64_t(c->sk1.G), uint64_t(c->sk1.tiles), uint64_t(c->sk2.G), uint64_t(c->sk2.tiles)};
-    if (!c->graph || key != c->graph_key) {
-        if (c->graph) cudaGraphExecDestroy(c->graph);
-        c->graph = nullptr;
+    oocnmf_ctx::Graph* hit = nullptr;
+    for (auto& g : c->graphs)
+        if (g.key == key) hit = &g;
+    if (!hit) {
+        if (c->graphs.size() >= 4) {
+            cudaGraphExecDestroy(c->graphs.front().exec);
+            c->graphs.erase(c->graphs.begin());
+        }
+        cudaGraphExec_t exec = nullptr;
         const uint64_t l0 = c->launches;
         cudaGraph_t g = nullptr;
         bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
@@ -527,20 +583,20 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
             c->capturing = false;
             ok = cudaStreamEndCapture(c->stream, &g) == cudaSuccess && g;
         }
-        ok = ok && cudaGraphInstantiate(&c->graph, g, 0) == cudaSuccess;
+        ok = ok && cudaGraphInstantiate(&exec, g, 0) == cudaSuccess;
         if (g) cudaGraphDestroy(g);
-        c->graph_launches = c->launches - l0;
+        const uint64_t nl = c->launches - l0;
         c->launches = l0;
         if (!ok) {
             cudaGetLastError();
-            c->graph = nullptr;
             c->graph_broken = true;
             return eager();
         }
-        c->graph_key = key;
+        c->graphs.push_back({key, exec, nl});
+        hit = &c->graphs.back();
     }
-    ck(cudaGraphLaunch(c->graph, c->stream), "cudaGraphLaunch");
-    c->launches += c->graph_launches;
+    ck(cudaGraphLaunch(hit->exec, c->stream), "cudaGraphLaunch");
+    c->launches += hit->launches;
 }
 
 void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, double* trace_err,
@@ -571,26 +627,26 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     const uint64_t interval = cfg->error_check_interval;
     const double flops_per_iter = 4.0 * double(c->rows) * double(c->n) * double(c->k) +
                                   2.0 * double(c->rows + c->n) * double(c->k) * double(c->k);
-    ensure_events(c, size_t(kEvPerIter) * (interval + 1) + 2);
-    uint64_t pending = 0;  // iterations with recorded events since the last readback
-    uint64_t iter = 0, nt = 0;
-    bool converged = false;
-    // blocks of iterations end exactly at the error checks (iter % interval == 0, or the last)
-    for (uint64_t next = 1; next <= cfg->max_iters;) {
-        const uint64_t block = std::min<uint64_t>(interval - (next - 1) % interval, cfg->max_iters - next + 1);
-        run_iterations(c, eps, block, c->evs.data());
-        pending = block;
-        inf.flops += flops_per_iter * double(block);
-        iter = next + block - 1;
-        next += block;
-        cudaEvent_t* ce = c->evs.data() + kEvPerIter * pending;
-        ck(cudaEventRecord(ce[0], c->stream), "event");
-        int bad = 0;
-        const double err = error_check(c, cfg->error_mode, &bad);
-        ck(cudaEventRecord(ce[1], c->stream), "event");
+    // Two event sets alternate between consecutive blocks (a block = the iterations up to and
+    // including one error check), so the host reads a block's timings while the next one runs;
+    // the checks themselves are evaluated on the device into errs / flags. Only eta > 0 needs
+    // each value on the host before the next block (early exit), and then the loop syncs.
+    const size_t set_size = size_t(kEvPerIter) * interval + 2;
+    ensure_events(c, 2 * set_size);
+    const uint64_t max_checks = cfg->max_iters / interval + 2;
+    c->errs.alloc(std::max<size_t>(c->errs.bytes, max_checks * 8), "errs");
+    c->flags.alloc(std::max<size_t>(c->flags.bytes, max_checks * 4), "flags");
+    c->pred.alloc(std::max<size_t>(c->pred.bytes, 4), "pred");
+    struct Pending {
+        uint64_t iters;
+        cudaEvent_t* ev;
+    };
+    std::vector<Pending> pend;
+    auto drain = [&](const Pending& p) {
+        cudaEvent_t* ce = p.ev + kEvPerIter * p.iters;
         ck(cudaEventSynchronize(ce[1]), "sync");
-        for (uint64_t p = 0; p < pending; ++p) {
-            cudaEvent_t* e = c->evs.data() + kEvPerIter * p;
+        for (uint64_t i = 0; i < p.iters; ++i) {
+            cudaEvent_t* e = p.ev + kEvPerIter * i;
             inf.aht_pass_ms += elapsed(e[eStart], e[eAht]);
             inf.wta_pass_ms += elapsed(e[eWdone], e[eWta]);
             inf.w_update_s += elapsed(e[eStart], e[eWdone]) * 1e-3;
@@ -600,17 +656,57 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
             inf.wta_pass_launches += 1;
         }
         inf.error_check_s += elapsed(ce[0], ce[1]) * 1e-3;
-        pending = 0;
-        if (bad)
-            fail(OOCNMF_ERR_DATA, "nmf: non-finite factor entries at iteration " + std::to_string(iter));
-        if (trace_iter && nt < trace_cap) {
-            trace_iter[nt] = iter;
-            trace_err[nt] = err;
+    };
+    const bool sync_each = cfg->eta > 0.0;
+    std::vector<uint64_t> check_iter;
+    uint64_t iter = 0, nt = 0;
+    bool converged = false;
+    for (uint64_t next = 1, b = 0; next <= cfg->max_iters; ++b) {
+        const uint64_t block = std::min<uint64_t>(interval - (next - 1) % interval, cfg->max_iters - next + 1);
+        cudaEvent_t* ev = c->evs.data() + set_size * (b & 1);
+        if (pend.size() == 2) {  // the set this block reuses belongs to block b - 2
+            drain(pend.front());
+            pend.erase(pend.begin());
         }
+        run_iterations(c, eps, block, ev);
+        cudaEvent_t* ce = ev + kEvPerIter * block;
+        ck(cudaEventRecord(ce[0], c->stream), "event");
+        enqueue_check(c, cfg->error_mode, nt);
+        ck(cudaEventRecord(ce[1], c->stream), "event");
+        pend.push_back({block, ev});
+        inf.flops += flops_per_iter * double(block);
+        iter = next + block - 1;
+        next += block;
+        check_iter.push_back(iter);
         ++nt;
-        if (err <= cfg->eta) {
-            converged = true;
-            break;
+        if (sync_each) {
+            double e = 0.0;
+            int f = 0;
+            ck(cudaMemcpyAsync(c->hpin, c->errs.as<double>() + nt - 1, 8, cudaMemcpyDeviceToHost, c->stream), "D2H err");
+            ck(cudaMemcpyAsync(c->hpin + 1, c->flags.as<int>() + nt - 1, 4, cudaMemcpyDeviceToHost, c->stream),
+               "D2H flag");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+            std::memcpy(&e, c->hpin, 8);
+            std::memcpy(&f, c->hpin + 1, 4);
+            if (f) break;  // reported below, with the iteration of the first bad check
+            if (e <= cfg->eta) {
+                converged = true;
+                break;
+            }
+        }
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    for (const auto& p : pend) drain(p);
+    std::vector<double> errs(nt);
+    std::vector<int> flags(nt);
+    ck(cudaMemcpy(errs.data(), c->errs.p, nt * 8, cudaMemcpyDeviceToHost), "D2H errs");
+    ck(cudaMemcpy(flags.data(), c->flags.p, nt * 4, cudaMemcpyDeviceToHost), "D2H flags");
+    for (uint64_t i = 0; i < nt; ++i) {
+        if (flags[i])
+            fail(OOCNMF_ERR_DATA, "nmf: non-finite factor entries at iteration " + std::to_string(check_iter[i]));
+        if (trace_iter && i < trace_cap) {
+            trace_iter[i] = check_iter[i];
+            trace_err[i] = errs[i];
         }
     }
     ck(cudaStreamSynchronize(c->stream), "sync");
@@ -634,6 +730,7 @@ void set_problem_impl(oocnmf_ctx* c, uint64_t m, uint64_t n, uint64_t k, uint64_
         fail(OOCNMF_ERR_SHAPE, "dimension exceeds the 2^31 index range of the device layout");
     reset_source(c);
     c->m = m, c->n = n, c->k = k, c->row0 = row0, c->rows = rows;
+    c->cnmf = false, c->col0 = 0, c->n_global = n;
     // Tensor-core passes for every k (measured on B200: the FFMA passes reach only 64% / 48% /
     // 32% of the HBM roofline at kp = 8 / 16 / 32); k <= 8 rides in the kp = 16 layout. The
     // FFMA passes remain selectable (OOCNMF_FORCE_FFMA=1) as an independent cross-check.
@@ -674,6 +771,7 @@ void set_rank_impl(oocnmf_ctx* c, uint64_t k) {
 // A <- A0 o (1 - delta + 2 delta U(seed, 21, .)) from the pristine copy (kept on first use).
 void perturb_impl(oocnmf_ctx* c, double delta, uint64_t seed) {
     need_problem(c);
+    if (c->cnmf) fail(OOCNMF_ERR_SHAPE, "perturb: needs a row-window context (model selection holds the full A)");
     if (!(delta >= 0.0 && delta < 1.0)) fail(OOCNMF_ERR_SHAPE, "perturb: delta must lie in [0, 1)");
     cudaStream_t s = c->stream;
     if (c->kind == Kind::dense) {
@@ -866,9 +964,9 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
         cudaSetDevice(c->device);
         if (c->stream) cudaStreamSynchronize(c->stream);
         if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
-        // the graph holds NCCL work on c->comm: release it before the communicator
-        if (c->graph) cudaGraphExecDestroy(c->graph);
-        c->graph = nullptr;
+        // the graphs hold NCCL work on c->comm: release them before the communicator
+        for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+        c->graphs.clear();
         if (c->comm) ncclCommDestroy(c->comm);
         for (auto e : c->evs) cudaEventDestroy(e);
         for (int i = 0; i < 2; ++i) {
@@ -947,6 +1045,8 @@ int oocnmf_load_dense_device_f32(oocnmf_ctx* c, const float* d_a, uint64_t lda) 
 int oocnmf_generate_dense_uniform(oocnmf_ctx* c, uint64_t seed, uint64_t stream) {
     return guarded([&] {
         set_dev(c);
+        need_problem(c);
+        if (c->cnmf) fail(OOCNMF_ERR_SHAPE, "generators produce row windows; load a column slab instead");
         load_dense_common(c);
         ck(launch_gen_dense_uniform(c->A.as<float>(), c->np, c->rows, c->n, c->row0, c->n, seed, stream, c->stream),
            "generate");
@@ -990,6 +1090,7 @@ int oocnmf_generate_csr_uniform(oocnmf_ctx* c, double density, uint64_t seed) {
         set_dev(c);
         need_problem(c);
         if (!(density >= 0.0) || density > 1.0) fail(OOCNMF_ERR_SHAPE, "density must lie in [0, 1]");
+        if (c->cnmf) fail(OOCNMF_ERR_SHAPE, "generators produce row windows; load a column slab instead");
         reset_source(c);
         // U < density  <=>  bits53 < ceil(density * 2^53)  (exact: power-of-two scaling)
         const uint64_t thresh = uint64_t(std::ceil(density * 0x1.0p53));
@@ -1016,6 +1117,7 @@ int oocnmf_attach_host_dense_f32(oocnmf_ctx* c, const float* a, uint64_t lda, ui
     return guarded([&] {
         set_dev(c);
         need_problem(c);
+        if (c->cnmf) fail(OOCNMF_ERR_SHAPE, "out-of-core streaming is row-partitioned (RNMF) only");
         if (lda < c->n) fail(OOCNMF_ERR_SHAPE, "lda < n");
         reset_source(c);
         int64_t br = int64_t(batch_rows);
@@ -1124,6 +1226,7 @@ int oocnmf_get_factors_f64(oocnmf_ctx* c, double* w, double* h) {
 }
 
 int oocnmf_gather_w_f64(oocnmf_ctx* c, double* w_full) {
+    if (c && c->cnmf) return oocnmf_get_factors_f64(c, w_full, nullptr);  // W is replicated under CNMF
     return guarded([&] {
         set_dev(c);
         need_problem(c);
@@ -1220,6 +1323,40 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
                 hht[r * k + j] = g1[r * kp + j];
                 wtw[r * k + j] = g2[r * kp + j];
             }
+    });
+}
+
+int oocnmf_set_problem_cols(oocnmf_ctx* c, uint64_t m, uint64_t n, uint64_t k, uint64_t col0, uint64_t cols) {
+    return guarded([&] {
+        set_dev(c);
+        if (cols < 1 || col0 + cols > n) fail(OOCNMF_ERR_SHAPE, "column slab out of bounds");
+        set_problem_impl(c, m, cols, k, 0, m);
+        c->cnmf = true, c->col0 = col0, c->n_global = n;
+    });
+}
+
+int oocnmf_gather_h_f64(oocnmf_ctx* c, double* h_full) {
+    return guarded([&] {
+        set_dev(c);
+        need_problem(c);
+        if (!c->factors_valid) fail(OOCNMF_ERR_SHAPE, "factors are not initialised");
+        const int kp = c->kp;
+        std::vector<float> hh(size_t(c->np) * kp);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        ck(cudaMemcpy(hh.data(), c->Ht.p, hh.size() * 4, cudaMemcpyDeviceToHost), "D2H H");
+        // zero-padded sum over the ranks' column slabs (the reference's gather,
+        // src/nmf_distributed.cpp:267-273)
+        std::fill(h_full, h_full + c->k * c->n_global, 0.0);
+        for (uint64_t r = 0; r < c->k; ++r)
+            for (uint64_t j = 0; j < c->n; ++j) h_full[r * c->n_global + c->col0 + j] = hh[j * kp + r];
+        if (c->collective()) {
+            DevBuf d;
+            d.alloc(c->k * c->n_global * 8, "gather H");
+            ck(cudaMemcpyAsync(d.p, h_full, d.bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+            nck(ncclAllReduce(d.p, d.p, c->k * c->n_global, ncclDouble, ncclSum, c->comm, c->stream), "allreduce H");
+            ck(cudaMemcpyAsync(h_full, d.p, d.bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+        }
     });
 }
 

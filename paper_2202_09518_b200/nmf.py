@@ -184,6 +184,14 @@ class CsrMatrix:
         b, e = int(rp[0]), int(rp[-1])
         return CsrMatrix(r1 - r0, self.cols, (rp - b).astype(np.uint64), self.col_idx[b:e], self.values[b:e])
 
+    def col_window(self, c0, c1):
+        """All rows, columns [c0, c1), column indices rebased to the window."""
+        ci = self.col_idx.astype(np.int64)
+        keep = (ci >= c0) & (ci < c1)
+        rows = np.repeat(np.arange(self.rows), np.diff(self.row_ptr.astype(np.int64)))
+        rp = np.concatenate([[0], np.cumsum(np.bincount(rows[keep], minlength=self.rows))]).astype(np.uint64)
+        return CsrMatrix(self.rows, c1 - c0, rp, (ci[keep] - c0).astype(np.uint64), self.values[keep])
+
 
 # ----------------------------------------------------------------------------- helpers
 def device_count() -> int:
@@ -258,6 +266,7 @@ class Context:
         rows = m - row0 if rows is None else rows
         check(_capi.lib().oocnmf_set_problem(self._h, m, n, k, row0, rows))
         self.m, self.n, self.k, self.row0, self.rows = m, n, k, row0, rows
+        self.n_global, self.col0 = n, 0
 
     def load_dense(self, a: np.ndarray):
         a = np.asarray(a)
@@ -321,10 +330,22 @@ class Context:
         check(_capi.lib().oocnmf_get_factors_f64(self._h, _p(w, C.c_double), _p(h, C.c_double)))
         return w, h
 
+    def set_problem_cols(self, m, n, k, col0, cols):
+        """Column partition (CNMF): all m rows, columns [col0, col0 + cols) of the m x n A."""
+        check(_capi.lib().oocnmf_set_problem_cols(self._h, m, n, k, col0, cols))
+        self.m, self.n, self.k, self.row0, self.rows = m, cols, k, 0, m
+        self.n_global, self.col0 = n, col0
+
     def gather_w(self):
         w = np.empty((self.m, self.k))
         check(_capi.lib().oocnmf_gather_w_f64(self._h, _p(w, C.c_double)))
         return w
+
+    def gather_h(self):
+        """CNMF: the full H (k x n_global) on every rank."""
+        h = np.empty((self.k, self.n_global))
+        check(_capi.lib().oocnmf_gather_h_f64(self._h, _p(h, C.c_double)))
+        return h
 
     def solve(self, cfg: NmfConfig):
         cfg.validate()
@@ -479,10 +500,24 @@ def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host
         raise ShapeError(f"nmf_distributed: cfg.k={cfg.k} disagrees with plan.k={plan.k}")
     if comm.size != plan.n_workers:
         raise ShapeError(f"nmf_distributed: group size {comm.size} != plan workers {plan.n_workers}")
-    if plan.strategy != Strategy.rnmf:
-        raise ShapeError("nmf_distributed: the B200 backend implements the row partition (RNMF) only")
-    (r0, r1), _ = plan.slabs[comm.rank]
     ctx = comm.ctx
+    if plan.strategy == Strategy.cnmf:
+        # column partition (src/nmf_distributed.cpp:112-149): W replicated, H column slabs
+        if host_slab is not None:
+            raise ShapeError("nmf_distributed: out-of-core streaming is row-partitioned (RNMF) only")
+        _, (c0, c1) = plan.slabs[comm.rank]
+        ctx.set_problem_cols(plan.m, plan.n, plan.k, c0, c1 - c0)
+        if isinstance(a, CsrMatrix):
+            ctx.load_csr(a.col_window(c0, c1))
+        else:
+            ctx.load_dense(np.ascontiguousarray(np.asarray(a)[:, c0:c1]))
+        if cfg.init == FactorInit.from_files:
+            ctx.set_factors(cfg.init_w, np.ascontiguousarray(np.asarray(cfg.init_h)[:, c0:c1]))
+        trace, info = ctx.solve(cfg)
+        w, _ = ctx.get_factors()
+        h = ctx.gather_h()
+        return NmfResult(w, h, trace, int(info["iterations_run"]), bool(info["converged"]), _counters(info), info)
+    (r0, r1), _ = plan.slabs[comm.rank]
     ctx.set_problem(plan.m, plan.n, plan.k, r0, r1 - r0)
     if host_slab is not None:
         ctx.attach_host(host_slab, batch_rows)

@@ -30,8 +30,8 @@ def main(out_path):
     port = oracle.port
     results = {}
 
-    def run(name, a, m, n, k, iters, interval, host_slab=None, batch_rows=0, **kw):
-        plan = nmf.make_plan(m, n, k, world, 1, nmf.Strategy.rnmf)
+    def run(name, a, m, n, k, iters, interval, host_slab=None, batch_rows=0, strategy=nmf.Strategy.rnmf, **kw):
+        plan = nmf.make_plan(m, n, k, world, 1, strategy)
         w0, h0 = port.init_factors(m, n, k, 0)
         cfg = nmf.NmfConfig(k=k, max_iters=iters, error_check_interval=interval, eta=0.0,
                             init=nmf.FactorInit.from_files, init_w=f32(w0), init_h=f32(h0), device=local, **kw)
@@ -51,6 +51,12 @@ def main(out_path):
     rp, ci, v, (m, n) = port.gen_sparse(1500, 1200, 0.02, 3)
     run("csr_k16", nmf.CsrMatrix(m, n, rp, ci, f32(v)), m, n, 16, 20, 10)
     run("ooc_k32", None, 1100, 900, 32, 20, 10, host_slab=a, batch_rows=128)
+    # column partition (CNMF) on wide inputs: W replicated, H column slabs
+    wide = port.uniform_dense(700, 1300, 7, 99).astype(np.float32)
+    run("cnmf_dense_k16", wide, 700, 1300, 16, 30, 10, strategy=nmf.Strategy.cnmf)
+    run("cnmf_dense_k32", wide, 700, 1300, 32, 30, 10, strategy=nmf.Strategy.cnmf)
+    rp2, ci2, v2, (m2, n2) = port.gen_sparse(900, 1600, 0.02, 5)
+    run("cnmf_csr_k16", nmf.CsrMatrix(m2, n2, rp2, ci2, f32(v2)), m2, n2, 16, 20, 10, strategy=nmf.Strategy.cnmf)
     # model selection: the P runs of each k spread over the ranks as replicas
     lr = oracle.ref.gen_lowrank(96, 64, 3, 0.01, 5)[0] if oracle.ref.available else port.uniform_dense(96, 64, 5, 1)
     scfg = nmf.SelectionConfig(k_min=1, k_max=4, n_perturbations=5, seed=3,

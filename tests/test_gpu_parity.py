@@ -380,3 +380,26 @@ def test_resident_warm_restart_continues_trajectory(gpu):
         tr, _ = ctx.solve(nmf.NmfConfig(k=16, max_iters=10, error_check_interval=10, eta=0.0,
                                         init=nmf.FactorInit.resident))
     assert tr[0][1] == pytest.approx(ref.trace_err[1], rel=TRACE_TOL)
+
+
+@pytest.mark.parametrize("csr", [False, True])
+def test_column_partition_on_one_gpu_equals_serial(gpu, csr):
+    # CNMF with one rank: the A·H^T reduction path and the H-slab bookkeeping must reproduce
+    # nmf_serial on the same inputs (the multi-rank case is tests/test_multi_gpu.py)
+    m, n, k = 300, 520, 12
+    d = port.uniform_dense(m, n, 3, 99)
+    if csr:
+        d[d < 0.7] = 0.0
+    a = nmf.CsrMatrix.from_dense(f32(d)) if csr else d.astype(np.float32)
+    w0, h0 = port.init_factors(m, n, k, 0)
+    cfg = nmf.NmfConfig(k=k, max_iters=30, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0), device=gpu)
+    ser = nmf.nmf_serial(a, cfg)
+    comm = nmf.DistComm(0, 1, gpu)
+    try:
+        res = nmf.nmf_distributed(a, cfg, nmf.make_plan(m, n, k, 1, 1, nmf.Strategy.cnmf), comm)
+    finally:
+        comm.close()
+    np.testing.assert_allclose([e for _, e in res.error_trace], [e for _, e in ser.error_trace], rtol=1e-6)
+    assert rel_fro(res.w, ser.w) < 1e-5 and rel_fro(res.h, ser.h) < 1e-5
+    assert res.h.shape == (k, n)

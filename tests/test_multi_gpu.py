@@ -95,3 +95,27 @@ def test_distributed_select_k_equals_single_gpu(dist_results):
         assert got == [want.k, want.valid, want.runs_used, want.min_silhouette, want.mean_silhouette,
                        want.mean_relative_error]
     assert r["medians_sum"] == [float(x.medians.sum()) for x in rep.records]
+
+
+@pytest.mark.parametrize("name,k", [("cnmf_dense_k16", 16), ("cnmf_dense_k32", 32)])
+def test_dense_cnmf_matches_reference(dist_results, name, k):
+    # column partition vs the compiled reference's CNMF worker (threads, same plan)
+    if not oracle.ref.available:
+        pytest.skip("needs oracle/_ref")
+    world, res = dist_results
+    a = f32(oracle.port.uniform_dense(700, 1300, 7, 99))
+    w0, h0 = oracle.port.init_factors(700, 1300, k, 0)
+    ref = oracle.ref.nmf_distributed(a, k, world, 1, strategy=1, w0=f32(w0), h0=f32(h0), max_iters=30, interval=10)
+    _check(res[name], ref)
+    assert res[name]["w_shape"] == [700, k]
+
+
+def test_csr_cnmf_matches_reference(dist_results):
+    if not oracle.ref.available:
+        pytest.skip("needs oracle/_ref")
+    world, res = dist_results
+    rp, ci, v, shape = oracle.port.gen_sparse(900, 1600, 0.02, 5)
+    w0, h0 = oracle.port.init_factors(900, 1600, 16, 0)
+    ref = oracle.ref.nmf_distributed((rp, ci, f32(v), shape), 16, world, 1, strategy=1, w0=f32(w0), h0=f32(h0),
+                                     max_iters=20, interval=10)
+    _check(res["cnmf_csr_k16"], ref)
