@@ -528,8 +528,8 @@ void prepare_factors(oocnmf_ctx* c, const oocnmf_config* cfg) {
 }
 
 // `count` MU iterations; iteration i records its events into ev + kEvPerIter * i. In-core
-// problems replay a captured CUDA graph of the whole block (one launch instead of ~10 per
-// iteration and no host round trips between them); OOCNMF_NO_GRAPH=1 iterates eagerly.
+// single-rank problems replay a captured CUDA graph of the whole block (one launch instead of
+// ~10 per iteration); OOCNMF_NO_GRAPH=1 iterates eagerly.
 void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
     static const bool no_graph = [] {
         const char* e = std::getenv("OOCNMF_NO_GRAPH");
@@ -541,7 +541,11 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
             h_update(c, eps, true, ev + kEvPerIter * i);
         }
     };
-    if (no_graph || c->graph_broken || c->kind == Kind::host) return eager();
+    // Graphs for single-rank solves only: replaying NCCL work from graphs made every launch
+    // pay NCCL's graph/non-graph mixing synchronisation (4 x B200: 555 it/s with graphs, 634
+    // eager, 627 with NCCL_GRAPH_MIXING_SUPPORT=0), while the eager loop keeps the queue full
+    // now that the error checks no longer sync the host.
+    if (no_graph || c->graph_broken || c->kind == Kind::host || c->collective()) return eager();
     uint32_t eps_bits;
     std::memcpy(&eps_bits, &eps, 4);
     const std::vector<uint64_t> key = {
@@ -657,7 +661,11 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         }
         inf.error_check_s += elapsed(ce[0], ce[1]) * 1e-3;
     };
-    const bool sync_each = cfg->eta > 0.0;
+    static const bool force_sync = [] {
+        const char* e = std::getenv("OOCNMF_SYNC_CHECKS");
+        return e && e[0] == '1';
+    }();
+    const bool sync_each = cfg->eta > 0.0 || force_sync;
     std::vector<uint64_t> check_iter;
     uint64_t iter = 0, nt = 0;
     bool converged = false;
