@@ -238,6 +238,32 @@ int oocnmf_cluster_silhouette(const double* runs, uint64_t nruns, uint64_t m, ui
 int oocnmf_pearson_correlation(const double* w_true, uint64_t m, uint64_t k1, const double* w_est,
                                uint64_t k2, double* corr);
 
+/* ----- matrix files (include/oocnmf/io.hpp:28-66, src/io.cpp), host-side -----
+ * PDN1: "PDNMF\0v1", u8 kind (0 dense, 1 CSR), u8 dtype, u64 rows, u64 cols, little-endian;
+ * dense payload row-major; CSR payload u64 nnz, u64 row_ptr[rows+1], u64 col_idx[nnz], values.
+ * dtype 0 = f64 (the reference's only type), 1 = f32 (B200 extension in the reserved byte).
+ * Matrix Market: array (column-major) / coordinate, real or integer, general. */
+int oocnmf_pdn1_info(const char* path, int32_t* kind, int32_t* dtype, uint64_t* rows, uint64_t* cols,
+                     uint64_t* nnz);
+/* dense window [r0, r1) x [c0, c1), row-major (Pdn1File::read_dense_window) */
+int oocnmf_pdn1_read_dense(const char* path, uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1, double* out);
+int oocnmf_pdn1_read_dense_f32(const char* path, uint64_t r0, uint64_t r1, uint64_t c0, uint64_t c1,
+                               float* out);
+/* CSR rows [r0, r1), row_ptr rebased, global column indices (Pdn1File::read_csr_rows) */
+int oocnmf_pdn1_csr_rows_nnz(const char* path, uint64_t r0, uint64_t r1, uint64_t* nnz);
+int oocnmf_pdn1_read_csr_rows(const char* path, uint64_t r0, uint64_t r1, uint64_t* row_ptr, uint64_t* col_idx,
+                              double* vals);
+int oocnmf_pdn1_write_dense(const char* path, const double* a, uint64_t rows, uint64_t cols, int32_t dtype);
+int oocnmf_pdn1_write_dense_f32(const char* path, const float* a, uint64_t rows, uint64_t cols);
+int oocnmf_pdn1_write_csr(const char* path, uint64_t rows, uint64_t cols, const uint64_t* row_ptr,
+                          const uint64_t* col_idx, const double* vals, int32_t dtype);
+/* kind 0 = array (dense), 1 = coordinate (CSR; repeated cells keep their last value) */
+int oocnmf_mtx_info(const char* path, int32_t* kind, uint64_t* rows, uint64_t* cols, uint64_t* nnz);
+int oocnmf_mtx_read(const char* path, double* dense_out, uint64_t* row_ptr, uint64_t* col_idx, double* vals);
+int oocnmf_mtx_write_dense(const char* path, const double* a, uint64_t rows, uint64_t cols);
+int oocnmf_mtx_write_csr(const char* path, uint64_t rows, uint64_t cols, const uint64_t* row_ptr,
+                         const uint64_t* col_idx, const double* vals);
+
 /* ----- one-shot drop-ins for nmf_serial(MatrixRef a, const NmfConfig& cfg) on host
  * buffers: upload, solve, download. w0/h0 are used iff cfg->init == 1. */
 int oocnmf_nmf_serial_dense_f64(int device, const double* a, uint64_t m, uint64_t n,

@@ -17,6 +17,7 @@
 #include <stdexcept>
 #include <string>
 #include <utility>
+#include <variant>
 #include <vector>
 
 #include "oocnmf_b200.h"
@@ -248,6 +249,49 @@ struct StoreCounters {
 /// Returns the gathered W (m x k) and replicated H on every rank.
 NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan, CommHandle& comm,
                           const StoreConfig& store_cfg = {}, StoreCounters* store_counters_out = nullptr);
+
+// ---- matrix files (reference: include/oocnmf/io.hpp) ----
+struct AnyMatrix {
+    std::variant<DenseMatrix, CsrMatrix> value;
+    bool is_dense() const { return std::holds_alternative<DenseMatrix>(value); }
+    const DenseMatrix& dense() const { return std::get<DenseMatrix>(value); }
+    const CsrMatrix& sparse() const { return std::get<CsrMatrix>(value); }
+    MatrixRef ref() const { return is_dense() ? MatrixRef(dense()) : MatrixRef(sparse()); }
+    index_t rows() const { return is_dense() ? dense().rows() : sparse().rows(); }
+    index_t cols() const { return is_dense() ? dense().cols() : sparse().cols(); }
+};
+
+void write_pdn1(const std::string& path, const DenseMatrix& m);
+void write_pdn1(const std::string& path, const CsrMatrix& m);
+/// B200 extension: PDN1 dtype 1 (f32 values), the byte the reference reserves.
+void write_pdn1_f32(const std::string& path, const DenseMatrix& m);
+void write_pdn1_f32(const std::string& path, const CsrMatrix& m);
+AnyMatrix read_pdn1(const std::string& path);
+
+/// Random-access reader over a PDN1 file (f64 or f32 payload).
+class Pdn1File {
+public:
+    explicit Pdn1File(const std::string& path);
+    bool is_dense() const { return kind_ == 0; }
+    index_t rows() const { return rows_; }
+    index_t cols() const { return cols_; }
+    index_t nnz() const { return nnz_; }
+    int dtype() const { return dtype_; }
+    DenseMatrix read_dense_window(IndexRange r, IndexRange c) const;
+    CsrMatrix read_csr_rows(IndexRange r) const;  // global column indices
+    index_t window_bytes(IndexRange r, IndexRange c) const;
+
+private:
+    std::string path_;
+    int kind_ = 0, dtype_ = 0;
+    index_t rows_ = 0, cols_ = 0, nnz_ = 0;
+};
+
+void write_mtx(const std::string& path, const DenseMatrix& m);
+void write_mtx(const std::string& path, const CsrMatrix& m);
+AnyMatrix read_mtx(const std::string& path);
+/// Dispatch on extension: .mtx -> Matrix Market, anything else -> PDN1.
+AnyMatrix read_matrix(const std::string& path);
 
 // ---- model selection (reference: include/oocnmf/model_selection.hpp) ----
 struct SelectionConfig {

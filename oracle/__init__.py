@@ -423,6 +423,53 @@ class Ref(_Lib):
         self._check(f(_ptr(a), a.shape[0], a.shape[1], delta, seed, _ptr(out)))
         return out
 
+    # ---- matrix files (include/oocnmf/io.hpp) ----
+    def write_pdn1(self, path, a):
+        b = str(path).encode()
+        if isinstance(a, tuple):
+            rp, ci, v, (m, n) = a
+            rp, ci = np.ascontiguousarray(rp, np.uint64), np.ascontiguousarray(ci, np.uint64)
+            v = np.ascontiguousarray(v, np.float64)
+            f = self.lib.ref_write_pdn1_csr
+            f.argtypes = [C.c_char_p, _u64, _u64, _pu, _pu, _pd]
+            self._check(f(b, m, n, _ptr(rp, _pu), _ptr(ci, _pu), _ptr(v)))
+        else:
+            a = np.ascontiguousarray(a, np.float64)
+            f = self.lib.ref_write_pdn1_dense
+            f.argtypes = [C.c_char_p, _pd, _u64, _u64]
+            self._check(f(b, _ptr(a), a.shape[0], a.shape[1]))
+
+    def write_mtx(self, path, a):
+        b = str(path).encode()
+        if isinstance(a, tuple):
+            rp, ci, v, (m, n) = a
+            rp, ci = np.ascontiguousarray(rp, np.uint64), np.ascontiguousarray(ci, np.uint64)
+            v = np.ascontiguousarray(v, np.float64)
+            f = self.lib.ref_write_mtx_csr
+            f.argtypes = [C.c_char_p, _u64, _u64, _pu, _pu, _pd]
+            self._check(f(b, m, n, _ptr(rp, _pu), _ptr(ci, _pu), _ptr(v)))
+        else:
+            a = np.ascontiguousarray(a, np.float64)
+            f = self.lib.ref_write_mtx_dense
+            f.argtypes = [C.c_char_p, _pd, _u64, _u64]
+            self._check(f(b, _ptr(a), a.shape[0], a.shape[1]))
+
+    def read_matrix(self, path):
+        """dense ndarray or (row_ptr, col_idx, values, (m, n))"""
+        b = str(path).encode()
+        f = self.lib.ref_read_matrix
+        f.argtypes = [C.c_char_p, _pi, _pu, _pu, _pu, _pd, _pu, _pu, _pd]
+        kind, m, n, nnz = C.c_int(), _u64(), _u64(), _u64()
+        self._check(f(b, C.byref(kind), C.byref(m), C.byref(n), C.byref(nnz), None, None, None, None))
+        if kind.value == 0:
+            d = np.zeros((m.value, n.value))
+            self._check(f(b, C.byref(kind), C.byref(m), C.byref(n), C.byref(nnz), _ptr(d), None, None, None))
+            return d
+        rp, ci, v = np.zeros(m.value + 1, np.uint64), np.zeros(nnz.value, np.uint64), np.zeros(nnz.value)
+        self._check(f(b, C.byref(kind), C.byref(m), C.byref(n), C.byref(nnz), None, _ptr(rp, _pu), _ptr(ci, _pu),
+                      _ptr(v)))
+        return rp, ci, v, (m.value, n.value)
+
 
 port = Port()
 ref = Ref()

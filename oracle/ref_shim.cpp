@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "oocnmf/io.hpp"
 #include "oocnmf/kernels.hpp"
 #include "oocnmf/model_selection.hpp"
 #include "oocnmf/nmf.hpp"
@@ -395,6 +396,43 @@ int ref_perturb_dense(const double* a, std::uint64_t m, std::uint64_t n, double 
         DenseMatrix A = copy_dense(a, m, n);
         DenseMatrix P = perturb_dense(MatrixRef(A), delta, seed);
         std::memcpy(out, P.data(), m * n * sizeof(double));
+    });
+}
+
+// ---- matrix files (include/oocnmf/io.hpp) ----
+int ref_write_pdn1_dense(const char* path, const double* a, std::uint64_t m, std::uint64_t n) {
+    return guarded([&] { write_pdn1(path, copy_dense(a, m, n)); });
+}
+int ref_write_mtx_dense(const char* path, const double* a, std::uint64_t m, std::uint64_t n) {
+    return guarded([&] { write_mtx(path, copy_dense(a, m, n)); });
+}
+static CsrMatrix io_csr(std::uint64_t m, std::uint64_t n, const std::uint64_t* rp, const std::uint64_t* ci,
+                          const double* v) {
+    return CsrMatrix(m, n, std::vector<index_t>(rp, rp + m + 1), std::vector<index_t>(ci, ci + rp[m]),
+                     std::vector<double>(v, v + rp[m]));
+}
+int ref_write_pdn1_csr(const char* path, std::uint64_t m, std::uint64_t n, const std::uint64_t* rp,
+                       const std::uint64_t* ci, const double* v) {
+    return guarded([&] { write_pdn1(path, io_csr(m, n, rp, ci, v)); });
+}
+int ref_write_mtx_csr(const char* path, std::uint64_t m, std::uint64_t n, const std::uint64_t* rp,
+                      const std::uint64_t* ci, const double* v) {
+    return guarded([&] { write_mtx(path, io_csr(m, n, rp, ci, v)); });
+}
+// read_matrix: dims first (outputs null), then fill
+int ref_read_matrix(const char* path, int* kind, std::uint64_t* m, std::uint64_t* n, std::uint64_t* nnz,
+                    double* dense, std::uint64_t* rp, std::uint64_t* ci, double* v) {
+    return guarded([&] {
+        AnyMatrix a = read_matrix(path);
+        *kind = a.is_dense() ? 0 : 1;
+        *m = a.rows(), *n = a.cols();
+        *nnz = a.is_dense() ? 0 : a.sparse().nnz();
+        if (a.is_dense() && dense) std::memcpy(dense, a.dense().data(), a.dense().size() * sizeof(double));
+        if (!a.is_dense() && rp) {
+            const CsrMatrix& s = a.sparse();
+            for (index_t i = 0; i <= s.rows(); ++i) rp[i] = s.row_ptr()[i];
+            for (index_t p = 0; p < s.nnz(); ++p) ci[p] = s.col_idx()[p], v[p] = s.values()[p];
+        }
     });
 }
 

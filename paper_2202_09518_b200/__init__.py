@@ -41,4 +41,6 @@ from .nmf import (  # noqa: F401
     split_even,
 )
 
+from .io import Pdn1File, read_matrix, read_mtx, read_pdn1, write_mtx, write_pdn1  # noqa: F401,E402
+
 __version__ = "0.1.0"

@@ -90,6 +90,18 @@ _SIGS = {
                         C.c_int),
     "oocnmf_cluster_silhouette": ([pd, u64, u64, u64, pd, pd, pd, pd, pu, pi64], C.c_int),
     "oocnmf_pearson_correlation": ([pd, u64, u64, pd, u64, pd], C.c_int),
+    "oocnmf_pdn1_info": ([C.c_char_p, C.POINTER(i32), C.POINTER(i32), pu, pu, pu], C.c_int),
+    "oocnmf_pdn1_read_dense": ([C.c_char_p, u64, u64, u64, u64, pd], C.c_int),
+    "oocnmf_pdn1_read_dense_f32": ([C.c_char_p, u64, u64, u64, u64, pf], C.c_int),
+    "oocnmf_pdn1_csr_rows_nnz": ([C.c_char_p, u64, u64, pu], C.c_int),
+    "oocnmf_pdn1_read_csr_rows": ([C.c_char_p, u64, u64, pu, pu, pd], C.c_int),
+    "oocnmf_pdn1_write_dense": ([C.c_char_p, pd, u64, u64, i32], C.c_int),
+    "oocnmf_pdn1_write_dense_f32": ([C.c_char_p, pf, u64, u64], C.c_int),
+    "oocnmf_pdn1_write_csr": ([C.c_char_p, u64, u64, pu, pu, pd, i32], C.c_int),
+    "oocnmf_mtx_info": ([C.c_char_p, C.POINTER(i32), pu, pu, pu], C.c_int),
+    "oocnmf_mtx_read": ([C.c_char_p, pd, pu, pu, pd], C.c_int),
+    "oocnmf_mtx_write_dense": ([C.c_char_p, pd, u64, u64], C.c_int),
+    "oocnmf_mtx_write_csr": ([C.c_char_p, u64, u64, pu, pu, pd], C.c_int),
     "oocnmf_nmf_serial_dense_f64": ([C.c_int, pd, u64, u64, C.POINTER(Config), pd, pd, pd, pd, pu, pd, u64,
                                      C.POINTER(Info)], C.c_int),
     "oocnmf_nmf_serial_dense_f32": ([C.c_int, pf, u64, u64, C.POINTER(Config), pd, pd, pd, pd, pu, pd, u64,

@@ -284,6 +284,50 @@ CommHandle::CommHandle(int rank, int size, int device, const UniqueId& id) : ran
     ctx_ = std::shared_ptr<oocnmf_ctx>(c, [](oocnmf_ctx* p) { oocnmf_ctx_destroy(p); });
 }
 
+namespace {
+// This rank's window of A (rows for RNMF, columns for CNMF) from memory or from a PDN1 /
+// Matrix Market file (ASource::file: a PDN1 file is read window-only, like the reference's
+// ChunkStore over a file).
+void upload_slab(oocnmf_ctx* c, const ASource& a, const PartitionPlan& plan, const WorkerSlab& slab) {
+    const bool col = plan.strategy == Strategy::cnmf;
+    auto put = [&](MatrixRef full_or_win, bool is_window) {
+        if (is_window) {
+            upload(c, full_or_win, 0, full_or_win.rows());
+            return;
+        }
+        if (full_or_win.rows() != plan.m || full_or_win.cols() != plan.n)
+            throw ShapeError("nmf_distributed: A does not match the plan");
+        if (col)
+            upload(c, full_or_win.window({0, plan.m}, slab.a_cols), 0, plan.m);
+        else
+            upload(c, full_or_win, slab.a_rows.begin, slab.a_rows.end);
+    };
+    if (a.pdn1_path.empty()) {
+        if (a.mem.empty()) throw ShapeError("nmf_distributed: empty A source");
+        put(a.mem, false);
+        return;
+    }
+    const std::string& p = a.pdn1_path;
+    if (p.size() >= 4 && p.compare(p.size() - 4, 4, ".mtx") == 0) {
+        const AnyMatrix full = read_mtx(p);
+        put(full.ref(), false);
+        return;
+    }
+    Pdn1File f(p);
+    if (f.rows() != plan.m || f.cols() != plan.n) throw ShapeError("nmf_distributed: file A does not match the plan");
+    if (f.is_dense()) {
+        const DenseMatrix win = f.read_dense_window(slab.a_rows, slab.a_cols);
+        put(MatrixRef(win), true);
+    } else if (col) {
+        const CsrMatrix all = f.read_csr_rows({0, plan.m});
+        put(MatrixRef(all).window({0, plan.m}, slab.a_cols), true);
+    } else {
+        const CsrMatrix rows = f.read_csr_rows(slab.a_rows);
+        put(MatrixRef(rows), true);
+    }
+}
+}  // namespace
+
 NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan, CommHandle& comm,
                           const StoreConfig& store_cfg, StoreCounters* store_counters_out) {
     cfg.validate();
@@ -293,18 +337,15 @@ NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const Partitio
     if (comm.size() != plan.n_workers)
         throw ShapeError("nmf_distributed: group size " + std::to_string(comm.size()) + " != plan workers " +
                          std::to_string(plan.n_workers));
-    if (!a.pdn1_path.empty()) throw IoError("nmf_distributed: PDN1 file sources are not supported by the B200 backend");
     if (!comm.context()) throw CommError("nmf_distributed: CommHandle has no device context");
     oocnmf_ctx* c = comm.context();
     const WorkerSlab& slab = plan.slabs[std::size_t(comm.rank())];
     if (plan.strategy == Strategy::cnmf) {
         // column partition (src/nmf_distributed.cpp:112-149): W replicated, H column slabs
         if (a.host_f32) throw ShapeError("nmf_distributed: out-of-core streaming is row-partitioned (RNMF) only");
-        if (a.mem.empty()) throw ShapeError("nmf_distributed: empty A source");
         const index_t m = plan.m, n = plan.n, k = plan.k, c0 = slab.a_cols.begin, cols = slab.a_cols.extent();
-        if (a.mem.rows() != m || a.mem.cols() != n) throw ShapeError("nmf_distributed: A does not match the plan");
         throw_status(oocnmf_set_problem_cols(c, m, n, k, c0, cols));
-        upload(c, a.mem.window({0, m}, {c0, c0 + cols}), 0, m);
+        upload_slab(c, a, plan, slab);
         if (cfg.init == FactorInit::from_files) {
             if (cfg.init_w->rows() != m || cfg.init_w->cols() != k || cfg.init_h->rows() != k ||
                 cfg.init_h->cols() != n)
@@ -335,9 +376,7 @@ NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const Partitio
         const index_t batch = store_cfg.budget_bytes ? std::max<index_t>(128, store_cfg.budget_bytes / 2 / per_row) : 0;
         throw_status(oocnmf_attach_host_dense_f32(c, a.host_f32, a.host_ld ? a.host_ld : n, batch));
     } else {
-        if (a.mem.empty()) throw ShapeError("nmf_distributed: empty A source");
-        if (a.mem.rows() != m || a.mem.cols() != n) throw ShapeError("nmf_distributed: A does not match the plan");
-        upload(c, a.mem, r0, r0 + rows);
+        upload_slab(c, a, plan, slab);
     }
     if (cfg.init == FactorInit::from_files) {
         if (cfg.init_w->rows() != m || cfg.init_w->cols() != k || cfg.init_h->rows() != k || cfg.init_h->cols() != n)
@@ -530,6 +569,92 @@ DenseMatrix pearson_correlation_matrix(const DenseMatrix& w_true, const DenseMat
     } catch (const std::domain_error& e) {
         throw DataError(e.what());
     }
+}
+
+// ------------------------------------------------------------------------- matrix files
+namespace {
+std::vector<std::uint64_t> u64s(const std::vector<index_t>& v) { return {v.begin(), v.end()}; }
+}  // namespace
+
+void write_pdn1(const std::string& path, const DenseMatrix& m) {
+    throw_status(oocnmf_pdn1_write_dense(path.c_str(), m.data(), m.rows(), m.cols(), 0));
+}
+void write_pdn1_f32(const std::string& path, const DenseMatrix& m) {
+    throw_status(oocnmf_pdn1_write_dense(path.c_str(), m.data(), m.rows(), m.cols(), 1));
+}
+void write_pdn1(const std::string& path, const CsrMatrix& m) {
+    const auto rp = u64s(m.row_ptr()), ci = u64s(m.col_idx());
+    throw_status(oocnmf_pdn1_write_csr(path.c_str(), m.rows(), m.cols(), rp.data(), ci.data(), m.values().data(), 0));
+}
+void write_pdn1_f32(const std::string& path, const CsrMatrix& m) {
+    const auto rp = u64s(m.row_ptr()), ci = u64s(m.col_idx());
+    throw_status(oocnmf_pdn1_write_csr(path.c_str(), m.rows(), m.cols(), rp.data(), ci.data(), m.values().data(), 1));
+}
+
+Pdn1File::Pdn1File(const std::string& path) : path_(path) {
+    std::int32_t kind = 0, dtype = 0;
+    std::uint64_t r = 0, c = 0, z = 0;
+    throw_status(oocnmf_pdn1_info(path.c_str(), &kind, &dtype, &r, &c, &z));
+    kind_ = kind, dtype_ = dtype, rows_ = r, cols_ = c, nnz_ = z;
+}
+
+DenseMatrix Pdn1File::read_dense_window(IndexRange r, IndexRange c) const {
+    DenseMatrix out(r.extent(), c.extent());
+    throw_status(oocnmf_pdn1_read_dense(path_.c_str(), r.begin, r.end, c.begin, c.end, out.data()));
+    return out;
+}
+
+CsrMatrix Pdn1File::read_csr_rows(IndexRange r) const {
+    std::uint64_t nnz = 0;
+    throw_status(oocnmf_pdn1_csr_rows_nnz(path_.c_str(), r.begin, r.end, &nnz));
+    std::vector<std::uint64_t> rp(r.extent() + 1), ci(nnz);
+    std::vector<double> v(nnz);
+    throw_status(oocnmf_pdn1_read_csr_rows(path_.c_str(), r.begin, r.end, rp.data(), ci.data(), v.data()));
+    return CsrMatrix(r.extent(), cols_, std::vector<index_t>(rp.begin(), rp.end()),
+                     std::vector<index_t>(ci.begin(), ci.end()), std::move(v));
+}
+
+index_t Pdn1File::window_bytes(IndexRange r, IndexRange c) const {
+    const index_t vb = dtype_ == 1 ? 4 : 8;
+    if (kind_ == 0) return r.extent() * c.extent() * vb;
+    std::uint64_t nnz = 0;
+    throw_status(oocnmf_pdn1_csr_rows_nnz(path_.c_str(), r.begin, r.end, &nnz));
+    return (r.extent() + 1) * 8 + nnz * (8 + vb);
+}
+
+AnyMatrix read_pdn1(const std::string& path) {
+    Pdn1File f(path);
+    if (f.is_dense()) return AnyMatrix{f.read_dense_window({0, f.rows()}, {0, f.cols()})};
+    return AnyMatrix{f.read_csr_rows({0, f.rows()})};
+}
+
+void write_mtx(const std::string& path, const DenseMatrix& m) {
+    throw_status(oocnmf_mtx_write_dense(path.c_str(), m.data(), m.rows(), m.cols()));
+}
+void write_mtx(const std::string& path, const CsrMatrix& m) {
+    const auto rp = u64s(m.row_ptr()), ci = u64s(m.col_idx());
+    throw_status(oocnmf_mtx_write_csr(path.c_str(), m.rows(), m.cols(), rp.data(), ci.data(), m.values().data()));
+}
+
+AnyMatrix read_mtx(const std::string& path) {
+    std::int32_t kind = 0;
+    std::uint64_t r = 0, c = 0, z = 0;
+    throw_status(oocnmf_mtx_info(path.c_str(), &kind, &r, &c, &z));
+    if (kind == 0) {
+        DenseMatrix d(r, c);
+        throw_status(oocnmf_mtx_read(path.c_str(), d.data(), nullptr, nullptr, nullptr));
+        return AnyMatrix{std::move(d)};
+    }
+    std::vector<std::uint64_t> rp(r + 1), ci(z);
+    std::vector<double> v(z);
+    throw_status(oocnmf_mtx_read(path.c_str(), nullptr, rp.data(), ci.data(), v.data()));
+    return AnyMatrix{CsrMatrix(r, c, std::vector<index_t>(rp.begin(), rp.end()),
+                               std::vector<index_t>(ci.begin(), ci.end()), std::move(v))};
+}
+
+AnyMatrix read_matrix(const std::string& path) {
+    if (path.size() >= 4 && path.compare(path.size() - 4, 4, ".mtx") == 0) return read_mtx(path);
+    return read_pdn1(path);
 }
 
 }  // namespace oocnmf

@@ -15,6 +15,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 from dataclasses import dataclass, field
 from typing import List, Optional, Tuple
 
@@ -488,18 +489,60 @@ class DistComm:
         self.ctx.close()
 
 
+class _Window:
+    """This rank's window of a file-backed A, placed so nmf_distributed's slicing selects it."""
+
+    def __init__(self, part, plan, rank):
+        self.part, self.plan, self.rank = part, plan, rank
+
+
+def _file_window(path, plan: PartitionPlan, rank: int):
+    """Read only this rank's slab of a PDN1 file (Pdn1File windows, like the reference's
+    ChunkStore over a file); Matrix Market files are parsed whole. Returns an object that the
+    RNMF / CNMF branches below slice exactly as they slice an in-memory A."""
+    from .io import Pdn1File, read_mtx
+
+    (r0, r1), (c0, c1) = plan.slabs[rank]
+    if str(path).endswith(".mtx"):
+        full = read_mtx(path)
+        shape = full.shape
+    else:
+        f = Pdn1File(path)
+        shape = (f.rows, f.cols)
+        if f.is_dense():
+            full = None
+            win = f.read_dense_window(r0, r1, c0, c1, np.float32)
+        else:
+            full = None
+            win = f.read_csr_rows(r0, r1)
+            if plan.strategy == Strategy.cnmf:
+                win = win.col_window(c0, c1)
+    if shape != (plan.m, plan.n):
+        raise ShapeError(f"nmf_distributed: file A is {shape[0]}x{shape[1]}, plan is {plan.m}x{plan.n}")
+    if full is not None:
+        if isinstance(full, CsrMatrix):
+            win = full.row_window(r0, r1) if plan.strategy == Strategy.rnmf else full.col_window(c0, c1)
+        else:
+            win = np.ascontiguousarray(full[r0:r1, c0:c1], np.float32)
+    return _Window(win, plan, rank)
+
+
 def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host_slab: Optional[np.ndarray] = None,
                     batch_rows: int = 0) -> NmfResult:
-    """Row-partitioned MU (src/nmf_distributed.cpp:151-289) — collective over ``comm``.
+    """Row- (RNMF) or column-partitioned (CNMF) MU (src/nmf_distributed.cpp:112-289) —
+    collective over ``comm``.
 
-    ``a`` is the full A (ndarray / CsrMatrix; only this rank's rows are uploaded), or None
-    with ``host_slab`` (this rank's rows, float32) for the out-of-core mode.
+    ``a`` is the full A (ndarray / CsrMatrix; only this rank's window is uploaded), a path to a
+    PDN1 / Matrix Market file (ASource::file: this rank reads only its window of a PDN1 file),
+    or None with ``host_slab`` (this rank's rows, float32) for the out-of-core mode.
     """
     cfg.validate()
     if cfg.k != plan.k:
         raise ShapeError(f"nmf_distributed: cfg.k={cfg.k} disagrees with plan.k={plan.k}")
     if comm.size != plan.n_workers:
         raise ShapeError(f"nmf_distributed: group size {comm.size} != plan workers {plan.n_workers}")
+    if isinstance(a, (str, os.PathLike)):
+        a = _file_window(a, plan, comm.rank)
     ctx = comm.ctx
     if plan.strategy == Strategy.cnmf:
         # column partition (src/nmf_distributed.cpp:112-149): W replicated, H column slabs
@@ -507,7 +550,9 @@ def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host
             raise ShapeError("nmf_distributed: out-of-core streaming is row-partitioned (RNMF) only")
         _, (c0, c1) = plan.slabs[comm.rank]
         ctx.set_problem_cols(plan.m, plan.n, plan.k, c0, c1 - c0)
-        if isinstance(a, CsrMatrix):
+        if isinstance(a, _Window):
+            ctx.load_csr(a.part) if isinstance(a.part, CsrMatrix) else ctx.load_dense(a.part)
+        elif isinstance(a, CsrMatrix):
             ctx.load_csr(a.col_window(c0, c1))
         else:
             ctx.load_dense(np.ascontiguousarray(np.asarray(a)[:, c0:c1]))
@@ -521,6 +566,8 @@ def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host
     ctx.set_problem(plan.m, plan.n, plan.k, r0, r1 - r0)
     if host_slab is not None:
         ctx.attach_host(host_slab, batch_rows)
+    elif isinstance(a, _Window):
+        ctx.load_csr(a.part) if isinstance(a.part, CsrMatrix) else ctx.load_dense(a.part)
     elif isinstance(a, CsrMatrix):
         ctx.load_csr(a.row_window(r0, r1))
     else:

@@ -403,3 +403,36 @@ def test_column_partition_on_one_gpu_equals_serial(gpu, csr):
     np.testing.assert_allclose([e for _, e in res.error_trace], [e for _, e in ser.error_trace], rtol=1e-6)
     assert rel_fro(res.w, ser.w) < 1e-5 and rel_fro(res.h, ser.h) < 1e-5
     assert res.h.shape == (k, n)
+
+
+@pytest.mark.parametrize("fmt", ["pdn1", "pdn1_f32", "mtx", "csr_pdn1"])
+@pytest.mark.parametrize("strategy", ["rnmf", "cnmf"])
+def test_file_source_equals_in_memory(gpu, tmp_path, fmt, strategy):
+    # ASource::file: the rank reads only its window of the PDN1 file (f32 files straight into
+    # the upload buffer); results equal the in-memory solve on the same (f32-rounded) values
+    m, n, k = 260, 300, 8
+    d = f32(port.uniform_dense(m, n, 9, 99))
+    if fmt == "csr_pdn1":
+        d[d < 0.6] = 0.0
+        a = nmf.CsrMatrix.from_dense(d)
+        nmf.write_pdn1(tmp_path / "a.pdn1", a)
+        path = tmp_path / "a.pdn1"
+    elif fmt == "mtx":
+        a = d
+        nmf.write_mtx(tmp_path / "a.mtx", d)
+        path = tmp_path / "a.mtx"
+    else:
+        a = d
+        nmf.write_pdn1(tmp_path / "a.pdn1", d, dtype="f32" if fmt == "pdn1_f32" else "f64")
+        path = tmp_path / "a.pdn1"
+    st = nmf.Strategy.cnmf if strategy == "cnmf" else nmf.Strategy.rnmf
+    cfg = nmf.NmfConfig(k=k, max_iters=20, error_check_interval=10, eta=0.0, seed=4, device=gpu)
+    plan = nmf.make_plan(m, n, k, 1, 1, st)
+    comm = nmf.DistComm(0, 1, gpu)
+    try:
+        from_file = nmf.nmf_distributed(str(path), cfg, plan, comm)
+        in_mem = nmf.nmf_distributed(a, cfg, plan, comm)
+    finally:
+        comm.close()
+    assert from_file.error_trace == in_mem.error_trace
+    assert np.array_equal(from_file.w, in_mem.w) and np.array_equal(from_file.h, in_mem.h)
