@@ -30,8 +30,12 @@ cudaError_t launch_wta(int kp, const float* A, int64_t lda, const float* W, floa
 bool tc_supported(int kp);
 cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np,
                           const float* Ht_cat, float* slots, const StreamK& sk, cudaStream_t s);
+// out_final (optional): the pass reduces its stream-K partials itself (ascending CTA order)
+// and writes the np x kp result there; flags: 4 u32 per slot, zero before the launch (the
+// kernel leaves them zero again), epoch: the nonzero "published" value.
 cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np,
-                          const float* W_cat, float* slots, const StreamK& sk, cudaStream_t s);
+                          const float* W_cat, float* slots, const StreamK& sk, cudaStream_t s,
+                          float* out_final = nullptr, unsigned* flags = nullptr, unsigned epoch = 0);
 
 // ---- factor kernels (kernels_factor.cu) ----
 // F (rows x kp, rows a multiple of 128) <- F * N / (F G + eps) rowwise, where N is either

@@ -239,7 +239,8 @@ struct ChainClock {
 template <int KP, int PASS>
 __global__ void __launch_bounds__(512, 1)
     k_pass_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-              float* __restrict__ slots, StreamK sk, int drain_units) {
+              float* __restrict__ slots, StreamK sk, int drain_units, float* __restrict__ out_final,
+              unsigned* __restrict__ flags, unsigned epoch) {
     using C = TcCfg<KP, PASS>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte aligned, derived from the __shared__ array so loads compile to LDS, not LD
@@ -485,12 +486,49 @@ __global__ void __launch_bounds__(512, 1)
                 if (++lb == C::NLO) lb = 0, lph ^= 1u;
             }
             if (tile_end || u + 1 == u1) {
-                float* out = slots + sk.slot(cta, tile) * int64_t(128 * KP) + int64_t(t) * KP;
+                // In-kernel stream-K fix-up (out_final set): the CTA holding a tile's FIRST unit
+                // finishes that tile last (it reaches it at the end of its range, while the CTAs
+                // holding the later units started their ranges with it), so it adds the peers'
+                // published partials in ascending CTA order — the order k_streamk_reduce uses —
+                // and writes the reduced rows; peers publish their slot and a per-warp flag.
+                const bool owner = out_final && tile * sk.ipt >= u0;
+                if (owner) {
+                    const int64_t c_last = sk.cta_of((tile + 1) * sk.ipt - 1);
+                    for (int64_t c = cta + 1; c <= c_last; ++c) {
+                        const int64_t sl = sk.slot(c, tile);
+                        const unsigned* fl = flags + sl * 4 + (warp & 3);
+                        unsigned v;
+                        do {
+                            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(fl) : "memory");
+                        } while (v != epoch);
+                        const float4* src = reinterpret_cast<const float4*>(slots + sl * int64_t(128 * KP) +
+                                                                            int64_t(t) * KP);
+#pragma unroll
+                        for (int j4 = 0; j4 < KP / 4; ++j4) {
+                            const float4 p = src[j4];
+                            acc[4 * j4] += p.x, acc[4 * j4 + 1] += p.y, acc[4 * j4 + 2] += p.z, acc[4 * j4 + 3] += p.w;
+                        }
+                        // consumed: re-arm the flag for the next launch (graph replays reuse the
+                        // same epoch value)
+                        __syncwarp();
+                        if (lane == 0) *const_cast<unsigned*>(fl) = 0u;
+                    }
+                }
+                float* out = owner ? out_final + (tile * 128 + t) * int64_t(KP)
+                                   : slots + sk.slot(cta, tile) * int64_t(128 * KP) + int64_t(t) * KP;
 #pragma unroll
                 for (int j4 = 0; j4 < KP / 4; ++j4) {
                     reinterpret_cast<float4*>(out)[j4] =
                         make_float4(acc[4 * j4], acc[4 * j4 + 1], acc[4 * j4 + 2], acc[4 * j4 + 3]);
                     acc[4 * j4] = acc[4 * j4 + 1] = acc[4 * j4 + 2] = acc[4 * j4 + 3] = 0.f;
+                }
+                if (out_final && !owner) {
+                    __threadfence();
+                    __syncwarp();
+                    if (lane == 0) {
+                        unsigned* fl = flags + sk.slot(cta, tile) * 4 + (warp & 3);
+                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(fl), "r"(epoch) : "memory");
+                    }
                 }
                 ++tile;
             }
@@ -556,12 +594,13 @@ int tc_drain_units() {
 }
 
 template <int KP, int PASS>
-cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, float* slots, const StreamK& sk, cudaStream_t s) {
+cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, float* slots, const StreamK& sk, cudaStream_t s,
+                      float* out_final = nullptr, unsigned* flags = nullptr, unsigned epoch = 0) {
     using C = TcCfg<KP, PASS>;
     auto kern = k_pass_tc<KP, PASS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
-    kern<<<unsigned(sk.G), 512, C::SMEM, s>>>(a, b, slots, sk, tc_drain_units());
+    kern<<<unsigned(sk.G), 512, C::SMEM, s>>>(a, b, slots, sk, tc_drain_units(), out_final, flags, epoch);
     return cudaGetLastError();
 }
 
@@ -593,14 +632,15 @@ cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
 
 // Pass 2 on the tensor cores: A MN-major (4 column atoms per 128-column tile), W_cat (mp x 2kp).
 cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* W_cat,
-                          float* slots, const StreamK& sk, cudaStream_t s) {
+                          float* slots, const StreamK& sk, cudaStream_t s, float* out_final,
+                          unsigned* flags, unsigned epoch) {
     CUtensorMap ma, mb;
     cudaError_t e;
     if ((e = make_map(&ma, A, mp, np, lda, kTcStep, 4, true)) != cudaSuccess) return e;
     if ((e = make_map(&mb, W_cat, mp, 2 * kp, 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
-    return kp == 16   ? launch_tc<16, 2>(ma, mb, slots, sk, s)
-           : kp == 32 ? launch_tc<32, 2>(ma, mb, slots, sk, s)
-                      : launch_tc<64, 2>(ma, mb, slots, sk, s);
+    return kp == 16   ? launch_tc<16, 2>(ma, mb, slots, sk, s, out_final, flags, epoch)
+           : kp == 32 ? launch_tc<32, 2>(ma, mb, slots, sk, s, out_final, flags, epoch)
+                      : launch_tc<64, 2>(ma, mb, slots, sk, s, out_final, flags, epoch);
 }
 
 }  // namespace ooc

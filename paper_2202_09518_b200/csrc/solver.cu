@@ -137,6 +137,7 @@ struct oocnmf_ctx {
     DevBuf W, Ht, HHt, packed, N1, slots1, slots2, gram_w, gram_h, err_slots, red_slots, scal, flag;
     DevBuf HHt64, WtW64;         // f64 Grams for the trace-form error (f32 copies drive the updates)
     DevBuf W_cat, Ht_cat;        // [F | F - tf32(F)] (rows x 2kp): tensor-core operands only
+    DevBuf fix_flags;            // in-kernel stream-K fix-up of pass 2 (tensor-core path)
     bool use_tc = false;         // kp in {32, 64}: tcgen05 passes; else CUDA-core FFMA passes
     StreamK sk1, sk2;            // in-core dense passes
     StreamK sk1b[2], sk2b[2];    // out-of-core: full batch / last batch
@@ -216,6 +217,8 @@ void plan_dense(oocnmf_ctx* c) {
     plan_wta(c->sk2, c->mp, c->np, c->num_sms, step);
     c->slots1.alloc(size_t(c->sk1.G * c->sk1.smax) * kTile * c->kp * 4, "slots1");
     c->slots2.alloc(size_t(c->sk2.G * c->sk2.smax) * kTile * c->kp * 4, "slots2");
+    c->fix_flags.alloc(size_t(c->sk2.G * c->sk2.smax) * 4 * 4, "fix flags");
+    ck(cudaMemsetAsync(c->fix_flags.p, 0, c->fix_flags.bytes, c->stream), "memset");
     if (c->cnmf) {
         c->N1.alloc(size_t(c->mp) * c->kp * 4, "AHt");
         ck(cudaMemsetAsync(c->N1.p, 0, c->N1.bytes, c->stream), "memset");
@@ -279,8 +282,10 @@ cudaError_t pass1(oocnmf_ctx* c, const float* A, int64_t rows_p, float* slots, c
 }
 // Pass 2 over an A slab with its W rows (W rows x kp, Wcat rows x 2kp): slots <- A^T·W partials.
 cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W, const float* Wcat, float* slots,
-                  const StreamK& sk, cudaStream_t s) {
-    if (c->use_tc) return launch_wta_tc(c->kp, A, c->np, rows_p, c->np, Wcat, slots, sk, s);
+                  const StreamK& sk, cudaStream_t s, float* out_final = nullptr) {
+    if (c->use_tc)
+        return launch_wta_tc(c->kp, A, c->np, rows_p, c->np, Wcat, slots, sk, s, out_final,
+                             out_final ? c->fix_flags.as<unsigned>() : nullptr, 1u);
     return launch_wta(c->kp, A, c->np, W, slots, sk, s);
 }
 
@@ -353,10 +358,18 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         }
         count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
-        count(c, pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s),
-              "wta");
-        rec(eWta);
-        count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce WtA");
+        if (c->use_tc) {
+            // the tensor-core pass reduces its own stream-K partials into W^T A
+            count(c, pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s,
+                           c->wta()),
+                  "wta");
+            rec(eWta);
+        } else {
+            count(c, pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s),
+                  "wta");
+            rec(eWta);
+            count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce WtA");
+        }
         rec(eReduced);
     } else if (c->kind == Kind::csr) {
         count(c, launch_spmm(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows,

@@ -436,3 +436,14 @@ def test_file_source_equals_in_memory(gpu, tmp_path, fmt, strategy):
         comm.close()
     assert from_file.error_trace == in_mem.error_trace
     assert np.array_equal(from_file.w, in_mem.w) and np.array_equal(from_file.h, in_mem.h)
+
+
+def test_tall_skinny_stream_k_fixup(gpu):
+    # 8192 x 256: pass 2 has only 2 column tiles, each split over ~74 CTAs — the in-kernel
+    # stream-K fix-up (owner CTA sums 73 published partials in CTA order) must match the oracle
+    m, n, k = 8192, 256, 16
+    a = f32(port.uniform_dense(m, n, 13, 99))
+    w0, h0 = port.init_factors(m, n, k, 2)
+    ref = port.nmf_serial(a, k, f32(w0), f32(h0), max_iters=20, interval=5)
+    res = solve_from(a.astype(np.float32), k, 20, 5, seed=2)
+    check_parity(res, ref.trace_iters, ref.trace_err, ref.w, ref.h)
