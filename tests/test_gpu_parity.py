@@ -447,3 +447,18 @@ def test_tall_skinny_stream_k_fixup(gpu):
     ref = port.nmf_serial(a, k, f32(w0), f32(h0), max_iters=20, interval=5)
     res = solve_from(a.astype(np.float32), k, 20, 5, seed=2)
     check_parity(res, ref.trace_iters, ref.trace_err, ref.w, ref.h)
+
+
+def test_column_partition_refuses_unsupported_sources(gpu):
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem_cols(64, 100, 4, 10, 50)
+        with pytest.raises(nmf.ShapeError, match="row windows"):
+            ctx.generate_dense_uniform(1, 2)
+        with pytest.raises(nmf.ShapeError, match="row-partitioned"):
+            ctx.attach_host(np.ones((64, 50), np.float32))
+        ctx.load_dense(np.ones((64, 50), np.float32))
+        with pytest.raises(nmf.ShapeError, match="row-window"):
+            ctx.perturb(0.1, 3)
+    with pytest.raises(nmf.ShapeError, match="column slab out of bounds"):
+        with nmf.Context(gpu) as ctx:
+            ctx.set_problem_cols(64, 100, 4, 60, 50)
