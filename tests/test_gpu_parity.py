@@ -281,6 +281,11 @@ def test_error_behaviour(gpu):
     bad[3, 4] = np.nan
     with pytest.raises(nmf.DataError):
         nmf.nmf_serial(bad, nmf.NmfConfig(k=2, max_iters=3, error_check_interval=1))
+    # the checks are evaluated on the device and read back at the end (eta = 0) or per check
+    # (eta > 0): either way the first bad check's iteration is reported, like the reference
+    for eta in (0.0, 1e-9):
+        with pytest.raises(nmf.DataError, match="non-finite factor entries at iteration 3$"):
+            nmf.nmf_serial(bad, nmf.NmfConfig(k=2, max_iters=7, error_check_interval=3, eta=eta))
     with nmf.Context(gpu) as ctx:
         with pytest.raises(nmf.ShapeError):
             ctx.set_problem(10, 10, 2, row0=5, rows=6)
