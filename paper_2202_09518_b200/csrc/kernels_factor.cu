@@ -7,6 +7,8 @@
 //   gram_t           symmetric k x k, mirrored triangle     (:127-179)
 // With H stored transposed (Ht, n x kp) both factors are row-major "tall" matrices, so one
 // kernel updates W rows (G = HH^T, N = A·H^T) and Ht rows (G = W^T W, N = (W^T A)^T).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace ooc {
@@ -284,7 +286,12 @@ int factor_grid(int64_t tiles) {
         if (cudaGetDevice(&d) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
         return n;
     }();
-    const int64_t cap = int64_t(sms) * kFuCtasPerSm;
+    static int64_t per_sm = [] {  // OOCNMF_FU_CTAS_PER_SM: developer knob (tools/fu_bench.cu)
+        const char* e = std::getenv("OOCNMF_FU_CTAS_PER_SM");
+        const int v = e ? std::atoi(e) : 0;
+        return int64_t(v > 0 ? v : kFuCtasPerSm);
+    }();
+    const int64_t cap = int64_t(sms) * per_sm;
     return int(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
 }
 
