@@ -163,6 +163,13 @@ struct oocnmf_ctx {
     DevBuf A0, v0, vT0;
     bool pristine = false, local = false;
     bool collective() const { return nranks > 1 && !local; }
+    // RNMF on CSR: W^T A is n x k (537 MB at config 3), so instead of all-reducing it and
+    // repeating the n-row H update on every rank, the ranks reduce-scatter it, update their
+    // own n/N rows of H, and all-gather H (the same bytes as the all-reduce, 1/N of the update).
+    // Needs whole 128-row tiles per rank (n a multiple of 128 N, as at config 3); else all-reduce.
+    bool shard_h() const { return collective() && !cnmf && kind == Kind::csr && np % (int64_t(kTile) * nranks) == 0; }
+    int64_t h_rows() const { return shard_h() ? np / nranks : np; }
+    int64_t h_row0() const { return shard_h() ? h_rows() * rank : 0; }
 
     float* wta() const { return packed.as<float>(); }
     float* wtw() const { return packed.as<float>() + np * kp; }
@@ -292,12 +299,12 @@ cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W,
 // HH^T from the per-CTA Gram slots of the last H pass; under CNMF each rank holds a column
 // slab of H, so the f32 and f64 Grams are summed over the ranks (the reference's HH^T
 // all-reduce, src/nmf_distributed.cpp:115).
-void finish_hht(oocnmf_ctx* c) {
+void finish_hht(oocnmf_ctx* c, int64_t rows, bool partial) {
     const int kp = c->kp;
-    count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(c->np / kTile), int64_t(kp) * kp,
+    count(c, launch_reduce_slots(c->gram_h.as<double>(), factor_grid(rows / kTile), int64_t(kp) * kp,
                                  c->HHt.as<float>(), c->HHt64.as<double>(), c->stream),
           "reduce HHt");
-    if (c->cnmf && c->collective()) {
+    if (partial) {
         nck(ncclGroupStart(), "ncclGroupStart");
         nck(ncclAllReduce(c->HHt.p, c->HHt.p, size_t(kp) * kp, ncclFloat, ncclSum, c->comm, c->stream),
             "allreduce HHt");
@@ -313,7 +320,7 @@ void gram_h(oocnmf_ctx* c) {
     count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, nullptr, nullptr, nullptr, nullptr, 0.f, false,
                                   c->gram_h.as<double>(), nullptr, c->flag.as<int>(), htlo(c), c->stream),
           "gram H");
-    finish_hht(c);
+    finish_hht(c, c->np, c->cnmf && c->collective());  // a CNMF rank holds a column slab of H
 }
 
 // CNMF: A·H^T of this rank's column slab (in N1) summed over the ranks before the
@@ -431,7 +438,19 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
 void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     const int kp = c->kp;
     cudaStream_t s = c->stream;
-    if (c->collective() && !c->cnmf) {
+    const int64_t hr = c->h_rows(), h0 = c->h_row0();
+    if (c->shard_h()) {
+        // reduce-scatter W^T A (each rank keeps its n/N rows, in place) + the small Grams
+        const size_t slice = size_t(hr) * kp;
+        float* wta = c->wta();
+        nck(ncclGroupStart(), "ncclGroupStart");
+        nck(ncclReduceScatter(wta, wta + size_t(c->rank) * slice, slice, ncclFloat, ncclSum, c->comm, s),
+            "reduce-scatter WtA");
+        nck(ncclAllReduce(c->wtw(), c->wtw(), size_t(kp) * kp, ncclFloat, ncclSum, c->comm, s), "allreduce WtW");
+        nck(ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
+            "allreduce WtW64");
+        nck(ncclGroupEnd(), "ncclGroupEnd");
+    } else if (c->collective() && !c->cnmf) {
         // One fused NCCL launch: the packed f32 [W^T A | W^T W] the update consumes and the f64
         // W^T W the trace-form error consumes. (CNMF: W^T A of the column slab and W^T W of the
         // replicated W are already complete on every rank.)
@@ -443,10 +462,15 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         nck(ncclGroupEnd(), "ncclGroupEnd");
     }
     if (timed) record(c, ev[eComm], s);
-    count(c, launch_factor_update(kp, c->Ht.as<float>(), c->np, c->wta(), nullptr, nullptr, c->wtw(), eps, true,
-                                  c->gram_h.as<double>(), c->err_slots.as<double>(), c->flag.as<int>(), htlo(c), s),
+    float* hcat = htlo(c);
+    count(c, launch_factor_update(kp, c->Ht.as<float>() + h0 * kp, hr, c->wta() + h0 * kp, nullptr, nullptr,
+                                  c->wtw(), eps, true, c->gram_h.as<double>(), c->err_slots.as<double>(),
+                                  c->flag.as<int>(), hcat ? hcat + h0 * 2 * kp : nullptr, s),
           "H update");
-    finish_hht(c);
+    if (c->shard_h())
+        nck(ncclAllGather(c->Ht.as<float>() + h0 * kp, c->Ht.p, size_t(hr) * kp, ncclFloat, c->comm, s),
+            "all-gather H");
+    finish_hht(c, hr, c->collective() && (c->cnmf || c->shard_h()));
     if (timed) record(c, ev[eHdone], s);
 }
 
@@ -471,9 +495,9 @@ void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
     const bool direct = error_mode != 2 && c->kind != Kind::host;
     const double threshold = error_mode == 1 ? INFINITY : kAutoDirectBelow;
     const double* eslots = c->err_slots.as<double>();
-    int64_t n_err = factor_grid(c->np / kTile);
-    if (c->cnmf && c->collective()) {
-        // CNMF: <W^T A, H> is a sum over the column slabs
+    int64_t n_err = factor_grid(c->h_rows() / kTile);
+    if (c->collective() && (c->cnmf || c->shard_h())) {
+        // CNMF / sharded H: <W^T A, H> is a sum over the ranks' slabs
         count(c, launch_reduce_f64(eslots, n_err, scal + kCross, s), "reduce cross");
         nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s), "allreduce cross");
         eslots = scal + kCross;

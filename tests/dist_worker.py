@@ -50,6 +50,9 @@ def main(out_path):
     run("dense_k32", a, 1100, 900, 32, 30, 10)
     rp, ci, v, (m, n) = port.gen_sparse(1500, 1200, 0.02, 3)
     run("csr_k16", nmf.CsrMatrix(m, n, rp, ci, f32(v)), m, n, 16, 20, 10)
+    # n = 2048: whole 128-row H tiles per rank up to N = 16 -> the sharded H update path
+    rp3, ci3, v3, (m3, n3) = port.gen_sparse(1100, 2048, 0.02, 8)
+    run("csr_shard_k16", nmf.CsrMatrix(m3, n3, rp3, ci3, f32(v3)), m3, n3, 16, 20, 10)
     run("ooc_k32", None, 1100, 900, 32, 20, 10, host_slab=a, batch_rows=128)
     # column partition (CNMF) on wide inputs: W replicated, H column slabs
     wide = port.uniform_dense(700, 1300, 7, 99).astype(np.float32)

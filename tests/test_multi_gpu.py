@@ -119,3 +119,13 @@ def test_csr_cnmf_matches_reference(dist_results):
     ref = oracle.ref.nmf_distributed((rp, ci, f32(v), shape), 16, world, 1, strategy=1, w0=f32(w0), h0=f32(h0),
                                      max_iters=20, interval=10)
     _check(res["cnmf_csr_k16"], ref)
+
+
+def test_csr_sharded_h_update_matches_oracle(dist_results):
+    # RNMF on CSR with n a multiple of 128 N: reduce-scatter W^T A, each rank updates its n/N
+    # rows of H, all-gather H (instead of all-reduce + replicated update)
+    world, res = dist_results
+    rp, ci, v, shape = oracle.port.gen_sparse(1100, 2048, 0.02, 8)
+    w0, h0 = oracle.port.init_factors(1100, 2048, 16, 0)
+    ref = oracle.port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
+    _check(res["csr_shard_k16"], ref)
