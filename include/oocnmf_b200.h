@@ -238,6 +238,25 @@ int oocnmf_cluster_silhouette(const double* runs, uint64_t nruns, uint64_t m, ui
 int oocnmf_pearson_correlation(const double* w_true, uint64_t m, uint64_t k1, const double* w_est,
                                uint64_t k2, double* corr);
 
+/* ----- memory_estimate (include/oocnmf/partition.hpp:51-64, src/partition.cpp:147-197) -----
+ * Per-rank device bytes of THIS backend's layout (f32, padded to 128, tensor-core [F | F_lo]
+ * copies, stream-K slots) for the largest slab of a plan, and the row-batch count the
+ * out-of-core mode needs to fit budget_bytes. min_n_b = 1: the in-core path fits; > 1:
+ * out-of-core with that many row batches (dense RNMF); 0: infeasible. Host-side. */
+typedef struct {
+    uint64_t a_slab_bytes;       /* A slab resident in HBM (CSR: values + indices, both CSR(A) and CSR(A^T)) */
+    uint64_t store_peak_bytes;   /* out-of-core: the two row-batch staging buffers at min_n_b */
+    uint64_t factor_bytes;       /* W, H and their tensor-core [F | F_lo] copies */
+    uint64_t intermediate_bytes; /* packed W^T A, stream-K slots, Gram / error slots, A·H^T (CSR / CNMF) */
+    uint64_t peak_bytes;         /* (a_slab or store_peak) + factors + intermediates */
+    uint64_t min_n_b;
+    int32_t feasible;
+    int32_t in_core;
+} oocnmf_memory_report;
+/* strategy: 1 = CNMF, 2 = RNMF; density 1 = dense; num_sms 0 = 148 */
+int oocnmf_memory_estimate(uint64_t m, uint64_t n, uint64_t k, int n_workers, int strategy, double density,
+                           uint64_t budget_bytes, int num_sms, oocnmf_memory_report* out);
+
 /* ----- matrix files (include/oocnmf/io.hpp:28-66, src/io.cpp), host-side -----
  * PDN1: "PDNMF\0v1", u8 kind (0 dense, 1 CSR), u8 dtype, u64 rows, u64 cols, little-endian;
  * dense payload row-major; CSR payload u64 nnz, u64 row_ptr[rows+1], u64 col_idx[nnz], values.

@@ -207,6 +207,21 @@ struct PartitionPlan {
 };
 PartitionPlan make_plan(index_t m, index_t n, index_t k, int n_workers, index_t n_b, Strategy strategy);
 
+/// Per-rank device bytes of the B200 layout (f32, padded, tensor-core operand copies, stream-K
+/// slots) for the plan's largest slab; min_n_b: 1 = in-core fits, > 1 = out-of-core row batches
+/// (dense RNMF), 0 = infeasible (reference: partition.hpp:51-64).
+struct MemoryReport {
+    index_t a_slab_bytes = 0;
+    index_t store_peak_bytes = 0;
+    index_t factor_bytes = 0;
+    index_t intermediate_bytes = 0;
+    index_t peak_bytes = 0;
+    index_t min_n_b = 0;
+    bool feasible = false;
+    bool in_core = false;
+};
+MemoryReport memory_estimate(const PartitionPlan& plan, double density, index_t budget_bytes, index_t n_cb = 1);
+
 // ---- distributed (reference: include/oocnmf/nmf_distributed.hpp, comm.hpp) ----
 /// One rank of an NCCL group (one process or host thread per GPU). Created collectively:
 /// rank 0 calls new_unique_id(), ships it to the others, every rank constructs a handle.

@@ -31,6 +31,7 @@ from .nmf import (  # noqa: F401
     device_count,
     init_factors,
     make_plan,
+    memory_estimate,
     nmf_distributed,
     nmf_serial,
     pearson_correlation_matrix,

@@ -48,6 +48,12 @@ class KRecord(C.Structure):
 
 pi64 = C.POINTER(C.c_int64)
 
+
+class MemoryReport(C.Structure):
+    _fields_ = [("a_slab_bytes", u64), ("store_peak_bytes", u64), ("factor_bytes", u64),
+                ("intermediate_bytes", u64), ("peak_bytes", u64), ("min_n_b", u64), ("feasible", i32),
+                ("in_core", i32)]
+
 _SIGS = {
     "oocnmf_last_error": ([], C.c_char_p),
     "oocnmf_abi_version": ([], C.c_int),
@@ -81,6 +87,7 @@ _SIGS = {
     "oocnmf_sq_norm": ([vp, pd], C.c_int),
     "oocnmf_problem_dims": ([vp, pu, pu, pu, pu, pu], C.c_int),
     "oocnmf_set_problem_cols": ([vp, u64, u64, u64, u64, u64], C.c_int),
+    "oocnmf_memory_estimate": ([u64, u64, u64, C.c_int, C.c_int, dbl, u64, C.c_int, C.POINTER(MemoryReport)], C.c_int),
     "oocnmf_gather_h_f64": ([vp, pd], C.c_int),
     "oocnmf_set_rank": ([vp, u64], C.c_int),
     "oocnmf_perturb": ([vp, dbl, u64], C.c_int),

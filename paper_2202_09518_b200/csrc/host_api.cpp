@@ -271,6 +271,18 @@ PartitionPlan make_plan(index_t m, index_t n, index_t k, int n_workers, index_t 
     return p;
 }
 
+MemoryReport memory_estimate(const PartitionPlan& plan, double density, index_t budget_bytes, index_t n_cb) {
+    if (n_cb < 1) throw ShapeError("memory_estimate: n_cb must be >= 1");
+    oocnmf_memory_report r{};
+    throw_status(oocnmf_memory_estimate(plan.m, plan.n, plan.k, plan.n_workers, plan.strategy == Strategy::cnmf ? 1 : 2,
+                                        density, budget_bytes, 0, &r));
+    MemoryReport out;
+    out.a_slab_bytes = r.a_slab_bytes, out.store_peak_bytes = r.store_peak_bytes, out.factor_bytes = r.factor_bytes;
+    out.intermediate_bytes = r.intermediate_bytes, out.peak_bytes = r.peak_bytes, out.min_n_b = r.min_n_b;
+    out.feasible = r.feasible != 0, out.in_core = r.in_core != 0;
+    return out;
+}
+
 // ------------------------------------------------------------------------- distributed
 CommHandle::UniqueId CommHandle::new_unique_id() {
     UniqueId id{};

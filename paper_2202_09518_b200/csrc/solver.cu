@@ -1405,6 +1405,65 @@ int oocnmf_gather_h_f64(oocnmf_ctx* c, double* h_full) {
     });
 }
 
+int oocnmf_memory_estimate(uint64_t m, uint64_t n, uint64_t k, int n_workers, int strategy, double density,
+                           uint64_t budget_bytes, int num_sms, oocnmf_memory_report* out) {
+    return guarded([&] {
+        if (m < 1 || n < 1 || k < 1) fail(OOCNMF_ERR_SHAPE, "memory_estimate: dimensions must be >= 1");
+        if (n_workers < 1) fail(OOCNMF_ERR_SHAPE, "memory_estimate: need at least one worker");
+        if (!(density > 0.0) || density > 1.0) fail(OOCNMF_ERR_SHAPE, "memory_estimate: density must be in (0, 1]");
+        if (budget_bytes == 0) fail(OOCNMF_ERR_SHAPE, "memory_estimate: budget must be > 0");
+        const bool cnmf = strategy == 1;
+        const int sms = num_sms > 0 ? num_sms : 148;
+        const uint64_t N = uint64_t(n_workers);
+        const int64_t rows = int64_t(cnmf ? m : (m + N - 1) / N), cols = int64_t(cnmf ? (n + N - 1) / N : n);
+        int kp = pad_k(k);
+        kp = std::max(kp, 16);  // the tensor-core layout
+        const int64_t mp = round_up(rows, kTile), np = round_up(cols, kTile);
+        const bool dense = density >= 1.0;
+        // resident A
+        uint64_t a_bytes;
+        if (dense) {
+            a_bytes = uint64_t(mp) * np * 4;
+        } else {
+            const double nnz = std::ceil(density * double(rows) * double(cols));
+            a_bytes = uint64_t(nnz) * 8 * 2 + uint64_t(rows + 1) * 8 + uint64_t(cols + 1) * 8;
+        }
+        const uint64_t factors = uint64_t(mp + np) * kp * 4 * 3;  // W, Ht and [F | F_lo] copies
+        auto inter_for = [&](int64_t mrows) {
+            StreamK s1, s2;
+            plan_aht(s1, mrows, np, sms, kTcStep);
+            plan_wta(s2, mrows, np, sms, kTcStep);
+            uint64_t b = uint64_t(np * kp + kp * kp) * 4;                                   // packed
+            b += uint64_t(s1.G * s1.smax + s2.G * s2.smax) * kTile * kp * 4;              // slots
+            b += uint64_t(factor_grid(mp / kTile) + factor_grid(np / kTile)) * kp * kp * 8; // Gram slots
+            if (!dense || cnmf) b += uint64_t(mp) * kp * 4;                               // A·H^T
+            return b + (1u << 20);                                                         // scalars, flags
+        };
+        oocnmf_memory_report r{};
+        r.a_slab_bytes = a_bytes;
+        r.factor_bytes = factors;
+        r.intermediate_bytes = inter_for(mp);
+        r.peak_bytes = a_bytes + factors + r.intermediate_bytes;
+        if (r.peak_bytes <= budget_bytes) {
+            r.min_n_b = 1, r.feasible = 1, r.in_core = 1;
+        } else if (dense && !cnmf) {
+            // out-of-core row batches: two staging buffers of br rows
+            const uint64_t fixed = factors + r.intermediate_bytes;
+            if (fixed > budget_bytes)
+                fail(OOCNMF_ERR_SHAPE, "memory_estimate: factor arrays alone (" + std::to_string(fixed) +
+                                           " B) exceed the budget of " + std::to_string(budget_bytes) + " B");
+            const int64_t br = int64_t((budget_bytes - fixed) / (2 * uint64_t(np) * 4)) / kTile * kTile;
+            if (br >= kTile) {
+                r.min_n_b = uint64_t((rows + br - 1) / br);
+                r.store_peak_bytes = 2 * uint64_t(br) * np * 4;
+                r.peak_bytes = r.store_peak_bytes + fixed;
+                r.feasible = 1;
+            }
+        }
+        *out = r;
+    });
+}
+
 int oocnmf_set_rank(oocnmf_ctx* c, uint64_t k) {
     return guarded([&] {
         set_dev(c);

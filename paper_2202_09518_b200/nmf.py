@@ -457,6 +457,33 @@ def make_plan(m, n, k, n_workers, n_b, strategy: Strategy) -> PartitionPlan:
                          [(int(b[i]), int(b[i + 1])) for i in range(n_b)])
 
 
+@dataclass
+class MemoryReport:
+    """Per-rank device bytes of the B200 layout (reference MemoryReport, partition.hpp:51-61)."""
+    a_slab_bytes: int
+    store_peak_bytes: int
+    factor_bytes: int
+    intermediate_bytes: int
+    peak_bytes: int
+    min_n_b: int  # 1: in-core fits; > 1: out-of-core row batches; 0: infeasible
+    feasible: bool
+    in_core: bool
+
+
+def memory_estimate(plan: "PartitionPlan", density: float, budget_bytes: int, n_cb: int = 1,
+                    num_sms: int = 0) -> MemoryReport:
+    """memory_estimate (src/partition.cpp:147-197) for this backend's device layout."""
+    if n_cb < 1:
+        raise ShapeError("memory_estimate: n_cb must be >= 1")
+    r = _capi.MemoryReport()
+    check(_capi.lib().oocnmf_memory_estimate(plan.m, plan.n, plan.k, plan.n_workers,
+                                             1 if plan.strategy == Strategy.cnmf else 2, float(density),
+                                             int(budget_bytes), num_sms, C.byref(r)))
+    return MemoryReport(int(r.a_slab_bytes), int(r.store_peak_bytes), int(r.factor_bytes),
+                        int(r.intermediate_bytes), int(r.peak_bytes), int(r.min_n_b), bool(r.feasible),
+                        bool(r.in_core))
+
+
 def exchange_unique_id(rank: int, make_id, device: Optional[int] = None, group=None) -> bytes:
     """Broadcast rank 0's 128-byte NCCL unique id to every rank with torch.distributed
     (gloo or nccl process group; plumbing only)."""

@@ -144,3 +144,26 @@ def test_streamk_split_tiles_each_unit_once(tiles, ipt, G):
     # balance: every CTA streams the same number of A bytes to within one step
     sizes = [sk.begin(c + 1) - sk.begin(c) for c in range(sk.G)]
     assert max(sizes) - min(sizes) <= 1
+
+
+def test_memory_estimate_layout_and_batches():
+    # config 2 on one 180 GB B200: in core; on an 8 GB budget: out-of-core row batches
+    p = nmf.make_plan(65536, 65536, 32, 1, 1, nmf.Strategy.rnmf)
+    big = nmf.memory_estimate(p, 1.0, 180 << 30)
+    assert big.in_core and big.min_n_b == 1 and big.a_slab_bytes == 65536 * 65536 * 4
+    small = nmf.memory_estimate(p, 1.0, 8 << 30)
+    assert small.feasible and not small.in_core and small.min_n_b > 1 and small.peak_bytes <= 8 << 30
+    tighter = nmf.memory_estimate(p, 1.0, 4 << 30)
+    assert tighter.min_n_b >= small.min_n_b                      # fewer bytes -> more batches
+    # per-rank slabs shrink with the worker count
+    p8 = nmf.make_plan(65536, 65536, 32, 8, 1, nmf.Strategy.rnmf)
+    assert nmf.memory_estimate(p8, 1.0, 180 << 30).a_slab_bytes == 8192 * 65536 * 4
+    # CSR: 8 B per stored entry in CSR(A) and CSR(A^T), plus both row pointers
+    ps = nmf.make_plan(1 << 16, 1 << 16, 16, 1, 1, nmf.Strategy.rnmf)
+    rep = nmf.memory_estimate(ps, 1e-3, 180 << 30)
+    nnz = int(np.ceil(1e-3 * (1 << 16) * (1 << 16)))
+    assert rep.a_slab_bytes == nnz * 16 + 2 * ((1 << 16) + 1) * 8
+    with pytest.raises(nmf.ShapeError, match="exceed the budget"):
+        nmf.memory_estimate(p, 1.0, 1 << 20)
+    with pytest.raises(nmf.ShapeError, match="density"):
+        nmf.memory_estimate(p, 0.0, 1 << 30)

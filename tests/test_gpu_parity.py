@@ -467,3 +467,24 @@ def test_column_partition_refuses_unsupported_sources(gpu):
     with pytest.raises(nmf.ShapeError, match="column slab out of bounds"):
         with nmf.Context(gpu) as ctx:
             ctx.set_problem_cols(64, 100, 4, 60, 50)
+
+
+def test_memory_estimate_matches_the_device_allocation(gpu):
+    # the estimate describes what a context actually allocates for an in-core dense solve
+    import torch
+
+    m, n, k = 8192, 6144, 32
+    plan = nmf.make_plan(m, n, k, 1, 1, nmf.Strategy.rnmf)
+    est = nmf.memory_estimate(plan, 1.0, 180 << 30)
+    with nmf.Context(gpu) as warm:  # device context and library state first
+        warm.set_problem(256, 256, k)
+        warm.generate_dense_uniform(1, 2)
+        warm.solve(nmf.NmfConfig(k=k, max_iters=2, error_check_interval=1, eta=0.0))
+    torch.cuda.synchronize(gpu)
+    free0 = torch.cuda.mem_get_info(gpu)[0]
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.generate_dense_uniform(1, 2)
+        ctx.solve(nmf.NmfConfig(k=k, max_iters=2, error_check_interval=1, eta=0.0))
+        used = free0 - torch.cuda.mem_get_info(gpu)[0]
+    assert abs(used - est.peak_bytes) <= 0.05 * est.peak_bytes + (64 << 20), (used, est)
