@@ -488,3 +488,17 @@ def test_memory_estimate_matches_the_device_allocation(gpu):
         ctx.solve(nmf.NmfConfig(k=k, max_iters=2, error_check_interval=1, eta=0.0))
         used = free0 - torch.cuda.mem_get_info(gpu)[0]
     assert abs(used - est.peak_bytes) <= 0.05 * est.peak_bytes + (64 << 20), (used, est)
+
+
+@pytest.mark.parametrize("k", [8, 32])
+def test_ffma_cross_check_path_matches_tensor_core_path(gpu, monkeypatch, k):
+    # the CUDA-core FFMA passes stay selectable as an independent implementation of the same
+    # contractions; both must track the oracle and each other
+    a = port.uniform_dense(700, 520, 21, 99).astype(np.float32)
+    w0, h0 = port.init_factors(700, 520, k, 0)
+    ref = port.nmf_serial(f32(a), k, f32(w0), f32(h0), max_iters=30, interval=10)
+    tc = solve_from(a, k, 30, 10)
+    monkeypatch.setenv("OOCNMF_FORCE_FFMA", "1")
+    ff = solve_from(a, k, 30, 10)
+    check_parity(ff, ref.trace_iters, ref.trace_err, ref.w, ref.h)
+    np.testing.assert_allclose([e for _, e in ff.error_trace], [e for _, e in tc.error_trace], rtol=2e-5)
