@@ -10,6 +10,8 @@
 //   generator  reference semantics of gen_sparse_random (src/synth.cpp:60-86) on device.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace ooc {
@@ -57,6 +59,45 @@ __global__ void __launch_bounds__(256) k_spmm(const int64_t* __restrict__ rp,
             else
                 reinterpret_cast<float2*>(out + row * KP)[l] = make_float2(acc[0], acc[1]);
         }
+    }
+}
+
+// Vectorised variant: each lane owns 4 consecutive outputs (one float4 of the factor row), so
+// a warp covers 128 / kp rows at once (kp = 32: 8 lanes per row, 4 rows per warp) — four times
+// the independent gathers in flight per warp and a quarter of the load instructions of the
+// one-float-per-lane kernel.
+template <int KP>
+__global__ void __launch_bounds__(256) k_spmm_v4(const int64_t* __restrict__ rp,
+                                                 const int32_t* __restrict__ ci,
+                                                 const float* __restrict__ v, int64_t rows,
+                                                 const float* __restrict__ B, float* __restrict__ out) {
+    constexpr int LPR = KP / 4;    // lanes per row
+    constexpr int RPW = 32 / LPR;  // rows per warp
+    const int lane = threadIdx.x & 31, sub = lane / LPR, l = lane % LPR;
+    const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t wg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wg * RPW < rows; wg += warps) {
+        const int64_t row = wg * RPW + sub;
+        const bool live = row < rows;
+        const int64_t beg = live ? rp[row] : 0, end = live ? rp[row + 1] : 0;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t p0 = beg; __any_sync(0xffffffffu, p0 < end); p0 += LPR) {
+            const int64_t p = p0 + l;
+            const int col = p < end ? ci[p] : 0;
+            const float val = p < end ? v[p] : 0.f;
+#pragma unroll
+            for (int t = 0; t < LPR; ++t) {
+                const int c = __shfl_sync(0xffffffffu, col, sub * LPR + t);
+                const float w = __shfl_sync(0xffffffffu, val, sub * LPR + t);
+                if (p0 + t < end) {
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(B + int64_t(c) * KP) + l);
+                    acc.x = fmaf(w, b.x, acc.x);
+                    acc.y = fmaf(w, b.y, acc.y);
+                    acc.z = fmaf(w, b.z, acc.z);
+                    acc.w = fmaf(w, b.w, acc.w);
+                }
+            }
+        }
+        if (live) reinterpret_cast<float4*>(out + row * KP)[l] = acc;
     }
 }
 
@@ -199,6 +240,22 @@ unsigned grid_for(int64_t work) {
 
 cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
                         const float* B, float* out, cudaStream_t s) {
+    static const int mode = [] {  // OOCNMF_SPMM=1: the one-float-per-lane kernel (developer knob)
+        const char* e = std::getenv("OOCNMF_SPMM");
+        return e ? std::atoi(e) : 4;
+    }();
+    if (mode == 4 && kp >= 8) {
+        const int64_t warps = (rows * (kp / 4) + 31) / 32;
+        const unsigned grid = grid_for(warps * 32);
+        switch (kp) {
+            case 8: k_spmm_v4<8><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+            case 16: k_spmm_v4<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+            case 32: k_spmm_v4<32><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+            case 64: k_spmm_v4<64><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    }
     const int64_t warps = (rows * (kp < 32 ? kp : 32) + 31) / 32;
     const unsigned grid = grid_for(warps * 32);
     switch (kp) {
