@@ -39,8 +39,9 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--workload", choices=["dense", "sparse", "ooc", "select"], default="dense")
-    p.add_argument("--m", type=int, default=None)
-    p.add_argument("--n", type=int, default=None)
+    # (--rows / --cols aliases: torchrun's own parser swallows an abbreviated --m)
+    p.add_argument("--m", "--rows", dest="m", type=int, default=None)
+    p.add_argument("--n", "--cols", dest="n", type=int, default=None)
     p.add_argument("--k", type=int, default=None)
     p.add_argument("--density", type=float, default=1e-5)
     p.add_argument("--ooc-gb", type=float, default=64.0, help="host A slab per rank (GB) for --workload ooc")

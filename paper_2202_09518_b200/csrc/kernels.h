@@ -73,6 +73,10 @@ cudaError_t launch_gen_dense_uniform(float* A, int64_t lda, int64_t rows, int64_
 cudaError_t launch_init_factors(float* W, float* Ht, int kp, int64_t k, int64_t rows,
                                 int64_t row0, int64_t n, int64_t n_global, int64_t col0, uint64_t seed,
                                 cudaStream_t s);
+// out(r, c) = in(r, c) over an R x C block with element strides (is_*, os_*), casting the type.
+enum class CastKind { f32_f64, f64_f32, i32_u64 };
+cudaError_t launch_strided_cast(CastKind kind, const void* in, int64_t is_r, int64_t is_c, void* out, int64_t os_r,
+                                int64_t os_c, int64_t R, int64_t C, cudaStream_t s);
 cudaError_t launch_cast_pad_f64(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
                                 float* dst, int64_t ld_dst, cudaStream_t s);
 // Partial f64 sums of squares of A (dense, padded) -> out_slots[sqnorm_grid()].
@@ -116,5 +120,12 @@ cudaError_t launch_gen_csr_fill(int64_t rows, int64_t row0, int64_t n, uint64_t 
                                 uint64_t seed, const int64_t* rp, int32_t* ci, float* v,
                                 cudaStream_t s);
 cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaStream_t s);
+// CSR upload: narrow a chunk of reference-format entries (u64 column, f64 value) to the device
+// layout, flagging columns >= n; then check the row structure of the whole upload.
+constexpr unsigned kCsrBadRowPtr = 1u, kCsrBadColumn = 2u, kCsrBadOrder = 4u;
+cudaError_t launch_csr_ingest(const uint64_t* ci_in, const double* v_in, int64_t count, uint64_t n,
+                              int32_t* ci, float* v, unsigned* bad, cudaStream_t s);
+cudaError_t launch_csr_check_rows(const int64_t* rp, const int32_t* ci, int64_t rows, int64_t nnz,
+                                  unsigned* bad, cudaStream_t s);
 
 }  // namespace ooc

@@ -53,6 +53,20 @@ __global__ void k_cast_pad_f64(const double* __restrict__ src, int64_t ld_src, i
     }
 }
 
+// Layout conversion for the copy-in / copy-out calls of the C-ABI: out(r, c) = in(r, c) for an
+// R x C block with arbitrary element strides, converting the element type; the loop runs along
+// the output's unit-stride axis so the writes coalesce.
+template <class Tin, class Tout>
+__global__ void k_strided_cast(const Tin* __restrict__ in, int64_t is_r, int64_t is_c, Tout* __restrict__ out,
+                               int64_t os_r, int64_t os_c, int64_t R, int64_t C, bool rows_fast) {
+    const int64_t total = R * C;
+    for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total;
+         q += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = rows_fast ? q % R : q / C, c = rows_fast ? q / R : q % C;
+        out[r * os_r + c * os_c] = Tout(in[r * is_r + c * is_c]);
+    }
+}
+
 __device__ double block_sum(double v) {
     __shared__ double sh[256];
     sh[threadIdx.x] = v;
@@ -210,6 +224,28 @@ cudaError_t launch_init_factors(float* W, float* Ht, int kp, int64_t k, int64_t 
 cudaError_t launch_cast_pad_f64(const double* src, int64_t ld_src, int64_t rows, int64_t cols,
                                 float* dst, int64_t ld_dst, cudaStream_t s) {
     k_cast_pad_f64<<<grid_for(rows * cols, 4), 256, 0, s>>>(src, ld_src, rows, cols, dst, ld_dst);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_strided_cast(CastKind kind, const void* in, int64_t is_r, int64_t is_c, void* out, int64_t os_r,
+                                int64_t os_c, int64_t R, int64_t C, cudaStream_t s) {
+    if (R <= 0 || C <= 0) return cudaSuccess;
+    const bool rows_fast = os_r == 1 && os_c != 1;
+    const int g = grid_for(R * C, 4);
+    switch (kind) {
+        case CastKind::f32_f64:
+            k_strided_cast<<<g, 256, 0, s>>>(static_cast<const float*>(in), is_r, is_c, static_cast<double*>(out),
+                                             os_r, os_c, R, C, rows_fast);
+            break;
+        case CastKind::f64_f32:
+            k_strided_cast<<<g, 256, 0, s>>>(static_cast<const double*>(in), is_r, is_c, static_cast<float*>(out),
+                                             os_r, os_c, R, C, rows_fast);
+            break;
+        case CastKind::i32_u64:
+            k_strided_cast<<<g, 256, 0, s>>>(static_cast<const int32_t*>(in), is_r, is_c,
+                                             static_cast<unsigned long long*>(out), os_r, os_c, R, C, rows_fast);
+            break;
+    }
     return cudaGetLastError();
 }
 

@@ -10,6 +10,7 @@
 //   generator  reference semantics of gen_sparse_random (src/synth.cpp:60-86) on device.
 #include <cub/cub.cuh>
 
+#include <algorithm>
 #include <cstdlib>
 
 #include "kernels.h"
@@ -352,6 +353,73 @@ cudaError_t launch_gen_csr_fill(int64_t rows, int64_t row0, int64_t n, uint64_t 
     const unsigned grid = unsigned(rows < 148 * 16 ? rows : 148 * 16);
     k_gen_csr_fill<<<grid, 256, 0, s>>>(rows, row0, n, thresh, rng_key(seed, kStreamSparseMask),
                                         rng_key(seed, kStreamSparseVal), rp, ci, v);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------- ingest
+// Upload path of oocnmf_load_csr_f64: the reference's CsrMatrix arrays (u64 columns, f64
+// values; include/oocnmf/matrix.hpp) arrive in chunks and are narrowed to the device layout
+// (i32 columns, f32 values) here, with the reference constructor's checks
+// (src/matrix.cpp CsrMatrix validation) done on device instead of on one host core.
+namespace {
+
+__global__ void k_csr_ingest(const uint64_t* __restrict__ ci_in, const double* __restrict__ v_in,
+                             int64_t count, uint64_t n, int32_t* __restrict__ ci, float* __restrict__ v,
+                             unsigned* __restrict__ bad) {
+    bool out_of_range = false;
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < count;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t c = ci_in[i];
+        out_of_range |= c >= n;
+        ci[i] = int32_t(c);
+        v[i] = float(v_in[i]);
+    }
+    if (__any_sync(0xffffffffu, out_of_range) && (threadIdx.x & 31) == 0) atomicOr(bad, kCsrBadColumn);
+}
+
+// One thread per row. A row pointer outside [0, nnz] or below its predecessor is reported as
+// "not nondecreasing" (a nondecreasing row_ptr from 0 to nnz stays inside), so the column walk
+// never leaves the arrays.
+__global__ void k_csr_check_rows(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                 int64_t rows, int64_t nnz, unsigned* __restrict__ bad) {
+    unsigned flags = 0;
+    for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < rows;
+         r += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t b = rp[r], e = rp[r + 1];
+        if (b < 0 || e < b || e > nnz) {
+            flags |= kCsrBadRowPtr;
+            continue;
+        }
+        for (int64_t p = b + 1; p < e; ++p)
+            if (ci[p] <= ci[p - 1]) {
+                flags |= kCsrBadOrder;
+                break;
+            }
+    }
+    flags = __reduce_or_sync(0xffffffffu, flags);
+    if (flags && (threadIdx.x & 31) == 0) atomicOr(bad, flags);
+}
+
+int ingest_grid(int64_t work) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return int(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, int64_t(sms) * 8)));
+}
+
+}  // namespace
+
+cudaError_t launch_csr_ingest(const uint64_t* ci_in, const double* v_in, int64_t count, uint64_t n,
+                              int32_t* ci, float* v, unsigned* bad, cudaStream_t s) {
+    if (count <= 0) return cudaSuccess;
+    k_csr_ingest<<<ingest_grid(count), 256, 0, s>>>(ci_in, v_in, count, n, ci, v, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csr_check_rows(const int64_t* rp, const int32_t* ci, int64_t rows, int64_t nnz,
+                                  unsigned* bad, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    k_csr_check_rows<<<ingest_grid(rows), 256, 0, s>>>(rp, ci, rows, nnz, bad);
     return cudaGetLastError();
 }
 

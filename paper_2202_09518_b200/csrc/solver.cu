@@ -17,9 +17,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "kernels.h"
@@ -144,6 +146,10 @@ struct oocnmf_ctx {
     bool norm_valid = false, factors_set = false, factors_valid = false;
     double norm_a2 = 0.0;
     double* hpin = nullptr;      // pinned readback: [err, flag]
+    // copy-in / copy-out staging of the C-ABI's pageable-array calls (see Stage), lazily made
+    void* stage_pin = nullptr;
+    DevBuf stage_dev;
+    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     std::vector<cudaEvent_t> evs;
     uint64_t launches = 0;
     // CUDA graph of one block of iterations (the launches between two error checks),
@@ -279,8 +285,10 @@ reduced:
     c->norm_valid = true;
 }
 
-float* wlo(oocnmf_ctx* c) { return c->use_tc ? c->W_cat.as<float>() : nullptr; }
-float* htlo(oocnmf_ctx* c) { return c->use_tc ? c->Ht_cat.as<float>() : nullptr; }
+// [F | F_lo] operand copies: only the dense tensor-core passes read them (the CSR SpMMs read
+// W / Ht), so CSR solves skip writing them (2 GB per iteration at config 3)
+float* wlo(oocnmf_ctx* c) { return c->use_tc && c->kind != Kind::csr ? c->W_cat.as<float>() : nullptr; }
+float* htlo(oocnmf_ctx* c) { return c->use_tc && c->kind != Kind::csr ? c->Ht_cat.as<float>() : nullptr; }
 
 // Pass 1 over an A slab (rows_p x np, rows_p a multiple of 128): slots <- A·Ht partials.
 cudaError_t pass1(oocnmf_ctx* c, const float* A, int64_t rows_p, float* slots, const StreamK& sk, cudaStream_t s) {
@@ -859,6 +867,190 @@ void load_dense_common(oocnmf_ctx* c) {
     plan_dense(c);
 }
 
+// ----------------------------------------------------------------- pageable copy-in / copy-out
+// The reference API hands arrays over in pageable host memory (f64 values, u64 indices,
+// reference layouts). The calls that take or return them stream through two pinned slots:
+// host threads pack the caller's array into one slot while the other slot's DMA and the
+// on-device layout work (narrowing, padding, transposition) run, so the host copy, the PCIe
+// transfer and the conversion overlap and no layout loop runs on one host core.
+//
+// A transfer moves `count` elements of one or more parts; part p's element e is elem bytes
+// at host + e * stride. A chunk of len elements occupies the slot as the parts back to back
+// (part p at len * sum of the earlier parts' elem).
+struct Part {
+    const void* host;  // copy-in source / copy-out destination (cast away const for the latter)
+    size_t elem, stride;
+};
+
+constexpr size_t kStageSlot = size_t(64) << 20;
+
+size_t stage_slot_bytes(oocnmf_ctx* c, size_t unit) {
+    const size_t want = std::max(kStageSlot, unit);
+    if (!c->stage_pin || c->stage_dev.bytes < 2 * want) {
+        if (c->stage_pin) cudaFreeHost(c->stage_pin), c->stage_pin = nullptr;
+        ck(cudaMallocHost(&c->stage_pin, 2 * want), "cudaMallocHost (staging)");
+        c->stage_dev.alloc(2 * want, "staging");
+        for (auto& e : c->stage_ev)
+            if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    }
+    return c->stage_dev.bytes / 2;
+}
+
+// OOCNMF_PROFILE_IO=1: per-phase wall times of the copy-in calls on stderr
+bool io_profile() {
+    static const bool on = [] {
+        const char* e = std::getenv("OOCNMF_PROFILE_IO");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+double io_clock() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+int host_threads() { return int(std::clamp<unsigned>(std::thread::hardware_concurrency(), 1u, 8u)); }
+
+// Pack (in = true: host parts -> slot) or unpack (slot -> host parts) elements [off, off + len).
+void pack_chunk(const std::vector<Part>& parts, char* slot, int64_t off, int64_t len, bool in) {
+    struct Job {
+        char* slot;
+        char* host;
+        size_t elem, stride;
+    };
+    std::vector<Job> jobs;
+    size_t at = 0;
+    for (const Part& p : parts) {
+        jobs.push_back({slot + at, const_cast<char*>(static_cast<const char*>(p.host)) + off * p.stride, p.elem,
+                        p.stride});
+        at += size_t(len) * p.elem;
+    }
+    const int nt = host_threads();
+    auto work = [&](int t) {
+        for (const Job& j : jobs) {
+            if (j.stride == j.elem) {  // contiguous: split the bytes
+                const size_t bytes = size_t(len) * j.elem, per = (bytes + nt - 1) / nt;
+                const size_t b = std::min(bytes, t * per), e = std::min(bytes, b + per);
+                if (in)
+                    std::memcpy(j.slot + b, j.host + b, e - b);
+                else
+                    std::memcpy(j.host + b, j.slot + b, e - b);
+            } else {  // strided: split the elements
+                const int64_t per = (len + nt - 1) / nt, b = std::min(len, t * per), e = std::min(len, b + per);
+                for (int64_t q = b; q < e; ++q) {
+                    if (in)
+                        std::memcpy(j.slot + q * j.elem, j.host + q * j.stride, j.elem);
+                    else
+                        std::memcpy(j.host + q * j.stride, j.slot + q * j.elem, j.elem);
+                }
+            }
+        }
+    };
+    const size_t total = size_t(len) * (at / std::max<int64_t>(len, 1));
+    if (nt == 1 || total < (size_t(1) << 20)) {
+        for (int t = 0; t < nt; ++t) work(t);
+        return;
+    }
+    std::vector<std::thread> pool;
+    for (int t = 1; t < nt; ++t) pool.emplace_back(work, t);
+    work(0);
+    for (auto& t : pool) t.join();
+}
+
+// Copy-in: consume(dev_slot, off, len) enqueues on c->stream the device work that reads the
+// staged chunk (parts back to back in dev_slot).
+template <class Consume>
+void copy_in(oocnmf_ctx* c, const std::vector<Part>& parts, int64_t count, Consume&& consume) {
+    if (count <= 0) return;
+    size_t unit = 0;
+    for (const Part& p : parts) unit += p.elem;
+    const size_t slot = stage_slot_bytes(c, unit);
+    const int64_t chunk = std::max<int64_t>(1, int64_t(slot / unit));
+    double t_wait = 0, t_pack = 0;
+    const double t0 = io_clock();
+    for (int64_t off = 0, i = 0; off < count; off += chunk, ++i) {
+        const int si = int(i & 1);
+        const int64_t len = std::min(chunk, count - off);
+        char* hs = static_cast<char*>(c->stage_pin) + si * slot;
+        char* ds = c->stage_dev.as<char>() + si * slot;
+        const double ta = io_clock();
+        if (i >= 2) ck(cudaEventSynchronize(c->stage_ev[si]), "sync");
+        const double tb = io_clock();
+        pack_chunk(parts, hs, off, len, true);
+        t_wait += tb - ta, t_pack += io_clock() - tb;
+        ck(cudaMemcpyAsync(ds, hs, size_t(len) * unit, cudaMemcpyHostToDevice, c->stream), "H2D");
+        consume(ds, off, len);
+        ck(cudaEventRecord(c->stage_ev[si], c->stream), "event");
+    }
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    if (io_profile())
+        std::fprintf(stderr, "[oocnmf io] copy_in %.1f MB: %.1f ms (host pack %.1f ms, slot waits %.1f ms, %d threads)\n",
+                     double(count) * unit / 1e6, (io_clock() - t0) * 1e3, t_pack * 1e3, t_wait * 1e3, host_threads());
+}
+
+// Copy-out: produce(dev_slot, off, len) enqueues on c->stream the device work that writes the
+// chunk (parts back to back) into dev_slot.
+template <class Produce>
+void copy_out(oocnmf_ctx* c, const std::vector<Part>& parts, int64_t count, Produce&& produce) {
+    if (count <= 0) return;
+    size_t unit = 0;
+    for (const Part& p : parts) unit += p.elem;
+    const size_t slot = stage_slot_bytes(c, unit);
+    const int64_t chunk = std::max<int64_t>(1, int64_t(slot / unit));
+    const int64_t nchunks = (count + chunk - 1) / chunk;
+    auto issue = [&](int64_t i) {
+        const int si = int(i & 1);
+        const int64_t off = i * chunk, len = std::min(chunk, count - off);
+        char* ds = c->stage_dev.as<char>() + si * slot;
+        produce(ds, off, len);
+        ck(cudaMemcpyAsync(static_cast<char*>(c->stage_pin) + si * slot, ds, size_t(len) * unit,
+                           cudaMemcpyDeviceToHost, c->stream),
+           "D2H");
+        ck(cudaEventRecord(c->stage_ev[si], c->stream), "event");
+    };
+    issue(0);
+    for (int64_t i = 0; i < nchunks; ++i) {
+        if (i + 1 < nchunks) issue(i + 1);  // its slot was unpacked in the previous round
+        const int si = int(i & 1);
+        ck(cudaEventSynchronize(c->stage_ev[si]), "sync");
+        const int64_t off = i * chunk, len = std::min(chunk, count - off);
+        pack_chunk(parts, static_cast<char*>(c->stage_pin) + si * slot, off, len, false);
+    }
+}
+
+// Device layout of the factors: W rows x kp (row i at W + i kp), Ht n x kp. The reference's:
+// W m x k row-major, H k x n row-major (f64).
+void import_w(oocnmf_ctx* c, const double* w) {
+    ck(cudaMemsetAsync(c->W.p, 0, c->W.bytes, c->stream), "memset");
+    const int64_t k = int64_t(c->k), kp = c->kp;
+    copy_in(c, {Part{w, size_t(k) * 8, size_t(k) * 8}}, int64_t(c->rows), [&](char* ds, int64_t off, int64_t len) {
+        ck(launch_strided_cast(CastKind::f64_f32, ds, k, 1, c->W.as<float>() + off * kp, kp, 1, len, k, c->stream),
+           "import W");
+    });
+}
+void import_h(oocnmf_ctx* c, const double* h) {
+    ck(cudaMemsetAsync(c->Ht.p, 0, c->Ht.bytes, c->stream), "memset");
+    const int64_t n = int64_t(c->n), kp = c->kp;
+    // element = one row r of H (n values) -> column r of Ht
+    copy_in(c, {Part{h, size_t(n) * 8, size_t(n) * 8}}, int64_t(c->k), [&](char* ds, int64_t off, int64_t len) {
+        ck(launch_strided_cast(CastKind::f64_f32, ds, n, 1, c->Ht.as<float>() + off, 1, kp, len, n, c->stream),
+           "import H");
+    });
+}
+void export_w(oocnmf_ctx* c, const float* W, int64_t rows, double* w) {
+    const int64_t k = int64_t(c->k), kp = c->kp;
+    copy_out(c, {Part{w, size_t(k) * 8, size_t(k) * 8}}, rows, [&](char* ds, int64_t off, int64_t len) {
+        ck(launch_strided_cast(CastKind::f32_f64, W + off * kp, kp, 1, ds, k, 1, len, k, c->stream), "export W");
+    });
+}
+// H rows [0, k) of the local n columns into h (row stride ldh doubles)
+void export_h(oocnmf_ctx* c, double* h, int64_t ldh) {
+    const int64_t n = int64_t(c->n), kp = c->kp;
+    copy_out(c, {Part{h, size_t(n) * 8, size_t(ldh) * 8}}, int64_t(c->k), [&](char* ds, int64_t off, int64_t len) {
+        ck(launch_strided_cast(CastKind::f32_f64, c->Ht.as<float>() + off, 1, kp, ds, n, 1, len, n, c->stream),
+           "export H");
+    });
+}
+
 void csr_finish(oocnmf_ctx* c) {
     // CSR(A^T) once: A is iteration-invariant.
     c->rpT.alloc(size_t(c->n + 1) * 8, "rpT");
@@ -1019,6 +1211,9 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
             if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
         }
         if (c->hpin) cudaFreeHost(c->hpin);
+        if (c->stage_pin) cudaFreeHost(c->stage_pin);
+        for (auto e : c->stage_ev)
+            if (e) cudaEventDestroy(e);
         if (c->stream) cudaStreamDestroy(c->stream);
         if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
         delete c;
@@ -1045,20 +1240,13 @@ int oocnmf_load_dense_f64(oocnmf_ctx* c, const double* a, uint64_t lda) {
         need_problem(c);
         if (lda < c->n) fail(OOCNMF_ERR_SHAPE, "lda < n");
         load_dense_common(c);
-        // Stage f64 rows in bounded chunks, cast to f32 in HBM.
-        const int64_t chunk_rows = std::max<int64_t>(1, (int64_t(256) << 20) / int64_t(c->n * 8));
-        DevBuf tmp;
-        tmp.alloc(size_t(std::min<int64_t>(chunk_rows, c->rows)) * c->n * 8, "staging");
-        for (int64_t r0 = 0; r0 < int64_t(c->rows); r0 += chunk_rows) {
-            const int64_t br = std::min<int64_t>(chunk_rows, int64_t(c->rows) - r0);
-            ck(cudaMemcpy2DAsync(tmp.p, c->n * 8, a + r0 * lda, lda * 8, c->n * 8, br, cudaMemcpyHostToDevice,
-                                 c->stream),
-               "H2D");
-            ck(launch_cast_pad_f64(tmp.as<double>(), c->n, br, c->n, c->A.as<float>() + r0 * c->np, c->np,
-                                   c->stream),
-               "cast");
-            ck(cudaStreamSynchronize(c->stream), "sync");
-        }
+        // rows through the staging slots, narrowed and padded in HBM
+        copy_in(c, {Part{a, size_t(c->n) * 8, size_t(lda) * 8}}, int64_t(c->rows),
+                [&](char* ds, int64_t off, int64_t len) {
+                    ck(launch_cast_pad_f64(reinterpret_cast<const double*>(ds), c->n, len, c->n,
+                                           c->A.as<float>() + off * c->np, c->np, c->stream),
+                       "cast");
+                });
     });
 }
 
@@ -1068,9 +1256,22 @@ int oocnmf_load_dense_f32(oocnmf_ctx* c, const float* a, uint64_t lda) {
         need_problem(c);
         if (lda < c->n) fail(OOCNMF_ERR_SHAPE, "lda < n");
         load_dense_common(c);
-        ck(cudaMemcpy2DAsync(c->A.p, c->np * 4, a, lda * 4, c->n * 4, c->rows, cudaMemcpyHostToDevice, c->stream),
-           "H2D A");
-        ck(cudaStreamSynchronize(c->stream), "sync");
+        cudaPointerAttributes at{};
+        const bool pinned = cudaPointerGetAttributes(&at, a) == cudaSuccess && at.type == cudaMemoryTypeHost;
+        cudaGetLastError();
+        if (pinned) {  // page-locked (oocnmf_host_register / cudaMallocHost): one DMA
+            ck(cudaMemcpy2DAsync(c->A.p, c->np * 4, a, lda * 4, c->n * 4, c->rows, cudaMemcpyHostToDevice,
+                                 c->stream),
+               "H2D A");
+            ck(cudaStreamSynchronize(c->stream), "sync");
+            return;
+        }
+        copy_in(c, {Part{a, size_t(c->n) * 4, size_t(lda) * 4}}, int64_t(c->rows),
+                [&](char* ds, int64_t off, int64_t len) {
+                    ck(cudaMemcpy2DAsync(c->A.as<float>() + off * c->np, c->np * 4, ds, c->n * 4, c->n * 4, len,
+                                         cudaMemcpyDeviceToDevice, c->stream),
+                       "copy A");
+                });
     });
 }
 
@@ -1104,29 +1305,51 @@ int oocnmf_load_csr_f64(oocnmf_ctx* c, const uint64_t* row_ptr, const uint64_t* 
         set_dev(c);
         need_problem(c);
         if (row_ptr[0] != 0) fail(OOCNMF_ERR_SHAPE, "CsrMatrix: row_ptr[0] must be 0");
-        for (uint64_t i = 0; i < c->rows; ++i)
-            if (row_ptr[i + 1] < row_ptr[i]) fail(OOCNMF_ERR_SHAPE, "CsrMatrix: row_ptr must be nondecreasing");
+        const double t_start = io_clock();
         const int64_t nnz = int64_t(row_ptr[c->rows]);
-        for (uint64_t i = 0; i < c->rows; ++i)
-            for (uint64_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
-                if (col_idx[p] >= c->n) fail(OOCNMF_ERR_SHAPE, "CsrMatrix: column index out of range");
-                if (p > row_ptr[i] && col_idx[p] <= col_idx[p - 1])
-                    fail(OOCNMF_ERR_SHAPE, "CsrMatrix: column indices must strictly increase within a row");
-            }
+        if (nnz < 0 || uint64_t(nnz) > c->rows * c->n)
+            fail(OOCNMF_ERR_SHAPE, "CsrMatrix: row_ptr must be nondecreasing");
         reset_source(c);
-        std::vector<int64_t> rp(c->rows + 1);
-        std::vector<int32_t> ci(std::max<int64_t>(nnz, 1));
-        std::vector<float> v(std::max<int64_t>(nnz, 1));
-        for (uint64_t i = 0; i <= c->rows; ++i) rp[i] = int64_t(row_ptr[i]);
-        for (int64_t p = 0; p < nnz; ++p) ci[p] = int32_t(col_idx[p]), v[p] = float(vals[p]);
         c->nnz = nnz;
-        c->rp.alloc(rp.size() * 8, "rp");
-        c->ci.alloc(ci.size() * 4, "ci");
-        c->v.alloc(v.size() * 4, "v");
-        ck(cudaMemcpy(c->rp.p, rp.data(), rp.size() * 8, cudaMemcpyHostToDevice), "H2D");
-        ck(cudaMemcpy(c->ci.p, ci.data(), ci.size() * 4, cudaMemcpyHostToDevice), "H2D");
-        ck(cudaMemcpy(c->v.p, v.data(), v.size() * 4, cudaMemcpyHostToDevice), "H2D");
+        c->rp.alloc(size_t(c->rows + 1) * 8, "rp");
+        c->ci.alloc(size_t(std::max<int64_t>(nnz, 1)) * 4, "ci");
+        c->v.alloc(size_t(std::max<int64_t>(nnz, 1)) * 4, "v");
+        DevBuf bad;
+        bad.alloc(4, "flags");
+        ck(cudaMemsetAsync(bad.p, 0, 4, c->stream), "memset");
+        // row_ptr: u64 -> i64 is the same bits
+        copy_in(c, {Part{row_ptr, 8, 8}}, int64_t(c->rows + 1), [&](char* ds, int64_t off, int64_t len) {
+            ck(cudaMemcpyAsync(c->rp.as<int64_t>() + off, ds, size_t(len) * 8, cudaMemcpyDeviceToDevice, c->stream),
+               "copy rp");
+        });
+        // entries: narrowed to (i32, f32) with the column-range check on device
+        copy_in(c, {Part{col_idx, 8, 8}, Part{vals, 8, 8}}, nnz, [&](char* ds, int64_t off, int64_t len) {
+            ck(launch_csr_ingest(reinterpret_cast<const uint64_t*>(ds), reinterpret_cast<const double*>(ds + len * 8),
+                                 len, c->n, c->ci.as<int32_t>() + off, c->v.as<float>() + off, bad.as<unsigned>(),
+                                 c->stream),
+               "csr ingest");
+        });
+        const double t_entries = io_clock();
+        ck(launch_csr_check_rows(c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->rows, nnz, bad.as<unsigned>(),
+                                 c->stream),
+           "csr check");
+        unsigned flags = 0;
+        ck(cudaMemcpyAsync(&flags, bad.p, 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        // the reference constructor's messages, in its order of checks
+        const char* msg = flags & kCsrBadRowPtr   ? "CsrMatrix: row_ptr must be nondecreasing"
+                          : flags & kCsrBadColumn ? "CsrMatrix: column index out of range"
+                          : flags & kCsrBadOrder  ? "CsrMatrix: column indices must strictly increase within a row"
+                                                  : nullptr;
+        if (msg) {
+            reset_source(c);
+            fail(OOCNMF_ERR_SHAPE, msg);
+        }
+        const double t_check = io_clock();
         csr_finish(c);
+        if (io_profile())
+            std::fprintf(stderr, "[oocnmf io] load_csr: %.1f ms upload+ingest, %.1f ms check, %.1f ms transpose\n",
+                         (t_entries - t_start) * 1e3, (t_check - t_entries) * 1e3, (io_clock() - t_check) * 1e3);
     });
 }
 
@@ -1224,14 +1447,17 @@ int oocnmf_download_csr(oocnmf_ctx* c, uint64_t* row_ptr, uint64_t* col_idx, dou
     return guarded([&] {
         set_dev(c);
         if (c->kind != Kind::csr) fail(OOCNMF_ERR_SHAPE, "no CSR A resident in HBM");
-        std::vector<int64_t> rp(c->rows + 1);
-        std::vector<int32_t> ci(size_t(std::max<int64_t>(c->nnz, 1)));
-        std::vector<float> v(ci.size());
-        ck(cudaMemcpy(rp.data(), c->rp.p, rp.size() * 8, cudaMemcpyDeviceToHost), "D2H");
-        ck(cudaMemcpy(ci.data(), c->ci.p, ci.size() * 4, cudaMemcpyDeviceToHost), "D2H");
-        ck(cudaMemcpy(v.data(), c->v.p, v.size() * 4, cudaMemcpyDeviceToHost), "D2H");
-        for (size_t i = 0; i < rp.size(); ++i) row_ptr[i] = uint64_t(rp[i]);
-        for (int64_t p = 0; p < c->nnz; ++p) col_idx[p] = uint64_t(ci[p]), vals[p] = double(v[p]);
+        copy_out(c, {Part{row_ptr, 8, 8}}, int64_t(c->rows + 1), [&](char* ds, int64_t off, int64_t len) {
+            ck(cudaMemcpyAsync(ds, c->rp.as<int64_t>() + off, size_t(len) * 8, cudaMemcpyDeviceToDevice, c->stream),
+               "copy rp");
+        });
+        copy_out(c, {Part{col_idx, 8, 8}, Part{vals, 8, 8}}, c->nnz, [&](char* ds, int64_t off, int64_t len) {
+            ck(launch_strided_cast(CastKind::i32_u64, c->ci.as<int32_t>() + off, 1, 1, ds, 1, 1, len, 1, c->stream),
+               "widen ci");
+            ck(launch_strided_cast(CastKind::f32_f64, c->v.as<float>() + off, 1, 1, ds + len * 8, 1, 1, len, 1,
+                                   c->stream),
+               "widen v");
+        });
     });
 }
 
@@ -1239,14 +1465,8 @@ int oocnmf_set_factors_f64(oocnmf_ctx* c, const double* w, const double* h) {
     return guarded([&] {
         set_dev(c);
         need_problem(c);
-        const int kp = c->kp;
-        std::vector<float> hw(size_t(c->mp) * kp, 0.f), hh(size_t(c->np) * kp, 0.f);
-        for (uint64_t i = 0; i < c->rows; ++i)
-            for (uint64_t j = 0; j < c->k; ++j) hw[i * kp + j] = float(w[i * c->k + j]);
-        for (uint64_t r = 0; r < c->k; ++r)
-            for (uint64_t j = 0; j < c->n; ++j) hh[j * kp + r] = float(h[r * c->n + j]);
-        ck(cudaMemcpy(c->W.p, hw.data(), hw.size() * 4, cudaMemcpyHostToDevice), "H2D W");
-        ck(cudaMemcpy(c->Ht.p, hh.data(), hh.size() * 4, cudaMemcpyHostToDevice), "H2D H");
+        import_w(c, w);
+        import_h(c, h);
         c->factors_set = c->factors_valid = true;
     });
 }
@@ -1256,17 +1476,8 @@ int oocnmf_get_factors_f64(oocnmf_ctx* c, double* w, double* h) {
         set_dev(c);
         need_problem(c);
         if (!c->factors_valid) fail(OOCNMF_ERR_SHAPE, "factors are not initialised");
-        const int kp = c->kp;
-        std::vector<float> hw(size_t(c->mp) * kp), hh(size_t(c->np) * kp);
-        ck(cudaStreamSynchronize(c->stream), "sync");
-        ck(cudaMemcpy(hw.data(), c->W.p, hw.size() * 4, cudaMemcpyDeviceToHost), "D2H W");
-        ck(cudaMemcpy(hh.data(), c->Ht.p, hh.size() * 4, cudaMemcpyDeviceToHost), "D2H H");
-        if (w)
-            for (uint64_t i = 0; i < c->rows; ++i)
-                for (uint64_t j = 0; j < c->k; ++j) w[i * c->k + j] = hw[i * kp + j];
-        if (h)
-            for (uint64_t r = 0; r < c->k; ++r)
-                for (uint64_t j = 0; j < c->n; ++j) h[r * c->n + j] = hh[j * kp + r];
+        if (w) export_w(c, c->W.as<float>(), int64_t(c->rows), w);
+        if (h) export_h(c, h, int64_t(c->n));
     });
 }
 
@@ -1292,12 +1503,8 @@ int oocnmf_gather_w_f64(oocnmf_ctx* c, double* w_full) {
             nck(ncclAllGather(c->W.p, all.p, size_t(maxr) * kp, ncclFloat, c->comm, c->stream), "allgather W");
         else
             ck(cudaMemcpyAsync(all.p, c->W.p, size_t(maxr) * kp * 4, cudaMemcpyDeviceToDevice, c->stream), "copy");
-        std::vector<float> hw(size_t(N) * maxr * kp);
-        ck(cudaMemcpyAsync(hw.data(), all.p, hw.size() * 4, cudaMemcpyDeviceToHost, c->stream), "D2H");
-        ck(cudaStreamSynchronize(c->stream), "sync");
         for (int p = 0; p < N; ++p)
-            for (uint64_t i = beg[p]; i < beg[p + 1]; ++i)
-                for (uint64_t j = 0; j < c->k; ++j) w_full[i * c->k + j] = hw[(size_t(p) * maxr + (i - beg[p])) * kp + j];
+            export_w(c, all.as<float>() + size_t(p) * maxr * kp, int64_t(beg[p + 1] - beg[p]), w_full + beg[p] * c->k);
     });
 }
 
@@ -1385,23 +1592,23 @@ int oocnmf_gather_h_f64(oocnmf_ctx* c, double* h_full) {
         set_dev(c);
         need_problem(c);
         if (!c->factors_valid) fail(OOCNMF_ERR_SHAPE, "factors are not initialised");
-        const int kp = c->kp;
-        std::vector<float> hh(size_t(c->np) * kp);
-        ck(cudaStreamSynchronize(c->stream), "sync");
-        ck(cudaMemcpy(hh.data(), c->Ht.p, hh.size() * 4, cudaMemcpyDeviceToHost), "D2H H");
         // zero-padded sum over the ranks' column slabs (the reference's gather,
-        // src/nmf_distributed.cpp:267-273)
-        std::fill(h_full, h_full + c->k * c->n_global, 0.0);
-        for (uint64_t r = 0; r < c->k; ++r)
-            for (uint64_t j = 0; j < c->n; ++j) h_full[r * c->n_global + c->col0 + j] = hh[j * kp + r];
-        if (c->collective()) {
-            DevBuf d;
-            d.alloc(c->k * c->n_global * 8, "gather H");
-            ck(cudaMemcpyAsync(d.p, h_full, d.bytes, cudaMemcpyHostToDevice, c->stream), "H2D");
+        // src/nmf_distributed.cpp:267-273), assembled in HBM
+        const int64_t ng = int64_t(c->n_global);
+        DevBuf d;
+        d.alloc(c->k * c->n_global * 8, "gather H");
+        ck(cudaMemsetAsync(d.p, 0, d.bytes, c->stream), "memset");
+        ck(launch_strided_cast(CastKind::f32_f64, c->Ht.as<float>(), 1, c->kp, d.as<double>() + c->col0, ng, 1,
+                               int64_t(c->k), int64_t(c->n), c->stream),
+           "export H");
+        if (c->collective())
             nck(ncclAllReduce(d.p, d.p, c->k * c->n_global, ncclDouble, ncclSum, c->comm, c->stream), "allreduce H");
-            ck(cudaMemcpyAsync(h_full, d.p, d.bytes, cudaMemcpyDeviceToHost, c->stream), "D2H");
-            ck(cudaStreamSynchronize(c->stream), "sync");
-        }
+        copy_out(c, {Part{h_full, size_t(ng) * 8, size_t(ng) * 8}}, int64_t(c->k),
+                 [&](char* ds, int64_t off, int64_t len) {
+                     ck(cudaMemcpyAsync(ds, d.as<double>() + off * ng, size_t(len) * ng * 8,
+                                        cudaMemcpyDeviceToDevice, c->stream),
+                        "copy H");
+                 });
     });
 }
 

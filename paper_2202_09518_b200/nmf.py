@@ -132,12 +132,13 @@ class NmfResult:
 class CsrMatrix:
     """CSR with u64 indices and f64 values (reference CsrMatrix, matrix.hpp:63-102)."""
 
-    def __init__(self, rows, cols, row_ptr, col_idx, values):
+    def __init__(self, rows, cols, row_ptr, col_idx, values, _validated=False):
         self.rows, self.cols = int(rows), int(cols)
         self.row_ptr = np.ascontiguousarray(row_ptr, np.uint64)
         self.col_idx = np.ascontiguousarray(col_idx, np.uint64)
         self.values = np.ascontiguousarray(values, np.float64)
-        self.validate_structure()
+        if not _validated:  # (downloads of a resident CSR were checked when it was loaded)
+            self.validate_structure()
 
     @property
     def nnz(self):
@@ -309,7 +310,7 @@ class Context:
         ci = np.empty(max(nnz.value, 1), np.uint64)
         v = np.empty(max(nnz.value, 1))
         check(_capi.lib().oocnmf_download_csr(self._h, _p(rp, C.c_uint64), _p(ci, C.c_uint64), _p(v, C.c_double)))
-        return CsrMatrix(self.rows, self.n, rp, ci[:nnz.value], v[:nnz.value])
+        return CsrMatrix(self.rows, self.n, rp, ci[:nnz.value], v[:nnz.value], _validated=True)
 
     def attach_host(self, a: np.ndarray, batch_rows: int = 0):
         """Out-of-core: ``a`` (rows x n float32, ideally pinned) stays in host memory."""

@@ -355,6 +355,51 @@ def test_csr_with_empty_rows_and_columns(gpu):
     assert np.all(res.w[10:40] == 0)
 
 
+def test_csr_upload_checks_run_on_device(gpu):
+    """The C-ABI's CSR upload validates on device (k_csr_ingest / k_csr_check_rows) with the
+    reference constructor's messages; the Python class checks earlier, so call the C-ABI."""
+    import ctypes as C
+
+    lib = nmf._capi.lib()
+
+    def load(rp, ci, v, m=4, n=5):
+        rp, ci, v = (np.ascontiguousarray(x, t) for x, t in ((rp, np.uint64), (ci, np.uint64), (v, np.float64)))
+        with nmf.Context(gpu) as ctx:
+            ctx.set_problem(m, n, 2)
+            rc = lib.oocnmf_load_csr_f64(ctx._h, rp.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                         ci.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                         v.ctypes.data_as(C.POINTER(C.c_double)))
+            return rc, lib.oocnmf_last_error().decode()
+
+    ok = load([0, 2, 2, 3, 4], [0, 4, 1, 3], [1, 2, 3, 4])
+    assert ok[0] == 0, ok
+    assert "nondecreasing" in load([0, 3, 2, 3, 4], [0, 4, 1, 3], [1, 2, 3, 4])[1]
+    assert "out of range" in load([0, 2, 2, 3, 4], [0, 5, 1, 3], [1, 2, 3, 4])[1]
+    assert "strictly increase" in load([0, 2, 2, 3, 4], [4, 4, 1, 3], [1, 2, 3, 4])[1]
+    assert "strictly increase" in load([0, 2, 2, 3, 4], [3, 1, 1, 3], [1, 2, 3, 4])[1]
+    # a decreasing pair across a row boundary is legal
+    assert load([0, 1, 2, 3, 4], [4, 0, 3, 1], [1, 2, 3, 4])[0] == 0
+
+
+def test_csr_upload_spanning_many_staging_chunks(gpu):
+    """> 2 staging chunks (4 Mi entries each) through the pipelined upload, bit-exact back."""
+    m, n = 20000, 4000
+    rng = np.random.default_rng(5)
+    counts = rng.integers(0, 1000, m)
+    rp = np.zeros(m + 1, np.uint64)
+    rp[1:] = np.cumsum(counts)
+    ci = np.concatenate([np.sort(rng.choice(n, c, replace=False)) for c in counts]).astype(np.uint64)
+    v = rng.random(ci.size)
+    assert ci.size > 2 * (1 << 22)
+    a = nmf.CsrMatrix(m, n, rp, ci, v)
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, 4)
+        ctx.load_csr(a)
+        b = ctx.download_csr()
+    assert np.array_equal(b.row_ptr, rp) and np.array_equal(b.col_idx, ci)
+    assert np.array_equal(b.values, v.astype(np.float32).astype(np.float64))
+
+
 def test_out_of_core_batch_larger_than_slab_and_ragged_last_batch(gpu):
     m, n, k = 333, 200, 32
     a = port.uniform_dense(m, n, 9, 99).astype(np.float32)
