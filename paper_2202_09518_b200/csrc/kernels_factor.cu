@@ -14,26 +14,59 @@
 namespace ooc {
 namespace {
 
-// A CTA of 512 threads owns whole 128-row tiles and loops over them:
-//   1. the tile's F rows and numerator rows (plain, or the sum of the tile's stream-K
-//      partials in ascending CTA order) are staged in shared memory with coalesced loads,
-//      each thread keeping all of its kp/4 loads in flight;
-//   2. warp w updates 32 rows x one quarter of the columns: lane = row, so f[q] is a
-//      conflict-free read of the lane's own (padded) row and the G row segment is the same
-//      for the whole warp (a broadcast) — kp/4 FMAs per f[q], 3 wavefronts per 8 FMAs; the
-//      update f * n / (de + eps) and its n·f_new term of the trace-form error follow;
-//   3. the new rows go back to global memory (and [F | lo(F)] for the tensor-core operand)
-//      with coalesced stores;
-//   4. Gram partial: thread (block b, row group g) accumulates a GT x GT block of
-//      F_new^T F_new over its row group in f32 registers across the CTA's tiles; at the end the
-//      row groups are summed in f64 (fixed order) into one kp x kp slot per CTA.
-// With 16 warps per CTA and up to 4 CTAs per SM the per-row dependent chain is hidden by
-// occupancy (the previous layouts were latency-bound at 40-55 us for 65536 x 32 —
-// tools/fu_bench.cu).
-constexpr int kFuRows = kTile;          // rows per tile
-constexpr int kFuThreads = 4 * kFuRows;  // 4 threads per row in the update
-constexpr int kFuCtasPerSm = 2;
-constexpr int kFuMaxParts = 64;          // stream-K partials of one tile summed via smem offsets
+// A CTA of 256 threads owns whole 128-row tiles and loops over them, software-pipelined:
+//   0. the next tile's F rows and plain numerator rows are prefetched with cp.async into the
+//      other of two shared-memory stages while the current tile is computed (stream-K
+//      numerators — the sum of the tile's partials in ascending CTA order — are summed from
+//      global memory at the start of the tile instead);
+//   1. rows are stored unpadded with the 16-byte chunks of row r XOR-swizzled by swz(r), so
+//      the row-broadcast and column reads below are conflict-free and every access is 16 B;
+//   2. update: thread (row block rb, column group cg) owns R rows (rb + i * RB) x C columns:
+//      per 4 q it reads R float4 of F rows and C/4 float4 of G and issues 4 R C FMAs
+//      (8 loads per 64 FMAs at kp 32); then f * n / (de + eps) and the n · f_new term of the
+//      trace-form error, written in place over the numerator;
+//   3. the new rows go back with 16-byte coalesced stores (and [F | lo(F)] for the
+//      tensor-core operand);
+//   4. Gram partial of the new rows, upper-triangle 4x4 blocks only (the Gram is mirrored
+//      from its upper triangle anyway): thread (block b, row group g) accumulates in f32
+//      registers across the CTA's tiles; at the end the row groups are summed in f64 (fixed
+//      order) into one kp x kp slot per CTA.
+// The FFMA work (kp^2 for the denominator + kp(kp+4)/2 for the Gram per row) is about the
+// same time as the 12 kp bytes per row of HBM traffic at kp 32, so both are kept busy
+// (3 CTAs / SM at kp <= 32).
+#ifndef OOC_FU_CTAS
+#define OOC_FU_CTAS 3
+#endif
+constexpr int kFuRows = kTile;  // rows per tile
+constexpr int kFuThreads = 256;
+constexpr int kFuMaxParts = 64;  // stream-K partials of one tile summed via smem offsets
+
+template <int KP>
+struct FuCfg {
+    static constexpr int NCH = KP / 4;                   // 16-byte chunks per row
+    static constexpr int TILE = kFuRows * KP;            // floats per tile
+    static constexpr int C = KP >= 64 ? 8 : 4;           // update columns per thread
+    static constexpr int NCG = KP / C;                   // column groups
+    static constexpr int R = TILE / (kFuThreads * C);    // update rows per thread
+    static constexpr int RB = kFuRows / R;               // row blocks
+    static_assert(RB * NCG == kFuThreads, "update mapping");
+    static constexpr int NGB = NCH * (NCH + 1) / 2;      // upper-triangle Gram blocks
+    static constexpr int RG0 = kFuThreads / NGB;
+    static constexpr int RG = RG0 > 32 ? 32 : RG0;       // Gram row groups
+    static constexpr int CTAS = KP >= 64 ? 1 : OOC_FU_CTAS;  // resident CTAs per SM (smem)
+    // smem (floats): 2 stages x [F tile | N tile] | G (KP x KP) | f64 reduction scratch
+    static constexpr size_t STAGES_F = size_t(4) * TILE;
+    static constexpr size_t SMEM = (STAGES_F + size_t(KP) * KP) * 4 + size_t(kFuThreads) * 8;
+    static_assert(size_t(RG) * KP * KP <= STAGES_F, "Gram partials fit in the stages");
+    // chunk swizzle: rows sharing a 128-byte bank line get distinct chunk offsets
+    static __device__ __forceinline__ int swz(int r) {
+        constexpr int per_line = KP >= 32 ? 1 : 32 / KP;
+        constexpr int mask = NCH - 1 < 7 ? NCH - 1 : 7;
+        return (r / per_line) & mask;
+    }
+    // float offset of chunk ch of row r
+    static __device__ __forceinline__ int at(int r, int ch) { return r * KP + ((ch ^ swz(r)) << 2); }
+};
 
 // Fixed-shape block reduction of a double (deterministic).
 __device__ double block_sum_f64(double v, double* sh) {
@@ -49,166 +82,241 @@ __device__ double block_sum_f64(double v, double* sh) {
     return r;
 }
 
+#ifdef OOC_FU_PROFILE
+// developer instrumentation (tools/fu_bench.cu): per-phase SM cycles summed over CTAs (thread 0)
+__device__ unsigned long long g_fu_prof[8];
+#define FU_MARK(i)                                               \
+    if (threadIdx.x == 0) {                                      \
+        const long long now_ = clock64();                        \
+        prof_acc[i] += now_ - prof_last, prof_last = now_;       \
+    }
+#else
+#define FU_MARK(i)
+#endif
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Copy one 128-row tile (contiguous in global memory) into a swizzled stage.
 template <int KP>
-struct FuCfg {
-    static constexpr int FS = KP + 1;                  // padded f32 row stride
-    static constexpr int QC = KP / 4;                  // update columns per thread
-    static constexpr int GT = KP >= 32 ? 4 : 2;        // Gram thread block GT x GT
-    static constexpr int GB = KP / GT;
-    static constexpr int NGB = GB * GB;                // Gram blocks (<= 512)
-    static constexpr int RG = kFuThreads / NGB;        // row groups
-    static_assert(NGB <= kFuThreads && kFuThreads % NGB == 0 && kFuRows % RG == 0, "Gram blocking");
-    static constexpr int EPT = kFuRows * KP / kFuThreads;  // staged elements per thread
-    // smem: G (f32) | Fs | Ns (f32, padded rows) ; the Gram partials (RG x KP x KP f32) reuse
-    // Fs/Ns at the end
-    static constexpr size_t ROWS_BYTES = 2 * size_t(kFuRows) * FS * 4;
-    static constexpr size_t PART_BYTES = size_t(RG) * KP * KP * 4;
-    static_assert(PART_BYTES <= ROWS_BYTES, "Gram partials fit in the row buffers");
-    static constexpr size_t SMEM = size_t(KP * KP) * 4 + ROWS_BYTES + size_t(kFuThreads) * 8;
-};
+__device__ __forceinline__ void stage_tile(float* dst, const float* src) {
+    using C = FuCfg<KP>;
+#pragma unroll
+    for (int i = 0; i < C::TILE / 4 / kFuThreads; ++i) {
+        const int c = threadIdx.x + i * kFuThreads, r = c / C::NCH, ch = c % C::NCH;
+        cp_async16(dst + C::at(r, ch), src + c * 4);
+    }
+}
 
 template <int KP>
-__global__ void __launch_bounds__(kFuThreads, 2)
+__global__ void __launch_bounds__(kFuThreads, FuCfg<KP>::CTAS)
     k_factor_update(float* __restrict__ F, int64_t tiles, const float* __restrict__ n_plain,
                     const float* __restrict__ n_slots, StreamK sk, const float* __restrict__ G,
                     float eps, int update, double* __restrict__ gram_slots,
                     double* __restrict__ err_slots, int* __restrict__ flag, float* __restrict__ cat_out) {
     using C = FuCfg<KP>;
-    constexpr int FS = C::FS, GT = C::GT, QC = C::QC;
+    constexpr int TILE = C::TILE, NCH = C::NCH, CC = C::C, R = C::R;
     extern __shared__ __align__(16) unsigned char fu_smem[];
-    float* Gs = reinterpret_cast<float*>(fu_smem);  // KP x KP
-    float* Fs = Gs + KP * KP;                         // kFuRows x FS: old rows
-    float* Ns = Fs + kFuRows * FS;                    // kFuRows x FS: numerator, then new rows
-    double* red = reinterpret_cast<double*>(Ns + kFuRows * FS);  // kFuThreads (8-byte aligned)
+    float* stages = reinterpret_cast<float*>(fu_smem);      // [F0 | N0 | F1 | N1]
+    float* Gs = stages + C::STAGES_F;                        // KP x KP
+    double* red = reinterpret_cast<double*>(Gs + KP * KP);   // kFuThreads
     __shared__ int64_t part_off[kFuMaxParts];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
+    const bool plain = update && n_plain;
     if (update)
         for (int e = tid; e < KP * KP; e += kFuThreads) Gs[e] = G[e];
-    // update role: warp -> (row block of 32, column quarter)
-    const int urow = (warp & 3) * 32 + lane, uc0 = (warp >> 2) * QC;
-    // Gram role
+    // update role
+    const int cg = tid % C::NCG, rb = tid / C::NCG;
+    // Gram role: upper-triangle block (bi <= bj) and row group
     const int gblk = tid % C::NGB, grg = tid / C::NGB;
-    const int gi0 = (gblk / C::GB) * GT, gj0 = (gblk % C::GB) * GT;
-    float gacc[GT * GT];
+    int bi = 0, bj = gblk;
+    while (bj >= NCH - bi) bj -= NCH - bi, ++bi;
+    bj += bi;
+    const bool gram_live = grg < C::RG;
+    float gacc[16];
 #pragma unroll
-    for (int q = 0; q < GT * GT; ++q) gacc[q] = 0.f;
+    for (int q = 0; q < 16; ++q) gacc[q] = 0.f;
     double eacc = 0.0;
     bool bad = false;
 
-    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int64_t base = t * kFuRows * KP;
-        int nparts = 0;
-        int64_t cfirst = 0;
-        if (update && !n_plain) {
-            // the tile's partials, ascending CTA order (64-bit divisions once per tile)
-            cfirst = sk.cta_of(t * sk.ipt);
-            nparts = int(sk.cta_of((t + 1) * sk.ipt - 1) - cfirst + 1);
-            for (int q = tid; q < nparts && q < kFuMaxParts; q += kFuThreads)
-                part_off[q] = sk.slot(cfirst + q, t) * int64_t(kTile * KP);
-            __syncthreads();
+#ifdef OOC_FU_PROFILE
+    long long prof_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0}, prof_last = clock64();
+#endif
+    if (int64_t(blockIdx.x) < tiles) {
+        const int64_t t0 = blockIdx.x;
+        stage_tile<KP>(stages, F + t0 * TILE);
+        if (plain) stage_tile<KP>(stages + TILE, n_plain + t0 * TILE);
+    }
+    cp_async_commit();
+    int it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        float* Fs = stages + (it & 1) * 2 * TILE;
+        float* Ns = Fs + TILE;
+        {   // prefetch the next tile into the other stage (freed by the previous iteration's
+            // final barrier)
+            const int64_t tn = t + gridDim.x;
+            if (tn < tiles) {
+                float* Fn = stages + ((it + 1) & 1) * 2 * TILE;
+                stage_tile<KP>(Fn, F + tn * TILE);
+                if (plain) stage_tile<KP>(Fn + TILE, n_plain + tn * TILE);
+            }
+            cp_async_commit();
         }
-        // 1. stage (element e = tid + kFuThreads * i)
-        {
-            float fv[C::EPT], nv[C::EPT];
+        FU_MARK(0)  // prefetch issue
+        if (update && !n_plain) {
+            // the tile's stream-K partials, ascending CTA order (64-bit divisions once per tile)
+            const int64_t cfirst = sk.cta_of(t * sk.ipt);
+            const int nparts = int(sk.cta_of((t + 1) * sk.ipt - 1) - cfirst + 1);
+            for (int q = tid; q < nparts && q < kFuMaxParts; q += kFuThreads)
+                part_off[q] = sk.slot(cfirst + q, t) * int64_t(TILE);
+            __syncthreads();
+            constexpr int PER = TILE / 4 / kFuThreads;
+            float4 acc[PER];
 #pragma unroll
-            for (int i = 0; i < C::EPT; ++i) fv[i] = F[base + tid + i * kFuThreads];
-            if (update) {
-                if (n_plain) {
+            for (int i = 0; i < PER; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < nparts; ++q) {
+                const float4* src = reinterpret_cast<const float4*>(
+                    n_slots + (q < kFuMaxParts ? part_off[q] : sk.slot(cfirst + q, t) * int64_t(TILE)));
+                float4 pv[PER];
 #pragma unroll
-                    for (int i = 0; i < C::EPT; ++i) nv[i] = n_plain[base + tid + i * kFuThreads];
-                } else {
+                for (int i = 0; i < PER; ++i) pv[i] = src[tid + i * kFuThreads];
 #pragma unroll
-                    for (int i = 0; i < C::EPT; ++i) nv[i] = 0.f;
-                    for (int q = 0; q < nparts; ++q) {
-                        const float* src =
-                            n_slots + (q < kFuMaxParts ? part_off[q] : sk.slot(cfirst + q, t) * int64_t(kTile * KP));
-                        float pv[C::EPT];
+                for (int i = 0; i < PER; ++i)
+                    acc[i].x += pv[i].x, acc[i].y += pv[i].y, acc[i].z += pv[i].z, acc[i].w += pv[i].w;
+            }
 #pragma unroll
-                        for (int i = 0; i < C::EPT; ++i) pv[i] = src[tid + i * kFuThreads];
+            for (int i = 0; i < PER; ++i) {
+                const int c = tid + i * kFuThreads;
+                *reinterpret_cast<float4*>(Ns + C::at(c / NCH, c % NCH)) = acc[i];
+            }
+        }
+        FU_MARK(1)  // stream-K numerator
+        cp_async_wait<1>();  // this tile's group (the prefetch may still be in flight)
+        FU_MARK(2)  // cp.async wait
+        __syncthreads();
+        FU_MARK(3)  // barrier
+        // 2. update
+        if (update) {
+            float de[R][CC];
 #pragma unroll
-                        for (int i = 0; i < C::EPT; ++i) nv[i] += pv[i];
+            for (int i = 0; i < R; ++i)
+#pragma unroll
+                for (int j = 0; j < CC; ++j) de[i][j] = 0.f;
+#pragma unroll 2
+            for (int q4 = 0; q4 < NCH; ++q4) {
+                float4 f[R];
+#pragma unroll
+                for (int i = 0; i < R; ++i) f[i] = *reinterpret_cast<const float4*>(Fs + C::at(rb + i * C::RB, q4));
+#pragma unroll
+                for (int qq = 0; qq < 4; ++qq) {
+                    float g[CC];
+#pragma unroll
+                    for (int j = 0; j < CC; j += 4) {
+                        const float4 gv = *reinterpret_cast<const float4*>(Gs + (q4 * 4 + qq) * KP + cg * CC + j);
+                        g[j] = gv.x, g[j + 1] = gv.y, g[j + 2] = gv.z, g[j + 3] = gv.w;
+                    }
+#pragma unroll
+                    for (int i = 0; i < R; ++i) {
+                        const float fq = qq == 0 ? f[i].x : qq == 1 ? f[i].y : qq == 2 ? f[i].z : f[i].w;
+#pragma unroll
+                        for (int j = 0; j < CC; ++j) de[i][j] = fmaf(fq, g[j], de[i][j]);
                     }
                 }
             }
+            // n · f_new: f32 products (round-to-nearest, unbiased) summed over the thread's
+            // R x C elements, then one f64 add per tile (f32 -> f64 conversions are slow)
+            float e = 0.f;
 #pragma unroll
-            for (int i = 0; i < C::EPT; ++i) {
-                const int e = tid + i * kFuThreads, r = e / KP, j = e % KP;
-                Fs[r * FS + j] = fv[i];
-                if (update) Ns[r * FS + j] = nv[i];
+            for (int i = 0; i < R; ++i) {
+                const int r = rb + i * C::RB;
+#pragma unroll
+                for (int j = 0; j < CC; j += 4) {
+                    const int off = C::at(r, (cg * CC + j) >> 2);
+                    const float4 fo = *reinterpret_cast<const float4*>(Fs + off);
+                    const float4 nu = *reinterpret_cast<const float4*>(Ns + off);
+                    // t * nu / (de + eps) as (t * nu) * rcp_rn(de + eps): the denominator is a
+                    // normal number (>= eps), so the reciprocal never takes the IEEE-division
+                    // slow path that tiny (decaying) numerators would trigger; <= 1.5 ulp
+                    float4 nf;
+                    nf.x = (fo.x * nu.x) * __frcp_rn(de[i][j] + eps);
+                    nf.y = (fo.y * nu.y) * __frcp_rn(de[i][j + 1] + eps);
+                    nf.z = (fo.z * nu.z) * __frcp_rn(de[i][j + 2] + eps);
+                    nf.w = (fo.w * nu.w) * __frcp_rn(de[i][j + 3] + eps);
+                    bad |= !isfinite(nf.x) || !isfinite(nf.y) || !isfinite(nf.z) || !isfinite(nf.w);
+                    e = fmaf(nu.x, nf.x, e);
+                    e = fmaf(nu.y, nf.y, e);
+                    e = fmaf(nu.z, nf.z, e);
+                    e = fmaf(nu.w, nf.w, e);
+                    *reinterpret_cast<float4*>(Ns + off) = nf;  // (row, chunk) private to this thread
+                }
+            }
+            eacc += double(e);
+            FU_MARK(4)  // update
+            __syncthreads();
+            FU_MARK(5)  // barrier
+        }
+        const float* src = update ? Ns : Fs;
+        // 3. write back (16-byte coalesced)
+        if (update || cat_out) {
+#pragma unroll
+            for (int i = 0; i < TILE / 4 / kFuThreads; ++i) {
+                const int c = tid + i * kFuThreads, r = c / NCH, ch = c % NCH;
+                const float4 v = *reinterpret_cast<const float4*>(src + C::at(r, ch));
+                if (update) reinterpret_cast<float4*>(F + t * TILE)[c] = v;
+                if (cat_out) {
+                    float* cw = cat_out + (t * kFuRows + r) * 2 * KP + ch * 4;
+                    *reinterpret_cast<float4*>(cw) = v;
+                    *reinterpret_cast<float4*>(cw + KP) = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
+                }
             }
         }
-        __syncthreads();
-        // 2. update: lane = row urow, columns [uc0, uc0 + QC)
-        if (update) {
-            const float* fr = Fs + urow * FS;
-            float de[QC];
-#pragma unroll
-            for (int j = 0; j < QC; ++j) de[j] = 0.f;
-#pragma unroll 8
-            for (int q = 0; q < KP; ++q) {
-                const float fq = fr[q];
-                const float* g = Gs + q * KP + uc0;
-#pragma unroll
-                for (int j = 0; j < QC; ++j) de[j] = fmaf(fq, g[j], de[j]);
-            }
-            float* nr = Ns + urow * FS + uc0;
-            double e = 0.0;
-#pragma unroll
-            for (int j = 0; j < QC; ++j) {
-                const float nu = nr[j];
-                const float nf = fr[uc0 + j] * nu / (de[j] + eps);
-                bad |= !isfinite(nf);
-                e += double(nu) * double(nf);
-                nr[j] = nf;  // (row, column quarter) is private to this thread
-            }
-            eacc += e;
-        } else {
-            for (int e = tid; e < kFuRows * KP; e += kFuThreads) {
-                const int r = e / KP, j = e % KP;
-                Ns[r * FS + j] = Fs[r * FS + j];
-            }
-        }
-        __syncthreads();
-        // 3. write back (coalesced)
-#pragma unroll
-        for (int i = 0; i < C::EPT; ++i) {
-            const int e = tid + i * kFuThreads, r = e / KP, j = e % KP;
-            const float v = Ns[r * FS + j];
-            if (update) F[base + e] = v;
-            if (cat_out) {
-                float* cw = cat_out + (t * kFuRows + r) * 2 * KP;
-                cw[j] = v;
-                cw[KP + j] = tf32_lo(v);
-            }
-        }
+        FU_MARK(6)  // write back
         // 4. Gram partial of the tile's new rows
+        if (gram_live) {
 #pragma unroll 4
-        for (int r = grg; r < kFuRows; r += C::RG) {
-            const float* row = Ns + r * FS;
-            float fi[GT], fj[GT];
+            for (int r = grg; r < kFuRows; r += C::RG) {
+                const float4 a = *reinterpret_cast<const float4*>(src + C::at(r, bi));
+                const float4 b = *reinterpret_cast<const float4*>(src + C::at(r, bj));
+                const float fa[4] = {a.x, a.y, a.z, a.w}, fb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-            for (int a = 0; a < GT; ++a) fi[a] = row[gi0 + a], fj[a] = row[gj0 + a];
+                for (int x = 0; x < 4; ++x)
 #pragma unroll
-            for (int a = 0; a < GT; ++a)
-#pragma unroll
-                for (int b = 0; b < GT; ++b) gacc[a * GT + b] = fmaf(fi[a], fj[b], gacc[a * GT + b]);
+                    for (int y = 0; y < 4; ++y) gacc[x * 4 + y] = fmaf(fa[x], fb[y], gacc[x * 4 + y]);
+            }
         }
-        __syncthreads();  // Fs / Ns are rewritten by the next tile
+        FU_MARK(7)  // Gram
+        __syncthreads();  // this stage is refilled by the next iteration's prefetch
+        FU_MARK(3)
     }
-    // row groups -> f64 CTA sum in fixed order (partials parked in the row buffers)
-    float* part = Fs;
+#ifdef OOC_FU_PROFILE
+    if (threadIdx.x == 0)
+        for (int i = 0; i < 8; ++i) atomicAdd(&g_fu_prof[i], (unsigned long long)prof_acc[i]);
+#endif
+    cp_async_wait<0>();
+    __syncthreads();
+    // row groups -> f64 CTA sum in fixed order (partials parked in the stages)
+    float* part = stages;
+    if (gram_live) {
 #pragma unroll
-    for (int a = 0; a < GT; ++a)
+        for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int b = 0; b < GT; ++b) part[(grg * KP + gi0 + a) * KP + gj0 + b] = gacc[a * GT + b];
+            for (int y = 0; y < 4; ++y) part[(grg * KP + bi * 4 + x) * KP + bj * 4 + y] = gacc[x * 4 + y];
+    }
     __syncthreads();
     double* gout = gram_slots + int64_t(blockIdx.x) * KP * KP;
     for (int e = tid; e < KP * KP; e += kFuThreads) {
         const int i = e / KP, j = e % KP;
-        // mirror the upper triangle so the Gram is symmetric to the bit
-        const int src = i <= j ? e : j * KP + i;
+        // the upper triangle, mirrored, so the Gram is symmetric to the bit
+        const int src_e = i <= j ? e : j * KP + i;
         double sum = 0.0;
-        for (int g = 0; g < C::RG; ++g) sum += double(part[g * KP * KP + src]);
+        for (int g = 0; g < C::RG; ++g) sum += double(part[g * KP * KP + src_e]);
         gout[e] = sum;
     }
     if (err_slots) {
@@ -280,6 +388,16 @@ __global__ void k_finalize_error(int kp, const double* __restrict__ err_slots, i
 
 }  // namespace
 
+#ifdef OOC_FU_PROFILE
+void fu_profile_read(unsigned long long* out, bool reset) {
+    cudaMemcpyFromSymbol(out, g_fu_prof, sizeof(unsigned long long) * 8);
+    if (reset) {
+        unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_fu_prof, z, sizeof z);
+    }
+}
+#endif
+
 int factor_grid(int64_t tiles) {
     static int sms = [] {
         int d = 0, n = 148;
@@ -289,7 +407,7 @@ int factor_grid(int64_t tiles) {
     static int64_t per_sm = [] {  // OOCNMF_FU_CTAS_PER_SM: developer knob (tools/fu_bench.cu)
         const char* e = std::getenv("OOCNMF_FU_CTAS_PER_SM");
         const int v = e ? std::atoi(e) : 0;
-        return int64_t(v > 0 ? v : kFuCtasPerSm);
+        return int64_t(v > 0 ? v : FuCfg<32>::CTAS);
     }();
     const int64_t cap = int64_t(sms) * per_sm;
     return int(tiles < cap ? (tiles < 1 ? 1 : tiles) : cap);
