@@ -104,6 +104,13 @@ cudaError_t launch_split_cat(const float* F, float* cat, int64_t rows, int kp, c
 // out (rows x kp) = CSR(rp, ci, v) · B (B rows indexed by column, kp wide).
 cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const float* v,
                         int64_t rows, const float* B, float* out, cudaStream_t s);
+// Column chunks of a CSR with column-sorted rows: seg[c * rows + i] = first entry of row i
+// with column >= c * chunk_cols (c = 0..C); chunk c of row i is [seg[c][i], seg[c+1][i]).
+cudaError_t launch_csr_segments(const int64_t* rp, const int32_t* ci, int64_t rows, int64_t chunk_cols, int C,
+                                int64_t* seg, cudaStream_t s);
+// out (rows x kp) = (or +=, accumulate) the chunk [lo[i], hi[i]) of each row of a CSR · B.
+cudaError_t launch_spmm_seg(int kp, const int64_t* lo, const int64_t* hi, const int32_t* ci, const float* v,
+                            int64_t rows, const float* B, float* out, bool accumulate, cudaStream_t s);
 cudaError_t launch_residual_csr(int kp, const int64_t* rp, const int32_t* ci, const float* v,
                                 int64_t rows, int64_t cols, const float* W, const float* Ht,
                                 double* out_slots, cudaStream_t s,

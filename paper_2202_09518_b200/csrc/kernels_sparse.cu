@@ -102,6 +102,119 @@ __global__ void __launch_bounds__(256) k_spmm_v4(const int64_t* __restrict__ rp,
     }
 }
 
+// ---------------------------------------------------------------------------- column chunks
+// A uniformly sparse A gathers a random kp-wide row of B per nonzero: 42 gathers per B row at
+// config 3, each a DRAM read because B (512 MB) is four times the L2. Splitting the columns
+// into chunks whose B slice fits in L2 and running one pass per chunk turns those gathers
+// into L2 hits: B is read from DRAM once, the A entries once, and the price is the f32
+// output accumulated across the chunk passes (read + write per chunk). Rows are sorted by
+// column, so chunk c of row i is the contiguous range [seg[c][i], seg[c+1][i]).
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ld_hint_f4(const float* a, uint64_t pol) {
+    float4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int ld_hint_i32(const int32_t* a, uint64_t pol) {
+    int r;
+    asm volatile("ld.global.nc.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ float ld_hint_f32(const float* a, uint64_t pol) {
+    float r;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ int64_t ld_hint_i64(const int64_t* a, uint64_t pol) {
+    int64_t r;
+    asm volatile("ld.global.nc.L2::cache_hint.b64 %0, [%1], %2;" : "=l"(r) : "l"(a), "l"(pol));
+    return r;
+}
+__device__ __forceinline__ void st_hint_f4(float* a, float4 v, uint64_t pol) {
+    asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(a), "f"(v.x), "f"(v.y),
+                 "f"(v.z), "f"(v.w), "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ float4 ld_plain_hint_f4(const float* a, uint64_t pol) {
+    float4 r;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+                 : "l"(a), "l"(pol));
+    return r;
+}
+
+__global__ void k_csr_segments(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci, int64_t rows,
+                               int64_t chunk_cols, int C, int64_t* __restrict__ seg) {
+    for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < rows;
+         i += int64_t(gridDim.x) * blockDim.x) {
+        int64_t p = rp[i];
+        const int64_t e = rp[i + 1];
+        seg[i] = p;
+        for (int c = 1; c < C; ++c) {
+            const int64_t lim = int64_t(c) * chunk_cols;
+            while (p < e && ci[p] < lim) ++p;
+            seg[int64_t(c) * rows + i] = p;
+        }
+        seg[int64_t(C) * rows + i] = e;
+    }
+}
+
+// k_spmm_v4 over one column chunk: row i's entries [lo[i], hi[i]); B gathers marked
+// evict-last (the chunk's slice is what L2 should keep), the streams evict-first.
+template <int KP>
+__global__ void __launch_bounds__(256) k_spmm_seg(const int64_t* __restrict__ lo, const int64_t* __restrict__ hi,
+                                                  const int32_t* __restrict__ ci, const float* __restrict__ v,
+                                                  int64_t rows, const float* __restrict__ B,
+                                                  float* __restrict__ out, int accumulate) {
+    constexpr int LPR = KP / 4;    // lanes per row
+    constexpr int RPW = 32 / LPR;  // rows per warp
+    const int lane = threadIdx.x & 31, sub = lane / LPR, l = lane % LPR;
+    const uint64_t keep = policy_evict_last(), stream = policy_evict_first();
+    const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    for (int64_t wg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wg * RPW < rows; wg += warps) {
+        const int64_t row = wg * RPW + sub;
+        const bool live = row < rows;
+        const int64_t beg = live ? ld_hint_i64(lo + row, stream) : 0, end = live ? ld_hint_i64(hi + row, stream) : 0;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t p0 = beg; __any_sync(0xffffffffu, p0 < end); p0 += LPR) {
+            const int64_t p = p0 + l;
+            const int col = p < end ? ld_hint_i32(ci + p, stream) : 0;
+            const float val = p < end ? ld_hint_f32(v + p, stream) : 0.f;
+#pragma unroll
+            for (int t = 0; t < LPR; ++t) {
+                const int c = __shfl_sync(0xffffffffu, col, sub * LPR + t);
+                const float w = __shfl_sync(0xffffffffu, val, sub * LPR + t);
+                if (p0 + t < end) {
+                    const float4 b = ld_hint_f4(B + int64_t(c) * KP + 4 * l, keep);
+                    acc.x = fmaf(w, b.x, acc.x);
+                    acc.y = fmaf(w, b.y, acc.y);
+                    acc.z = fmaf(w, b.z, acc.z);
+                    acc.w = fmaf(w, b.w, acc.w);
+                }
+            }
+        }
+        if (live) {
+            float* o = out + row * KP + 4 * l;
+            if (accumulate) {
+                const float4 prev = ld_plain_hint_f4(o, stream);
+                acc.x += prev.x, acc.y += prev.y, acc.z += prev.z, acc.w += prev.w;
+            }
+            st_hint_f4(o, acc, stream);
+        }
+    }
+}
+
 __device__ double block_sum256(double v) {
     __shared__ double sh[256];
     sh[threadIdx.x] = v;
@@ -264,6 +377,28 @@ cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const floa
         case 16: k_spmm<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
         case 32: k_spmm<32><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
         case 64: k_spmm<64><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, out); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_csr_segments(const int64_t* rp, const int32_t* ci, int64_t rows, int64_t chunk_cols, int C,
+                                int64_t* seg, cudaStream_t s) {
+    if (rows <= 0) return cudaSuccess;
+    k_csr_segments<<<grid_for(rows), 256, 0, s>>>(rp, ci, rows, chunk_cols, C, seg);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spmm_seg(int kp, const int64_t* lo, const int64_t* hi, const int32_t* ci, const float* v,
+                            int64_t rows, const float* B, float* out, bool accumulate, cudaStream_t s) {
+    const int64_t warps = (rows * (kp / 4) + 31) / 32;
+    const unsigned grid = grid_for(warps * 32);
+    const int acc = accumulate ? 1 : 0;
+    switch (kp) {
+        case 8: k_spmm_seg<8><<<grid, 256, 0, s>>>(lo, hi, ci, v, rows, B, out, acc); break;
+        case 16: k_spmm_seg<16><<<grid, 256, 0, s>>>(lo, hi, ci, v, rows, B, out, acc); break;
+        case 32: k_spmm_seg<32><<<grid, 256, 0, s>>>(lo, hi, ci, v, rows, B, out, acc); break;
+        case 64: k_spmm_seg<64><<<grid, 256, 0, s>>>(lo, hi, ci, v, rows, B, out, acc); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

@@ -129,6 +129,13 @@ struct oocnmf_ctx {
     Kind kind = Kind::none;
     DevBuf A;                       // dense: mp x np f32
     DevBuf rp, ci, v, rpT, ciT, vT; // csr: slab rows x n and its transpose n x rows
+    // column chunks of the two SpMMs (csr_chunks): A over its n columns (gathers Ht), A^T over
+    // its rows columns (gathers W); C = 1 is the single-pass SpMM
+    struct Chunks {
+        DevBuf seg;
+        int C = 1, kp = 0;
+        int64_t cols = 0;
+    } chA, chT;
     int64_t nnz = 0;
     const float* hA = nullptr;      // out-of-core host slab
     uint64_t hlda = 0;
@@ -195,6 +202,63 @@ void count(oocnmf_ctx* c, cudaError_t e, const char* what) {
     ++c->launches;
 }
 
+// Column-chunked SpMM plan (kernels_sparse.cu, launch_spmm_seg): chunk the gathered operand
+// so each pass's slice stays in L2, when the traffic model says the chunk passes move fewer
+// bytes than one gathering pass. Per row: one pass gathers nnz_row x kp x 4 bytes from DRAM;
+// C passes read 16 bytes of segment bounds and read + write the kp x 4 accumulator row per
+// pass, plus the gathered operand once. OOCNMF_SPMM_CHUNK_MB sets the slice size (default
+// 40 MB: a third of the 126 MB L2); 0 disables chunking.
+void plan_chunks(oocnmf_ctx* c, oocnmf_ctx::Chunks& ch, const int64_t* rp, const int32_t* ci, int64_t rows,
+                 int64_t cols) {
+    const char* e = std::getenv("OOCNMF_SPMM_CHUNK_MB");  // (fractions allowed: tests force chunks)
+    const int64_t target = int64_t((e ? std::atof(e) : 40.0) * 1048576.0);
+    const char* f = std::getenv("OOCNMF_SPMM_CHUNK_FORCE");
+    const bool force = f && *f && *f != '0';
+    const int kp = c->kp;
+    ch.kp = kp;
+    ch.C = 1;
+    ch.seg.release();
+    const int64_t b_bytes = cols * kp * 4;
+    if (target <= 0 || rows <= 0 || b_bytes <= target) return;
+    const int C = int((b_bytes + target - 1) / target);
+    const double nnz_row = double(c->nnz) / double(rows);
+    const double one_pass = nnz_row * kp * 4;
+    const double chunked = C * 16.0 + (2.0 * C - 1.0) * kp * 4 + double(b_bytes) / double(rows);
+    // (measured at config 3, 42 entries per row: 8-13 chunk passes of ~4 entries per row are
+    // latency-bound on the per-row bounds and accumulator round trips — 5.5-6.8 ms against
+    // 3.8 ms for the one gathering pass — so chunks also need >= 16 entries per row each)
+    if (C > 64 || (!force && (chunked * 1.25 > one_pass || nnz_row < 16.0 * C))) return;
+    ch.C = C;
+    ch.cols = (cols + C - 1) / C;
+    ch.seg.alloc(size_t(C + 1) * rows * 8, "spmm chunks");
+    ck(launch_csr_segments(rp, ci, rows, ch.cols, C, ch.seg.as<int64_t>(), c->stream), "csr chunks");
+}
+
+void ensure_chunks(oocnmf_ctx* c) {
+    if (c->kind != Kind::csr) return;
+    if (c->chA.kp != c->kp)
+        plan_chunks(c, c->chA, c->rp.as<int64_t>(), c->ci.as<int32_t>(), int64_t(c->rows), int64_t(c->n));
+    if (c->chT.kp != c->kp)
+        plan_chunks(c, c->chT, c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), int64_t(c->n), int64_t(c->rows));
+}
+
+// out = A · Ht (transpose = false: rows x kp) or A^T · W (n x kp), chunked per the plan.
+void spmm(oocnmf_ctx* c, bool transpose, const float* B, float* out, cudaStream_t s) {
+    const auto& ch = transpose ? c->chT : c->chA;
+    const int64_t* rp = (transpose ? c->rpT : c->rp).as<int64_t>();
+    const int32_t* ci = (transpose ? c->ciT : c->ci).as<int32_t>();
+    const float* v = (transpose ? c->vT : c->v).as<float>();
+    const int64_t rows = transpose ? int64_t(c->n) : int64_t(c->rows);
+    if (ch.C <= 1) {
+        count(c, launch_spmm(c->kp, rp, ci, v, rows, B, out, s), transpose ? "spmm At W" : "spmm A Ht");
+        return;
+    }
+    const int64_t* seg = ch.seg.as<int64_t>();
+    for (int k = 0; k < ch.C; ++k)
+        count(c, launch_spmm_seg(c->kp, seg + k * rows, seg + (k + 1) * rows, ci, v, rows, B, out, k > 0, s),
+              transpose ? "spmm At W (chunk)" : "spmm A Ht (chunk)");
+}
+
 void alloc_factors(oocnmf_ctx* c) {
     const int kp = c->kp;
     c->W.alloc(size_t(c->mp) * kp * 4, "W");
@@ -242,6 +306,8 @@ void reset_source(oocnmf_ctx* c) {
     c->A.release();
     c->rp.release(), c->ci.release(), c->v.release();
     c->rpT.release(), c->ciT.release(), c->vT.release();
+    c->chA.seg.release(), c->chT.seg.release();
+    c->chA.C = c->chT.C = 1, c->chA.kp = c->chT.kp = 0;
     c->stage[0].release(), c->stage[1].release();
     c->hA = nullptr;
     c->kind = Kind::none;
@@ -387,9 +453,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         }
         rec(eReduced);
     } else if (c->kind == Kind::csr) {
-        count(c, launch_spmm(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows,
-                             c->Ht.as<float>(), c->N1.as<float>(), s),
-              "spmm A Ht");
+        spmm(c, false, c->Ht.as<float>(), c->N1.as<float>(), s);
         rec(eAht);
         allreduce_aht(c);
         count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
@@ -398,9 +462,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
               "W update");
         count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
-        count(c, launch_spmm(kp, c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), c->vT.as<float>(), c->n,
-                             c->W.as<float>(), c->wta(), s),
-              "spmm At W");
+        spmm(c, true, c->W.as<float>(), c->wta(), s);
         rec(eWta);
         rec(eReduced);
     } else {
@@ -603,7 +665,9 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
         uint64_t(reinterpret_cast<uintptr_t>(c->packed.p)), uint64_t(reinterpret_cast<uintptr_t>(c->slots1.p)),
         uint64_t(reinterpret_cast<uintptr_t>(c->slots2.p)), uint64_t(reinterpret_cast<uintptr_t>(c->N1.p)),
         uint64_t(reinterpret_cast<uintptr_t>(c->gram_w.p)), uint64_t(reinterpret_cast<uintptr_t>(c->gram_h.p)),
-        uint64_t(c->sk1.G), uint64_t(c->sk1.tiles), uint64_t(c->sk2.G), uint64_t(c->sk2.tiles)};
+        uint64_t(c->sk1.G), uint64_t(c->sk1.tiles), uint64_t(c->sk2.G), uint64_t(c->sk2.tiles),
+        uint64_t(reinterpret_cast<uintptr_t>(c->chA.seg.p)), uint64_t(reinterpret_cast<uintptr_t>(c->chT.seg.p)),
+        uint64_t(c->chA.C), uint64_t(c->chT.C)};
     oocnmf_ctx::Graph* hit = nullptr;
     for (auto& g : c->graphs)
         if (g.key == key) hit = &g;
@@ -667,6 +731,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     c->launches = 0;
     oocnmf_info inf{};
     prepare_factors(c, cfg);
+    ensure_chunks(c);
     if (!c->norm_valid) compute_norm(c);
     if (c->norm_a2 == 0.0) fail(OOCNMF_ERR_DATA, "nmf: ||A||_F is zero");
     ck(cudaMemsetAsync(c->flag.p, 0, 4, c->stream), "memset flag");
@@ -1555,12 +1620,9 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
             ck(pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s), "wta");
             ck(launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce");
         } else {
-            ck(launch_spmm(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows, c->Ht.as<float>(),
-                           t1.as<float>(), s),
-               "spmm");
-            ck(launch_spmm(kp, c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), c->vT.as<float>(), c->n, c->W.as<float>(),
-                           c->wta(), s),
-               "spmm");
+            ensure_chunks(c);
+            spmm(c, false, c->Ht.as<float>(), t1.as<float>(), s);
+            spmm(c, true, c->W.as<float>(), c->wta(), s);
         }
         gram_h(c);
         ck(launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, 0.f, false,

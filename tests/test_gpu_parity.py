@@ -152,6 +152,31 @@ def test_csr_matches_reference(gpu):
     check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
 
 
+@pytest.mark.parametrize("chunk_mb", ["0.01", "0.003"])
+def test_csr_column_chunked_spmm_matches_reference(gpu, monkeypatch, chunk_mb):
+    """The L2 column-chunked SpMM (launch_spmm_seg; on by default for operands >> L2) forced on
+    a small case: ~6 and ~20 chunks per pass, ragged last chunk, against the reference golden."""
+    monkeypatch.setenv("OOCNMF_SPMM_CHUNK_MB", chunk_mb)
+    monkeypatch.setenv("OOCNMF_SPMM_CHUNK_FORCE", "1")
+    g = _golden("csr_3000x2500_d001_k16")
+    m, n = g["shape"].tolist()
+    a = nmf.CsrMatrix(m, n, g["rp"], g["ci"], g["v"])
+    w0, h0 = port.init_factors(m, n, 16, 0)
+    cfg = nmf.NmfConfig(k=16, max_iters=40, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    res = nmf.nmf_serial(a, cfg)
+    check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
+    # products through the chunked passes vs f64 on the same factors
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, 16)
+        ctx.load_csr(a)
+        ctx.set_factors(f32(w0), f32(h0))
+        aht, wta, _, _ = ctx.products()
+    d = a.to_dense()
+    np.testing.assert_allclose(aht, d @ f32(h0).T, rtol=2e-5, atol=1e-6)
+    np.testing.assert_allclose(wta, f32(w0).T @ d, rtol=2e-5, atol=1e-6)
+
+
 def test_device_sparse_generator_is_reference_generator(gpu):
     m, n, dens, seed = 900, 1100, 0.01, 7
     rp, ci, v, _ = port.gen_sparse(m, n, dens, seed)
