@@ -9,7 +9,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "liboocnmf_b200.so")
+# (OOCNMF_LIB_PATH: developer A/B of two builds of the same library on one box)
+LIB_PATH = os.environ.get("OOCNMF_LIB_PATH") or os.path.join(_HERE, "lib", "liboocnmf_b200.so")
 
 u64 = C.c_uint64
 i32 = C.c_int32

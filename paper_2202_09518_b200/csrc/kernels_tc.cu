@@ -164,11 +164,34 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
-// tf32_lo(x) as the MMA will read it: adding half a tf32 ulp to the bits of the remainder
-// and letting the tensor core's truncation drop the low 13 bits is round-to-nearest (ties
-// away), one integer add instead of cvt.rna on the split warps' critical path.
-__device__ __forceinline__ uint32_t lo_bits(float x) {
-    return __float_as_uint(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)) + 0x1000u;
+// (a0, a1) += (b0, b1) as one packed FADD2 (sm_100 f32x2): two IEEE round-to-nearest adds,
+// bit-identical to the scalar pair at half the issue slots (the split and drain warps'
+// adds are ~20% of the pass's instructions, and under the power cap issue costs clock)
+__device__ __forceinline__ void add2(float& a0, float& a1, float b0, float b1) {
+    asm("{\n.reg .b64 ra, rb;\nmov.b64 ra, {%0, %1};\nmov.b64 rb, {%2, %3};\n"
+        "add.rn.f32x2 ra, ra, rb;\nmov.b64 {%0, %1}, ra;\n}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(b0), "f"(b1));
+}
+// tf32_lo(x) of two values as the MMA will read them: adding half a tf32 ulp to the bits of
+// the remainder x - trunc(x) and letting the tensor core's truncation drop the low 13 bits is
+// round-to-nearest (ties away) — one integer add instead of cvt.rna (a 4-instruction
+// emulation) — and the two remainders come from one FADD2.
+__device__ __forceinline__ void lo_bits2(float x0, float x1, uint32_t& r0, uint32_t& r1) {
+    float d0 = x0, d1 = x1;
+    add2(d0, d1, -__uint_as_float(__float_as_uint(x0) & 0xFFFFE000u), -__uint_as_float(__float_as_uint(x1) & 0xFFFFE000u));
+    r0 = __float_as_uint(d0) + 0x1000u;
+    r1 = __float_as_uint(d1) + 0x1000u;
+}
+// acc[j] += a[j] + b[j] for an even-length run, in pairs
+template <int N>
+__device__ __forceinline__ void acc_add2(float* acc, const uint32_t* a, const uint32_t* b) {
+#pragma unroll
+    for (int j = 0; j < N; j += 2) {
+        float s0 = __uint_as_float(a[j]), s1 = __uint_as_float(a[j + 1]);
+        add2(s0, s1, __uint_as_float(b[j]), __uint_as_float(b[j + 1]));
+        add2(acc[j], acc[j + 1], s0, s1);
+    }
 }
 
 // ------------------------------------------------------------------ kernel
@@ -398,8 +421,8 @@ __global__ void __launch_bounds__(512, 1)
                         const float4 v = row[c ^ (t & 7)];
                         x[4 * c] = __float_as_uint(v.x), x[4 * c + 1] = __float_as_uint(v.y),
                         x[4 * c + 2] = __float_as_uint(v.z), x[4 * c + 3] = __float_as_uint(v.w);
-                        r[4 * c] = lo_bits(v.x), r[4 * c + 1] = lo_bits(v.y), r[4 * c + 2] = lo_bits(v.z),
-                        r[4 * c + 3] = lo_bits(v.w);
+                        lo_bits2(v.x, v.y, r[4 * c], r[4 * c + 1]);
+                        lo_bits2(v.z, v.w, r[4 * c + 2], r[4 * c + 3]);
                     }
                 } else {
                     // column t of the MN-major BASE32B tile (atom t/32, element e = t%32), rows
@@ -407,11 +430,12 @@ __global__ void __launch_bounds__(512, 1)
                     const float* atom = reinterpret_cast<const float*>(sA + (t >> 5) * C::ATOM_STRIDE);
                     const int e = t & 31;
 #pragma unroll
-                    for (int kr = 0; kr < 32; ++kr) {
+                    for (int kr = 0; kr < 32; kr += 2) {
                         const int k = 32 * h + kr;
-                        const float v = atom[k * 32 + (((e >> 3) ^ (k & 3)) << 3) + (e & 7)];
-                        x[kr] = __float_as_uint(v);
-                        r[kr] = lo_bits(v);
+                        const float v0 = atom[k * 32 + (((e >> 3) ^ (k & 3)) << 3) + (e & 7)];
+                        const float v1 = atom[(k + 1) * 32 + (((e >> 3) ^ ((k + 1) & 3)) << 3) + (e & 7)];
+                        x[kr] = __float_as_uint(v0), x[kr + 1] = __float_as_uint(v1);
+                        lo_bits2(v0, v1, r[kr], r[kr + 1]);
                     }
                 }
                 tmem_st32(dst + 32 * h, x);         // A_hi: raw bits, the MMA truncates to tf32
@@ -443,15 +467,14 @@ __global__ void __launch_bounds__(512, 1)
             if constexpr (KP == 16) {
                 uint32_t v[32];  // D' = [hi(16) | lo(16)] in one 32-column load
                 tmem_ld32(src, v);
-#pragma unroll
-                for (int j = 0; j < 16; ++j) acc[j] += __uint_as_float(v[j]) + __uint_as_float(v[16 + j]);
+                acc_add2<16>(acc, v, v + 16);
             } else if constexpr (C::SEP) {  // one chain's kp columns
 #pragma unroll
                 for (int h = 0; h < KP / 32; ++h) {
                     uint32_t v[32];
                     tmem_ld32(src + h * 32, v);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) acc[32 * h + j] += __uint_as_float(v[j]);
+                    for (int j = 0; j < 32; j += 2) add2(acc[32 * h + j], acc[32 * h + j + 1], __uint_as_float(v[j]), __uint_as_float(v[j + 1]));
                 }
             } else {  // D' = [H | L]
 #pragma unroll
@@ -459,8 +482,7 @@ __global__ void __launch_bounds__(512, 1)
                     uint32_t hi[32], lo[32];
                     tmem_ld32(src + h * 32, hi);
                     tmem_ld32(src + KP + h * 32, lo);
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) acc[32 * h + j] += __uint_as_float(hi[j]) + __uint_as_float(lo[j]);
+                    acc_add2<32>(acc + 32 * h, hi, lo);
                 }
             }
         };
