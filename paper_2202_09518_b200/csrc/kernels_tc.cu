@@ -15,11 +15,12 @@
 // Numerics (tools/bias_probe.py, signed mean relative error of A·Ht vs f64): the tensor
 // core's f32 accumulation truncates once per MMA, so one TMEM accumulator carried through a
 // tile's whole K range biased the products by -1e-5..-4e-5 — enough to drift low-rank
-// trajectories past the 1e-4 parity bar. The hi chain therefore restarts every K step (64,
-// 8 MMAs) in a fresh TMEM buffer that drain warps add into round-to-nearest f32 register
+// trajectories past the 1e-4 parity bar. The hi chain therefore restarts every two K steps
+// (128, 16 MMAs) in a fresh TMEM buffer that drain warps add into round-to-nearest f32 register
 // sums (kp = 64: the lo chain, values ~2^-11 of H so its own truncation is negligible,
-// restarts every LO_UNITS steps). The remaining bias is a constant ~-3e-7 for any K (FFMA path: unbiased,
-// rms 5e-8..1.3e-7); OOCNMF_TC_DRAIN=n lengthens the hi chain to n steps (developer knob).
+// restarts every LO_UNITS steps). The remaining bias is a constant ~-6e-7 for any K with the
+// default 2-step chains (~-3e-7 with 1; FFMA path: unbiased, rms 5e-8..1.3e-7);
+// OOCNMF_TC_DRAIN=n sets the hi chain to n steps (developer knob).
 //
 // Pipeline (one persistent CTA per SM, 16 warps, stream-K split as the FFMA path):
 //   warp 0       TMA producer: A ring (32 KB stages, freed by the split warps as soon as the
@@ -606,11 +607,14 @@ cudaError_t make_map(CUtensorMap* m, const float* base, int64_t rows, int64_t co
 }
 
 // K steps (64 each) per TMEM accumulation chain; OOCNMF_TC_DRAIN overrides (developer knob).
+// 2 steps (16 MMAs, 128 deep): signed bias ≈ -6e-7 relative (tools/bias_probe.py: 1 step
+// -3e-7, 4 steps -1.3e-6; 8 steps fails the low-rank 1e-4 trajectory test), half the drain
+// work of 1 step — ≈ +3% at config 2 under the power cap.
 int tc_drain_units() {
     static int du = [] {
         const char* e = getenv("OOCNMF_TC_DRAIN");
         const int v = e ? atoi(e) : 0;
-        return v > 0 ? v : 1;
+        return v > 0 ? v : 2;
     }();
     return du;
 }
