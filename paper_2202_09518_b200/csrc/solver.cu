@@ -1032,11 +1032,36 @@ void pack_chunk(const std::vector<Part>& parts, char* slot, int64_t off, int64_t
 
 // Copy-in: consume(dev_slot, off, len) enqueues on c->stream the device work that reads the
 // staged chunk (parts back to back in dev_slot).
+// Small transfers skip the slots (their first use allocates 128 MB of pinned memory, ~50 ms):
+// one device buffer, the driver's pageable copy per part (2-D when strided).
+bool direct_transfer(oocnmf_ctx* c, size_t bytes) {
+    return bytes <= (size_t(4) << 20) || (!c->stage_pin && bytes <= (size_t(64) << 20));
+}
+
 template <class Consume>
 void copy_in(oocnmf_ctx* c, const std::vector<Part>& parts, int64_t count, Consume&& consume) {
     if (count <= 0) return;
     size_t unit = 0;
     for (const Part& p : parts) unit += p.elem;
+    if (direct_transfer(c, size_t(count) * unit)) {
+        DevBuf tmp;
+        tmp.alloc(size_t(count) * unit, "copy-in");
+        size_t at = 0;
+        for (const Part& p : parts) {
+            if (p.stride == p.elem)
+                ck(cudaMemcpyAsync(tmp.as<char>() + at, p.host, size_t(count) * p.elem, cudaMemcpyHostToDevice,
+                                   c->stream),
+                   "H2D");
+            else
+                ck(cudaMemcpy2DAsync(tmp.as<char>() + at, p.elem, p.host, p.stride, p.elem, size_t(count),
+                                     cudaMemcpyHostToDevice, c->stream),
+                   "H2D");
+            at += size_t(count) * p.elem;
+        }
+        consume(tmp.as<char>(), int64_t(0), count);
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        return;
+    }
     const size_t slot = stage_slot_bytes(c, unit);
     const int64_t chunk = std::max<int64_t>(1, int64_t(slot / unit));
     double t_wait = 0, t_pack = 0;
@@ -1068,6 +1093,25 @@ void copy_out(oocnmf_ctx* c, const std::vector<Part>& parts, int64_t count, Prod
     if (count <= 0) return;
     size_t unit = 0;
     for (const Part& p : parts) unit += p.elem;
+    if (direct_transfer(c, size_t(count) * unit)) {
+        DevBuf tmp;
+        tmp.alloc(size_t(count) * unit, "copy-out");
+        produce(tmp.as<char>(), int64_t(0), count);
+        size_t at = 0;
+        for (const Part& p : parts) {
+            if (p.stride == p.elem)
+                ck(cudaMemcpyAsync(const_cast<void*>(p.host), tmp.as<char>() + at, size_t(count) * p.elem,
+                                   cudaMemcpyDeviceToHost, c->stream),
+                   "D2H");
+            else
+                ck(cudaMemcpy2DAsync(const_cast<void*>(p.host), p.stride, tmp.as<char>() + at, p.elem, p.elem,
+                                     size_t(count), cudaMemcpyDeviceToHost, c->stream),
+                   "D2H");
+            at += size_t(count) * p.elem;
+        }
+        ck(cudaStreamSynchronize(c->stream), "sync");
+        return;
+    }
     const size_t slot = stage_slot_bytes(c, unit);
     const int64_t chunk = std::max<int64_t>(1, int64_t(slot / unit));
     const int64_t nchunks = (count + chunk - 1) / chunk;
@@ -1779,6 +1823,8 @@ int oocnmf_allreduce_sum_f64(oocnmf_ctx* c, double* buf, uint64_t count) {
 static int one_shot(int device, uint64_t m, uint64_t n, const oocnmf_config* cfg, const double* w0, const double* h0,
                     double* w_out, double* h_out, uint64_t* ti, double* te, uint64_t cap, oocnmf_info* info,
                     int (*load)(oocnmf_ctx*, const void*), const void* src) {
+    double tp[6];
+    tp[0] = io_clock();
     oocnmf_ctx* c = nullptr;
     int st = oocnmf_ctx_create(device, &c);
     if (st) return st;
@@ -1788,6 +1834,7 @@ static int one_shot(int device, uint64_t m, uint64_t n, const oocnmf_config* cfg
         return OOCNMF_ERR_SHAPE;
     }
     st = oocnmf_set_problem(c, m, n, cfg->k, 0, m);
+    tp[1] = io_clock();
     if (!st) st = load(c, src);
     if (!st && cfg->init == 1) {
         if (!w0 || !h0) {
@@ -1797,11 +1844,19 @@ static int one_shot(int device, uint64_t m, uint64_t n, const oocnmf_config* cfg
             st = oocnmf_set_factors_f64(c, w0, h0);
         }
     }
+    tp[2] = io_clock();
     if (!st) st = oocnmf_solve(c, cfg, ti, te, cap, info);
+    tp[3] = io_clock();
     if (!st) st = oocnmf_get_factors_f64(c, w_out, h_out);
+    tp[4] = io_clock();
     const std::string keep = g_err;
     oocnmf_ctx_destroy(c);
     g_err = keep;
+    tp[5] = io_clock();
+    if (io_profile())
+        std::fprintf(stderr, "[oocnmf io] one-shot: create+problem %.1f ms, load %.1f ms, solve %.1f ms, "
+                     "factors out %.1f ms, destroy %.1f ms\n", (tp[1] - tp[0]) * 1e3, (tp[2] - tp[1]) * 1e3,
+                     (tp[3] - tp[2]) * 1e3, (tp[4] - tp[3]) * 1e3, (tp[5] - tp[4]) * 1e3);
     return st;
 }
 
