@@ -949,9 +949,16 @@ struct Part {
 
 constexpr size_t kStageSlot = size_t(64) << 20;
 
+// OOCNMF_STAGE_SLOT_KB: smaller slots (tests drive the multi-chunk pipeline at small sizes)
+size_t stage_slot_target() {
+    const char* e = std::getenv("OOCNMF_STAGE_SLOT_KB");
+    const long long kb = e ? std::atoll(e) : 0;
+    return kb > 0 ? size_t(kb) << 10 : kStageSlot;
+}
+
 size_t stage_slot_bytes(oocnmf_ctx* c, size_t unit) {
-    const size_t want = std::max(kStageSlot, unit);
-    if (!c->stage_pin || c->stage_dev.bytes < 2 * want) {
+    const size_t want = std::max(stage_slot_target(), unit);
+    if (!c->stage_pin || c->stage_dev.bytes != 2 * want) {
         if (c->stage_pin) cudaFreeHost(c->stage_pin), c->stage_pin = nullptr;
         ck(cudaMallocHost(&c->stage_pin, 2 * want), "cudaMallocHost (staging)");
         c->stage_dev.alloc(2 * want, "staging");
@@ -1035,6 +1042,8 @@ void pack_chunk(const std::vector<Part>& parts, char* slot, int64_t off, int64_t
 // Small transfers skip the slots (their first use allocates 128 MB of pinned memory, ~50 ms):
 // one device buffer, the driver's pageable copy per part (2-D when strided).
 bool direct_transfer(oocnmf_ctx* c, size_t bytes) {
+    const char* f = std::getenv("OOCNMF_STAGE_FORCE");  // tests: always take the slots
+    if (f && *f && *f != '0') return false;
     return bytes <= (size_t(4) << 20) || (!c->stage_pin && bytes <= (size_t(64) << 20));
 }
 

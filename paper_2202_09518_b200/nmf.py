@@ -274,12 +274,18 @@ class Context:
         a = np.asarray(a)
         if a.shape != (self.rows, self.n):
             raise ShapeError(f"load_dense: expected {self.rows}x{self.n}, got {a.shape}")
-        if a.dtype == np.float32:
+        if a.dtype not in (np.float32, np.float64):
+            a = a.astype(np.float64)
+        # a row window of a larger array (the reference's MatrixRef window) goes in place, with
+        # its row stride as lda; anything else is made contiguous first
+        it = a.itemsize
+        if not (a.strides[1] == it and a.strides[0] % it == 0 and a.strides[0] >= a.shape[1] * it):
             a = np.ascontiguousarray(a)
-            check(_capi.lib().oocnmf_load_dense_f32(self._h, _p(a, C.c_float), self.n))
+        lda = a.strides[0] // it if a.shape[0] > 1 else self.n
+        if a.dtype == np.float32:
+            check(_capi.lib().oocnmf_load_dense_f32(self._h, C.cast(a.ctypes.data, C.POINTER(C.c_float)), lda))
         else:
-            a = np.ascontiguousarray(a, np.float64)
-            check(_capi.lib().oocnmf_load_dense_f64(self._h, _p(a, C.c_double), self.n))
+            check(_capi.lib().oocnmf_load_dense_f64(self._h, C.cast(a.ctypes.data, C.POINTER(C.c_double)), lda))
 
     def load_dense_device(self, ptr: int, lda: int):
         check(_capi.lib().oocnmf_load_dense_device_f32(self._h, C.c_void_p(ptr), lda))

@@ -406,6 +406,48 @@ def test_csr_upload_checks_run_on_device(gpu):
     assert load([0, 1, 2, 3, 4], [4, 0, 3, 1], [1, 2, 3, 4])[0] == 0
 
 
+@pytest.mark.parametrize("staged", [False, True])
+def test_copy_in_and_out_paths_are_exact(gpu, monkeypatch, staged):
+    """Every pageable copy-in / copy-out call of the C-ABI through both transfer paths: direct
+    pageable copies, and the pipelined pinned slots (forced, 64 KB slots -> many chunks, with
+    row windows of larger arrays as strided sources)."""
+    if staged:
+        monkeypatch.setenv("OOCNMF_STAGE_FORCE", "1")
+        monkeypatch.setenv("OOCNMF_STAGE_SLOT_KB", "64")
+    m, n, k = 700, 530, 12
+    rng = np.random.default_rng(3)
+    big64 = rng.random((m, n + 9))
+    win64 = big64[:, 4:4 + n]  # row stride n + 9: the reference's MatrixRef window
+    big32 = rng.random((m, n + 5)).astype(np.float32)
+    win32 = big32[:, :n]
+    w, h = rng.random((m, k)), rng.random((k, n))
+    r32 = lambda x: np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.load_dense(win64)
+        assert np.array_equal(ctx.download_dense(), win64.astype(np.float32))
+        ctx.load_dense(win32)
+        assert np.array_equal(ctx.download_dense(), win32)
+        ctx.set_factors(w, h)
+        w2, h2 = ctx.get_factors()
+        assert np.array_equal(w2, r32(w)) and np.array_equal(h2, r32(h))
+        assert np.array_equal(ctx.gather_w(), r32(w))
+    with nmf.Context(gpu) as ctx:  # column slab: H lands at its columns of the full width
+        ctx.set_problem_cols(m, n + 40, k, 25, n)
+        ctx.load_dense(win32)
+        ctx.set_factors(w, h)
+        hf = ctx.gather_h()
+        assert np.array_equal(hf[:, 25:25 + n], r32(h)) and not hf[:, :25].any() and not hf[:, 25 + n:].any()
+    d = np.where(rng.random((m, n)) < 0.03, rng.random((m, n)), 0.0)
+    a = nmf.CsrMatrix.from_dense(d)
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.load_csr(a)
+        b = ctx.download_csr()
+    assert np.array_equal(b.row_ptr, a.row_ptr) and np.array_equal(b.col_idx, a.col_idx)
+    assert np.array_equal(b.values, r32(a.values))
+
+
 def test_csr_upload_spanning_many_staging_chunks(gpu):
     """> 2 staging chunks (4 Mi entries each) through the pipelined upload, bit-exact back."""
     m, n = 20000, 4000
