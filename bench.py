@@ -31,6 +31,27 @@ sys.path.insert(0, ROOT)
 CPU_CORES = os.cpu_count() or 1
 os.environ.setdefault("OMP_NUM_THREADS", str(CPU_CORES))
 
+# stdout carries exactly the one JSON line: native libraries (NCCL's version banner, ...) write
+# to file descriptor 1 directly, so fd 1 is pointed at stderr and the line goes to a saved copy
+_JSON_FD = None
+
+
+def emit(obj):
+    global _JSON_FD
+    line = (json.dumps(obj) + "\n").encode()
+    if _JSON_FD is None:
+        sys.stdout.write(line.decode())
+        sys.stdout.flush()
+    else:
+        os.write(_JSON_FD, line)
+
+
+def _quiet_stdout():
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
 
 def parse():
     p = argparse.ArgumentParser()
@@ -315,7 +336,7 @@ def bench_select(args, nmf, np, torch, ctx, comm, rank, world, local, barrier, m
                "clocks": clk.summary(), "sweep_s": sweep_s, "chosen_k": rep.chosen_k,
                "records": [[r.k, r.runs_used, round(r.min_silhouette, 4), round(r.mean_relative_error, 6),
                             r.iterations] for r in rep.records]}
-        print(json.dumps(out))
+        emit(out)
     if comm:
         comm.close()
 
@@ -332,20 +353,20 @@ def main():
             return
         m, n = args.m or 65536, args.n
         if args.workload != "dense":
-            print(json.dumps({"impl": "reference", "unavailable": f"--impl reference implemented for the "
-                                                                  f"default (dense) workload only"}))
+            emit({"impl": "reference", "unavailable": f"--impl reference implemented for the "
+                                                                  f"default (dense) workload only"})
             return
         rate, cb = cpu_reference_dense(m, n, k, args.cpu_seconds, steps=K, warmup=W)
         cb["sample"] = cb["sample"].replace("MU iterations", f"timed MU iterations after {W} warm-up")
         workload = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
-        print(json.dumps({"impl": "reference", "metric": f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, "
+        emit({"impl": "reference", "metric": f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, "
                                                          f"NCCL all-reduce)",
                           "value": rate, "unit": "it/s", "n_gpus": args.gpus,
                           "steps": K, "warmup": W, "ms_per_step": 1e3 / rate, "higher_is_better": True,
                           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                           "config": {"workload": workload, "m": m, "n": n, "k": k, "parallelism": "host cores"},
                           "cpu_baseline": cb,
-                          "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+                          "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
         return
 
     import numpy as np
@@ -559,7 +580,7 @@ def main():
                "phase_ms_per_step": {p_: info[p_ + "_s"] * 1e3 / K for p_ in
                                      ("w_update", "h_update", "allreduce", "error_check")}}
         out.update({k_: v for k_, v in extra.items() if v is not None})
-        print(json.dumps(out))
+        emit(out)
     if host_buf is not None:
         ctx.close()
         nmf._capi.lib().oocnmf_host_unregister(host_buf.ctypes.data)
@@ -571,4 +592,5 @@ def main():
 
 
 if __name__ == "__main__":
+    _quiet_stdout()
     main()

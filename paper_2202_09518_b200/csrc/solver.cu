@@ -116,6 +116,13 @@ struct oocnmf_ctx {
     int device = 0, rank = 0, nranks = 1, num_sms = 148;
     ncclComm_t comm = nullptr;
     cudaStream_t stream = nullptr, copy_stream = nullptr;
+    // sharded CSR H update: the reduce-scatter of W^T A runs chunk by chunk on comm_stream
+    // (high priority) while the SpMM computes the next chunk (see spmm_wta_reduce_scatter)
+    cudaStream_t comm_stream = nullptr;
+    static constexpr int kMaxRsChunks = 16;
+    cudaEvent_t ev_rs[kMaxRsChunks + 1] = {};
+    DevBuf wtp;                  // W^T A in chunk-major order [chunk][rank][rows][kp] (send side)
+    bool rs_done = false;        // this iteration's reduce-scatter was issued with the SpMM
 
     uint64_t m = 0, n = 0, k = 0, row0 = 0, rows = 0;
     // Column partition (CNMF, src/nmf_distributed.cpp:112-149): this rank owns all m rows and
@@ -410,6 +417,51 @@ void record(oocnmf_ctx* c, cudaEvent_t e, cudaStream_t s) {
     ck(c->capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s), "event");
 }
 
+// Sharded CSR H update, compute/communication overlap: rank r's rows of W^T A are
+// [r hr, (r+1) hr). The SpMM A^T W runs in S row chunks; chunk c covers sub-range c of every
+// rank's segment and is written in chunk-major order ([rank][rows][kp] contiguous), so it is
+// exactly one ncclReduceScatter's send buffer. Each chunk's reduce-scatter is issued on the
+// high-priority comm stream as soon as its SpMM launches retire, landing in this rank's rows of
+// W^T A while the SpMM computes the next chunk; only the last chunk's transfer is exposed.
+// OOCNMF_RS_CHUNKS sets S (default 4; 1 = the unoverlapped reduce-scatter in h_update).
+int rs_chunks(oocnmf_ctx* c) {
+    static const int S = [] {
+        const char* e = std::getenv("OOCNMF_RS_CHUNKS");
+        const int v = e ? std::atoi(e) : 4;
+        return std::clamp(v, 1, int(oocnmf_ctx::kMaxRsChunks));
+    }();
+    return c->shard_h() && c->chT.C <= 1 ? int(std::min<int64_t>(S, c->h_rows())) : 1;
+}
+
+void spmm_wta_reduce_scatter(oocnmf_ctx* c, cudaStream_t s) {
+    const int kp = c->kp, N = c->nranks, S = rs_chunks(c);
+    const int64_t hr = c->h_rows(), h0 = c->h_row0(), n = int64_t(c->n);
+    if (c->wtp.bytes != size_t(c->np) * kp * 4) {
+        c->wtp.alloc(size_t(c->np) * kp * 4, "W^T A (chunk-major)");
+        ck(cudaMemsetAsync(c->wtp.p, 0, c->wtp.bytes, s), "memset");  // padding rows stay 0
+    }
+    float* wtp = c->wtp.as<float>();
+    const int64_t* rpT = c->rpT.as<int64_t>();
+    for (int ch = 0; ch < S; ++ch) {
+        const int64_t r0 = hr * ch / S, r1 = hr * (ch + 1) / S, len = r1 - r0;
+        float* base = wtp + size_t(N) * r0 * kp;
+        for (int r = 0; r < N; ++r) {
+            const int64_t g0 = int64_t(r) * hr + r0, g1 = std::min(int64_t(r) * hr + r1, n);
+            if (g1 > g0)
+                count(c, launch_spmm(kp, rpT + g0, c->ciT.as<int32_t>(), c->vT.as<float>(), g1 - g0,
+                                     c->W.as<float>(), base + size_t(r) * len * kp, s),
+                      "spmm At W (chunk)");
+        }
+        ck(cudaEventRecord(c->ev_rs[ch], s), "event");
+        ck(cudaStreamWaitEvent(c->comm_stream, c->ev_rs[ch], 0), "wait");
+        nck(ncclReduceScatter(base, c->wta() + size_t(h0 + r0) * kp, size_t(len) * kp, ncclFloat, ncclSum, c->comm,
+                              c->comm_stream),
+            "reduce-scatter WtA (chunk)");
+    }
+    ck(cudaEventRecord(c->ev_rs[oocnmf_ctx::kMaxRsChunks], c->comm_stream), "event");
+    c->rs_done = true;
+}
+
 // W update + accumulation of the rank-local [W^T A | W^T W] into c->packed.
 void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     const int kp = c->kp;
@@ -462,7 +514,10 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
               "W update");
         count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
-        spmm(c, true, c->W.as<float>(), c->wta(), s);
+        if (rs_chunks(c) > 1)
+            spmm_wta_reduce_scatter(c, s);
+        else
+            spmm(c, true, c->W.as<float>(), c->wta(), s);
         rec(eWta);
         rec(eReduced);
     } else {
@@ -510,12 +565,16 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     cudaStream_t s = c->stream;
     const int64_t hr = c->h_rows(), h0 = c->h_row0();
     if (c->shard_h()) {
-        // reduce-scatter W^T A (each rank keeps its n/N rows, in place) + the small Grams
+        // reduce-scatter W^T A (each rank keeps its n/N rows, in place) + the small Grams; with
+        // the overlapped SpMM the scatter is already on the comm stream
         const size_t slice = size_t(hr) * kp;
         float* wta = c->wta();
+        if (c->rs_done) ck(cudaStreamWaitEvent(s, c->ev_rs[oocnmf_ctx::kMaxRsChunks], 0), "wait reduce-scatter");
         nck(ncclGroupStart(), "ncclGroupStart");
-        nck(ncclReduceScatter(wta, wta + size_t(c->rank) * slice, slice, ncclFloat, ncclSum, c->comm, s),
-            "reduce-scatter WtA");
+        if (!c->rs_done)
+            nck(ncclReduceScatter(wta, wta + size_t(c->rank) * slice, slice, ncclFloat, ncclSum, c->comm, s),
+                "reduce-scatter WtA");
+        c->rs_done = false;
         nck(ncclAllReduce(c->wtw(), c->wtw(), size_t(kp) * kp, ncclFloat, ncclSum, c->comm, s), "allreduce WtW");
         nck(ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
             "allreduce WtW64");
@@ -1270,6 +1329,10 @@ static void ctx_init_common(oocnmf_ctx* c, int device) {
     c->num_sms = prop.multiProcessorCount;
     ck(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "stream");
     ck(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking), "stream");
+    int prio_lo = 0, prio_hi = 0;
+    ck(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi), "stream priorities");
+    ck(cudaStreamCreateWithPriority(&c->comm_stream, cudaStreamNonBlocking, prio_hi), "stream");
+    for (auto& e : c->ev_rs) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     for (int i = 0; i < 2; ++i) {
         ck(cudaEventCreateWithFlags(&c->ev_copied[i], cudaEventDisableTiming), "event");
         ck(cudaEventCreateWithFlags(&c->ev_free[i], cudaEventDisableTiming), "event");
@@ -1328,6 +1391,7 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
         cudaSetDevice(c->device);
         if (c->stream) cudaStreamSynchronize(c->stream);
         if (c->copy_stream) cudaStreamSynchronize(c->copy_stream);
+        if (c->comm_stream) cudaStreamSynchronize(c->comm_stream);
         // the graphs hold NCCL work on c->comm: release them before the communicator
         for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
         c->graphs.clear();
@@ -1343,6 +1407,9 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
             if (e) cudaEventDestroy(e);
         if (c->stream) cudaStreamDestroy(c->stream);
         if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+        if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+        for (auto e : c->ev_rs)
+            if (e) cudaEventDestroy(e);
         delete c;
     });
 }
