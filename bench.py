@@ -533,15 +533,22 @@ def main():
                     ti.ctypes.data_as(C.POINTER(C.c_uint64)), te.ctypes.data_as(C.POINTER(C.c_double)), ti.size,
                     C.byref(inf)))
             else:
+                marks = [time.perf_counter()]
                 ctx.set_problem(m, n, k, r0, rows)
                 if args.workload == "dense":
                     ctx.load_dense(host)
                 else:
                     ctx.load_csr(host)
+                marks.append(time.perf_counter())
                 ctx.solve(ecfg)
+                marks.append(time.perf_counter())
                 ctx.get_factors()
                 if world > 1:
                     ctx.gather_w()
+                marks.append(time.perf_counter())
+                if os.environ.get("BENCH_E2E_DEBUG"):
+                    print(f"[e2e rank {rank}] load {marks[1] - marks[0]:.3f} s, solve {marks[2] - marks[1]:.3f} s, "
+                          f"factors out {marks[3] - marks[2]:.3f} s", file=sys.stderr)
             torch.cuda.synchronize()
             e2e_s = max_over_ranks(time.perf_counter() - t0)
         finally:
