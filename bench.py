@@ -474,11 +474,13 @@ def main():
     ms = max_over_ranks(ev0.elapsed_time(ev1))
     value = K / (ms / 1e3)
 
-    traffic = None
-    if args.workload == "dense" and world == 1 and (m, n, k) == (65536, 65536, 32):
-        prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
-        if os.path.exists(prof):
+    traffic = None  # ncu dram bytes per launch of the dominant kernel, when captured for this config
+    prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
+    if world == 1 and os.path.exists(prof):
+        if args.workload == "dense" and (m, n, k) == (65536, 65536, 32):
             traffic = json.load(open(prof))
+        elif args.workload == "sparse" and (m, n, k) == (1 << 22, 1 << 22, 32) and args.density == 1e-5:
+            traffic = json.load(open(prof)).get("sparse")
     if args.workload == "ooc":
         # host-link roofline: measured pinned H2D bandwidth on this GPU (concurrently on all ranks)
         probe = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
