@@ -545,12 +545,14 @@ def main():
                 ctx.solve(ecfg)
                 marks.append(time.perf_counter())
                 ctx.get_factors()
+                marks.append(time.perf_counter())
                 if world > 1:
                     ctx.gather_w()
                 marks.append(time.perf_counter())
                 if os.environ.get("BENCH_E2E_DEBUG"):
                     print(f"[e2e rank {rank}] load {marks[1] - marks[0]:.3f} s, solve {marks[2] - marks[1]:.3f} s, "
-                          f"factors out {marks[3] - marks[2]:.3f} s", file=sys.stderr)
+                          f"factors {marks[3] - marks[2]:.3f} s, gather W {marks[4] - marks[3]:.3f} s",
+                          file=sys.stderr)
             torch.cuda.synchronize()
             e2e_s = max_over_ranks(time.perf_counter() - t0)
         finally:

@@ -1162,8 +1162,10 @@ void copy_out(oocnmf_ctx* c, const std::vector<Part>& parts, int64_t count, Prod
     size_t unit = 0;
     for (const Part& p : parts) unit += p.elem;
     if (direct_transfer(c, size_t(count) * unit)) {
+        const double t0 = io_clock();
         DevBuf tmp;
         tmp.alloc(size_t(count) * unit, "copy-out");
+        const double t1 = io_clock();
         produce(tmp.as<char>(), int64_t(0), count);
         size_t at = 0;
         for (const Part& p : parts) {
@@ -1178,6 +1180,11 @@ void copy_out(oocnmf_ctx* c, const std::vector<Part>& parts, int64_t count, Prod
             at += size_t(count) * p.elem;
         }
         ck(cudaStreamSynchronize(c->stream), "sync");
+        const double t2 = io_clock();
+        tmp.release();
+        if (io_profile())
+            std::fprintf(stderr, "[oocnmf io] copy_out %.1f MB direct: alloc %.1f ms, produce+D2H %.1f ms, free %.1f ms\n",
+                         double(count) * unit / 1e6, (t1 - t0) * 1e3, (t2 - t1) * 1e3, (io_clock() - t2) * 1e3);
         return;
     }
     const size_t slot = stage_slot_bytes(c, unit);
