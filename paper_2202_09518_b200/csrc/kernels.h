@@ -111,6 +111,11 @@ cudaError_t launch_csr_segments(const int64_t* rp, const int32_t* ci, int64_t ro
 // out (rows x kp) = (or +=, accumulate) the chunk [lo[i], hi[i]) of each row of a CSR · B.
 cudaError_t launch_spmm_seg(int kp, const int64_t* lo, const int64_t* hi, const int32_t* ci, const float* v,
                             int64_t rows, const float* B, float* out, bool accumulate, cudaStream_t s);
+// F[row] <- F * (CSR · B)[row] * rcp_rn(F[row] · G + eps) for rows [0, rows): the SpMM fused with
+// the MU update of the same rows (non-finite results set *flag). The Gram of the new F is left
+// to launch_factor_update(update = false).
+cudaError_t launch_spmm_mu(int kp, const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
+                           const float* B, float* F, const float* G, float eps, int* flag, cudaStream_t s);
 cudaError_t launch_residual_csr(int kp, const int64_t* rp, const int32_t* ci, const float* v,
                                 int64_t rows, int64_t cols, const float* W, const float* Ht,
                                 double* out_slots, cudaStream_t s,

@@ -226,6 +226,80 @@ __device__ double block_sum256(double v) {
     return sh[0];
 }
 
+// k_spmm_v4 fused with the MU update of the same rows (the W update of a local-numerator CSR
+// solve): the row's A·Ht stays in the lane group's registers and becomes the numerator of
+// F[row] <- F * nu * rcp_rn(F·G + eps) (kernels_factor.cu's formula and summation order, so
+// the result is bit-identical to SpMM + k_factor_update), instead of a 537 MB round trip
+// through HBM and a second pass over F. The Gram of the new rows follows in
+// k_factor_update's Gram-only mode.
+template <int KP>
+__global__ void __launch_bounds__(256) k_spmm_mu(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                                                 const float* __restrict__ v, int64_t rows,
+                                                 const float* __restrict__ B, float* __restrict__ F,
+                                                 const float* __restrict__ G, float eps, int* __restrict__ flag) {
+    constexpr int LPR = KP / 4;    // lanes per row
+    constexpr int RPW = 32 / LPR;  // rows per warp
+    __shared__ __align__(16) float Gs[KP * KP];
+    for (int e = threadIdx.x; e < KP * KP; e += blockDim.x) Gs[e] = G[e];
+    __syncthreads();
+    const int lane = threadIdx.x & 31, sub = lane / LPR, l = lane % LPR;
+    const int64_t warps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+    bool bad = false;
+    for (int64_t wg = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; wg * RPW < rows; wg += warps) {
+        const int64_t row = wg * RPW + sub;
+        const bool live = row < rows;
+        const int64_t beg = live ? rp[row] : 0, end = live ? rp[row + 1] : 0;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int64_t p0 = beg; __any_sync(0xffffffffu, p0 < end); p0 += LPR) {
+            const int64_t p = p0 + l;
+            const int col = p < end ? ci[p] : 0;
+            const float val = p < end ? v[p] : 0.f;
+#pragma unroll
+            for (int t = 0; t < LPR; ++t) {
+                const int c = __shfl_sync(0xffffffffu, col, sub * LPR + t);
+                const float w = __shfl_sync(0xffffffffu, val, sub * LPR + t);
+                if (p0 + t < end) {
+                    const float4 b = __ldg(reinterpret_cast<const float4*>(B + int64_t(c) * KP) + l);
+                    acc.x = fmaf(w, b.x, acc.x);
+                    acc.y = fmaf(w, b.y, acc.y);
+                    acc.z = fmaf(w, b.z, acc.z);
+                    acc.w = fmaf(w, b.w, acc.w);
+                }
+            }
+        }
+        // the update: lane l owns columns 4l..4l+3 of the row; F[row][q] comes from lane q/4
+        float4* frow = reinterpret_cast<float4*>(F + (live ? row : 0) * KP);
+        const float4 f = live ? frow[l] : make_float4(0.f, 0.f, 0.f, 0.f);
+        float de0 = 0.f, de1 = 0.f, de2 = 0.f, de3 = 0.f;
+#pragma unroll
+        for (int q4 = 0; q4 < LPR; ++q4) {
+            const float fx = __shfl_sync(0xffffffffu, f.x, sub * LPR + q4);
+            const float fy = __shfl_sync(0xffffffffu, f.y, sub * LPR + q4);
+            const float fz = __shfl_sync(0xffffffffu, f.z, sub * LPR + q4);
+            const float fw = __shfl_sync(0xffffffffu, f.w, sub * LPR + q4);
+            const float fq[4] = {fx, fy, fz, fw};
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+                const float4 g = *reinterpret_cast<const float4*>(Gs + (4 * q4 + qq) * KP + 4 * l);
+                de0 = fmaf(fq[qq], g.x, de0);
+                de1 = fmaf(fq[qq], g.y, de1);
+                de2 = fmaf(fq[qq], g.z, de2);
+                de3 = fmaf(fq[qq], g.w, de3);
+            }
+        }
+        if (live) {
+            float4 nf;
+            nf.x = (f.x * acc.x) * __frcp_rn(de0 + eps);
+            nf.y = (f.y * acc.y) * __frcp_rn(de1 + eps);
+            nf.z = (f.z * acc.z) * __frcp_rn(de2 + eps);
+            nf.w = (f.w * acc.w) * __frcp_rn(de3 + eps);
+            bad |= !isfinite(nf.x) || !isfinite(nf.y) || !isfinite(nf.z) || !isfinite(nf.w);
+            frow[l] = nf;
+        }
+    }
+    if (bad) atomicOr(flag, 1);
+}
+
 // sum over nonzeros of a_ij * (W_i · Ht_j)  (f64) — the cross term of ||A - WH||^2.
 template <int KP>
 __global__ void __launch_bounds__(256) k_cross_csr(const int64_t* __restrict__ rp,
@@ -399,6 +473,20 @@ cudaError_t launch_spmm_seg(int kp, const int64_t* lo, const int64_t* hi, const 
         case 16: k_spmm_seg<16><<<grid, 256, 0, s>>>(lo, hi, ci, v, rows, B, out, acc); break;
         case 32: k_spmm_seg<32><<<grid, 256, 0, s>>>(lo, hi, ci, v, rows, B, out, acc); break;
         case 64: k_spmm_seg<64><<<grid, 256, 0, s>>>(lo, hi, ci, v, rows, B, out, acc); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_spmm_mu(int kp, const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
+                           const float* B, float* F, const float* G, float eps, int* flag, cudaStream_t s) {
+    const int64_t warps = (rows * (kp / 4) + 31) / 32;
+    const unsigned grid = grid_for(warps * 32);
+    switch (kp) {
+        case 8: k_spmm_mu<8><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, F, G, eps, flag); break;
+        case 16: k_spmm_mu<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, F, G, eps, flag); break;
+        case 32: k_spmm_mu<32><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, F, G, eps, flag); break;
+        case 64: k_spmm_mu<64><<<grid, 256, 0, s>>>(rp, ci, v, rows, B, F, G, eps, flag); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

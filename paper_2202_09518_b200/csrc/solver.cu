@@ -417,6 +417,15 @@ void record(oocnmf_ctx* c, cudaEvent_t e, cudaStream_t s) {
     ck(c->capturing ? cudaEventRecordWithFlags(e, s, cudaEventRecordExternal) : cudaEventRecord(e, s), "event");
 }
 
+// CSR W update fused into the A·Ht SpMM (launch_spmm_mu) whenever the numerator is local and
+// one-pass: not under CNMF (A·Ht is all-reduced first) nor with column-chunked SpMM passes.
+// OOCNMF_FUSE_W=0 selects the separate SpMM + factor-update kernels (bit-identical results).
+bool fuse_w_update(const oocnmf_ctx* c) {
+    if (c->kind != Kind::csr || c->cnmf || c->chA.C > 1) return false;
+    const char* e = std::getenv("OOCNMF_FUSE_W");
+    return !(e && *e == '0');
+}
+
 // Sharded CSR H update, compute/communication overlap: rank r's rows of W^T A are
 // [r hr, (r+1) hr). The SpMM A^T W runs in S row chunks; chunk c covers sub-range c of every
 // rank's segment and is written in chunk-major order ([rank][rows][kp] contiguous), so it is
@@ -505,13 +514,24 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         }
         rec(eReduced);
     } else if (c->kind == Kind::csr) {
-        spmm(c, false, c->Ht.as<float>(), c->N1.as<float>(), s);
-        rec(eAht);
-        allreduce_aht(c);
-        count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
-                                      c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
-                                      c->flag.as<int>(), nullptr, s),
-              "W update");
+        if (fuse_w_update(c)) {
+            // A·Ht and the W update in one pass over the rows, then the Gram of the new W
+            count(c, launch_spmm_mu(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows,
+                                    c->Ht.as<float>(), c->W.as<float>(), c->HHt.as<float>(), eps, c->flag.as<int>(), s),
+                  "spmm A Ht + W update");
+            rec(eAht);
+            count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, eps, false,
+                                          c->gram_w.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
+                  "W Gram");
+        } else {
+            spmm(c, false, c->Ht.as<float>(), c->N1.as<float>(), s);
+            rec(eAht);
+            allreduce_aht(c);
+            count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
+                                          c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
+                                          c->flag.as<int>(), nullptr, s),
+                  "W update");
+        }
         count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
         if (rs_chunks(c) > 1)
@@ -726,7 +746,7 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
         uint64_t(reinterpret_cast<uintptr_t>(c->gram_w.p)), uint64_t(reinterpret_cast<uintptr_t>(c->gram_h.p)),
         uint64_t(c->sk1.G), uint64_t(c->sk1.tiles), uint64_t(c->sk2.G), uint64_t(c->sk2.tiles),
         uint64_t(reinterpret_cast<uintptr_t>(c->chA.seg.p)), uint64_t(reinterpret_cast<uintptr_t>(c->chT.seg.p)),
-        uint64_t(c->chA.C), uint64_t(c->chT.C)};
+        uint64_t(c->chA.C), uint64_t(c->chT.C), uint64_t(fuse_w_update(c))};
     oocnmf_ctx::Graph* hit = nullptr;
     for (auto& g : c->graphs)
         if (g.key == key) hit = &g;

@@ -177,6 +177,24 @@ def test_csr_column_chunked_spmm_matches_reference(gpu, monkeypatch, chunk_mb):
     np.testing.assert_allclose(wta, f32(w0).T @ d, rtol=2e-5, atol=1e-6)
 
 
+def test_csr_fused_w_update_is_bit_identical(gpu, monkeypatch):
+    """The CSR W update fused into the A·Ht SpMM (launch_spmm_mu) reproduces the separate
+    SpMM + factor-update kernels bit for bit (same formula and summation order)."""
+    m, n, k = 700, 900, 24
+    rng = np.random.default_rng(11)
+    d = np.where(rng.random((m, n)) < 0.02, rng.random((m, n)), 0.0)
+    d[5:9] = 0.0  # empty rows
+    a = nmf.CsrMatrix.from_dense(d)
+    w0, h0 = port.init_factors(m, n, k, 0)
+    cfg = nmf.NmfConfig(k=k, max_iters=25, error_check_interval=5, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    fused = nmf.nmf_serial(a, cfg)
+    monkeypatch.setenv("OOCNMF_FUSE_W", "0")
+    split = nmf.nmf_serial(a, cfg)
+    assert np.array_equal(fused.w, split.w) and np.array_equal(fused.h, split.h)
+    assert [e for _, e in fused.error_trace] == [e for _, e in split.error_trace]
+
+
 def test_device_sparse_generator_is_reference_generator(gpu):
     m, n, dens, seed = 900, 1100, 0.01, 7
     rp, ci, v, _ = port.gen_sparse(m, n, dens, seed)
