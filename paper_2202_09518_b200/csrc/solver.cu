@@ -123,6 +123,8 @@ struct oocnmf_ctx {
     cudaEvent_t ev_rs[kMaxRsChunks + 1] = {};
     DevBuf wtp;                  // W^T A in chunk-major order [chunk][rank][rows][kp] (send side)
     bool rs_done = false;        // this iteration's reduce-scatter was issued with the SpMM
+    bool no_check_next = false;  // the iteration being enqueued is not followed by an error check
+    bool h_fused = false;        // ... and its H update ran inside the A^T W SpMM
 
     uint64_t m = 0, n = 0, k = 0, row0 = 0, rows = 0;
     // Column partition (CNMF, src/nmf_distributed.cpp:112-149): this rank owns all m rows and
@@ -425,6 +427,15 @@ bool fuse_w_update(const oocnmf_ctx* c) {
     const char* e = std::getenv("OOCNMF_FUSE_W");
     return !(e && *e == '0');
 }
+// The H update fused into the A^T W SpMM likewise, when W^T A needs no collective (one rank,
+// or the replicas of model selection) — on iterations not followed by an error check, whose
+// trace-form cross term <W^T A, H> needs the numerator the fused kernel never stores.
+// OOCNMF_FUSE_H=0 keeps the separate kernels.
+bool fuse_h_update(const oocnmf_ctx* c) {
+    if (c->kind != Kind::csr || c->cnmf || c->collective() || c->chT.C > 1) return false;
+    const char* e = std::getenv("OOCNMF_FUSE_H");
+    return !(e && *e == '0');
+}
 
 // Sharded CSR H update, compute/communication overlap: rank r's rows of W^T A are
 // [r hr, (r+1) hr). The SpMM A^T W runs in S row chunks; chunk c covers sub-range c of every
@@ -534,10 +545,16 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         }
         count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
         rec(eWdone);
-        if (rs_chunks(c) > 1)
+        if (c->no_check_next && fuse_h_update(c)) {
+            count(c, launch_spmm_mu(kp, c->rpT.as<int64_t>(), c->ciT.as<int32_t>(), c->vT.as<float>(), c->n,
+                                    c->W.as<float>(), c->Ht.as<float>(), c->wtw(), eps, c->flag.as<int>(), s),
+                  "spmm At W + H update");
+            c->h_fused = true;
+        } else if (rs_chunks(c) > 1) {
             spmm_wta_reduce_scatter(c, s);
-        else
+        } else {
             spmm(c, true, c->W.as<float>(), c->wta(), s);
+        }
         rec(eWta);
         rec(eReduced);
     } else {
@@ -612,10 +629,17 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     }
     if (timed) record(c, ev[eComm], s);
     float* hcat = htlo(c);
-    count(c, launch_factor_update(kp, c->Ht.as<float>() + h0 * kp, hr, c->wta() + h0 * kp, nullptr, nullptr,
-                                  c->wtw(), eps, true, c->gram_h.as<double>(), c->err_slots.as<double>(),
-                                  c->flag.as<int>(), hcat ? hcat + h0 * 2 * kp : nullptr, s),
-          "H update");
+    if (c->h_fused) {  // updated inside the SpMM: the Gram of the new rows only
+        count(c, launch_factor_update(kp, c->Ht.as<float>(), hr, nullptr, nullptr, nullptr, nullptr, eps, false,
+                                      c->gram_h.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
+              "H Gram");
+        c->h_fused = false;
+    } else {
+        count(c, launch_factor_update(kp, c->Ht.as<float>() + h0 * kp, hr, c->wta() + h0 * kp, nullptr, nullptr,
+                                      c->wtw(), eps, true, c->gram_h.as<double>(), c->err_slots.as<double>(),
+                                      c->flag.as<int>(), hcat ? hcat + h0 * 2 * kp : nullptr, s),
+              "H update");
+    }
     if (c->shard_h())
         nck(ncclAllGather(c->Ht.as<float>() + h0 * kp, c->Ht.p, size_t(hr) * kp, ncclFloat, c->comm, s),
             "all-gather H");
@@ -723,9 +747,11 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
     }();
     auto eager = [&] {
         for (uint64_t i = 0; i < count; ++i) {
+            c->no_check_next = i + 1 < count;  // a block's last iteration precedes its error check
             w_update_and_wta(c, eps, true, ev + kEvPerIter * i);
             h_update(c, eps, true, ev + kEvPerIter * i);
         }
+        c->no_check_next = false;
     };
     // Graphs for single-rank solves only: replaying NCCL work from graphs made every launch
     // pay NCCL's graph/non-graph mixing synchronisation (4 x B200: 555 it/s with graphs, 634
@@ -746,7 +772,7 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
         uint64_t(reinterpret_cast<uintptr_t>(c->gram_w.p)), uint64_t(reinterpret_cast<uintptr_t>(c->gram_h.p)),
         uint64_t(c->sk1.G), uint64_t(c->sk1.tiles), uint64_t(c->sk2.G), uint64_t(c->sk2.tiles),
         uint64_t(reinterpret_cast<uintptr_t>(c->chA.seg.p)), uint64_t(reinterpret_cast<uintptr_t>(c->chT.seg.p)),
-        uint64_t(c->chA.C), uint64_t(c->chT.C), uint64_t(fuse_w_update(c))};
+        uint64_t(c->chA.C), uint64_t(c->chT.C), uint64_t(fuse_w_update(c)), uint64_t(fuse_h_update(c))};
     oocnmf_ctx::Graph* hit = nullptr;
     for (auto& g : c->graphs)
         if (g.key == key) hit = &g;

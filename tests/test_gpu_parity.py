@@ -177,9 +177,10 @@ def test_csr_column_chunked_spmm_matches_reference(gpu, monkeypatch, chunk_mb):
     np.testing.assert_allclose(wta, f32(w0).T @ d, rtol=2e-5, atol=1e-6)
 
 
-def test_csr_fused_w_update_is_bit_identical(gpu, monkeypatch):
-    """The CSR W update fused into the A·Ht SpMM (launch_spmm_mu) reproduces the separate
-    SpMM + factor-update kernels bit for bit (same formula and summation order)."""
+def test_csr_fused_updates_are_bit_identical(gpu, monkeypatch):
+    """The CSR W update fused into the A·Ht SpMM and the H update fused into the A^T·W SpMM
+    (launch_spmm_mu; H only on iterations without an error check) reproduce the separate SpMM +
+    factor-update kernels bit for bit (same formula and summation order)."""
     m, n, k = 700, 900, 24
     rng = np.random.default_rng(11)
     d = np.where(rng.random((m, n)) < 0.02, rng.random((m, n)), 0.0)
@@ -190,6 +191,7 @@ def test_csr_fused_w_update_is_bit_identical(gpu, monkeypatch):
                         init_w=f32(w0), init_h=f32(h0))
     fused = nmf.nmf_serial(a, cfg)
     monkeypatch.setenv("OOCNMF_FUSE_W", "0")
+    monkeypatch.setenv("OOCNMF_FUSE_H", "0")
     split = nmf.nmf_serial(a, cfg)
     assert np.array_equal(fused.w, split.w) and np.array_equal(fused.h, split.h)
     assert [e for _, e in fused.error_trace] == [e for _, e in split.error_trace]
