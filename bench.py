@@ -506,8 +506,9 @@ def main():
     else:
         roof = roofline(info, bytes_per_launch, hbm, peak_src, traffic)
         if args.workload == "sparse" and world == 1:
-            roof["note"] = ("aht_pass is k_spmm_mu: the A.H^T SpMM with the W update fused into it (the "
-                            "algorithmic bytes count the SpMM only); wta_pass is the plain A^T.W SpMM")
+            roof["note"] = ("both passes are k_spmm_mu launches: the SpMM with the factor update fused into it "
+                            "(A.H^T + W update; A^T.W + H update except on error-check iterations); the "
+                            "algorithmic bytes count the SpMM only")
     extra["a_pass_gbs_total"] = sum_over_ranks(2 * rows * n * 4 * value / 1e9) if args.workload == "dense" else None
 
     # ------------------------------------------------------------------ e2e through the public API
