@@ -1,3 +1,5 @@
+"""Developer probe: pageable (fresh / touched) vs pinned 16 MB device-to-host copies in every rank at
+once (torchrun --nproc-per-node N tools/d2h_probe.py) — sizing the direct copy-out path."""
 import os, time, numpy as np, torch, torch.distributed as dist
 r = int(os.environ.get("LOCAL_RANK", 0)); torch.cuda.set_device(r)
 dist.init_process_group("gloo")

@@ -1,3 +1,5 @@
+"""Developer probe: phases of the config-3 end-to-end call (CSR generation, download, set_problem,
+load_csr, solve, get_factors) — run with PYTHONPATH=. and OOCNMF_PROFILE_IO=1."""
 import time, numpy as np, torch
 import paper_2202_09518_b200 as nmf
 m=n=4194304; k=32
