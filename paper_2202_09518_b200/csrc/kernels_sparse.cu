@@ -231,9 +231,10 @@ __device__ double block_sum256(double v) {
 // F[row] <- F * nu * rcp_rn(F·G + eps) (kernels_factor.cu's formula and summation order, so
 // the result is bit-identical to SpMM + k_factor_update), instead of a 537 MB round trip
 // through HBM and a second pass over F. The Gram of the new rows follows in
-// k_factor_update's Gram-only mode.
+// k_factor_update's Gram-only mode. Bounded to 48 registers: 5 resident CTAs per SM like the
+// plain SpMM (54 registers / 4 CTAs cost 0.1 ms per pass at config 3).
 template <int KP>
-__global__ void __launch_bounds__(256) k_spmm_mu(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
+__global__ void __launch_bounds__(256, 5) k_spmm_mu(const int64_t* __restrict__ rp, const int32_t* __restrict__ ci,
                                                  const float* __restrict__ v, int64_t rows,
                                                  const float* __restrict__ B, float* __restrict__ F,
                                                  const float* __restrict__ G, float eps, int* __restrict__ flag) {
