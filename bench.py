@@ -93,25 +93,68 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """Clock / throttle sampling during the timed region (B200_PROFILING.md clocks line).
+
+    NVML is polled in-process every ~2 ms from a thread (ctypes releases the GIL while the solve
+    runs), so even a ~70 ms timed region (config 2 at N=4) gets samples; only samples taken
+    after ``__enter__`` returns count. Falls back to ``nvidia-smi -lms 100`` without pynvml."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksEventReason{HwSlowdown,HwThermalSlowdown,SwThermalSlowdown,SwPowerCap}
 
     def __init__(self, index):
         self.index = str(index)
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.samples = []  # (t, sm_mhz, max_mhz, power_w, reasons bitmask)
+        self.stop = threading.Event()
+        self.t_begin = None
+
+    def _nvml_handle(self, pynvml):
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "").strip()
+        ent = [x.strip() for x in vis.split(",") if x.strip()] if vis else []
+        local = int(self.index)
+        if ent and local < len(ent):
+            e = ent[local]
+            if e.isdigit():
+                return pynvml.nvmlDeviceGetHandleByIndex(int(e))
+            return pynvml.nvmlDeviceGetHandleByUUID(e)
+        return pynvml.nvmlDeviceGetHandleByIndex(local)
+
+    def _poll(self, pynvml, h):
+        mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                pw = pynvml.nvmlDeviceGetPowerUsage(h) / 1e3
+                rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((time.perf_counter(), float(sm), float(mx), pw, int(rs)))
+            except Exception:
+                pass
+            self.stop.wait(0.002)
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            h = self._nvml_handle(pynvml)
+            self.nvml = pynvml
+            self.t = threading.Thread(target=self._poll, args=(pynvml, h), daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nvml = None
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.FIELDS, "--format=csv,noheader,nounits",
+                                              "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=self._read, daemon=True)
+                self.t.start()
+            except Exception:
+                self.proc = None
+        self.t_begin = time.perf_counter()
         return self
 
     def _read(self):
@@ -119,6 +162,13 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        if self.nvml:
+            self.stop.set()
+            self.t.join(timeout=5)
+            try:
+                self.nvml.nvmlShutdown()
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -128,7 +178,13 @@ class ClockSampler:
 
     def summary(self):
         sm, mx, pw, reasons = [], [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for t, s, m, p, rs in self.samples:
+            if t < self.t_begin:
+                continue
+            sm.append(s), mx.append(m), pw.append(p)
+            for nm, bit in zip(self.NAMES, self.BITS):
+                if rs & bit:
+                    reasons.add(nm)
         for ln in self.lines:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 9 or f[0] != self.index:
@@ -139,13 +195,14 @@ class ClockSampler:
                 pw.append(float(f[3]))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
+            for nm, v in zip(self.NAMES, f[5:9]):
                 if v.lower() == "active":
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm), "power_w": statistics.median(pw) if pw else None}
+                "samples": len(sm), "power_w": statistics.median(pw) if pw else None,
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- CPU reference
