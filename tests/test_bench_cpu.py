@@ -30,3 +30,25 @@ def test_reference_arm_prints_one_json_line():
     assert d["value"] > 0 and d["unit"] == "it/s" and d["warmup"] >= 3
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+
+
+def test_clock_sampler_counts_only_timed_region_samples():
+    """bench.ClockSampler.summary keeps the NVML samples taken after the timed region opened and
+    decodes the throttle bits the contract names (hw_slowdown 0x8, hw_thermal 0x40,
+    sw_thermal 0x20, sw_power_cap 0x4)."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    s = bench.ClockSampler(0)
+    s.t_begin = 10.0
+    s.samples = [(9.0, 600.0, 1965.0, 200.0, 0x8),       # before the region: ignored
+                 (10.5, 1400.0, 1965.0, 900.0, 0x4),
+                 (11.0, 1500.0, 1965.0, 910.0, 0x0),
+                 (11.5, 1600.0, 1965.0, 920.0, 0x4 | 0x20)]
+    d = s.summary()
+    assert d["samples"] == 3 and d["sm_mhz"] == 1500.0 and d["sm_max_mhz"] == 1965.0
+    assert d["reasons"] == ["sw_power_cap", "sw_thermal_slowdown"]
+    assert d["source"] == "nvml"
+    empty = bench.ClockSampler(0)
+    empty.t_begin = 0.0
+    assert empty.summary()["samples"] == 0
