@@ -4,13 +4,17 @@
 // R rows, 8192/(32R) atoms) — R = 128 is pass 1's layout (256 B per row), R = 64 pass 2's
 // (512 B per row), R = 32 1 KB per row. Each CTA walks its contiguous range of row-block-major
 // stages (the pass's stream-K order). Configs alternate over several rounds so board power state
-// is shared; each timing covers 20 passes (≈50 ms).
-// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/box_shape_bench tools/box_shape_bench.cu -lcuda
+// is shared; each timing covers 200 passes (≈0.5 s) and reads NVML's energy counter around
+// them (mJ per pass: a pattern that activates more DRAM rows costs more energy at equal speed,
+// which is what matters under the board's power cap).
+// Build: nvcc -O3 -gencode arch=compute_100a,code=sm_100a -o tools/box_shape_bench tools/box_shape_bench.cu -lcuda \
+//   -L/usr/local/cuda/lib64/stubs -lnvidia-ml
 #include <cstdio>
 #include <cstdint>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <nvml.h>
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t par) {
@@ -106,21 +110,30 @@ int main() {
     }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0), cudaEventCreate(&e1);
-    const int passes = 20;
+    const int passes = 200;
+    nvmlDevice_t dev;
+    const bool nv = nvmlInit() == NVML_SUCCESS && nvmlDeviceGetHandleByIndex(0, &dev) == NVML_SUCCESS;
     for (int round = 0; round < 4; ++round)
         for (int i = 0; i < 3; ++i) {
             const int R = Rs[i], A = kStageBytes / (R * 128);
             const int spr = int(N / 32 / A);
             const int64_t n_stages = (M / R) * spr;
             k_stream<<<sms, 64, smem>>>(maps[i], n_stages, spr, R, A, sink);
+            cudaDeviceSynchronize();
+            unsigned long long en0 = 0, en1 = 0;
+            if (nv) nvmlDeviceGetTotalEnergyConsumption(dev, &en0);
             cudaEventRecord(e0);
             for (int p = 0; p < passes; ++p) k_stream<<<sms, 64, smem>>>(maps[i], n_stages, spr, R, A, sink);
             cudaEventRecord(e1);
             const cudaError_t err = cudaEventSynchronize(e1);
+            if (nv) nvmlDeviceGetTotalEnergyConsumption(dev, &en1);
+            unsigned sm_mhz = 0;
+            if (nv) nvmlDeviceGetClockInfo(dev, NVML_CLOCK_SM, &sm_mhz);
             float ms = 0;
             cudaEventElapsedTime(&ms, e0, e1);
-            printf("round %d box %3d rows x %d atoms (%4d B/row): %s %.3f ms/pass %.1f GB/s\n", round, R, A, A * 128,
-                   cudaGetErrorString(err), ms / passes, M * N * 4.0 * passes / (ms * 1e-3) / 1e9);
+            printf("round %d box %3d rows x %d atoms (%4d B/row): %s %.3f ms/pass %.1f GB/s, %.1f mJ/pass, %.0f W, SM %u MHz\n",
+                   round, R, A, A * 128, cudaGetErrorString(err), ms / passes, M * N * 4.0 * passes / (ms * 1e-3) / 1e9,
+                   double(en1 - en0) / passes, double(en1 - en0) / ms, sm_mhz);
         }
     return 0;
 }
