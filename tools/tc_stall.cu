@@ -17,6 +17,15 @@ using namespace ooc;
 
 #define CK(x) do { cudaError_t e_ = (x); if (e_ != cudaSuccess) { printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__); exit(1); } } while (0)
 
+__global__ void k_fill(float* a, int64_t n, uint32_t salt, float scale) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t x = uint32_t(i) * 2654435761u ^ uint32_t(i >> 32) * 40503u ^ salt;
+        x ^= x >> 15, x *= 2246822519u, x ^= x >> 13;
+        a[i] = float(x >> 8) * (scale / 16777216.f);
+    }
+}
+
+// argv: kp mp np [random=0|1] (random: hash-filled A and factors instead of zeros)
 int main(int argc, char** argv) {
     const int kp = argc > 1 ? atoi(argv[1]) : 32;
     const int64_t mp = argc > 2 ? atoll(argv[2]) : 65536, np = argc > 3 ? atoll(argv[3]) : 65536;
@@ -28,9 +37,15 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&Wc, size_t(mp) * 2 * kp * 4));
     CK(cudaMemset(Hc, 0, size_t(np) * 2 * kp * 4));
     CK(cudaMemset(Wc, 0, size_t(mp) * 2 * kp * 4));
+    if (argc > 4 && atoi(argv[4])) {
+        k_fill<<<148 * 8, 256>>>(A, mp * np, 1u, 1.f);
+        k_fill<<<148 * 8, 256>>>(Hc, np * 2 * kp, 2u, 0.01f);
+        k_fill<<<148 * 8, 256>>>(Wc, mp * 2 * kp, 3u, 0.01f);
+    }
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    for (int pass = 1; pass <= 2; ++pass) {
+    for (int pass_i = 0; pass_i < 4; ++pass_i) {
+        const int pass = 1 + (pass_i & 1);
         StreamK sk;
         if (pass == 1) plan_aht(sk, mp, np, sms, kTcStep); else plan_wta(sk, mp, np, sms, kTcStep);
         CK(cudaMalloc(&slots, size_t(sk.G * sk.smax) * 128 * kp * 4));
