@@ -67,6 +67,12 @@ def parse():
     p.add_argument("--density", type=float, default=1e-5)
     p.add_argument("--ooc-gb", type=float, default=64.0, help="host A slab per rank (GB) for --workload ooc")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-e2e-f64", action="store_true", help="skip the reference-shaped f64 pageable e2e run")
+    p.add_argument("--no-sparse", action="store_true", help="dense workload: skip the config-3 sub-record")
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="weak: m = N x --m rows (a fixed slab per GPU)")
+    p.add_argument("--ref-sample", action="store_true",
+                   help="--impl reference: time a 1024-row sample instead of the full workload")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     # --workload select (config 5: select_k over k=2..16 on dense 32768 x 16384)
@@ -400,6 +406,73 @@ def bench_select(args, nmf, np, torch, ctx, comm, rank, world, local, barrier, m
         comm.close()
 
 
+def reference_arm(args, rank, K, W, k):
+    """--impl reference: the reference's own CPU solver (oracle/_ref) on this box's host cores.
+
+    dense (default): the SAME configuration as our arm — the full 65536 x 65536 A (f64, the
+    reference's type, values rounded from the same f32 uniform draw), W warm-up MU iterations,
+    then one timed nmf_serial of K iterations with the reference's check cadence (every 10 and
+    the last; src/nmf_serial.cpp:83-117), so value = K / that time. When the host cannot hold the
+    f64 A (or --ref-sample is given) it falls back to the row-sample extrapolation."""
+    if rank != 0:
+        return
+    m, n = args.m or 65536, args.n
+    if args.workload != "dense":
+        emit({"impl": "reference", "unavailable": "--impl reference implemented for the default (dense) workload only"})
+        return
+    workload = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
+    metric = f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, NCCL all-reduce)"
+    import numpy as np
+
+    impl, kind = _ref_impl()
+    cores = int(os.environ.get("OMP_NUM_THREADS", CPU_CORES))
+    try:
+        ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES")
+    except (ValueError, OSError):
+        ram = 0
+    full = not args.ref_sample and kind == "reference" and m * n * 8 < 0.8 * ram
+    if full:
+        import oracle
+
+        t0 = time.perf_counter()
+        hnd = impl.dense_uniform_handle(m, n, 42, 99, round_f32=True)  # built in place, OpenMP
+        gen_s = time.perf_counter() - t0
+        w, h = oracle.port.init_factors(m, n, k, 0)
+        try:
+            t0 = time.perf_counter()
+            for _ in range(W):
+                impl.mu_iteration_handle(hnd, w, h)  # the loop body of nmf_serial (nmf_serial.cpp:84-101)
+            warm_s = time.perf_counter() - t0
+            t0 = time.perf_counter()
+            r = impl.nmf_serial_handle(hnd, m, n, k, max_iters=K, interval=10, eta=0.0, seed=0)
+            secs = time.perf_counter() - t0
+        finally:
+            impl.dense_free(hnd)
+        rate = K / secs
+        cb = {"value": rate, "unit": "it/s", "cores": cores, "kind": kind,
+              "sample": f"the full workload: nmf_serial (f64) on the {m}x{n} A, k={k}, {K} iterations with error "
+                        f"checks every 10 and on the last ({len(r.trace_err)} checks, final error "
+                        f"{r.trace_err[-1]:.6f}), after {W} warm-up MU iterations ({warm_s:.1f} s); A generated in "
+                        f"{gen_s:.1f} s (not timed)",
+              "same_config": True}
+        extra = {"timed_s": secs, "final_rel_error": float(r.trace_err[-1])}
+    else:
+        rate, cb = cpu_reference_dense(m, n, k, args.cpu_seconds, steps=K, warmup=W)
+        cb["sample"] = cb["sample"].replace("MU iterations", f"timed MU iterations after {W} warm-up")
+        cb["same_config"] = False
+        extra = {}
+    out = {"impl": "reference", "metric": metric, "value": rate, "unit": "it/s", "n_gpus": args.gpus,
+           "steps": K, "warmup": W, "ms_per_step": 1e3 / rate, "higher_is_better": True,
+           "scaling": "weak" if args.scaling == "weak" else "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic",
+           "config": {"workload": workload, "m": m, "n": n, "k": k, "parallelism": f"host cores ({cores} threads)",
+                      "error_check_interval": 10},
+           "cpu_baseline": cb,
+           "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    out.update(extra)
+    emit(out)
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -408,25 +481,7 @@ def main():
     K, W, k = args.steps, max(3, args.warmup), args.k
 
     if args.impl == "reference":
-        if rank != 0:
-            return
-        m, n = args.m or 65536, args.n
-        if args.workload != "dense":
-            emit({"impl": "reference", "unavailable": f"--impl reference implemented for the "
-                                                                  f"default (dense) workload only"})
-            return
-        rate, cb = cpu_reference_dense(m, n, k, args.cpu_seconds, steps=K, warmup=W)
-        cb["sample"] = cb["sample"].replace("MU iterations", f"timed MU iterations after {W} warm-up")
-        workload = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
-        emit({"impl": "reference", "metric": f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, "
-                                                         f"NCCL all-reduce)",
-                          "value": rate, "unit": "it/s", "n_gpus": args.gpus,
-                          "steps": K, "warmup": W, "ms_per_step": 1e3 / rate, "higher_is_better": True,
-                          "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                          "config": {"workload": workload, "m": m, "n": n, "k": k, "parallelism": "host cores"},
-                          "cpu_baseline": cb,
-                          "e2e": {"value": rate, "unit": "it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
-        return
+        return reference_arm(args, rank, K, W, k)
 
     import numpy as np
     import torch
@@ -462,39 +517,65 @@ def main():
     ctx = comm.ctx if comm else nmf.Context(local)
     if args.workload == "select":
         return bench_select(args, nmf, np, torch, ctx, comm, rank, world, local, barrier, max_over_ranks)
+    env = dict(nmf=nmf, np=np, torch=torch, ctx=ctx, rank=rank, world=world, local=local, barrier=barrier,
+               max_over_ranks=max_over_ranks, sum_over_ranks=sum_over_ranks)
+    out = run_workload(args, args.workload, args.m, args.n, k, K, W, env)
+    # BASELINE.json's metric is "dense+sparse": the default dense line carries config 3 too
+    if args.workload == "dense" and not args.no_sparse:
+        if comm is None:
+            ctx.close()
+            ctx = nmf.Context(local)
+            env["ctx"] = ctx
+        sp = run_workload(args, "sparse", 1 << 22, 1 << 22, 32, K, W, env)
+        if out is not None:
+            out["sparse"] = sp
+    if rank == 0:
+        emit(out)
+    if comm:
+        comm.close()
+        torch.distributed.destroy_process_group()
+    else:
+        ctx.close()
+
+
+def run_workload(args, workload, m, n, k, K, W, env):
+    nmf, np, torch, ctx = env["nmf"], env["np"], env["torch"], env["ctx"]
+    rank, world, local = env["rank"], env["world"], env["local"]
+    barrier, max_over_ranks, sum_over_ranks = env["barrier"], env["max_over_ranks"], env["sum_over_ranks"]
     kp = 8 if k <= 8 else 16 if k <= 16 else 32 if k <= 32 else 64
     hbm, peak_src = peaks()
     extra = {}
     host_buf = None
 
     # ------------------------------------------------------------------ set up A
-    n = args.n
-    if args.workload == "ooc":
-        rows_per_rank = args.m // world if args.m else int(args.ooc_gb * 1e9 / (n * 4)) // 128 * 128
+    weak = args.scaling == "weak" and workload != "ooc"
+    if workload == "ooc":
+        rows_per_rank = m // world if m else int(args.ooc_gb * 1e9 / (n * 4)) // 128 * 128
         m = rows_per_rank * world
-    else:
-        m = args.m
+    elif weak:
+        m = m * world  # weak scaling: a fixed slab per GPU (the paper's [N x 65536, ...] pattern)
     plan = nmf.make_plan(m, n, k, world, 1, nmf.Strategy.rnmf)
     (r0, r1), _ = plan.slabs[rank]
     rows = r1 - r0
     t_setup = time.perf_counter()
-    if args.workload == "dense":
+    density = args.density
+    if workload == "dense":
         ctx.set_problem(m, n, k, r0, rows)
         ctx.generate_dense_uniform(42, 99)
-        workload = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
+        wl = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
         metric = f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, NCCL all-reduce)"
         bytes_per_launch = rows * n * 4 + (n + rows) * k * 4
-    elif args.workload == "sparse":
+    elif workload == "sparse":
         ctx.set_problem(m, n, k, r0, rows)
-        ctx.generate_csr_uniform(args.density, 1)
+        ctx.generate_csr_uniform(density, 1)
         import ctypes as C
 
         cnt = C.c_uint64()
         nmf.check(nmf._capi.lib().oocnmf_csr_nnz(ctx._h, C.byref(cnt)))
         nnz = int(cnt.value)
-        workload = (f"sparse synthetic CSR {m}x{n}, density {args.density} (reference generator "
-                    f"synth.cpp:60-86 on device, seed 1), nnz/rank={nnz}, k={k}, RNMF row slabs")
-        metric = f"MU iters/sec (sparse CSR {m}x{n} density {args.density}, k={k}, 1D row-partitioned)"
+        wl = (f"sparse synthetic CSR {m}x{n}, density {density} (reference generator "
+              f"synth.cpp:60-86 on device, seed 1), nnz/rank={nnz}, k={k}, RNMF row slabs")
+        metric = f"MU iters/sec (sparse CSR {m}x{n} density {density}, k={k}, 1D row-partitioned)"
         # gather model: CSR (8 B/nnz) + row_ptr + one kp-wide factor row per
         # nonzero + output, per SpMM; pass 2 runs on CSR(A^T) (n rows)
         bytes_per_launch = {"aht_pass (A.H^T)": nnz * 8 + (rows + 1) * 8 + nnz * kp * 4 + rows * kp * 4,
@@ -513,8 +594,8 @@ def main():
                 gen.generate_dense_uniform(42, 99)
                 gen.download_dense(host_buf[c0:c0 + cr])
         ctx.attach_host(host_buf)
-        workload = (f"out-of-core dense {m}x{n} f32 uniform A, {rows * n * 4 / 1e9:.1f} GB pinned host slab/rank "
-                    f"(config 4 scaled to this host's RAM), k={k}, streamed every iteration")
+        wl = (f"out-of-core dense {m}x{n} f32 uniform A, {rows * n * 4 / 1e9:.1f} GB pinned host slab/rank "
+              f"(config 4 scaled to this host's RAM), k={k}, streamed every iteration")
         metric = f"MU iters/sec (out-of-core dense {m}x{n}, k={k}, host-link streaming)"
         bytes_per_launch = rows * n * 4
     extra["setup_s"] = time.perf_counter() - t_setup
@@ -536,11 +617,11 @@ def main():
     traffic = None  # ncu dram bytes per launch of the dominant kernel, when captured for this config
     prof = os.path.join(ROOT, "profiles", "ncu_dram_per_launch.json")
     if world == 1 and os.path.exists(prof):
-        if args.workload == "dense" and (m, n, k) == (65536, 65536, 32):
+        if workload == "dense" and (m, n, k) == (65536, 65536, 32):
             traffic = json.load(open(prof))
-        elif args.workload == "sparse" and (m, n, k) == (1 << 22, 1 << 22, 32) and args.density == 1e-5:
+        elif workload == "sparse" and (m, n, k) == (1 << 22, 1 << 22, 32) and density == 1e-5:
             traffic = json.load(open(prof)).get("sparse")
-    if args.workload == "ooc":
+    if workload == "ooc":
         # host-link roofline: measured pinned H2D bandwidth on this GPU (concurrently on all ranks)
         probe = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
         dev = torch.empty_like(probe, device="cuda")
@@ -564,105 +645,130 @@ def main():
                                 "wta_pass (A^T.W)": info["wta_pass_ms"] / max(1, info["wta_pass_launches"])}}
     else:
         roof = roofline(info, bytes_per_launch, hbm, peak_src, traffic)
-        if args.workload == "sparse" and world == 1:
+        if workload == "sparse":
             roof["note"] = ("both passes are k_spmm_mu launches: the SpMM with the factor update fused into it "
-                            "(A.H^T + W update; A^T.W + H update except on error-check iterations); the "
-                            "algorithmic bytes count the SpMM only")
-    extra["a_pass_gbs_total"] = sum_over_ranks(2 * rows * n * 4 * value / 1e9) if args.workload == "dense" else None
+                            "(A.H^T + W update; A^T.W + H update except on error-check iterations, single rank); "
+                            "the algorithmic bytes count the SpMM only")
+    extra["a_pass_gbs_total"] = sum_over_ranks(2 * rows * n * 4 * value / 1e9) if workload == "dense" else None
 
     # ------------------------------------------------------------------ e2e through the public API
     e2e = None
-    if not args.no_e2e and args.workload in ("dense", "sparse"):
-        if args.workload == "dense":
-            host = np.empty((rows, n), np.float32)
-            ctx.download_dense(host)
-            nmf.check(nmf._capi.lib().oocnmf_host_register(host.ctypes.data, host.nbytes))
-            h2d = rows * n * 4
-        else:
-            host = ctx.download_csr()
-            h2d = host.nnz * 12 + (rows + 1) * 8
-        try:
-            barrier()
-            t0 = time.perf_counter()
-            ecfg = nmf.NmfConfig(k=k, max_iters=K, error_check_interval=10, eta=0.0, seed=0, device=local)
-            if world == 1 and args.workload == "dense":
-                import ctypes as C
-
-                c = ecfg.to_c()
-                wout, hout = np.empty((rows, k)), np.empty((k, n))
-                ti, te = np.zeros(K // 10 + 2, np.uint64), np.zeros(K // 10 + 2)
-                inf = nmf._capi.Info()
-                nmf.check(nmf._capi.lib().oocnmf_nmf_serial_dense_f32(
-                    local, host.ctypes.data_as(C.POINTER(C.c_float)), rows, n, C.byref(c), None, None,
-                    wout.ctypes.data_as(C.POINTER(C.c_double)), hout.ctypes.data_as(C.POINTER(C.c_double)),
-                    ti.ctypes.data_as(C.POINTER(C.c_uint64)), te.ctypes.data_as(C.POINTER(C.c_double)), ti.size,
-                    C.byref(inf)))
-            else:
-                marks = [time.perf_counter()]
-                ctx.set_problem(m, n, k, r0, rows)
-                if args.workload == "dense":
-                    ctx.load_dense(host)
-                else:
-                    ctx.load_csr(host)
-                marks.append(time.perf_counter())
-                ctx.solve(ecfg)
-                marks.append(time.perf_counter())
-                ctx.get_factors()
-                marks.append(time.perf_counter())
-                if world > 1:
-                    ctx.gather_w()
-                marks.append(time.perf_counter())
-                if os.environ.get("BENCH_E2E_DEBUG"):
-                    print(f"[e2e rank {rank}] load {marks[1] - marks[0]:.3f} s, solve {marks[2] - marks[1]:.3f} s, "
-                          f"factors {marks[3] - marks[2]:.3f} s, gather W {marks[4] - marks[3]:.3f} s",
-                          file=sys.stderr)
-            torch.cuda.synchronize()
-            e2e_s = max_over_ranks(time.perf_counter() - t0)
-        finally:
-            if args.workload == "dense":
-                nmf._capi.lib().oocnmf_host_unregister(host.ctypes.data)
-        d2h = (((rows + 127) // 128 * 128) + (n + 127) // 128 * 128) * kp * 4 + 16 * (K // 10 + 1)
-        e2e = {"value": K / e2e_s, "unit": "it/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-               "note": f"one public-API solve of {K} iterations on host buffers (A uploaded once: {h2d / 1e9:.2f} "
-                       f"GB/rank; W/H downloaded once); bytes are per step"}
-    elif args.workload == "ooc":
+    if not args.no_e2e and workload in ("dense", "sparse"):
+        e2e = e2e_runs(args, workload, m, n, k, K, rows, r0, kp, env)
+    elif workload == "ooc":
         e2e = {"value": value, "unit": "it/s", "h2d_bytes_per_step": rows * n * 4, "d2h_bytes_per_step": 16,
                "note": "out-of-core: the timed solve already reads A from pinned host memory every iteration"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        if args.workload == "dense":
+        if workload == "dense":
             _, cpu = cpu_reference_dense(m, n, k, args.cpu_seconds)
-        elif args.workload == "sparse":
+        elif workload == "sparse":
             samples = []
             for sr in (2048, 65536):  # a wide row range keeps the per-row slope above the noise
                 with nmf.Context(local) as g:
                     g.set_problem(m, n, k, 0, sr)
-                    g.generate_csr_uniform(args.density, 1)
+                    g.generate_csr_uniform(density, 1)
                     samples.append((sr, g.download_csr()))
             _, cpu = cpu_reference_sparse(samples, m, k, args.cpu_seconds)
 
-    if rank == 0:
-        out = {"metric": metric, "value": value, "unit": "it/s", "n_gpus": world, "steps": K, "warmup": W,
-               "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "f32", "data": "synthetic",
-               "config": {"workload": workload, "m": m, "n": n, "k": k, "parallelism": f"rnmf-dp{world}",
-                          "rows_per_rank": rows, "error_check_interval": 10,
-                          "l2": f"A slab >> 126 MB L2 (no flush needed)"},
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-               "gpu_launches": int(info["gpu_launches"]), "final_rel_error": trace[-1][1] if trace else None,
-               "phase_ms_per_step": {p_: info[p_ + "_s"] * 1e3 / K for p_ in
-                                     ("w_update", "h_update", "allreduce", "error_check")}}
-        out.update({k_: v for k_, v in extra.items() if v is not None})
-        emit(out)
     if host_buf is not None:
-        ctx.close()
+        ctx.set_problem(m, n, k, r0, rows)  # detach the host slab before unregistering it
         nmf._capi.lib().oocnmf_host_unregister(host_buf.ctypes.data)
-    if comm:
-        comm.close()
-        torch.distributed.destroy_process_group()
+    if rank != 0:
+        return None
+    out = {"metric": metric, "value": value, "unit": "it/s", "n_gpus": world, "steps": K, "warmup": W,
+           "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak" if weak else "strong",
+           "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+           "config": {"workload": wl, "m": m, "n": n, "k": k, "parallelism": f"rnmf-dp{world}",
+                      "rows_per_rank": rows, "error_check_interval": 10,
+                      "l2": f"A slab >> 126 MB L2 (no flush needed)"},
+           "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+           "gpu_launches": int(info["gpu_launches"]), "final_rel_error": trace[-1][1] if trace else None,
+           "phase_ms_per_step": {p_: info[p_ + "_s"] * 1e3 / K for p_ in
+                                 ("w_update", "h_update", "allreduce", "error_check")}}
+    out.update({k_: v for k_, v in extra.items() if v is not None})
+    return out
+
+
+def e2e_runs(args, workload, m, n, k, K, rows, r0, kp, env):
+    """End to end through the public API on HOST buffers, K iterations, every phase timed with
+    the device synchronised at its end (phases sum to the total): context creation, A upload
+    (host -> device, narrowing / layout on the device), the solve, the factor download
+    (device -> host, f64 reference layouts), context destruction.
+
+    Two runs: the headline uses the library's f32 extension on page-locked host memory
+    (oocnmf_load_dense_f32 / the CSR upload); the second is the reference-shaped call, an f64
+    pageable row-major A handed to nmf_serial exactly as a reference caller holds it
+    (include/oocnmf/nmf.hpp:64 via MatrixRef(DenseMatrix)), dense at N = 1 only (34 GB)."""
+    nmf, np, torch = env["nmf"], env["np"], env["torch"]
+    world, local, barrier, max_over_ranks = env["world"], env["local"], env["barrier"], env["max_over_ranks"]
+    ctx = env["ctx"]
+    if workload == "dense":
+        host = np.empty((rows, n), np.float32)
+        ctx.download_dense(host)
+        h2d = rows * n * 4
     else:
-        ctx.close()
+        host = ctx.download_csr()
+        h2d = host.nnz * 12 + (rows + 1) * 8
+    d2h = rows * k * 8 + k * n * 8 + 16 * (K // 10 + 1)
+    ecfg = nmf.NmfConfig(k=k, max_iters=K, error_check_interval=10, eta=0.0, seed=0, device=local)
+
+    def one(a_host, use_comm_ctx):
+        ph = {}
+        barrier()
+        t0 = time.perf_counter()
+        t = t0
+        c = ctx if use_comm_ctx else nmf.Context(local)
+
+        def mark(name):
+            nonlocal t
+            torch.cuda.synchronize()
+            now = time.perf_counter()
+            ph[name] = now - t
+            t = now
+        mark("create")
+        c.set_problem(m, n, k, r0, rows)
+        if workload == "dense":
+            c.load_dense(a_host)
+        else:
+            c.load_csr(a_host)
+        mark("upload")
+        c.solve(ecfg)
+        mark("solve")
+        c.get_factors()
+        if world > 1:
+            c.gather_w()
+        mark("download")
+        if not use_comm_ctx:
+            c.close()
+        mark("destroy")
+        total = max_over_ranks(time.perf_counter() - t0)
+        return total, {k_: round(v, 4) for k_, v in ph.items()}
+
+    pinned = workload == "dense"
+    if pinned:
+        nmf.check(nmf._capi.lib().oocnmf_host_register(host.ctypes.data, host.nbytes))
+    try:
+        total, ph = one(host, world > 1)
+    finally:
+        if pinned:
+            nmf._capi.lib().oocnmf_host_unregister(host.ctypes.data)
+    e2e = {"value": K / total, "unit": "it/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
+           "phases_s": ph, "total_s": total,
+           "note": f"public API on host buffers: A ({h2d / 1e9:.2f} GB/rank, "
+                   f"{'f32 page-locked' if pinned else 'CSR u64/f64 pageable'}) uploaded once, {K} iterations, "
+                   f"W/H downloaded as f64; phases sum to total_s"}
+    if workload == "dense" and world == 1 and not args.no_e2e_f64:
+        a64 = host.astype(np.float64)
+        del host
+        t64, ph64 = one(a64, False)
+        e2e["reference_shaped"] = {"value": K / t64, "unit": "it/s", "h2d_bytes_per_step": a64.nbytes / K,
+                                   "d2h_bytes_per_step": d2h / K, "phases_s": ph64, "total_s": t64,
+                                   "note": "f64 pageable row-major A as a reference caller holds it "
+                                           "(nmf_serial(MatrixRef(DenseMatrix))): staged copy-in, narrowing to f32 "
+                                           "on the device"}
+    return e2e
 
 
 if __name__ == "__main__":

@@ -243,7 +243,7 @@ private:
 
 struct ASource {
     MatrixRef mem;
-    std::string pdn1_path;  // not supported by the B200 backend (IoError)
+    std::string pdn1_path;  // PDN1 (.pdn1) or Matrix Market (.mtx) file; PDN1 is read window-wise
     const float* host_f32 = nullptr;  // B200 extension: out-of-core host slab (rows of this rank)
     index_t host_ld = 0;
     static ASource memory(MatrixRef a) { return {a, {}, nullptr, 0}; }

@@ -350,6 +350,31 @@ class Ref(_Lib):
         f.argtypes = [C.c_void_p, _u64, _pd, _pd, _dbl]
         self._check(f(hnd, w.shape[1], _ptr(w), _ptr(h), eps))
 
+    def dense_uniform_handle(self, m, n, seed=42, stream=99, round_f32=True):
+        """The uniform synthetic A built in place inside the library (no numpy copy)."""
+        f = self.lib.ref_dense_create_uniform
+        f.restype = C.c_void_p
+        f.argtypes = [_u64, _u64, _u64, _u64, C.c_int]
+        return f(m, n, seed, stream, 1 if round_f32 else 0)
+
+    def nmf_serial_handle(self, hnd, m, n, k, w0=None, h0=None, max_iters=100, interval=10, eta=0.0, eps=1e-12,
+                          seed=0):
+        cap = max_iters // interval + 2
+        w, h, ti, te, nt, run, conv, cnt = self._res(m, n, k, cap)
+        keep = None
+        w0p = h0p = None
+        if w0 is not None:
+            keep = (np.ascontiguousarray(w0, np.float64), np.ascontiguousarray(h0, np.float64))
+            w0p, h0p = _ptr(keep[0]), _ptr(keep[1])
+        f = self.lib.ref_nmf_serial_dense_handle
+        f.argtypes = [C.c_void_p, _u64, _u64, _u64, _dbl, _dbl, _u64, _pd, _pd, _pd, _pd, _pu, _pd, _u64, _pu, _pu,
+                      _pi, _pd]
+        st = f(hnd, k, max_iters, interval, eta, eps, seed, w0p, h0p, _ptr(w), _ptr(h), _ptr(ti, _pu), _ptr(te),
+               cap, C.byref(nt), C.byref(run), C.byref(conv), _ptr(cnt))
+        self._check(st)
+        del keep
+        return self._pack(w, h, ti, te, nt, run, conv, cnt, cap)
+
     def csr_handle(self, rp, ci, v, m, n):
         self._csr_keep = (np.ascontiguousarray(rp, np.uint64), np.ascontiguousarray(ci, np.uint64),
                           np.ascontiguousarray(v, np.float64))

@@ -278,6 +278,38 @@ int ref_mu_iteration_handle(void* a_handle, std::uint64_t k, double* w, double* 
     });
 }
 
+// The uniform synthetic A (CounterRng(seed, stream).uniform(i * n + j), as
+// bench/kernels_bench.cpp:12-18), optionally rounded to f32, built in place in a
+// DenseMatrix held by the caller: a full-size (65536^2, 34 GB) A then exists once, not as a
+// numpy array plus the DenseMatrix copy nmf_serial would otherwise need.
+void* ref_dense_create_uniform(std::uint64_t m, std::uint64_t n, std::uint64_t seed, std::uint64_t stream,
+                               int round_f32) {
+    auto* A = new DenseMatrix(m, n);
+    double* a = A->data();
+    const CounterRng rng(seed, stream);
+#pragma omp parallel for schedule(static)
+    for (std::int64_t i = 0; i < std::int64_t(m); ++i)
+        for (std::uint64_t j = 0; j < n; ++j) {
+            const double v = rng.uniform(std::uint64_t(i) * n + j);
+            a[std::uint64_t(i) * n + j] = round_f32 ? double(float(v)) : v;
+        }
+    return A;
+}
+
+// nmf_serial (src/nmf_serial.cpp:56) on a held DenseMatrix.
+int ref_nmf_serial_dense_handle(void* a_handle, std::uint64_t k, std::uint64_t max_iters, std::uint64_t interval,
+                                double eta, double eps, std::uint64_t seed, const double* w0, const double* h0,
+                                double* w, double* h, std::uint64_t* trace_it, double* trace_err,
+                                std::uint64_t trace_cap, std::uint64_t* n_trace, std::uint64_t* iters_run,
+                                int* converged, double* counters) {
+    return guarded([&] {
+        const DenseMatrix& A = *static_cast<DenseMatrix*>(a_handle);
+        NmfConfig cfg = make_cfg(k, max_iters, interval, eta, eps, seed, w0, h0, A.rows(), A.cols());
+        write_out(nmf_serial(MatrixRef(A), cfg),
+                  {w, h, trace_it, trace_err, trace_cap, n_trace, iters_run, converged, counters});
+    });
+}
+
 // CSR variant for the sparse bench sample (A held by the library across timed iterations).
 void* ref_csr_create(const std::uint64_t* rp, const std::uint64_t* ci, const double* v, std::uint64_t m,
                      std::uint64_t n) {

@@ -338,21 +338,24 @@ __global__ void k_col_hist(const int32_t* __restrict__ ci, int64_t nnz,
         atomicAdd(cnt + ci[p], 1ull);
 }
 
-__global__ void k_gather_t(const int32_t* __restrict__ perm, const int32_t* __restrict__ rid,
+// (I: the permutation's index type — int64 once nnz exceeds the int32 range)
+template <class I>
+__global__ void k_gather_t(const I* __restrict__ perm, const int32_t* __restrict__ rid,
                            const float* __restrict__ v, int64_t nnz, int32_t* __restrict__ ciT,
                            float* __restrict__ vT) {
     for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < nnz;
          q += int64_t(gridDim.x) * blockDim.x) {
-        const int32_t p = perm[q];
+        const int64_t p = perm[q];
         ciT[q] = rid[p];
         vT[q] = v[p];
     }
 }
 
-__global__ void k_iota(int32_t* x, int64_t n) {
+template <class I>
+__global__ void k_iota(I* x, int64_t n) {
     for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n;
          q += int64_t(gridDim.x) * blockDim.x)
-        x[q] = int32_t(q);
+        x[q] = I(q);
 }
 
 // Generator: each thread tests kCpt consecutive cells of a row; rows are strided over blocks.
@@ -519,11 +522,15 @@ cudaError_t exclusive_scan_i64(const int64_t* in, int64_t* out, int64_t n, cudaS
     return e;
 }
 
-cudaError_t csr_transpose(const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
-                          int64_t cols, int64_t nnz, int64_t* rpT, int32_t* ciT, float* vT,
-                          cudaStream_t s) {
+// Stable radix sort of the entries by column (cub), carrying the entry index: the transpose
+// keeps ascending row order inside each column (deterministic CSR(A^T)). The permutation is
+// int32 while nnz fits, int64 beyond (a B200 holds A and A^T past 2^31 entries).
+template <class I>
+cudaError_t csr_transpose_t(const int64_t* rp, const int32_t* ci, const float* v, int64_t rows, int64_t cols,
+                            int64_t nnz, int64_t* rpT, int32_t* ciT, float* vT, cudaStream_t s) {
     cudaError_t e;
-    int32_t *rid = nullptr, *keys_out = nullptr, *perm_in = nullptr, *perm = nullptr;
+    int32_t *rid = nullptr, *keys_out = nullptr;
+    I *perm_in = nullptr, *perm = nullptr;
     unsigned long long* cnt = nullptr;
     void* tmp = nullptr;
     size_t bytes = 0;
@@ -534,13 +541,13 @@ cudaError_t csr_transpose(const int64_t* rp, const int32_t* ci, const float* v, 
     }
     OOC_TRY(cudaMallocAsync(&rid, nz * sizeof(int32_t), s));
     OOC_TRY(cudaMallocAsync(&keys_out, nz * sizeof(int32_t), s));
-    OOC_TRY(cudaMallocAsync(&perm_in, nz * sizeof(int32_t), s));
-    OOC_TRY(cudaMallocAsync(&perm, nz * sizeof(int32_t), s));
+    OOC_TRY(cudaMallocAsync(&perm_in, nz * sizeof(I), s));
+    OOC_TRY(cudaMallocAsync(&perm, nz * sizeof(I), s));
     OOC_TRY(cudaMallocAsync(&cnt, (cols + 1) * sizeof(unsigned long long), s));
     OOC_TRY(cudaMemsetAsync(cnt, 0, (cols + 1) * sizeof(unsigned long long), s));
     if (nnz > 0) {
         k_row_ids<<<grid_for(rows), 256, 0, s>>>(rp, rows, rid);
-        k_iota<<<grid_for(nnz), 256, 0, s>>>(perm_in, nnz);
+        k_iota<I><<<grid_for(nnz), 256, 0, s>>>(perm_in, nnz);
         k_col_hist<<<grid_for(nnz), 256, 0, s>>>(ci, nnz, cnt);
         int bits = 1;
         while ((int64_t(1) << bits) < cols) ++bits;
@@ -549,7 +556,7 @@ cudaError_t csr_transpose(const int64_t* rp, const int32_t* ci, const float* v, 
         OOC_TRY(cudaMallocAsync(&tmp, bytes, s));
         OOC_TRY(cub::DeviceRadixSort::SortPairs(tmp, bytes, ci, keys_out, perm_in, perm, nnz, 0, bits,
                                                 s));
-        k_gather_t<<<grid_for(nnz), 256, 0, s>>>(perm, rid, v, nnz, ciT, vT);
+        k_gather_t<I><<<grid_for(nnz), 256, 0, s>>>(perm, rid, v, nnz, ciT, vT);
     }
     static_assert(sizeof(unsigned long long) == sizeof(int64_t), "");
     OOC_TRY(exclusive_scan_i64(reinterpret_cast<const int64_t*>(cnt), rpT, cols + 1, s));
@@ -563,6 +570,13 @@ done:
     if (cnt) cudaFreeAsync(cnt, s);
     if (tmp) cudaFreeAsync(tmp, s);
     return e;
+}
+
+cudaError_t csr_transpose(const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
+                          int64_t cols, int64_t nnz, int64_t* rpT, int32_t* ciT, float* vT,
+                          cudaStream_t s) {
+    if (nnz > int64_t(INT32_MAX)) return csr_transpose_t<int64_t>(rp, ci, v, rows, cols, nnz, rpT, ciT, vT, s);
+    return csr_transpose_t<int32_t>(rp, ci, v, rows, cols, nnz, rpT, ciT, vT, s);
 }
 
 cudaError_t launch_gen_csr_count(int64_t rows, int64_t row0, int64_t n, uint64_t thresh, uint64_t seed,

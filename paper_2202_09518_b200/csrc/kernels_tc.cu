@@ -626,8 +626,32 @@ cudaError_t launch_tc(const CUtensorMap& a, const CUtensorMap& b, float* slots, 
     auto kern = k_pass_tc<KP, PASS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM));
     if (e != cudaSuccess) return e;
-    kern<<<unsigned(sk.G), 512, C::SMEM, s>>>(a, b, slots, sk, tc_drain_units(), out_final, flags, epoch);
-    return cudaGetLastError();
+    if (!out_final) {
+        kern<<<unsigned(sk.G), 512, C::SMEM, s>>>(a, b, slots, sk, tc_drain_units(), nullptr, nullptr, 0u);
+        return cudaGetLastError();
+    }
+    // The in-kernel fix-up has owner CTAs wait for peers' partials, so every CTA must be
+    // resident at once: a cooperative launch guarantees that or fails (MPS SM limits, green
+    // contexts, a concurrent kernel holding SMs). On failure the pass runs without the fix-up
+    // and the partials go through k_streamk_reduce (same ascending-CTA order, same result).
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(unsigned(sk.G));
+    lc.blockDim = dim3(512);
+    lc.dynamicSmemBytes = C::SMEM;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    e = cudaLaunchKernelEx(&lc, kern, a, b, slots, sk, tc_drain_units(), out_final, flags, epoch);
+    if (e == cudaErrorCooperativeLaunchTooLarge || e == cudaErrorNotSupported) {
+        cudaGetLastError();
+        kern<<<unsigned(sk.G), 512, C::SMEM, s>>>(a, b, slots, sk, tc_drain_units(), nullptr, nullptr, 0u);
+        if ((e = cudaGetLastError()) != cudaSuccess) return e;
+        return launch_streamk_reduce(KP, slots, sk, out_final, false, s);
+    }
+    return e;
 }
 
 }  // namespace

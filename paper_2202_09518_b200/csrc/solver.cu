@@ -177,6 +177,7 @@ struct oocnmf_ctx {
     };
     std::vector<Graph> graphs;  // small cache: the two event sets of the solve loop alternate
     DevBuf errs, flags, pred;   // device-side error checks: per-check value / NaN flag, predicate
+    DevBuf snapW[2], snapH[2];  // eta > 0: the factors at the last two checks (lagged early exit)
     bool graph_broken = false;   // capture failed once: iterate eagerly (same kernels)
     bool capturing = false;
 
@@ -880,10 +881,35 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         const char* e = std::getenv("OOCNMF_SYNC_CHECKS");
         return e && e[0] == '1';
     }();
+    // eta > 0: the early exit (nmf_serial.cpp:111 `if (err <= cfg.eta) break`) is taken one
+    // block late so the device never idles on the host: block b is enqueued before check b-1's
+    // value is read. Each check therefore snapshots W and Ht (two alternating device copies,
+    // ~5 us at config 2), and an exit at check b-1 restores its snapshot, discarding block b.
     const bool sync_each = cfg->eta > 0.0 || force_sync;
+    if (sync_each)
+        for (int p = 0; p < 2; ++p) {
+            c->snapW[p].alloc(c->W.bytes, "W snapshot");
+            c->snapH[p].alloc(c->Ht.bytes, "Ht snapshot");
+        }
     std::vector<uint64_t> check_iter;
     uint64_t iter = 0, nt = 0;
-    bool converged = false;
+    bool converged = false, stopped = false;
+    // decide on the check enqueued as block bb (its values were copied to hpin[2 (bb & 1)]);
+    // returns true when the solve stops there
+    auto decide = [&](uint64_t bb, cudaEvent_t done) -> bool {
+        ck(cudaEventSynchronize(done), "sync check");
+        double e = 0.0;
+        int f = 0;
+        std::memcpy(&e, c->hpin + 2 * (bb & 1), 8);
+        std::memcpy(&f, c->hpin + 2 * (bb & 1) + 1, 4);
+        if (f) return true;  // reported below, with the iteration of the first bad check
+        if (e <= cfg->eta) {
+            converged = true;
+            return true;
+        }
+        return false;
+    };
+    cudaEvent_t prev_done = nullptr;
     for (uint64_t next = 1, b = 0; next <= cfg->max_iters; ++b) {
         const uint64_t block = std::min<uint64_t>(interval - (next - 1) % interval, cfg->max_iters - next + 1);
         cudaEvent_t* ev = c->evs.data() + set_size * (b & 1);
@@ -895,6 +921,14 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         cudaEvent_t* ce = ev + kEvPerIter * block;
         ck(cudaEventRecord(ce[0], c->stream), "event");
         enqueue_check(c, cfg->error_mode, nt);
+        if (sync_each) {
+            double* hp = c->hpin + 2 * (b & 1);
+            ck(cudaMemcpyAsync(hp, c->errs.as<double>() + nt, 8, cudaMemcpyDeviceToHost, c->stream), "D2H err");
+            ck(cudaMemcpyAsync(hp + 1, c->flags.as<int>() + nt, 4, cudaMemcpyDeviceToHost, c->stream), "D2H flag");
+            ck(cudaMemcpyAsync(c->snapW[b & 1].p, c->W.p, c->W.bytes, cudaMemcpyDeviceToDevice, c->stream), "snapshot W");
+            ck(cudaMemcpyAsync(c->snapH[b & 1].p, c->Ht.p, c->Ht.bytes, cudaMemcpyDeviceToDevice, c->stream),
+               "snapshot Ht");
+        }
         ck(cudaEventRecord(ce[1], c->stream), "event");
         pend.push_back({block, ev});
         inf.flops += flops_per_iter * double(block);
@@ -903,27 +937,45 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         check_iter.push_back(iter);
         ++nt;
         if (sync_each) {
-            double e = 0.0;
-            int f = 0;
-            ck(cudaMemcpyAsync(c->hpin, c->errs.as<double>() + nt - 1, 8, cudaMemcpyDeviceToHost, c->stream), "D2H err");
-            ck(cudaMemcpyAsync(c->hpin + 1, c->flags.as<int>() + nt - 1, 4, cudaMemcpyDeviceToHost, c->stream),
-               "D2H flag");
-            ck(cudaStreamSynchronize(c->stream), "sync");
-            std::memcpy(&e, c->hpin, 8);
-            std::memcpy(&f, c->hpin + 1, 4);
-            if (f) break;  // reported below, with the iteration of the first bad check
-            if (e <= cfg->eta) {
-                converged = true;
+            if (b > 0 && decide(b - 1, prev_done)) {
+                // stop at check b - 1: drop block b and restore the factors as they were there
+                ck(cudaStreamSynchronize(c->stream), "sync");
+                ck(cudaMemcpyAsync(c->W.p, c->snapW[(b - 1) & 1].p, c->W.bytes, cudaMemcpyDeviceToDevice, c->stream),
+                   "restore W");
+                ck(cudaMemcpyAsync(c->Ht.p, c->snapH[(b - 1) & 1].p, c->Ht.bytes, cudaMemcpyDeviceToDevice,
+                                   c->stream),
+                   "restore Ht");
+                inf.flops -= flops_per_iter * double(block);
+                --nt;
+                check_iter.pop_back();
+                iter = check_iter.back();
+                stopped = true;
                 break;
             }
+            prev_done = ce[1];
         }
     }
+    if (sync_each && !stopped && nt > 0) decide(nt - 1, prev_done);
     ck(cudaStreamSynchronize(c->stream), "sync");
     for (const auto& p : pend) drain(p);
     std::vector<double> errs(nt);
     std::vector<int> flags(nt);
     ck(cudaMemcpy(errs.data(), c->errs.p, nt * 8, cudaMemcpyDeviceToHost), "D2H errs");
     ck(cudaMemcpy(flags.data(), c->flags.p, nt * 4, cudaMemcpyDeviceToHost), "D2H flags");
+    if (!sync_each) {
+        // eta = 0 runs without host round trips; the reference still stops at a check whose
+        // error is <= 0 (an exact fit), so the trace ends at the first such check. (The factors
+        // are then those of the last iteration: at an exact fit the MU ratios are 1.)
+        for (uint64_t i = 0; i < nt; ++i)
+            if (!flags[i] && errs[i] <= cfg->eta) {
+                nt = i + 1;
+                iter = check_iter[i];
+                converged = true;
+                break;
+            } else if (flags[i]) {
+                break;
+            }
+    }
     for (uint64_t i = 0; i < nt; ++i) {
         if (flags[i])
             fail(OOCNMF_ERR_DATA, "nmf: non-finite factor entries at iteration " + std::to_string(check_iter[i]));
@@ -1744,12 +1796,19 @@ int oocnmf_gather_w_f64(oocnmf_ctx* c, double* w_full) {
         if (beg[c->rank] != c->row0 || beg[c->rank + 1] != c->row0 + c->rows)
             fail(OOCNMF_ERR_SHAPE, "gather_w requires split_even row slabs");
         const int64_t maxr = int64_t(beg[1] - beg[0]);
+        // A rank's W holds round_up(rows, 128) rows, which can be fewer than maxr (a rank with
+        // maxr - 1 rows, a multiple of 128): the send side is this rank's slot of `all`, filled
+        // with its rows and zero-padded to maxr, so NCCL never reads past the W allocation.
         DevBuf all;
         all.alloc(size_t(N) * maxr * kp * 4, "gather");
+        float* mine = all.as<float>() + size_t(c->rank) * maxr * kp;
+        const size_t own = size_t(c->rows) * kp * 4;
+        ck(cudaMemcpyAsync(mine, c->W.p, own, cudaMemcpyDeviceToDevice, c->stream), "copy W");
+        if (size_t(maxr) * kp * 4 > own)
+            ck(cudaMemsetAsync(reinterpret_cast<char*>(mine) + own, 0, size_t(maxr) * kp * 4 - own, c->stream),
+               "memset W tail");
         if (N > 1)
-            nck(ncclAllGather(c->W.p, all.p, size_t(maxr) * kp, ncclFloat, c->comm, c->stream), "allgather W");
-        else
-            ck(cudaMemcpyAsync(all.p, c->W.p, size_t(maxr) * kp * 4, cudaMemcpyDeviceToDevice, c->stream), "copy");
+            nck(ncclAllGather(mine, all.p, size_t(maxr) * kp, ncclFloat, c->comm, c->stream), "allgather W");
         for (int p = 0; p < N; ++p)
             export_w(c, all.as<float>() + size_t(p) * maxr * kp, int64_t(beg[p + 1] - beg[p]), w_full + beg[p] * c->k);
     });

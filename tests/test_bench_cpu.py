@@ -15,10 +15,13 @@ def _ref_built():
 
 
 @pytest.mark.skipif(not _ref_built(), reason="oracle/_ref not built")
-def test_reference_arm_prints_one_json_line():
-    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
-                        "--warmup", "3", "--cpu-seconds", "1"], capture_output=True, text=True, timeout=600,
-                       cwd=ROOT)
+@pytest.mark.parametrize("mode", ["full", "sample"])
+def test_reference_arm_prints_one_json_line(mode):
+    # full: the same-config path (the whole A, nmf_serial with its checks) on a small A;
+    # sample: the row-sample extrapolation used when the host cannot hold the f64 A
+    extra = ["--m", "2048", "--n", "1024"] if mode == "full" else ["--ref-sample", "--cpu-seconds", "1"]
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "12",
+                        "--warmup", "3"] + extra, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert p.returncode == 0, p.stderr[-2000:]
     lines = [ln for ln in p.stdout.splitlines() if ln.strip()]
     assert len(lines) == 1, p.stdout
@@ -30,6 +33,9 @@ def test_reference_arm_prints_one_json_line():
     assert d["value"] > 0 and d["unit"] == "it/s" and d["warmup"] >= 3
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
     assert d["cpu_baseline"]["kind"] in ("reference", "port") and d["cpu_baseline"]["cores"] >= 1
+    assert d["cpu_baseline"]["same_config"] == (mode == "full")
+    if mode == "full":
+        assert d["config"]["m"] == 2048 and 0 < d["final_rel_error"] < 1
 
 
 def test_clock_sampler_counts_only_timed_region_samples():
