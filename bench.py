@@ -306,11 +306,16 @@ def cpu_reference_sparse(samples, m, k, seconds):
 
 
 # ----------------------------------------------------------------------------- helpers
+FUSED = "mu_fused (A.H^T, W update, A^T.W; A read from HBM once)"
+
+
 def roofline(info, bytes_per_launch, peak, peak_src, traffic=None, bound="hbm", unit="GB/s"):
     per = {}
-    for name, key in (("aht_pass (A.H^T)", "aht_pass_ms"), ("wta_pass (A^T.W)", "wta_pass_ms")):
-        launches = max(1, int(info[key.replace("_ms", "_launches")]))
-        per[name] = info[key] / launches
+    for name, key in (("aht_pass (A.H^T)", "aht_pass_ms"), ("wta_pass (A^T.W)", "wta_pass_ms"),
+                      (FUSED, "fused_pass_ms")):
+        launches = int(info.get(key.replace("_ms", "_launches"), 0))
+        if launches:
+            per[name] = info[key] / launches
     dom = max(per, key=per.get)
     b = bytes_per_launch[dom] if isinstance(bytes_per_launch, dict) else bytes_per_launch
     achieved = b / (per[dom] * 1e-3) / 1e9
@@ -564,7 +569,11 @@ def run_workload(args, workload, m, n, k, K, W, env):
         ctx.generate_dense_uniform(42, 99)
         wl = f"dense synthetic {m}x{n} f32 uniform A (CounterRng(42,99)), k={k}, RNMF row slabs"
         metric = f"MU iters/sec (dense {m}x{n}, k={k}, 1D row-partitioned, NCCL all-reduce)"
-        bytes_per_launch = rows * n * 4 + (n + rows) * k * 4
+        # one streaming pass reads the A slab once plus its factor operand and output
+        # (SURVEY.md §8(d)); the one-pass kernel reads A from HBM once for both contractions
+        bytes_per_launch = {"aht_pass (A.H^T)": rows * n * 4 + (n + rows) * k * 4,
+                            "wta_pass (A^T.W)": rows * n * 4 + (n + rows) * k * 4,
+                            FUSED: rows * n * 4 + (n + 2 * rows) * k * 4}
     elif workload == "sparse":
         ctx.set_problem(m, n, k, r0, rows)
         ctx.generate_csr_uniform(density, 1)

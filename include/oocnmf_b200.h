@@ -90,6 +90,8 @@ typedef struct {
     uint64_t wta_pass_launches;
     uint64_t gpu_launches; /* all kernels this library launched inside oocnmf_solve */
     double h2d_bytes;      /* host->device bytes moved inside oocnmf_solve (out-of-core) */
+    double fused_pass_ms;  /* one-pass dense W half (A read once: A·H^T, W update, W^T·A) */
+    uint64_t fused_launches;
 } oocnmf_info;
 
 typedef struct oocnmf_ctx oocnmf_ctx;

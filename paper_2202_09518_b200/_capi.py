@@ -31,7 +31,8 @@ class Info(C.Structure):
                 ("io_s", dbl), ("total_s", dbl), ("flops", dbl), ("peak_resident_bytes", u64),
                 ("iterations_run", u64), ("converged", i32), ("reserved", i32), ("n_trace", u64),
                 ("aht_pass_ms", dbl), ("wta_pass_ms", dbl), ("aht_pass_launches", u64),
-                ("wta_pass_launches", u64), ("gpu_launches", u64), ("h2d_bytes", dbl)]
+                ("wta_pass_launches", u64), ("gpu_launches", u64), ("h2d_bytes", dbl),
+                ("fused_pass_ms", dbl), ("fused_launches", u64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "common.cuh"
 
 namespace ooc {
@@ -36,6 +38,37 @@ cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
 cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np,
                           const float* W_cat, float* slots, const StreamK& sk, cudaStream_t s,
                           float* out_final = nullptr, unsigned* flags = nullptr, unsigned epoch = 0);
+
+// ---- one-pass dense MU W-half (kernels_fused.cu): P1 (A·Ht partials), the W update, and
+// P2 (W^T A with the new W) in one persistent tcgen05 kernel, A read from HBM once ----
+struct FusedArgs {
+    int NB, D, NS, G1;     // row blocks, P2 lookahead (blocks), P1 slot ring depth, P1 publishers
+    int drain_units;       // P1 chain length (kernels_tc.cu numerics)
+    const int* q0;         // [G + 1] P1 chunk (64 cols) range per CTA
+    const int* t0;         // [G + 1] owned W^T A tile (128 cols) range per CTA
+    const int* act;        // [G1] CTAs with P1 work, ascending
+    float* p1slots;        // [NS][G][128][kp] published P1 partials
+    unsigned* count;       // [NB] P1 partials published per block (zero before the launch)
+    unsigned* wdone;       // [NB] rows of the block updated (zero before the launch)
+    float* W;              // mp x kp, updated in place
+    float* Wcat;           // mp x 2kp [W | W_lo] of the new W
+    const float* HHt;      // kp x kp
+    float eps;
+    int* flag;             // non-finite W entries
+    float* wta;            // np x kp: W^T A (transposed) of the new W
+    uint64_t pol_p1, pol_p2;  // L2 policies of the A loads of P1 / P2
+};
+struct FusedPlan {
+    int G = 0, NB = 0, NT = 0, NQ = 0, D = 1, NS = 3, G1 = 0;
+    std::vector<int> q0, t0, act;
+};
+bool fused_supported(int kp, int64_t mp, int64_t np, int num_sms);
+namespace tc {
+int tc_drain_units();  // kernels_tc.cu: K steps per TMEM accumulation chain
+}
+void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahead);
+cudaError_t launch_mu_fused(int kp, const FusedPlan& fp, const float* A, int64_t mp, int64_t np, const float* Ht_cat,
+                            const FusedArgs& args, cudaStream_t s);
 
 // ---- factor kernels (kernels_factor.cu) ----
 // F (rows x kp, rows a multiple of 128) <- F * N / (F G + eps) rowwise, where N is either

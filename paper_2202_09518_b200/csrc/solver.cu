@@ -158,6 +158,10 @@ struct oocnmf_ctx {
     DevBuf fix_flags;            // in-kernel stream-K fix-up of pass 2 (tensor-core path)
     bool use_tc = false;         // kp in {32, 64}: tcgen05 passes; else CUDA-core FFMA passes
     StreamK sk1, sk2;            // in-core dense passes
+    // one-pass W half (kernels_fused.cu): dense in-core RNMF / serial, kp <= 32
+    bool use_fused = false;
+    FusedPlan fplan;
+    DevBuf fz_idx, fz_slots, fz_count;  // [q0 | t0 | act] ints, P1 partial ring, [count | wdone]
     StreamK sk1b[2], sk2b[2];    // out-of-core: full batch / last batch
     bool norm_valid = false, factors_set = false, factors_valid = false;
     double norm_a2 = 0.0;
@@ -298,7 +302,35 @@ void alloc_factors(oocnmf_ctx* c) {
     ck(cudaMemsetAsync(c->flag.p, 0, 4, c->stream), "memset flag");
 }
 
+// OOCNMF_FUSED=0 keeps the two-pass W half; OOCNMF_FUSED_D sets the P2 lookahead in row
+// blocks (default 2: three 32 MB blocks of A live in L2 at n = 65536); OOCNMF_FUSED_POL picks
+// the L2 policies of the two A loads (0: normal / first, 1: last / first, 2: normal / normal).
+bool fused_wanted(const oocnmf_ctx* c) {
+    const char* e = std::getenv("OOCNMF_FUSED");
+    if (e && e[0] == '0') return false;
+    return c->use_tc && !c->cnmf && fused_supported(c->kp, c->mp, c->np, c->num_sms);
+}
+int env_int(const char* name, int dflt) {
+    const char* e = std::getenv(name);
+    return e && *e ? std::atoi(e) : dflt;
+}
+
+void plan_fused_buffers(oocnmf_ctx* c) {
+    FusedPlan& fp = c->fplan;
+    plan_fused(fp, c->mp, c->np, c->num_sms, env_int("OOCNMF_FUSED_D", 2));
+    std::vector<int> idx;
+    idx.insert(idx.end(), fp.q0.begin(), fp.q0.end());
+    idx.insert(idx.end(), fp.t0.begin(), fp.t0.end());
+    idx.insert(idx.end(), fp.act.begin(), fp.act.end());
+    c->fz_idx.alloc(idx.size() * 4, "fused plan");
+    ck(cudaMemcpy(c->fz_idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice), "H2D fused plan");
+    c->fz_slots.alloc(size_t(fp.NS) * fp.G * kTile * c->kp * 4, "fused P1 slots");
+    c->fz_count.alloc(size_t(2) * fp.NB * 4, "fused counters");
+}
+
 void plan_dense(oocnmf_ctx* c) {
+    c->use_fused = fused_wanted(c);
+    if (c->use_fused) plan_fused_buffers(c);
     const int step = c->use_tc ? kTcStep : kFfmaStep;
     plan_aht(c->sk1, c->mp, c->np, c->num_sms, step);
     plan_wta(c->sk2, c->mp, c->np, c->num_sms, step);
@@ -492,7 +524,33 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         if (timed) record(c, ev[i], s);
     };
     rec(eStart);
-    if (c->kind == Kind::dense) {
+    if (c->kind == Kind::dense && c->use_fused) {
+        // one pass over A: P1, the W update and P2 (W^T A of the new W) in one kernel; then the
+        // Gram of the new W
+        const FusedPlan& fp = c->fplan;
+        ck(cudaMemsetAsync(c->fz_count.p, 0, c->fz_count.bytes, s), "memset fused counters");
+        const int* idx = c->fz_idx.as<int>();
+        static const int pol = env_int("OOCNMF_FUSED_POL", 0);
+        FusedArgs a{};
+        a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = tc::tc_drain_units();
+        a.q0 = idx, a.t0 = idx + fp.G + 1, a.act = idx + 2 * (fp.G + 1);
+        a.p1slots = c->fz_slots.as<float>();
+        a.count = c->fz_count.as<unsigned>(), a.wdone = a.count + fp.NB;
+        a.W = c->W.as<float>(), a.Wcat = c->W_cat.as<float>(), a.HHt = c->HHt.as<float>();
+        a.eps = eps, a.flag = c->flag.as<int>(), a.wta = c->wta();
+        a.pol_p1 = pol == 1 ? 0x14F0000000000000ull : 0x1000000000000000ull;
+        a.pol_p2 = pol == 2 ? 0x1000000000000000ull : 0x12F0000000000000ull;
+        count(c, launch_mu_fused(kp, fp, c->A.as<float>(), c->mp, c->np, c->Ht_cat.as<float>(), a, s), "mu fused");
+        rec(eAht);
+        count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, eps, false,
+                                      c->gram_w.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
+              "W Gram");
+        count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s),
+              "reduce WtW");
+        rec(eWdone);
+        rec(eWta);
+        rec(eReduced);
+    } else if (c->kind == Kind::dense) {
         count(c, pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
         rec(eAht);
         if (c->cnmf) {
@@ -773,7 +831,10 @@ void run_iterations(oocnmf_ctx* c, float eps, uint64_t count, cudaEvent_t* ev) {
         uint64_t(reinterpret_cast<uintptr_t>(c->gram_w.p)), uint64_t(reinterpret_cast<uintptr_t>(c->gram_h.p)),
         uint64_t(c->sk1.G), uint64_t(c->sk1.tiles), uint64_t(c->sk2.G), uint64_t(c->sk2.tiles),
         uint64_t(reinterpret_cast<uintptr_t>(c->chA.seg.p)), uint64_t(reinterpret_cast<uintptr_t>(c->chT.seg.p)),
-        uint64_t(c->chA.C), uint64_t(c->chT.C), uint64_t(fuse_w_update(c)), uint64_t(fuse_h_update(c))};
+        uint64_t(c->chA.C), uint64_t(c->chT.C), uint64_t(fuse_w_update(c)), uint64_t(fuse_h_update(c)),
+        uint64_t(c->use_fused), uint64_t(reinterpret_cast<uintptr_t>(c->fz_idx.p)),
+        uint64_t(reinterpret_cast<uintptr_t>(c->fz_slots.p)), uint64_t(reinterpret_cast<uintptr_t>(c->fz_count.p)),
+        uint64_t(c->fplan.D), uint64_t(c->HHt.p ? reinterpret_cast<uintptr_t>(c->HHt.p) : 0)};
     oocnmf_ctx::Graph* hit = nullptr;
     for (auto& g : c->graphs)
         if (g.key == key) hit = &g;
@@ -862,18 +923,24 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         cudaEvent_t* ev;
     };
     std::vector<Pending> pend;
+    const bool fused_run = c->kind == Kind::dense && c->use_fused;
     auto drain = [&](const Pending& p) {
         cudaEvent_t* ce = p.ev + kEvPerIter * p.iters;
         ck(cudaEventSynchronize(ce[1]), "sync");
         for (uint64_t i = 0; i < p.iters; ++i) {
             cudaEvent_t* e = p.ev + kEvPerIter * i;
-            inf.aht_pass_ms += elapsed(e[eStart], e[eAht]);
-            inf.wta_pass_ms += elapsed(e[eWdone], e[eWta]);
+            if (fused_run) {
+                inf.fused_pass_ms += elapsed(e[eStart], e[eAht]);
+                inf.fused_launches += 1;
+            } else {
+                inf.aht_pass_ms += elapsed(e[eStart], e[eAht]);
+                inf.wta_pass_ms += elapsed(e[eWdone], e[eWta]);
+                inf.aht_pass_launches += 1;
+                inf.wta_pass_launches += 1;
+            }
             inf.w_update_s += elapsed(e[eStart], e[eWdone]) * 1e-3;
             inf.allreduce_s += elapsed(e[eReduced], e[eComm]) * 1e-3;
             inf.h_update_s += (elapsed(e[eWdone], e[eReduced]) + elapsed(e[eComm], e[eHdone])) * 1e-3;
-            inf.aht_pass_launches += 1;
-            inf.wta_pass_launches += 1;
         }
         inf.error_check_s += elapsed(ce[0], ce[1]) * 1e-3;
     };

@@ -137,3 +137,45 @@ def test_config2_two_iterations_match_reference(gpu):
     check_trace(trace, g)
     check_factors(w, h, g)
     assert abs(trace[-1][1] - 0.502504328195) <= 1e-4 * 0.502504328195
+
+
+# ------------------------------------------------------------------ the one-pass kernel
+@pytest.mark.parametrize("m,n,k,lookahead", [
+    (4096, 2048, 16, "2"),     # config 1 shape, kp 16
+    (1536, 1024, 32, "1"),     # NQ = 16 < 148 CTAs: most CTAs publish no P1 partial
+    (333, 517, 7, "2"),        # ragged, one tile of padding each way
+    (2048, 18944, 32, "3"),    # 148 column tiles: one owned tile per CTA
+    (640, 40960, 32, "2"),     # 320 tiles: 2-3 owned tiles per CTA, 5 row blocks
+    (128, 256, 32, "2"),       # one row block (D capped at 1), two column tiles
+])
+def test_fused_pass_matches_two_pass_kernels(gpu, monkeypatch, m, n, k, lookahead):
+    """kernels_fused.cu (A read once per iteration: P1, the distributed W update, P2 from L2)
+    against the two streaming passes + factor-update kernel (OOCNMF_FUSED=0) and the f64
+    reference arithmetic (oracle port) on the same f32 inputs."""
+    a = port.uniform_dense(m, n, 7, 99).astype(np.float32)
+    w0, h0 = port.init_factors(m, n, k, 3)
+    cfg = nmf.NmfConfig(k=k, max_iters=30, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    monkeypatch.setenv("OOCNMF_FUSED_D", lookahead)
+    fused = nmf.nmf_serial(a, cfg)
+    assert fused.info["fused_launches"] == 30
+    monkeypatch.setenv("OOCNMF_FUSED", "0")
+    split = nmf.nmf_serial(a, cfg)
+    assert split.info["fused_launches"] == 0
+    ref = port.nmf_serial(f32(a), k, f32(w0), f32(h0), max_iters=30, interval=10)
+    ef = np.array([e for _, e in fused.error_trace])
+    es = np.array([e for _, e in split.error_trace])
+    np.testing.assert_allclose(ef, es, rtol=2e-6)
+    assert np.all(np.abs(ef - ref.trace_err) <= TRACE_TOL * ref.trace_err)
+    assert rel_fro(fused.w, ref.w) <= FACTOR_TOL and rel_fro(fused.h, ref.h) <= FACTOR_TOL
+    assert rel_fro(fused.w, split.w) <= 1e-4 and rel_fro(fused.h, split.h) <= 1e-4
+
+
+def test_fused_pass_is_deterministic(gpu):
+    a = port.uniform_dense(1024, 4096, 5, 99).astype(np.float32)
+    w0, h0 = port.init_factors(1024, 4096, 32, 1)
+    cfg = nmf.NmfConfig(k=32, max_iters=12, error_check_interval=4, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    r1, r2 = nmf.nmf_serial(a, cfg), nmf.nmf_serial(a, cfg)
+    assert np.array_equal(r1.w, r2.w) and np.array_equal(r1.h, r2.h)
+    assert [e for _, e in r1.error_trace] == [e for _, e in r2.error_trace]

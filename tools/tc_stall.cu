@@ -4,7 +4,7 @@
 // product. build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DOOC_TC_PROFILE -I include \
 //     -I paper_2202_09518_b200/csrc tools/tc_stall.cu paper_2202_09518_b200/csrc/kernels_tc.cu \
-//     paper_2202_09518_b200/csrc/kernels_dense.cu -lcuda -o tools/tc_stall
+//     paper_2202_09518_b200/csrc/kernels_dense.cu paper_2202_09518_b200/csrc/kernels_factor.cu -lcuda -o tools/tc_stall
 #include <cstdio>
 #include <cstdlib>
 
@@ -25,11 +25,11 @@ __global__ void k_fill(float* a, int64_t n, uint32_t salt, float scale) {
     }
 }
 
-// argv: kp mp np [random=0|1] (random: hash-filled A and factors instead of zeros)
+// argv: kp mp np [random=0|1] [reps] (random: hash-filled A and factors instead of zeros)
 int main(int argc, char** argv) {
     const int kp = argc > 1 ? atoi(argv[1]) : 32;
     const int64_t mp = argc > 2 ? atoll(argv[2]) : 65536, np = argc > 3 ? atoll(argv[3]) : 65536;
-    const int reps = 5;
+    const int reps = argc > 5 ? atoi(argv[5]) : 5;
     float *A, *Hc, *Wc, *slots;
     CK(cudaMalloc(&A, size_t(mp) * np * 4));
     CK(cudaMemset(A, 0, size_t(mp) * np * 4));
