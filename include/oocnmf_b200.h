@@ -91,7 +91,7 @@ typedef struct {
     uint64_t gpu_launches; /* all kernels this library launched inside oocnmf_solve */
     double h2d_bytes;      /* host->device bytes moved inside oocnmf_solve (out-of-core) */
     double fused_pass_ms;  /* one-pass dense W half (A read once: A·H^T, W update, W^T·A) */
-    uint64_t fused_launches;
+    uint64_t fused_pass_launches;
 } oocnmf_info;
 
 typedef struct oocnmf_ctx oocnmf_ctx;
@@ -218,6 +218,25 @@ int oocnmf_perturb(oocnmf_ctx* ctx, double delta, uint64_t seed);
 int oocnmf_set_local(oocnmf_ctx* ctx, int local);
 /* Sum a host f64 buffer over the ranks of a communicator context (NCCL, in place). */
 int oocnmf_allreduce_sum_f64(oocnmf_ctx* ctx, double* buf, uint64_t count);
+
+/* ---- collectives of the group (reference CommHandle, include/oocnmf/comm.hpp:48-67) ----
+ * tag: PhaseTag (comm.hpp:13-20): 0 generic, 1 w_update, 2 h_update, 3 error_check, 4 gather,
+ * 5 barrier. All are collective (every rank calls them) and blocking. */
+int oocnmf_allreduce_f64(oocnmf_ctx* ctx, double* buf, uint64_t count, int tag);  /* all_reduce_sum */
+int oocnmf_barrier(oocnmf_ctx* ctx);                                              /* barrier */
+/* CollectiveStats (comm.hpp:28-43): per tag bytes, calls, seconds (device time of the
+ * collectives, the solve's own included); any pointer may be null. */
+int oocnmf_comm_stats(oocnmf_ctx* ctx, uint64_t bytes[6], uint64_t calls[6], double seconds[6]);
+int oocnmf_comm_reset_stats(oocnmf_ctx* ctx);
+/* Failure semantics (src/comm.cpp:89-111: 60 s timeout, then the group is poisoned): a host
+ * wait that sees no collective complete for `seconds` (or an NCCL async error) aborts the
+ * communicator (ncclCommAbort) and returns OOCNMF_ERR_COMM; every later collective on the
+ * context fails with OOCNMF_ERR_COMM. Default 60 s. */
+int oocnmf_set_comm_timeout(oocnmf_ctx* ctx, double seconds);
+/* spawn_group(n, Backend::threads) (comm.hpp:80-82): n contexts of one process on
+ * devices[0..n) (distinct), one NCCL communicator clique (ncclCommInitAll); each context is
+ * then driven by its own host thread (run_distributed_threads, nmf_distributed.hpp:40). */
+int oocnmf_ctx_create_group(int n, const int* devices, oocnmf_ctx** out);
 /* select_k (model_selection.cpp:316-406) on the full A resident in ctx (row0 = 0, rows = m):
  * P perturbed MU runs per k on the GPU, then cluster_columns / silhouette / selection rule on
  * the host. On a communicator context the runs of each k are spread over the ranks as

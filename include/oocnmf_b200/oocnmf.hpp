@@ -223,23 +223,77 @@ struct MemoryReport {
 MemoryReport memory_estimate(const PartitionPlan& plan, double density, index_t budget_bytes, index_t n_cb = 1);
 
 // ---- distributed (reference: include/oocnmf/nmf_distributed.hpp, comm.hpp) ----
-/// One rank of an NCCL group (one process or host thread per GPU). Created collectively:
-/// rank 0 calls new_unique_id(), ships it to the others, every rank constructs a handle.
+/// Group transports (comm.hpp:10). B200: loopback (one rank) and threads (one process, one
+/// GPU per rank thread, NCCL clique); multi-process groups use the CommHandle constructor with
+/// an NCCL unique id (the reference's tcp backend role). tcp is not offered.
+enum class Backend { loopback, threads, tcp };
+Backend backend_from_string(const std::string& s);
+
+/// Tags collectives so stats can be attributed to algorithm phases (comm.hpp:13-20).
+enum class PhaseTag : std::uint32_t {
+    generic = 0,
+    w_update = 1,
+    h_update = 2,
+    error_check = 3,
+    gather = 4,
+    barrier = 5,
+};
+inline constexpr std::size_t kNumPhaseTags = 6;
+
+/// comm.hpp:28-43. seconds = device time of the collectives (NCCL over NVLink).
+struct CollectiveStats {
+    struct PerTag {
+        index_t bytes = 0;
+        index_t calls = 0;
+        double seconds = 0;
+    };
+    std::array<PerTag, kNumPhaseTags> per_tag{};
+    PerTag& operator[](PhaseTag t) { return per_tag[static_cast<std::size_t>(t)]; }
+    const PerTag& operator[](PhaseTag t) const { return per_tag[static_cast<std::size_t>(t)]; }
+    index_t total_bytes() const;
+    index_t total_calls() const;
+    double total_seconds() const;
+};
+
+/// One rank of an NCCL group (one process or host thread per GPU). Multi-process: rank 0
+/// calls new_unique_id(), ships it to the others, every rank constructs a handle. In one
+/// process: spawn_group(n, Backend::threads). Collectives are blocking; a collective that makes
+/// no progress for timeout_s (default 60 s, comm.cpp:89-111) throws CommError and poisons the
+/// group (the communicator is aborted, every later collective throws).
 class CommHandle {
 public:
     using UniqueId = std::array<unsigned char, 128>;
     static UniqueId new_unique_id();
     CommHandle() = default;
-    CommHandle(int rank, int size, int device, const UniqueId& id);
+    CommHandle(int rank, int size, int device, const UniqueId& id, double timeout_s = 60.0);
+    /// Adopt a context made by oocnmf_ctx_create_group (takes ownership).
+    CommHandle(oocnmf_ctx* ctx, int rank, int size, int device);
     int rank() const { return rank_; }
     int size() const { return size_; }
     int device() const { return device_; }
     oocnmf_ctx* context() const { return ctx_.get(); }
+    /// In-place elementwise sum across all ranks (comm.hpp:61).
+    void all_reduce_sum(DenseMatrix& buffer, PhaseTag tag);
+    /// Returns once every rank has entered.
+    void barrier();
+    /// This rank's collective statistics, the solver's own collectives included.
+    const CollectiveStats& stats() const;
+    void reset_stats();
+    void set_timeout(double seconds);
 
 private:
     int rank_ = 0, size_ = 1, device_ = 0;
     std::shared_ptr<oocnmf_ctx> ctx_;
+    std::shared_ptr<CollectiveStats> stats_ = std::make_shared<CollectiveStats>();
 };
+
+/// All handles of an in-process group (comm.hpp:75-77).
+struct CommGroup {
+    std::vector<CommHandle> handles;
+};
+/// loopback: n must be 1. threads: n handles on GPUs 0..n-1 sharing one NCCL clique, one per
+/// worker thread (comm.hpp:80-82).
+CommGroup spawn_group(int n, Backend backend, double timeout_s = 60.0);
 
 struct ASource {
     MatrixRef mem;
@@ -264,6 +318,11 @@ struct StoreCounters {
 /// Returns the gathered W (m x k) and replicated H on every rank.
 NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan, CommHandle& comm,
                           const StoreConfig& store_cfg = {}, StoreCounters* store_counters_out = nullptr);
+/// Convenience driver: runs all ranks of a threads-backend group on worker threads, one GPU
+/// each, and returns the per-rank results (index = rank) (nmf_distributed.hpp:40-43).
+std::vector<NmfResult> run_distributed_threads(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan,
+                                               const StoreConfig& store_cfg = {},
+                                               std::vector<CollectiveStats>* stats_out = nullptr);
 
 // ---- matrix files (reference: include/oocnmf/io.hpp) ----
 struct AnyMatrix {

@@ -5,6 +5,7 @@ The product is ``lib/liboocnmf_b200.so`` (C-ABI: ``include/oocnmf_b200.h``; C++ 
 ``oocnmf::`` API names.
 """
 from .nmf import (  # noqa: F401
+    CollectiveStats,
     ColumnClusters,
     CommError,
     Context,
@@ -19,6 +20,7 @@ from .nmf import (  # noqa: F401
     NmfResult,
     PartitionPlan,
     PhaseCounters,
+    PhaseTag,
     SelectionConfig,
     SelectionReport,
     ShapeError,
@@ -35,9 +37,11 @@ from .nmf import (  # noqa: F401
     nmf_distributed,
     nmf_serial,
     pearson_correlation_matrix,
+    run_distributed_threads,
     perturb_dense,
     perturb_sparse,
     select_k,
+    spawn_group,
     select_k_distributed,
     split_even,
 )

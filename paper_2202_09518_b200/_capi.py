@@ -32,7 +32,7 @@ class Info(C.Structure):
                 ("iterations_run", u64), ("converged", i32), ("reserved", i32), ("n_trace", u64),
                 ("aht_pass_ms", dbl), ("wta_pass_ms", dbl), ("aht_pass_launches", u64),
                 ("wta_pass_launches", u64), ("gpu_launches", u64), ("h2d_bytes", dbl),
-                ("fused_pass_ms", dbl), ("fused_launches", u64)]
+                ("fused_pass_ms", dbl), ("fused_pass_launches", u64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}
@@ -95,6 +95,12 @@ _SIGS = {
     "oocnmf_perturb": ([vp, dbl, u64], C.c_int),
     "oocnmf_set_local": ([vp, C.c_int], C.c_int),
     "oocnmf_allreduce_sum_f64": ([vp, pd, u64], C.c_int),
+    "oocnmf_allreduce_f64": ([vp, pd, u64, C.c_int], C.c_int),
+    "oocnmf_barrier": ([vp], C.c_int),
+    "oocnmf_comm_stats": ([vp, pu, pu, pd], C.c_int),
+    "oocnmf_comm_reset_stats": ([vp], C.c_int),
+    "oocnmf_set_comm_timeout": ([vp, dbl], C.c_int),
+    "oocnmf_ctx_create_group": ([C.c_int, C.POINTER(C.c_int), C.POINTER(vp)], C.c_int),
     "oocnmf_select_k": ([vp, C.POINTER(SelectionConfig), C.POINTER(KRecord), u64, pd, pi64, C.c_char_p, u64],
                         C.c_int),
     "oocnmf_cluster_silhouette": ([pd, u64, u64, u64, pd, pd, pd, pd, pu, pi64], C.c_int),

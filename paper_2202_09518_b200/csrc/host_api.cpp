@@ -4,6 +4,9 @@
 #include <cmath>
 
 #include "oocnmf_b200/oocnmf.hpp"
+
+#include <exception>
+#include <thread>
 #include "selection.hpp"
 
 namespace oocnmf {
@@ -290,10 +293,86 @@ CommHandle::UniqueId CommHandle::new_unique_id() {
     return id;
 }
 
-CommHandle::CommHandle(int rank, int size, int device, const UniqueId& id) : rank_(rank), size_(size), device_(device) {
+CommHandle::CommHandle(int rank, int size, int device, const UniqueId& id, double timeout_s)
+    : rank_(rank), size_(size), device_(device) {
     oocnmf_ctx* c = nullptr;
     throw_status(oocnmf_ctx_create_comm(device, rank, size, id.data(), &c));
     ctx_ = std::shared_ptr<oocnmf_ctx>(c, [](oocnmf_ctx* p) { oocnmf_ctx_destroy(p); });
+    set_timeout(timeout_s);
+}
+
+CommHandle::CommHandle(oocnmf_ctx* ctx, int rank, int size, int device)
+    : rank_(rank), size_(size), device_(device), ctx_(ctx, [](oocnmf_ctx* p) { oocnmf_ctx_destroy(p); }) {}
+
+void CommHandle::all_reduce_sum(DenseMatrix& buffer, PhaseTag tag) {
+    if (!ctx_) throw CommError("all_reduce_sum: CommHandle has no device context");
+    throw_status(oocnmf_allreduce_f64(ctx_.get(), buffer.data(), buffer.size(), int(tag)));
+}
+
+void CommHandle::barrier() {
+    if (!ctx_) throw CommError("barrier: CommHandle has no device context");
+    throw_status(oocnmf_barrier(ctx_.get()));
+}
+
+const CollectiveStats& CommHandle::stats() const {
+    if (ctx_) {
+        std::uint64_t b[kNumPhaseTags], c[kNumPhaseTags];
+        double sec[kNumPhaseTags];
+        throw_status(oocnmf_comm_stats(ctx_.get(), b, c, sec));
+        for (std::size_t t = 0; t < kNumPhaseTags; ++t)
+            stats_->per_tag[t] = {index_t(b[t]), index_t(c[t]), sec[t]};
+    }
+    return *stats_;
+}
+
+void CommHandle::reset_stats() {
+    if (ctx_) throw_status(oocnmf_comm_reset_stats(ctx_.get()));
+    *stats_ = CollectiveStats{};
+}
+
+void CommHandle::set_timeout(double seconds) {
+    if (ctx_) throw_status(oocnmf_set_comm_timeout(ctx_.get(), seconds));
+}
+
+index_t CollectiveStats::total_bytes() const {
+    index_t s = 0;
+    for (const auto& t : per_tag) s += t.bytes;
+    return s;
+}
+index_t CollectiveStats::total_calls() const {
+    index_t s = 0;
+    for (const auto& t : per_tag) s += t.calls;
+    return s;
+}
+double CollectiveStats::total_seconds() const {
+    double s = 0;
+    for (const auto& t : per_tag) s += t.seconds;
+    return s;
+}
+
+Backend backend_from_string(const std::string& s) {
+    if (s == "loopback") return Backend::loopback;
+    if (s == "threads") return Backend::threads;
+    if (s == "tcp") return Backend::tcp;
+    throw ShapeError("unknown comm backend '" + s + "' (expected loopback|threads|tcp)");
+}
+
+CommGroup spawn_group(int n, Backend backend, double timeout_s) {
+    if (n < 1) throw ShapeError("spawn_group: need at least one rank");
+    if (backend == Backend::loopback && n != 1) throw ShapeError("spawn_group: loopback needs n == 1");
+    if (backend == Backend::tcp)
+        throw ShapeError("spawn_group: the tcp backend is not offered; one process per GPU uses "
+                         "CommHandle(rank, size, device, unique_id) over NCCL");
+    std::vector<int> devs(static_cast<std::size_t>(n));
+    for (int r = 0; r < n; ++r) devs[std::size_t(r)] = r;
+    std::vector<oocnmf_ctx*> cs(static_cast<std::size_t>(n), nullptr);
+    throw_status(oocnmf_ctx_create_group(n, devs.data(), cs.data()));
+    CommGroup g;
+    for (int r = 0; r < n; ++r) {
+        g.handles.emplace_back(cs[std::size_t(r)], r, n, r);
+        g.handles.back().set_timeout(timeout_s);
+    }
+    return g;
 }
 
 namespace {
@@ -412,6 +491,33 @@ NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const Partitio
         store_counters_out->bytes_read = index_t(info.h2d_bytes);
     }
     return res;
+}
+
+std::vector<NmfResult> run_distributed_threads(const ASource& a, const NmfConfig& cfg, const PartitionPlan& plan,
+                                               const StoreConfig& store_cfg, std::vector<CollectiveStats>* stats_out) {
+    auto group = spawn_group(plan.n_workers, plan.n_workers == 1 ? Backend::loopback : Backend::threads);
+    const std::size_t n = std::size_t(plan.n_workers);
+    std::vector<NmfResult> results(n);
+    std::vector<std::exception_ptr> errors(n);
+    std::vector<std::thread> threads;
+    for (std::size_t r = 0; r < n; ++r)
+        threads.emplace_back([&, r] {
+            try {
+                NmfConfig c = cfg;
+                c.device = group.handles[r].device();
+                results[r] = nmf_distributed(a, c, plan, group.handles[r], store_cfg);
+            } catch (...) {
+                errors[r] = std::current_exception();
+            }
+        });
+    for (auto& t : threads) t.join();
+    if (stats_out) {
+        stats_out->clear();
+        for (auto& h : group.handles) stats_out->push_back(h.stats());
+    }
+    for (auto& e : errors)
+        if (e) std::rethrow_exception(e);
+    return results;
 }
 
 // ------------------------------------------------------------------------- model selection

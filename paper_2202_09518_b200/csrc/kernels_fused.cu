@@ -84,6 +84,20 @@ __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+// Developer stall profile (tools/fz_stall.cu, -DOOC_FZ_PROFILE): cycles each role spends in
+// each wait, summed over CTAs. Compiled out of the product.
+#ifdef OOC_FZ_PROFILE
+__device__ unsigned long long g_fz_prof[16];
+#define FZ_WAIT(idx, call)              \
+    do {                                \
+        const long long t_ = clock64(); \
+        call;                           \
+        prof[idx] += clock64() - t_;    \
+    } while (0)
+#else
+#define FZ_WAIT(idx, call) call
+#endif
+
 template <int KP>
 __global__ void __launch_bounds__(512, 1)
     k_mu_fused(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
@@ -128,6 +142,10 @@ __global__ void __launch_bounds__(512, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+#ifdef OOC_FZ_PROFILE
+    long long prof[16] = {};
+    const long long t_start = clock64();
+#endif
     auto a_stage = [&](int s) { return smem + s * C::A_BYTES; };
     auto b_stage = [&](int s) { return smem + C::A_STAGES * C::A_BYTES + s * C::B_BYTES; };
     const int du = p.drain_units;
@@ -138,13 +156,13 @@ __global__ void __launch_bounds__(512, 1)
             int sa = 0, sb = 0;
             uint32_t pha = 0, phb = 0;
             auto load_a = [&](const CUtensorMap* m, int y, int z, uint64_t pol) {
-                mbar_wait(emptyA + sa, pha ^ 1u);
+                FZ_WAIT(0, mbar_wait(emptyA + sa, pha ^ 1u));
                 mbar_expect_tx(fullA + sa, C::A_BYTES);
                 tma_load_3d(a_stage(sa), m, fullA + sa, 0, y, z, pol);
                 if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
             };
             auto load_b = [&](const CUtensorMap* m, int y, uint64_t pol) {
-                mbar_wait(emptyB + sb, phb ^ 1u);
+                FZ_WAIT(1, mbar_wait(emptyB + sb, phb ^ 1u));
                 mbar_expect_tx(fullB + sb, C::B_BYTES);
                 tma_load_3d(b_stage(sb), m, fullB + sb, 0, y, 0, pol);
                 if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
@@ -155,14 +173,19 @@ __global__ void __launch_bounds__(512, 1)
                         load_a(&tmA1, s * 128, 2 * q, p.pol_p1);     // rows of block s, K-atoms 2q, 2q+1
                         load_b(&tmB1, q * C::BK, kEvictLast);        // Ht_cat rows of chunk q
                     }
-                if (s >= D && t1 > t0) {
+                if (s >= D && t1 == t0) {
+                    // no owned tiles: still wait for block s - D's update, which throttles this
+                    // CTA's P1 publishing to the slot ring (block s + 1 + ... reuses slots of
+                    // blocks whose updaters must have read them: NS = D + 2)
+                    FZ_WAIT(2, wait_count(p.wdone + (s - D), 128u));
+                } else if (s >= D) {
                     const int b = s - D;
                     bool ready = false;
                     for (int j = t0; j < t1; ++j)
                         for (int h = 0; h < 2; ++h) {
                             load_a(&tmA2, b * 128 + 64 * h, 4 * j, p.pol_p2);  // 64 rows x 128 cols
                             if (!ready) {  // the block's new W rows (written by the updaters)
-                                wait_count(p.wdone + b, 128u);
+                                FZ_WAIT(2, wait_count(p.wdone + b, 128u));
                                 fence_proxy_async_global();
                                 ready = true;
                             }
@@ -177,9 +200,9 @@ __global__ void __launch_bounds__(512, 1)
         uint32_t phb = 0, rph = 0, aph = 0;
         bool open = true;
         auto unit = [&](bool close) {
-            if (open) mbar_wait(accempty + buf, aph ^ 1u);
-            mbar_wait(fullB + sb, phb);
-            mbar_wait(split + r, rph);
+            if (open) FZ_WAIT(5, mbar_wait(accempty + buf, aph ^ 1u));
+            FZ_WAIT(6, mbar_wait(fullB + sb, phb));
+            FZ_WAIT(7, mbar_wait(split + r, rph));
             tc_fence_after();
             const uint32_t d = tmem + uint32_t(buf * C::ACC_COLS);
             const uint64_t db0 = desc_mnmajor(smem_u32(b_stage(sb)), 0, C::ATOM_STRIDE);
@@ -228,7 +251,7 @@ __global__ void __launch_bounds__(512, 1)
         bool bad = false;
         for (int64_t g = cta; g < int64_t(NB) * 128; g += G) {
             const int b = int(g >> 7), row = int(g & 127);
-            wait_count(p.count + b, target);
+            FZ_WAIT(9, wait_count(p.count + b, target));
             const float* base = p.p1slots + (int64_t(b % p.NS) * G) * (128 * KP) + row * KP + j;
             float acc = 0.f;
             int c = c_lo;
@@ -279,8 +302,8 @@ __global__ void __launch_bounds__(512, 1)
         int sa = 0, rs = 0;
         uint32_t pha = 0, rph = 0;
         auto unit = [&](bool p1) {
-            mbar_wait(fullA + sa, pha);
-            mbar_wait(afree + rs, rph ^ 1u);
+            FZ_WAIT(3, mbar_wait(fullA + sa, pha));
+            FZ_WAIT(4, mbar_wait(afree + rs, rph ^ 1u));
             tc_fence_after();
             const uint8_t* sA = a_stage(sa);
             const uint32_t dst = tmem + lane_bits + uint32_t(C::A_COL0 + rs * C::ASLOT_COLS);
@@ -339,7 +362,7 @@ __global__ void __launch_bounds__(512, 1)
         uint32_t aph = 0;
         // fold one closed chain D' = [H | L] into acc
         auto take = [&]() {
-            mbar_wait(accfull + buf, aph);
+            FZ_WAIT(8, mbar_wait(accfull + buf, aph));
             tc_fence_after();
             const uint32_t src = tmem + lane_bits + uint32_t(buf * C::ACC_COLS);
             if constexpr (KP == 16) {
@@ -422,6 +445,15 @@ __global__ void __launch_bounds__(512, 1)
             }
         }
     }
+#ifdef OOC_FZ_PROFILE
+    // per role: lane 0 of warp 0 (producer), 1 (MMA), 2 (updater), 4 (split), 12 (drain)
+    if (lane == 0 && (warp == 0 || warp == 1 || warp == 2 || warp == 4 || warp == 12)) {
+        for (int j = 0; j < 10; ++j)
+            if (prof[j]) atomicAdd(&g_fz_prof[j], (unsigned long long)prof[j]);
+        atomicAdd(&g_fz_prof[10 + (warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == 4 ? 3 : 4)],
+                  (unsigned long long)(clock64() - t_start));
+    }
+#endif
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
@@ -493,6 +525,16 @@ void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahea
         if (fp.q0[c + 1] > fp.q0[c]) fp.act.push_back(c);
     fp.G1 = int(fp.act.size());
 }
+
+#ifdef OOC_FZ_PROFILE
+void fz_profile_read(unsigned long long* out16, bool reset) {
+    cudaMemcpyFromSymbol(out16, g_fz_prof, 16 * sizeof(unsigned long long));
+    if (reset) {
+        unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(g_fz_prof, z, sizeof(z));
+    }
+}
+#endif
 
 cudaError_t launch_mu_fused(int kp, const FusedPlan& fp, const float* A, int64_t mp, int64_t np, const float* Ht_cat,
                             const FusedArgs& args, cudaStream_t s) {

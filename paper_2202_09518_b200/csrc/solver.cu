@@ -22,6 +22,8 @@
 #include <cstring>
 #include <string>
 #include <thread>
+#include <deque>
+#include <mutex>
 #include <vector>
 
 #include "kernels.h"
@@ -190,6 +192,21 @@ struct oocnmf_ctx {
     DevBuf A0, v0, vT0;
     bool pristine = false, local = false;
     bool collective() const { return nranks > 1 && !local; }
+    // Collective bookkeeping (reference CommHandle stats, include/oocnmf/comm.hpp:28-43) and the
+    // progress watchdog (src/comm.cpp:89-111): every collective is bracketed by two events; a
+    // host wait that sees no collective complete for comm_timeout seconds aborts the
+    // communicator (ncclCommAbort) and poisons the context (every later collective fails).
+    struct CollMark {
+        cudaEvent_t beg, end;
+        int tag;
+    };
+    std::deque<CollMark> marks;
+    std::vector<cudaEvent_t> ev_pool;
+    cudaEvent_t mark_beg = nullptr;
+    uint64_t tag_bytes[6] = {}, tag_calls[6] = {};
+    double tag_secs[6] = {};
+    double comm_timeout = 60.0;
+    bool poisoned = false;
     // RNMF on CSR: W^T A is n x k (537 MB at config 3), so instead of all-reducing it and
     // repeating the n-row H update on every rank, the ranks reduce-scatter it, update their
     // own n/N rows of H, and all-gather H (the same bytes as the all-reduce, 1/N of the update).
@@ -214,6 +231,95 @@ void need_problem(oocnmf_ctx* c) {
 void count(oocnmf_ctx* c, cudaError_t e, const char* what) {
     ck(e, what);
     ++c->launches;
+}
+
+// ------------------------------------------------------------------ collectives
+// PhaseTag values (include/oocnmf/comm.hpp:13-20)
+enum Tag { kTagGeneric = 0, kTagW = 1, kTagH = 2, kTagErr = 3, kTagGather = 4, kTagBarrier = 5 };
+
+cudaEvent_t pool_event(oocnmf_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+// Open / close the bracket of one collective (or one NCCL group) on stream s.
+void coll_begin(oocnmf_ctx* c, cudaStream_t s) {
+    if (!c->comm) return;
+    c->mark_beg = pool_event(c);
+    ck(cudaEventRecord(c->mark_beg, s), "event");
+}
+void coll_end(oocnmf_ctx* c, cudaStream_t s, int tag, size_t bytes) {
+    if (!c->comm || !c->mark_beg) return;
+    cudaEvent_t e = pool_event(c);
+    ck(cudaEventRecord(e, s), "event");
+    c->marks.push_back({c->mark_beg, e, tag});
+    c->mark_beg = nullptr;
+    c->tag_bytes[tag] += bytes;
+    c->tag_calls[tag] += 1;
+}
+// Retire completed collectives (their device time goes to the tag); returns how many.
+size_t reap_marks(oocnmf_ctx* c) {
+    size_t n = 0;
+    while (!c->marks.empty()) {
+        const auto& m = c->marks.front();
+        const cudaError_t q = cudaEventQuery(m.end);
+        if (q == cudaErrorNotReady) break;
+        if (q != cudaSuccess) ck(q, "collective event");
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, m.beg, m.end) == cudaSuccess) c->tag_secs[m.tag] += ms * 1e-3;
+        cudaGetLastError();
+        c->ev_pool.push_back(m.beg);
+        c->ev_pool.push_back(m.end);
+        c->marks.pop_front();
+        ++n;
+    }
+    return n;
+}
+[[noreturn]] void abort_comm(oocnmf_ctx* c, const std::string& why) {
+    if (c->comm) ncclCommAbort(c->comm);  // NCCL kernels of the group exit; the stream drains
+    c->comm = nullptr;
+    c->poisoned = true;
+    cudaStreamSynchronize(c->stream);
+    cudaGetLastError();
+    for (auto& m : c->marks) c->ev_pool.push_back(m.beg), c->ev_pool.push_back(m.end);
+    c->marks.clear();
+    fail(OOCNMF_ERR_COMM, "rank " + std::to_string(c->rank) + " of " + std::to_string(c->nranks) + ": " + why +
+                              "; communicator aborted (the group is poisoned)");
+}
+void need_comm(const oocnmf_ctx* c) {
+    if (c->poisoned) fail(OOCNMF_ERR_COMM, "communicator was aborted after an earlier collective failure");
+}
+// Host wait for an event (or the whole stream when e is null). With a communicator it polls:
+// no collective completing for comm_timeout seconds, or an NCCL async error, aborts the group
+// instead of hanging on a dead peer.
+void wait_for(oocnmf_ctx* c, cudaStream_t s, cudaEvent_t e, const char* what) {
+    if (!c->comm) {
+        ck(e ? cudaEventSynchronize(e) : cudaStreamSynchronize(s), what);
+        return;
+    }
+    auto last = std::chrono::steady_clock::now();
+    for (int spins = 0;; ++spins) {
+        const cudaError_t q = e ? cudaEventQuery(e) : cudaStreamQuery(s);
+        if (reap_marks(c)) last = std::chrono::steady_clock::now();
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) ck(q, what);
+        ncclResult_t ar = ncclSuccess;
+        if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
+            abort_comm(c, std::string("NCCL async error (") + ncclGetErrorString(ar) + ") while waiting for " + what);
+        const double idle = std::chrono::duration<double>(std::chrono::steady_clock::now() - last).count();
+        if (!c->marks.empty() && idle > c->comm_timeout)
+            abort_comm(c, "no collective completed for " + std::to_string(c->comm_timeout) +
+                              " s while waiting for " + what + " (unresponsive peer)");
+        if (spins < 4096)
+            std::this_thread::yield();
+        else
+            std::this_thread::sleep_for(std::chrono::microseconds(100));
+    }
 }
 
 // Column-chunked SpMM plan (kernels_sparse.cu, launch_spmm_seg): chunk the gathered operand
@@ -387,9 +493,13 @@ void compute_norm(oocnmf_ctx* c) {
     }
     count(c, launch_reduce_f64(slots, sqnorm_grid(), out, c->stream), "reduce_f64");
 reduced:
-    if (c->collective()) nck(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
+    if (c->collective()) {
+        coll_begin(c, c->stream);
+        nck(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
+        coll_end(c, c->stream, kTagErr, 8);  // ||A||^2 (src/nmf_distributed.cpp:232, error_check)
+    }
     ck(cudaMemcpyAsync(&c->norm_a2, out, 8, cudaMemcpyDeviceToHost, c->stream), "D2H norm");
-    ck(cudaStreamSynchronize(c->stream), "sync");
+    wait_for(c, c->stream, nullptr, "||A||^2 all-reduce");
     c->norm_valid = true;
 }
 
@@ -421,12 +531,14 @@ void finish_hht(oocnmf_ctx* c, int64_t rows, bool partial) {
                                  c->HHt.as<float>(), c->HHt64.as<double>(), c->stream),
           "reduce HHt");
     if (partial) {
+        coll_begin(c, c->stream);
         nck(ncclGroupStart(), "ncclGroupStart");
         nck(ncclAllReduce(c->HHt.p, c->HHt.p, size_t(kp) * kp, ncclFloat, ncclSum, c->comm, c->stream),
             "allreduce HHt");
         nck(ncclAllReduce(c->HHt64.p, c->HHt64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, c->stream),
             "allreduce HHt64");
         nck(ncclGroupEnd(), "ncclGroupEnd");
+        coll_end(c, c->stream, kTagW, size_t(kp) * kp * 12);  // CNMF HH^T (nmf_distributed.cpp:116)
     }
 }
 
@@ -442,9 +554,12 @@ void gram_h(oocnmf_ctx* c) {
 // CNMF: A·H^T of this rank's column slab (in N1) summed over the ranks before the
 // (replicated) W update (src/nmf_distributed.cpp:124).
 void allreduce_aht(oocnmf_ctx* c) {
-    if (c->cnmf && c->collective())
+    if (c->cnmf && c->collective()) {
+        coll_begin(c, c->stream);
         nck(ncclAllReduce(c->N1.p, c->N1.p, size_t(c->mp) * c->kp, ncclFloat, ncclSum, c->comm, c->stream),
             "allreduce AHt");
+        coll_end(c, c->stream, kTagW, size_t(c->mp) * c->kp * 4);  // nmf_distributed.cpp:124
+    }
 }
 
 // A timing event: inside a graph capture it must be an external event-record node.
@@ -507,9 +622,11 @@ void spmm_wta_reduce_scatter(oocnmf_ctx* c, cudaStream_t s) {
         }
         ck(cudaEventRecord(c->ev_rs[ch], s), "event");
         ck(cudaStreamWaitEvent(c->comm_stream, c->ev_rs[ch], 0), "wait");
+        coll_begin(c, c->comm_stream);
         nck(ncclReduceScatter(base, c->wta() + size_t(h0 + r0) * kp, size_t(len) * kp, ncclFloat, ncclSum, c->comm,
                               c->comm_stream),
             "reduce-scatter WtA (chunk)");
+        coll_end(c, c->comm_stream, kTagH, size_t(N) * len * kp * 4);
     }
     ck(cudaEventRecord(c->ev_rs[oocnmf_ctx::kMaxRsChunks], c->comm_stream), "event");
     c->rs_done = true;
@@ -666,25 +783,29 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         const size_t slice = size_t(hr) * kp;
         float* wta = c->wta();
         if (c->rs_done) ck(cudaStreamWaitEvent(s, c->ev_rs[oocnmf_ctx::kMaxRsChunks], 0), "wait reduce-scatter");
+        coll_begin(c, s);
         nck(ncclGroupStart(), "ncclGroupStart");
         if (!c->rs_done)
             nck(ncclReduceScatter(wta, wta + size_t(c->rank) * slice, slice, ncclFloat, ncclSum, c->comm, s),
                 "reduce-scatter WtA");
-        c->rs_done = false;
         nck(ncclAllReduce(c->wtw(), c->wtw(), size_t(kp) * kp, ncclFloat, ncclSum, c->comm, s), "allreduce WtW");
         nck(ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
             "allreduce WtW64");
         nck(ncclGroupEnd(), "ncclGroupEnd");
+        coll_end(c, s, kTagH, (c->rs_done ? 0 : size_t(c->nranks) * slice * 4) + size_t(kp) * kp * 12);
+        c->rs_done = false;
     } else if (c->collective() && !c->cnmf) {
         // One fused NCCL launch: the packed f32 [W^T A | W^T W] the update consumes and the f64
         // W^T W the trace-form error consumes. (CNMF: W^T A of the column slab and W^T W of the
         // replicated W are already complete on every rank.)
+        coll_begin(c, s);
         nck(ncclGroupStart(), "ncclGroupStart");
         nck(ncclAllReduce(c->packed.p, c->packed.p, size_t(c->packed_count()), ncclFloat, ncclSum, c->comm, s),
             "allreduce [WtA|WtW]");
         nck(ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
             "allreduce WtW64");
         nck(ncclGroupEnd(), "ncclGroupEnd");
+        coll_end(c, s, kTagH, size_t(c->packed_count()) * 4 + size_t(kp) * kp * 8);  // nmf_distributed.cpp:171,178
     }
     if (timed) record(c, ev[eComm], s);
     float* hcat = htlo(c);
@@ -700,8 +821,12 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
               "H update");
     }
     if (c->shard_h())
+    {
+        coll_begin(c, s);
         nck(ncclAllGather(c->Ht.as<float>() + h0 * kp, c->Ht.p, size_t(hr) * kp, ncclFloat, c->comm, s),
             "all-gather H");
+        coll_end(c, s, kTagH, size_t(c->nranks) * hr * kp * 4);
+    }
     finish_hht(c, hr, c->collective() && (c->cnmf || c->shard_h()));
     if (timed) record(c, ev[eHdone], s);
 }
@@ -731,7 +856,9 @@ void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
     if (c->collective() && (c->cnmf || c->shard_h())) {
         // CNMF / sharded H: <W^T A, H> is a sum over the ranks' slabs
         count(c, launch_reduce_f64(eslots, n_err, scal + kCross, s), "reduce cross");
+        coll_begin(c, s);
         nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s), "allreduce cross");
+        coll_end(c, s, kTagErr, 8);
         eslots = scal + kCross;
         n_err = 1;
     }
@@ -744,8 +871,11 @@ void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
                                            c->Ht.as<float>(), c->red_slots.as<double>(), s, pred),
                   "residual");
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kRes, s), "reduce");
-            if (c->collective())
+            if (c->collective()) {
+                coll_begin(c, s);
                 nck(ncclAllReduce(scal + kRes, scal + kRes, 1, ncclDouble, ncclSum, c->comm, s), "allreduce res");
+                coll_end(c, s, kTagErr, 8);  // nmf_distributed.cpp:254
+            }
             count(c, launch_finalize_error(kp, nullptr, 0, c->WtW64.as<double>(), c->HHt64.as<double>(),
                                            scal + kNormA2, scal + kRes, out, s, pred),
                   "finalize direct");
@@ -755,9 +885,12 @@ void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
                                          pred),
                   "cross");
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kCross, s), "reduce");
-            if (c->collective())
+            if (c->collective()) {
+                coll_begin(c, s);
                 nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s),
                     "allreduce cross");
+                coll_end(c, s, kTagErr, 8);
+            }
             count(c, launch_finalize_error(kp, scal + kCross, 1, c->WtW64.as<double>(), c->HHt64.as<double>(),
                                            scal + kNormA2, nullptr, out, s, pred),
                   "finalize direct");
@@ -893,6 +1026,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     if (cfg->error_mode == 1 && c->kind == Kind::host)
         fail(OOCNMF_ERR_SHAPE, "error_mode=direct is not supported out-of-core");
     if (c->kind == Kind::none) fail(OOCNMF_ERR_SHAPE, "no A loaded");
+    if (c->collective()) need_comm(c);
 
     const auto t0 = std::chrono::steady_clock::now();
     c->launches = 0;
@@ -926,12 +1060,12 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     const bool fused_run = c->kind == Kind::dense && c->use_fused;
     auto drain = [&](const Pending& p) {
         cudaEvent_t* ce = p.ev + kEvPerIter * p.iters;
-        ck(cudaEventSynchronize(ce[1]), "sync");
+        wait_for(c, c->stream, ce[1], "an iteration block");
         for (uint64_t i = 0; i < p.iters; ++i) {
             cudaEvent_t* e = p.ev + kEvPerIter * i;
             if (fused_run) {
                 inf.fused_pass_ms += elapsed(e[eStart], e[eAht]);
-                inf.fused_launches += 1;
+                inf.fused_pass_launches += 1;
             } else {
                 inf.aht_pass_ms += elapsed(e[eStart], e[eAht]);
                 inf.wta_pass_ms += elapsed(e[eWdone], e[eWta]);
@@ -964,7 +1098,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     // decide on the check enqueued as block bb (its values were copied to hpin[2 (bb & 1)]);
     // returns true when the solve stops there
     auto decide = [&](uint64_t bb, cudaEvent_t done) -> bool {
-        ck(cudaEventSynchronize(done), "sync check");
+        wait_for(c, c->stream, done, "an error check");
         double e = 0.0;
         int f = 0;
         std::memcpy(&e, c->hpin + 2 * (bb & 1), 8);
@@ -1006,7 +1140,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         if (sync_each) {
             if (b > 0 && decide(b - 1, prev_done)) {
                 // stop at check b - 1: drop block b and restore the factors as they were there
-                ck(cudaStreamSynchronize(c->stream), "sync");
+                wait_for(c, c->stream, nullptr, "the discarded block");
                 ck(cudaMemcpyAsync(c->W.p, c->snapW[(b - 1) & 1].p, c->W.bytes, cudaMemcpyDeviceToDevice, c->stream),
                    "restore W");
                 ck(cudaMemcpyAsync(c->Ht.p, c->snapH[(b - 1) & 1].p, c->Ht.bytes, cudaMemcpyDeviceToDevice,
@@ -1023,7 +1157,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
         }
     }
     if (sync_each && !stopped && nt > 0) decide(nt - 1, prev_done);
-    ck(cudaStreamSynchronize(c->stream), "sync");
+    wait_for(c, c->stream, nullptr, "the solve");
     for (const auto& p : pend) drain(p);
     std::vector<double> errs(nt);
     std::vector<int> flags(nt);
@@ -1180,11 +1314,44 @@ size_t stage_slot_target() {
     return kb > 0 ? size_t(kb) << 10 : kStageSlot;
 }
 
+// Page-locked staging buffers outlive their contexts: pinning 128 MB costs ~0.1-0.3 s, which
+// a one-shot call (context create, upload, solve, download, destroy) would otherwise pay every
+// time. A context takes a buffer of its size from this process-wide free list (or pins a new
+// one) and returns it on destruction; buffers are never unpinned (UVA: usable by any device).
+struct PinnedPool {
+    std::mutex mu;
+    std::vector<std::pair<size_t, void*>> free;
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool;  // intentionally leaked: process lifetime
+    return *p;
+}
+void* pinned_take(size_t bytes) {
+    {
+        std::lock_guard<std::mutex> g(pinned_pool().mu);
+        auto& f = pinned_pool().free;
+        for (size_t i = 0; i < f.size(); ++i)
+            if (f[i].first == bytes) {
+                void* p = f[i].second;
+                f.erase(f.begin() + i);
+                return p;
+            }
+    }
+    void* p = nullptr;
+    ck(cudaMallocHost(&p, bytes), "cudaMallocHost (staging)");
+    return p;
+}
+void pinned_give(void* p, size_t bytes) {
+    if (!p) return;
+    std::lock_guard<std::mutex> g(pinned_pool().mu);
+    pinned_pool().free.emplace_back(bytes, p);
+}
+
 size_t stage_slot_bytes(oocnmf_ctx* c, size_t unit) {
     const size_t want = std::max(stage_slot_target(), unit);
     if (!c->stage_pin || c->stage_dev.bytes != 2 * want) {
-        if (c->stage_pin) cudaFreeHost(c->stage_pin), c->stage_pin = nullptr;
-        ck(cudaMallocHost(&c->stage_pin, 2 * want), "cudaMallocHost (staging)");
+        if (c->stage_pin) pinned_give(c->stage_pin, c->stage_dev.bytes), c->stage_pin = nullptr;
+        c->stage_pin = pinned_take(2 * want);
         c->stage_dev.alloc(2 * want, "staging");
         for (auto& e : c->stage_ev)
             if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -1569,12 +1736,15 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
         c->graphs.clear();
         if (c->comm) ncclCommDestroy(c->comm);
         for (auto e : c->evs) cudaEventDestroy(e);
+        for (auto& m : c->marks) c->ev_pool.push_back(m.beg), c->ev_pool.push_back(m.end);
+        if (c->mark_beg) c->ev_pool.push_back(c->mark_beg);
+        for (auto e : c->ev_pool) cudaEventDestroy(e);
         for (int i = 0; i < 2; ++i) {
             if (c->ev_copied[i]) cudaEventDestroy(c->ev_copied[i]);
             if (c->ev_free[i]) cudaEventDestroy(c->ev_free[i]);
         }
         if (c->hpin) cudaFreeHost(c->hpin);
-        if (c->stage_pin) cudaFreeHost(c->stage_pin);
+        if (c->stage_pin) pinned_give(c->stage_pin, c->stage_dev.bytes);
         for (auto e : c->stage_ev)
             if (e) cudaEventDestroy(e);
         if (c->stream) cudaStreamDestroy(c->stream);
@@ -1874,8 +2044,13 @@ int oocnmf_gather_w_f64(oocnmf_ctx* c, double* w_full) {
         if (size_t(maxr) * kp * 4 > own)
             ck(cudaMemsetAsync(reinterpret_cast<char*>(mine) + own, 0, size_t(maxr) * kp * 4 - own, c->stream),
                "memset W tail");
-        if (N > 1)
+        if (N > 1) {
+            need_comm(c);
+            coll_begin(c, c->stream);
             nck(ncclAllGather(mine, all.p, size_t(maxr) * kp, ncclFloat, c->comm, c->stream), "allgather W");
+            coll_end(c, c->stream, kTagGather, size_t(N) * maxr * kp * 4);  // nmf_distributed.cpp:280
+            wait_for(c, c->stream, nullptr, "W all-gather");
+        }
         for (int p = 0; p < N; ++p)
             export_w(c, all.as<float>() + size_t(p) * maxr * kp, int64_t(beg[p + 1] - beg[p]), w_full + beg[p] * c->k);
     });
@@ -1971,8 +2146,13 @@ int oocnmf_gather_h_f64(oocnmf_ctx* c, double* h_full) {
         ck(launch_strided_cast(CastKind::f32_f64, c->Ht.as<float>(), 1, c->kp, d.as<double>() + c->col0, ng, 1,
                                int64_t(c->k), int64_t(c->n), c->stream),
            "export H");
-        if (c->collective())
+        if (c->collective()) {
+            need_comm(c);
+            coll_begin(c, c->stream);
             nck(ncclAllReduce(d.p, d.p, c->k * c->n_global, ncclDouble, ncclSum, c->comm, c->stream), "allreduce H");
+            coll_end(c, c->stream, kTagGather, c->k * c->n_global * 8);  // nmf_distributed.cpp:272
+            wait_for(c, c->stream, nullptr, "H gather");
+        }
         copy_out(c, {Part{h_full, size_t(ng) * 8, size_t(ng) * 8}}, int64_t(c->k),
                  [&](char* ds, int64_t off, int64_t len) {
                      ck(cudaMemcpyAsync(ds, d.as<double>() + off * ng, size_t(len) * ng * 8,
@@ -2063,15 +2243,104 @@ int oocnmf_set_local(oocnmf_ctx* c, int local) {
 }
 
 int oocnmf_allreduce_sum_f64(oocnmf_ctx* c, double* buf, uint64_t count) {
+    return oocnmf_allreduce_f64(c, buf, count, kTagGeneric);
+}
+
+int oocnmf_allreduce_f64(oocnmf_ctx* c, double* buf, uint64_t count, int tag) {
     return guarded([&] {
         set_dev(c);
-        if (c->nranks <= 1 || count == 0) return;
+        if (tag < 0 || tag > 5) fail(OOCNMF_ERR_SHAPE, "all_reduce_sum: unknown PhaseTag");
+        if (c->nranks <= 1 || count == 0) {
+            c->tag_calls[tag] += 1;  // loopback: counted like the reference's single-rank group
+            c->tag_bytes[tag] += count * 8;
+            return;
+        }
         DevBuf d;
         d.alloc(count * 8, "allreduce scratch");
+        need_comm(c);
         ck(cudaMemcpyAsync(d.p, buf, count * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
+        coll_begin(c, c->stream);
         nck(ncclAllReduce(d.p, d.p, count, ncclDouble, ncclSum, c->comm, c->stream), "allreduce");
+        coll_end(c, c->stream, tag, count * 8);
         ck(cudaMemcpyAsync(buf, d.p, count * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-        ck(cudaStreamSynchronize(c->stream), "sync");
+        wait_for(c, c->stream, nullptr, "all_reduce_sum");
+    });
+}
+
+int oocnmf_barrier(oocnmf_ctx* c) {
+    return guarded([&] {
+        set_dev(c);
+        if (c->nranks <= 1) {
+            c->tag_calls[kTagBarrier] += 1;
+            return;
+        }
+        need_comm(c);
+        DevBuf d;
+        d.alloc(4, "barrier");
+        ck(cudaMemsetAsync(d.p, 0, 4, c->stream), "memset");
+        coll_begin(c, c->stream);
+        nck(ncclAllReduce(d.p, d.p, 1, ncclFloat, ncclSum, c->comm, c->stream), "barrier");
+        coll_end(c, c->stream, kTagBarrier, 0);
+        wait_for(c, c->stream, nullptr, "barrier");
+    });
+}
+
+int oocnmf_comm_stats(oocnmf_ctx* c, uint64_t bytes[6], uint64_t calls[6], double seconds[6]) {
+    return guarded([&] {
+        set_dev(c);
+        reap_marks(c);
+        for (int t = 0; t < 6; ++t) {
+            if (bytes) bytes[t] = c->tag_bytes[t];
+            if (calls) calls[t] = c->tag_calls[t];
+            if (seconds) seconds[t] = c->tag_secs[t];
+        }
+    });
+}
+
+int oocnmf_comm_reset_stats(oocnmf_ctx* c) {
+    return guarded([&] {
+        set_dev(c);
+        reap_marks(c);
+        for (int t = 0; t < 6; ++t) c->tag_bytes[t] = c->tag_calls[t] = 0, c->tag_secs[t] = 0.0;
+    });
+}
+
+int oocnmf_set_comm_timeout(oocnmf_ctx* c, double seconds) {
+    return guarded([&] {
+        if (!(seconds > 0)) fail(OOCNMF_ERR_SHAPE, "comm timeout must be > 0");
+        c->comm_timeout = seconds;
+    });
+}
+
+int oocnmf_ctx_create_group(int n, const int* devices, oocnmf_ctx** out) {
+    return guarded([&] {
+        if (n < 1) fail(OOCNMF_ERR_SHAPE, "spawn_group: need at least one rank");
+        for (int r = 0; r < n; ++r) out[r] = nullptr;
+        std::vector<int> devs(devices, devices + n);
+        for (int r = 0; r < n; ++r)
+            for (int q = 0; q < r; ++q)
+                if (devs[q] == devs[r])
+                    fail(OOCNMF_ERR_SHAPE, "spawn_group: one GPU per rank (device " + std::to_string(devs[r]) +
+                                               " repeats; NCCL runs one rank per device)");
+        std::vector<oocnmf_ctx*> cs(n, nullptr);
+        try {
+            for (int r = 0; r < n; ++r) {
+                cs[r] = new oocnmf_ctx();
+                ctx_init_common(cs[r], devs[r]);
+                cs[r]->rank = r;
+                cs[r]->nranks = n;
+            }
+            if (n > 1) {
+                std::vector<ncclComm_t> comms(n);
+                nck(ncclCommInitAll(comms.data(), n, devs.data()), "ncclCommInitAll");
+                for (int r = 0; r < n; ++r) cs[r]->comm = comms[r];
+            }
+        } catch (...) {
+            for (auto* c : cs)
+                if (c) oocnmf_ctx_destroy(c);
+            throw;
+        }
+        for (int r = 0; r < n; ++r) out[r] = cs[r];
     });
 }
 

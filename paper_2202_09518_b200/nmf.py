@@ -16,8 +16,9 @@ from __future__ import annotations
 import ctypes as C
 import enum
 import os
+import dataclasses
 from dataclasses import dataclass, field
-from typing import List, Optional, Tuple
+from typing import Dict, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -509,18 +510,133 @@ def exchange_unique_id(rank: int, make_id, device: Optional[int] = None, group=N
     return bytes(t.cpu().numpy().tobytes())
 
 
-class DistComm:
-    """One rank of an NCCL group over NVLink (the B200 CommHandle). The NCCL unique id is
-    exchanged with torch.distributed; all traffic of the solve goes through NCCL inside the
-    C-ABI library."""
+class PhaseTag(enum.IntEnum):
+    """Collective tags (include/oocnmf/comm.hpp:13-20)."""
+    generic = 0
+    w_update = 1
+    h_update = 2
+    error_check = 3
+    gather = 4
+    barrier = 5
 
-    def __init__(self, rank: int, size: int, device: int, group=None):
+
+@dataclass
+class CollectiveStats:
+    """Per-tag collective statistics (include/oocnmf/comm.hpp:28-43): bytes, calls, seconds
+    (device time of the collectives, the solve's own included)."""
+    bytes: Dict[PhaseTag, int] = field(default_factory=dict)
+    calls: Dict[PhaseTag, int] = field(default_factory=dict)
+    seconds: Dict[PhaseTag, float] = field(default_factory=dict)
+
+    def total_bytes(self) -> int:
+        return sum(self.bytes.values())
+
+    def total_calls(self) -> int:
+        return sum(self.calls.values())
+
+    def total_seconds(self) -> float:
+        return sum(self.seconds.values())
+
+
+class DistComm:
+    """One rank of an NCCL group over NVLink (the B200 CommHandle, include/oocnmf/comm.hpp:48-67).
+    Built per process from a torch.distributed unique-id exchange, or per thread by
+    :func:`spawn_group`; all traffic of the solve goes through NCCL inside the C-ABI library.
+    Collectives time out (default 60 s, src/comm.cpp:89-111): a rank whose peer stops
+    responding gets :class:`CommError` and the group is poisoned."""
+
+    def __init__(self, rank: int, size: int, device: int, group=None, timeout_s: float = 60.0):
         uid = exchange_unique_id(rank, Context.unique_id, device, group) if size > 1 else b"\0" * 128
         self.rank, self.size, self.device = rank, size, device
         self.ctx = Context(device, rank, size, uid)
+        self.set_timeout(timeout_s)
+
+    @classmethod
+    def _wrap(cls, ctx: "Context", rank: int, size: int, device: int) -> "DistComm":
+        self = cls.__new__(cls)
+        self.rank, self.size, self.device, self.ctx = rank, size, device, ctx
+        return self
+
+    def all_reduce_sum(self, buf: np.ndarray, tag: PhaseTag = PhaseTag.generic) -> None:
+        """In-place elementwise sum of a float64 array across the group (collective)."""
+        if buf.dtype != np.float64 or not buf.flags.c_contiguous:
+            raise ShapeError("all_reduce_sum: expected a C-contiguous float64 array")
+        check(_capi.lib().oocnmf_allreduce_f64(self.ctx._h, _p(buf, C.c_double), buf.size, int(tag)))
+
+    def barrier(self) -> None:
+        check(_capi.lib().oocnmf_barrier(self.ctx._h))
+
+    def stats(self) -> CollectiveStats:
+        b, c, s = np.zeros(6, np.uint64), np.zeros(6, np.uint64), np.zeros(6)
+        check(_capi.lib().oocnmf_comm_stats(self.ctx._h, _p(b, C.c_uint64), _p(c, C.c_uint64), _p(s, C.c_double)))
+        return CollectiveStats({t: int(b[t]) for t in PhaseTag}, {t: int(c[t]) for t in PhaseTag},
+                               {t: float(s[t]) for t in PhaseTag})
+
+    def reset_stats(self) -> None:
+        check(_capi.lib().oocnmf_comm_reset_stats(self.ctx._h))
+
+    def set_timeout(self, seconds: float) -> None:
+        check(_capi.lib().oocnmf_set_comm_timeout(self.ctx._h, float(seconds)))
 
     def close(self):
         self.ctx.close()
+
+
+def spawn_group(n: int, devices: Optional[Sequence[int]] = None, timeout_s: float = 60.0) -> List[DistComm]:
+    """``spawn_group(n, Backend::threads)`` (include/oocnmf/comm.hpp:80-82): n ranks of this
+    process, one GPU each (devices, default 0..n-1), sharing one NCCL clique; hand one handle
+    to each worker thread."""
+    devs = list(range(n)) if devices is None else list(devices)
+    if len(devs) != n:
+        raise ShapeError("spawn_group: need one device per rank")
+    if n > device_count():
+        raise ShapeError(f"spawn_group: {n} ranks need {n} GPUs, {device_count()} visible")
+    ctxs = (C.c_void_p * n)()
+    check(_capi.lib().oocnmf_ctx_create_group(n, (C.c_int * n)(*devs), ctxs))
+    out = []
+    for r in range(n):
+        ctx = Context.__new__(Context)
+        ctx._h = C.c_void_p(ctxs[r])
+        ctx.device, ctx.rank, ctx.nranks = devs[r], r, n
+        ctx.m = ctx.n = ctx.k = ctx.row0 = ctx.rows = 0
+        ctx._keep = None
+        comm = DistComm._wrap(ctx, r, n, devs[r])
+        comm.set_timeout(timeout_s)
+        out.append(comm)
+    return out
+
+
+def run_distributed_threads(a, cfg: "NmfConfig", plan: "PartitionPlan", stats_out: Optional[list] = None,
+                            devices: Optional[Sequence[int]] = None) -> List["NmfResult"]:
+    """All ranks of a one-process group on worker threads, one GPU each
+    (src/nmf_distributed.cpp:291-319); returns the per-rank results (index = rank) and, in
+    ``stats_out``, each rank's CollectiveStats. The first rank exception is re-raised."""
+    import threading
+
+    group = spawn_group(plan.n_workers, devices)
+    results: List[Optional[NmfResult]] = [None] * plan.n_workers
+    errors: List[Optional[BaseException]] = [None] * plan.n_workers
+
+    def work(r):
+        try:
+            results[r] = nmf_distributed(a, dataclasses.replace(cfg, device=group[r].device), plan, group[r])
+        except BaseException as e:  # noqa: BLE001 - re-raised below, like std::exception_ptr
+            errors[r] = e
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(plan.n_workers)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if stats_out is not None:
+        stats_out.clear()
+        stats_out.extend(g.stats() for g in group)
+    for g in group:
+        g.close()
+    for e in errors:
+        if e is not None:
+            raise e
+    return results  # type: ignore[return-value]
 
 
 class _Window:

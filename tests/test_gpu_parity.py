@@ -246,7 +246,9 @@ def test_direct_error_mode_matches_trace_form(gpu):
     r3 = solve_from(a, 16, 30, 10)  # auto: error ~0.5 -> trace form
     e1 = np.array([e for _, e in r1.error_trace])
     e2 = np.array([e for _, e in r2.error_trace])
-    np.testing.assert_allclose(e1, e2, rtol=2e-6)
+    # the trace form subtracts O(||A||^2) terms: f32-level rounding (~1e-7) of <W^T A, H> grows
+    # by ~2/err^2 ~ 8 at err ~ 0.49
+    np.testing.assert_allclose(e1, e2, rtol=5e-6)
     assert np.array_equal(r1.w, r2.w)
     assert [e for _, e in r3.error_trace] == e1.tolist()
 
@@ -537,7 +539,9 @@ def test_column_partition_on_one_gpu_equals_serial(gpu, csr):
         res = nmf.nmf_distributed(a, cfg, nmf.make_plan(m, n, k, 1, 1, nmf.Strategy.cnmf), comm)
     finally:
         comm.close()
-    np.testing.assert_allclose([e for _, e in res.error_trace], [e for _, e in ser.error_trace], rtol=1e-6)
+    # (dense nmf_serial runs the one-pass kernel, CNMF the two passes: same arithmetic, different
+    # f32 summation order)
+    np.testing.assert_allclose([e for _, e in res.error_trace], [e for _, e in ser.error_trace], rtol=5e-6)
     assert rel_fro(res.w, ser.w) < 1e-5 and rel_fro(res.h, ser.h) < 1e-5
     assert res.h.shape == (k, n)
 

@@ -158,10 +158,10 @@ def test_fused_pass_matches_two_pass_kernels(gpu, monkeypatch, m, n, k, lookahea
                         init_w=f32(w0), init_h=f32(h0))
     monkeypatch.setenv("OOCNMF_FUSED_D", lookahead)
     fused = nmf.nmf_serial(a, cfg)
-    assert fused.info["fused_launches"] == 30
+    assert fused.info["fused_pass_launches"] == 30
     monkeypatch.setenv("OOCNMF_FUSED", "0")
     split = nmf.nmf_serial(a, cfg)
-    assert split.info["fused_launches"] == 0
+    assert split.info["fused_pass_launches"] == 0
     ref = port.nmf_serial(f32(a), k, f32(w0), f32(h0), max_iters=30, interval=10)
     ef = np.array([e for _, e in fused.error_trace])
     es = np.array([e for _, e in split.error_trace])

@@ -51,7 +51,8 @@ def test_select_k_matches_reference(gpu, k_true, kmax, expect):
     assert rep.rationale.split(" and ")[0] == why.split(" and ")[0]
     for got, want, med in zip(rep.records, recs, meds):
         assert (got.k, got.valid, got.runs_used) == (want["k"], want["valid"], want["runs_used"])
-        assert got.mean_relative_error == pytest.approx(want["mean_relative_error"], rel=2e-5)
+        # the north-star trajectory bar (1e-4), here on the mean over the P perturbed runs
+        assert got.mean_relative_error == pytest.approx(want["mean_relative_error"], rel=1e-4)
         # silhouettes are cosine statistics of factors that agree to ~1e-5 (measured ~1e-6)
         assert got.min_silhouette == pytest.approx(want["min_silhouette"], abs=1e-4)
         assert got.mean_silhouette == pytest.approx(want["mean_silhouette"], abs=1e-4)

@@ -1,0 +1,113 @@
+// Developer probe (not part of the product): the one-pass kernel (kernels_fused.cu) alone at a
+// config-2 shape on hash-filled data, timed with CUDA events, with per-role wait cycles when
+// built with -DOOC_FZ_PROFILE. build:
+//   nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DOOC_FZ_PROFILE -I include \
+//     -I paper_2202_09518_b200/csrc tools/fz_stall.cu paper_2202_09518_b200/csrc/kernels_fused.cu \
+//     paper_2202_09518_b200/csrc/kernels_tc.cu paper_2202_09518_b200/csrc/kernels_factor.cu -lcuda -o tools/fz_stall
+// argv: kp mp np lookahead reps pol
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "kernels.h"
+
+#ifdef OOC_FZ_PROFILE
+namespace ooc {
+void fz_profile_read(unsigned long long* out16, bool reset);
+}
+#else
+static void fz_profile_read(unsigned long long* out16, bool) {
+    for (int i = 0; i < 16; ++i) out16[i] = 0;
+}
+#endif
+using namespace ooc;
+
+#define CK(x)                                                                                     \
+    do {                                                                                          \
+        cudaError_t e_ = (x);                                                                     \
+        if (e_ != cudaSuccess) {                                                                  \
+            printf("CUDA %s at %s:%d\n", cudaGetErrorString(e_), __FILE__, __LINE__);            \
+            exit(1);                                                                              \
+        }                                                                                         \
+    } while (0)
+
+__global__ void k_fill(float* a, int64_t n, uint32_t salt, float scale) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        uint32_t x = uint32_t(i) * 2654435761u ^ uint32_t(i >> 32) * 40503u ^ salt;
+        x ^= x >> 15, x *= 2246822519u, x ^= x >> 13;
+        a[i] = float(x >> 8) * (scale / 16777216.f) + 1e-3f;
+    }
+}
+
+int main(int argc, char** argv) {
+    const int kp = argc > 1 ? atoi(argv[1]) : 32;
+    const int64_t mp = argc > 2 ? atoll(argv[2]) : 65536, np = argc > 3 ? atoll(argv[3]) : 65536;
+    const int D = argc > 4 ? atoi(argv[4]) : 2;
+    const int reps = argc > 5 ? atoi(argv[5]) : 10;
+    const int pol = argc > 6 ? atoi(argv[6]) : 0;
+    int sms = 0;
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+    float *A, *W, *Wc, *Hc, *HHt, *wta, *slots;
+    unsigned* cnt;
+    int *flag, *idx;
+    CK(cudaMalloc(&A, size_t(mp) * np * 4));
+    CK(cudaMalloc(&W, size_t(mp) * kp * 4));
+    CK(cudaMalloc(&Wc, size_t(mp) * 2 * kp * 4));
+    CK(cudaMalloc(&Hc, size_t(np) * 2 * kp * 4));
+    CK(cudaMalloc(&HHt, size_t(kp) * kp * 4));
+    CK(cudaMalloc(&wta, size_t(np) * kp * 4));
+    CK(cudaMalloc(&flag, 4));
+    k_fill<<<sms * 8, 256>>>(A, mp * np, 1u, 1.f);
+    k_fill<<<sms * 8, 256>>>(W, mp * kp, 2u, 0.5f);
+    k_fill<<<sms * 8, 256>>>(Hc, np * 2 * kp, 3u, 0.01f);
+    k_fill<<<sms * 8, 256>>>(HHt, kp * kp, 4u, 100.f);
+    FusedPlan fp;
+    plan_fused(fp, mp, np, sms, D);
+    std::vector<int> h;
+    h.insert(h.end(), fp.q0.begin(), fp.q0.end());
+    h.insert(h.end(), fp.t0.begin(), fp.t0.end());
+    h.insert(h.end(), fp.act.begin(), fp.act.end());
+    CK(cudaMalloc(&idx, h.size() * 4));
+    CK(cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
+    CK(cudaMalloc(&slots, size_t(fp.NS) * fp.G * 128 * kp * 4));
+    CK(cudaMalloc(&cnt, size_t(2) * fp.NB * 4));
+    FusedArgs a{};
+    a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = 2;
+    a.q0 = idx, a.t0 = idx + fp.G + 1, a.act = idx + 2 * (fp.G + 1);
+    a.p1slots = slots, a.count = cnt, a.wdone = cnt + fp.NB;
+    a.W = W, a.Wcat = Wc, a.HHt = HHt, a.eps = 1e-12f, a.flag = flag, a.wta = wta;
+    a.pol_p1 = pol == 1 ? 0x14F0000000000000ull : 0x1000000000000000ull;
+    a.pol_p2 = pol == 2 ? 0x1000000000000000ull : 0x12F0000000000000ull;
+    printf("plan: G %d NB %d NT %d NQ %d D %d NS %d G1 %d; CTA 0: q [%d,%d) t [%d,%d)\n", fp.G, fp.NB, fp.NT, fp.NQ,
+           fp.D, fp.NS, fp.G1, fp.q0[0], fp.q0[1], fp.t0[0], fp.t0[1]);
+    auto run = [&] {
+        CK(cudaMemsetAsync(cnt, 0, size_t(2) * fp.NB * 4, 0));
+        CK(launch_mu_fused(kp, fp, A, mp, np, Hc, a, 0));
+    };
+    run();
+    CK(cudaDeviceSynchronize());
+    unsigned long long p[16];
+    fz_profile_read(p, true);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0), cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) run();
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    fz_profile_read(p, true);
+    const double units = double(fp.NB) * (fp.NQ + 2.0 * fp.NT) / fp.G * reps;  // per CTA
+    const double ctas = fp.G;
+    printf("kp %d %ldx%ld D %d pol %d: %.3f ms per launch (%.2f TB/s of A once)\n", kp, long(mp), long(np), D, pol,
+           ms / reps, double(mp) * np * 4 / (ms / reps) / 1e9);
+    const char* role[5] = {"producer", "mma", "updater", "split", "drain"};
+    printf("  total cycles per unit:");
+    for (int r = 0; r < 5; ++r) printf(" %s %.0f", role[r], p[10 + r] / ctas / units);
+    printf("\n");
+    const char* name[10] = {"producer wait emptyA", "producer wait emptyB", "producer wait wdone", "split wait fullA",
+                            "split wait afree",     "mma wait accempty",    "mma wait fullB",      "mma wait split",
+                            "drain wait accfull",   "updater wait count"};
+    for (int j = 0; j < 10; ++j) printf("  %-22s %8.0f cycles/unit\n", name[j], p[j] / ctas / units);
+    return 0;
+}
