@@ -43,7 +43,7 @@ struct FzCfg {
     static constexpr uint32_t ATOM_STRIDE = BK * 128;  // MN-major atoms: BK rows x 128 B
     static constexpr int A_BYTES = 128 * BK * 4;       // 32 KB (P1: 128 rows x 64 cols, P2: 64 x 128)
     static constexpr int B_BYTES = BK * 2 * KP * 4;    // [F | F_lo] rows
-    static constexpr int A_STAGES = KP == 32 ? 5 : 6;
+    static constexpr int A_STAGES = KP == 32 ? 4 : 5;
     static constexpr int B_STAGES = 4;
     static constexpr int ACC_COLS = 2 * KP;            // D' = [H | L]
     static constexpr int NBUF = 2;
@@ -57,7 +57,9 @@ struct FzCfg {
     static constexpr int MAX_G = 192;                  // CTAs (smem list of P1 publishers)
     static constexpr size_t RING_BYTES = size_t(A_STAGES) * A_BYTES + size_t(B_STAGES) * B_BYTES;
     static constexpr size_t BAR_BYTES = 512;
-    static constexpr size_t SMEM = RING_BYTES + 1024 + BAR_BYTES + MAX_G * 4 + 64 * 4;
+    // updater gather buffer: one row of every CTA's published P1 partial (TMA, G x kp floats)
+    static constexpr size_t GATHER_OFF = RING_BYTES + BAR_BYTES + MAX_G * 4 + 64 * 4;  // 128-aligned
+    static constexpr size_t SMEM = GATHER_OFF + size_t(MAX_G) * KP * 4 + 1024;
     static_assert(SMEM <= 232448, "shared memory budget");
     static constexpr uint32_t IDESC_HI = idesc_tf32(2 * KP, 0, 1);
     static constexpr uint32_t IDESC_KP = idesc_tf32(KP, 0, 1);
@@ -102,7 +104,7 @@ template <int KP>
 __global__ void __launch_bounds__(512, 1)
     k_mu_fused(const __grid_constant__ CUtensorMap tmA1, const __grid_constant__ CUtensorMap tmA2,
                const __grid_constant__ CUtensorMap tmB1, const __grid_constant__ CUtensorMap tmB2,
-               const __grid_constant__ FusedArgs p) {
+               const __grid_constant__ CUtensorMap tmS, const __grid_constant__ FusedArgs p) {
     using C = FzCfg<KP>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -115,9 +117,11 @@ __global__ void __launch_bounds__(512, 1)
     uint64_t* afree = split + C::ASLOTS;      // [ASLOTS]
     uint64_t* accfull = afree + C::ASLOTS;    // [NBUF]
     uint64_t* accempty = accfull + C::NBUF;   // [NBUF]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accempty + C::NBUF);
+    uint64_t* gbar = accempty + C::NBUF;       // updater gather (TMA -> updaters)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbar + 1);
     int* act = reinterpret_cast<int*>(smem + C::RING_BYTES + C::BAR_BYTES);  // [G1] P1 publishers
     float* red = reinterpret_cast<float*>(act + C::MAX_G);                   // [64] updater scratch
+    float* gbuf = reinterpret_cast<float*>(smem + C::GATHER_OFF);            // [G][kp] gathered partials
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
@@ -129,6 +133,7 @@ __global__ void __launch_bounds__(512, 1)
         for (int s = 0; s < C::B_STAGES; ++s) mbar_init(fullB + s, 1), mbar_init(emptyB + s, 1);
         for (int r = 0; r < C::ASLOTS; ++r) mbar_init(split + r, 8), mbar_init(afree + r, 1);
         for (int b = 0; b < C::NBUF; ++b) mbar_init(accfull + b, 1), mbar_init(accempty + b, 4);
+        mbar_init(gbar, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int i = tid; i < p.G1; i += blockDim.x) act[i] = p.act[i];
@@ -243,26 +248,28 @@ __global__ void __launch_bounds__(512, 1)
         const int u = tid - 64;
         constexpr int P = 64 / KP;  // parts of the CTA range, summed in ascending order
         const int j = u % KP, part = u / KP;
-        const int c_lo = part * p.G1 / P, c_hi = (part + 1) * p.G1 / P;
+        const int c_lo = part * G / P, c_hi = (part + 1) * G / P;
         float hcol[KP];  // column u of HH^T (warp 2, lanes < KP)
 #pragma unroll
         for (int q = 0; q < KP; ++q) hcol[q] = warp == 2 && lane < KP ? p.HHt[q * KP + lane] : 0.f;
         const unsigned target = 4u * unsigned(p.G1);
         bool bad = false;
+        uint32_t gph = 0;
         for (int64_t g = cta; g < int64_t(NB) * 128; g += G) {
             const int b = int(g >> 7), row = int(g & 127);
             FZ_WAIT(9, wait_count(p.count + b, target));
-            const float* base = p.p1slots + (int64_t(b % p.NS) * G) * (128 * KP) + row * KP + j;
-            float acc = 0.f;
-            int c = c_lo;
-            for (; c + 4 <= c_hi; c += 4) {
-                const float v0 = __ldcg(base + int64_t(act[c]) * (128 * KP));
-                const float v1 = __ldcg(base + int64_t(act[c + 1]) * (128 * KP));
-                const float v2 = __ldcg(base + int64_t(act[c + 2]) * (128 * KP));
-                const float v3 = __ldcg(base + int64_t(act[c + 3]) * (128 * KP));
-                acc += v0, acc += v1, acc += v2, acc += v3;
+            // one TMA operation gathers row `row` of every CTA's partial (G x kp floats, CTAs
+            // without P1 work hold zeros); then each part sums its CTA range in ascending order
+            if (u == 0) {
+                fence_proxy_async_global();  // the partials were written by generic stores
+                mbar_expect_tx(gbar, uint32_t(G * KP * 4));
+                tma_load_3d(gbuf, &tmS, gbar, 0, row, (b % p.NS) * G, kEvictFirst);
             }
-            for (; c < c_hi; ++c) acc += __ldcg(base + int64_t(act[c]) * (128 * KP));
+            FZ_WAIT(10, mbar_wait(gbar, gph));
+            gph ^= 1u;
+            float acc = 0.f;
+#pragma unroll 8
+            for (int c = c_lo; c < c_hi; ++c) acc += gbuf[c * KP + j];
             red[u] = acc;
             asm volatile("bar.sync 1, 64;" ::: "memory");
             if (warp == 2) {
@@ -397,6 +404,7 @@ __global__ void __launch_bounds__(512, 1)
                 }
                 __syncwarp();
                 if (lane == 0) {
+                    fence_proxy_async_global();  // read back by the updaters' TMA (async proxy)
                     __threadfence();
                     atomicAdd(p.count + s, 1u);
                 }
@@ -448,9 +456,9 @@ __global__ void __launch_bounds__(512, 1)
 #ifdef OOC_FZ_PROFILE
     // per role: lane 0 of warp 0 (producer), 1 (MMA), 2 (updater), 4 (split), 12 (drain)
     if (lane == 0 && (warp == 0 || warp == 1 || warp == 2 || warp == 4 || warp == 12)) {
-        for (int j = 0; j < 10; ++j)
+        for (int j = 0; j < 11; ++j)
             if (prof[j]) atomicAdd(&g_fz_prof[j], (unsigned long long)prof[j]);
-        atomicAdd(&g_fz_prof[10 + (warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == 4 ? 3 : 4)],
+        atomicAdd(&g_fz_prof[11 + (warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == 4 ? 3 : 4)],
                   (unsigned long long)(clock64() - t_start));
     }
 #endif
@@ -471,6 +479,19 @@ cudaError_t launch_fused_t(const FusedPlan& fp, const float* A, int64_t mp, int6
     if ((e = make_map(&a2, A, mp, np, np, kTcStep, 4, true)) != cudaSuccess) return e;
     if ((e = make_map(&b1, Ht_cat, np, 2 * KP, 2 * KP, kTcStep, 2 * KP / 32, true)) != cudaSuccess) return e;
     if ((e = make_map(&b2, args.Wcat, mp, 2 * KP, 2 * KP, kTcStep, 2 * KP / 32, true)) != cudaSuccess) return e;
+    CUtensorMap sm;  // P1 slots [NS * G][128][kp]: box (kp, 1 row, G slots) = one row of every CTA
+    {
+        auto fn = encode_fn();
+        if (!fn) return cudaErrorNotSupported;
+        const cuuint64_t dims[3] = {cuuint64_t(KP), 128u, cuuint64_t(fp.NS) * fp.G};
+        const cuuint64_t strides[2] = {cuuint64_t(KP) * 4, cuuint64_t(128) * KP * 4};
+        const cuuint32_t box[3] = {cuuint32_t(KP), 1u, cuuint32_t(fp.G)};
+        const cuuint32_t estr[3] = {1u, 1u, 1u};
+        if (fn(&sm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, args.p1slots, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return cudaErrorInvalidValue;
+    }
     auto kern = k_mu_fused<KP>;
     if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(C::SMEM))) != cudaSuccess)
         return e;
@@ -484,7 +505,7 @@ cudaError_t launch_fused_t(const FusedPlan& fp, const float* A, int64_t mp, int6
     at[0].val.cooperative = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
-    return cudaLaunchKernelEx(&lc, kern, a1, a2, b1, b2, args);
+    return cudaLaunchKernelEx(&lc, kern, a1, a2, b1, b2, sm, args);
 }
 
 }  // namespace

@@ -1,0 +1,109 @@
+"""The distributed drop-in boundary on the GPU: a reference-style C++ caller of
+run_distributed_threads / spawn_group / CommHandle (tests/cpp/dist_demo.cpp, compiled unchanged
+against the reference header names) and the Python mirror, against the CPU oracle's
+row-partitioned run (oracle/mu_oracle.c, pinned to src/nmf_distributed.cpp:151-289).
+
+One rank per visible GPU (up to 4); on a one-GPU box the group is the loopback backend.
+"""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_2202_09518_b200 as nmf
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+port = oracle.port
+
+
+def f32(x):
+    return np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+
+
+def _workers():
+    return max(1, min(nmf.device_count(), 4))
+
+
+def test_cpp_run_distributed_threads_is_a_drop_in(gpu):
+    workers = _workers()
+    m, n, k = 700, 500, 8
+    exe = os.path.join(ROOT, "paper_2202_09518_b200", "lib", "dist_demo")
+    out = subprocess.run([exe, str(workers), str(m), str(n), str(k)], capture_output=True, text=True, check=True,
+                         timeout=300).stdout
+    lines = [json.loads(x) for x in out.strip().splitlines()]
+    trace = [d["err"] for d in lines if "err" in d]
+    a = f32(port.uniform_dense(m, n, 42, 99))
+    w0, h0 = port.init_factors(m, n, k, 0)
+    ref = port.nmf_rnmf(a, k, f32(w0), f32(h0), n_workers=workers, max_iters=30, interval=10)
+    np.testing.assert_allclose(trace, ref.trace_err, rtol=1e-4)
+    norms = [d for d in lines if "w_fro" in d][0]
+    assert norms["ranks"] == workers and norms["identical"]
+    assert norms["w_fro"] == pytest.approx(np.linalg.norm(ref.w), rel=1e-3)
+    assert norms["h_fro"] == pytest.approx(np.linalg.norm(ref.h), rel=1e-3)
+    st = [d for d in lines if "h_update_calls" in d][0]
+    if workers > 1:
+        # one grouped all-reduce of [W^T A | W^T W] per iteration, one W gather, ||A||^2 + one
+        # residual all-reduce per check (CollectiveStats per PhaseTag, comm.hpp:28-43)
+        assert st["h_update_calls"] == 30 and st["gather_calls"] == 1 and st["error_check_calls"] == 4
+        assert st["h_update_bytes"] > 30 * (512 * 8 * 4)
+    grp = [d for d in lines if "allreduce_last" in d][0]
+    assert grp["allreduce_last"] == 6.0 * workers * (workers + 1) / 2
+    assert grp["generic_calls"] == 1 and grp["barrier_calls"] == 1
+    assert any(d.get("shape_error") for d in lines)
+
+
+def test_python_run_distributed_threads_matches_oracle(gpu):
+    workers = _workers()
+    m, n, k = 640, 480, 16
+    a = port.uniform_dense(m, n, 3, 99).astype(np.float32)
+    w0, h0 = port.init_factors(m, n, k, 0)
+    cfg = nmf.NmfConfig(k=k, max_iters=20, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    plan = nmf.make_plan(m, n, k, workers, 1, nmf.Strategy.rnmf)
+    stats = []
+    res = nmf.run_distributed_threads(a, cfg, plan, stats_out=stats)
+    ref = port.nmf_rnmf(f32(a), k, f32(w0), f32(h0), n_workers=workers, max_iters=20, interval=10)
+    assert len(res) == workers and len(stats) == workers
+    for r in res:
+        np.testing.assert_allclose([e for _, e in r.error_trace], ref.trace_err, rtol=1e-4)
+        assert np.linalg.norm(r.w - ref.w) <= 1e-3 * np.linalg.norm(ref.w)
+        assert np.array_equal(r.w, res[0].w) and np.array_equal(r.h, res[0].h)
+    if workers > 1:
+        assert stats[0].calls[nmf.PhaseTag.h_update] == 20
+        assert stats[0].seconds[nmf.PhaseTag.h_update] > 0
+
+
+def test_group_collectives_and_stats(gpu):
+    import threading
+
+    workers = _workers()
+    group = nmf.spawn_group(workers)
+    out = [None] * workers
+
+    def work(r):
+        buf = np.arange(6, dtype=np.float64) * (r + 1)
+        group[r].all_reduce_sum(buf, nmf.PhaseTag.gather)
+        group[r].barrier()
+        out[r] = buf
+
+    ts = [threading.Thread(target=work, args=(r,)) for r in range(workers)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    want = np.arange(6, dtype=np.float64) * workers * (workers + 1) / 2
+    for r in range(workers):
+        assert np.array_equal(out[r], want)
+        s = group[r].stats()
+        assert s.calls[nmf.PhaseTag.gather] == 1 and s.bytes[nmf.PhaseTag.gather] == 48
+        assert s.calls[nmf.PhaseTag.barrier] == 1
+        group[r].reset_stats()
+        assert group[r].stats().total_calls() == 0
+    for g in group:
+        g.close()
+    with pytest.raises(nmf.ShapeError):
+        nmf.spawn_group(nmf.device_count() + 1)

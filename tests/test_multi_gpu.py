@@ -129,3 +129,20 @@ def test_csr_sharded_h_update_matches_oracle(dist_results):
     w0, h0 = oracle.port.init_factors(1100, 2048, 16, 0)
     ref = oracle.port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
     _check(res["csr_shard_k16"], ref)
+
+
+def test_dead_rank_raises_comm_error(tmp_path):
+    """A rank that dies after joining the group: the survivor's collective times out (5 s here,
+    60 s default as src/comm.cpp:89-111), raises CommError instead of hanging, and the group is
+    poisoned (later collectives fail too)."""
+    if nmf.device_count() < 2:
+        pytest.skip("needs >= 2 GPUs")
+    out = tmp_path / "fail.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "dist_fail_worker.py"),
+           str(out)]
+    subprocess.run(cmd, timeout=180, cwd=ROOT)
+    v = json.load(open(out))
+    assert v["first"] == "CommError", v
+    assert "communicator aborted" in v["message"] and v["seconds"] < 60
+    assert v["second"] == "CommError" and "aborted" in v["second_message"]

@@ -70,6 +70,7 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&idx, h.size() * 4));
     CK(cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMalloc(&slots, size_t(fp.NS) * fp.G * 128 * kp * 4));
+    CK(cudaMemset(slots, 0, size_t(fp.NS) * fp.G * 128 * kp * 4));
     CK(cudaMalloc(&cnt, size_t(2) * fp.NB * 4));
     FusedArgs a{};
     a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = 2;
@@ -103,11 +104,11 @@ int main(int argc, char** argv) {
            ms / reps, double(mp) * np * 4 / (ms / reps) / 1e9);
     const char* role[5] = {"producer", "mma", "updater", "split", "drain"};
     printf("  total cycles per unit:");
-    for (int r = 0; r < 5; ++r) printf(" %s %.0f", role[r], p[10 + r] / ctas / units);
+    for (int r = 0; r < 5; ++r) printf(" %s %.0f", role[r], p[11 + r] / ctas / units);
     printf("\n");
-    const char* name[10] = {"producer wait emptyA", "producer wait emptyB", "producer wait wdone", "split wait fullA",
+    const char* name[11] = {"producer wait emptyA", "producer wait emptyB", "producer wait wdone", "split wait fullA",
                             "split wait afree",     "mma wait accempty",    "mma wait fullB",      "mma wait split",
-                            "drain wait accfull",   "updater wait count"};
-    for (int j = 0; j < 10; ++j) printf("  %-22s %8.0f cycles/unit\n", name[j], p[j] / ctas / units);
+                            "drain wait accfull",   "updater wait count",   "updater wait gather"};
+    for (int j = 0; j < 11; ++j) printf("  %-22s %8.0f cycles/unit\n", name[j], p[j] / ctas / units);
     return 0;
 }
