@@ -49,7 +49,7 @@ struct FusedArgs {
     const int* act;        // [G1] CTAs with P1 work, ascending
     float* p1slots;        // [NS][G][128][kp] published P1 partials
     unsigned* count;       // [NB] P1 partials published per block (zero before the launch)
-    unsigned* wdone;       // [NB] rows of the block updated (zero before the launch)
+    unsigned* wdone;       // [2 NB] rows of each 64-row half block updated (zero before the launch)
     float* W;              // mp x kp, updated in place
     float* Wcat;           // mp x 2kp [W | W_lo] of the new W
     const float* HHt;      // kp x kp

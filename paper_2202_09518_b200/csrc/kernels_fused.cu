@@ -156,16 +156,30 @@ __global__ void __launch_bounds__(512, 1)
     const int du = p.drain_units;
 
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- A producer (never waits on other CTAs: P2's A tiles load ahead)
         if (lane == 0) {
-            int sa = 0, sb = 0;
-            uint32_t pha = 0, phb = 0;
+            int sa = 0;
+            uint32_t pha = 0;
             auto load_a = [&](const CUtensorMap* m, int y, int z, uint64_t pol) {
                 FZ_WAIT(0, mbar_wait(emptyA + sa, pha ^ 1u));
                 mbar_expect_tx(fullA + sa, C::A_BYTES);
                 tma_load_3d(a_stage(sa), m, fullA + sa, 0, y, z, pol);
                 if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
             };
+            for (int s = 0; s < NB + D; ++s) {
+                if (s < NB)
+                    for (int q = q0; q < q1; ++q) load_a(&tmA1, s * 128, 2 * q, p.pol_p1);  // block s, K-atoms 2q..
+                if (s >= D)
+                    for (int j = t0; j < t1; ++j)
+                        for (int h = 0; h < 2; ++h) load_a(&tmA2, (s - D) * 128 + 64 * h, 4 * j, p.pol_p2);
+            }
+        }
+    } else if (warp == 3) {
+        // ---------------- B producer: [Ht | Ht_lo] chunk rows for P1; for P2 the block's new
+        // [W | W_lo] rows, each 64-row half once its updaters are done (wdone[2 b + h] = 64)
+        if (lane == 0) {
+            int sb = 0;
+            uint32_t phb = 0;
             auto load_b = [&](const CUtensorMap* m, int y, uint64_t pol) {
                 FZ_WAIT(1, mbar_wait(emptyB + sb, phb ^ 1u));
                 mbar_expect_tx(fullB + sb, C::B_BYTES);
@@ -174,27 +188,22 @@ __global__ void __launch_bounds__(512, 1)
             };
             for (int s = 0; s < NB + D; ++s) {
                 if (s < NB)
-                    for (int q = q0; q < q1; ++q) {
-                        load_a(&tmA1, s * 128, 2 * q, p.pol_p1);     // rows of block s, K-atoms 2q, 2q+1
-                        load_b(&tmB1, q * C::BK, kEvictLast);        // Ht_cat rows of chunk q
-                    }
+                    for (int q = q0; q < q1; ++q) load_b(&tmB1, q * C::BK, kEvictLast);
                 if (s >= D && t1 == t0) {
                     // no owned tiles: still wait for block s - D's update, which throttles this
-                    // CTA's P1 publishing to the slot ring (block s + 1 + ... reuses slots of
-                    // blocks whose updaters must have read them: NS = D + 2)
-                    FZ_WAIT(2, wait_count(p.wdone + (s - D), 128u));
+                    // CTA's P1 publishing to the slot ring (the MMA runs P1(s + 1) after these
+                    // loads; blocks reuse slots NS = D + 2 apart)
+                    FZ_WAIT(2, wait_count(p.wdone + 2 * (s - D), 64u));
+                    FZ_WAIT(2, wait_count(p.wdone + 2 * (s - D) + 1, 64u));
                 } else if (s >= D) {
                     const int b = s - D;
-                    bool ready = false;
                     for (int j = t0; j < t1; ++j)
                         for (int h = 0; h < 2; ++h) {
-                            load_a(&tmA2, b * 128 + 64 * h, 4 * j, p.pol_p2);  // 64 rows x 128 cols
-                            if (!ready) {  // the block's new W rows (written by the updaters)
-                                FZ_WAIT(2, wait_count(p.wdone + b, 128u));
+                            if (j == t0) {
+                                FZ_WAIT(2, wait_count(p.wdone + 2 * b + h, 64u));
                                 fence_proxy_async_global();
-                                ready = true;
                             }
-                            load_b(&tmB2, b * 128 + 64 * h, kEvictNormal);  // W_cat rows
+                            load_b(&tmB2, b * 128 + 64 * h, kEvictNormal);
                         }
                 }
             }
@@ -243,15 +252,14 @@ __global__ void __launch_bounds__(512, 1)
             if (s >= D)
                 for (int j = t0; j < t1; ++j) unit(false), unit(true);
         }
-    } else if (warp == 2 || warp == 3) {
-        // ---------------- updaters: row r of block b -> CTA (128 b + r) mod G
-        const int u = tid - 64;
-        constexpr int P = 64 / KP;  // parts of the CTA range, summed in ascending order
-        const int j = u % KP, part = u / KP;
+    } else if (warp == 2) {
+        // ---------------- updater: row r of block b -> CTA (128 b + r) mod G
+        constexpr int P = 32 / KP;  // parts of the CTA range (kp 16: two), summed in fixed order
+        const int j = lane % KP, part = lane / KP;
         const int c_lo = part * G / P, c_hi = (part + 1) * G / P;
-        float hcol[KP];  // column u of HH^T (warp 2, lanes < KP)
+        float hcol[KP];  // column j of HH^T
 #pragma unroll
-        for (int q = 0; q < KP; ++q) hcol[q] = warp == 2 && lane < KP ? p.HHt[q * KP + lane] : 0.f;
+        for (int q = 0; q < KP; ++q) hcol[q] = p.HHt[q * KP + j];
         const unsigned target = 4u * unsigned(p.G1);
         bool bad = false;
         uint32_t gph = 0;
@@ -259,46 +267,39 @@ __global__ void __launch_bounds__(512, 1)
             const int b = int(g >> 7), row = int(g & 127);
             FZ_WAIT(9, wait_count(p.count + b, target));
             // one TMA operation gathers row `row` of every CTA's partial (G x kp floats, CTAs
-            // without P1 work hold zeros); then each part sums its CTA range in ascending order
-            if (u == 0) {
+            // without P1 work hold zeros); each lane sums its column over the CTAs in order
+            if (lane == 0) {
                 fence_proxy_async_global();  // the partials were written by generic stores
                 mbar_expect_tx(gbar, uint32_t(G * KP * 4));
                 tma_load_3d(gbuf, &tmS, gbar, 0, row, (b % p.NS) * G, kEvictFirst);
             }
             FZ_WAIT(10, mbar_wait(gbar, gph));
             gph ^= 1u;
-            float acc = 0.f;
+            float nu = 0.f;
 #pragma unroll 8
-            for (int c = c_lo; c < c_hi; ++c) acc += gbuf[c * KP + j];
-            red[u] = acc;
-            asm volatile("bar.sync 1, 64;" ::: "memory");
-            if (warp == 2) {
-                float nu = red[lane < KP ? lane : 0];
+            for (int c = c_lo; c < c_hi; ++c) nu += gbuf[c * KP + j];
+            if constexpr (P == 2) nu += __shfl_down_sync(0xffffffffu, nu, 16);  // part 0 + part 1
+            float* wrow = p.W + g * KP;
+            const float wold = wrow[j];
+            float de = 0.f;
 #pragma unroll
-                for (int pp = 1; pp < P; ++pp) nu += red[pp * KP + (lane < KP ? lane : 0)];
-                float* wrow = p.W + g * KP;
-                const float wold = lane < KP ? wrow[lane] : 0.f;
-                float de = 0.f;
-#pragma unroll
-                for (int q = 0; q < KP; ++q) de = fmaf(__shfl_sync(0xffffffffu, wold, q), hcol[q], de);
-                if (lane < KP) {
-                    // t * nu / (de + eps) as (t * nu) * rcp_rn(de + eps), the factor-update
-                    // kernel's formula (kernels_factor.cu)
-                    const float wn = (wold * nu) * __frcp_rn(de + p.eps);
-                    bad |= !isfinite(wn);
-                    wrow[lane] = wn;
-                    float* cw = p.Wcat + g * (2 * KP);
-                    cw[lane] = wn;
-                    cw[KP + lane] = tf32_lo(wn);
-                }
-                __syncwarp();
-                if (lane == 0) {
-                    fence_proxy_async_global();
-                    __threadfence();
-                    atomicAdd(p.wdone + b, 1u);
-                }
+            for (int q = 0; q < KP; ++q) de = fmaf(__shfl_sync(0xffffffffu, wold, q), hcol[q], de);
+            if (lane < KP) {
+                // t * nu / (de + eps) as (t * nu) * rcp_rn(de + eps), the factor-update
+                // kernel's formula (kernels_factor.cu)
+                const float wn = (wold * nu) * __frcp_rn(de + p.eps);
+                bad |= !isfinite(wn);
+                wrow[lane] = wn;
+                float* cw = p.Wcat + g * (2 * KP);
+                cw[lane] = wn;
+                cw[KP + lane] = tf32_lo(wn);
             }
-            asm volatile("bar.sync 1, 64;" ::: "memory");  // red is reused by the next row
+            __syncwarp();  // (also: gbuf is refilled by the next row's TMA)
+            if (lane == 0) {
+                fence_proxy_async_global();  // read by the B producers' TMA
+                __threadfence();
+                atomicAdd(p.wdone + 2 * b + (row >> 6), 1u);
+            }
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.flag, 1);
     } else if (warp >= 4 && warp < 12) {

@@ -433,7 +433,7 @@ void plan_fused_buffers(oocnmf_ctx* c) {
     c->fz_slots.alloc(size_t(fp.NS) * fp.G * kTile * c->kp * 4, "fused P1 slots");
     // CTAs without P1 work never publish: their slots must read as zeros in the updaters' gather
     ck(cudaMemsetAsync(c->fz_slots.p, 0, c->fz_slots.bytes, c->stream), "memset fused slots");
-    c->fz_count.alloc(size_t(2) * fp.NB * 4, "fused counters");
+    c->fz_count.alloc(size_t(3) * fp.NB * 4, "fused counters");  // count[NB] | wdone[2 NB]
 }
 
 void plan_dense(oocnmf_ctx* c) {

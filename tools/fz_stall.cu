@@ -71,7 +71,7 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
     CK(cudaMalloc(&slots, size_t(fp.NS) * fp.G * 128 * kp * 4));
     CK(cudaMemset(slots, 0, size_t(fp.NS) * fp.G * 128 * kp * 4));
-    CK(cudaMalloc(&cnt, size_t(2) * fp.NB * 4));
+    CK(cudaMalloc(&cnt, size_t(3) * fp.NB * 4));
     FusedArgs a{};
     a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = 2;
     a.q0 = idx, a.t0 = idx + fp.G + 1, a.act = idx + 2 * (fp.G + 1);
@@ -82,7 +82,7 @@ int main(int argc, char** argv) {
     printf("plan: G %d NB %d NT %d NQ %d D %d NS %d G1 %d; CTA 0: q [%d,%d) t [%d,%d)\n", fp.G, fp.NB, fp.NT, fp.NQ,
            fp.D, fp.NS, fp.G1, fp.q0[0], fp.q0[1], fp.t0[0], fp.t0[1]);
     auto run = [&] {
-        CK(cudaMemsetAsync(cnt, 0, size_t(2) * fp.NB * 4, 0));
+        CK(cudaMemsetAsync(cnt, 0, size_t(3) * fp.NB * 4, 0));
         CK(launch_mu_fused(kp, fp, A, mp, np, Hc, a, 0));
     };
     run();
