@@ -92,6 +92,7 @@ typedef struct {
     double h2d_bytes;      /* host->device bytes moved inside oocnmf_solve (out-of-core) */
     double fused_pass_ms;  /* one-pass dense W half (A read once: A·H^T, W update, W^T·A) */
     uint64_t fused_pass_launches;
+    uint64_t h2d_batches;  /* out-of-core: row batches copied host -> device inside the solve */
 } oocnmf_info;
 
 typedef struct oocnmf_ctx oocnmf_ctx;

@@ -32,7 +32,7 @@ class Info(C.Structure):
                 ("iterations_run", u64), ("converged", i32), ("reserved", i32), ("n_trace", u64),
                 ("aht_pass_ms", dbl), ("wta_pass_ms", dbl), ("aht_pass_launches", u64),
                 ("wta_pass_launches", u64), ("gpu_launches", u64), ("h2d_bytes", dbl),
-                ("fused_pass_ms", dbl), ("fused_pass_launches", u64)]
+                ("fused_pass_ms", dbl), ("fused_pass_launches", u64), ("h2d_batches", u64)]
 
     def as_dict(self):
         return {name: getattr(self, name) for name, _ in self._fields_ if name != "reserved"}

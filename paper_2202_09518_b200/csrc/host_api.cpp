@@ -5,6 +5,7 @@
 
 #include "oocnmf_b200/oocnmf.hpp"
 
+#include <chrono>
 #include <exception>
 #include <thread>
 #include "selection.hpp"
@@ -462,13 +463,55 @@ NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const Partitio
     }
     const index_t m = plan.m, n = plan.n, k = plan.k, r0 = slab.a_rows.begin, rows = slab.a_rows.extent();
     throw_status(oocnmf_set_problem(c, m, n, k, r0, rows));
-    if (a.host_f32) {
-        const index_t per_row = ((n + 127) / 128 * 128) * 4;
-        const index_t batch = store_cfg.budget_bytes ? std::max<index_t>(128, store_cfg.budget_bytes / 2 / per_row) : 0;
-        throw_status(oocnmf_attach_host_dense_f32(c, a.host_f32, a.host_ld ? a.host_ld : n, batch));
-    } else {
-        upload_slab(c, a, plan, slab);
+    const index_t per_row = ((n + 127) / 128 * 128) * 4;  // one padded f32 row of the device layout
+    const index_t batch = store_cfg.budget_bytes ? std::max<index_t>(128, store_cfg.budget_bytes / 2 / per_row) : 0;
+    StoreCounters sc{};
+    // ASource::file under a budget the dense window does not fit (the reference's ChunkStore over
+    // a PDN1 file, src/chunk_store.cpp:106-168): the window is read from the file once into
+    // page-locked host memory and streamed to the GPU in budget-sized row batches every
+    // iteration (out-of-core mode), instead of re-reading the file every iteration.
+    std::vector<float> host_window;
+    bool registered = false;
+    const bool pdn1 = !a.pdn1_path.empty() &&
+                      !(a.pdn1_path.size() >= 4 && a.pdn1_path.compare(a.pdn1_path.size() - 4, 4, ".mtx") == 0);
+    bool file_ooc = false;
+    if (pdn1 && store_cfg.budget_bytes) {
+        Pdn1File f(a.pdn1_path);
+        file_ooc = f.is_dense() && rows * per_row > store_cfg.budget_bytes;
+        if (file_ooc && (f.rows() != m || f.cols() != n))
+            throw ShapeError("nmf_distributed: file A does not match the plan");
     }
+    if (a.host_f32) {
+        throw_status(oocnmf_attach_host_dense_f32(c, a.host_f32, a.host_ld ? a.host_ld : n, batch));
+    } else if (file_ooc) {
+        const auto t_io = std::chrono::steady_clock::now();
+        host_window.resize(rows * n);
+        throw_status(oocnmf_pdn1_read_dense_f32(a.pdn1_path.c_str(), r0, r0 + rows, 0, n, host_window.data()));
+        sc.io_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_io).count();
+        sc.bytes_read = rows * n * index_t(Pdn1File(a.pdn1_path).dtype() == 1 ? 4 : 8);
+        throw_status(oocnmf_host_register(host_window.data(), host_window.size() * sizeof(float)));
+        registered = true;
+        throw_status(oocnmf_attach_host_dense_f32(c, host_window.data(), n, batch));
+    } else {
+        const auto t_io = std::chrono::steady_clock::now();
+        upload_slab(c, a, plan, slab);
+        if (!a.pdn1_path.empty()) {
+            sc.io_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_io).count();
+            if (pdn1) {
+                Pdn1File f(a.pdn1_path);
+                sc.bytes_read = f.is_dense() ? rows * n * index_t(f.dtype() == 1 ? 4 : 8) : f.window_bytes(slab.a_rows, {0, n});
+            }
+        }
+        sc.loads = 1;  // the slab is resident in HBM for the whole solve
+        sc.resident_bytes = sc.peak_resident_bytes = rows * per_row;
+    }
+    struct Unregister {
+        bool on;
+        void* p;
+        ~Unregister() {
+            if (on) oocnmf_host_unregister(p);
+        }
+    } unreg{registered, host_window.data()};
     if (cfg.init == FactorInit::from_files) {
         if (cfg.init_w->rows() != m || cfg.init_w->cols() != k || cfg.init_h->rows() != k || cfg.init_h->cols() != n)
             throw ShapeError("nmf_distributed: provided factors do not match plan");
@@ -485,11 +528,15 @@ NmfResult nmf_distributed(const ASource& a, const NmfConfig& cfg, const Partitio
     throw_status(oocnmf_get_factors_f64(c, nullptr, res.h.data()));
     throw_status(oocnmf_gather_w_f64(c, res.w.data()));
     fill_result(res, info, ti, te);
-    if (store_counters_out) {
-        *store_counters_out = StoreCounters{};
-        store_counters_out->peak_resident_bytes = info.peak_resident_bytes;
-        store_counters_out->bytes_read = index_t(info.h2d_bytes);
+    if (a.host_f32 || file_ooc) {
+        // every streamed row batch is a load into one of the two staging buffers, reclaimed by the
+        // batch two after it (the reference's load / evict counting, chunk_store.cpp:65-104)
+        sc.loads = info.h2d_batches;
+        sc.evictions = info.h2d_batches > 2 ? info.h2d_batches - 2 : 0;
+        sc.resident_bytes = sc.peak_resident_bytes = info.peak_resident_bytes;
+        res.counters.io_s = sc.io_seconds;
     }
+    if (store_counters_out) *store_counters_out = sc;
     return res;
 }
 

@@ -1195,6 +1195,7 @@ void solve_impl(oocnmf_ctx* c, const oocnmf_config* cfg, uint64_t* trace_iter, d
     if (c->kind == Kind::host) {
         inf.io_s = 0;  // overlapped with compute; reported through h2d_bytes
         inf.h2d_bytes = double(inf.iterations_run) * double(c->rows) * double(c->n) * 4.0;
+        inf.h2d_batches = inf.iterations_run * uint64_t((int64_t(c->rows) + c->batch_rows - 1) / c->batch_rows);
         inf.peak_resident_bytes = uint64_t(c->stage[0].bytes + c->stage[1].bytes);
     }
     inf.total_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();

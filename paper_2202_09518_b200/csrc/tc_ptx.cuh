@@ -83,6 +83,17 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int n, int a_mn, int b_mn) {
     return (1u << 4) | (2u << 7) | (2u << 10) | (uint32_t(a_mn) << 15) | (uint32_t(b_mn) << 16) |
            (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
 }
+// K-major SWIZZLE_128B operand (layout 2): 8-row x 128-byte swizzle atoms, 1024 B apart (SBO);
+// an MMA's 8-deep tf32 K slice is +32 B inside the atom row. (LBO is unused for swizzled K-major.)
+constexpr uint32_t kLayoutSW128 = 2;
+__device__ __forceinline__ uint64_t desc_kmajor_sw128(uint32_t addr) { return sdesc(addr, 16, 1024, kLayoutSW128); }
+// both operands from shared memory
+__device__ __forceinline__ void mma_ss(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(acc)
+        : "memory");
+}
 __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
     asm volatile(
         "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(
