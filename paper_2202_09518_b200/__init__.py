@@ -24,6 +24,8 @@ from .nmf import (  # noqa: F401
     SelectionConfig,
     SelectionReport,
     ShapeError,
+    StoreConfig,
+    StoreCounters,
     StoreError,
     Strategy,
     check,

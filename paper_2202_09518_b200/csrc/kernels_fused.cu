@@ -50,10 +50,8 @@ struct FzCfg {
     static constexpr int MAXT = KP == 16 ? 8 : 4;      // owned W^T A tiles (TMEM running sums)
     static constexpr int RUN_COL0 = NBUF * ACC_COLS;
     static constexpr int A_COL0 = RUN_COL0 + MAXT * KP;
-    // A_hi is read by the MMA straight from the TMA-loaded stage (shared memory, the tensor
-    // core's tf32 truncation); only A_lo = rna_tf32(A - A_hi) goes to a TMEM slot
-    static constexpr int ASLOT_COLS = BK;
-    static constexpr int ASLOTS = (512 - A_COL0) / ASLOT_COLS > 4 ? 4 : (512 - A_COL0) / ASLOT_COLS;
+    static constexpr int ASLOT_COLS = 2 * BK;
+    static constexpr int ASLOTS = (512 - A_COL0) / ASLOT_COLS;
     static_assert(ASLOTS >= 2, "TMEM budget");
     static constexpr int TMEM_COLS = 512;
     static constexpr int MAX_G = 192;                  // CTAs (smem list of P1 publishers)
@@ -63,9 +61,7 @@ struct FzCfg {
     static constexpr size_t GATHER_OFF = RING_BYTES + BAR_BYTES + MAX_G * 4 + 64 * 4;  // 128-aligned
     static constexpr size_t SMEM = GATHER_OFF + size_t(MAX_G) * KP * 4 + 1024;
     static_assert(SMEM <= 232448, "shared memory budget");
-    static constexpr uint32_t IDESC_HI_P1 = idesc_tf32(2 * KP, 0, 1);  // A K-major (rows x K)
-    static constexpr uint32_t IDESC_HI_P2 = idesc_tf32(2 * KP, 1, 1);  // A MN-major (A^T of the tile)
-    static constexpr uint32_t ATOM_A2 = 64 * 128;                      // P2 tile: 4 MN atoms of 64 K-rows
+    static constexpr uint32_t IDESC_HI = idesc_tf32(2 * KP, 0, 1);
     static constexpr uint32_t IDESC_KP = idesc_tf32(KP, 0, 1);
 };
 
@@ -133,7 +129,7 @@ __global__ void __launch_bounds__(512, 1)
     const int NB = p.NB, D = p.D;
 
     if (tid == 0) {
-        for (int s = 0; s < C::A_STAGES; ++s) mbar_init(fullA + s, 1), mbar_init(emptyA + s, 1);
+        for (int s = 0; s < C::A_STAGES; ++s) mbar_init(fullA + s, 1), mbar_init(emptyA + s, 8);
         for (int s = 0; s < C::B_STAGES; ++s) mbar_init(fullB + s, 1), mbar_init(emptyB + s, 1);
         for (int r = 0; r < C::ASLOTS; ++r) mbar_init(split + r, 8), mbar_init(afree + r, 1);
         for (int b = 0; b < C::NBUF; ++b) mbar_init(accfull + b, 1), mbar_init(accempty + b, 4);
@@ -213,35 +209,28 @@ __global__ void __launch_bounds__(512, 1)
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer: A_hi (shared memory) · [B_hi | B_lo] into D' = [H | L],
-        // A_lo (TMEM) · B_hi into L; commits release the B stage, the A stage and the A_lo slot
-        int sa = 0, sb = 0, r = 0, buf = 0;
-        uint32_t pha = 0, phb = 0, rph = 0, aph = 0;
+        // ---------------- MMA issuer
+        int sb = 0, r = 0, buf = 0;
+        uint32_t phb = 0, rph = 0, aph = 0;
         bool open = true;
-        auto unit = [&](bool close, bool p1) {
+        auto unit = [&](bool close) {
             if (open) FZ_WAIT(5, mbar_wait(accempty + buf, aph ^ 1u));
             FZ_WAIT(6, mbar_wait(fullB + sb, phb));
-            mbar_wait(fullA + sa, pha);
             FZ_WAIT(7, mbar_wait(split + r, rph));
             tc_fence_after();
             const uint32_t d = tmem + uint32_t(buf * C::ACC_COLS);
             const uint64_t db0 = desc_mnmajor(smem_u32(b_stage(sb)), 0, C::ATOM_STRIDE);
-            const uint32_t abase = smem_u32(a_stage(sa));
-            const uint32_t alo = tmem + uint32_t(C::A_COL0 + r * C::ASLOT_COLS);
+            const uint32_t ahi = tmem + uint32_t(C::A_COL0 + r * C::ASLOT_COLS), alo = ahi + C::BK;
             if (elect_one()) {
 #pragma unroll
                 for (int kk = 0; kk < C::KSTEPS; ++kk) {
                     const uint64_t db = db0 + uint64_t(kk * 64);
-                    const uint64_t da = p1 ? desc_kmajor_sw128(abase + (kk >> 2) * 16384 + (kk & 3) * 32)
-                                           : desc_mnmajor(abase, kk, C::ATOM_A2);
-                    mma_ss(d, da, db, p1 ? C::IDESC_HI_P1 : C::IDESC_HI_P2, (open && kk == 0) ? 0u : 1u);
+                    mma_ts(d, ahi + 8 * kk, db, C::IDESC_HI, (open && kk == 0) ? 0u : 1u);
                     mma_ts(d + KP, alo + 8 * kk, db, C::IDESC_KP, 1u);
                 }
                 mma_commit(emptyB + sb);
-                mma_commit(emptyA + sa);
                 mma_commit(afree + r);
             }
-            if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
             if (++r == C::ASLOTS) r = 0, rph ^= 1u;
             if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
             if (close) {
@@ -257,11 +246,11 @@ __global__ void __launch_bounds__(512, 1)
                 for (int q = q0; q < q1; ++q) {
                     const bool close = ++cu == du || q + 1 == q1;
                     if (close) cu = 0;
-                    unit(close, true);
+                    unit(close);
                 }
             }
             if (s >= D)
-                for (int j = t0; j < t1; ++j) unit(false, false), unit(true, false);
+                for (int j = t0; j < t1; ++j) unit(false), unit(true);
         }
     } else if (warp == 2) {
         // ---------------- updater: row r of block b -> CTA (128 b + r) mod G
@@ -314,7 +303,7 @@ __global__ void __launch_bounds__(512, 1)
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.flag, 1);
     } else if (warp >= 4 && warp < 12) {
-        // ---------------- split warps: A_lo of the stage -> TMEM slot (A_hi is the stage itself)
+        // ---------------- split warps: A tile -> [A_hi | A_lo] in TMEM slot
         const int t = 32 * (warp & 3) + lane;
         const int h = (warp - 4) >> 2;
         const uint32_t lane_bits = uint32_t(32 * (warp & 3)) << 16;
@@ -326,13 +315,15 @@ __global__ void __launch_bounds__(512, 1)
             tc_fence_after();
             const uint8_t* sA = a_stage(sa);
             const uint32_t dst = tmem + lane_bits + uint32_t(C::A_COL0 + rs * C::ASLOT_COLS);
-            uint32_t r[32];
+            uint32_t r[32], x[32];
             if (p1) {
                 // row t of K-atom h (K-major SW128): 8 chunks of 16 B, chunk c at (c ^ t%8)
                 const float4* row = reinterpret_cast<const float4*>(sA + h * 16384 + t * 128);
 #pragma unroll
                 for (int c = 0; c < 8; ++c) {
                     const float4 v = row[c ^ (t & 7)];
+                    x[4 * c] = __float_as_uint(v.x), x[4 * c + 1] = __float_as_uint(v.y),
+                    x[4 * c + 2] = __float_as_uint(v.z), x[4 * c + 3] = __float_as_uint(v.w);
                     lo_bits2(v.x, v.y, r[4 * c], r[4 * c + 1]);
                     lo_bits2(v.z, v.w, r[4 * c + 2], r[4 * c + 3]);
                 }
@@ -346,10 +337,14 @@ __global__ void __launch_bounds__(512, 1)
                     const int k = 32 * h + kr;
                     const float v0 = atom[k * 32 + (((e >> 3) ^ (k & 3)) << 3) + (e & 7)];
                     const float v1 = atom[(k + 1) * 32 + (((e >> 3) ^ ((k + 1) & 3)) << 3) + (e & 7)];
+                    x[kr] = __float_as_uint(v0), x[kr + 1] = __float_as_uint(v1);
                     lo_bits2(v0, v1, r[kr], r[kr + 1]);
                 }
             }
-            tmem_st32(dst + 32 * h, r);  // A_lo; A_hi stays in the stage for the MMA
+            tmem_st32(dst + 32 * h, x);
+            tmem_st32(dst + C::BK + 32 * h, r);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(emptyA + sa);
             if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
             tmem_st_wait();
             tc_fence_before();

@@ -639,6 +639,26 @@ def run_distributed_threads(a, cfg: "NmfConfig", plan: "PartitionPlan", stats_ou
     return results  # type: ignore[return-value]
 
 
+@dataclass
+class StoreConfig:
+    """include/oocnmf/nmf_distributed.hpp StoreConfig: budget_bytes = HBM staging budget of the
+    out-of-core row batches (0 = unlimited: A resident in HBM)."""
+    budget_bytes: int = 0
+    n_cb: int = 1
+    prefetch: bool = False
+
+
+@dataclass
+class StoreCounters:
+    """include/oocnmf/chunk_store.hpp:21-28, filled by nmf_distributed."""
+    loads: int = 0
+    evictions: int = 0
+    bytes_read: int = 0
+    resident_bytes: int = 0
+    peak_resident_bytes: int = 0
+    io_seconds: float = 0.0
+
+
 class _Window:
     """This rank's window of a file-backed A, placed so nmf_distributed's slicing selects it."""
 
@@ -677,8 +697,14 @@ def _file_window(path, plan: PartitionPlan, rank: int):
     return _Window(win, plan, rank)
 
 
+def _batch_rows(n: int, store_cfg: Optional[StoreConfig]) -> int:
+    per_row = (n + 127) // 128 * 128 * 4
+    return max(128, store_cfg.budget_bytes // 2 // per_row) if store_cfg and store_cfg.budget_bytes else 0
+
+
 def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host_slab: Optional[np.ndarray] = None,
-                    batch_rows: int = 0) -> NmfResult:
+                    batch_rows: int = 0, store_cfg: Optional[StoreConfig] = None,
+                    store_counters: Optional[StoreCounters] = None) -> NmfResult:
     """Row- (RNMF) or column-partitioned (CNMF) MU (src/nmf_distributed.cpp:112-289) —
     collective over ``comm``.
 
@@ -691,8 +717,39 @@ def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host
         raise ShapeError(f"nmf_distributed: cfg.k={cfg.k} disagrees with plan.k={plan.k}")
     if comm.size != plan.n_workers:
         raise ShapeError(f"nmf_distributed: group size {comm.size} != plan workers {plan.n_workers}")
+    import time
+
+    sc = StoreCounters()
     if isinstance(a, (str, os.PathLike)):
-        a = _file_window(a, plan, comm.rank)
+        (r0_, r1_), _ = plan.slabs[comm.rank]
+        per_row = (plan.n + 127) // 128 * 128 * 4
+        dense_pdn1 = False
+        if not str(a).endswith(".mtx"):
+            from .io import Pdn1File
+
+            f = Pdn1File(a)
+            dense_pdn1 = f.is_dense()
+        t_io = time.perf_counter()
+        if (plan.strategy == Strategy.rnmf and dense_pdn1 and store_cfg and store_cfg.budget_bytes
+                and host_slab is None and (r1_ - r0_) * per_row > store_cfg.budget_bytes):
+            # ASource::file over budget (src/chunk_store.cpp:106-168): read the window once into
+            # page-locked host memory, stream it in budget-sized row batches every iteration
+            w = _file_window(a, plan, comm.rank)
+            host_slab = np.ascontiguousarray(w.part, np.float32)
+            batch_rows = _batch_rows(plan.n, store_cfg)
+            sc.bytes_read = (r1_ - r0_) * plan.n * (4 if f.dtype == 1 else 8)
+            a = None
+        else:
+            a = _file_window(a, plan, comm.rank)
+            sc.loads, sc.resident_bytes = 1, (r1_ - r0_) * per_row
+            sc.peak_resident_bytes = sc.resident_bytes
+        sc.io_seconds = time.perf_counter() - t_io
+    elif host_slab is None:
+        (r0_, r1_), _ = plan.slabs[comm.rank]
+        sc.loads = 1
+        sc.resident_bytes = sc.peak_resident_bytes = (r1_ - r0_) * ((plan.n + 127) // 128 * 128 * 4)
+    if host_slab is not None and not batch_rows:
+        batch_rows = _batch_rows(plan.n, store_cfg)
     ctx = comm.ctx
     if plan.strategy == Strategy.cnmf:
         # column partition (src/nmf_distributed.cpp:112-149): W replicated, H column slabs
@@ -714,7 +771,11 @@ def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host
         return NmfResult(w, h, trace, int(info["iterations_run"]), bool(info["converged"]), _counters(info), info)
     (r0, r1), _ = plan.slabs[comm.rank]
     ctx.set_problem(plan.m, plan.n, plan.k, r0, r1 - r0)
+    registered = False
     if host_slab is not None:
+        if store_cfg is not None and sc.bytes_read:  # our own window buffer: page-lock it
+            check(_capi.lib().oocnmf_host_register(host_slab.ctypes.data, host_slab.nbytes))
+            registered = True
         ctx.attach_host(host_slab, batch_rows)
     elif isinstance(a, _Window):
         ctx.load_csr(a.part) if isinstance(a.part, CsrMatrix) else ctx.load_dense(a.part)
@@ -724,9 +785,20 @@ def nmf_distributed(a, cfg: NmfConfig, plan: PartitionPlan, comm: DistComm, host
         ctx.load_dense(np.asarray(a)[r0:r1])
     if cfg.init == FactorInit.from_files:
         ctx.set_factors(np.asarray(cfg.init_w)[r0:r1], cfg.init_h)
-    trace, info = ctx.solve(cfg)
-    _, h = ctx.get_factors()
-    w = ctx.gather_w()
+    try:
+        trace, info = ctx.solve(cfg)
+        _, h = ctx.get_factors()
+        w = ctx.gather_w()
+    finally:
+        if registered:
+            ctx.set_problem(plan.m, plan.n, plan.k, r0, r1 - r0)  # detach before unpinning
+            _capi.lib().oocnmf_host_unregister(host_slab.ctypes.data)
+    if host_slab is not None:
+        nb = int(info["h2d_batches"])
+        sc.loads, sc.evictions = nb, max(0, nb - 2)
+        sc.resident_bytes = sc.peak_resident_bytes = int(info["peak_resident_bytes"])
+    if store_counters is not None:
+        store_counters.__dict__.update(sc.__dict__)
     return NmfResult(w, h, trace, int(info["iterations_run"]), bool(info["converged"]), _counters(info), info)
 
 

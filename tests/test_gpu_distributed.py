@@ -107,3 +107,32 @@ def test_group_collectives_and_stats(gpu):
         g.close()
     with pytest.raises(nmf.ShapeError):
         nmf.spawn_group(nmf.device_count() + 1)
+
+
+@pytest.mark.parametrize("dtype", ["f32", "f64"])
+def test_file_source_over_budget_streams_out_of_core(gpu, tmp_path, dtype):
+    """ASource::file with a StoreConfig budget the rank's dense window exceeds (the reference's
+    ChunkStore over a PDN1 file, src/chunk_store.cpp:106-168): the window is read once into
+    page-locked host memory and streamed in budget-sized row batches every iteration; the result
+    equals the in-HBM solve and StoreCounters report the loads / bytes / residency."""
+    m, n, k = 1000, 700, 8
+    d = f32(port.uniform_dense(m, n, 9, 99))
+    nmf.write_pdn1(tmp_path / "a.pdn1", d, dtype=dtype)
+    cfg = nmf.NmfConfig(k=k, max_iters=20, error_check_interval=10, eta=0.0, seed=4, device=gpu)
+    plan = nmf.make_plan(m, n, k, 1, 1, nmf.Strategy.rnmf)
+    budget = 2 * 256 * 768 * 4  # two 256-row staging batches of the padded 768-column layout
+    comm = nmf.DistComm(0, 1, gpu)
+    try:
+        sc = nmf.StoreCounters()
+        ooc = nmf.nmf_distributed(str(tmp_path / "a.pdn1"), cfg, plan, comm,
+                                  store_cfg=nmf.StoreConfig(budget_bytes=budget), store_counters=sc)
+        sc_mem = nmf.StoreCounters()
+        mem = nmf.nmf_distributed(str(tmp_path / "a.pdn1"), cfg, plan, comm, store_counters=sc_mem)
+    finally:
+        comm.close()
+    np.testing.assert_allclose([e for _, e in ooc.error_trace], [e for _, e in mem.error_trace], rtol=5e-6)
+    assert np.linalg.norm(ooc.w - mem.w) <= 1e-5 * np.linalg.norm(mem.w)
+    assert sc.loads == 20 * 4 and sc.evictions == sc.loads - 2  # 4 batches of <= 256 rows per iteration
+    assert sc.bytes_read == m * n * (4 if dtype == "f32" else 8) and sc.io_seconds > 0
+    assert sc.peak_resident_bytes == 2 * 256 * 768 * 4 <= budget
+    assert sc_mem.loads == 1 and sc_mem.peak_resident_bytes == m * 768 * 4
