@@ -89,7 +89,7 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 // Developer stall profile (tools/fz_stall.cu, -DOOC_FZ_PROFILE): cycles each role spends in
 // each wait, summed over CTAs. Compiled out of the product.
 #ifdef OOC_FZ_PROFILE
-__device__ unsigned long long g_fz_prof[16];
+__device__ unsigned long long g_fz_prof[24];
 #define FZ_WAIT(idx, call)              \
     do {                                \
         const long long t_ = clock64(); \
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(512, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 #ifdef OOC_FZ_PROFILE
-    long long prof[16] = {};
+    long long prof[24] = {};
     const long long t_start = clock64();
 #endif
     auto a_stage = [&](int s) { return smem + s * C::A_BYTES; };
@@ -455,12 +455,12 @@ __global__ void __launch_bounds__(512, 1)
         }
     }
 #ifdef OOC_FZ_PROFILE
-    // per role: lane 0 of warp 0 (producer), 1 (MMA), 2 (updater), 4 (split), 12 (drain)
-    if (lane == 0 && (warp == 0 || warp == 1 || warp == 2 || warp == 4 || warp == 12)) {
+    // per role: lane 0 of warp 0 (A producer), 1 (MMA), 2 (updater), 3 (B producer), 4 (split),
+    // 12 (drain); the B producer's waits go to slots 11 (emptyB) and 12 (W ready)
+    if (lane == 0 && (warp <= 4 || warp == 12)) {
         for (int j = 0; j < 11; ++j)
-            if (prof[j]) atomicAdd(&g_fz_prof[j], (unsigned long long)prof[j]);
-        atomicAdd(&g_fz_prof[11 + (warp == 0 ? 0 : warp == 1 ? 1 : warp == 2 ? 2 : warp == 4 ? 3 : 4)],
-                  (unsigned long long)(clock64() - t_start));
+            if (prof[j]) atomicAdd(&g_fz_prof[warp == 3 && (j == 1 || j == 2) ? 10 + j : j], (unsigned long long)prof[j]);
+        atomicAdd(&g_fz_prof[16 + (warp == 12 ? 5 : warp)], (unsigned long long)(clock64() - t_start));
     }
 #endif
     __syncthreads();
@@ -549,10 +549,10 @@ void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahea
 }
 
 #ifdef OOC_FZ_PROFILE
-void fz_profile_read(unsigned long long* out16, bool reset) {
-    cudaMemcpyFromSymbol(out16, g_fz_prof, 16 * sizeof(unsigned long long));
+void fz_profile_read(unsigned long long* out24, bool reset) {
+    cudaMemcpyFromSymbol(out24, g_fz_prof, 24 * sizeof(unsigned long long));
     if (reset) {
-        unsigned long long z[16] = {};
+        unsigned long long z[24] = {};
         cudaMemcpyToSymbol(g_fz_prof, z, sizeof(z));
     }
 }

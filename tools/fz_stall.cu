@@ -4,7 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DOOC_FZ_PROFILE -I include \
 //     -I paper_2202_09518_b200/csrc tools/fz_stall.cu paper_2202_09518_b200/csrc/kernels_fused.cu \
 //     paper_2202_09518_b200/csrc/kernels_tc.cu paper_2202_09518_b200/csrc/kernels_factor.cu -lcuda -o tools/fz_stall
-// argv: kp mp np lookahead reps pol
+// argv: kp mp np lookahead reps pol drain_units
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -13,11 +13,11 @@
 
 #ifdef OOC_FZ_PROFILE
 namespace ooc {
-void fz_profile_read(unsigned long long* out16, bool reset);
+void fz_profile_read(unsigned long long* out24, bool reset);
 }
 #else
-static void fz_profile_read(unsigned long long* out16, bool) {
-    for (int i = 0; i < 16; ++i) out16[i] = 0;
+static void fz_profile_read(unsigned long long* out24, bool) {
+    for (int i = 0; i < 24; ++i) out24[i] = 0;
 }
 #endif
 using namespace ooc;
@@ -45,6 +45,7 @@ int main(int argc, char** argv) {
     const int D = argc > 4 ? atoi(argv[4]) : 2;
     const int reps = argc > 5 ? atoi(argv[5]) : 10;
     const int pol = argc > 6 ? atoi(argv[6]) : 0;
+    const int du = argc > 7 ? atoi(argv[7]) : 2;
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     float *A, *W, *Wc, *Hc, *HHt, *wta, *slots;
@@ -73,7 +74,7 @@ int main(int argc, char** argv) {
     CK(cudaMemset(slots, 0, size_t(fp.NS) * fp.G * 128 * kp * 4));
     CK(cudaMalloc(&cnt, size_t(3) * fp.NB * 4));
     FusedArgs a{};
-    a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = 2;
+    a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = du;
     a.q0 = idx, a.t0 = idx + fp.G + 1, a.act = idx + 2 * (fp.G + 1);
     a.p1slots = slots, a.count = cnt, a.wdone = cnt + fp.NB;
     a.W = W, a.Wcat = Wc, a.HHt = HHt, a.eps = 1e-12f, a.flag = flag, a.wta = wta;
@@ -87,7 +88,7 @@ int main(int argc, char** argv) {
     };
     run();
     CK(cudaDeviceSynchronize());
-    unsigned long long p[16];
+    unsigned long long p[24];
     fz_profile_read(p, true);
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0), cudaEventCreate(&e1);
@@ -102,13 +103,14 @@ int main(int argc, char** argv) {
     const double ctas = fp.G;
     printf("kp %d %ldx%ld D %d pol %d: %.3f ms per launch (%.2f TB/s of A once)\n", kp, long(mp), long(np), D, pol,
            ms / reps, double(mp) * np * 4 / (ms / reps) / 1e9);
-    const char* role[5] = {"producer", "mma", "updater", "split", "drain"};
+    const char* role[6] = {"producerA", "mma", "updater", "producerB", "split", "drain"};
     printf("  total cycles per unit:");
-    for (int r = 0; r < 5; ++r) printf(" %s %.0f", role[r], p[11 + r] / ctas / units);
+    for (int r = 0; r < 6; ++r) printf(" %s %.0f", role[r], p[16 + r] / ctas / units);
     printf("\n");
-    const char* name[11] = {"producer wait emptyA", "producer wait emptyB", "producer wait wdone", "split wait fullA",
-                            "split wait afree",     "mma wait accempty",    "mma wait fullB",      "mma wait split",
-                            "drain wait accfull",   "updater wait count",   "updater wait gather"};
-    for (int j = 0; j < 11; ++j) printf("  %-22s %8.0f cycles/unit\n", name[j], p[j] / ctas / units);
+    const char* name[13] = {"prodA wait emptyA",  "(unused)",          "(unused)",          "split wait fullA",
+                            "split wait afree",   "mma wait accempty", "mma wait fullB",    "mma wait split",
+                            "drain wait accfull", "updater wait count", "updater wait gather", "prodB wait emptyB",
+                            "prodB wait W ready"};
+    for (int j = 0; j < 13; ++j) printf("  %-22s %8.0f cycles/unit\n", name[j], p[j] / ctas / units);
     return 0;
 }
