@@ -211,7 +211,16 @@ struct oocnmf_ctx {
     // repeating the n-row H update on every rank, the ranks reduce-scatter it, update their
     // own n/N rows of H, and all-gather H (the same bytes as the all-reduce, 1/N of the update).
     // Needs whole 128-row tiles per rank (n a multiple of 128 N, as at config 3); else all-reduce.
-    bool shard_h() const { return collective() && !cnmf && kind == Kind::csr && np % (int64_t(kTile) * nranks) == 0; }
+    // Dense RNMF does the same (OOCNMF_SHARD_H=0 keeps the all-reduce): W^T A is 8.4 MB at
+    // config 2, and at N = 8 the replicated H update is a visible share of a 0.7 ms iteration.
+    bool shard_h() const {
+        static const bool dense_ok = [] {
+            const char* e = std::getenv("OOCNMF_SHARD_H");
+            return !(e && e[0] == '0');
+        }();
+        return collective() && !cnmf && (kind == Kind::csr || (kind == Kind::dense && dense_ok)) &&
+               np % (int64_t(kTile) * nranks) == 0;
+    }
     int64_t h_rows() const { return shard_h() ? np / nranks : np; }
     int64_t h_row0() const { return shard_h() ? h_rows() * rank : 0; }
 
@@ -810,7 +819,8 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         coll_end(c, s, kTagH, size_t(c->packed_count()) * 4 + size_t(kp) * kp * 8);  // nmf_distributed.cpp:171,178
     }
     if (timed) record(c, ev[eComm], s);
-    float* hcat = htlo(c);
+    // sharded H: the [H | H_lo] operand of the next pass is rebuilt from the gathered H below
+    float* hcat = c->shard_h() ? nullptr : htlo(c);
     if (c->h_fused) {  // updated inside the SpMM: the Gram of the new rows only
         count(c, launch_factor_update(kp, c->Ht.as<float>(), hr, nullptr, nullptr, nullptr, nullptr, eps, false,
                                       c->gram_h.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
@@ -828,6 +838,7 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         nck(ncclAllGather(c->Ht.as<float>() + h0 * kp, c->Ht.p, size_t(hr) * kp, ncclFloat, c->comm, s),
             "all-gather H");
         coll_end(c, s, kTagH, size_t(c->nranks) * hr * kp * 4);
+        if (htlo(c)) count(c, launch_split_cat(c->Ht.as<float>(), htlo(c), c->np, kp, s), "split H");
     }
     finish_hht(c, hr, c->collective() && (c->cnmf || c->shard_h()));
     if (timed) record(c, ev[eHdone], s);
