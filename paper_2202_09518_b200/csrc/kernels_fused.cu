@@ -82,6 +82,16 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
         if (t - t0 > 4000000000ull) asm volatile("trap;");
     }
 }
+// Publish: after the warp's stores (__syncwarp orders them before lane 0's release), one
+// gpu-scope release add on the counter (no separate membar.gl).
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+#ifdef OOC_FZ_AB_FENCE  // developer A/B: membar.gl + relaxed add
+    __threadfence();
+    atomicAdd(p, v);
+#else
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+#endif
+}
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -98,6 +108,23 @@ __device__ unsigned long long g_fz_prof[24];
     } while (0)
 #else
 #define FZ_WAIT(idx, call) call
+#endif
+// Latency trace of the first kFzTraceBlocks blocks (profile builds): globaltimer ns at each
+// CTA's P1 publish, at each row's updater seeing the count / finishing, at each CTA's B producer
+// seeing the block's rows 0-63 ready. [4][kFzTraceBlocks][128 or G]
+#ifdef OOC_FZ_PROFILE
+constexpr int kFzTraceBlocks = 64;
+__device__ unsigned long long* g_fz_trace = nullptr;
+__device__ __forceinline__ void fz_trace(int kind, int b, int i) {
+    if (g_fz_trace && b < kFzTraceBlocks) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        g_fz_trace[(size_t(kind) * kFzTraceBlocks + b) * 256 + i] = t;
+    }
+}
+#define FZ_TRACE(kind, b, i) fz_trace(kind, b, i)
+#else
+#define FZ_TRACE(kind, b, i)
 #endif
 
 template <int KP>
@@ -202,6 +229,7 @@ __global__ void __launch_bounds__(512, 1)
                             if (j == t0) {
                                 FZ_WAIT(2, wait_count(p.wdone + 2 * b + h, 64u));
                                 fence_proxy_async_global();
+                                if (h == 0) FZ_TRACE(3, b, cta);
                             }
                             load_b(&tmB2, b * 128 + 64 * h, kEvictNormal);
                         }
@@ -265,7 +293,10 @@ __global__ void __launch_bounds__(512, 1)
         uint32_t gph = 0;
         for (int64_t g = cta; g < int64_t(NB) * 128; g += G) {
             const int b = int(g >> 7), row = int(g & 127);
+            float* wrow = p.W + g * KP;
+            const float wold = wrow[j];  // last iteration's row: load it while P1 of the block runs
             FZ_WAIT(9, wait_count(p.count + b, target));
+            if (lane == 0) FZ_TRACE(1, b, row);
             // one TMA operation gathers row `row` of every CTA's partial (G x kp floats, CTAs
             // without P1 work hold zeros); each lane sums its column over the CTAs in order
             if (lane == 0) {
@@ -279,8 +310,6 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll 8
             for (int c = c_lo; c < c_hi; ++c) nu += gbuf[c * KP + j];
             if constexpr (P == 2) nu += __shfl_down_sync(0xffffffffu, nu, 16);  // part 0 + part 1
-            float* wrow = p.W + g * KP;
-            const float wold = wrow[j];
             float de = 0.f;
 #pragma unroll
             for (int q = 0; q < KP; ++q) de = fmaf(__shfl_sync(0xffffffffu, wold, q), hcol[q], de);
@@ -297,8 +326,8 @@ __global__ void __launch_bounds__(512, 1)
             __syncwarp();  // (also: gbuf is refilled by the next row's TMA)
             if (lane == 0) {
                 fence_proxy_async_global();  // read by the B producers' TMA
-                __threadfence();
-                atomicAdd(p.wdone + 2 * b + (row >> 6), 1u);
+                red_release_add(p.wdone + 2 * b + (row >> 6), 1u);
+                FZ_TRACE(2, b, row);
             }
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.flag, 1);
@@ -406,8 +435,8 @@ __global__ void __launch_bounds__(512, 1)
                 __syncwarp();
                 if (lane == 0) {
                     fence_proxy_async_global();  // read back by the updaters' TMA (async proxy)
-                    __threadfence();
-                    atomicAdd(p.count + s, 1u);
+                    red_release_add(p.count + s, 1u);
+                    if (warp == 15) FZ_TRACE(0, s, cta);
                 }
             }
             if (s >= D) {
@@ -549,6 +578,7 @@ void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahea
 }
 
 #ifdef OOC_FZ_PROFILE
+void fz_trace_set(unsigned long long* buf) { cudaMemcpyToSymbol(g_fz_trace, &buf, sizeof(buf)); }
 void fz_profile_read(unsigned long long* out24, bool reset) {
     cudaMemcpyFromSymbol(out24, g_fz_prof, 24 * sizeof(unsigned long long));
     if (reset) {

@@ -7,6 +7,7 @@
 // argv: kp mp np lookahead reps pol drain_units
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <vector>
 
 #include "kernels.h"
@@ -14,6 +15,7 @@
 #ifdef OOC_FZ_PROFILE
 namespace ooc {
 void fz_profile_read(unsigned long long* out24, bool reset);
+void fz_trace_set(unsigned long long* buf);
 }
 #else
 static void fz_profile_read(unsigned long long* out24, bool) {
@@ -112,5 +114,75 @@ int main(int argc, char** argv) {
                             "drain wait accfull", "updater wait count", "updater wait gather", "prodB wait emptyB",
                             "prodB wait W ready"};
     for (int j = 0; j < 13; ++j) printf("  %-22s %8.0f cycles/unit\n", name[j], p[j] / ctas / units);
+#ifdef OOC_FZ_PROFILE
+    // latency trace of blocks 8..63 of one more launch (ns, relative to the block's first publish)
+    {
+        const int TB = 64;
+        unsigned long long* tr;
+        CK(cudaMalloc(&tr, size_t(4) * TB * 256 * 8));
+        CK(cudaMemset(tr, 0, size_t(4) * TB * 256 * 8));
+        fz_trace_set(tr);
+        run();
+        CK(cudaDeviceSynchronize());
+        fz_trace_set(nullptr);
+        std::vector<unsigned long long> h(size_t(4) * TB * 256);
+        CK(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost));
+        auto at = [&](int kind, int b, int i) { return h[(size_t(kind) * TB + b) * 256 + i]; };
+        double s_last = 0, s_cnt = 0, s_upd_med = 0, s_upd = 0, s_wr = 0, s_wr_max = 0, s_step = 0;
+        int nb = 0;
+        for (int b = 8; b < TB && b < fp.NB; ++b) {
+            unsigned long long p0 = ~0ull, p1 = 0, c0 = ~0ull, u1 = 0, w0 = ~0ull, w1 = 0;
+            std::vector<unsigned long long> ups;
+            for (int c = 0; c < fp.G; ++c)
+                if (at(0, b, c)) p0 = std::min(p0, at(0, b, c)), p1 = std::max(p1, at(0, b, c));
+            for (int r = 0; r < 128; ++r) {
+                if (at(1, b, r)) c0 = std::min(c0, at(1, b, r));
+                if (at(2, b, r) && r < 64) u1 = std::max(u1, at(2, b, r)), ups.push_back(at(2, b, r));
+            }
+            for (int c = 0; c < fp.G; ++c)
+                if (at(3, b, c)) w0 = std::min(w0, at(3, b, c)), w1 = std::max(w1, at(3, b, c));
+            std::sort(ups.begin(), ups.end());
+            s_last += double(p1 - p0), s_cnt += double(c0 - p1), s_upd += double(u1 - c0);
+            s_upd_med += double(ups[ups.size() / 2] - c0);
+            s_wr += double(w0 - u1), s_wr_max += double(w1 - u1);
+            if (b > 8) s_step += double(p1 - at(0, b - 1, 0));
+            ++nb;
+        }
+        // per-CTA publish offset vs the block's median publish (us), averaged over blocks
+        std::vector<double> off(fp.G, 0.0);
+        for (int b = 8; b < TB && b < fp.NB; ++b) {
+            std::vector<unsigned long long> v;
+            for (int c = 0; c < fp.G; ++c) v.push_back(at(0, b, c));
+            std::vector<unsigned long long> srt = v;
+            std::sort(srt.begin(), srt.end());
+            const double med = double(srt[srt.size() / 2]);
+            for (int c = 0; c < fp.G; ++c) off[c] += (double(v[c]) - med) / 1e3 / nb;
+        }
+        std::vector<int> idx(fp.G);
+        for (int c = 0; c < fp.G; ++c) idx[c] = c;
+        std::sort(idx.begin(), idx.end(), [&](int x, int y) { return off[x] < off[y]; });
+        printf("  earliest CTAs (cta:offset_us:n1:n2):");
+        for (int i = 0; i < 6; ++i)
+            printf(" %d:%.2f:%d:%d", idx[i], off[idx[i]], fp.q0[idx[i] + 1] - fp.q0[idx[i]],
+                   2 * (fp.t0[idx[i] + 1] - fp.t0[idx[i]]));
+        printf("\n  latest CTAs:");
+        for (int i = fp.G - 6; i < fp.G; ++i)
+            printf(" %d:%.2f:%d:%d", idx[i], off[idx[i]], fp.q0[idx[i] + 1] - fp.q0[idx[i]],
+                   2 * (fp.t0[idx[i] + 1] - fp.t0[idx[i]]));
+        double by_n1[16] = {}, cnt_n1[16] = {};
+        for (int c = 0; c < fp.G; ++c) {
+            const int n1 = fp.q0[c + 1] - fp.q0[c];
+            if (n1 < 16) by_n1[n1] += off[c], cnt_n1[n1] += 1;
+        }
+        printf("\n  mean offset by P1 units:");
+        for (int k = 0; k < 16; ++k)
+            if (cnt_n1[k]) printf(" n1=%d:%.2f(%d)", k, by_n1[k] / cnt_n1[k], int(cnt_n1[k]));
+        printf("\n");
+        printf("  latency (us, mean over %d blocks): publish spread %.2f | last publish -> first updater sees count "
+               "%.2f | -> all 64 rows updated %.2f (median row %.2f) | -> first B producer sees W %.2f, last %.2f\n",
+               nb, s_last / nb / 1e3, s_cnt / nb / 1e3, s_upd / nb / 1e3, s_upd_med / nb / 1e3, s_wr / nb / 1e3,
+               s_wr_max / nb / 1e3);
+    }
+#endif
     return 0;
 }
