@@ -74,7 +74,9 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
     uint64_t t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while (true) {
+#ifndef OOC_FZ_SPIN
         __nanosleep(64);
+#endif
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
         if (v >= target) return;
         uint64_t t;

@@ -125,6 +125,13 @@ struct oocnmf_ctx {
     cudaEvent_t ev_rs[kMaxRsChunks + 1] = {};
     DevBuf wtp;                  // W^T A in chunk-major order [chunk][rank][rows][kp] (send side)
     bool rs_done = false;        // this iteration's reduce-scatter was issued with the SpMM
+    // sharded CSR H: the new H rows reach the other ranks as N broadcasts on comm_stream, and the
+    // next A·Ht SpMM consumes Ht slice by slice as they land (own slice first): ev_bc[root]
+    bool ag_pending = false;
+    std::vector<cudaEvent_t> ev_bc;
+    cudaEvent_t ev_hdone = nullptr;
+    DevBuf segR;                 // CSR row segments at the rank-slice column boundaries
+    int segR_n = 0;
     bool no_check_next = false;  // the iteration being enqueued is not followed by an error check
     bool h_fused = false;        // ... and its H update ran inside the A^T W SpMM
 
@@ -277,8 +284,7 @@ size_t reap_marks(oocnmf_ctx* c) {
     while (!c->marks.empty()) {
         const auto& m = c->marks.front();
         const cudaError_t q = cudaEventQuery(m.end);
-        if (q == cudaErrorNotReady) break;
-        if (q != cudaSuccess) ck(q, "collective event");
+        if (q != cudaSuccess) break;  // not ready (or a fault, reported by the caller's wait)
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, m.beg, m.end) == cudaSuccess) c->tag_secs[m.tag] += ms * 1e-3;
         cudaGetLastError();
@@ -294,6 +300,7 @@ size_t reap_marks(oocnmf_ctx* c) {
     c->comm = nullptr;
     c->poisoned = true;
     cudaStreamSynchronize(c->stream);
+    cudaStreamSynchronize(c->comm_stream);
     cudaGetLastError();
     for (auto& m : c->marks) c->ev_pool.push_back(m.beg), c->ev_pool.push_back(m.end);
     c->marks.clear();
@@ -316,7 +323,14 @@ void wait_for(oocnmf_ctx* c, cudaStream_t s, cudaEvent_t e, const char* what) {
         const cudaError_t q = e ? cudaEventQuery(e) : cudaStreamQuery(s);
         if (reap_marks(c)) last = std::chrono::steady_clock::now();
         if (q == cudaSuccess) return;
-        if (q != cudaErrorNotReady) ck(q, what);
+        if (q != cudaErrorNotReady) {
+            // a device fault while collectives are in flight: typically a peer process died and
+            // its NVLink-mapped buffers vanished under the NCCL kernels (the context is lost)
+            if (!c->marks.empty())
+                abort_comm(c, std::string("device error (") + cudaGetErrorString(q) + ") while waiting for " + what +
+                                  " with collectives in flight (a peer rank failed?)");
+            ck(q, what);
+        }
         ncclResult_t ar = ncclSuccess;
         if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess && ar != ncclInProgress)
             abort_comm(c, std::string("NCCL async error (") + ncclGetErrorString(ar) + ") while waiting for " + what);
@@ -466,6 +480,7 @@ void reset_source(oocnmf_ctx* c) {
     c->rp.release(), c->ci.release(), c->v.release();
     c->rpT.release(), c->ciT.release(), c->vT.release();
     c->chA.seg.release(), c->chT.seg.release();
+    c->segR.release(), c->segR_n = 0, c->ag_pending = false;
     c->chA.C = c->chT.C = 1, c->chA.kp = c->chT.kp = 0;
     c->stage[0].release(), c->stage[1].release();
     c->hA = nullptr;
@@ -612,6 +627,46 @@ int rs_chunks(oocnmf_ctx* c) {
     return c->shard_h() && c->chT.C <= 1 ? int(std::min<int64_t>(S, c->h_rows())) : 1;
 }
 
+// Sharded CSR H update: overlap the H all-gather with the next iteration's A·Ht SpMM
+// (OOCNMF_AG_OVERLAP=0 keeps the single all-gather).
+bool ag_overlap(const oocnmf_ctx* c) {
+    static const bool on = [] {
+        const char* e = std::getenv("OOCNMF_AG_OVERLAP");
+        return !(e && e[0] == '0');
+    }();
+    return on && c->kind == Kind::csr && c->shard_h() && c->chA.C <= 1;
+}
+// The main stream waits for every pending Ht slice (anything but the sliced SpMM reads all of Ht).
+void ht_ready(oocnmf_ctx* c) {
+    if (!c->ag_pending) return;
+    ck(cudaStreamWaitEvent(c->stream, c->ev_bc[c->nranks - 1], 0), "wait H broadcasts");
+    c->ag_pending = false;
+}
+// A·Ht into N1 over the rank slices of Ht: this rank's slice first, then the others as their
+// broadcasts land (k_spmm_seg over the column ranges, accumulating).
+void spmm_aht_sliced(oocnmf_ctx* c, cudaStream_t s) {
+    const int N = c->nranks;
+    const int64_t rows = int64_t(c->rows), hr = c->h_rows();
+    if (c->segR_n != N) {
+        c->segR.alloc(size_t(N + 1) * rows * 8, "rank-slice segments");
+        ck(launch_csr_segments(c->rp.as<int64_t>(), c->ci.as<int32_t>(), rows, hr, N, c->segR.as<int64_t>(), s),
+           "rank-slice segments");
+        c->segR_n = N;
+    }
+    const int64_t* seg = c->segR.as<int64_t>();
+    bool first = true;
+    for (int i = -1; i < N; ++i) {
+        const int r = i < 0 ? c->rank : i;
+        if (i >= 0 && r == c->rank) continue;
+        if (i >= 0) ck(cudaStreamWaitEvent(s, c->ev_bc[r], 0), "wait H slice");
+        count(c, launch_spmm_seg(c->kp, seg + int64_t(r) * rows, seg + int64_t(r + 1) * rows, c->ci.as<int32_t>(),
+                                 c->v.as<float>(), rows, c->Ht.as<float>(), c->N1.as<float>(), !first, s),
+              "spmm A Ht (slice)");
+        first = false;
+    }
+    c->ag_pending = false;
+}
+
 void spmm_wta_reduce_scatter(oocnmf_ctx* c, cudaStream_t s) {
     const int kp = c->kp, N = c->nranks, S = rs_chunks(c);
     const int64_t hr = c->h_rows(), h0 = c->h_row0(), n = int64_t(c->n);
@@ -712,7 +767,15 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         }
         rec(eReduced);
     } else if (c->kind == Kind::csr) {
-        if (fuse_w_update(c)) {
+        if (c->ag_pending) {
+            // H slices still arriving: the SpMM consumes them as they land, then the W update
+            spmm_aht_sliced(c, s);
+            rec(eAht);
+            count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
+                                          c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
+                                          c->flag.as<int>(), nullptr, s),
+                  "W update");
+        } else if (fuse_w_update(c)) {
             // A·Ht and the W update in one pass over the rows, then the Gram of the new W
             count(c, launch_spmm_mu(kp, c->rp.as<int64_t>(), c->ci.as<int32_t>(), c->v.as<float>(), c->rows,
                                     c->Ht.as<float>(), c->W.as<float>(), c->HHt.as<float>(), eps, c->flag.as<int>(), s),
@@ -832,8 +895,26 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
                                       c->flag.as<int>(), hcat ? hcat + h0 * 2 * kp : nullptr, s),
               "H update");
     }
-    if (c->shard_h())
-    {
+    if (c->shard_h() && ag_overlap(c)) {
+        // the all-gather as N broadcasts on the comm stream; the next SpMM starts on this rank's
+        // slice and picks up the others as their events fire (spmm_aht_sliced)
+        if (int(c->ev_bc.size()) < c->nranks) {
+            c->ev_bc.resize(c->nranks, nullptr);
+            for (auto& e : c->ev_bc)
+                if (!e) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            if (!c->ev_hdone) ck(cudaEventCreateWithFlags(&c->ev_hdone, cudaEventDisableTiming), "event");
+        }
+        ck(cudaEventRecord(c->ev_hdone, s), "event");
+        ck(cudaStreamWaitEvent(c->comm_stream, c->ev_hdone, 0), "wait H update");
+        coll_begin(c, c->comm_stream);
+        for (int r = 0; r < c->nranks; ++r) {
+            float* sl = c->Ht.as<float>() + size_t(r) * hr * kp;
+            nck(ncclBroadcast(sl, sl, size_t(hr) * kp, ncclFloat, r, c->comm, c->comm_stream), "broadcast H slice");
+            ck(cudaEventRecord(c->ev_bc[r], c->comm_stream), "event");
+        }
+        coll_end(c, c->comm_stream, kTagH, size_t(c->nranks) * hr * kp * 4);
+        c->ag_pending = true;
+    } else if (c->shard_h()) {
         coll_begin(c, s);
         nck(ncclAllGather(c->Ht.as<float>() + h0 * kp, c->Ht.p, size_t(hr) * kp, ncclFloat, c->comm, s),
             "all-gather H");
@@ -857,6 +938,7 @@ constexpr double kAutoDirectBelow = 0.1;
 // when it is 0); 1 (direct) always takes the residual; 2 (trace) never. Out-of-core runs use
 // the trace form only.
 void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
+    ht_ready(c);  // the direct residual reads all of Ht
     const int kp = c->kp;
     cudaStream_t s = c->stream;
     double* scal = c->scal.as<double>();
@@ -1766,6 +1848,9 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
         if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
         for (auto e : c->ev_rs)
             if (e) cudaEventDestroy(e);
+        for (auto e : c->ev_bc)
+            if (e) cudaEventDestroy(e);
+        if (c->ev_hdone) cudaEventDestroy(c->ev_hdone);
         delete c;
     });
 }
