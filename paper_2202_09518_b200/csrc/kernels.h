@@ -44,6 +44,7 @@ cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
 struct FusedArgs {
     int NB, D, NS, G1;     // row blocks, P2 lookahead (blocks), P1 slot ring depth, P1 publishers
     int drain_units;       // P1 chain length (kernels_tc.cu numerics)
+    int p2_first;          // unit order of step s: P2(s - D) before P1(s) (else after)
     const int* q0;         // [G + 1] P1 chunk (64 cols) range per CTA
     const int* t0;         // [G + 1] owned W^T A tile (128 cols) range per CTA
     const int* act;        // [G1] CTAs with P1 work, ascending

@@ -195,13 +195,16 @@ __global__ void __launch_bounds__(512, 1)
                 tma_load_3d(a_stage(sa), m, fullA + sa, 0, y, z, pol);
                 if (++sa == C::A_STAGES) sa = 0, pha ^= 1u;
             };
-            for (int s = 0; s < NB + D; ++s) {
+            auto p1 = [&](int s) {
                 if (s < NB)
                     for (int q = q0; q < q1; ++q) load_a(&tmA1, s * 128, 2 * q, p.pol_p1);  // block s, K-atoms 2q..
+            };
+            auto p2 = [&](int s) {
                 if (s >= D)
                     for (int j = t0; j < t1; ++j)
                         for (int h = 0; h < 2; ++h) load_a(&tmA2, (s - D) * 128 + 64 * h, 4 * j, p.pol_p2);
-            }
+            };
+            for (int s = 0; s < NB + D; ++s) p.p2_first ? (p2(s), p1(s)) : (p1(s), p2(s));
         }
     } else if (warp == 3) {
         // ---------------- B producer: [Ht | Ht_lo] chunk rows for P1; for P2 the block's new
@@ -215,9 +218,11 @@ __global__ void __launch_bounds__(512, 1)
                 tma_load_3d(b_stage(sb), m, fullB + sb, 0, y, 0, pol);
                 if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
             };
-            for (int s = 0; s < NB + D; ++s) {
+            auto p1 = [&](int s) {
                 if (s < NB)
                     for (int q = q0; q < q1; ++q) load_b(&tmB1, q * C::BK, kEvictLast);
+            };
+            auto p2 = [&](int s) {
                 if (s >= D && t1 == t0) {
                     // no owned tiles: still wait for block s - D's update, which throttles this
                     // CTA's P1 publishing to the slot ring (the MMA runs P1(s + 1) after these
@@ -236,7 +241,8 @@ __global__ void __launch_bounds__(512, 1)
                             load_b(&tmB2, b * 128 + 64 * h, kEvictNormal);
                         }
                 }
-            }
+            };
+            for (int s = 0; s < NB + D; ++s) p.p2_first ? (p2(s), p1(s)) : (p1(s), p2(s));
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer
@@ -270,7 +276,7 @@ __global__ void __launch_bounds__(512, 1)
             open = close;
             __syncwarp();
         };
-        for (int s = 0; s < NB + D; ++s) {
+        auto p1 = [&](int s) {
             if (s < NB) {
                 int cu = 0;
                 for (int q = q0; q < q1; ++q) {
@@ -279,9 +285,12 @@ __global__ void __launch_bounds__(512, 1)
                     unit(close);
                 }
             }
+        };
+        auto p2 = [&](int s) {
             if (s >= D)
                 for (int j = t0; j < t1; ++j) unit(false), unit(true);
-        }
+        };
+        for (int s = 0; s < NB + D; ++s) p.p2_first ? (p2(s), p1(s)) : (p1(s), p2(s));
     } else if (warp == 2) {
         // ---------------- updater: row r of block b -> CTA (128 b + r) mod G
         constexpr int P = 32 / KP;  // parts of the CTA range (kp 16: two), summed in fixed order
@@ -383,12 +392,15 @@ __global__ void __launch_bounds__(512, 1)
             if (lane == 0) mbar_arrive(split + rs);
             if (++rs == C::ASLOTS) rs = 0, rph ^= 1u;
         };
-        for (int s = 0; s < NB + D; ++s) {
+        auto p1 = [&](int s) {
             if (s < NB)
                 for (int q = q0; q < q1; ++q) unit(true);
+        };
+        auto p2 = [&](int s) {
             if (s >= D)
                 for (int j = t0; j < t1; ++j) unit(false), unit(false);
-        }
+        };
+        for (int s = 0; s < NB + D; ++s) p.p2_first ? (p2(s), p1(s)) : (p1(s), p2(s));
     } else if (warp >= 12) {
         // ---------------- drain: P1 chains -> f32 row sums -> published partial; P2 chains
         // (one per block and owned tile) -> TMEM running sums of W^T A
@@ -419,7 +431,7 @@ __global__ void __launch_bounds__(512, 1)
             if (lane == 0) mbar_arrive(accempty + buf);
             if (++buf == C::NBUF) buf = 0, aph ^= 1u;
         };
-        for (int s = 0; s < NB + D; ++s) {
+        auto p1 = [&](int s) {
             if (s < NB && q1 > q0) {
                 int cu = 0;
                 for (int q = q0; q < q1; ++q) {
@@ -441,6 +453,8 @@ __global__ void __launch_bounds__(512, 1)
                     if (warp == 15) FZ_TRACE(0, s, cta);
                 }
             }
+        };
+        auto p2 = [&](int s) {
             if (s >= D) {
                 const int b = s - D;
                 for (int j = t0; j < t1; ++j) {
@@ -468,7 +482,8 @@ __global__ void __launch_bounds__(512, 1)
                     for (int jj = 0; jj < KP; ++jj) acc[jj] = 0.f;
                 }
             }
-        }
+        };
+        for (int s = 0; s < NB + D; ++s) p.p2_first ? (p2(s), p1(s)) : (p1(s), p2(s));
         // the owned tiles of W^T A (np x kp, row = column of A)
         for (int j = t0; j < t1; ++j) {
             const uint32_t run = tmem + lane_bits + uint32_t(C::RUN_COL0 + (j - t0) * KP);

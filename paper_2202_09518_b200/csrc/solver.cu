@@ -431,9 +431,11 @@ void alloc_factors(oocnmf_ctx* c) {
     ck(cudaMemsetAsync(c->flag.p, 0, 4, c->stream), "memset flag");
 }
 
-// OOCNMF_FUSED=0 keeps the two-pass W half; OOCNMF_FUSED_D sets the P2 lookahead in row
-// blocks (default 2: three 32 MB blocks of A live in L2 at n = 65536); OOCNMF_FUSED_POL picks
-// the L2 policies of the two A loads (0: normal / first, 1: last / first, 2: normal / normal).
+// OOCNMF_FUSED=0 keeps the two-pass W half; OOCNMF_FUSED_D sets the P2 lag in row blocks
+// (default 1: two 32 MB blocks of A in L2 at n = 65536 — at 2 the third block pushes the A
+// re-reads out of L2, 32 GB instead of 19 GB of DRAM reads per launch); OOCNMF_FUSED_P2FIRST=1
+// orders each step P2(s - D) before P1(s); OOCNMF_FUSED_POL picks the L2 policies of the two A
+// loads (0: normal / first, 1: last / first, 2: normal / normal).
 bool fused_wanted(const oocnmf_ctx* c) {
     const char* e = std::getenv("OOCNMF_FUSED");
     if (e && e[0] == '0') return false;
@@ -446,7 +448,7 @@ int env_int(const char* name, int dflt) {
 
 void plan_fused_buffers(oocnmf_ctx* c) {
     FusedPlan& fp = c->fplan;
-    plan_fused(fp, c->mp, c->np, c->num_sms, env_int("OOCNMF_FUSED_D", 2));
+    plan_fused(fp, c->mp, c->np, c->num_sms, env_int("OOCNMF_FUSED_D", 1));
     std::vector<int> idx;
     idx.insert(idx.end(), fp.q0.begin(), fp.q0.end());
     idx.insert(idx.end(), fp.t0.begin(), fp.t0.end());
@@ -715,7 +717,9 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         const int* idx = c->fz_idx.as<int>();
         static const int pol = env_int("OOCNMF_FUSED_POL", 0);
         FusedArgs a{};
+        static const int p2f = env_int("OOCNMF_FUSED_P2FIRST", 0);
         a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = tc::tc_drain_units();
+        a.p2_first = p2f;
         a.q0 = idx, a.t0 = idx + fp.G + 1, a.act = idx + 2 * (fp.G + 1);
         a.p1slots = c->fz_slots.as<float>();
         a.count = c->fz_count.as<unsigned>(), a.wdone = a.count + fp.NB;

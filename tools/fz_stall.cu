@@ -4,7 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DOOC_FZ_PROFILE -I include \
 //     -I paper_2202_09518_b200/csrc tools/fz_stall.cu paper_2202_09518_b200/csrc/kernels_fused.cu \
 //     paper_2202_09518_b200/csrc/kernels_tc.cu paper_2202_09518_b200/csrc/kernels_factor.cu -lcuda -o tools/fz_stall
-// argv: kp mp np lookahead reps pol drain_units
+// argv: kp mp np lookahead reps pol drain_units p2_first
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
@@ -48,6 +48,7 @@ int main(int argc, char** argv) {
     const int reps = argc > 5 ? atoi(argv[5]) : 10;
     const int pol = argc > 6 ? atoi(argv[6]) : 0;
     const int du = argc > 7 ? atoi(argv[7]) : 2;
+    const int p2f = argc > 8 ? atoi(argv[8]) : 0;
     int sms = 0;
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
     float *A, *W, *Wc, *Hc, *HHt, *wta, *slots;
@@ -77,6 +78,7 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&cnt, size_t(3) * fp.NB * 4));
     FusedArgs a{};
     a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = du;
+    a.p2_first = p2f;
     a.q0 = idx, a.t0 = idx + fp.G + 1, a.act = idx + 2 * (fp.G + 1);
     a.p1slots = slots, a.count = cnt, a.wdone = cnt + fp.NB;
     a.W = W, a.Wcat = Wc, a.HHt = HHt, a.eps = 1e-12f, a.flag = flag, a.wta = wta;
@@ -103,7 +105,7 @@ int main(int argc, char** argv) {
     fz_profile_read(p, true);
     const double units = double(fp.NB) * (fp.NQ + 2.0 * fp.NT) / fp.G * reps;  // per CTA
     const double ctas = fp.G;
-    printf("kp %d %ldx%ld D %d pol %d: %.3f ms per launch (%.2f TB/s of A once)\n", kp, long(mp), long(np), D, pol,
+    printf("p2_first %d kp %d %ldx%ld D %d pol %d: %.3f ms per launch (%.2f TB/s of A once)\n", p2f, kp, long(mp), long(np), D, pol,
            ms / reps, double(mp) * np * 4 / (ms / reps) / 1e9);
     const char* role[6] = {"producerA", "mma", "updater", "producerB", "split", "drain"};
     printf("  total cycles per unit:");
