@@ -15,6 +15,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <atomic>
+#include <memory>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -218,12 +220,12 @@ struct oocnmf_ctx {
     // repeating the n-row H update on every rank, the ranks reduce-scatter it, update their
     // own n/N rows of H, and all-gather H (the same bytes as the all-reduce, 1/N of the update).
     // Needs whole 128-row tiles per rank (n a multiple of 128 N, as at config 3); else all-reduce.
-    // Dense RNMF does the same (OOCNMF_SHARD_H=0 keeps the all-reduce): W^T A is 8.4 MB at
-    // config 2, and at N = 8 the replicated H update is a visible share of a 0.7 ms iteration.
+    // Dense RNMF can do the same (OOCNMF_SHARD_H=1); W^T A is only 8.4 MB at config 2, and the
+    // all-reduce + replicated H update measured faster (649 vs 607 it/s at N = 4), so it is off.
     bool shard_h() const {
-        static const bool dense_ok = [] {
+        static const bool dense_ok = [] {  // measured slower at N = 4 (607 vs 649 it/s): off by default
             const char* e = std::getenv("OOCNMF_SHARD_H");
-            return !(e && e[0] == '0');
+            return e && e[0] == '1';
         }();
         return collective() && !cnmf && (kind == Kind::csr || (kind == Kind::dense && dense_ok)) &&
                np % (int64_t(kTile) * nranks) == 0;
@@ -295,12 +297,32 @@ size_t reap_marks(oocnmf_ctx* c) {
     }
     return n;
 }
-[[noreturn]] void abort_comm(oocnmf_ctx* c, const std::string& why) {
-    if (c->comm) ncclCommAbort(c->comm);  // NCCL kernels of the group exit; the stream drains
+// Abort the group after a collective failure. A live context (timeout, NCCL async error) gets
+// ncclCommAbort — on a helper thread, bounded, since an abort that itself blocks must not turn
+// the failure into a hang — and its streams are drained (bounded). After a device fault the
+// context is lost: nothing is waited for. Either way the context is poisoned.
+[[noreturn]] void abort_comm(oocnmf_ctx* c, const std::string& why, bool device_fault = false) {
+    ncclComm_t comm = c->comm;
     c->comm = nullptr;
     c->poisoned = true;
-    cudaStreamSynchronize(c->stream);
-    cudaStreamSynchronize(c->comm_stream);
+    auto bounded = [](auto&& done, int max_ms) {
+        for (int ms = 0; ms < max_ms && !done(); ms += 10) std::this_thread::sleep_for(std::chrono::milliseconds(10));
+    };
+    if (comm && !device_fault) {
+        auto flag = std::make_shared<std::atomic<bool>>(false);
+        std::thread t([comm, flag] {
+            ncclCommAbort(comm);
+            flag->store(true);
+        });
+        bounded([&] { return flag->load(); }, 10000);
+        if (flag->load())
+            t.join();
+        else
+            t.detach();
+        bounded([&] {
+            return cudaStreamQuery(c->stream) != cudaErrorNotReady && cudaStreamQuery(c->comm_stream) != cudaErrorNotReady;
+        }, 10000);
+    }
     cudaGetLastError();
     for (auto& m : c->marks) c->ev_pool.push_back(m.beg), c->ev_pool.push_back(m.end);
     c->marks.clear();
@@ -328,7 +350,8 @@ void wait_for(oocnmf_ctx* c, cudaStream_t s, cudaEvent_t e, const char* what) {
             // its NVLink-mapped buffers vanished under the NCCL kernels (the context is lost)
             if (!c->marks.empty())
                 abort_comm(c, std::string("device error (") + cudaGetErrorString(q) + ") while waiting for " + what +
-                                  " with collectives in flight (a peer rank failed?)");
+                                  " with collectives in flight (a peer rank failed?)",
+                           true);
             ck(q, what);
         }
         ncclResult_t ar = ncclSuccess;
@@ -632,9 +655,9 @@ int rs_chunks(oocnmf_ctx* c) {
 // Sharded CSR H update: overlap the H all-gather with the next iteration's A·Ht SpMM
 // (OOCNMF_AG_OVERLAP=0 keeps the single all-gather).
 bool ag_overlap(const oocnmf_ctx* c) {
-    static const bool on = [] {
+    static const bool on = [] {  // measured slower at N = 4 (221 vs 269 it/s): off by default
         const char* e = std::getenv("OOCNMF_AG_OVERLAP");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     return on && c->kind == Kind::csr && c->shard_h() && c->chA.C <= 1;
 }
