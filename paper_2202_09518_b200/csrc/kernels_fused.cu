@@ -113,7 +113,7 @@ __device__ unsigned long long g_fz_prof[24];
 #endif
 // Latency trace of the first kFzTraceBlocks blocks (profile builds): globaltimer ns at each
 // CTA's P1 publish, at each row's updater seeing the count / finishing, at each CTA's B producer
-// seeing the block's rows 0-63 ready. [4][kFzTraceBlocks][128 or G]
+// seeing the block's rows 0-63 ready, at each row's gather landing. [5][kFzTraceBlocks][128 or G]
 #ifdef OOC_FZ_PROFILE
 constexpr int kFzTraceBlocks = 64;
 __device__ unsigned long long* g_fz_trace = nullptr;
@@ -317,13 +317,22 @@ __global__ void __launch_bounds__(512, 1)
             }
             FZ_WAIT(10, mbar_wait(gbar, gph));
             gph ^= 1u;
-            float nu = 0.f;
-#pragma unroll 8
-            for (int c = c_lo; c < c_hi; ++c) nu += gbuf[c * KP + j];
-            if constexpr (P == 2) nu += __shfl_down_sync(0xffffffffu, nu, 16);  // part 0 + part 1
-            float de = 0.f;
+            if (lane == 0) FZ_TRACE(4, b, row);
+            // four interleaved partial sums (CTAs c = c_lo + 4 i + l), combined in a fixed order:
+            // deterministic, and a quarter of the dependent-add chain of one running sum
+            float s4[4] = {0.f, 0.f, 0.f, 0.f};
+            int c = c_lo;
+#pragma unroll 2
+            for (; c + 4 <= c_hi; c += 4)
 #pragma unroll
-            for (int q = 0; q < KP; ++q) de = fmaf(__shfl_sync(0xffffffffu, wold, q), hcol[q], de);
+                for (int l = 0; l < 4; ++l) s4[l] += gbuf[(c + l) * KP + j];
+            for (int l = 0; c < c_hi; ++c, ++l) s4[l] += gbuf[c * KP + j];
+            float nu = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+            if constexpr (P == 2) nu += __shfl_down_sync(0xffffffffu, nu, 16);  // part 0 + part 1
+            float d4[4] = {0.f, 0.f, 0.f, 0.f};  // W_old · HH^T column j, four interleaved chains
+#pragma unroll
+            for (int q = 0; q < KP; ++q) d4[q & 3] = fmaf(__shfl_sync(0xffffffffu, wold, q), hcol[q], d4[q & 3]);
+            const float de = (d4[0] + d4[1]) + (d4[2] + d4[3]);
             if (lane < KP) {
                 // t * nu / (de + eps) as (t * nu) * rcp_rn(de + eps), the factor-update
                 // kernel's formula (kernels_factor.cu)

@@ -46,6 +46,23 @@ def dist_results(tmp_path_factory):
     return world, json.load(open(out))
 
 
+@pytest.fixture(scope="module")
+def dist_results_optin(tmp_path_factory):
+    """The opt-in collective variants: dense sharded H update (OOCNMF_SHARD_H=1) and the sparse
+    H broadcasts consumed slice by slice by the next SpMM (OOCNMF_AG_OVERLAP=1)."""
+    n = nmf.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    out = tmp_path_factory.mktemp("dist_optin") / "r.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "dist_worker.py"),
+           str(out)]
+    env = dict(os.environ, OOCNMF_SHARD_H="1", OOCNMF_AG_OVERLAP="1")
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env)
+    return world, json.load(open(out))
+
+
 def _check(r, ref, tol=1e-4):
     assert r["iters"] == ref.trace_iters.tolist()
     rel = np.max(np.abs(np.array(r["trace"]) - ref.trace_err) / ref.trace_err)
@@ -125,6 +142,23 @@ def test_csr_sharded_h_update_matches_oracle(dist_results):
     # RNMF on CSR with n a multiple of 128 N: reduce-scatter W^T A, each rank updates its n/N
     # rows of H, all-gather H (instead of all-reduce + replicated update)
     world, res = dist_results
+    rp, ci, v, shape = oracle.port.gen_sparse(1100, 2048, 0.02, 8)
+    w0, h0 = oracle.port.init_factors(1100, 2048, 16, 0)
+    ref = oracle.port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
+    _check(res["csr_shard_k16"], ref)
+
+
+@pytest.mark.parametrize("name,k", [("dense_k16", 16), ("dense_k32", 32)])
+def test_dense_sharded_h_update_matches_oracle(dist_results_optin, name, k):
+    world, res = dist_results_optin
+    a = f32(oracle.port.uniform_dense(1100, 900, 42, 99))
+    w0, h0 = oracle.port.init_factors(1100, 900, k, 0)
+    ref = oracle.port.nmf_rnmf(a, k, f32(w0), f32(h0), world, 1, max_iters=30, interval=10)
+    _check(res[name], ref)
+
+
+def test_csr_h_broadcast_overlap_matches_oracle(dist_results_optin):
+    world, res = dist_results_optin
     rp, ci, v, shape = oracle.port.gen_sparse(1100, 2048, 0.02, 8)
     w0, h0 = oracle.port.init_factors(1100, 2048, 16, 0)
     ref = oracle.port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
