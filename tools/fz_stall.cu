@@ -121,13 +121,13 @@ int main(int argc, char** argv) {
     {
         const int TB = 64;
         unsigned long long* tr;
-        CK(cudaMalloc(&tr, size_t(5) * TB * 256 * 8));
-        CK(cudaMemset(tr, 0, size_t(5) * TB * 256 * 8));
+        CK(cudaMalloc(&tr, size_t(6) * TB * 256 * 8));
+        CK(cudaMemset(tr, 0, size_t(6) * TB * 256 * 8));
         fz_trace_set(tr);
         run();
         CK(cudaDeviceSynchronize());
         fz_trace_set(nullptr);
-        std::vector<unsigned long long> h(size_t(5) * TB * 256);
+        std::vector<unsigned long long> h(size_t(6) * TB * 256);
         CK(cudaMemcpy(h.data(), tr, h.size() * 8, cudaMemcpyDeviceToHost));
         auto at = [&](int kind, int b, int i) { return h[(size_t(kind) * TB + b) * 256 + i]; };
         double s_last = 0, s_cnt = 0, s_upd_med = 0, s_upd = 0, s_wr = 0, s_wr_max = 0, s_step = 0;
@@ -181,7 +181,7 @@ int main(int argc, char** argv) {
             if (cnt_n1[k]) printf(" n1=%d:%.2f(%d)", k, by_n1[k] / cnt_n1[k], int(cnt_n1[k]));
         printf("\n");
         {   // per row (first half): count seen - first count seen, gather latency, compute + publish
-            double d1 = 0, d2 = 0, d3 = 0;
+            double d1 = 0, d2 = 0, d3 = 0, d4 = 0;
             int nr = 0;
             for (int b = 8; b < TB && b < fp.NB; ++b) {
                 unsigned long long c0 = ~0ull;
@@ -190,11 +190,11 @@ int main(int argc, char** argv) {
                 for (int r = 0; r < 64; ++r)
                     if (at(1, b, r) && at(4, b, r) && at(2, b, r)) {
                         d1 += double(at(1, b, r) - c0), d2 += double(at(4, b, r) - at(1, b, r));
-                        d3 += double(at(2, b, r) - at(4, b, r)), ++nr;
+                        d3 += double(at(5, b, r) - at(4, b, r)), d4 += double(at(2, b, r) - at(5, b, r)), ++nr;
                     }
             }
-            printf("  per row (us): count seen after the first %.2f | gather %.2f | sum + update + publish %.2f\n",
-                   d1 / nr / 1e3, d2 / nr / 1e3, d3 / nr / 1e3);
+            printf("  per row (us): count seen after the first %.2f | gather %.2f | sum + update + stores %.2f | "
+                   "publish %.2f\n", d1 / nr / 1e3, d2 / nr / 1e3, d3 / nr / 1e3, d4 / nr / 1e3);
         }
         printf("  latency (us, mean over %d blocks): publish spread %.2f | last publish -> first updater sees count "
                "%.2f | -> all 64 rows updated %.2f (median row %.2f) | -> first B producer sees W %.2f, last %.2f\n",
