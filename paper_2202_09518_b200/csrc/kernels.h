@@ -30,14 +30,17 @@ cudaError_t launch_wta(int kp, const float* A, int64_t lda, const float* W, floa
 // Tensor-core passes, kernels_tc.cu: kp in {32, 64}, 3xTF32 split precision; the factor
 // operand is its [F | F_lo] concatenation (rows x 2kp).
 bool tc_supported(int kp);
+// ldb: row stride of the [F | F_lo] operand in floats (0 = 2 kp; wide factors pass the full
+// 2 kp_total with the group's column offset folded into the pointer)
 cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np,
-                          const float* Ht_cat, float* slots, const StreamK& sk, cudaStream_t s);
+                          const float* Ht_cat, float* slots, const StreamK& sk, cudaStream_t s, int64_t ldb = 0);
 // out_final (optional): the pass reduces its stream-K partials itself (ascending CTA order)
 // and writes the np x kp result there; flags: 4 u32 per slot, zero before the launch (the
 // kernel leaves them zero again), epoch: the nonzero "published" value.
 cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np,
                           const float* W_cat, float* slots, const StreamK& sk, cudaStream_t s,
-                          float* out_final = nullptr, unsigned* flags = nullptr, unsigned epoch = 0);
+                          float* out_final = nullptr, unsigned* flags = nullptr, unsigned epoch = 0,
+                          int64_t ldb = 0);
 
 // ---- one-pass dense MU W-half (kernels_fused.cu): P1 (A·Ht partials), the W update, and
 // P2 (W^T A with the new W) in one persistent tcgen05 kernel, A read from HBM once ----
@@ -133,6 +136,24 @@ cudaError_t launch_perturb_csr(const float* in, float* out, const int64_t* rp, c
                                cudaStream_t s);
 // cat (rows x 2kp) <- [F | F - tf32_trunc(F)] for F (rows x kp)
 cudaError_t launch_split_cat(const float* F, float* cat, int64_t rows, int kp, cudaStream_t s);
+
+// ---- k > 64 (kernels_wide.cu): kp a multiple of 64 up to kMaxWideKp; the contractions run
+// per 64-column group on the kp = 64 passes, factor operands group-interleaved [F_g | F_lo_g] ----
+constexpr int kMaxWideKp = 512;
+// gram / err slots: nslots (= factor_grid(rows / kTile), the count the caller reduces)
+cudaError_t launch_factor_update_wide(int kp, float* F, int64_t rows, const float* n_plain, const float* G, float eps,
+                                      bool update, double* gram_slots, int nslots, double* err_slots, int* flag,
+                                      float* cat_out, cudaStream_t s);
+cudaError_t launch_spmm_wide(int kp, const int64_t* rp, const int32_t* ci, const float* v, int64_t rows, const float* B,
+                             float* out, cudaStream_t s);
+cudaError_t launch_residual_dense_wide(int kp, const float* A, int64_t lda, int64_t rows, int64_t cols, const float* W,
+                                       const float* Ht, double* out_slots, int nslots, cudaStream_t s, const int* pred);
+cudaError_t launch_cross_csr_wide(int kp, const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
+                                  const float* W, const float* Ht, double* out_slots, int nslots, cudaStream_t s,
+                                  const int* pred);
+// a kp = 64 pass's stream-K partials -> a 64-column group of a wider output (row stride ldo)
+cudaError_t launch_streamk_reduce_ld(const float* slots, const StreamK& sk, float* out, int64_t ldo, bool accumulate,
+                                     cudaStream_t s);
 
 // ---- CSR kernels (kernels_sparse.cu) ----
 // out (rows x kp) = CSR(rp, ci, v) · B (B rows indexed by column, kp wide).

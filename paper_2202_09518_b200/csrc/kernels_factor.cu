@@ -419,6 +419,11 @@ cudaError_t launch_factor_update(int kp, float* F, int64_t rows, const float* n_
                                  int* flag, float* cat_out, cudaStream_t s) {
     const int64_t tiles = rows / kTile;
     const int grid = factor_grid(tiles);
+    if (kp > 64) {  // wide factors: plain numerators only (the solver reduces the group passes)
+        if (update && !n_plain) return cudaErrorInvalidValue;
+        return launch_factor_update_wide(kp, F, rows, n_plain, G, eps, update, gram_slots, grid, err_slots, flag,
+                                         cat_out, s);
+    }
     StreamK skv = sk ? *sk : StreamK{};
 #define OOC_FU(K)                                                                              \
     case K: {                                                                                  \

@@ -588,6 +588,10 @@ void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahea
     fp.q0.assign(G + 1, 0);
     fp.t0.assign(G + 1, 0);
     for (int c = 0; c <= G; ++c) fp.t0[c] = int(int64_t(c) * fp.NT / G);
+    const char* pm = std::getenv("OOCNMF_FUSED_PLAN");  // developer knob: 1 = even P1 ranges
+    if (pm && pm[0] == '1') {
+        for (int c = 0; c <= G; ++c) fp.q0[c] = int(int64_t(c) * fp.NQ / G);
+    } else {
     int prev = 0;
     for (int c = 0; c <= G; ++c) {
         const int64_t share = (int64_t(c) * U + G / 2) / G;
@@ -596,6 +600,7 @@ void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahea
         if (c == G) q = fp.NQ;
         fp.q0[c] = q;
         prev = q;
+    }
     }
     fp.act.clear();
     for (int c = 0; c < G; ++c)

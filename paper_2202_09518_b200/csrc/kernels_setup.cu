@@ -160,13 +160,17 @@ __global__ void k_check_finite(const float* __restrict__ x, int64_t n, int* flag
     if (bad) atomicOr(flag, 1);
 }
 
+// [F_g | F_lo_g] per group of gw = min(kp, 64) columns (one group for kp <= 64: [F | F_lo])
 __global__ void k_split_cat(const float* __restrict__ F, float* __restrict__ cat, int64_t rows, int kp) {
     const int64_t n = rows * kp;
+    const int gw = kp < 64 ? kp : 64;
     for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < n; q += int64_t(gridDim.x) * blockDim.x) {
-        const int64_t r = q / kp, j = q % kp;
+        const int64_t r = q / kp;
+        const int j = int(q % kp);
         const float v = F[q];
-        cat[r * 2 * kp + j] = v;
-        cat[r * 2 * kp + kp + j] = tf32_lo(v);
+        float* c = cat + r * 2 * kp + 2 * gw * (j / gw) + j % gw;
+        c[0] = v;
+        c[gw] = tf32_lo(v);
     }
 }
 
@@ -268,6 +272,7 @@ cudaError_t launch_reduce_f64(const double* slots, int64_t n, double* out, cudaS
 cudaError_t launch_residual_dense(int kp, const float* A, int64_t lda, int64_t rows, int64_t cols,
                                   const float* W, const float* Ht, double* out_slots, cudaStream_t s,
                                   const int* pred) {
+    if (kp > 64) return launch_residual_dense_wide(kp, A, lda, rows, cols, W, Ht, out_slots, kRedGrid, s, pred);
     switch (kp) {
         case 8: k_residual_dense<8><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots, pred); break;
         case 16: k_residual_dense<16><<<kRedGrid, 256, 0, s>>>(A, lda, rows, cols, W, Ht, out_slots, pred); break;

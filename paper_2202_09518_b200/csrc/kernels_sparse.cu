@@ -432,6 +432,7 @@ unsigned grid_for(int64_t work) {
 
 cudaError_t launch_spmm(int kp, const int64_t* rp, const int32_t* ci, const float* v, int64_t rows,
                         const float* B, float* out, cudaStream_t s) {
+    if (kp > 64) return launch_spmm_wide(kp, rp, ci, v, rows, B, out, s);
     static const int mode = [] {  // OOCNMF_SPMM=1: the one-float-per-lane kernel (developer knob)
         const char* e = std::getenv("OOCNMF_SPMM");
         return e ? std::atoi(e) : 4;
@@ -501,6 +502,7 @@ cudaError_t launch_residual_csr(int kp, const int64_t* rp, const int32_t* ci, co
                                 double* out_slots, cudaStream_t s, const int* pred) {
     (void)cols;
     const unsigned grid = 4 * 148;
+    if (kp > 64) return launch_cross_csr_wide(kp, rp, ci, v, rows, W, Ht, out_slots, int(grid), s, pred);
     switch (kp) {
         case 8: k_cross_csr<8><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots, pred); break;
         case 16: k_cross_csr<16><<<grid, 256, 0, s>>>(rp, ci, v, rows, W, Ht, out_slots, pred); break;

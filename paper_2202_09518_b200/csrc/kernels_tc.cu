@@ -528,11 +528,11 @@ bool tc_supported(int kp) { return (kp == 16 || kp == 32 || kp == 64) && encode_
 
 // Pass 1 on the tensor cores: A (mp x np, ld lda) K-major, Ht_cat (np x 2kp) MN-major.
 cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* Ht_cat,
-                          float* slots, const StreamK& sk, cudaStream_t s) {
+                          float* slots, const StreamK& sk, cudaStream_t s, int64_t ldb) {
     CUtensorMap ma, mb;
     cudaError_t e;
     if ((e = make_map(&ma, A, mp, np, lda, 128, kTcStep / 32, false)) != cudaSuccess) return e;
-    if ((e = make_map(&mb, Ht_cat, np, 2 * kp, 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, Ht_cat, np, 2 * kp, ldb ? ldb : 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
     return kp == 16   ? launch_tc<16, 1>(ma, mb, slots, sk, s)
            : kp == 32 ? launch_tc<32, 1>(ma, mb, slots, sk, s)
                       : launch_tc<64, 1>(ma, mb, slots, sk, s);
@@ -541,11 +541,11 @@ cudaError_t launch_aht_tc(int kp, const float* A, int64_t lda, int64_t mp, int64
 // Pass 2 on the tensor cores: A MN-major (4 column atoms per 128-column tile), W_cat (mp x 2kp).
 cudaError_t launch_wta_tc(int kp, const float* A, int64_t lda, int64_t mp, int64_t np, const float* W_cat,
                           float* slots, const StreamK& sk, cudaStream_t s, float* out_final,
-                          unsigned* flags, unsigned epoch) {
+                          unsigned* flags, unsigned epoch, int64_t ldb) {
     CUtensorMap ma, mb;
     cudaError_t e;
     if ((e = make_map(&ma, A, mp, np, lda, kTcStep, 4, true)) != cudaSuccess) return e;
-    if ((e = make_map(&mb, W_cat, mp, 2 * kp, 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
+    if ((e = make_map(&mb, W_cat, mp, 2 * kp, ldb ? ldb : 2 * kp, kTcStep, 2 * kp / 32, true)) != cudaSuccess) return e;
     return kp == 16   ? launch_tc<16, 2>(ma, mb, slots, sk, s, out_final, flags, epoch)
            : kp == 32 ? launch_tc<32, 2>(ma, mb, slots, sk, s, out_final, flags, epoch)
                       : launch_tc<64, 2>(ma, mb, slots, sk, s, out_final, flags, epoch);

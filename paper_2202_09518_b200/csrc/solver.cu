@@ -73,8 +73,12 @@ int pad_k(uint64_t k) {
     if (k <= 16) return 16;
     if (k <= 32) return 32;
     if (k <= 64) return 64;
-    fail(OOCNMF_ERR_SHAPE, "k=" + std::to_string(k) + " exceeds the supported maximum of 64");
+    // wide factors (kernels_wide.cu): 64-column groups on the kp = 64 passes
+    if (k <= uint64_t(kMaxWideKp)) return int((k + 63) / 64 * 64);
+    fail(OOCNMF_ERR_SHAPE, "k=" + std::to_string(k) + " exceeds the supported maximum of " + std::to_string(kMaxWideKp));
 }
+// tensor-core passes at this kp (wide factors run them per 64-column group)
+bool tc_for(int kp) { return tc_supported(kp > 64 ? 64 : std::max(kp, 16)); }
 
 struct DevBuf {
     void* p = nullptr;
@@ -385,7 +389,7 @@ void plan_chunks(oocnmf_ctx* c, oocnmf_ctx::Chunks& ch, const int64_t* rp, const
     ch.C = 1;
     ch.seg.release();
     const int64_t b_bytes = cols * kp * 4;
-    if (target <= 0 || rows <= 0 || b_bytes <= target) return;
+    if (target <= 0 || rows <= 0 || b_bytes <= target || kp > 64) return;  // (no wide chunk kernel)
     const int C = int((b_bytes + target - 1) / target);
     const double nnz_row = double(c->nnz) / double(rows);
     const double one_pass = nnz_row * kp * 4;
@@ -494,7 +498,7 @@ void plan_dense(oocnmf_ctx* c) {
     c->slots2.alloc(size_t(c->sk2.G * c->sk2.smax) * kTile * c->kp * 4, "slots2");
     c->fix_flags.alloc(size_t(c->sk2.G * c->sk2.smax) * 4 * 4, "fix flags");
     ck(cudaMemsetAsync(c->fix_flags.p, 0, c->fix_flags.bytes, c->stream), "memset");
-    if (c->cnmf) {
+    if (c->cnmf || c->kp > 64) {
         c->N1.alloc(size_t(c->mp) * c->kp * 4, "AHt");
         ck(cudaMemsetAsync(c->N1.p, 0, c->N1.bytes, c->stream), "memset");
     }
@@ -560,13 +564,40 @@ float* wlo(oocnmf_ctx* c) { return c->use_tc && c->kind != Kind::csr ? c->W_cat.
 float* htlo(oocnmf_ctx* c) { return c->use_tc && c->kind != Kind::csr ? c->Ht_cat.as<float>() : nullptr; }
 
 // Pass 1 over an A slab (rows_p x np, rows_p a multiple of 128): slots <- A·Ht partials.
-cudaError_t pass1(oocnmf_ctx* c, const float* A, int64_t rows_p, float* slots, const StreamK& sk, cudaStream_t s) {
+// Wide factors (kp > 64): each pass runs once per 64-column group of the [F_g | F_lo_g]
+// group-interleaved operand (kp = 64 tensor-core passes), and its stream-K partials are
+// reduced into the group's columns of a plain rows x kp output right away.
+bool wide(const oocnmf_ctx* c) { return c->kp > 64; }
+cudaError_t pass1(oocnmf_ctx* c, const float* A, int64_t rows_p, float* slots, const StreamK& sk, cudaStream_t s,
+                  float* out = nullptr) {
+    if (wide(c)) {
+        if (!out) return cudaErrorInvalidValue;
+        for (int g = 0; g < c->kp / 64; ++g) {
+            cudaError_t e = launch_aht_tc(64, A, c->np, rows_p, c->np, c->Ht_cat.as<float>() + 128 * g, slots, sk, s,
+                                          2 * c->kp);
+            if (e == cudaSuccess) e = launch_streamk_reduce_ld(slots, sk, out + 64 * g, c->kp, false, s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     if (c->use_tc) return launch_aht_tc(c->kp, A, c->np, rows_p, c->np, c->Ht_cat.as<float>(), slots, sk, s);
     return launch_aht(c->kp, A, c->np, c->Ht.as<float>(), slots, sk, s);
 }
-// Pass 2 over an A slab with its W rows (W rows x kp, Wcat rows x 2kp): slots <- A^T·W partials.
+// Pass 2 over an A slab with its W rows (W rows x kp, Wcat rows x 2kp): slots <- A^T·W partials
+// (out_final set: reduced into it; wide factors always reduce into out_final, adding to it when
+// accumulate is set).
 cudaError_t pass2(oocnmf_ctx* c, const float* A, int64_t rows_p, const float* W, const float* Wcat, float* slots,
-                  const StreamK& sk, cudaStream_t s, float* out_final = nullptr) {
+                  const StreamK& sk, cudaStream_t s, float* out_final = nullptr, bool accumulate = false) {
+    if (wide(c)) {
+        if (!out_final) return cudaErrorInvalidValue;
+        for (int g = 0; g < c->kp / 64; ++g) {
+            cudaError_t e = launch_wta_tc(64, A, c->np, rows_p, c->np, Wcat + 128 * g, slots, sk, s, nullptr, nullptr,
+                                          0u, 2 * c->kp);
+            if (e == cudaSuccess) e = launch_streamk_reduce_ld(slots, sk, out_final + 64 * g, c->kp, accumulate, s);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
+    }
     if (c->use_tc)
         return launch_wta_tc(c->kp, A, c->np, rows_p, c->np, Wcat, slots, sk, s, out_final,
                              out_final ? c->fix_flags.as<unsigned>() : nullptr, 1u);
@@ -622,7 +653,7 @@ void record(oocnmf_ctx* c, cudaEvent_t e, cudaStream_t s) {
 // one-pass: not under CNMF (A·Ht is all-reduced first) nor with column-chunked SpMM passes.
 // OOCNMF_FUSE_W=0 selects the separate SpMM + factor-update kernels (bit-identical results).
 bool fuse_w_update(const oocnmf_ctx* c) {
-    if (c->kind != Kind::csr || c->cnmf || c->chA.C > 1) return false;
+    if (c->kind != Kind::csr || c->cnmf || c->chA.C > 1 || c->kp > 64) return false;
     const char* e = std::getenv("OOCNMF_FUSE_W");
     return !(e && *e == '0');
 }
@@ -631,7 +662,7 @@ bool fuse_w_update(const oocnmf_ctx* c) {
 // trace-form cross term <W^T A, H> needs the numerator the fused kernel never stores.
 // OOCNMF_FUSE_H=0 keeps the separate kernels.
 bool fuse_h_update(const oocnmf_ctx* c) {
-    if (c->kind != Kind::csr || c->cnmf || c->collective() || c->chT.C > 1) return false;
+    if (c->kind != Kind::csr || c->cnmf || c->collective() || c->chT.C > 1 || c->kp > 64) return false;
     const char* e = std::getenv("OOCNMF_FUSE_H");
     return !(e && *e == '0');
 }
@@ -761,12 +792,14 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         rec(eWta);
         rec(eReduced);
     } else if (c->kind == Kind::dense) {
-        count(c, pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
+        count(c, pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s, c->N1.as<float>()), "aht");
         rec(eAht);
-        if (c->cnmf) {
-            // the column slab's A·H^T partials -> one m x kp buffer, summed over the ranks
-            count(c, launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, c->N1.as<float>(), false, s),
-                  "reduce AHt");
+        if (c->cnmf || wide(c)) {
+            // the column slab's A·H^T partials -> one m x kp buffer, summed over the ranks (wide
+            // factors: already reduced there by the group passes)
+            if (!wide(c))
+                count(c, launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, c->N1.as<float>(), false, s),
+                      "reduce AHt");
             allreduce_aht(c);
             count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, c->N1.as<float>(), nullptr, nullptr,
                                           c->HHt.as<float>(), eps, true, c->gram_w.as<double>(), nullptr,
@@ -857,13 +890,18 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
             ck(cudaStreamWaitEvent(s, c->ev_copied[si], 0), "wait copied");
             float* Wb = c->W.as<float>() + b0 * kp;
             float* Wlob = c->use_tc ? c->W_cat.as<float>() + b0 * 2 * kp : nullptr;
-            count(c, pass1(c, st, brp, c->slots1.as<float>(), s1, s), "aht");
-            count(c, launch_factor_update(kp, Wb, brp, nullptr, c->slots1.as<float>(), &s1, c->HHt.as<float>(),
-                                          eps, true, c->gram_w.as<double>() + b * gwb * kp * kp, nullptr,
+            count(c, pass1(c, st, brp, c->slots1.as<float>(), s1, s, c->N1.as<float>()), "aht");
+            count(c, launch_factor_update(kp, Wb, brp, wide(c) ? c->N1.as<float>() : nullptr,
+                                          wide(c) ? nullptr : c->slots1.as<float>(), &s1, c->HHt.as<float>(), eps,
+                                          true, c->gram_w.as<double>() + b * gwb * kp * kp, nullptr,
                                           c->flag.as<int>(), Wlob, s),
                   "W update");
-            count(c, pass2(c, st, brp, Wb, Wlob, c->slots2.as<float>(), s2, s), "wta");
-            count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), s2, c->wta(), b > 0, s), "reduce WtA");
+            if (wide(c)) {
+                count(c, pass2(c, st, brp, Wb, Wlob, c->slots2.as<float>(), s2, s, c->wta(), b > 0), "wta");
+            } else {
+                count(c, pass2(c, st, brp, Wb, Wlob, c->slots2.as<float>(), s2, s), "wta");
+                count(c, launch_streamk_reduce(kp, c->slots2.as<float>(), s2, c->wta(), b > 0, s), "reduce WtA");
+            }
             ck(cudaEventRecord(c->ev_free[si], s), "event");
         }
         count(c, launch_reduce_slots(c->gram_w.as<double>(), nb * gwb, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s), "reduce WtW");
@@ -1335,7 +1373,8 @@ void set_problem_impl(oocnmf_ctx* c, uint64_t m, uint64_t n, uint64_t k, uint64_
     // FFMA passes remain selectable (OOCNMF_FORCE_FFMA=1) as an independent cross-check.
     const char* force = std::getenv("OOCNMF_FORCE_FFMA");
     int kp = pad_k(k);
-    c->use_tc = !(force && force[0] == '1') && tc_supported(std::max(kp, 16));
+    c->use_tc = (kp > 64 || !(force && force[0] == '1')) && tc_for(kp);
+    if (kp > 64 && !c->use_tc) fail(OOCNMF_ERR_DEVICE, "k > 64 needs the tensor-core passes");
     if (c->use_tc) kp = std::max(kp, 16);
     c->kp = kp;
     c->mp = round_up(int64_t(rows), kTile);
@@ -1351,7 +1390,8 @@ void set_rank_impl(oocnmf_ctx* c, uint64_t k) {
     if (k < 1) fail(OOCNMF_ERR_SHAPE, "k must be >= 1");
     const char* force = std::getenv("OOCNMF_FORCE_FFMA");
     int kp = pad_k(k);
-    c->use_tc = !(force && force[0] == '1') && tc_supported(std::max(kp, 16));
+    c->use_tc = (kp > 64 || !(force && force[0] == '1')) && tc_for(kp);
+    if (kp > 64 && !c->use_tc) fail(OOCNMF_ERR_DEVICE, "k > 64 needs the tensor-core passes");
     if (c->use_tc) kp = std::max(kp, 16);
     c->k = k;
     c->kp = kp;
@@ -2073,6 +2113,7 @@ int oocnmf_attach_host_dense_f32(oocnmf_ctx* c, const float* a, uint64_t lda, ui
         const int64_t s2 = std::max(c->sk2b[0].G * c->sk2b[0].smax, c->sk2b[1].G * c->sk2b[1].smax);
         c->slots1.alloc(size_t(s1) * kTile * c->kp * 4, "slots1");
         c->slots2.alloc(size_t(s2) * kTile * c->kp * 4, "slots2");
+        if (c->kp > 64) c->N1.alloc(size_t(br) * c->kp * 4, "AHt (batch)");  // wide: plain numerators
         c->gram_w.alloc(size_t(nb) * factor_grid(br / kTile) * c->kp * c->kp * 8, "gram_w");
         ck(cudaMemsetAsync(c->gram_w.p, 0, c->gram_w.bytes, c->stream), "memset");
         ck(cudaStreamSynchronize(c->stream), "sync");
@@ -2215,10 +2256,18 @@ int oocnmf_products_f64(oocnmf_ctx* c, double* aht, double* wta, double* hht, do
                 ck(launch_split_cat(c->Ht.as<float>(), c->Ht_cat.as<float>(), c->np, kp, s), "split");
                 ck(launch_split_cat(c->W.as<float>(), c->W_cat.as<float>(), c->mp, kp, s), "split");
             }
-            ck(pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s), "aht");
-            ck(launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, t1.as<float>(), false, s), "reduce");
-            ck(pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s), "wta");
-            ck(launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce");
+            ck(pass1(c, c->A.as<float>(), c->mp, c->slots1.as<float>(), c->sk1, s, t1.as<float>()), "aht");
+            if (!wide(c))
+                ck(launch_streamk_reduce(kp, c->slots1.as<float>(), c->sk1, t1.as<float>(), false, s), "reduce");
+            if (wide(c)) {
+                ck(pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s,
+                         c->wta()),
+                   "wta");
+            } else {
+                ck(pass2(c, c->A.as<float>(), c->mp, c->W.as<float>(), wlo(c), c->slots2.as<float>(), c->sk2, s),
+                   "wta");
+                ck(launch_streamk_reduce(kp, c->slots2.as<float>(), c->sk2, c->wta(), false, s), "reduce");
+            }
         } else {
             ensure_chunks(c);
             spmm(c, false, c->Ht.as<float>(), t1.as<float>(), s);

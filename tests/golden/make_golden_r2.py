@@ -12,7 +12,8 @@ parity tests compare arithmetic precision only. The fixtures pin the cases round
   (src/synth.cpp:60-86), k = 32, 20 iterations;
 * long-K dense shapes (1024 x 65536 and 65536 x 1024, k = 32, 10 iterations): config 2's
   65536-deep passes;
-* config 2 itself (65536 x 65536, k = 32) for 2 iterations with an error check after each.
+* config 2 itself (65536 x 65536, k = 32) for 2 iterations with an error check after each;
+* k > 64 (96, 200 dense; 80 CSR): the wide-factor path.
 
 Large factors are stored as strided samples (rows of W, columns of H) plus their full
 Frobenius norms and sums; the tests compare the same samples (relative Frobenius on the sample).
@@ -96,7 +97,18 @@ def config2():
     print(f"config2_65536_k32_2it: {r.trace_err.tolist()} ({time.time() - t:.1f} s)", flush=True)
 
 
-CASES = {"csr": csr_k32_k48, "config3": csr_config3_scaled, "longk": long_k, "config2": config2}
+def wide():
+    # k > 64 (kp 128 / 256: the paper's scaling study runs k = 128 and 256)
+    a, _, _ = ref.gen_lowrank(1024, 768, 12, 0.01, 3)
+    run_case("wide_lowrank_1024x768_k96", f32(a), a.shape, 96, 30, 10)
+    a = f32(ref.uniform_dense(512, 640, 42, 99))
+    run_case("wide_uniform_512x640_k200", a, a.shape, 200, 20, 10)
+    g = np.load(os.path.join(HERE, "csr_3000x2500_d001_k16.npz"))
+    m, n = g["shape"].tolist()
+    run_case("wide_csr_3000x2500_d001_k80", (g["rp"], g["ci"], g["v"].astype(np.float64), (m, n)), (m, n), 80, 20, 10)
+
+
+CASES = {"csr": csr_k32_k48, "config3": csr_config3_scaled, "longk": long_k, "config2": config2, "wide": wide}
 
 if __name__ == "__main__":
     for name in sys.argv[1:] or list(CASES):

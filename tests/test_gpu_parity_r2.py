@@ -179,3 +179,70 @@ def test_fused_pass_is_deterministic(gpu):
     r1, r2 = nmf.nmf_serial(a, cfg), nmf.nmf_serial(a, cfg)
     assert np.array_equal(r1.w, r2.w) and np.array_equal(r1.h, r2.h)
     assert [e for _, e in r1.error_trace] == [e for _, e in r2.error_trace]
+
+
+# ------------------------------------------------------------------ k > 64 (wide factors)
+def _wide_input(name):
+    if name == "wide_lowrank_1024x768_k96":
+        if not oracle.ref.available:
+            pytest.skip("low-rank input regeneration needs oracle/_ref")
+        return oracle.ref.gen_lowrank(1024, 768, 12, 0.01, 3)[0].astype(np.float32)
+    return port.uniform_dense(512, 640, 42, 99).astype(np.float32)
+
+
+@pytest.mark.parametrize("name", ["wide_lowrank_1024x768_k96", "wide_uniform_512x640_k200"])
+@pytest.mark.parametrize("mode", ["in_core", "out_of_core", "cnmf"])
+def test_wide_k_matches_reference(gpu, name, mode):
+    """k > 64 (kp 128 / 256): the kp = 64 tensor-core passes per 64-column group, the wide factor /
+    Gram / residual kernels (kernels_wide.cu), in core, streamed from host memory in row batches,
+    and column-partitioned, against the compiled reference."""
+    g = golden(name)
+    a = _wide_input(name)
+    m, n = a.shape
+    cfg = cfg_from(g, m, n)
+    if mode == "in_core":
+        res = nmf.nmf_serial(a, cfg)
+        trace, w, h = res.error_trace, res.w, res.h
+    elif mode == "out_of_core":
+        with nmf.Context(gpu) as ctx:
+            ctx.set_problem(m, n, cfg.k)
+            ctx.attach_host(np.ascontiguousarray(a), 256)
+            ctx.set_factors(cfg.init_w, cfg.init_h)
+            trace, _ = ctx.solve(cfg)
+            w, h = ctx.get_factors()
+    else:
+        comm = nmf.DistComm(0, 1, gpu)
+        try:
+            res = nmf.nmf_distributed(a, cfg, nmf.make_plan(m, n, cfg.k, 1, 1, nmf.Strategy.cnmf), comm)
+        finally:
+            comm.close()
+        trace, w, h = res.error_trace, res.w, res.h
+    check_trace(trace, g)
+    check_factors(w, h, g)
+
+
+def test_wide_k_csr_matches_reference(gpu):
+    base = golden("csr_3000x2500_d001_k16")
+    g = golden("wide_csr_3000x2500_d001_k80")
+    m, n = base["shape"].tolist()
+    a = nmf.CsrMatrix(m, n, base["rp"], base["ci"], base["v"])
+    res = nmf.nmf_serial(a, cfg_from(g, m, n))
+    check_trace(res.error_trace, g)
+    check_factors(res.w, res.h, g)
+
+
+def test_wide_k_products_match_f64(gpu):
+    m, n, k = 300, 520, 130  # kp 192: three groups, ragged k
+    rng = np.random.default_rng(7)
+    a = rng.random((m, n)).astype(np.float32)
+    w = f32(rng.random((m, k)))
+    h = f32(rng.random((k, n)))
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(m, n, k)
+        ctx.load_dense(a)
+        ctx.set_factors(w, h)
+        aht, wta, hht, wtw = ctx.products()
+    a64 = a.astype(np.float64)
+    assert rel_fro(aht, a64 @ h.T) < 3e-6 and rel_fro(wta, w.T @ a64) < 3e-6
+    assert rel_fro(hht, h @ h.T) < 3e-6 and rel_fro(wtw, w.T @ w) < 3e-6
+    assert np.array_equal(hht, hht.T) and np.array_equal(wtw, wtw.T)
