@@ -3,7 +3,7 @@
 // built with -DOOC_FZ_PROFILE. build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DOOC_FZ_PROFILE -I include \
 //     -I paper_2202_09518_b200/csrc tools/fz_stall.cu paper_2202_09518_b200/csrc/kernels_fused.cu \
-//     paper_2202_09518_b200/csrc/kernels_tc.cu paper_2202_09518_b200/csrc/kernels_factor.cu -lcuda -o tools/fz_stall
+//     paper_2202_09518_b200/csrc/kernels_tc.cu paper_2202_09518_b200/csrc/kernels_factor.cu paper_2202_09518_b200/csrc/kernels_wide.cu paper_2202_09518_b200/csrc/kernels_setup.cu -lcuda -o tools/fz_stall
 // argv: kp mp np lookahead reps pol drain_units p2_first
 #include <cstdio>
 #include <cstdlib>

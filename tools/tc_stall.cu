@@ -4,7 +4,7 @@
 // product. build:
 //   nvcc -gencode arch=compute_100a,code=sm_100a -std=c++17 -O3 -DOOC_TC_PROFILE -I include \
 //     -I paper_2202_09518_b200/csrc tools/tc_stall.cu paper_2202_09518_b200/csrc/kernels_tc.cu \
-//     paper_2202_09518_b200/csrc/kernels_dense.cu paper_2202_09518_b200/csrc/kernels_factor.cu -lcuda -o tools/tc_stall
+//     paper_2202_09518_b200/csrc/kernels_dense.cu paper_2202_09518_b200/csrc/kernels_factor.cu paper_2202_09518_b200/csrc/kernels_wide.cu paper_2202_09518_b200/csrc/kernels_setup.cu -lcuda -o tools/tc_stall
 #include <cstdio>
 #include <cstdlib>
 
