@@ -336,6 +336,11 @@ size_t reap_marks(oocnmf_ctx* c) {
 void need_comm(const oocnmf_ctx* c) {
     if (c->poisoned) fail(OOCNMF_ERR_COMM, "communicator was aborted after an earlier collective failure");
 }
+// A failing NCCL call on the group (a dead peer detected at enqueue, an async error surfacing
+// at group end): abort and poison like a timeout.
+void ncc(oocnmf_ctx* c, ncclResult_t r, const char* what) {
+    if (r != ncclSuccess && r != ncclInProgress) abort_comm(c, std::string(what) + ": " + ncclGetErrorString(r));
+}
 // Host wait for an event (or the whole stream when e is null). With a communicator it polls:
 // no collective completing for comm_timeout seconds, or an NCCL async error, aborts the group
 // instead of hanging on a dead peer.
@@ -550,7 +555,7 @@ void compute_norm(oocnmf_ctx* c) {
 reduced:
     if (c->collective()) {
         coll_begin(c, c->stream);
-        nck(ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
+        ncc(c, ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
         coll_end(c, c->stream, kTagErr, 8);  // ||A||^2 (src/nmf_distributed.cpp:232, error_check)
     }
     ck(cudaMemcpyAsync(&c->norm_a2, out, 8, cudaMemcpyDeviceToHost, c->stream), "D2H norm");
@@ -615,11 +620,11 @@ void finish_hht(oocnmf_ctx* c, int64_t rows, bool partial) {
     if (partial) {
         coll_begin(c, c->stream);
         nck(ncclGroupStart(), "ncclGroupStart");
-        nck(ncclAllReduce(c->HHt.p, c->HHt.p, size_t(kp) * kp, ncclFloat, ncclSum, c->comm, c->stream),
+        ncc(c, ncclAllReduce(c->HHt.p, c->HHt.p, size_t(kp) * kp, ncclFloat, ncclSum, c->comm, c->stream),
             "allreduce HHt");
-        nck(ncclAllReduce(c->HHt64.p, c->HHt64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, c->stream),
+        ncc(c, ncclAllReduce(c->HHt64.p, c->HHt64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, c->stream),
             "allreduce HHt64");
-        nck(ncclGroupEnd(), "ncclGroupEnd");
+        ncc(c, ncclGroupEnd(), "ncclGroupEnd");
         coll_end(c, c->stream, kTagW, size_t(kp) * kp * 12);  // CNMF HH^T (nmf_distributed.cpp:116)
     }
 }
@@ -638,7 +643,7 @@ void gram_h(oocnmf_ctx* c) {
 void allreduce_aht(oocnmf_ctx* c) {
     if (c->cnmf && c->collective()) {
         coll_begin(c, c->stream);
-        nck(ncclAllReduce(c->N1.p, c->N1.p, size_t(c->mp) * c->kp, ncclFloat, ncclSum, c->comm, c->stream),
+        ncc(c, ncclAllReduce(c->N1.p, c->N1.p, size_t(c->mp) * c->kp, ncclFloat, ncclSum, c->comm, c->stream),
             "allreduce AHt");
         coll_end(c, c->stream, kTagW, size_t(c->mp) * c->kp * 4);  // nmf_distributed.cpp:124
     }
@@ -745,7 +750,7 @@ void spmm_wta_reduce_scatter(oocnmf_ctx* c, cudaStream_t s) {
         ck(cudaEventRecord(c->ev_rs[ch], s), "event");
         ck(cudaStreamWaitEvent(c->comm_stream, c->ev_rs[ch], 0), "wait");
         coll_begin(c, c->comm_stream);
-        nck(ncclReduceScatter(base, c->wta() + size_t(h0 + r0) * kp, size_t(len) * kp, ncclFloat, ncclSum, c->comm,
+        ncc(c, ncclReduceScatter(base, c->wta() + size_t(h0 + r0) * kp, size_t(len) * kp, ncclFloat, ncclSum, c->comm,
                               c->comm_stream),
             "reduce-scatter WtA (chunk)");
         coll_end(c, c->comm_stream, kTagH, size_t(N) * len * kp * 4);
@@ -925,12 +930,12 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         coll_begin(c, s);
         nck(ncclGroupStart(), "ncclGroupStart");
         if (!c->rs_done)
-            nck(ncclReduceScatter(wta, wta + size_t(c->rank) * slice, slice, ncclFloat, ncclSum, c->comm, s),
+            ncc(c, ncclReduceScatter(wta, wta + size_t(c->rank) * slice, slice, ncclFloat, ncclSum, c->comm, s),
                 "reduce-scatter WtA");
-        nck(ncclAllReduce(c->wtw(), c->wtw(), size_t(kp) * kp, ncclFloat, ncclSum, c->comm, s), "allreduce WtW");
-        nck(ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
+        ncc(c, ncclAllReduce(c->wtw(), c->wtw(), size_t(kp) * kp, ncclFloat, ncclSum, c->comm, s), "allreduce WtW");
+        ncc(c, ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
             "allreduce WtW64");
-        nck(ncclGroupEnd(), "ncclGroupEnd");
+        ncc(c, ncclGroupEnd(), "ncclGroupEnd");
         coll_end(c, s, kTagH, (c->rs_done ? 0 : size_t(c->nranks) * slice * 4) + size_t(kp) * kp * 12);
         c->rs_done = false;
     } else if (c->collective() && !c->cnmf) {
@@ -939,11 +944,11 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         // replicated W are already complete on every rank.)
         coll_begin(c, s);
         nck(ncclGroupStart(), "ncclGroupStart");
-        nck(ncclAllReduce(c->packed.p, c->packed.p, size_t(c->packed_count()), ncclFloat, ncclSum, c->comm, s),
+        ncc(c, ncclAllReduce(c->packed.p, c->packed.p, size_t(c->packed_count()), ncclFloat, ncclSum, c->comm, s),
             "allreduce [WtA|WtW]");
-        nck(ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
+        ncc(c, ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
             "allreduce WtW64");
-        nck(ncclGroupEnd(), "ncclGroupEnd");
+        ncc(c, ncclGroupEnd(), "ncclGroupEnd");
         coll_end(c, s, kTagH, size_t(c->packed_count()) * 4 + size_t(kp) * kp * 8);  // nmf_distributed.cpp:171,178
     }
     if (timed) record(c, ev[eComm], s);
@@ -974,14 +979,14 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         coll_begin(c, c->comm_stream);
         for (int r = 0; r < c->nranks; ++r) {
             float* sl = c->Ht.as<float>() + size_t(r) * hr * kp;
-            nck(ncclBroadcast(sl, sl, size_t(hr) * kp, ncclFloat, r, c->comm, c->comm_stream), "broadcast H slice");
+            ncc(c, ncclBroadcast(sl, sl, size_t(hr) * kp, ncclFloat, r, c->comm, c->comm_stream), "broadcast H slice");
             ck(cudaEventRecord(c->ev_bc[r], c->comm_stream), "event");
         }
         coll_end(c, c->comm_stream, kTagH, size_t(c->nranks) * hr * kp * 4);
         c->ag_pending = true;
     } else if (c->shard_h()) {
         coll_begin(c, s);
-        nck(ncclAllGather(c->Ht.as<float>() + h0 * kp, c->Ht.p, size_t(hr) * kp, ncclFloat, c->comm, s),
+        ncc(c, ncclAllGather(c->Ht.as<float>() + h0 * kp, c->Ht.p, size_t(hr) * kp, ncclFloat, c->comm, s),
             "all-gather H");
         coll_end(c, s, kTagH, size_t(c->nranks) * hr * kp * 4);
         if (htlo(c)) count(c, launch_split_cat(c->Ht.as<float>(), htlo(c), c->np, kp, s), "split H");
@@ -1017,7 +1022,7 @@ void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
         // CNMF / sharded H: <W^T A, H> is a sum over the ranks' slabs
         count(c, launch_reduce_f64(eslots, n_err, scal + kCross, s), "reduce cross");
         coll_begin(c, s);
-        nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s), "allreduce cross");
+        ncc(c, ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s), "allreduce cross");
         coll_end(c, s, kTagErr, 8);
         eslots = scal + kCross;
         n_err = 1;
@@ -1033,7 +1038,7 @@ void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kRes, s), "reduce");
             if (c->collective()) {
                 coll_begin(c, s);
-                nck(ncclAllReduce(scal + kRes, scal + kRes, 1, ncclDouble, ncclSum, c->comm, s), "allreduce res");
+                ncc(c, ncclAllReduce(scal + kRes, scal + kRes, 1, ncclDouble, ncclSum, c->comm, s), "allreduce res");
                 coll_end(c, s, kTagErr, 8);  // nmf_distributed.cpp:254
             }
             count(c, launch_finalize_error(kp, nullptr, 0, c->WtW64.as<double>(), c->HHt64.as<double>(),
@@ -1047,7 +1052,7 @@ void enqueue_check(oocnmf_ctx* c, int error_mode, uint64_t slot) {
             count(c, launch_reduce_f64(c->red_slots.as<double>(), sqnorm_grid(), scal + kCross, s), "reduce");
             if (c->collective()) {
                 coll_begin(c, s);
-                nck(ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s),
+                ncc(c, ncclAllReduce(scal + kCross, scal + kCross, 1, ncclDouble, ncclSum, c->comm, s),
                     "allreduce cross");
                 coll_end(c, s, kTagErr, 8);
             }
@@ -2214,7 +2219,7 @@ int oocnmf_gather_w_f64(oocnmf_ctx* c, double* w_full) {
         if (N > 1) {
             need_comm(c);
             coll_begin(c, c->stream);
-            nck(ncclAllGather(mine, all.p, size_t(maxr) * kp, ncclFloat, c->comm, c->stream), "allgather W");
+            ncc(c, ncclAllGather(mine, all.p, size_t(maxr) * kp, ncclFloat, c->comm, c->stream), "allgather W");
             coll_end(c, c->stream, kTagGather, size_t(N) * maxr * kp * 4);  // nmf_distributed.cpp:280
             wait_for(c, c->stream, nullptr, "W all-gather");
         }
@@ -2324,7 +2329,7 @@ int oocnmf_gather_h_f64(oocnmf_ctx* c, double* h_full) {
         if (c->collective()) {
             need_comm(c);
             coll_begin(c, c->stream);
-            nck(ncclAllReduce(d.p, d.p, c->k * c->n_global, ncclDouble, ncclSum, c->comm, c->stream), "allreduce H");
+            ncc(c, ncclAllReduce(d.p, d.p, c->k * c->n_global, ncclDouble, ncclSum, c->comm, c->stream), "allreduce H");
             coll_end(c, c->stream, kTagGather, c->k * c->n_global * 8);  // nmf_distributed.cpp:272
             wait_for(c, c->stream, nullptr, "H gather");
         }
@@ -2435,7 +2440,7 @@ int oocnmf_allreduce_f64(oocnmf_ctx* c, double* buf, uint64_t count, int tag) {
         need_comm(c);
         ck(cudaMemcpyAsync(d.p, buf, count * 8, cudaMemcpyHostToDevice, c->stream), "H2D");
         coll_begin(c, c->stream);
-        nck(ncclAllReduce(d.p, d.p, count, ncclDouble, ncclSum, c->comm, c->stream), "allreduce");
+        ncc(c, ncclAllReduce(d.p, d.p, count, ncclDouble, ncclSum, c->comm, c->stream), "allreduce");
         coll_end(c, c->stream, tag, count * 8);
         ck(cudaMemcpyAsync(buf, d.p, count * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
         wait_for(c, c->stream, nullptr, "all_reduce_sum");
@@ -2454,7 +2459,7 @@ int oocnmf_barrier(oocnmf_ctx* c) {
         d.alloc(4, "barrier");
         ck(cudaMemsetAsync(d.p, 0, 4, c->stream), "memset");
         coll_begin(c, c->stream);
-        nck(ncclAllReduce(d.p, d.p, 1, ncclFloat, ncclSum, c->comm, c->stream), "barrier");
+        ncc(c, ncclAllReduce(d.p, d.p, 1, ncclFloat, ncclSum, c->comm, c->stream), "barrier");
         coll_end(c, c->stream, kTagBarrier, 0);
         wait_for(c, c->stream, nullptr, "barrier");
     });

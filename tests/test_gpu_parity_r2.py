@@ -246,3 +246,24 @@ def test_wide_k_products_match_f64(gpu):
     assert rel_fro(aht, a64 @ h.T) < 3e-6 and rel_fro(wta, w.T @ a64) < 3e-6
     assert rel_fro(hht, h @ h.T) < 3e-6 and rel_fro(wtw, w.T @ w) < 3e-6
     assert np.array_equal(hht, hht.T) and np.array_equal(wtw, wtw.T)
+
+
+def test_eta_exit_restores_the_factors_of_the_stopping_check(gpu):
+    """eta > 0: the early exit (src/nmf_serial.cpp:111) is taken one block late so the device never
+    waits on the host; the factors must still be those of the stopping check (snapshot
+    restore), the trace must end there and iterations_run must match the reference."""
+    g = golden("uniform_1536x1024_k32") if os.path.exists(os.path.join(GOLD, "uniform_1536x1024_k32.npz")) else None
+    a = port.uniform_dense(1536, 1024, 42, 99).astype(np.float32)
+    w0, h0 = port.init_factors(1536, 1024, 32, 0)
+    full = port.nmf_serial(f32(a), 32, f32(w0), f32(h0), max_iters=50, interval=10)
+    eta = 0.5 * (full.trace_err[2] + full.trace_err[3])  # between the checks at 30 and 40
+    ref = port.nmf_serial(f32(a), 32, f32(w0), f32(h0), max_iters=50, interval=10, eta=eta)
+    assert ref.converged and ref.iterations_run == 40
+    cfg = nmf.NmfConfig(k=32, max_iters=50, error_check_interval=10, eta=eta, init=nmf.FactorInit.from_files,
+                        init_w=f32(w0), init_h=f32(h0))
+    r = nmf.nmf_serial(a, cfg)
+    assert r.converged and r.iterations_run == 40 and [i for i, _ in r.error_trace] == [10, 20, 30, 40]
+    assert rel_fro(r.w, ref.w) <= FACTOR_TOL and rel_fro(r.h, ref.h) <= FACTOR_TOL
+    assert rel_fro(r.w, full.w) > 10 * rel_fro(r.w, ref.w)  # not the factors of iteration 50
+    if g is not None:
+        np.testing.assert_allclose([e for _, e in r.error_trace], g["trace_err"][:4], rtol=TRACE_TOL)

@@ -178,5 +178,5 @@ def test_dead_rank_raises_comm_error(tmp_path):
     subprocess.run(cmd, timeout=180, cwd=ROOT)
     v = json.load(open(out))
     assert v["first"] == "CommError", v
-    assert "communicator aborted" in v["message"] and v["seconds"] < 60
+    assert "communicator aborted" in v["message"] and v["seconds"] < 60  # (NCCL may see the dead peer first)
     assert v["second"] == "CommError" and "aborted" in v["second_message"]
