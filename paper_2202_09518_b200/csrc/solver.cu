@@ -558,8 +558,11 @@ reduced:
         ncc(c, ncclAllReduce(out, out, 1, ncclDouble, ncclSum, c->comm, c->stream), "allreduce norm");
         coll_end(c, c->stream, kTagErr, 8);  // ||A||^2 (src/nmf_distributed.cpp:232, error_check)
     }
-    ck(cudaMemcpyAsync(&c->norm_a2, out, 8, cudaMemcpyDeviceToHost, c->stream), "D2H norm");
+    // (into the pinned scratch: a pageable D2H would block the host behind a hung collective,
+    // out of the watchdog's reach)
+    ck(cudaMemcpyAsync(c->hpin + 4, out, 8, cudaMemcpyDeviceToHost, c->stream), "D2H norm");
     wait_for(c, c->stream, nullptr, "||A||^2 all-reduce");
+    std::memcpy(&c->norm_a2, c->hpin + 4, 8);
     c->norm_valid = true;
 }
 
@@ -1821,6 +1824,12 @@ int oocnmf_split_even(uint64_t extent, uint64_t parts, uint64_t* begins) {
     });
 }
 
+// Establish the group's NVLink / network connections during communicator creation, while every
+// rank is alive (NCCL otherwise connects lazily inside the first collective, where a peer that
+// died meanwhile blocks the host in the NCCL call for its own ~60 s socket timeout, out of reach
+// of the progress watchdog). Respects a caller's own NCCL_RUNTIME_CONNECT.
+static void eager_connect() { setenv("NCCL_RUNTIME_CONNECT", "0", 0); }
+
 static void ctx_init_common(oocnmf_ctx* c, int device) {
     int nd = 0;
     if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
@@ -1882,6 +1891,7 @@ int oocnmf_ctx_create_comm(int device, int rank, int nranks, const unsigned char
             if (nranks > 1) {
                 ncclUniqueId uid;
                 std::memcpy(&uid, id, 128);
+                eager_connect();
                 nck(ncclCommInitRank(&c->comm, nranks, uid, rank), "ncclCommInitRank");
             }
         } catch (...) {
@@ -2442,8 +2452,8 @@ int oocnmf_allreduce_f64(oocnmf_ctx* c, double* buf, uint64_t count, int tag) {
         coll_begin(c, c->stream);
         ncc(c, ncclAllReduce(d.p, d.p, count, ncclDouble, ncclSum, c->comm, c->stream), "allreduce");
         coll_end(c, c->stream, tag, count * 8);
-        ck(cudaMemcpyAsync(buf, d.p, count * 8, cudaMemcpyDeviceToHost, c->stream), "D2H");
-        wait_for(c, c->stream, nullptr, "all_reduce_sum");
+        wait_for(c, c->stream, nullptr, "all_reduce_sum");  // (before the pageable D2H, which would block)
+        ck(cudaMemcpy(buf, d.p, count * 8, cudaMemcpyDeviceToHost), "D2H");
     });
 }
 
@@ -2512,6 +2522,7 @@ int oocnmf_ctx_create_group(int n, const int* devices, oocnmf_ctx** out) {
             }
             if (n > 1) {
                 std::vector<ncclComm_t> comms(n);
+                eager_connect();
                 nck(ncclCommInitAll(comms.data(), n, devs.data()), "ncclCommInitAll");
                 for (int r = 0; r < n; ++r) cs[r]->comm = comms[r];
             }
