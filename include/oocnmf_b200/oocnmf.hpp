@@ -204,6 +204,8 @@ struct PartitionPlan {
     std::vector<IndexRange> batches;
     index_t max_slab_extent() const;
     index_t max_batch_extent() const;
+    /// The reference's JSON (src/partition.cpp:89-104: nlohmann dump(2), sorted keys).
+    std::string to_json() const;
 };
 PartitionPlan make_plan(index_t m, index_t n, index_t k, int n_workers, index_t n_b, Strategy strategy);
 
@@ -219,6 +221,9 @@ struct MemoryReport {
     index_t min_n_b = 0;
     bool feasible = false;
     bool in_core = false;
+    /// The reference's JSON (src/partition.cpp:199-209; in_core is this backend's extra field
+    /// and, like the reference, not serialised).
+    std::string to_json() const;
 };
 MemoryReport memory_estimate(const PartitionPlan& plan, double density, index_t budget_bytes, index_t n_cb = 1);
 

@@ -350,6 +350,23 @@ class Ref(_Lib):
         f.argtypes = [C.c_void_p, _u64, _pd, _pd, _dbl]
         self._check(f(hnd, w.shape[1], _ptr(w), _ptr(h), eps))
 
+    def plan_to_json(self, m, n, k, n_workers, n_b, strategy):
+        f = self.lib.ref_plan_to_json
+        f.restype = C.c_long
+        f.argtypes = [_u64, _u64, _u64, C.c_int, _u64, C.c_int, C.c_char_p, _u64]
+        buf = C.create_string_buffer(1 << 20)
+        ln = f(m, n, k, n_workers, n_b, strategy, buf, len(buf))
+        return buf.raw[:ln].decode()
+
+    def memreport_to_json(self, values7, feasible):
+        f = self.lib.ref_memreport_to_json
+        f.restype = C.c_long
+        f.argtypes = [_pu, C.c_int, C.c_char_p, _u64]
+        v = np.ascontiguousarray(values7, np.uint64)
+        buf = C.create_string_buffer(4096)
+        ln = f(_ptr(v, _pu), int(feasible), buf, len(buf))
+        return buf.raw[:ln].decode()
+
     def dense_uniform_handle(self, m, n, seed=42, stream=99, round_f32=True):
         """The uniform synthetic A built in place inside the library (no numpy copy)."""
         f = self.lib.ref_dense_create_uniform

@@ -310,6 +310,26 @@ int ref_nmf_serial_dense_handle(void* a_handle, std::uint64_t k, std::uint64_t m
     });
 }
 
+// PartitionPlan::to_json / MemoryReport::to_json of the reference (src/partition.cpp:89,199) into
+// buf (NUL-terminated); returns the length or -1 if cap is too small.
+long ref_plan_to_json(std::uint64_t m, std::uint64_t n, std::uint64_t k, int n_workers, std::uint64_t n_b,
+                      int strategy, char* buf, std::uint64_t cap) {
+    const PartitionPlan p = make_plan(m, n, k, n_workers, n_b, strategy == 1 ? Strategy::cnmf : Strategy::rnmf);
+    const std::string j = p.to_json();
+    if (j.size() + 1 > cap) return -1;
+    std::memcpy(buf, j.c_str(), j.size() + 1);
+    return long(j.size());
+}
+long ref_memreport_to_json(const std::uint64_t* v7, int feasible, char* buf, std::uint64_t cap) {
+    MemoryReport r;
+    r.a_slab_bytes = v7[0], r.store_peak_bytes = v7[1], r.factor_bytes = v7[2], r.intermediate_bytes = v7[3];
+    r.peak_bytes = v7[4], r.min_n_b = v7[5], r.feasible = feasible != 0;
+    const std::string j = r.to_json();
+    if (j.size() + 1 > cap) return -1;
+    std::memcpy(buf, j.c_str(), j.size() + 1);
+    return long(j.size());
+}
+
 // CSR variant for the sparse bench sample (A held by the library across timed iterations).
 void* ref_csr_create(const std::uint64_t* rp, const std::uint64_t* ci, const double* v, std::uint64_t m,
                      std::uint64_t n) {

@@ -275,6 +275,54 @@ PartitionPlan make_plan(index_t m, index_t n, index_t k, int n_workers, index_t 
     return p;
 }
 
+namespace {
+// Minimal writer for the reference's nlohmann::json::dump(2) output (2-space indent, objects one
+// member per line, arrays of numbers on one line, keys emitted in sorted order by the callers).
+std::string jpad(int d) { return std::string(size_t(2 * d), ' '); }
+std::string jrange(const IndexRange& r, int) {  // (numeric arrays stay on one line)
+    return "[" + std::to_string(r.begin) + "," + std::to_string(r.end) + "]";
+}
+}  // namespace
+
+std::string PartitionPlan::to_json() const {
+    const bool col = strategy == Strategy::cnmf;
+    std::string o = "{\n";
+    if (!batches.empty()) {
+        o += jpad(1) + "\"batches\": [\n";
+        for (size_t i = 0; i < batches.size(); ++i)
+            o += jpad(2) + jrange(batches[i], 2) + (i + 1 < batches.size() ? ",\n" : "\n");
+        o += jpad(1) + "],\n";
+    }
+    o += jpad(1) + "\"h_role\": \"" + (col ? "slab" : "replicated") + "\",\n";
+    o += jpad(1) + "\"k\": " + std::to_string(k) + ",\n";
+    o += jpad(1) + "\"m\": " + std::to_string(m) + ",\n";
+    o += jpad(1) + "\"n\": " + std::to_string(n) + ",\n";
+    o += jpad(1) + "\"n_b\": " + std::to_string(n_b) + ",\n";
+    o += jpad(1) + "\"n_workers\": " + std::to_string(n_workers) + ",\n";
+    o += jpad(1) + "\"strategy\": \"" + (col ? "cnmf" : "rnmf") + "\",\n";
+    o += jpad(1) + "\"w_role\": \"" + (col ? "replicated" : "slab") + "\"";
+    if (!slabs.empty()) {
+        o += ",\n" + jpad(1) + "\"workers\": [\n";
+        for (size_t i = 0; i < slabs.size(); ++i) {
+            const auto& w = slabs[i];
+            o += jpad(2) + "{\n" + jpad(3) + "\"a_cols\": " + jrange(w.a_cols, 3) + ",\n" + jpad(3) +
+                 "\"a_rows\": " + jrange(w.a_rows, 3) + ",\n" + jpad(3) + "\"rank\": " + std::to_string(w.rank) +
+                 "\n" + jpad(2) + "}" + (i + 1 < slabs.size() ? ",\n" : "\n");
+        }
+        o += jpad(1) + "]";
+    }
+    return o + "\n}";
+}
+
+std::string MemoryReport::to_json() const {
+    return "{\n" + jpad(1) + "\"a_slab_bytes\": " + std::to_string(a_slab_bytes) + ",\n" + jpad(1) +
+           "\"factor_bytes\": " + std::to_string(factor_bytes) + ",\n" + jpad(1) + "\"feasible\": " +
+           (feasible ? "true" : "false") + ",\n" + jpad(1) + "\"intermediate_bytes\": " +
+           std::to_string(intermediate_bytes) + ",\n" + jpad(1) + "\"min_n_b\": " + std::to_string(min_n_b) +
+           ",\n" + jpad(1) + "\"peak_bytes\": " + std::to_string(peak_bytes) + ",\n" + jpad(1) +
+           "\"store_peak_bytes\": " + std::to_string(store_peak_bytes) + "\n}";
+}
+
 MemoryReport memory_estimate(const PartitionPlan& plan, double density, index_t budget_bytes, index_t n_cb) {
     if (n_cb < 1) throw ShapeError("memory_estimate: n_cb must be >= 1");
     oocnmf_memory_report r{};

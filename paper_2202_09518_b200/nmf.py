@@ -431,6 +431,15 @@ def choose_strategy(m: int, n: int) -> Strategy:
     return Strategy.cnmf if n > m else Strategy.rnmf
 
 
+def _ref_json(d) -> str:
+    """The reference's nlohmann dump(2) layout: sorted keys, 2-space indent, arrays of numbers on
+    one line without spaces."""
+    import json
+    import re
+    s = json.dumps(d, indent=2, sort_keys=True)
+    return re.sub(r"\[\s*((?:-?\d+,\s*)*-?\d+)\s*\]", lambda mt: "[" + re.sub(r"\s+", "", mt.group(1)) + "]", s)
+
+
 @dataclass
 class PartitionPlan:
     strategy: Strategy
@@ -441,6 +450,18 @@ class PartitionPlan:
     n_b: int
     slabs: List[Tuple[Tuple[int, int], Tuple[int, int]]]  # per rank: ((row0,row1),(col0,col1))
     batches: List[Tuple[int, int]]
+
+    def to_json(self) -> str:
+        """The reference's plan JSON (src/partition.cpp:89-104, nlohmann dump(2))."""
+        col = self.strategy == Strategy.cnmf
+        d = {"strategy": self.strategy.value, "n_workers": self.n_workers, "m": self.m, "n": self.n, "k": self.k,
+             "n_b": self.n_b, "w_role": "replicated" if col else "slab", "h_role": "slab" if col else "replicated"}
+        if self.slabs:
+            d["workers"] = [{"rank": r, "a_rows": list(rows), "a_cols": list(cols)}
+                            for r, (rows, cols) in enumerate(self.slabs)]
+        if self.batches:
+            d["batches"] = [list(b) for b in self.batches]
+        return _ref_json(d)
 
 
 def make_plan(m, n, k, n_workers, n_b, strategy: Strategy) -> PartitionPlan:
@@ -476,6 +497,11 @@ class MemoryReport:
     min_n_b: int  # 1: in-core fits; > 1: out-of-core row batches; 0: infeasible
     feasible: bool
     in_core: bool
+
+    def to_json(self) -> str:
+        """The reference's report JSON (src/partition.cpp:199-209; in_core is not serialised)."""
+        return _ref_json({k: getattr(self, k) for k in ("a_slab_bytes", "store_peak_bytes", "factor_bytes",
+                                                        "intermediate_bytes", "peak_bytes", "min_n_b", "feasible")})
 
 
 def memory_estimate(plan: "PartitionPlan", density: float, budget_bytes: int, n_cb: int = 1,

@@ -8,7 +8,20 @@
 #include "oocnmf/matrix.hpp"
 #include "oocnmf/model_selection.hpp"
 #include "oocnmf/nmf.hpp"
+#include "oocnmf/partition.hpp"
 #include "oocnmf/rng.hpp"
+
+#include <string>
+
+static std::string jesc(const std::string& s) {
+    std::string o;
+    for (char ch : s) {
+        if (ch == '\n') o += "\\n";
+        else if (ch == '"') o += "\\\"";
+        else o += ch;
+    }
+    return o;
+}
 
 int main(int argc, char** argv) {
     using namespace oocnmf;
@@ -55,6 +68,14 @@ int main(int argc, char** argv) {
         SelectionReport rep = select_k(MatrixRef(lr), sc);
         std::printf("{\"select_chosen\": %lld, \"select_records\": %zu}\n",
                     rep.chosen_k ? (long long)*rep.chosen_k : -1LL, rep.records.size());
+    }
+    // The plan / memory-report JSON of the reference (src/partition.cpp:89,199)
+    {
+        const std::string pj = make_plan(1000, 900, 8, 4, 3, Strategy::rnmf).to_json();
+        MemoryReport mr;
+        mr.a_slab_bytes = 1, mr.store_peak_bytes = 2, mr.factor_bytes = 3, mr.intermediate_bytes = 4;
+        mr.peak_bytes = 5, mr.min_n_b = 6, mr.feasible = true;
+        std::printf("{\"plan_json\": \"%s\", \"report_json\": \"%s\"}\n", jesc(pj).c_str(), jesc(mr.to_json()).c_str());
     }
     // Error mapping: an invalid config throws ShapeError like the reference.
     try {

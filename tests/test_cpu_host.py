@@ -167,3 +167,18 @@ def test_memory_estimate_layout_and_batches():
         nmf.memory_estimate(p, 1.0, 1 << 20)
     with pytest.raises(nmf.ShapeError, match="density"):
         nmf.memory_estimate(p, 0.0, 1 << 30)
+
+
+def test_plan_and_report_json_match_reference():
+    """PartitionPlan.to_json / MemoryReport.to_json byte-identical to the reference's
+    (src/partition.cpp:89-104, 199-209: nlohmann dump(2))."""
+    import oracle
+    from paper_2202_09518_b200.nmf import MemoryReport
+
+    if not oracle.ref.available:
+        pytest.skip("needs oracle/_ref")
+    for m, n, k, w, nb, st in [(1000, 900, 8, 4, 3, 0), (700, 1300, 16, 3, 2, 1), (10, 10, 2, 1, 1, 0)]:
+        plan = nmf.make_plan(m, n, k, w, nb, nmf.Strategy.cnmf if st == 1 else nmf.Strategy.rnmf)
+        assert plan.to_json() == oracle.ref.plan_to_json(m, n, k, w, nb, st)
+    mr = MemoryReport(1, 2, 3, 4, 5, 6, True, False)
+    assert mr.to_json() == oracle.ref.memreport_to_json([1, 2, 3, 4, 5, 6, 0], 1)

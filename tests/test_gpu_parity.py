@@ -373,6 +373,10 @@ def test_cpp_host_core_is_a_drop_in(gpu):
     assert any(d.get("shape_error") for d in lines)
     sel = [d for d in lines if "select_chosen" in d][0]  # oocnmf::select_k through the C++ host core
     assert sel == {"select_chosen": 2, "select_records": 3}
+    js = [d for d in lines if "plan_json" in d][0]  # PartitionPlan / MemoryReport::to_json
+    if oracle.ref.available:
+        assert js["plan_json"] == oracle.ref.plan_to_json(1000, 900, 8, 4, 3, 0)
+        assert js["report_json"] == oracle.ref.memreport_to_json([1, 2, 3, 4, 5, 6, 0], 1)
 
 
 # ---------------------------------------------------------------------------- edge cases
