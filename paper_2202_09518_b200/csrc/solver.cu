@@ -468,19 +468,35 @@ void alloc_factors(oocnmf_ctx* c) {
 // re-reads out of L2, 32 GB instead of 19 GB of DRAM reads per launch); OOCNMF_FUSED_P2FIRST=1
 // orders each step P2(s - D) before P1(s); OOCNMF_FUSED_POL picks the L2 policies of the two A
 // loads (0: normal / first, 1: last / first, 2: normal / normal).
+// The one-pass kernel pays a fixed W-update latency per 128-row block (~4 us: every CTA's
+// partial published, gathered and summed); it beats the two streaming passes once a row block
+// is large enough to hide it. Measured on B200 (tools/fused_crossover.py,
+// profiles/r2_fused_crossover.jsonl): np = 65536 +8-13 %; np = 32768 (lag 2) +3-7 % at
+// kp = 16, -3..-8 % at kp = 32; np = 16384 -20-35 %; np = 8192 -55 %.
+// OOCNMF_FUSED=0 / 1 turns it off / on regardless of the shape.
 bool fused_wanted(const oocnmf_ctx* c) {
     const char* e = std::getenv("OOCNMF_FUSED");
     if (e && e[0] == '0') return false;
-    return c->use_tc && !c->cnmf && fused_supported(c->kp, c->mp, c->np, c->num_sms);
+    const bool forced = e && e[0] == '1';
+    const int64_t min_cols = c->kp == 16 ? 32768 : 65536;
+    return c->use_tc && !c->cnmf && (forced || c->np >= min_cols) &&
+           fused_supported(c->kp, c->mp, c->np, c->num_sms);
 }
 int env_int(const char* name, int dflt) {
     const char* e = std::getenv(name);
     return e && *e ? std::atoi(e) : dflt;
 }
+// P2 lags P1 by D row blocks; the D + 2 blocks in flight (128 np 4 bytes each) must stay in
+// L2 for P2's re-read, so D is what 64 MiB holds beyond the two in use, clamped to [1, 4]
+// (np = 65536: 1, 32768: 2, <= 16384: 4).
+int fused_lag(int64_t np) {
+    const int64_t blk = int64_t(kTile) * np * 4;
+    return int(std::max<int64_t>(1, std::min<int64_t>(4, (int64_t(64) << 20) / blk - 2)));
+}
 
 void plan_fused_buffers(oocnmf_ctx* c) {
     FusedPlan& fp = c->fplan;
-    plan_fused(fp, c->mp, c->np, c->num_sms, env_int("OOCNMF_FUSED_D", 1));
+    plan_fused(fp, c->mp, c->np, c->num_sms, env_int("OOCNMF_FUSED_D", fused_lag(c->np)));
     std::vector<int> idx;
     idx.insert(idx.end(), fp.q0.begin(), fp.q0.end());
     idx.insert(idx.end(), fp.t0.begin(), fp.t0.end());

@@ -97,7 +97,9 @@ def _golden(name):
     return np.load(os.path.join(GOLD, name + ".npz"))
 
 
-def test_config1_uniform_matches_reference(gpu):
+@pytest.mark.parametrize("engine", ["1", "0"])  # OOCNMF_FUSED: one-pass kernel / two passes
+def test_config1_uniform_matches_reference(gpu, monkeypatch, engine):
+    monkeypatch.setenv("OOCNMF_FUSED", engine)
     g = _golden("config1_uniform_f32in")
     a = port.uniform_dense(4096, 2048, 42, 99).astype(np.float32)
     res = solve_from(a, 16, 100, 10)
@@ -105,7 +107,9 @@ def test_config1_uniform_matches_reference(gpu):
     assert res.iterations_run == 100 and not res.converged
 
 
-def test_config1_lowrank_matches_reference(gpu):
+@pytest.mark.parametrize("engine", ["1", "0"])  # OOCNMF_FUSED: one-pass kernel / two passes
+def test_config1_lowrank_matches_reference(gpu, monkeypatch, engine):
+    monkeypatch.setenv("OOCNMF_FUSED", engine)
     g = _golden("config1_lowrank_f32in")
     if not oracle.ref.available:
         pytest.skip("low-rank input regeneration needs oracle/_ref")
@@ -114,7 +118,9 @@ def test_config1_lowrank_matches_reference(gpu):
     check_parity(res, g["trace_iters"], g["trace_err"], g["w"], g["h"])
 
 
-def test_k32_matches_reference(gpu):
+@pytest.mark.parametrize("engine", ["1", "0"])  # OOCNMF_FUSED: one-pass kernel / two passes
+def test_k32_matches_reference(gpu, monkeypatch, engine):
+    monkeypatch.setenv("OOCNMF_FUSED", engine)
     g = _golden("uniform_1536x1024_k32")
     a = port.uniform_dense(1536, 1024, 42, 99).astype(np.float32)
     res = solve_from(a, 32, 50, 10)
@@ -123,7 +129,9 @@ def test_k32_matches_reference(gpu):
 
 @pytest.mark.parametrize("name,k,iters,interval", [("lowrank_1024x768_k64", 64, 30, 10),
                                                     ("lowrank_1024x768_k5", 5, 40, 10)])
-def test_k64_and_padded_k_match_reference(gpu, name, k, iters, interval):
+@pytest.mark.parametrize("engine", ["1", "0"])
+def test_k64_and_padded_k_match_reference(gpu, monkeypatch, name, k, iters, interval, engine):
+    monkeypatch.setenv("OOCNMF_FUSED", engine)
     if not oracle.ref.available:
         pytest.skip("input regeneration needs oracle/_ref")
     g = _golden(name)
@@ -319,7 +327,7 @@ def test_error_behaviour(gpu):
     with pytest.raises(nmf.DataError):
         nmf.nmf_serial(np.zeros((20, 10), np.float32), nmf.NmfConfig(k=2, max_iters=3))
     with pytest.raises(nmf.ShapeError):
-        nmf.nmf_serial(a, nmf.NmfConfig(k=65, max_iters=3))
+        nmf.nmf_serial(a, nmf.NmfConfig(k=513, max_iters=3))  # beyond kMaxWideKp
     with pytest.raises(nmf.ShapeError):
         nmf.nmf_serial(a, nmf.NmfConfig(k=2, max_iters=0))
     with pytest.raises(nmf.ShapeError):

@@ -156,6 +156,7 @@ def test_fused_pass_matches_two_pass_kernels(gpu, monkeypatch, m, n, k, lookahea
     w0, h0 = port.init_factors(m, n, k, 3)
     cfg = nmf.NmfConfig(k=k, max_iters=30, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
                         init_w=f32(w0), init_h=f32(h0))
+    monkeypatch.setenv("OOCNMF_FUSED", "1")  # these shapes are below the automatic threshold
     monkeypatch.setenv("OOCNMF_FUSED_D", lookahead)
     fused = nmf.nmf_serial(a, cfg)
     assert fused.info["fused_pass_launches"] == 30
@@ -171,12 +172,14 @@ def test_fused_pass_matches_two_pass_kernels(gpu, monkeypatch, m, n, k, lookahea
     assert rel_fro(fused.w, split.w) <= 1e-4 and rel_fro(fused.h, split.h) <= 1e-4
 
 
-def test_fused_pass_is_deterministic(gpu):
+def test_fused_pass_is_deterministic(gpu, monkeypatch):
+    monkeypatch.setenv("OOCNMF_FUSED", "1")
     a = port.uniform_dense(1024, 4096, 5, 99).astype(np.float32)
     w0, h0 = port.init_factors(1024, 4096, 32, 1)
     cfg = nmf.NmfConfig(k=32, max_iters=12, error_check_interval=4, eta=0.0, init=nmf.FactorInit.from_files,
                         init_w=f32(w0), init_h=f32(h0))
     r1, r2 = nmf.nmf_serial(a, cfg), nmf.nmf_serial(a, cfg)
+    assert r1.info["fused_pass_launches"] == 12
     assert np.array_equal(r1.w, r2.w) and np.array_equal(r1.h, r2.h)
     assert [e for _, e in r1.error_trace] == [e for _, e in r2.error_trace]
 
@@ -248,7 +251,8 @@ def test_wide_k_products_match_f64(gpu):
     assert np.array_equal(hht, hht.T) and np.array_equal(wtw, wtw.T)
 
 
-def test_eta_exit_restores_the_factors_of_the_stopping_check(gpu):
+@pytest.mark.parametrize("fused", ["1", "0"])
+def test_eta_exit_restores_the_factors_of_the_stopping_check(gpu, monkeypatch, fused):
     """eta > 0: the early exit (src/nmf_serial.cpp:111) is taken one block late so the device never
     waits on the host; the factors must still be those of the stopping check (snapshot
     restore), the trace must end there and iterations_run must match the reference."""
@@ -261,7 +265,9 @@ def test_eta_exit_restores_the_factors_of_the_stopping_check(gpu):
     assert ref.converged and ref.iterations_run == 40
     cfg = nmf.NmfConfig(k=32, max_iters=50, error_check_interval=10, eta=eta, init=nmf.FactorInit.from_files,
                         init_w=f32(w0), init_h=f32(h0))
+    monkeypatch.setenv("OOCNMF_FUSED", fused)
     r = nmf.nmf_serial(a, cfg)
+    assert (r.info["fused_pass_launches"] > 0) == (fused == "1")
     assert r.converged and r.iterations_run == 40 and [i for i, _ in r.error_trace] == [10, 20, 30, 40]
     assert rel_fro(r.w, ref.w) <= FACTOR_TOL and rel_fro(r.h, ref.h) <= FACTOR_TOL
     assert rel_fro(r.w, full.w) > 10 * rel_fro(r.w, ref.w)  # not the factors of iteration 50
