@@ -228,9 +228,9 @@ struct MemoryReport {
 MemoryReport memory_estimate(const PartitionPlan& plan, double density, index_t budget_bytes, index_t n_cb = 1);
 
 // ---- distributed (reference: include/oocnmf/nmf_distributed.hpp, comm.hpp) ----
-/// Group transports (comm.hpp:10). B200: loopback (one rank) and threads (one process, one
-/// GPU per rank thread, NCCL clique); multi-process groups use the CommHandle constructor with
-/// an NCCL unique id (the reference's tcp backend role). tcp is not offered.
+/// Group transports (comm.hpp:10). B200: loopback (one rank), threads (one process, one GPU
+/// per rank thread, NCCL clique) and tcp (one process per rank: connect_tcp, a TCP rendezvous
+/// that hands out an NCCL unique id; the collectives themselves run over NCCL).
 enum class Backend { loopback, threads, tcp };
 Backend backend_from_string(const std::string& s);
 
@@ -299,6 +299,12 @@ struct CommGroup {
 /// loopback: n must be 1. threads: n handles on GPUs 0..n-1 sharing one NCCL clique, one per
 /// worker thread (comm.hpp:80-82).
 CommGroup spawn_group(int n, Backend backend, double timeout_s = 60.0);
+/// tcp backend (comm.hpp:84-87): rank 0 listens on peers[0] ("host:port"), the other ranks
+/// connect to it (retrying until timeout_s) and receive an NCCL unique id; every rank then
+/// joins one NCCL communicator on its GPU (OOCNMF_DEVICE, else LOCAL_RANK, else rank modulo the
+/// visible GPUs). One handle per process.
+CommHandle connect_tcp(int n, int rank, const std::vector<std::string>& peers, std::uint64_t group_id = 0,
+                       double timeout_s = 60.0);
 
 struct ASource {
     MatrixRef mem;
@@ -371,6 +377,34 @@ void write_mtx(const std::string& path, const CsrMatrix& m);
 AnyMatrix read_mtx(const std::string& path);
 /// Dispatch on extension: .mtx -> Matrix Market, anything else -> PDN1.
 AnyMatrix read_matrix(const std::string& path);
+
+// ---- synthetic inputs (reference: include/oocnmf/synth.hpp) ----
+struct LowrankSpec {
+    index_t m = 0;
+    index_t n = 0;
+    index_t k_true = 0;
+    double noise = 0.0;  ///< multiplicative noise amplitude (0 disables)
+    std::uint64_t seed = 0;
+};
+struct LowrankData {
+    DenseMatrix a;   // m x n
+    DenseMatrix w0;  // m x k_true
+    DenseMatrix h0;  // k_true x n
+};
+/// A = W0 H0 with Gaussian-bump columns of W0 (plus a 0.01 U floor) and U(0,1) H0, optionally
+/// scaled entrywise by U(1 - noise, 1 + noise) (src/synth.cpp:18-57). Host-side, bit-identical
+/// to the reference (same CounterRng streams, same f64 summation order).
+LowrankData gen_lowrank(const LowrankSpec& spec);
+struct SparseSpec {
+    index_t m = 0;
+    index_t n = 0;
+    double density = 0.0;  ///< independent per-entry Bernoulli probability
+    std::uint64_t seed = 0;
+};
+/// m x n CSR, entry (i, j) present iff U(seed, 14, i n + j) < density, value U(seed, 15, i n + j)
+/// (src/synth.cpp:59-86). Evaluated on GPU 0 (the reference generator, O(m n) draws, runs
+/// there at HBM speed) and downloaded; bit-identical to the reference.
+CsrMatrix gen_sparse_random(const SparseSpec& spec);
 
 // ---- model selection (reference: include/oocnmf/model_selection.hpp) ----
 struct SelectionConfig {

@@ -367,6 +367,30 @@ class Ref(_Lib):
         ln = f(_ptr(v, _pu), int(feasible), buf, len(buf))
         return buf.raw[:ln].decode()
 
+    def json_reformat(self, text, indent=2):
+        """nlohmann::json::parse(text).dump(indent) with the reference's JSON library."""
+        f = self.lib.ref_json_reformat
+        f.restype = C.c_long
+        f.argtypes = [C.c_char_p, C.c_int, C.c_char_p, _u64]
+        buf = C.create_string_buffer(1 << 22)
+        ln = f(text.encode(), indent, buf, len(buf))
+        if ln < 0:
+            raise ValueError(f"json_reformat failed ({ln}): {self._err()}")
+        return buf.raw[:ln].decode()
+
+    def selection_json_csv(self, records, chosen, rationale):
+        """The reference's SelectionReport::to_json / to_csv for the given records."""
+        rec = np.array([[r["k"], float(r["valid"]), r["runs_used"], r["min_silhouette"], r["mean_silhouette"],
+                         r["mean_relative_error"]] for r in records], np.float64).reshape(-1, 6)
+        f = self.lib.ref_selection_json_csv
+        f.restype = C.c_long
+        f.argtypes = [_pd, _u64, C.c_int64, C.c_char_p, C.c_char_p, _u64, C.c_char_p, _u64]
+        jb, cb = C.create_string_buffer(1 << 20), C.create_string_buffer(1 << 20)
+        rec = np.ascontiguousarray(rec)
+        assert f(_ptr(rec), len(rec), -1 if chosen is None else chosen, rationale.encode(), jb, len(jb), cb,
+                 len(cb)) == 0
+        return jb.value.decode(), cb.value.decode()
+
     def dense_uniform_handle(self, m, n, seed=42, stream=99, round_f32=True):
         """The uniform synthetic A built in place inside the library (no numpy copy)."""
         f = self.lib.ref_dense_create_uniform

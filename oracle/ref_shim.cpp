@@ -28,6 +28,8 @@
 #include "oocnmf/rng.hpp"
 #include "oocnmf/synth.hpp"
 
+#include <nlohmann/json.hpp>
+
 using namespace oocnmf;
 
 namespace {
@@ -328,6 +330,42 @@ long ref_memreport_to_json(const std::uint64_t* v7, int feasible, char* buf, std
     if (j.size() + 1 > cap) return -1;
     std::memcpy(buf, j.c_str(), j.size() + 1);
     return long(j.size());
+}
+
+// nlohmann::json::parse(text).dump(indent) with the JSON library the reference is compiled
+// against: the fixed-point check of the B200 CLI's JSON writer (csrc/json_out.hpp).
+long ref_json_reformat(const char* text, int indent, char* buf, std::uint64_t cap) {
+    std::string j;
+    try {
+        j = nlohmann::json::parse(text).dump(indent);
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -2;
+    }
+    if (j.size() + 1 > cap) return -1;
+    std::memcpy(buf, j.c_str(), j.size() + 1);
+    return long(j.size());
+}
+
+// SelectionReport::to_json / to_csv (src/model_selection.cpp:408-434) of a report holding the
+// given records (rec6 as ref_select_k_dense writes them), chosen k (-1 = none) and rationale.
+long ref_selection_json_csv(const double* rec6, std::uint64_t nrec, std::int64_t chosen, const char* why,
+                            char* json_buf, std::uint64_t json_cap, char* csv_buf, std::uint64_t csv_cap) {
+    SelectionReport rep;
+    for (std::uint64_t i = 0; i < nrec; ++i) {
+        KRecord r;
+        const double* o = rec6 + 6 * i;
+        r.k = index_t(o[0]), r.valid = o[1] != 0, r.runs_used = index_t(o[2]);
+        r.min_silhouette = o[3], r.mean_silhouette = o[4], r.mean_relative_error = o[5];
+        rep.records.push_back(std::move(r));
+    }
+    if (chosen >= 0) rep.chosen_k = index_t(chosen);
+    rep.rationale = why;
+    const std::string j = rep.to_json(), c = rep.to_csv();
+    if (j.size() + 1 > json_cap || c.size() + 1 > csv_cap) return -1;
+    std::memcpy(json_buf, j.c_str(), j.size() + 1);
+    std::memcpy(csv_buf, c.c_str(), c.size() + 1);
+    return 0;
 }
 
 // CSR variant for the sparse bench sample (A held by the library across timed iterations).

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <exception>
 #include <thread>
+#include "json_out.hpp"
 #include "selection.hpp"
 
 namespace oocnmf {
@@ -410,8 +411,7 @@ CommGroup spawn_group(int n, Backend backend, double timeout_s) {
     if (n < 1) throw ShapeError("spawn_group: need at least one rank");
     if (backend == Backend::loopback && n != 1) throw ShapeError("spawn_group: loopback needs n == 1");
     if (backend == Backend::tcp)
-        throw ShapeError("spawn_group: the tcp backend is not offered; one process per GPU uses "
-                         "CommHandle(rank, size, device, unique_id) over NCCL");
+        throw ShapeError("spawn_group: the tcp backend is one process per rank; use connect_tcp");
     std::vector<int> devs(static_cast<std::size_t>(n));
     for (int r = 0; r < n; ++r) devs[std::size_t(r)] = r;
     std::vector<oocnmf_ctx*> cs(static_cast<std::size_t>(n), nullptr);
@@ -661,11 +661,6 @@ std::string fmt_g(double v) {
     std::snprintf(b, sizeof b, "%g", v);
     return b;
 }
-std::string fmt_json(double v) {
-    char b[64];
-    std::snprintf(b, sizeof b, "%.17g", v);
-    return b;
-}
 
 }  // namespace
 
@@ -686,19 +681,22 @@ SelectionReport select_k(MatrixRef a, const SelectionConfig& cfg, CommHandle& co
     return run_select(comm.context(), a.rows(), cfg);
 }
 
-std::string SelectionReport::to_json() const {
-    std::string j = "{\n  \"chosen_k\": " + (chosen_k ? std::to_string(*chosen_k) : std::string("\"none\"")) +
-                    ",\n  \"rationale\": \"" + rationale + "\",\n  \"records\": [";
-    for (index_t i = 0; i < records.size(); ++i) {
-        const KRecord& r = records[i];
-        j += std::string(i ? "," : "") + "\n    {\n      \"k\": " + std::to_string(r.k) +
-             ",\n      \"mean_relative_error\": " + fmt_json(r.mean_relative_error) +
-             ",\n      \"mean_silhouette\": " + fmt_json(r.mean_silhouette) +
-             ",\n      \"min_silhouette\": " + fmt_json(r.min_silhouette) +
-             ",\n      \"runs_used\": " + std::to_string(r.runs_used) +
-             ",\n      \"valid\": " + (r.valid ? "true" : "false") + "\n    }";
+std::string SelectionReport::to_json() const {  // model_selection.cpp:408-424
+    jsonout::Json j;
+    j["chosen_k"] = chosen_k ? jsonout::Json(std::uint64_t(*chosen_k)) : jsonout::Json("none");
+    j["rationale"] = rationale;
+    j["records"] = jsonout::Json::array();
+    for (const KRecord& r : records) {
+        jsonout::Json rec;
+        rec["k"] = std::uint64_t(r.k);
+        rec["valid"] = r.valid;
+        rec["runs_used"] = std::uint64_t(r.runs_used);
+        rec["min_silhouette"] = r.min_silhouette;
+        rec["mean_silhouette"] = r.mean_silhouette;
+        rec["mean_relative_error"] = r.mean_relative_error;
+        j["records"].push_back(std::move(rec));
     }
-    return j + (records.empty() ? "]\n}" : "\n  ]\n}");
+    return j.dump(2);
 }
 
 std::string SelectionReport::to_csv() const {

@@ -1,0 +1,3 @@
+set -x
+timeout 900 python -m pytest tests/test_cli_gpu.py -q -rf -p no:cacheprovider > gpurun_out/r3b_cli.log 2>&1
+echo "rc=$?" >> gpurun_out/r3b_cli.log
