@@ -61,6 +61,8 @@ struct FusedArgs {
     int* flag;             // non-finite W entries
     float* wta;            // np x kp: W^T A (transposed) of the new W
     uint64_t pol_p1, pol_p2;  // L2 policies of the A loads of P1 / P2
+    uint64_t pol_p1s;         // P1 loads of the streamed (not kept) column tiles
+    int keep_num, keep_den;   // column tile j kept in L2 for P2 iff j % keep_den < keep_num
 };
 struct FusedPlan {
     int G = 0, NB = 0, NT = 0, NQ = 0, D = 1, NS = 3, G1 = 0;
@@ -71,6 +73,8 @@ namespace tc {
 int tc_drain_units();  // kernels_tc.cu: K steps per TMEM accumulation chain
 }
 void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahead);
+// L2 policies of the one-pass kernel's A loads (OOCNMF_FUSED_POL / _KEEP, defaults measured best)
+void fused_policies(FusedArgs& a);
 cudaError_t launch_mu_fused(int kp, const FusedPlan& fp, const float* A, int64_t mp, int64_t np, const float* Ht_cat,
                             const FusedArgs& args, cudaStream_t s);
 

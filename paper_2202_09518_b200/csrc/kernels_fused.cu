@@ -28,6 +28,7 @@
 // warps 4-11 split A into [A_hi | A_lo] TMEM slots, warps 12-15 drain), fed one unit sequence
 //   for s in [0, NB + D):  P1 units of block s (if s < NB), then P2 units of block s - D
 // plus warps 2-3 as the updaters. The Gram W^T W of the new W is a separate small kernel.
+#include <cstdio>
 #include <cstdlib>
 
 #include "tc_ptx.cuh"
@@ -197,7 +198,8 @@ __global__ void __launch_bounds__(512, 1)
             };
             auto p1 = [&](int s) {
                 if (s < NB)
-                    for (int q = q0; q < q1; ++q) load_a(&tmA1, s * 128, 2 * q, p.pol_p1);  // block s, K-atoms 2q..
+                    for (int q = q0; q < q1; ++q)  // block s, K-atoms 2q..
+                        load_a(&tmA1, s * 128, 2 * q, (q >> 1) % p.keep_den < p.keep_num ? p.pol_p1 : p.pol_p1s);
             };
             auto p2 = [&](int s) {
                 if (s >= D)
@@ -606,6 +608,19 @@ void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahea
     for (int c = 0; c < G; ++c)
         if (fp.q0[c + 1] > fp.q0[c]) fp.act.push_back(c);
     fp.G1 = int(fp.act.size());
+}
+
+void fused_policies(FusedArgs& a) {
+    const char* e = std::getenv("OOCNMF_FUSED_POL");  // 0 normal/first, 1 last/first, 2 normal/normal
+    const int pol = e && *e ? std::atoi(e) : 0;
+    a.pol_p1 = pol == 1 ? kEvictLast : kEvictNormal;
+    a.pol_p2 = pol == 2 ? kEvictNormal : kEvictFirst;
+    a.pol_p1s = kEvictFirst;
+    a.keep_num = a.keep_den = 1;
+    if (const char* k = std::getenv("OOCNMF_FUSED_KEEP"); k && *k) {  // "num/den"
+        int n = 1, d = 1;
+        if (std::sscanf(k, "%d/%d", &n, &d) == 2 && d >= 1 && n >= 0 && n <= d) a.keep_num = n, a.keep_den = d;
+    }
 }
 
 #ifdef OOC_FZ_PROFILE

@@ -793,7 +793,6 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         const FusedPlan& fp = c->fplan;
         ck(cudaMemsetAsync(c->fz_count.p, 0, c->fz_count.bytes, s), "memset fused counters");
         const int* idx = c->fz_idx.as<int>();
-        static const int pol = env_int("OOCNMF_FUSED_POL", 0);
         FusedArgs a{};
         static const int p2f = env_int("OOCNMF_FUSED_P2FIRST", 0);
         a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = tc::tc_drain_units();
@@ -803,8 +802,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         a.count = c->fz_count.as<unsigned>(), a.wdone = a.count + fp.NB;
         a.W = c->W.as<float>(), a.Wcat = c->W_cat.as<float>(), a.HHt = c->HHt.as<float>();
         a.eps = eps, a.flag = c->flag.as<int>(), a.wta = c->wta();
-        a.pol_p1 = pol == 1 ? 0x14F0000000000000ull : 0x1000000000000000ull;
-        a.pol_p2 = pol == 2 ? 0x1000000000000000ull : 0x12F0000000000000ull;
+        fused_policies(a);
         count(c, launch_mu_fused(kp, fp, c->A.as<float>(), c->mp, c->np, c->Ht_cat.as<float>(), a, s), "mu fused");
         rec(eAht);
         count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, eps, false,

@@ -8,6 +8,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <string>
 #include <vector>
 
 #include "kernels.h"
@@ -82,8 +83,8 @@ int main(int argc, char** argv) {
     a.q0 = idx, a.t0 = idx + fp.G + 1, a.act = idx + 2 * (fp.G + 1);
     a.p1slots = slots, a.count = cnt, a.wdone = cnt + fp.NB;
     a.W = W, a.Wcat = Wc, a.HHt = HHt, a.eps = 1e-12f, a.flag = flag, a.wta = wta;
-    a.pol_p1 = pol == 1 ? 0x14F0000000000000ull : 0x1000000000000000ull;
-    a.pol_p2 = pol == 2 ? 0x1000000000000000ull : 0x12F0000000000000ull;
+    setenv("OOCNMF_FUSED_POL", std::to_string(pol).c_str(), 0);
+    fused_policies(a);
     printf("plan: G %d NB %d NT %d NQ %d D %d NS %d G1 %d; CTA 0: q [%d,%d) t [%d,%d)\n", fp.G, fp.NB, fp.NT, fp.NQ,
            fp.D, fp.NS, fp.G1, fp.q0[0], fp.q0[1], fp.t0[0], fp.t0[1]);
     auto run = [&] {
