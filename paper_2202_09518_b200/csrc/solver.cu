@@ -226,12 +226,14 @@ struct oocnmf_ctx {
     // Needs whole 128-row tiles per rank (n a multiple of 128 N, as at config 3); else all-reduce.
     // Dense RNMF can do the same (OOCNMF_SHARD_H=1); W^T A is only 8.4 MB at config 2, and the
     // all-reduce + replicated H update measured faster (649 vs 607 it/s at N = 4), so it is off.
+    // OOCNMF_SHARD_H=1 / 0 forces the sharded / replicated H update for both kinds.
     bool shard_h() const {
-        static const bool dense_ok = [] {  // measured slower at N = 4 (607 vs 649 it/s): off by default
+        static const int force = [] {  // dense measured slower at N = 4 (607 vs 649 it/s): off by default
             const char* e = std::getenv("OOCNMF_SHARD_H");
-            return e && e[0] == '1';
+            return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
         }();
-        return collective() && !cnmf && (kind == Kind::csr || (kind == Kind::dense && dense_ok)) &&
+        const bool want = force >= 0 ? force == 1 : kind == Kind::csr;
+        return collective() && !cnmf && want && (kind == Kind::csr || kind == Kind::dense) &&
                np % (int64_t(kTile) * nranks) == 0;
     }
     int64_t h_rows() const { return shard_h() ? np / nranks : np; }
