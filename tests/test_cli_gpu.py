@@ -204,3 +204,26 @@ def test_gen_sparse_is_byte_identical_to_the_reference(gpu, tmp_path, ext):
     writer = oracle.ref.write_pdn1 if ext == "pdn1" else oracle.ref.write_mtx
     writer(tmp_path / f"r.{ext}", (rp, ci, v, shape))
     assert (tmp_path / f"s.{ext}").read_bytes() == (tmp_path / f"r.{ext}").read_bytes()
+
+
+@needs_ref
+def test_factorize_tcp_with_explicit_peers(gpu, tmp_path):
+    """--backend tcp --rank r --peers host:port: one process per rank started by the caller (the
+    multi-host form, oocnmf_cli.cpp:273-274), here two processes on two GPUs of this box."""
+    if nmf.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    a = _input(tmp_path, 640, 384, 4)
+    port = 20000 + os.getpid() % 20000
+    args = ["factorize", "--input", tmp_path / "a.pdn1", "--k", 4, "--eta", 0, "--max-iters", 30, "--workers", 2,
+            "--backend", "tcp", "--strategy", "rnmf", "--peers", f"127.0.0.1:{port}", "--out", tmp_path / "o"]
+    procs = []
+    for r in (0, 1):
+        env = dict(os.environ, OOCNMF_DEVICE=str(r))
+        procs.append(subprocess.Popen([CLI, *map(str, args), "--rank", str(r)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.PIPE, text=True, env=env))
+    outs = [p.communicate(timeout=300) for p in procs]
+    assert [p.returncode for p in procs] == [0, 0], outs
+    assert json.loads(outs[0][0].strip().splitlines()[-1])["iterations"] == 30
+    assert outs[1][0].strip() == "" or "final_error" not in outs[1][0]  # only rank 0 reports
+    ref = oracle.ref.nmf_distributed(a, 4, 2, strategy=2, max_iters=30, interval=10, eta=0.0, seed=0)
+    _check_outputs(tmp_path / "o", ref, 4, 30)
