@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "common.cuh"
 
@@ -75,6 +78,44 @@ int tc_drain_units();  // kernels_tc.cu: K steps per TMEM accumulation chain
 void plan_fused(FusedPlan& fp, int64_t mp, int64_t np, int num_sms, int lookahead);
 // L2 policies of the one-pass kernel's A loads (OOCNMF_FUSED_POL / _KEEP, defaults measured best)
 void fused_policies(FusedArgs& a);
+
+// kernels_nvls.cu: the sharded H update fused with its reduce-scatter and all-gather over NVLS
+// multicast (NCCL >= 2.28 symmetric memory). mc_* are multicast addresses of the symmetric
+// buffers, bar / ht this rank's local views.
+struct NvlsArgs {
+    const float* mc_wp;   // partial W^T A (np x kp), multicast
+    float* mc_ht;         // Ht (np x kp), multicast
+    unsigned* mc_bar;     // per-CTA barrier counters, multicast
+    const unsigned* bar;  // the same counters, local
+    const float* ht;      // Ht, local (the old rows)
+    const float* wtw;     // kp x kp W^T W (already all-reduced)
+    int* flag;
+    int64_t row0, rows;   // this rank's rows of H
+    unsigned epoch;       // launches so far on this group (the barrier phase)
+    int nranks;
+    float eps;
+    uint64_t timeout_ns;  // barrier spin limit (trap) for a peer that never arrives
+};
+bool nvls_compiled();
+// Symmetric buffers of one group (all ncclMemAlloc'd and registered as NCCL_WIN_COLL_SYMMETRIC
+// windows on every rank) and the device communicator with the lsa multicast mapping.
+struct NvlsState {
+    void* wp = nullptr;   // partial W^T A
+    void* ht = nullptr;   // Ht
+    void* bar = nullptr;  // barrier counters
+    size_t wp_bytes = 0, ht_bytes = 0, bar_bytes = 0;
+    void* win[3] = {};       // ncclWindow_t of wp, ht, bar
+    void* devcomm = nullptr; // ncclDevComm (heap)
+    void* mc[3] = {};        // multicast base addresses of wp, ht, bar
+    unsigned epoch = 0;
+};
+// Collective over comm (every rank, same sizes): allocate, zero, register, create the device
+// communicator, resolve the multicast addresses. On failure returns false with *why set and
+// leaves nothing allocated.
+bool nvls_setup(NvlsState& st, ncclComm_t comm, size_t wp_bytes, size_t ht_bytes, int nbar, cudaStream_t s,
+                std::string* why);
+void nvls_teardown(NvlsState& st, ncclComm_t comm);  // collective
+cudaError_t launch_h_update_nvls(int kp, const NvlsArgs& a, int grid, cudaStream_t s);
 cudaError_t launch_mu_fused(int kp, const FusedPlan& fp, const float* A, int64_t mp, int64_t np, const float* Ht_cat,
                             const FusedArgs& args, cudaStream_t s);
 

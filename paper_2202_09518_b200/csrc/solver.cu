@@ -87,10 +87,12 @@ struct DevBuf {
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
     ~DevBuf() { release(); }
+    bool external = false;  // storage owned elsewhere (the NVLS symmetric Ht): never cudaFree'd
     void release() {
-        if (p) cudaFree(p);
+        if (p && !external) cudaFree(p);
         p = nullptr;
         bytes = 0;
+        external = false;
     }
     void alloc(size_t b, const char* what) {
         if (b == bytes && p) return;
@@ -140,6 +142,11 @@ struct oocnmf_ctx {
     int segR_n = 0;
     bool no_check_next = false;  // the iteration being enqueued is not followed by an error check
     bool h_fused = false;        // ... and its H update ran inside the A^T W SpMM
+    // sharded CSR H update over NVLS multicast (kernels_nvls.cu, OOCNMF_NVLS=1): the A^T W SpMM
+    // writes this rank's partial W^T A into symmetric memory and one kernel reduces, updates and
+    // multicasts the rows; Ht itself lives in the symmetric buffer nv.ht while nvls_ready
+    NvlsState nv;
+    bool nvls_ready = false, nvls_failed = false, nvls_pending = false;
 
     uint64_t m = 0, n = 0, k = 0, row0 = 0, rows = 0;
     // Column partition (CNMF, src/nmf_distributed.cpp:112-149): this rank owns all m rows and
@@ -436,8 +443,11 @@ void spmm(oocnmf_ctx* c, bool transpose, const float* B, float* out, cudaStream_
               transpose ? "spmm At W (chunk)" : "spmm A Ht (chunk)");
 }
 
+void nvls_release(oocnmf_ctx* c);
+
 void alloc_factors(oocnmf_ctx* c) {
     const int kp = c->kp;
+    if (c->nvls_ready && c->nv.ht_bytes != size_t(c->np) * kp * 4) nvls_release(c);  // (collective: set_rank)
     c->W.alloc(size_t(c->mp) * kp * 4, "W");
     c->Ht.alloc(size_t(c->np) * kp * 4, "Ht");
     if (c->use_tc) {
@@ -687,6 +697,50 @@ bool fuse_w_update(const oocnmf_ctx* c) {
 // or the replicas of model selection) — on iterations not followed by an error check, whose
 // trace-form cross term <W^T A, H> needs the numerator the fused kernel never stores.
 // OOCNMF_FUSE_H=0 keeps the separate kernels.
+// ---- the NVLS sharded H update (kernels_nvls.cu) -------------------------------------------
+// CSR row partitions with a sharded H (shard_h) and a single-pass A^T W SpMM, from 4 ranks
+// (config 3 at N = 4: 292 vs 268 it/s; at N = 2, where multicast moves more bytes than a ring,
+// 183 vs 185.5). OOCNMF_NVLS=1 / 0 forces it on (from 2 ranks) / off.
+bool nvls_wanted(const oocnmf_ctx* c) {
+    static const int force = [] {
+        const char* e = std::getenv("OOCNMF_NVLS");
+        return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
+    }();
+    const bool want = force >= 0 ? force == 1 : c->nranks >= 4;
+    return want && !c->nvls_failed && nvls_compiled() && c->kind == Kind::csr && c->shard_h() && c->chT.C <= 1 &&
+           (c->kp == 16 || c->kp == 32 || c->kp == 64);
+}
+// Collective: every rank of the group reaches it in the same iteration. Moves Ht into the
+// symmetric buffer (the NCCL paths keep using it as plain device memory).
+void nvls_setup_ctx(oocnmf_ctx* c) {
+    std::string why;
+    const size_t bytes = size_t(c->np) * c->kp * 4;
+    if (!nvls_setup(c->nv, c->comm, bytes, bytes, c->num_sms, c->stream, &why)) {
+        c->nvls_failed = true;
+        if (c->rank == 0) std::fprintf(stderr, "[oocnmf] NVLS H update unavailable (%s): NCCL collectives\n", why.c_str());
+        return;
+    }
+    ck(cudaMemcpyAsync(c->nv.ht, c->Ht.p, bytes, cudaMemcpyDeviceToDevice, c->stream), "copy Ht");
+    ck(cudaStreamSynchronize(c->stream), "sync");
+    c->Ht.release();
+    c->Ht.p = c->nv.ht, c->Ht.bytes = bytes, c->Ht.external = true;
+    c->nvls_ready = true;
+}
+// Collective: back to a private Ht (contents kept) and the symmetric buffers released.
+void nvls_release(oocnmf_ctx* c) {
+    if (!c->nvls_ready) return;
+    cudaStreamSynchronize(c->stream);
+    void* keep = nullptr;
+    if (cudaMalloc(&keep, c->nv.ht_bytes) == cudaSuccess)
+        cudaMemcpy(keep, c->nv.ht, c->nv.ht_bytes, cudaMemcpyDeviceToDevice);
+    const size_t bytes = c->nv.ht_bytes;
+    c->Ht.release();  // external: not freed here
+    nvls_teardown(c->nv, c->comm);
+    c->Ht.p = keep, c->Ht.bytes = keep ? bytes : 0;
+    c->nvls_ready = c->nvls_pending = false;
+}
+bool nvls_use(const oocnmf_ctx* c) { return c->nvls_ready && c->no_check_next && nvls_wanted(c); }
+
 bool fuse_h_update(const oocnmf_ctx* c) {
     if (c->kind != Kind::csr || c->cnmf || c->collective() || c->chT.C > 1 || c->kp > 64) return false;
     const char* e = std::getenv("OOCNMF_FUSE_H");
@@ -851,6 +905,7 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         }
         rec(eReduced);
     } else if (c->kind == Kind::csr) {
+        if (!c->nvls_ready && nvls_wanted(c)) nvls_setup_ctx(c);
         if (c->ag_pending) {
             // H slices still arriving: the SpMM consumes them as they land, then the W update
             spmm_aht_sliced(c, s);
@@ -884,6 +939,10 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
                                     c->W.as<float>(), c->Ht.as<float>(), c->wtw(), eps, c->flag.as<int>(), s),
                   "spmm At W + H update");
             c->h_fused = true;
+        } else if (nvls_use(c)) {
+            // this rank's partial W^T A into symmetric memory; h_update reduces it over NVLS
+            spmm(c, true, c->W.as<float>(), static_cast<float*>(c->nv.wp), s);
+            c->nvls_pending = true;
         } else if (rs_chunks(c) > 1) {
             spmm_wta_reduce_scatter(c, s);
         } else {
@@ -940,6 +999,38 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     const int kp = c->kp;
     cudaStream_t s = c->stream;
     const int64_t hr = c->h_rows(), h0 = c->h_row0();
+    if (c->nvls_pending) {
+        // W^T W (f32 for the update, f64 for the trace-form error) over NCCL, then one kernel:
+        // reduce this rank's rows of W^T A over NVLS, update them, multicast the new rows
+        coll_begin(c, s);
+        nck(ncclGroupStart(), "ncclGroupStart");
+        ncc(c, ncclAllReduce(c->wtw(), c->wtw(), size_t(kp) * kp, ncclFloat, ncclSum, c->comm, s), "allreduce WtW");
+        ncc(c, ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
+            "allreduce WtW64");
+        ncc(c, ncclGroupEnd(), "ncclGroupEnd");
+        coll_end(c, s, kTagH, size_t(kp) * kp * 12);
+        if (timed) record(c, ev[eComm], s);
+        NvlsArgs a{};
+        a.mc_wp = static_cast<const float*>(c->nv.mc[0]);
+        a.mc_ht = static_cast<float*>(c->nv.mc[1]);
+        a.mc_bar = static_cast<unsigned*>(c->nv.mc[2]);
+        a.bar = static_cast<const unsigned*>(c->nv.bar);
+        a.ht = c->Ht.as<float>(), a.wtw = c->wtw(), a.flag = c->flag.as<int>();
+        a.row0 = h0, a.rows = hr, a.epoch = c->nv.epoch++, a.nranks = c->nranks, a.eps = eps;
+        // a peer that never arrives: the kernel traps after twice the group timeout (>= 30 s),
+        // after the watchdog has already raised CommError on the host
+        a.timeout_ns = uint64_t(std::max(30.0, 2.0 * c->comm_timeout) * 1e9);
+        coll_begin(c, s);
+        count(c, launch_h_update_nvls(kp, a, c->num_sms, s), "NVLS H update");
+        coll_end(c, s, kTagH, size_t(c->nranks) * hr * kp * 4 * 2);  // the reduce-scatter + all-gather it replaces
+        count(c, launch_factor_update(kp, c->Ht.as<float>() + h0 * kp, hr, nullptr, nullptr, nullptr, nullptr, eps,
+                                      false, c->gram_h.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
+              "H Gram");
+        finish_hht(c, hr, true);
+        c->nvls_pending = false;
+        if (timed) record(c, ev[eHdone], s);
+        return;
+    }
     if (c->shard_h()) {
         // reduce-scatter W^T A (each rank keeps its n/N rows, in place) + the small Grams; with
         // the overlapped SpMM the scatter is already on the comm stream
@@ -1928,6 +2019,7 @@ int oocnmf_ctx_destroy(oocnmf_ctx* c) {
         // the graphs hold NCCL work on c->comm: release them before the communicator
         for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
         c->graphs.clear();
+        if (c->nvls_ready && !c->poisoned) nvls_release(c);  // collective (all ranks destroy together)
         if (c->comm) ncclCommDestroy(c->comm);
         for (auto e : c->evs) cudaEventDestroy(e);
         for (auto& m : c->marks) c->ev_pool.push_back(m.beg), c->ev_pool.push_back(m.end);

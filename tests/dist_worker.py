@@ -39,8 +39,11 @@ def main(out_path):
         if host_slab is not None:
             (r0, r1), _ = plan.slabs[rank]
             slab = np.ascontiguousarray(host_slab[r0:r1])
+        comm.reset_stats()
         res = nmf.nmf_distributed(a, cfg, plan, comm, host_slab=slab, batch_rows=batch_rows)
+        h_calls = comm.stats().calls[nmf.PhaseTag.h_update]
         results[name] = {"trace": [e for _, e in res.error_trace], "iters": [i for i, _ in res.error_trace],
+                         "h_calls": h_calls,
                          "w_fro": float(np.linalg.norm(res.w)), "h_fro": float(np.linalg.norm(res.h)),
                          "w_sum": float(res.w.sum()), "h_sum": float(res.h.sum()),
                          "allreduce_s": res.counters.allreduce_s, "w_shape": list(res.w.shape)}

@@ -8,6 +8,7 @@ One rank per visible GPU (up to 4); on a one-GPU box the group is the loopback b
 import json
 import os
 import subprocess
+import sys
 
 import numpy as np
 import pytest
@@ -141,3 +142,47 @@ def test_file_source_over_budget_streams_out_of_core(gpu, tmp_path, dtype):
     assert sc.bytes_read == m * n * (4 if dtype == "f32" else 8) and sc.io_seconds > 0
     assert sc.peak_resident_bytes == 2 * 256 * 768 * 4 <= budget
     assert sc_mem.loads == 1 and sc_mem.peak_resident_bytes == m * 768 * 4
+
+
+_NVLS_THREADS = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle, paper_2202_09518_b200 as nmf
+workers = int(sys.argv[2])
+rp, ci, v, (m, n) = oracle.port.gen_sparse(1100, 2048, 0.02, 8)
+a = nmf.CsrMatrix(m, n, rp, ci, v.astype(np.float32).astype(np.float64))
+w0, h0 = oracle.port.init_factors(m, n, 16, 0)
+f32 = lambda x: np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+cfg = nmf.NmfConfig(k=16, max_iters=20, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                    init_w=f32(w0), init_h=f32(h0))
+stats = []
+res = nmf.run_distributed_threads(a, cfg, nmf.make_plan(m, n, 16, workers, 1, nmf.Strategy.rnmf), stats_out=stats)
+print(json.dumps({"trace": [[e for _, e in r.error_trace] for r in res],
+                  "w": [float(np.linalg.norm(r.w)) for r in res], "h": [float(np.linalg.norm(r.h)) for r in res],
+                  "h_calls": stats[0].calls[nmf.PhaseTag.h_update]}))
+"""
+
+
+@pytest.mark.parametrize("nvls", ["1", "0"])
+def test_threads_backend_sharded_csr_nvls(gpu, nvls):
+    """The sharded CSR H update over the threads backend (one process, ncclCommInitAll), with the
+    NVLS kernel (kernels_nvls.cu) forced on and off: both match the oracle's row-partitioned run."""
+    workers = _workers()
+    if workers < 2:
+        pytest.skip("needs >= 2 GPUs")
+    env = dict(os.environ, OOCNMF_NVLS=nvls)
+    out = subprocess.run([sys.executable, "-c", _NVLS_THREADS, ROOT, str(workers)], capture_output=True, text=True,
+                         env=env, timeout=300)
+    assert out.returncode == 0, out.stderr[-2000:]
+    d = json.loads(out.stdout.strip().splitlines()[-1])
+    rp, ci, v, shape = port.gen_sparse(1100, 2048, 0.02, 8)
+    w0, h0 = port.init_factors(1100, 2048, 16, 0)
+    ref = port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), workers, 1, max_iters=20, interval=10)
+    for tr in d["trace"]:
+        np.testing.assert_allclose(tr, ref.trace_err, rtol=1e-4)
+    assert d["w"][0] == pytest.approx(np.linalg.norm(ref.w), rel=1e-3)
+    assert d["h"][0] == pytest.approx(np.linalg.norm(ref.h), rel=1e-3)
+    # NVLS: 2 h_update collectives on the 18 non-check iterations (W^T W + the fused kernel) and
+    # the NCCL path's 6 (4 reduce-scatter chunks, W^T W, all-gather) on the 2 check iterations
+    assert d["h_calls"] == (18 * 2 + 2 * 6 if nvls == "1" else 20 * 6)

@@ -63,6 +63,23 @@ def dist_results_optin(tmp_path_factory):
     return world, json.load(open(out))
 
 
+@pytest.fixture(scope="module")
+def dist_results_nvls(tmp_path_factory):
+    """OOCNMF_NVLS=1: the sharded CSR H update as one kernel over NVLS multicast
+    (kernels_nvls.cu: reduce-scatter, update, all-gather fused)."""
+    n = nmf.device_count()
+    if n < 2:
+        pytest.skip("needs >= 2 GPUs")
+    world = min(n, 4)
+    out = tmp_path_factory.mktemp("dist_nvls") / "r.json"
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "dist_worker.py"),
+           str(out)]
+    env = dict(os.environ, OOCNMF_NVLS="1")
+    subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env)
+    return world, json.load(open(out))
+
+
 def _check(r, ref, tol=1e-4):
     assert r["iters"] == ref.trace_iters.tolist()
     rel = np.max(np.abs(np.array(r["trace"]) - ref.trace_err) / ref.trace_err)
@@ -163,6 +180,21 @@ def test_csr_h_broadcast_overlap_matches_oracle(dist_results_optin):
     w0, h0 = oracle.port.init_factors(1100, 2048, 16, 0)
     ref = oracle.port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
     _check(res["csr_shard_k16"], ref)
+
+
+def test_csr_nvls_h_update_matches_oracle(dist_results, dist_results_nvls):
+    world, res = dist_results_nvls
+    rp, ci, v, shape = oracle.port.gen_sparse(1100, 2048, 0.02, 8)
+    w0, h0 = oracle.port.init_factors(1100, 2048, 16, 0)
+    ref = oracle.port.nmf_rnmf((rp, ci, f32(v), shape), 16, f32(w0), f32(h0), world, 1, max_iters=20, interval=10)
+    _check(res["csr_shard_k16"], ref)
+    # the NVLS kernel replaced the reduce-scatter (4 chunks) + all-gather on the 18 non-check
+    # iterations: 2 h_update collectives there (the W^T W all-reduce and the kernel), 6 on the 2
+    # check iterations (NCCL path)
+    assert res["csr_shard_k16"]["h_calls"] == 18 * 2 + 2 * 6
+    # everything else unchanged
+    for name in ("dense_k16", "csr_k16", "cnmf_csr_k16"):
+        assert res[name]["trace"] == pytest.approx(dist_results[1][name]["trace"], rel=1e-6)
 
 
 def test_dead_rank_raises_comm_error(tmp_path):
