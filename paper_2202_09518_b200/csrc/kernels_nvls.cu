@@ -21,6 +21,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "common.cuh"
@@ -74,9 +75,9 @@ __device__ __forceinline__ void mc_st4(float* p, const float (&v)[4]) {
 }
 
 // KP / 4 lanes per row, each owning 4 columns; U rows per lane group in flight.
-template <int KP>
+template <int KP, int U>
 __global__ void __launch_bounds__(256) k_h_update_nvls(NvlsArgs a) {
-    constexpr int L = KP / 4, RPW = 32 / L, U = 2;
+    constexpr int L = KP / 4, RPW = 32 / L;
     __shared__ float wtw[KP * KP];
     const unsigned tgt = unsigned(a.nranks) * (2u * a.epoch + 1u);
     mc_barrier(a.mc_bar + blockIdx.x, a.bar + blockIdx.x, tgt, a.timeout_ns);
@@ -213,10 +214,17 @@ void nvls_teardown(NvlsState& st, ncclComm_t comm) {
 }
 
 cudaError_t launch_h_update_nvls(int kp, const NvlsArgs& a, int grid, cudaStream_t s) {
-    switch (kp) {
-        case 16: k_h_update_nvls<16><<<grid, 256, 0, s>>>(a); break;
-        case 32: k_h_update_nvls<32><<<grid, 256, 0, s>>>(a); break;
-        case 64: k_h_update_nvls<64><<<grid, 256, 0, s>>>(a); break;
+    static const int u = [] {  // developer knob: rows in flight per lane group (2 or 4)
+        const char* e = std::getenv("OOCNMF_NVLS_U");
+        return e && e[0] == '4' ? 4 : 2;
+    }();
+    switch (kp * 10 + u) {
+        case 162: k_h_update_nvls<16, 2><<<grid, 256, 0, s>>>(a); break;
+        case 322: k_h_update_nvls<32, 2><<<grid, 256, 0, s>>>(a); break;
+        case 642: k_h_update_nvls<64, 2><<<grid, 256, 0, s>>>(a); break;
+        case 164: k_h_update_nvls<16, 4><<<grid, 256, 0, s>>>(a); break;
+        case 324: k_h_update_nvls<32, 4><<<grid, 256, 0, s>>>(a); break;
+        case 644: k_h_update_nvls<64, 4><<<grid, 256, 0, s>>>(a); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();

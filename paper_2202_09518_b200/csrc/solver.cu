@@ -715,7 +715,7 @@ bool nvls_wanted(const oocnmf_ctx* c) {
 void nvls_setup_ctx(oocnmf_ctx* c) {
     std::string why;
     const size_t bytes = size_t(c->np) * c->kp * 4;
-    if (!nvls_setup(c->nv, c->comm, bytes, bytes, c->num_sms, c->stream, &why)) {
+    if (!nvls_setup(c->nv, c->comm, bytes, bytes, c->num_sms * 8, c->stream, &why)) {
         c->nvls_failed = true;
         if (c->rank == 0) std::fprintf(stderr, "[oocnmf] NVLS H update unavailable (%s): NCCL collectives\n", why.c_str());
         return;
@@ -1021,7 +1021,8 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         // after the watchdog has already raised CommError on the host
         a.timeout_ns = uint64_t(std::max(30.0, 2.0 * c->comm_timeout) * 1e9);
         coll_begin(c, s);
-        count(c, launch_h_update_nvls(kp, a, c->num_sms, s), "NVLS H update");
+        static const int ctas_per_sm = std::clamp(env_int("OOCNMF_NVLS_CTAS", 1), 1, 8);  // developer knob
+        count(c, launch_h_update_nvls(kp, a, c->num_sms * ctas_per_sm, s), "NVLS H update");
         coll_end(c, s, kTagH, size_t(c->nranks) * hr * kp * 4 * 2);  // the reduce-scatter + all-gather it replaces
         count(c, launch_factor_update(kp, c->Ht.as<float>() + h0 * kp, hr, nullptr, nullptr, nullptr, nullptr, eps,
                                       false, c->gram_h.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
