@@ -234,14 +234,22 @@ struct oocnmf_ctx {
     // Dense RNMF can do the same (OOCNMF_SHARD_H=1); W^T A is only 8.4 MB at config 2, and the
     // all-reduce + replicated H update measured faster (649 vs 607 it/s at N = 4), so it is off.
     // OOCNMF_SHARD_H=1 / 0 forces the sharded / replicated H update for both kinds.
+    // Dense: only with the NVLS H update on the one-pass path (OOCNMF_NVLS=1), which needs it.
     bool shard_h() const {
         static const int force = [] {  // dense measured slower at N = 4 (607 vs 649 it/s): off by default
             const char* e = std::getenv("OOCNMF_SHARD_H");
             return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
         }();
-        const bool want = force >= 0 ? force == 1 : kind == Kind::csr;
+        const bool want = force >= 0 ? force == 1 : (kind == Kind::csr || dense_nvls());
         return collective() && !cnmf && want && (kind == Kind::csr || kind == Kind::dense) &&
                np % (int64_t(kTile) * nranks) == 0;
+    }
+    bool dense_nvls() const {
+        static const bool on = [] {
+            const char* e = std::getenv("OOCNMF_NVLS");
+            return e && e[0] == '1';
+        }();
+        return on && kind == Kind::dense && use_fused && nvls_compiled();
     }
     int64_t h_rows() const { return shard_h() ? np / nranks : np; }
     int64_t h_row0() const { return shard_h() ? h_rows() * rank : 0; }
@@ -707,7 +715,8 @@ bool nvls_wanted(const oocnmf_ctx* c) {
         return e && (e[0] == '0' || e[0] == '1') ? e[0] - '0' : -1;
     }();
     const bool want = force >= 0 ? force == 1 : c->nranks >= 4;
-    return want && !c->nvls_failed && nvls_compiled() && c->kind == Kind::csr && c->shard_h() && c->chT.C <= 1 &&
+    const bool path = c->kind == Kind::csr ? c->chT.C <= 1 : (c->kind == Kind::dense && c->use_fused);
+    return want && !c->nvls_failed && nvls_compiled() && path && c->shard_h() &&
            (c->kp == 16 || c->kp == 32 || c->kp == 64);
 }
 // Collective: every rank of the group reaches it in the same iteration. Moves Ht into the
@@ -846,6 +855,8 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
     if (c->kind == Kind::dense && c->use_fused) {
         // one pass over A: P1, the W update and P2 (W^T A of the new W) in one kernel; then the
         // Gram of the new W
+        if (!c->nvls_ready && nvls_wanted(c)) nvls_setup_ctx(c);
+        const bool nvls = nvls_use(c);  // W^T A into symmetric memory for the NVLS H update
         const FusedPlan& fp = c->fplan;
         ck(cudaMemsetAsync(c->fz_count.p, 0, c->fz_count.bytes, s), "memset fused counters");
         const int* idx = c->fz_idx.as<int>();
@@ -857,7 +868,8 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         a.p1slots = c->fz_slots.as<float>();
         a.count = c->fz_count.as<unsigned>(), a.wdone = a.count + fp.NB;
         a.W = c->W.as<float>(), a.Wcat = c->W_cat.as<float>(), a.HHt = c->HHt.as<float>();
-        a.eps = eps, a.flag = c->flag.as<int>(), a.wta = c->wta();
+        a.eps = eps, a.flag = c->flag.as<int>(), a.wta = nvls ? static_cast<float*>(c->nv.wp) : c->wta();
+        c->nvls_pending = nvls;
         fused_policies(a);
         count(c, launch_mu_fused(kp, fp, c->A.as<float>(), c->mp, c->np, c->Ht_cat.as<float>(), a, s), "mu fused");
         rec(eAht);
@@ -1024,6 +1036,7 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         static const int ctas_per_sm = std::clamp(env_int("OOCNMF_NVLS_CTAS", 1), 1, 8);  // developer knob
         count(c, launch_h_update_nvls(kp, a, c->num_sms * ctas_per_sm, s), "NVLS H update");
         coll_end(c, s, kTagH, size_t(c->nranks) * hr * kp * 4 * 2);  // the reduce-scatter + all-gather it replaces
+        if (float* hc = htlo(c)) count(c, launch_split_cat(c->Ht.as<float>(), hc, c->np, kp, s), "split H");
         count(c, launch_factor_update(kp, c->Ht.as<float>() + h0 * kp, hr, nullptr, nullptr, nullptr, nullptr, eps,
                                       false, c->gram_h.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
               "H Gram");

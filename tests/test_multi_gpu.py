@@ -75,7 +75,9 @@ def dist_results_nvls(tmp_path_factory):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "dist_worker.py"),
            str(out)]
-    env = dict(os.environ, OOCNMF_NVLS="1")
+    # (OOCNMF_FUSED=1: the dense runs take the one-pass kernel at these small shapes, so the
+    # dense NVLS H update is exercised too)
+    env = dict(os.environ, OOCNMF_NVLS="1", OOCNMF_FUSED="1")
     subprocess.run(cmd, check=True, timeout=600, cwd=ROOT, env=env)
     return world, json.load(open(out))
 
@@ -182,7 +184,7 @@ def test_csr_h_broadcast_overlap_matches_oracle(dist_results_optin):
     _check(res["csr_shard_k16"], ref)
 
 
-def test_csr_nvls_h_update_matches_oracle(dist_results, dist_results_nvls):
+def test_nvls_h_update_matches_oracle(dist_results, dist_results_nvls):
     world, res = dist_results_nvls
     rp, ci, v, shape = oracle.port.gen_sparse(1100, 2048, 0.02, 8)
     w0, h0 = oracle.port.init_factors(1100, 2048, 16, 0)
@@ -192,8 +194,14 @@ def test_csr_nvls_h_update_matches_oracle(dist_results, dist_results_nvls):
     # iterations: 2 h_update collectives there (the W^T W all-reduce and the kernel), 6 on the 2
     # check iterations (NCCL path)
     assert res["csr_shard_k16"]["h_calls"] == 18 * 2 + 2 * 6
-    # everything else unchanged
-    for name in ("dense_k16", "csr_k16", "cnmf_csr_k16"):
+    # the dense one-pass kernel writing W^T A into symmetric memory + the NVLS H update (and
+    # the split of the gathered H into [H | H_lo] for the next pass)
+    a = f32(oracle.port.uniform_dense(1100, 900, 42, 99))
+    for name, k in (("dense_k16", 16), ("dense_k32", 32)):
+        w0, h0 = oracle.port.init_factors(1100, 900, k, 0)
+        _check(res[name], oracle.port.nmf_rnmf(a, k, f32(w0), f32(h0), world, 1, max_iters=30, interval=10))
+    # paths without a sharded H are unchanged
+    for name in ("csr_k16", "cnmf_csr_k16"):
         assert res[name]["trace"] == pytest.approx(dist_results[1][name]["trace"], rel=1e-6)
 
 
