@@ -7,7 +7,9 @@ HBM roofline).
 
 A "step" is one MU iteration (W update then H update; error every 10 iterations as the
 reference default). Default workload = config 2: synthetic dense 65536 x 65536 f32 A, k = 32,
-row-partitioned over N GPUs (strong scaling), one JSON line on rank 0.
+row-partitioned over N GPUs (strong scaling), one JSON line on rank 0; at N > 1 the line also
+carries a "weak" sub-record (65536 rows per GPU, m = N x 65536: the north star's weak-scaling
+target) and --scaling weak makes that the main measurement.
   --workload sparse : config 3, CSR 2^22 x 2^22, density 1e-5 (reference generator), k = 32
   --workload ooc    : config 4 (scaled to this host's RAM): A in pinned host memory, streamed
                       over the host link every iteration, k = 64
@@ -70,7 +72,10 @@ def parse():
     p.add_argument("--no-e2e-f64", action="store_true", help="skip the reference-shaped f64 pageable e2e run")
     p.add_argument("--no-sparse", action="store_true", help="dense workload: skip the config-3 sub-record")
     p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
-                   help="weak: m = N x --m rows (a fixed slab per GPU)")
+                   help="strong (default): the same m at every N (value = whole-job it/s, ideally N x); "
+                        "weak: m = N x --m rows (a fixed slab per GPU)")
+    p.add_argument("--no-weak", action="store_true",
+                   help="N > 1, strong: skip the weak-scaling sub-record of the dense line")
     p.add_argument("--ref-sample", action="store_true",
                    help="--impl reference: time a 1024-row sample instead of the full workload")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -420,7 +425,7 @@ def bench_select(args, nmf, np, torch, ctx, comm, rank, world, local, barrier, m
         comm.close()
 
 
-def reference_arm(args, rank, K, W, k):
+def reference_arm(args, rank, K, W, k, world=1):
     """--impl reference: the reference's own CPU solver (oracle/_ref) on this box's host cores.
 
     dense (default): the SAME configuration as our arm — the full 65536 x 65536 A (f64, the
@@ -430,7 +435,11 @@ def reference_arm(args, rank, K, W, k):
     f64 A (or --ref-sample is given) it falls back to the row-sample extrapolation."""
     if rank != 0:
         return
-    m, n = args.m or 65536, args.n
+    if world > 1 and os.environ.get("OMP_NUM_THREADS") == "1":
+        # torchrun pins OMP_NUM_THREADS=1 per process; rank 0 alone runs the reference here, with
+        # every host core as at N = 1 (set before the OpenMP runtime of oracle/_ref loads)
+        os.environ["OMP_NUM_THREADS"] = str(CPU_CORES)
+    m, n = (args.m or 65536) * (world if args.scaling == "weak" else 1), args.n
     if args.workload != "dense":
         emit({"impl": "reference", "unavailable": "--impl reference implemented for the default (dense) workload only"})
         return
@@ -444,7 +453,9 @@ def reference_arm(args, rank, K, W, k):
         ram = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_AVPHYS_PAGES")
     except (ValueError, OSError):
         ram = 0
-    full = not args.ref_sample and kind == "reference" and m * n * 8 < 0.8 * ram
+    # the full same-config run at N = 1 (the headline ratio); under torchrun (N > 1, where weak
+    # scaling makes A N times larger) the bounded row-sample fit keeps the arm within minutes
+    full = not args.ref_sample and world == 1 and kind == "reference" and m * n * 8 < 0.8 * ram
     if full:
         import oracle
 
@@ -502,7 +513,7 @@ def main():
     K, W, k = args.steps, max(3, args.warmup), args.k
 
     if args.impl == "reference":
-        return reference_arm(args, rank, K, W, k)
+        return reference_arm(args, rank, K, W, k, world)
 
     import numpy as np
     import torch
@@ -541,6 +552,18 @@ def main():
     env = dict(nmf=nmf, np=np, torch=torch, ctx=ctx, rank=rank, world=world, local=local, barrier=barrier,
                max_over_ranks=max_over_ranks, sum_over_ranks=sum_over_ranks)
     out = run_workload(args, args.workload, args.m, args.n, k, K, W, env)
+    if args.workload == "dense" and world > 1 and args.scaling == "strong" and not args.no_weak:
+        # the north star's multi-GPU target is weak scaling: the same line also times a fixed
+        # 65536-row slab per GPU (m = N x 65536; device-timed only). Its value is the whole job's
+        # it/s, so weak-scaling efficiency = weak.value / value at N = 1.
+        import copy
+
+        wa = copy.copy(args)
+        wa.scaling, wa.no_e2e, wa.no_cpu_baseline = "weak", True, True
+        wk = run_workload(wa, "dense", args.m, args.n, k, K, W, env)
+        if out is not None and wk is not None:
+            out["weak"] = {key: wk[key] for key in ("value", "unit", "ms_per_step", "scaling", "config", "roofline",
+                                                    "gpu_launches") if key in wk}
     # BASELINE.json's metric is "dense+sparse": the default dense line carries config 3 too
     if args.workload == "dense" and not args.no_sparse:
         if comm is None:
