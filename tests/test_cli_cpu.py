@@ -137,3 +137,19 @@ def test_selection_report_json_and_csv_are_the_reference_bytes(json_demo, chosen
     ref_js, ref_csv = oracle.ref.selection_json_csv(recs, chosen, why)
     assert js == ref_js
     assert csv == ref_csv
+
+
+@needs_ref
+def test_tcp_backend_argument_errors(tmp_path):
+    """--backend tcp without peers, and a malformed endpoint (connect_tcp, comm.hpp:84-87): usage
+    errors (exit 2) raised before any device or socket work."""
+    oracle.ref.write_pdn1(tmp_path / "a.pdn1", np.arange(1, 61, dtype=np.float64).reshape(6, 10))
+    base = ["factorize", "--input", tmp_path / "a.pdn1", "--k", 2, "--workers", 2, "--backend", "tcp"]
+    r = run(*base)
+    assert r.returncode == 2
+    assert json.loads(r.stderr)["error"] == {"message": "--backend tcp needs --peers or --spawn-local", "type": "usage"}
+    r = run(*base, "--rank", 1, "--peers", "no-port-here")
+    assert r.returncode == 2
+    assert json.loads(r.stderr)["error"]["message"] == "endpoint must be host:port, got no-port-here"
+    r = run(*base, "--rank", 5, "--peers", "127.0.0.1:1")
+    assert r.returncode == 2 and json.loads(r.stderr)["error"]["message"] == "tcp rank out of range"
