@@ -57,6 +57,16 @@ def main(out_path):
     rp3, ci3, v3, (m3, n3) = port.gen_sparse(1100, 2048, 0.02, 8)
     run("csr_shard_k16", nmf.CsrMatrix(m3, n3, rp3, ci3, f32(v3)), m3, n3, 16, 20, 10)
     run("ooc_k32", None, 1100, 900, 32, 20, 10, host_slab=a, batch_rows=128)
+    # config 3 scaled (2^15 x 2^15, density 4e-3, the reference generator on this rank's GPU)
+    # against the compiled reference's serial run (tests/golden): the sharded H update over
+    # NCCL, or over NVLS multicast from 4 ranks / with OOCNMF_NVLS=1
+    g3 = np.load(os.path.join(ROOT, "tests", "golden", "csr_config3_scaled_32768_d4e-3_k32.npz"))
+    m3g, n3g, seed3 = g3["gen"].tolist()
+    with nmf.Context(local) as gctx:
+        gctx.set_problem(m3g, n3g, 32)
+        gctx.generate_csr_uniform(float(g3["density"]), seed3)
+        c3 = gctx.download_csr()
+    run("csr_cfg3_k32", c3, m3g, n3g, 32, int(g3["iters"]), int(g3["interval"]))
     # column partition (CNMF) on wide inputs: W replicated, H column slabs
     wide = port.uniform_dense(700, 1300, 7, 99).astype(np.float32)
     run("cnmf_dense_k16", wide, 700, 1300, 16, 30, 10, strategy=nmf.Strategy.cnmf)

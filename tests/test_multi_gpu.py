@@ -167,6 +167,20 @@ def test_csr_sharded_h_update_matches_oracle(dist_results):
     _check(res["csr_shard_k16"], ref)
 
 
+def _check_cfg3(r):
+    g = np.load(os.path.join(ROOT, "tests", "golden", "csr_config3_scaled_32768_d4e-3_k32.npz"))
+    assert r["iters"] == g["trace_iters"].tolist()
+    assert np.max(np.abs(np.array(r["trace"]) - g["trace_err"]) / g["trace_err"]) <= 1e-4
+    assert r["w_fro"] == pytest.approx(float(g["w_fro"]), rel=1e-3)
+    assert r["h_fro"] == pytest.approx(float(g["h_fro"]), rel=1e-3)
+
+
+def test_csr_config3_scaled_matches_reference(dist_results):
+    """Config 3 scaled (2^15 square, density 4e-3, k = 32) row-partitioned over the GPUs with the
+    sharded H update, against the compiled reference's serial run (golden fixture)."""
+    _check_cfg3(dist_results[1]["csr_cfg3_k32"])
+
+
 @pytest.mark.parametrize("name,k", [("dense_k16", 16), ("dense_k32", 32)])
 def test_dense_sharded_h_update_matches_oracle(dist_results_optin, name, k):
     world, res = dist_results_optin
@@ -200,6 +214,7 @@ def test_nvls_h_update_matches_oracle(dist_results, dist_results_nvls):
     for name, k in (("dense_k16", 16), ("dense_k32", 32)):
         w0, h0 = oracle.port.init_factors(1100, 900, k, 0)
         _check(res[name], oracle.port.nmf_rnmf(a, k, f32(w0), f32(h0), world, 1, max_iters=30, interval=10))
+    _check_cfg3(res["csr_cfg3_k32"])  # the config-3-like density through the NVLS kernel
     # paths without a sharded H are unchanged
     for name in ("csr_k16", "cnmf_csr_k16"):
         assert res[name]["trace"] == pytest.approx(dist_results[1][name]["trace"], rel=1e-6)
