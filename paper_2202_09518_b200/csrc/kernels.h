@@ -72,6 +72,7 @@ struct FusedPlan {
     std::vector<int> q0, t0, act;
 };
 bool fused_supported(int kp, int64_t mp, int64_t np, int num_sms);
+size_t fused_slot_bytes(int kp, const FusedPlan& fp);  // the P1 slot ring (rows padded to 128 B)
 namespace tc {
 int tc_drain_units();  // kernels_tc.cu: K steps per TMEM accumulation chain
 }

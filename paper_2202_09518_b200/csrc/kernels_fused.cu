@@ -56,6 +56,7 @@ struct FzCfg {
     static_assert(ASLOTS >= 2, "TMEM budget");
     static constexpr int TMEM_COLS = 512;
     static constexpr int MAX_G = 192;                  // CTAs (smem list of P1 publishers)
+    static constexpr int RS = KP < 32 ? 32 : KP;       // P1 slot row stride: a whole 128-byte line
     static constexpr size_t RING_BYTES = size_t(A_STAGES) * A_BYTES + size_t(B_STAGES) * B_BYTES;
     static constexpr size_t BAR_BYTES = 512;
     // updater gather buffer: one row of every CTA's published P1 partial (TMA, G x kp floats)
@@ -320,6 +321,17 @@ __global__ void __launch_bounds__(512, 1)
             FZ_WAIT(10, mbar_wait(gbar, gph));
             gph ^= 1u;
             if (lane == 0) FZ_TRACE(4, b, row);
+#ifndef OOC_FZ_KEEP_SLOTS
+            {
+                // The gathered partials are dead (their slot is rewritten NS blocks later, after
+                // this row's W-ready release): drop the G dirty lines (one per CTA: slot rows are
+                // a whole 128-byte line) from L2 instead of letting the A stream evict them to HBM
+                // (≈ 1.2 GB of writes per iteration at config 2).
+                const float* sb = p.p1slots + (int64_t(b % p.NS) * G) * (128 * C::RS) + row * C::RS;
+                for (int c = lane; c < G; c += 32)
+                    asm volatile("discard.global.L2 [%0], 128;" ::"l"(sb + int64_t(c) * 128 * C::RS) : "memory");
+            }
+#endif
             // four interleaved partial sums (CTAs c = c_lo + 4 i + l), combined in a fixed order:
             // deterministic, and a quarter of the dependent-add chain of one running sum
             float s4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -450,7 +462,7 @@ __global__ void __launch_bounds__(512, 1)
                     if (close) cu = 0, take();
                 }
                 // publish this CTA's partial of block s: row t
-                float* out = p.p1slots + (int64_t(s % p.NS) * G + cta) * (128 * KP) + t * KP;
+                float* out = p.p1slots + (int64_t(s % p.NS) * G + cta) * (128 * C::RS) + t * C::RS;
 #pragma unroll
                 for (int j4 = 0; j4 < KP / 4; ++j4) {
                     __stcg(reinterpret_cast<float4*>(out) + j4,
@@ -542,7 +554,7 @@ cudaError_t launch_fused_t(const FusedPlan& fp, const float* A, int64_t mp, int6
         auto fn = encode_fn();
         if (!fn) return cudaErrorNotSupported;
         const cuuint64_t dims[3] = {cuuint64_t(KP), 128u, cuuint64_t(fp.NS) * fp.G};
-        const cuuint64_t strides[2] = {cuuint64_t(KP) * 4, cuuint64_t(128) * KP * 4};
+        const cuuint64_t strides[2] = {cuuint64_t(C::RS) * 4, cuuint64_t(128) * C::RS * 4};
         const cuuint32_t box[3] = {cuuint32_t(KP), 1u, cuuint32_t(fp.G)};
         const cuuint32_t estr[3] = {1u, 1u, 1u};
         if (fn(&sm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, args.p1slots, dims, strides, box, estr,
@@ -567,6 +579,10 @@ cudaError_t launch_fused_t(const FusedPlan& fp, const float* A, int64_t mp, int6
 }
 
 }  // namespace
+
+size_t fused_slot_bytes(int kp, const FusedPlan& fp) {
+    return size_t(fp.NS) * fp.G * 128 * size_t(kp < 32 ? 32 : kp) * 4;
+}
 
 bool fused_supported(int kp, int64_t mp, int64_t np, int num_sms) {
     if (!(kp == 16 || kp == 32) || !tc_supported(kp)) return false;

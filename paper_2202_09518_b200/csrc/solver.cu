@@ -523,7 +523,7 @@ void plan_fused_buffers(oocnmf_ctx* c) {
     idx.insert(idx.end(), fp.act.begin(), fp.act.end());
     c->fz_idx.alloc(idx.size() * 4, "fused plan");
     ck(cudaMemcpy(c->fz_idx.p, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice), "H2D fused plan");
-    c->fz_slots.alloc(size_t(fp.NS) * fp.G * kTile * c->kp * 4, "fused P1 slots");
+    c->fz_slots.alloc(fused_slot_bytes(c->kp, fp), "fused P1 slots");
     // CTAs without P1 work never publish: their slots must read as zeros in the updaters' gather
     ck(cudaMemsetAsync(c->fz_slots.p, 0, c->fz_slots.bytes, c->stream), "memset fused slots");
     c->fz_count.alloc(size_t(3) * fp.NB * 4, "fused counters");  // count[NB] | wdone[2 NB]

@@ -74,8 +74,8 @@ int main(int argc, char** argv) {
     h.insert(h.end(), fp.act.begin(), fp.act.end());
     CK(cudaMalloc(&idx, h.size() * 4));
     CK(cudaMemcpy(idx, h.data(), h.size() * 4, cudaMemcpyHostToDevice));
-    CK(cudaMalloc(&slots, size_t(fp.NS) * fp.G * 128 * kp * 4));
-    CK(cudaMemset(slots, 0, size_t(fp.NS) * fp.G * 128 * kp * 4));
+    CK(cudaMalloc(&slots, fused_slot_bytes(kp, fp)));
+    CK(cudaMemset(slots, 0, fused_slot_bytes(kp, fp)));
     CK(cudaMalloc(&cnt, size_t(3) * fp.NB * 4));
     FusedArgs a{};
     a.NB = fp.NB, a.D = fp.D, a.NS = fp.NS, a.G1 = fp.G1, a.drain_units = du;
