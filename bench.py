@@ -19,6 +19,7 @@ target) and --scaling weak makes that the main measurement.
 iteration per step on a bounded row sample, extrapolated to the full matrix.
 """
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -766,6 +767,10 @@ def e2e_runs(args, workload, m, n, k, K, rows, r0, kp, env):
 
     def one(a_host, use_comm_ctx):
         ph = {}
+        # Python's cyclic GC freeing earlier multi-GB arrays (munmap) must not land inside a
+        # phase: collect now, pause it for the timed call (re-enabled in e2e_runs)
+        gc.collect()
+        gc.disable()
         barrier()
         t0 = time.perf_counter()
         t = t0
@@ -802,6 +807,7 @@ def e2e_runs(args, workload, m, n, k, K, rows, r0, kp, env):
     try:
         total, ph = one(host, world > 1)
     finally:
+        gc.enable()
         if pinned:
             nmf._capi.lib().oocnmf_host_unregister(host.ctypes.data)
     e2e = {"value": K / total, "unit": "it/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
@@ -812,7 +818,10 @@ def e2e_runs(args, workload, m, n, k, K, rows, r0, kp, env):
     if workload == "dense" and world == 1 and not args.no_e2e_f64:
         a64 = host.astype(np.float64)
         del host
-        t64, ph64 = one(a64, False)
+        try:
+            t64, ph64 = one(a64, False)
+        finally:
+            gc.enable()
         e2e["reference_shaped"] = {"value": K / t64, "unit": "it/s", "h2d_bytes_per_step": a64.nbytes / K,
                                    "d2h_bytes_per_step": d2h / K, "phases_s": ph64, "total_s": t64,
                                    "note": "f64 pageable row-major A as a reference caller holds it "
