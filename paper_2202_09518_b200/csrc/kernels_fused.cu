@@ -233,16 +233,15 @@ __global__ void __launch_bounds__(512, 1)
                     FZ_WAIT(2, wait_count(p.wdone + 2 * (s - D), 64u));
                     FZ_WAIT(2, wait_count(p.wdone + 2 * (s - D) + 1, 64u));
                 } else if (s >= D) {
+                    // the two 64-row halves once per block: the MMA reuses them for every
+                    // owned tile (one 16 KB TMA load per half instead of one per tile)
                     const int b = s - D;
-                    for (int j = t0; j < t1; ++j)
-                        for (int h = 0; h < 2; ++h) {
-                            if (j == t0) {
-                                FZ_WAIT(2, wait_count(p.wdone + 2 * b + h, 64u));
-                                fence_proxy_async_global();
-                                if (h == 0) FZ_TRACE(3, b, cta);
-                            }
-                            load_b(&tmB2, b * 128 + 64 * h, kEvictNormal);
-                        }
+                    for (int h = 0; h < 2; ++h) {
+                        FZ_WAIT(2, wait_count(p.wdone + 2 * b + h, 64u));
+                        fence_proxy_async_global();
+                        if (h == 0) FZ_TRACE(3, b, cta);
+                        load_b(&tmB2, b * 128 + 64 * h, kEvictNormal);
+                    }
                 }
             };
             for (int s = 0; s < NB + D; ++s) p.p2_first ? (p2(s), p1(s)) : (p1(s), p2(s));
@@ -252,13 +251,15 @@ __global__ void __launch_bounds__(512, 1)
         int sb = 0, r = 0, buf = 0;
         uint32_t phb = 0, rph = 0, aph = 0;
         bool open = true;
-        auto unit = [&](bool close) {
+        // one unit on B stage st: wait for it to fill (wait_b) and release it when its MMAs
+        // are done (release_b); P2 holds a block's two W stages across all its tiles
+        auto unit_on = [&](bool close, int st, uint32_t ph, bool wait_b, bool release_b) {
             if (open) FZ_WAIT(5, mbar_wait(accempty + buf, aph ^ 1u));
-            FZ_WAIT(6, mbar_wait(fullB + sb, phb));
+            if (wait_b) FZ_WAIT(6, mbar_wait(fullB + st, ph));
             FZ_WAIT(7, mbar_wait(split + r, rph));
             tc_fence_after();
             const uint32_t d = tmem + uint32_t(buf * C::ACC_COLS);
-            const uint64_t db0 = desc_mnmajor(smem_u32(b_stage(sb)), 0, C::ATOM_STRIDE);
+            const uint64_t db0 = desc_mnmajor(smem_u32(b_stage(st)), 0, C::ATOM_STRIDE);
             const uint32_t ahi = tmem + uint32_t(C::A_COL0 + r * C::ASLOT_COLS), alo = ahi + C::BK;
             if (elect_one()) {
 #pragma unroll
@@ -267,11 +268,10 @@ __global__ void __launch_bounds__(512, 1)
                     mma_ts(d, ahi + 8 * kk, db, C::IDESC_HI, (open && kk == 0) ? 0u : 1u);
                     mma_ts(d + KP, alo + 8 * kk, db, C::IDESC_KP, 1u);
                 }
-                mma_commit(emptyB + sb);
+                if (release_b) mma_commit(emptyB + st);
                 mma_commit(afree + r);
             }
             if (++r == C::ASLOTS) r = 0, rph ^= 1u;
-            if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
             if (close) {
                 if (elect_one()) mma_commit(accfull + buf);
                 if (++buf == C::NBUF) buf = 0, aph ^= 1u;
@@ -279,19 +279,34 @@ __global__ void __launch_bounds__(512, 1)
             open = close;
             __syncwarp();
         };
+        auto next_b = [&]() {
+            if (++sb == C::B_STAGES) sb = 0, phb ^= 1u;
+        };
         auto p1 = [&](int s) {
             if (s < NB) {
                 int cu = 0;
                 for (int q = q0; q < q1; ++q) {
                     const bool close = ++cu == du || q + 1 == q1;
                     if (close) cu = 0;
-                    unit(close);
+                    unit_on(close, sb, phb, true, true);
+                    next_b();
                 }
             }
         };
         auto p2 = [&](int s) {
-            if (s >= D)
-                for (int j = t0; j < t1; ++j) unit(false), unit(true);
+            if (s >= D && t1 > t0) {
+                const int s0 = sb;
+                const uint32_t ph0 = phb;
+                next_b();
+                const int s1 = sb;
+                const uint32_t ph1 = phb;
+                next_b();
+                for (int j = t0; j < t1; ++j) {
+                    const bool first = j == t0, last = j + 1 == t1;
+                    unit_on(false, s0, ph0, first, last);
+                    unit_on(true, s1, ph1, first, last);
+                }
+            }
         };
         for (int s = 0; s < NB + D; ++s) p.p2_first ? (p2(s), p1(s)) : (p1(s), p2(s));
     } else if (warp == 2) {
