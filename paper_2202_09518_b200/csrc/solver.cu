@@ -735,17 +735,13 @@ void nvls_setup_ctx(oocnmf_ctx* c) {
     c->Ht.p = c->nv.ht, c->Ht.bytes = bytes, c->Ht.external = true;
     c->nvls_ready = true;
 }
-// Collective: back to a private Ht (contents kept) and the symmetric buffers released.
+// Collective: the symmetric buffers released (called when Ht is reallocated for a new rank, or
+// at context destruction; Ht's contents are not needed either way).
 void nvls_release(oocnmf_ctx* c) {
     if (!c->nvls_ready) return;
     cudaStreamSynchronize(c->stream);
-    void* keep = nullptr;
-    if (cudaMalloc(&keep, c->nv.ht_bytes) == cudaSuccess)
-        cudaMemcpy(keep, c->nv.ht, c->nv.ht_bytes, cudaMemcpyDeviceToDevice);
-    const size_t bytes = c->nv.ht_bytes;
-    c->Ht.release();  // external: not freed here
+    c->Ht.release();  // external: not freed here, the next alloc_factors makes a private Ht
     nvls_teardown(c->nv, c->comm);
-    c->Ht.p = keep, c->Ht.bytes = keep ? bytes : 0;
     c->nvls_ready = c->nvls_pending = false;
 }
 bool nvls_use(const oocnmf_ctx* c) { return c->nvls_ready && c->no_check_next && nvls_wanted(c); }
