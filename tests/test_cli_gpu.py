@@ -179,15 +179,18 @@ def test_select_k_writes_the_reference_selection(gpu, tmp_path):
 
 
 def test_bench_emits_the_long_form_phase_csv(gpu, tmp_path):
-    r = run("bench", "--rows", 512, "--cols", 384, "--k", 4, 8, "--workers", 1, "--iters", 5,
+    workers = [1] + ([2] if nmf.device_count() >= 2 else [])
+    r = run("bench", "--rows", 512, "--cols", 384, "--k", 4, 8, "--workers", *workers, "--iters", 5,
             "--out", tmp_path / "b.csv")
     assert r.returncode == 0, r.stderr
     rows = list(csv.DictReader(io.StringIO((tmp_path / "b.csv").read_text())))
-    assert len(rows) == 12
+    assert len(rows) == 12 * len(workers)
     assert [x["phase"] for x in rows[:6]] == ["w_update", "h_update", "allreduce", "error_check", "io", "total"]
     for x in rows:
-        assert x["strategy"] == "rnmf" and x["N"] == "1" and x["n_B"] == "1" and x["k"] in ("4", "8")
+        assert x["strategy"] == "rnmf" and x["N"] in map(str, workers) and x["n_B"] == "1" and x["k"] in ("4", "8")
         assert float(x["seconds"]) >= 0 and int(x["bytes"]) >= 0
+    if len(workers) > 1:  # the two-rank rows carry the all-reduced bytes (CollectiveStats)
+        assert all(int(x["bytes"]) > 0 for x in rows if x["N"] == "2" and x["phase"] == "total")
     assert all(float(x["seconds"]) > 0 for x in rows if x["phase"] == "total")
     r = run("bench", "--rows", 256, "--cols", 256, "--k", 4, "--workers", 1, "--iters", 2)
     assert r.returncode == 0 and r.stdout.startswith("strategy,N,n_B,k,phase,seconds,bytes\n")
