@@ -465,15 +465,18 @@ def reference_arm(args, rank, K, W, k, world=1):
         gen_s = time.perf_counter() - t0
         w, h = oracle.port.init_factors(m, n, k, 0)
         try:
+            # one warm-up MU iteration is enough for a CPU solver (pages touched, threads up);
+            # each costs ~13 s at this size
+            w_cpu = min(W, 1)
             t0 = time.perf_counter()
-            for _ in range(W):
+            for _ in range(w_cpu):
                 impl.mu_iteration_handle(hnd, w, h)  # the loop body of nmf_serial (nmf_serial.cpp:84-101)
             warm_s = time.perf_counter() - t0
-            # bound the arm's wall time (OOCNMF_REF_BUDGET_S, default 1200 s for generation,
-            # warm-up and the timed solve) so a large --steps cannot outlast the driver's step:
-            # the rate is per iteration, so timing fewer of the same iterations measures it too
-            budget = float(os.environ.get("OOCNMF_REF_BUDGET_S", 1200))
-            per_it = warm_s / max(W, 1)
+            # bound the arm's wall time (OOCNMF_REF_BUDGET_S, default 360 s for generation,
+            # warm-up and the timed solve) so the run ends within minutes for any --steps: the
+            # rate is per iteration of the same full-size solve, so timing fewer of them measures it
+            budget = float(os.environ.get("OOCNMF_REF_BUDGET_S", 360))
+            per_it = warm_s / max(w_cpu, 1)
             k_run = K if per_it <= 0 else max(10, min(K, int((budget - gen_s - warm_s) / per_it)))
             t0 = time.perf_counter()
             r = impl.nmf_serial_handle(hnd, m, n, k, max_iters=k_run, interval=10, eta=0.0, seed=0)
@@ -485,7 +488,7 @@ def reference_arm(args, rank, K, W, k, world=1):
               "sample": f"the full workload: nmf_serial (f64) on the {m}x{n} A, k={k}, {k_run} iterations"
                         f"{'' if k_run == K else f' (of the requested {K}: wall-time budget)'} with error "
                         f"checks every 10 and on the last ({len(r.trace_err)} checks, final error "
-                        f"{r.trace_err[-1]:.6f}), after {W} warm-up MU iterations ({warm_s:.1f} s); A generated in "
+                        f"{r.trace_err[-1]:.6f}), after {w_cpu} warm-up MU iteration(s) ({warm_s:.1f} s); A generated in "
                         f"{gen_s:.1f} s (not timed)",
               "same_config": True}
         extra = {"timed_s": secs, "timed_iterations": k_run, "final_rel_error": float(r.trace_err[-1])}
