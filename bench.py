@@ -476,7 +476,7 @@ def reference_arm(args, rank, K, W, k, world=1):
             # warm-up and the timed solve) so the run ends within minutes for any --steps: the
             # rate is per iteration of the same full-size solve, so timing fewer of them measures it
             budget = float(os.environ.get("OOCNMF_REF_BUDGET_S", 360))
-            per_it = warm_s / max(w_cpu, 1)
+            per_it = 1.25 * warm_s / max(w_cpu, 1)  # (+ the error checks the warm-up step skips)
             k_run = K if per_it <= 0 else max(10, min(K, int((budget - gen_s - warm_s) / per_it)))
             t0 = time.perf_counter()
             r = impl.nmf_serial_handle(hnd, m, n, k, max_iters=k_run, interval=10, eta=0.0, seed=0)
