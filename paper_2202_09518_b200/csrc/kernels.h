@@ -65,6 +65,7 @@ struct FusedArgs {
     float* wta;            // np x kp: W^T A (transposed) of the new W
     uint64_t pol_p1, pol_p2;  // L2 policies of the A loads of P1 / P2
     uint64_t pol_p1s;         // P1 loads of the streamed (not kept) column tiles
+    double* wgram;            // [G][kp * kp] per-CTA W^T W of the new rows (nullptr: not computed)
     int keep_num, keep_den;   // column tile j kept in L2 for P2 iff j % keep_den < keep_num
 };
 struct FusedPlan {

@@ -61,7 +61,8 @@ struct FzCfg {
     static constexpr size_t BAR_BYTES = 512;
     // updater gather buffer: one row of every CTA's published P1 partial (TMA, G x kp floats)
     static constexpr size_t GATHER_OFF = RING_BYTES + BAR_BYTES + MAX_G * 4 + 64 * 4;  // 128-aligned
-    static constexpr size_t SMEM = GATHER_OFF + size_t(MAX_G) * KP * 4 + 1024;
+    static constexpr size_t WGRAM_OFF = GATHER_OFF + size_t(MAX_G) * KP * 4;             // [KP][KP] f64
+    static constexpr size_t SMEM = WGRAM_OFF + size_t(KP) * KP * 8 + 1024;
     static_assert(SMEM <= 232448, "shared memory budget");
     static constexpr uint32_t IDESC_HI = idesc_tf32(2 * KP, 0, 1);
     static constexpr uint32_t IDESC_KP = idesc_tf32(KP, 0, 1);
@@ -153,6 +154,7 @@ __global__ void __launch_bounds__(512, 1)
     int* act = reinterpret_cast<int*>(smem + C::RING_BYTES + C::BAR_BYTES);  // [G1] P1 publishers
     float* red = reinterpret_cast<float*>(act + C::MAX_G);                   // [64] updater scratch
     float* gbuf = reinterpret_cast<float*>(smem + C::GATHER_OFF);            // [G][kp] gathered partials
+    double* wg = reinterpret_cast<double*>(smem + C::WGRAM_OFF);             // [kp][kp] Gram of the new W rows
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int cta = blockIdx.x, G = gridDim.x;
@@ -317,6 +319,8 @@ __global__ void __launch_bounds__(512, 1)
         float hcol[KP];  // column j of HH^T
 #pragma unroll
         for (int q = 0; q < KP; ++q) hcol[q] = p.HHt[q * KP + j];
+        for (int e = lane; e < KP * KP; e += 32) wg[e] = 0.0;
+        __syncwarp();
         const unsigned target = 4u * unsigned(p.G1);
         bool bad = false;
         uint32_t gph = 0;
@@ -362,10 +366,11 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
             for (int q = 0; q < KP; ++q) d4[q & 3] = fmaf(__shfl_sync(0xffffffffu, wold, q), hcol[q], d4[q & 3]);
             const float de = (d4[0] + d4[1]) + (d4[2] + d4[3]);
+            float wn = 0.f;
             if (lane < KP) {
                 // t * nu / (de + eps) as (t * nu) * rcp_rn(de + eps), the factor-update
                 // kernel's formula (kernels_factor.cu)
-                const float wn = (wold * nu) * __frcp_rn(de + p.eps);
+                wn = (wold * nu) * __frcp_rn(de + p.eps);
                 bad |= !isfinite(wn);
                 wrow[lane] = wn;
                 float* cw = p.Wcat + g * (2 * KP);
@@ -378,8 +383,21 @@ __global__ void __launch_bounds__(512, 1)
                 red_release_add(p.wdone + 2 * b + (row >> 6), 1u);
                 FZ_TRACE(2, b, row);
             }
+            if (p.wgram) {
+                // the row's contribution to W^T W (column `lane`), exact f32 products summed in
+                // f64 in row order, off the W-ready path (after the release)
+#pragma unroll 8
+                for (int i = 0; i < KP; ++i) {
+                    const float wi = __shfl_sync(0xffffffffu, wn, i);
+                    if (lane < KP) wg[i * KP + lane] += double(wi) * double(wn);
+                }
+            }
         }
         if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(p.flag, 1);
+        if (p.wgram) {  // this CTA's slot (zeros if it updated no row)
+            __syncwarp();
+            for (int e = lane; e < KP * KP; e += 32) p.wgram[int64_t(cta) * KP * KP + e] = wg[e];
+        }
     } else if (warp >= 4 && warp < 12) {
         // ---------------- split warps: A tile -> [A_hi | A_lo] in TMEM slot
         const int t = 32 * (warp & 3) + lane;

@@ -472,7 +472,8 @@ void alloc_factors(oocnmf_ctx* c) {
     c->WtW64.alloc(size_t(kp) * kp * 8, "WtW64");
     c->packed.alloc(size_t(c->packed_count()) * 4, "packed");
     const int gw = factor_grid(c->mp / kTile), gh = factor_grid(c->np / kTile);
-    c->gram_w.alloc(size_t(gw) * kp * kp * 8, "gram_w");
+    // (also the one-pass kernel's per-CTA Gram slots: one per SM)
+    c->gram_w.alloc(size_t(std::max(gw, c->num_sms)) * kp * kp * 8, "gram_w");
     c->gram_h.alloc(size_t(gh) * kp * kp * 8, "gram_h");
     c->err_slots.alloc(size_t(std::max(gh, sqnorm_grid())) * 8, "err_slots");
     c->red_slots.alloc(size_t(sqnorm_grid()) * 8, "red_slots");
@@ -867,12 +868,18 @@ void w_update_and_wta(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         a.eps = eps, a.flag = c->flag.as<int>(), a.wta = nvls ? static_cast<float*>(c->nv.wp) : c->wta();
         c->nvls_pending = nvls;
         fused_policies(a);
+        // the Gram of the new W is accumulated by the updater warps (one f64 slot per CTA);
+        // OOCNMF_FUSED_WGRAM=0: the separate Gram pass over W instead
+        static const bool wgram_in_kernel = env_int("OOCNMF_FUSED_WGRAM", 1) != 0;
+        a.wgram = wgram_in_kernel ? c->gram_w.as<double>() : nullptr;
         count(c, launch_mu_fused(kp, fp, c->A.as<float>(), c->mp, c->np, c->Ht_cat.as<float>(), a, s), "mu fused");
         rec(eAht);
-        count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, eps, false,
-                                      c->gram_w.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
-              "W Gram");
-        count(c, launch_reduce_slots(c->gram_w.as<double>(), gw, int64_t(kp) * kp, c->wtw(), c->WtW64.as<double>(), s),
+        if (!wgram_in_kernel)
+            count(c, launch_factor_update(kp, c->W.as<float>(), c->mp, nullptr, nullptr, nullptr, nullptr, eps, false,
+                                          c->gram_w.as<double>(), nullptr, c->flag.as<int>(), nullptr, s),
+                  "W Gram");
+        count(c, launch_reduce_slots(c->gram_w.as<double>(), wgram_in_kernel ? fp.G : gw, int64_t(kp) * kp, c->wtw(),
+                                     c->WtW64.as<double>(), s),
               "reduce WtW");
         rec(eWdone);
         rec(eWta);
