@@ -20,14 +20,17 @@
 //   * P1 is column-chunked: CTA c computes the partial A[b, q-chunks]·Ht of its 64-column chunks
 //     [q0(c), q1(c)) (chosen so every CTA has the same P1 + P2 unit count per block), drains it
 //     into f32 registers and publishes it to a slot ring.
-//   * U is row-distributed: row r of block b is reduced (partials in ascending CTA order:
-//     deterministic) and updated by the updater warps of CTA (128 b + r) mod G, which then bump
-//     the block's done-counter; the producer of every CTA waits for it before loading the block's
-//     W_cat rows for P2.
-// Pipeline per CTA: the tcgen05 roles of kernels_tc.cu (warp 0 TMA producer, warp 1 MMA issuer,
-// warps 4-11 split A into [A_hi | A_lo] TMEM slots, warps 12-15 drain), fed one unit sequence
-//   for s in [0, NB + D):  P1 units of block s (if s < NB), then P2 units of block s - D
-// plus warps 2-3 as the updaters. The Gram W^T W of the new W is a separate small kernel.
+//   * U is row-distributed: row r of block b is gathered (one TMA operation over the 148 slots),
+//     reduced (partials in a fixed order: deterministic) and updated by the updater warp of CTA
+//     (128 b + r) mod G, which then bumps the block's half-block done-counter; the B producer of
+//     every CTA waits for it before loading the block's two [W | W_lo] halves for P2 (once per
+//     block, reused for all the CTA's owned tiles). The gathered partial lines are discarded
+//     from L2 (dead data must not be written back to HBM), and the updater accumulates the new
+//     rows' W^T W in f64 (one slot per CTA) after the release.
+// Pipeline per CTA: warp 0 A producer (TMA), warp 3 B producer, warp 1 tcgen05 MMA issuer,
+// warps 4-11 split A into [A_hi | A_lo] TMEM slots, warps 12-15 drain, warp 2 the updater; one
+// unit sequence
+//   for s in [0, NB + D):  P1 units of block s (if s < NB), then P2 units of block s - D.
 #include <cstdio>
 #include <cstdlib>
 
