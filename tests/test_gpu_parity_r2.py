@@ -7,6 +7,7 @@ the compiled reference (oracle/_ref); inputs are regenerated on the device with 
 that tests/test_gpu_parity.py pins bit-for-bit against the reference's (src/synth.cpp:60-86,
 bench/kernels_bench.cpp:12-18).
 """
+import json
 import os
 
 import numpy as np
@@ -273,3 +274,38 @@ def test_eta_exit_restores_the_factors_of_the_stopping_check(gpu, monkeypatch, f
     assert rel_fro(r.w, full.w) > 10 * rel_fro(r.w, ref.w)  # not the factors of iteration 50
     if g is not None:
         np.testing.assert_allclose([e for _, e in r.error_trace], g["trace_err"][:4], rtol=TRACE_TOL)
+
+
+_WGRAM = r"""
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle, paper_2202_09518_b200 as nmf
+a = oracle.port.uniform_dense(1024, 4096, 5, 99).astype(np.float32)
+w0, h0 = oracle.port.init_factors(1024, 4096, 32, 1)
+f32 = lambda x: np.asarray(x, np.float64).astype(np.float32).astype(np.float64)
+cfg = nmf.NmfConfig(k=32, max_iters=30, error_check_interval=10, eta=0.0, init=nmf.FactorInit.from_files,
+                    init_w=f32(w0), init_h=f32(h0))
+r = nmf.nmf_serial(a, cfg)
+print(json.dumps({"trace": [e for _, e in r.error_trace], "w": float(np.linalg.norm(r.w)),
+                  "h": float(np.linalg.norm(r.h)), "fused": r.info["fused_pass_launches"]}))
+"""
+
+
+def test_in_kernel_w_gram_matches_the_gram_pass(gpu):
+    """The one-pass kernel's updaters accumulate W^T W of the new rows (f64 slots per CTA); the
+    separate Gram pass (OOCNMF_FUSED_WGRAM=0) gives the same trajectory to f32 rounding."""
+    import subprocess
+    import sys
+
+    out = {}
+    for w in ("1", "0"):
+        env = dict(os.environ, OOCNMF_FUSED="1", OOCNMF_FUSED_WGRAM=w)
+        r = subprocess.run([sys.executable, "-c", _WGRAM, os.path.dirname(os.path.dirname(os.path.abspath(__file__)))],
+                           capture_output=True, text=True, env=env, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        out[w] = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["1"]["fused"] == out["0"]["fused"] == 30
+    np.testing.assert_allclose(out["1"]["trace"], out["0"]["trace"], rtol=1e-6)
+    assert out["1"]["w"] == pytest.approx(out["0"]["w"], rel=1e-5)
+    assert out["1"]["h"] == pytest.approx(out["0"]["h"], rel=1e-5)
