@@ -309,3 +309,23 @@ def test_in_kernel_w_gram_matches_the_gram_pass(gpu):
     np.testing.assert_allclose(out["1"]["trace"], out["0"]["trace"], rtol=1e-6)
     assert out["1"]["w"] == pytest.approx(out["0"]["w"], rel=1e-5)
     assert out["1"]["h"] == pytest.approx(out["0"]["h"], rel=1e-5)
+
+
+def test_fused_pass_is_deterministic_at_scale(gpu):
+    """The one-pass kernel at a config-2 row width (8192 x 65536: 64 row blocks, every slot of
+    the partial ring reused 21 times, 3-4 owned tiles per CTA): two solves are bit-identical
+    (fixed-order sums everywhere; a race in the publish / gather / discard / W-stage reuse
+    paths would show up here as a difference)."""
+    m, n, k = 8192, 65536, 32
+    cfg = nmf.NmfConfig(k=k, max_iters=20, error_check_interval=10, eta=0.0, seed=3)
+    outs = []
+    for _ in range(2):
+        with nmf.Context(gpu) as ctx:
+            ctx.set_problem(m, n, k)
+            ctx.generate_dense_uniform(42, 99)
+            trace, info = ctx.solve(cfg)
+            assert info["fused_pass_launches"] == 20
+            outs.append((trace, *ctx.get_factors()))
+    (t1, w1, h1), (t2, w2, h2) = outs
+    assert [e for _, e in t1] == [e for _, e in t2]
+    assert np.array_equal(w1, w2) and np.array_equal(h1, h2)
