@@ -738,7 +738,8 @@ def run_workload(args, workload, m, n, k, K, W, env):
                       "rows_per_rank": rows, "error_check_interval": 10,
                       "l2": f"A slab >> 126 MB L2 (no flush needed)"},
            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-           "gpu_launches": int(info["gpu_launches"]), "final_rel_error": trace[-1][1] if trace else None,
+           "gpu_launches": int(info["gpu_launches"]), "paths": ctx.paths(),
+           "final_rel_error": trace[-1][1] if trace else None,
            "phase_ms_per_step": {p_: info[p_ + "_s"] * 1e3 / K for p_ in
                                  ("w_update", "h_update", "allreduce", "error_check")}}
     out.update({k_: v for k_, v in extra.items() if v is not None})

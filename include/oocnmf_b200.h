@@ -118,6 +118,10 @@ int oocnmf_ctx_create_comm(int device, int rank, int nranks, const unsigned char
                            oocnmf_ctx** out);
 int oocnmf_ctx_destroy(oocnmf_ctx* ctx);
 int oocnmf_ctx_rank(const oocnmf_ctx* ctx, int* rank, int* nranks);
+/* Which B200 paths the context's current problem uses (reporting only; no reference
+ * counterpart): bit 0 the one-pass dense kernel, bit 1 the two streaming tensor-core passes,
+ * bit 2 the NVLS multicast H update, bit 3 the sharded H update, bit 4 CSR, bit 5 out-of-core. */
+int oocnmf_ctx_paths(const oocnmf_ctx* ctx, int* flags);
 
 /* Global A is m x n with k latent features; this rank owns rows [row0, row0 + rows)
  * (the RNMF slab of PartitionPlan, src/partition.cpp:72-85). */

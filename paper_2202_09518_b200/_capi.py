@@ -68,6 +68,7 @@ _SIGS = {
     "oocnmf_ctx_create_comm": ([C.c_int, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)], C.c_int),
     "oocnmf_ctx_destroy": ([vp], C.c_int),
     "oocnmf_ctx_rank": ([vp, C.POINTER(C.c_int), C.POINTER(C.c_int)], C.c_int),
+    "oocnmf_ctx_paths": ([vp, C.POINTER(C.c_int)], C.c_int),
     "oocnmf_set_problem": ([vp, u64, u64, u64, u64, u64], C.c_int),
     "oocnmf_load_dense_f64": ([vp, pd, u64], C.c_int),
     "oocnmf_load_dense_f32": ([vp, pf, u64], C.c_int),

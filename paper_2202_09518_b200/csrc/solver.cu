@@ -2069,6 +2069,19 @@ int oocnmf_ctx_rank(const oocnmf_ctx* c, int* rank, int* nranks) {
     });
 }
 
+int oocnmf_ctx_paths(const oocnmf_ctx* c, int* flags) {
+    return guarded([&] {
+        int f = 0;
+        if (c->kind == Kind::dense && c->use_fused) f |= 1;
+        if ((c->kind == Kind::dense || c->kind == Kind::host) && c->use_tc && !c->use_fused) f |= 2;
+        if (c->nvls_ready) f |= 4;
+        if (c->shard_h()) f |= 8;
+        if (c->kind == Kind::csr) f |= 16;
+        if (c->kind == Kind::host) f |= 32;
+        *flags = f;
+    });
+}
+
 int oocnmf_set_problem(oocnmf_ctx* c, uint64_t m, uint64_t n, uint64_t k, uint64_t row0, uint64_t rows) {
     return guarded([&] {
         set_dev(c);

@@ -368,6 +368,13 @@ class Context:
         nt = min(int(info.n_trace), cap)
         return list(zip(ti[:nt].astype(int).tolist(), te[:nt].tolist())), info.as_dict()
 
+    def paths(self) -> Dict[str, bool]:
+        """Which B200 paths the current problem runs (reporting only)."""
+        f = C.c_int()
+        check(_capi.lib().oocnmf_ctx_paths(self._h, C.byref(f)))
+        names = ("one_pass", "two_pass_tc", "nvls_h_update", "sharded_h", "csr", "out_of_core")
+        return {n: bool(f.value >> i & 1) for i, n in enumerate(names)}
+
     def set_rank(self, k: int):
         """Change k keeping the resident A (model selection sweeps k over one matrix)."""
         check(_capi.lib().oocnmf_set_rank(self._h, k))
