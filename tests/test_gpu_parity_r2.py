@@ -329,3 +329,22 @@ def test_fused_pass_is_deterministic_at_scale(gpu):
     (t1, w1, h1), (t2, w2, h2) = outs
     assert [e for _, e in t1] == [e for _, e in t2]
     assert np.array_equal(w1, w2) and np.array_equal(h1, h2)
+
+
+def test_context_reports_its_paths(gpu, monkeypatch):
+    """Context.paths() (C-ABI oocnmf_ctx_paths): the shape dispatch between the one-pass kernel
+    and the two streaming passes, and the CSR path."""
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(1024, 2048, 32)
+        ctx.generate_dense_uniform(42, 99)
+        p = ctx.paths()
+        assert p["two_pass_tc"] and not p["one_pass"] and not p["csr"]
+        monkeypatch.setenv("OOCNMF_FUSED", "1")
+        ctx.set_rank(32)  # re-plans
+        p = ctx.paths()
+        assert p["one_pass"] and not p["two_pass_tc"]
+    with nmf.Context(gpu) as ctx:
+        ctx.set_problem(1000, 900, 16)
+        ctx.generate_csr_uniform(0.01, 3)
+        p = ctx.paths()
+        assert p["csr"] and not p["one_pass"] and not p["nvls_h_update"]
