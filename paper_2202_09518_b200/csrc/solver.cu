@@ -1069,14 +1069,17 @@ void h_update(oocnmf_ctx* c, float eps, bool timed, cudaEvent_t* ev) {
         // One fused NCCL launch: the packed f32 [W^T A | W^T W] the update consumes and the f64
         // W^T W the trace-form error consumes. (CNMF: W^T A of the column slab and W^T W of the
         // replicated W are already complete on every rank.)
+        // (the f64 copy only ahead of an error check: nothing else reads it)
+        const bool with64 = !c->no_check_next;
         coll_begin(c, s);
         nck(ncclGroupStart(), "ncclGroupStart");
         ncc(c, ncclAllReduce(c->packed.p, c->packed.p, size_t(c->packed_count()), ncclFloat, ncclSum, c->comm, s),
             "allreduce [WtA|WtW]");
-        ncc(c, ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
-            "allreduce WtW64");
+        if (with64)
+            ncc(c, ncclAllReduce(c->WtW64.p, c->WtW64.p, size_t(kp) * kp, ncclDouble, ncclSum, c->comm, s),
+                "allreduce WtW64");
         ncc(c, ncclGroupEnd(), "ncclGroupEnd");
-        coll_end(c, s, kTagH, size_t(c->packed_count()) * 4 + size_t(kp) * kp * 8);  // nmf_distributed.cpp:171,178
+        coll_end(c, s, kTagH, size_t(c->packed_count()) * 4 + (with64 ? size_t(kp) * kp * 8 : 0));  // nmf_distributed.cpp:171,178
     }
     if (timed) record(c, ev[eComm], s);
     // sharded H: the [H | H_lo] operand of the next pass is rebuilt from the gathered H below
